@@ -1,0 +1,63 @@
+"""ctypes binding of the C ABI declared in include/hlm_cuda.h.
+
+The shared library is built in-tree (``paper_2602_04816_b200/libhlm_b200.so``)
+by ``__graft_entry__.build()``; loading fails loudly when it is missing — there
+is no CPU fallback for any GPU stage.
+"""
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhlm_b200.so")
+
+_lib = None
+
+
+class HlmError(RuntimeError):
+    """Non-zero status from the C ABI; ``code`` is the HlmStatus value."""
+
+    def __init__(self, code, msg):
+        super().__init__(f"[hlm status {code}] {msg}")
+        self.code = code
+
+
+class HlmGemmDesc(ctypes.Structure):
+    _fields_ = [
+        ("M", ctypes.c_int), ("N", ctypes.c_int), ("K", ctypes.c_int), ("G", ctypes.c_int),
+        ("kgroup", ctypes.c_int),
+        ("a_mn", ctypes.c_int), ("b_mn", ctypes.c_int),
+        ("a_grouped", ctypes.c_int), ("b_grouped", ctypes.c_int),
+        ("epi", ctypes.c_int),
+        ("A", ctypes.c_void_p), ("lda", ctypes.c_longlong), ("a_gstride", ctypes.c_longlong),
+        ("B", ctypes.c_void_p), ("ldb", ctypes.c_longlong), ("b_gstride", ctypes.c_longlong),
+        ("C", ctypes.c_void_p), ("ldc", ctypes.c_longlong), ("c_gstride", ctypes.c_longlong),
+        ("R", ctypes.c_void_p), ("ldr", ctypes.c_longlong), ("r_gstride", ctypes.c_longlong),
+    ]
+
+
+EPI_BF16, EPI_F32, EPI_F32_ADD = 0, 1, 2
+
+
+def lib():
+    """Load libhlm_b200.so once; raise if it was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: run __graft_entry__.build() (make -C "
+                "paper_2602_04816_b200/csrc). The CUDA path has no fallback.")
+        _lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+        _lib.hlm_cuda_last_error.restype = ctypes.c_char_p
+        _lib.hlm_cuda_gemm.argtypes = [ctypes.POINTER(HlmGemmDesc), ctypes.c_void_p]
+    return _lib
+
+
+def check(rc):
+    if rc != 0:
+        raise HlmError(rc, lib().hlm_cuda_last_error().decode())
+    return rc
+
+
+def gemm(desc, stream=0):
+    check(lib().hlm_cuda_gemm(ctypes.byref(desc), ctypes.c_void_p(stream)))

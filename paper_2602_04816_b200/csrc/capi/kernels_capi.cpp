@@ -1,0 +1,19 @@
+// extern "C" kernel entry points: validate, launch, translate status codes.
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "capi_util.h"
+#include "hlm_cuda.h"
+#include "../kernels/gemm.h"
+
+extern "C" int hlm_cuda_gemm(const HlmGemmDesc* desc, void* stream) {
+  const int rc = hlm_gemm_launch(desc, static_cast<cudaStream_t>(stream));
+  if (rc != 0) {
+    static const char* names[] = {"args", "align", "tensor map", "launch", "driver entry point"};
+    const int i = rc - HLM_GEMM_ERR_ARGS;
+    hlm_capi::set_error(std::string("hlm_cuda_gemm: ") +
+                        (i >= 0 && i < 5 ? names[i] : "unknown") + " error");
+  }
+  return rc;
+}

@@ -1,0 +1,377 @@
+// Persistent, warp-specialised tcgen05 GEMM for sm_100a.
+//
+// One kernel template serves every projection of the block and the head:
+//   forward      X(T,in) . W(in,out)        A K-major, B MN-major
+//   dgrad        dY(T,out) . W(in,out)^T    A K-major, B K-major
+//   wgrad        X(T,in)^T . dY(T,out)      A MN-major, B MN-major
+// i.e. the three CPU loops matmul_nn / matmul_nt / matmul_grad_acc of
+// reference proj/include/hlm/kernels.hpp:164-205, with W kept in the
+// reference's (in, out) row-major tile layout (host_store.cpp:70-92) so no
+// transposed weight copy is ever made: majorness is a descriptor bit.
+//
+// Groups: three (h,h) matrices w_q|w_k|w_v (and w_up|w_gate) sit back to back
+// in the tile, so a "group" dimension lets one launch cover QKV (N-grouped:
+// independent outputs [G][M][N]) or sum the three dgrads into one output
+// (K-grouped: the K loop runs over groups too).
+//
+// Tile 128x256x64, 4-stage TMA->smem ring, 2 TMEM accumulators (512 cols) so
+// the epilogue of tile i overlaps the MMAs of tile i+1.
+// Warp roles: w0 TMA producer, w1 MMA issuer, w2 TMEM allocator, w4..7 epilogue.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "gemm.h"
+#include "sm100_ptx.cuh"
+
+using namespace hlm_sm100;
+
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_STAGE = BM * BK * 2;   // 16 KiB
+constexpr int B_STAGE = BN * BK * 2;   // 32 KiB
+constexpr int ATOM = 64 * BK * 2;      // one 64-wide MN atom of a MN-major stage: 8 KiB
+constexpr int NUM_THREADS = 256;
+constexpr int GROUP_M = 16;            // raster: 16 M-tiles share each B panel in L2
+constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + 1024 /*align*/ + 256 /*barriers*/;
+
+struct KArgs {
+  int M, N, K, G;
+  int kgroup, a_grouped, b_grouped;
+  int tiles_m, tiles_n, kblocks, num_tiles;
+  void* C;
+  long long ldc, c_gstride;
+  const float* R;
+  long long ldr, r_gstride;
+  int epi;
+};
+
+__device__ __forceinline__ void tile_coords(const KArgs& a, int t, int& g, int& m, int& n) {
+  const int per_group = a.tiles_m * a.tiles_n;
+  g = a.kgroup ? 0 : t / per_group;
+  const int rem = t - g * per_group;
+  const int per_panel = GROUP_M * a.tiles_n;
+  const int panel = rem / per_panel;
+  const int first_m = panel * GROUP_M;
+  const int gm = min(a.tiles_m - first_m, GROUP_M);
+  const int r = rem - panel * per_panel;
+  m = first_m + r % gm;
+  n = r / gm;
+}
+
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                const KArgs args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint64_t* tmem_empty = tmem_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&map_a);
+    tma_prefetch(&map_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tmem_full[s], 1);
+      mbar_init(&tmem_empty[s], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int g_iters = args.kgroup ? args.G : 1;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < args.num_tiles; t += gridDim.x) {
+        int tg, tm, tn;
+        tile_coords(args, t, tg, tm, tn);
+        const int m0 = tm * BM, n0 = tn * BN;
+        for (int gi = 0; gi < g_iters; ++gi) {
+          const int g = args.kgroup ? gi : tg;
+          const int ag = args.a_grouped ? g : 0;
+          const int bg = args.b_grouped ? g : 0;
+          for (int kb = 0; kb < args.kblocks; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full[stage], A_STAGE + B_STAGE);
+            const int k0 = kb * BK;
+            uint8_t* a_dst = sA + stage * A_STAGE;
+            uint8_t* b_dst = sB + stage * B_STAGE;
+            if (A_MN) {
+              tma_load_3d(a_dst, &map_a, &full[stage], m0, k0, ag);
+              tma_load_3d(a_dst + ATOM, &map_a, &full[stage], m0 + 64, k0, ag);
+            } else {
+              tma_load_3d(a_dst, &map_a, &full[stage], k0, m0, ag);
+            }
+            if (B_MN) {
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j)
+                tma_load_3d(b_dst + j * ATOM, &map_b, &full[stage], n0 + 64 * j, k0, bg);
+            } else {
+              tma_load_3d(b_dst, &map_b, &full[stage], k0, n0, bg);
+            }
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = make_idesc_bf16(BM, BN, A_MN, B_MN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int local = 0;
+    for (int t = blockIdx.x; t < args.num_tiles; t += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      bool first = true;
+      for (int gi = 0; gi < g_iters; ++gi) {
+        for (int kb = 0; kb < args.kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a_base = smem_u32(sA + stage * A_STAGE);
+            const uint32_t b_base = smem_u32(sB + stage * B_STAGE);
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              // K-major: advance 16 elements = 32 B inside the 128 B swizzle row.
+              // MN-major: advance 16 K-rows = 2 KiB (two 8-row swizzle atoms).
+              const uint64_t ad = A_MN ? make_sw128_desc(a_base + kk * 2048, ATOM, 1024)
+                                       : make_sw128_desc(a_base + kk * 32, 16, 1024);
+              const uint64_t bd = B_MN ? make_sw128_desc(b_base + kk * 2048, ATOM, 1024)
+                                       : make_sw128_desc(b_base + kk * 32, 16, 1024);
+              umma_bf16(d_tmem, ad, bd, idesc, (first && kk == 0) ? 0u : 1u);
+            }
+            umma_commit(&empty[stage]);
+          }
+          __syncwarp();
+          first = false;
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      if (lane == 0) umma_commit(&tmem_full[acc]);
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------ epilogue: TMEM -> regs -> global
+    const int ew = warp - 4;   // TMEM lanes 32*ew .. 32*ew+31
+    int local = 0;
+    for (int t = blockIdx.x; t < args.num_tiles; t += gridDim.x, ++local) {
+      int tg, tm, tn;
+      tile_coords(args, t, tg, tm, tn);
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&tmem_full[acc], acc_phase);
+      tc_fence_after();
+      const int row = tm * BM + ew * 32 + lane;
+      const bool row_ok = row < args.M;
+      const long long c_off = (long long)tg * args.c_gstride + (long long)row * args.ldc;
+      const long long r_off = (long long)tg * args.r_gstride + (long long)row * args.ldr;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32(tmem_base + acc * BN + c * 32 + ((uint32_t)(ew * 32) << 16), r);
+        tmem_ld_wait();
+        const int col0 = tn * BN + c * 32;
+        if (!row_ok || col0 >= args.N) continue;
+        const bool full_chunk = col0 + 32 <= args.N;
+        if (args.epi == HLM_EPI_BF16) {
+          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.C) + c_off + col0;
+          if (full_chunk && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint4 v;
+              v.x = pack_bf16x2(__uint_as_float(r[8 * j + 0]), __uint_as_float(r[8 * j + 1]));
+              v.y = pack_bf16x2(__uint_as_float(r[8 * j + 2]), __uint_as_float(r[8 * j + 3]));
+              v.z = pack_bf16x2(__uint_as_float(r[8 * j + 4]), __uint_as_float(r[8 * j + 5]));
+              v.w = pack_bf16x2(__uint_as_float(r[8 * j + 6]), __uint_as_float(r[8 * j + 7]));
+              d4[j] = v;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j < args.N) dst[j] = __float2bfloat16_rn(__uint_as_float(r[j]));
+          }
+        } else {
+          float* dst = reinterpret_cast<float*>(args.C) + c_off + col0;
+          const float* res = args.epi == HLM_EPI_F32_ADD ? args.R + r_off + col0 : nullptr;
+          if (full_chunk && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) &&
+              (res == nullptr || (reinterpret_cast<uintptr_t>(res) & 15) == 0)) {
+            float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float4 v = make_float4(__uint_as_float(r[4 * j + 0]), __uint_as_float(r[4 * j + 1]),
+                                     __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+              if (res) {
+                const float4 q = reinterpret_cast<const float4*>(res)[j];
+                v.x += q.x;
+                v.y += q.y;
+                v.z += q.z;
+                v.w += q.w;
+              }
+              d4[j] = v;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j < args.N) dst[j] = __uint_as_float(r[j]) + (res ? res[j] : 0.0f);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+    }
+  }
+
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem_base);
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 3-D bf16 map: dims {inner, outer, groups}; box {64, box_outer, 1}; 128 B swizzle.
+int make_map(CUtensorMap* map, const void* ptr, long long inner, long long outer, long long groups,
+             long long ld, long long gstride, int box_outer) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return HLM_GEMM_ERR_DRIVER;
+  if (groups <= 1) gstride = ld * outer;
+  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)(groups < 1 ? 1 : groups)};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 2), (cuuint64_t)(gstride * 2)};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_outer, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : HLM_GEMM_ERR_TMAP;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <bool A_MN, bool B_MN>
+int launch(const HlmGemmDesc& d, cudaStream_t stream) {
+  CUtensorMap ma, mb;
+  int rc;
+  const long long ga = d.a_grouped ? d.G : 1, gb = d.b_grouped ? d.G : 1;
+  if (A_MN)
+    rc = make_map(&ma, d.A, d.M, d.K, ga, d.lda, d.a_gstride, BK);
+  else
+    rc = make_map(&ma, d.A, d.K, d.M, ga, d.lda, d.a_gstride, BM);
+  if (rc) return rc;
+  if (B_MN)
+    rc = make_map(&mb, d.B, d.N, d.K, gb, d.ldb, d.b_gstride, BK);
+  else
+    rc = make_map(&mb, d.B, d.K, d.N, gb, d.ldb, d.b_gstride, BN);
+  if (rc) return rc;
+
+  KArgs a;
+  a.M = d.M;
+  a.N = d.N;
+  a.K = d.K;
+  a.G = d.G < 1 ? 1 : d.G;
+  a.kgroup = d.kgroup;
+  a.a_grouped = d.a_grouped;
+  a.b_grouped = d.b_grouped;
+  a.tiles_m = (d.M + BM - 1) / BM;
+  a.tiles_n = (d.N + BN - 1) / BN;
+  a.kblocks = (d.K + BK - 1) / BK;
+  a.num_tiles = a.tiles_m * a.tiles_n * (d.kgroup ? 1 : a.G);
+  a.C = d.C;
+  a.ldc = d.ldc;
+  a.c_gstride = d.c_gstride;
+  a.R = d.R;
+  a.ldr = d.ldr;
+  a.r_gstride = d.r_gstride;
+  a.epi = d.epi;
+
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemm_kernel<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         SMEM_BYTES);
+  }
+  const int grid = a.num_tiles < sm_count() ? a.num_tiles : sm_count();
+  gemm_kernel<A_MN, B_MN><<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, a);
+  attr_set = true;
+  return cudaGetLastError() == cudaSuccess ? 0 : HLM_GEMM_ERR_LAUNCH;
+}
+
+}  // namespace
+
+extern "C" int hlm_gemm_launch(const HlmGemmDesc* d, cudaStream_t stream) {
+  if (!d) return HLM_GEMM_ERR_ARGS;
+  if (d->M <= 0 || d->N <= 0 || d->K <= 0) return 0;
+  if (d->epi == HLM_EPI_F32_ADD && d->R == nullptr) return HLM_GEMM_ERR_ARGS;
+  // TMA: global strides must be multiples of 16 bytes, base 16-byte aligned.
+  if ((d->lda * 2) % 16 || (d->ldb * 2) % 16) return HLM_GEMM_ERR_ALIGN;
+  if ((reinterpret_cast<uintptr_t>(d->A) & 15) || (reinterpret_cast<uintptr_t>(d->B) & 15))
+    return HLM_GEMM_ERR_ALIGN;
+  if ((d->a_grouped && (d->a_gstride * 2) % 16) || (d->b_grouped && (d->b_gstride * 2) % 16))
+    return HLM_GEMM_ERR_ALIGN;
+  if (d->a_mn) {
+    if (d->b_mn) return launch<true, true>(*d, stream);
+    return launch<true, false>(*d, stream);
+  }
+  if (d->b_mn) return launch<false, true>(*d, stream);
+  return launch<false, false>(*d, stream);
+}
