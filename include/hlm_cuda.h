@@ -78,6 +78,78 @@ typedef struct HlmGemmDesc {
 
 int hlm_cuda_gemm(const HlmGemmDesc* desc, void* stream);
 
+/* ------------------------------------------------------------------ block
+ * One transformer block (reference kernels.hpp:313-383, plus the multi-head /
+ * RoPE extension): pre-RMSNorm causal attention + residual, pre-RMSNorm
+ * SwiGLU MLP + residual. Weights: the block's bf16 tile in the reference
+ * offset-table order (w_q w_k w_v w_o (h,h), w_up w_gate (h,f), w_down (f,h),
+ * norm1, norm2 (h); host_store.cpp:70-92). Residual stream and gradients are
+ * fp32; GEMM operands bf16 with fp32 accumulation.
+ *   acts: device buffer of hlm_cuda_block_acts_bytes() holding what backward
+ *         consumes (n1, q|k|v after RoPE, o, lse, y, n2, up|gate, act).
+ *   ws:   device scratch of hlm_cuda_block_ws_bytes().
+ *   rope_cos / rope_sin: device tables [seq][head_dim/2] from
+ *         hlm_cuda_rope_table(), or NULL when rope_theta == 0.
+ * Backward overwrites grad_tile (fp32, tile order, block_params elements);
+ * h_out must not alias h_in and g_in must not alias g_out (kernels.hpp:313,334). */
+typedef struct HlmBlockDims {
+  int64_t batch, seq, hidden, ffn;
+  int32_t n_heads;   /* 1 = reference semantics */
+  int32_t flags;     /* HLM_BLOCK_* */
+} HlmBlockDims;
+
+enum HlmBlockFlags {
+  HLM_BLOCK_GENERIC_ATTENTION = 1 /* force the any-head_dim CUDA-core attention */
+};
+
+size_t hlm_cuda_block_acts_bytes(const HlmBlockDims* d);
+size_t hlm_cuda_block_ws_bytes(const HlmBlockDims* d);
+int hlm_cuda_block_fwd(const HlmBlockDims* d, const void* w_tile, const float* h_in, float* h_out,
+                       void* acts, void* ws, const float* rope_cos, const float* rope_sin,
+                       void* stream);
+int hlm_cuda_block_bwd(const HlmBlockDims* d, const void* w_tile, const float* h_in,
+                       const void* acts, const float* g_out, float* g_in, float* grad_tile,
+                       void* ws, const float* rope_cos, const float* rope_sin, void* stream);
+
+/* RoPE tables [seq][head_dim/2]: angle = pos * theta^(-2i/head_dim) evaluated
+ * in double on the host, rounded to fp32, copied to the device. */
+int hlm_cuda_rope_table(float* dev_cos, float* dev_sin, int64_t seq, int64_t head_dim,
+                        double theta);
+
+/* ------------------------------------------------------------------ head + loss
+ * logits = x . head^T (head (V,h) bf16), mean cross entropy with d_logits =
+ * (softmax - onehot) * inv_rows, d_x = d_logits . head, d_head (+)= d_logits^T . x
+ * (reference head_fwd / ce_loss_and_grad / head_bwd, kernels.hpp:410-446).
+ * loss_rows[r] = (logz_r - logit_r[target_r]) * inv_rows; the caller sums.
+ * inv_rows is 1/global_rows under data parallelism. */
+size_t hlm_cuda_head_ws_bytes(int64_t rows, int64_t hidden, int64_t vocab);
+int hlm_cuda_head_loss(int64_t rows, int64_t hidden, int64_t vocab, const void* head,
+                       const float* x, const int32_t* targets, float inv_rows, float* d_x,
+                       float* d_head, int accumulate_d_head, float* loss_rows, void* ws,
+                       void* stream);
+
+/* ------------------------------------------------------------------ embedding
+ * embed_fwd: out[t] = table[tokens[t]] widened to fp32 (kernels.hpp:385-394);
+ *   an out-of-range id sets *err_flag |= 1 (device int) and yields zeros.
+ * embed_bwd: d_table[v] (+)= sum of g[t] over the positions t of token v in
+ *   ascending order (kernels.hpp:396-408 order, no atomics): row_ptr[V+1] and
+ *   pos[] are the CSR of the batch tokens (hlm_embed_csr builds it on the host). */
+int hlm_cuda_embed_fwd(const int32_t* tokens, const void* table, float* out, int64_t rows,
+                       int64_t hidden, int64_t vocab, int* err_flag, void* stream);
+int hlm_cuda_embed_bwd(const int32_t* row_ptr, const int32_t* pos, const float* g,
+                       float* d_table, int64_t vocab, int64_t hidden, int accumulate,
+                       void* stream);
+int hlm_embed_csr(const int32_t* tokens, int64_t rows, int64_t vocab, int32_t* row_ptr,
+                  int32_t* pos);
+
+/* ------------------------------------------------------------------ small ops */
+int hlm_cuda_cast_bf16(const float* in, void* out, int64_t n, void* stream);
+int hlm_cuda_attention_fwd(const HlmBlockDims* d, const void* q, const void* k, const void* v,
+                           void* o, float* lse, int64_t ld, void* stream);
+int hlm_cuda_attention_bwd(const HlmBlockDims* d, const void* q, const void* k, const void* v,
+                           const void* o, const void* d_o, const float* lse, float* dsum,
+                           void* dq, void* dk, void* dv, int64_t ld, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

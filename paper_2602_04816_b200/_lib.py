@@ -61,3 +61,47 @@ def check(rc):
 
 def gemm(desc, stream=0):
     check(lib().hlm_cuda_gemm(ctypes.byref(desc), ctypes.c_void_p(stream)))
+
+
+class HlmBlockDims(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int64), ("seq", ctypes.c_int64), ("hidden", ctypes.c_int64),
+                ("ffn", ctypes.c_int64), ("n_heads", ctypes.c_int32), ("flags", ctypes.c_int32)]
+
+
+BLOCK_GENERIC_ATTENTION = 1
+_vp = ctypes.c_void_p
+
+
+def _setup_block_protos(L):
+    L.hlm_cuda_block_acts_bytes.restype = ctypes.c_size_t
+    L.hlm_cuda_block_acts_bytes.argtypes = [ctypes.POINTER(HlmBlockDims)]
+    L.hlm_cuda_block_ws_bytes.restype = ctypes.c_size_t
+    L.hlm_cuda_block_ws_bytes.argtypes = [ctypes.POINTER(HlmBlockDims)]
+    L.hlm_cuda_block_fwd.argtypes = [ctypes.POINTER(HlmBlockDims)] + [_vp] * 8
+    L.hlm_cuda_block_bwd.argtypes = [ctypes.POINTER(HlmBlockDims)] + [_vp] * 10
+    L.hlm_cuda_rope_table.argtypes = [_vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_double]
+    L.hlm_cuda_head_ws_bytes.restype = ctypes.c_size_t
+    L.hlm_cuda_head_ws_bytes.argtypes = [ctypes.c_int64] * 3
+    L.hlm_cuda_head_loss.argtypes = [ctypes.c_int64] * 3 + [_vp, _vp, _vp, ctypes.c_float, _vp, _vp,
+                                                            ctypes.c_int, _vp, _vp, _vp]
+    L.hlm_cuda_embed_fwd.argtypes = [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                     _vp, _vp]
+    L.hlm_cuda_embed_bwd.argtypes = [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                     _vp]
+    L.hlm_embed_csr.argtypes = [_vp, ctypes.c_int64, ctypes.c_int64, _vp, _vp]
+    L.hlm_cuda_cast_bf16.argtypes = [_vp, _vp, ctypes.c_int64, _vp]
+    L.hlm_cuda_attention_fwd.argtypes = [ctypes.POINTER(HlmBlockDims)] + [_vp] * 5 + [ctypes.c_int64, _vp]
+    L.hlm_cuda_attention_bwd.argtypes = [ctypes.POINTER(HlmBlockDims)] + [_vp] * 10 + [ctypes.c_int64,
+                                                                                         _vp]
+
+
+_block_ready = False
+
+
+def blib():
+    global _block_ready
+    L = lib()
+    if not _block_ready:
+        _setup_block_protos(L)
+        _block_ready = True
+    return L

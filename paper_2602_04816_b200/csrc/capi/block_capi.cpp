@@ -1,0 +1,415 @@
+// Block / head / embedding orchestration behind the C ABI: the device-side
+// equivalents of reference block_forward / block_backward
+// (proj/include/hlm/kernels.hpp:313-383), anchor_loss_impl's head + CE
+// (proj/src/engine.cpp:227-269) and the embedding gather / scatter.
+//
+// Every GEMM reads the bf16 weight tile in place (offset-table order,
+// proj/src/host_store.cpp:70-92); the three q/k/v (and up/gate) projections
+// are single grouped launches. Weight gradients are written straight into the
+// fp32 flat tile gradient in the same order, ready for the D2H copy.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "capi_util.h"
+#include "hlm_cuda.h"
+#include "../kernels/block_ops.h"
+#include "../kernels/gemm.h"
+#include "../kernels/attention.h"
+
+namespace {
+
+using i64 = int64_t;
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Carves a device buffer into 256-byte aligned pieces in a fixed order.
+struct Carver {
+  char* base;
+  size_t off = 0;
+  explicit Carver(void* b) : base(static_cast<char*>(b)) {}
+  template <typename T>
+  T* take(size_t count) {
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += align_up(count * sizeof(T));
+    return p;
+  }
+};
+
+struct BlockActs {
+  uint16_t *n1, *qkv, *o, *n2, *ug, *act;
+  float *lse, *y;
+};
+
+BlockActs carve_acts(const HlmBlockDims& d, void* buf, size_t* total) {
+  const i64 T = d.batch * d.seq, h = d.hidden, f = d.ffn, H = d.n_heads;
+  Carver c(buf);
+  BlockActs a;
+  a.n1 = c.take<uint16_t>(T * h);
+  a.qkv = c.take<uint16_t>(3 * T * h);
+  a.o = c.take<uint16_t>(T * h);
+  a.lse = c.take<float>(d.batch * H * d.seq);
+  a.y = c.take<float>(T * h);
+  a.n2 = c.take<uint16_t>(T * h);
+  a.ug = c.take<uint16_t>(2 * T * f);
+  a.act = c.take<uint16_t>(T * f);
+  if (total) *total = c.off;
+  return a;
+}
+
+struct BlockWs {
+  uint16_t *g_bf, *d_act, *dug, *d_y_bf, *d_o, *dqkv;
+  float *d_n, *d_y, *dsum, *inv, *partial;
+};
+
+BlockWs carve_ws(const HlmBlockDims& d, void* buf, size_t* total) {
+  const i64 T = d.batch * d.seq, h = d.hidden, f = d.ffn, H = d.n_heads;
+  Carver c(buf);
+  BlockWs w;
+  w.g_bf = c.take<uint16_t>(T * h);
+  w.d_act = c.take<uint16_t>(T * f);
+  w.dug = c.take<uint16_t>(2 * T * f);
+  w.d_y_bf = c.take<uint16_t>(T * h);
+  w.d_o = c.take<uint16_t>(T * h);
+  w.dqkv = c.take<uint16_t>(3 * T * h);
+  w.d_n = c.take<float>(T * h);
+  w.d_y = c.take<float>(T * h);
+  w.dsum = c.take<float>(d.batch * H * d.seq);
+  w.inv = c.take<float>(T);
+  w.partial = c.take<float>(((T + HLM_NORM_ROWS_PER_CHUNK - 1) / HLM_NORM_ROWS_PER_CHUNK) * h);
+  if (total) *total = c.off;
+  return w;
+}
+
+// Tile offsets (elements), host_store.cpp:70-92.
+struct TileOff {
+  i64 q, o, up, down, norm1, norm2;
+  TileOff(i64 h, i64 f)
+      : q(0), o(3 * h * h), up(4 * h * h), down(4 * h * h + 2 * h * f), norm1(4 * h * h + 3 * h * f),
+        norm2(4 * h * h + 3 * h * f + h) {}
+};
+
+HlmGemmDesc gdesc(int M, int N, int K, const void* A, i64 lda, int a_mn, const void* B, i64 ldb, int b_mn,
+                  void* C, i64 ldc, int epi) {
+  HlmGemmDesc g{};
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.G = 1;
+  g.A = A;
+  g.lda = lda;
+  g.a_mn = a_mn;
+  g.B = B;
+  g.ldb = ldb;
+  g.b_mn = b_mn;
+  g.C = C;
+  g.ldc = ldc;
+  g.epi = epi;
+  return g;
+}
+
+struct Failure {
+  std::string msg;
+  int code;
+};
+
+void chk_gemm(const HlmGemmDesc& g, cudaStream_t s, const char* what) {
+  const int rc = hlm_gemm_launch(&g, s);
+  if (rc) throw Failure{std::string("gemm ") + what + " failed (code " + std::to_string(rc) + ")", HLM_ERR_CUDA};
+}
+void chk(int rc, const char* what) {
+  if (rc) {
+    const cudaError_t e = cudaGetLastError();
+    throw Failure{std::string(what) + " launch failed: " + cudaGetErrorString(e), HLM_ERR_CUDA};
+  }
+}
+
+void validate(const HlmBlockDims* d) {
+  if (!d || d->batch <= 0 || d->seq <= 0 || d->hidden <= 0 || d->ffn <= 0 || d->n_heads <= 0)
+    throw Failure{"block dims must be positive", HLM_ERR_CONFIG};
+  if (d->hidden % 8 || d->ffn % 8)
+    throw Failure{"hidden and ffn must be multiples of 8 (16-byte TMA rows)", HLM_ERR_CONFIG};
+  if (d->hidden % d->n_heads) throw Failure{"hidden must be divisible by n_heads", HLM_ERR_CONFIG};
+}
+
+template <typename F>
+int guarded(F&& fn) {
+  try {
+    fn();
+    return HLM_OK;
+  } catch (const Failure& f) {
+    hlm_capi::set_error(f.msg);
+    return f.code;
+  }
+}
+
+void attention_fwd(const HlmBlockDims& d, const uint16_t* q, const uint16_t* k, const uint16_t* v, uint16_t* o,
+                   float* lse, i64 ld, cudaStream_t s) {
+  const int hd = static_cast<int>(d.hidden / d.n_heads);
+  if (!(d.flags & HLM_BLOCK_GENERIC_ATTENTION) && hlm_flash_supported(hd, static_cast<int>(d.seq))) {
+    chk(hlm_flash_fwd(q, k, v, o, lse, (int)d.batch, (int)d.seq, (int)d.n_heads, hd, (int)ld, s), "flash fwd");
+  } else {
+    chk(hlm_ops_attention_fwd_generic(q, k, v, o, lse, (int)d.batch, (int)d.seq, (int)d.n_heads, hd, (int)ld, s),
+        "attention fwd");
+  }
+}
+
+void attention_bwd(const HlmBlockDims& d, const uint16_t* q, const uint16_t* k, const uint16_t* v,
+                   const uint16_t* o, const uint16_t* d_o, const float* lse, float* dsum, uint16_t* dq,
+                   uint16_t* dk, uint16_t* dv, i64 ld, cudaStream_t s) {
+  const int hd = static_cast<int>(d.hidden / d.n_heads);
+  if (!(d.flags & HLM_BLOCK_GENERIC_ATTENTION) && hlm_flash_supported(hd, static_cast<int>(d.seq))) {
+    chk(hlm_flash_bwd(q, k, v, o, d_o, lse, dsum, dq, dk, dv, (int)d.batch, (int)d.seq, (int)d.n_heads, hd,
+                      (int)ld, s),
+        "flash bwd");
+  } else {
+    chk(hlm_ops_attention_bwd_generic(q, k, v, o, d_o, lse, dsum, dq, dk, dv, (int)d.batch, (int)d.seq,
+                                      (int)d.n_heads, hd, (int)ld, s),
+        "attention bwd");
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t hlm_cuda_block_acts_bytes(const HlmBlockDims* d) {
+  size_t t = 0;
+  carve_acts(*d, nullptr, &t);
+  return t;
+}
+
+size_t hlm_cuda_block_ws_bytes(const HlmBlockDims* d) {
+  size_t t = 0;
+  carve_ws(*d, nullptr, &t);
+  return t;
+}
+
+int hlm_cuda_block_fwd(const HlmBlockDims* d, const void* w_tile, const float* h_in, float* h_out, void* acts,
+                       void* ws, const float* rope_cos, const float* rope_sin, void* stream) {
+  (void)ws;
+  return guarded([&] {
+    validate(d);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const i64 T = d->batch * d->seq, h = d->hidden, f = d->ffn;
+    const int Ti = (int)T, hi = (int)h, fi = (int)f;
+    const TileOff off(h, f);
+    const uint16_t* W = static_cast<const uint16_t*>(w_tile);
+    BlockActs a = carve_acts(*d, acts, nullptr);
+
+    chk(hlm_ops_rmsnorm_fwd(h_in, W + off.norm1, a.n1, T, hi, s), "rmsnorm1");
+    HlmGemmDesc g = gdesc(Ti, hi, hi, a.n1, h, 0, W + off.q, h, 1, a.qkv, h, HLM_EPI_BF16);
+    g.G = 3;
+    g.b_grouped = 1;
+    g.b_gstride = h * h;
+    g.c_gstride = T * h;
+    chk_gemm(g, s, "qkv");
+    if (rope_cos)
+      chk(hlm_ops_rope(a.qkv, rope_cos, rope_sin, T, hi, hi / d->n_heads, (int)d->seq, 0, 2, T * h, s), "rope");
+    attention_fwd(*d, a.qkv, a.qkv + T * h, a.qkv + 2 * T * h, a.o, a.lse, h, s);
+    g = gdesc(Ti, hi, hi, a.o, h, 0, W + off.o, h, 1, a.y, h, HLM_EPI_F32_ADD);
+    g.R = h_in;
+    g.ldr = h;
+    chk_gemm(g, s, "o-proj");
+    chk(hlm_ops_rmsnorm_fwd(a.y, W + off.norm2, a.n2, T, hi, s), "rmsnorm2");
+    g = gdesc(Ti, fi, hi, a.n2, h, 0, W + off.up, f, 1, a.ug, f, HLM_EPI_BF16);
+    g.G = 2;
+    g.b_grouped = 1;
+    g.b_gstride = h * f;
+    g.c_gstride = T * f;
+    chk_gemm(g, s, "up|gate");
+    chk(hlm_ops_swiglu_fwd(a.ug, a.act, T * f, s), "swiglu");
+    g = gdesc(Ti, hi, fi, a.act, f, 0, W + off.down, h, 1, h_out, h, HLM_EPI_F32_ADD);
+    g.R = a.y;
+    g.ldr = h;
+    chk_gemm(g, s, "down");
+  });
+}
+
+int hlm_cuda_block_bwd(const HlmBlockDims* d, const void* w_tile, const float* h_in, const void* acts,
+                       const float* g_out, float* g_in, float* grad_tile, void* ws, const float* rope_cos,
+                       const float* rope_sin, void* stream) {
+  return guarded([&] {
+    validate(d);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const i64 T = d->batch * d->seq, h = d->hidden, f = d->ffn;
+    const int Ti = (int)T, hi = (int)h, fi = (int)f;
+    const TileOff off(h, f);
+    const uint16_t* W = static_cast<const uint16_t*>(w_tile);
+    const BlockActs a = carve_acts(*d, const_cast<void*>(acts), nullptr);
+    BlockWs w = carve_ws(*d, ws, nullptr);
+    float* G = grad_tile;
+
+    // MLP branch
+    chk(hlm_ops_cast_bf16(g_out, w.g_bf, T * h, s), "cast g_out");
+    chk_gemm(gdesc(fi, hi, Ti, a.act, f, 1, w.g_bf, h, 1, G + off.down, h, HLM_EPI_F32), s, "wgrad down");
+    chk_gemm(gdesc(Ti, fi, hi, w.g_bf, h, 0, W + off.down, h, 0, w.d_act, f, HLM_EPI_BF16), s, "dgrad down");
+    chk(hlm_ops_swiglu_bwd(w.d_act, a.ug, w.dug, T * f, s), "swiglu bwd");
+    HlmGemmDesc g = gdesc(hi, fi, Ti, a.n2, h, 1, w.dug, f, 1, G + off.up, f, HLM_EPI_F32);
+    g.G = 2;
+    g.b_grouped = 1;
+    g.b_gstride = T * f;
+    g.c_gstride = h * f;
+    chk_gemm(g, s, "wgrad up|gate");
+    g = gdesc(Ti, hi, fi, w.dug, f, 0, W + off.up, f, 0, w.d_n, h, HLM_EPI_F32);
+    g.G = 2;
+    g.kgroup = 1;
+    g.a_grouped = 1;
+    g.a_gstride = T * f;
+    g.b_grouped = 1;
+    g.b_gstride = h * f;
+    chk_gemm(g, s, "dgrad up|gate");
+    chk(hlm_ops_rmsnorm_bwd(a.y, W + off.norm2, w.d_n, g_out, w.d_y, w.d_y_bf, w.inv, w.partial, G + off.norm2,
+                            T, hi, s),
+        "rmsnorm2 bwd");
+    // attention branch
+    chk_gemm(gdesc(hi, hi, Ti, a.o, h, 1, w.d_y_bf, h, 1, G + off.o, h, HLM_EPI_F32), s, "wgrad o");
+    chk_gemm(gdesc(Ti, hi, hi, w.d_y_bf, h, 0, W + off.o, h, 0, w.d_o, h, HLM_EPI_BF16), s, "dgrad o");
+    attention_bwd(*d, a.qkv, a.qkv + T * h, a.qkv + 2 * T * h, a.o, w.d_o, a.lse, w.dsum, w.dqkv, w.dqkv + T * h,
+                  w.dqkv + 2 * T * h, h, s);
+    if (rope_cos)
+      chk(hlm_ops_rope(w.dqkv, rope_cos, rope_sin, T, hi, hi / d->n_heads, (int)d->seq, 1, 2, T * h, s),
+          "rope bwd");
+    g = gdesc(hi, hi, Ti, a.n1, h, 1, w.dqkv, h, 1, G + off.q, h, HLM_EPI_F32);
+    g.G = 3;
+    g.b_grouped = 1;
+    g.b_gstride = T * h;
+    g.c_gstride = h * h;
+    chk_gemm(g, s, "wgrad qkv");
+    g = gdesc(Ti, hi, hi, w.dqkv, h, 0, W + off.q, h, 0, w.d_n, h, HLM_EPI_F32);
+    g.G = 3;
+    g.kgroup = 1;
+    g.a_grouped = 1;
+    g.a_gstride = T * h;
+    g.b_grouped = 1;
+    g.b_gstride = h * h;
+    chk_gemm(g, s, "dgrad qkv");
+    chk(hlm_ops_rmsnorm_bwd(h_in, W + off.norm1, w.d_n, w.d_y, g_in, nullptr, w.inv, w.partial, G + off.norm1, T,
+                            hi, s),
+        "rmsnorm1 bwd");
+  });
+}
+
+int hlm_cuda_rope_table(float* dev_cos, float* dev_sin, int64_t seq, int64_t head_dim, double theta) {
+  return guarded([&] {
+    if (head_dim % 2 || theta <= 0) throw Failure{"rope table: even head_dim and theta > 0 required", HLM_ERR_CONFIG};
+    const i64 half = head_dim / 2;
+    std::vector<float> c(static_cast<size_t>(seq * half)), sn(c.size());
+    for (i64 p = 0; p < seq; ++p)
+      for (i64 i = 0; i < half; ++i) {
+        // identical to oracle/hlm_oracle.cpp Rope (double math, fp32 angle)
+        const double inv = std::pow(theta, -2.0 * static_cast<double>(i) / static_cast<double>(head_dim));
+        const float ang = static_cast<float>(static_cast<double>(p) * inv);
+        c[p * half + i] = static_cast<float>(std::cos(static_cast<double>(ang)));
+        sn[p * half + i] = static_cast<float>(std::sin(static_cast<double>(ang)));
+      }
+    if (cudaMemcpy(dev_cos, c.data(), c.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(dev_sin, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+      throw Failure{"rope table copy failed", HLM_ERR_CUDA};
+  });
+}
+
+// ------------------------------------------------------------------ head + loss
+static i64 padded_vocab(i64 V) { return (V + 7) / 8 * 8; }
+
+size_t hlm_cuda_head_ws_bytes(int64_t rows, int64_t hidden, int64_t vocab) {
+  Carver c(nullptr);
+  const i64 ldv = padded_vocab(vocab);
+  c.take<uint16_t>(rows * hidden);
+  c.take<float>(rows * ldv);
+  c.take<uint16_t>(rows * ldv);
+  c.take<int>(4);
+  return c.off;
+}
+
+int hlm_cuda_head_loss(int64_t rows, int64_t hidden, int64_t vocab, const void* head, const float* x,
+                       const int32_t* targets, float inv_rows, float* d_x, float* d_head, int accumulate_d_head,
+                       float* loss_rows, void* ws, void* stream) {
+  return guarded([&] {
+    if (rows <= 0 || hidden <= 0 || vocab <= 0 || hidden % 8)
+      throw Failure{"head: bad dims (hidden must be a multiple of 8)", HLM_ERR_CONFIG};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const i64 ldv = padded_vocab(vocab);
+    Carver c(ws);
+    uint16_t* x_bf = c.take<uint16_t>(rows * hidden);
+    float* logits = c.take<float>(rows * ldv);
+    uint16_t* dl = c.take<uint16_t>(rows * ldv);
+    int* err = c.take<int>(4);
+    const int R = (int)rows, Hh = (int)hidden, V = (int)vocab;
+    chk(hlm_ops_cast_bf16(x, x_bf, rows * hidden, s), "cast x");
+    chk_gemm(gdesc(R, V, Hh, x_bf, hidden, 0, head, hidden, 0, logits, ldv, HLM_EPI_F32), s, "head fwd");
+    chk(hlm_ops_ce(logits, ldv, targets, dl, ldv, loss_rows, rows, V, inv_rows, err, s), "cross entropy");
+    chk_gemm(gdesc(R, Hh, V, dl, ldv, 0, head, hidden, 1, d_x, hidden, HLM_EPI_F32), s, "head dgrad");
+    HlmGemmDesc g = gdesc(V, Hh, R, dl, ldv, 1, x_bf, hidden, 1, d_head, hidden,
+                          accumulate_d_head ? HLM_EPI_F32_ADD : HLM_EPI_F32);
+    if (accumulate_d_head) {
+      g.R = d_head;
+      g.ldr = hidden;
+    }
+    chk_gemm(g, s, "head wgrad");
+  });
+}
+
+// ------------------------------------------------------------------ embedding
+int hlm_cuda_embed_fwd(const int32_t* tokens, const void* table, float* out, int64_t rows, int64_t hidden,
+                       int64_t vocab, int* err_flag, void* stream) {
+  return guarded([&] {
+    chk(hlm_ops_embed_fwd(tokens, table, out, rows, (int)hidden, (int)vocab, err_flag,
+                          static_cast<cudaStream_t>(stream)),
+        "embed fwd");
+  });
+}
+
+int hlm_cuda_embed_bwd(const int32_t* row_ptr, const int32_t* pos, const float* g, float* d_table, int64_t vocab,
+                       int64_t hidden, int accumulate, void* stream) {
+  return guarded([&] {
+    chk(hlm_ops_embed_bwd(row_ptr, pos, g, d_table, (int)vocab, (int)hidden, accumulate,
+                          static_cast<cudaStream_t>(stream)),
+        "embed bwd");
+  });
+}
+
+int hlm_embed_csr(const int32_t* tokens, int64_t rows, int64_t vocab, int32_t* row_ptr, int32_t* pos) {
+  for (int64_t v = 0; v <= vocab; ++v) row_ptr[v] = 0;
+  for (int64_t t = 0; t < rows; ++t) {
+    if (tokens[t] < 0 || tokens[t] >= vocab) {
+      hlm_capi::set_error("embed_bwd: token id out of range");
+      return HLM_ERR_RANGE;
+    }
+    ++row_ptr[tokens[t] + 1];
+  }
+  for (int64_t v = 0; v < vocab; ++v) row_ptr[v + 1] += row_ptr[v];
+  std::vector<int32_t> fill(row_ptr, row_ptr + vocab);
+  for (int64_t t = 0; t < rows; ++t) pos[fill[tokens[t]]++] = static_cast<int32_t>(t);
+  return HLM_OK;
+}
+
+// ------------------------------------------------------------------ small ops
+int hlm_cuda_cast_bf16(const float* in, void* out, int64_t n, void* stream) {
+  return guarded([&] { chk(hlm_ops_cast_bf16(in, out, n, static_cast<cudaStream_t>(stream)), "cast"); });
+}
+
+int hlm_cuda_attention_fwd(const HlmBlockDims* d, const void* q, const void* k, const void* v, void* o, float* lse,
+                           int64_t ld, void* stream) {
+  return guarded([&] {
+    validate(d);
+    attention_fwd(*d, (const uint16_t*)q, (const uint16_t*)k, (const uint16_t*)v, (uint16_t*)o, lse, ld,
+                  static_cast<cudaStream_t>(stream));
+  });
+}
+
+int hlm_cuda_attention_bwd(const HlmBlockDims* d, const void* q, const void* k, const void* v, const void* o,
+                           const void* d_o, const float* lse, float* dsum, void* dq, void* dk, void* dv, int64_t ld,
+                           void* stream) {
+  return guarded([&] {
+    validate(d);
+    attention_bwd(*d, (const uint16_t*)q, (const uint16_t*)k, (const uint16_t*)v, (const uint16_t*)o,
+                  (const uint16_t*)d_o, lse, dsum, (uint16_t*)dq, (uint16_t*)dk, (uint16_t*)dv, ld,
+                  static_cast<cudaStream_t>(stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,606 @@
+// Row-wise / elementwise kernels of the transformer block, head and embedding
+// (everything in reference proj/include/hlm/kernels.hpp that is not a GEMM):
+//   rmsnorm_fwd / rmsnorm_bwd        kernels.hpp:129-162
+//   SwiGLU fwd / bwd                 kernels.hpp:301-311, 329, 342-347
+//   embed gather / scatter-add       kernels.hpp:385-408
+//   cross entropy + d_logits         kernels.hpp:423-446
+//   RoPE (extension, Qwen2 rotate-half)
+// All HBM-bound: 16-byte vector accesses, one warp per row for row
+// reductions, fixed-order (deterministic) reductions everywhere.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "block_ops.h"
+
+namespace {
+
+constexpr float kEps = 1e-6f;   // kernels.hpp:127
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float bf(const __nv_bfloat16 x) { return __bfloat162float(x); }
+
+int grid_for(long long n, int per_block) {
+  long long g = (n + per_block - 1) / per_block;
+  if (g > 148LL * 64) g = 148LL * 64;
+  return static_cast<int>(g < 1 ? 1 : g);
+}
+
+// ------------------------------------------------------------------ RMSNorm
+// out_bf16[r] = x[r] * inv_rms(x[r]) * scale ; one warp per row.
+__global__ void rmsnorm_fwd_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ scale,
+                                   __nv_bfloat16* __restrict__ out, long long rows, int h) {
+  const long long warps = (long long)gridDim.x * (blockDim.x / 32);
+  const int lane = threadIdx.x & 31;
+  for (long long r = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; r < rows; r += warps) {
+    const float* xr = x + r * h;
+    float ss = 0.f;
+    if ((h & 3) == 0) {
+      for (int j = lane * 4; j < h; j += 128) {
+        const float4 v = *reinterpret_cast<const float4*>(xr + j);
+        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+      }
+    } else {
+      for (int j = lane; j < h; j += 32) ss += xr[j] * xr[j];
+    }
+    ss = warp_sum(ss);
+    const float inv = 1.0f / sqrtf(ss / (float)h + kEps);
+    __nv_bfloat16* o = out + r * h;
+    if ((h & 3) == 0) {
+      for (int j = lane * 4; j < h; j += 128) {
+        const float4 v = *reinterpret_cast<const float4*>(xr + j);
+        __nv_bfloat162 a = __floats2bfloat162_rn(v.x * inv * bf(scale[j]), v.y * inv * bf(scale[j + 1]));
+        __nv_bfloat162 b = __floats2bfloat162_rn(v.z * inv * bf(scale[j + 2]), v.w * inv * bf(scale[j + 3]));
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&a);
+        pk.y = *reinterpret_cast<uint32_t*>(&b);
+        *reinterpret_cast<uint2*>(o + j) = pk;
+      }
+    } else {
+      for (int j = lane; j < h; j += 32) o[j] = __float2bfloat16_rn(xr[j] * inv * bf(scale[j]));
+    }
+  }
+}
+
+// g_x = g*s*inv - inv^3 * (sum g*s*x)/h * x ;  out = g_x + resid ; also the
+// per-row inv (consumed by the deterministic scale-gradient reduction).
+__global__ void rmsnorm_bwd_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ scale,
+                                   const float* __restrict__ g, const float* __restrict__ resid,
+                                   float* __restrict__ out, __nv_bfloat16* __restrict__ out_bf,
+                                   float* __restrict__ inv_out, long long rows, int h) {
+  const long long warps = (long long)gridDim.x * (blockDim.x / 32);
+  const int lane = threadIdx.x & 31;
+  for (long long r = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; r < rows; r += warps) {
+    const float* xr = x + r * h;
+    const float* gr = g + r * h;
+    float ss = 0.f, dot = 0.f;
+    for (int j = lane; j < h; j += 32) {
+      const float xv = xr[j];
+      ss += xv * xv;
+      dot += gr[j] * bf(scale[j]) * xv;
+    }
+    ss = warp_sum(ss);
+    dot = warp_sum(dot);
+    const float inv = 1.0f / sqrtf(ss / (float)h + kEps);
+    const float c = inv * inv * inv * dot / (float)h;
+    if (lane == 0) inv_out[r] = inv;
+    const float* rr = resid ? resid + r * h : nullptr;
+    for (int j = lane; j < h; j += 32) {
+      float v = gr[j] * bf(scale[j]) * inv - c * xr[j];
+      if (rr) v += rr[j];
+      out[r * h + j] = v;
+      if (out_bf) out_bf[r * h + j] = __float2bfloat16_rn(v);
+    }
+  }
+}
+
+// partial[c][j] = sum_{r in chunk c} g[r][j] * x[r][j] * inv[r]   (columns across threads)
+__global__ void norm_scale_partial_kernel(const float* __restrict__ x, const float* __restrict__ g,
+                                          const float* __restrict__ inv, float* __restrict__ partial,
+                                          long long rows, int h, int rows_per_chunk) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (j >= h) return;
+  const long long r0 = (long long)c * rows_per_chunk;
+  const long long r1 = r0 + rows_per_chunk < rows ? r0 + rows_per_chunk : rows;
+  float acc = 0.f;
+  for (long long r = r0; r < r1; ++r) acc += g[r * h + j] * x[r * h + j] * inv[r];
+  partial[(long long)c * h + j] = acc;
+}
+
+__global__ void norm_scale_reduce_kernel(const float* __restrict__ partial, float* __restrict__ out,
+                                         int chunks, int h) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= h) return;
+  float acc = 0.f;
+  for (int c = 0; c < chunks; ++c) acc += partial[(long long)c * h + j];
+  out[j] = acc;
+}
+
+// ------------------------------------------------------------------ casts
+__global__ void cast_f32_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out, long long n) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long n4 = n / 4;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const float4 v = reinterpret_cast<const float4*>(in)[i];
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&a);
+    pk.y = *reinterpret_cast<uint32_t*>(&b);
+    reinterpret_cast<uint2*>(out)[i] = pk;
+  }
+  for (long long i = n4 * 4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = __float2bfloat16_rn(in[i]);
+}
+
+// ------------------------------------------------------------------ SwiGLU
+__device__ __forceinline__ float silu_f(float z) { return z * (1.0f / (1.0f + __expf(-z))); }
+
+// act = up * silu(gate) ; ug = [2][rows][f] (up then gate)
+__global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ ug, __nv_bfloat16* __restrict__ act,
+                                  long long n) {
+  const __nv_bfloat16* up = ug;
+  const __nv_bfloat16* gate = ug + n;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 8; i < n; i += stride * 8) {
+    if (i + 8 <= n) {
+      const uint4 u = *reinterpret_cast<const uint4*>(up + i);
+      const uint4 gg = *reinterpret_cast<const uint4*>(gate + i);
+      const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+      const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gg);
+      uint4 o;
+      __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 uf = __bfloat1622float2(u2[k]), gf = __bfloat1622float2(g2[k]);
+        o2[k] = __floats2bfloat162_rn(uf.x * silu_f(gf.x), uf.y * silu_f(gf.y));
+      }
+      *reinterpret_cast<uint4*>(act + i) = o;
+    } else {
+      for (long long k = i; k < n; ++k) act[k] = __float2bfloat16_rn(bf(up[k]) * silu_f(bf(gate[k])));
+    }
+  }
+}
+
+// d_up = d_act * silu(gate) ; d_gate = d_act * up * silu'(gate)  -> dug [2][rows][f]
+__global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ dact, const __nv_bfloat16* __restrict__ ug,
+                                  __nv_bfloat16* __restrict__ dug, long long n) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float da = bf(dact[i]), u = bf(ug[i]), z = bf(ug[n + i]);
+    const float s = 1.0f / (1.0f + __expf(-z));
+    dug[i] = __float2bfloat16_rn(da * z * s);
+    dug[n + i] = __float2bfloat16_rn(da * u * (s * (1.0f + z * (1.0f - s))));
+  }
+}
+
+// ------------------------------------------------------------------ RoPE
+// rotate-half per head on x (rows, h) bf16, in place; inverse for backward.
+__global__ void rope_kernel(__nv_bfloat16* __restrict__ x, const float* __restrict__ cs,
+                            const float* __restrict__ sn, long long rows, int h, int hd, int S,
+                            int inverse, int nmats, long long mat_stride) {
+  const int half = hd / 2;
+  const long long pairs = rows * (h / 2);
+  const long long total = pairs * nmats;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+    const int m = (int)(t / pairs);
+    const long long p = t - (long long)m * pairs;
+    const long long r = p / (h / 2);
+    const int k = (int)(p - r * (h / 2));
+    const int head = k / half, i = k - head * half;
+    const int pos = (int)(r % S);
+    __nv_bfloat16* v = x + m * mat_stride + r * h + head * hd;
+    const float c = cs[pos * half + i], s = sn[pos * half + i];
+    const float a = bf(v[i]), b = bf(v[i + half]);
+    if (!inverse) {
+      v[i] = __float2bfloat16_rn(a * c - b * s);
+      v[i + half] = __float2bfloat16_rn(b * c + a * s);
+    } else {
+      v[i] = __float2bfloat16_rn(a * c + b * s);
+      v[i + half] = __float2bfloat16_rn(b * c - a * s);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ embedding
+__global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ table,
+                                 float* __restrict__ out, long long rows, int h, int vocab,
+                                 int* __restrict__ err) {
+  const long long n = rows * h;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const long long r = i / h;
+    const int j = (int)(i - r * h);
+    const int id = tok[r];
+    if (id < 0 || id >= vocab) {
+      if (j == 0) atomicOr(err, 1);
+      out[i] = 0.f;
+      continue;
+    }
+    out[i] = bf(table[(long long)id * h + j]);
+  }
+}
+
+// d_table[v][j] = sum over positions p of token v (ascending) of g[p][j]:
+// the reference's in-order scatter-add (kernels.hpp:396-408) without atomics,
+// driven by a host-built CSR (row_ptr[V+1], pos[]) of the batch tokens.
+__global__ void embed_bwd_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ pos,
+                                 const float* __restrict__ g, float* __restrict__ d_table, int vocab, int h,
+                                 int accumulate) {
+  const long long n = (long long)vocab * h;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int v = (int)(i / h);
+    const int j = (int)(i - (long long)v * h);
+    float acc = accumulate ? d_table[i] : 0.f;
+    for (int k = row_ptr[v]; k < row_ptr[v + 1]; ++k) acc += g[(long long)pos[k] * h + j];
+    d_table[i] = acc;
+  }
+}
+
+// ------------------------------------------------------------------ cross entropy
+// One CTA per row. loss_row[r] = (logz - l[tgt]) * inv_rows ;
+// d_logits = (softmax - onehot) * inv_rows (bf16, row stride ld).
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) ce_kernel(const float* __restrict__ logits, long long ld_in,
+                                                     const int32_t* __restrict__ tgt,
+                                                     __nv_bfloat16* __restrict__ dl, long long ld_out,
+                                                     float* __restrict__ loss_row, int vocab, float inv_rows,
+                                                     int* __restrict__ err) {
+  __shared__ float red[THREADS / 32];
+  __shared__ float bcast;
+  const long long r = blockIdx.x;
+  const float* l = logits + r * ld_in;
+  const int lane = threadIdx.x & 31, w = threadIdx.x / 32;
+  float mx = -INFINITY;
+  for (int v = threadIdx.x; v < vocab; v += THREADS) mx = fmaxf(mx, l[v]);
+  mx = warp_max(mx);
+  if (lane == 0) red[w] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = red[0];
+    for (int i = 1; i < THREADS / 32; ++i) m = fmaxf(m, red[i]);
+    bcast = m;
+  }
+  __syncthreads();
+  mx = bcast;
+  float z = 0.f;
+  for (int v = threadIdx.x; v < vocab; v += THREADS) z += __expf(l[v] - mx);
+  z = warp_sum(z);
+  __syncthreads();
+  if (lane == 0) red[w] = z;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int i = 0; i < THREADS / 32; ++i) s += red[i];
+    bcast = s;
+  }
+  __syncthreads();
+  z = bcast;
+  const int t = tgt[r];
+  const bool ok = t >= 0 && t < vocab;
+  const float invz = 1.0f / z;
+  __nv_bfloat16* d = dl + r * ld_out;
+  for (int v = threadIdx.x; v < vocab; v += THREADS) {
+    float p = __expf(l[v] - mx) * invz * inv_rows;
+    if (v == t) p -= inv_rows;
+    d[v] = __float2bfloat16_rn(p);
+  }
+  for (int v = vocab + threadIdx.x; v < ld_out; v += THREADS) d[v] = __float2bfloat16_rn(0.f);
+  if (threadIdx.x == 0) {
+    if (!ok) {
+      atomicOr(err, 2);
+      loss_row[r] = 0.f;
+    } else {
+      loss_row[r] = (logf(z) + mx - l[t]) * inv_rows;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ generic attention
+// Causal softmax attention for any head_dim <= 32*VPL: one warp per
+// (batch, head, query row), online softmax over keys j <= i in fp32.
+// Reference-semantics path (single head, head_dim = h) and small shapes;
+// the tensor-core flash kernel (attention_sm100.cu) serves head_dim 64/128.
+template <int VPL>
+__global__ void attn_fwd_generic(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
+                                 const __nv_bfloat16* __restrict__ v, __nv_bfloat16* __restrict__ o,
+                                 float* __restrict__ lse, int B, int S, int H, int hd, int ld, float scale) {
+  const long long total = (long long)B * H * S;
+  const long long gw = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (gw >= total) return;
+  const int lane = threadIdx.x & 31;
+  const int i = (int)(gw % S);
+  const int hh = (int)((gw / S) % H);
+  const int b = (int)(gw / ((long long)S * H));
+  const long long base = (long long)b * S * ld + (long long)hh * hd;
+  float qv[VPL], acc[VPL];
+#pragma unroll
+  for (int e = 0; e < VPL; ++e) {
+    const int d = lane + 32 * e;
+    qv[e] = d < hd ? bf(q[base + (long long)i * ld + d]) : 0.f;
+    acc[e] = 0.f;
+  }
+  float m = -INFINITY, l = 0.f;
+  for (int j = 0; j <= i; ++j) {
+    float s = 0.f;
+#pragma unroll
+    for (int e = 0; e < VPL; ++e) {
+      const int d = lane + 32 * e;
+      if (d < hd) s += qv[e] * bf(k[base + (long long)j * ld + d]);
+    }
+    s = warp_sum(s) * scale;
+    const float mn = fmaxf(m, s);
+    const float corr = __expf(m - mn);
+    const float p = __expf(s - mn);
+    l = l * corr + p;
+#pragma unroll
+    for (int e = 0; e < VPL; ++e) {
+      const int d = lane + 32 * e;
+      acc[e] = acc[e] * corr + (d < hd ? p * bf(v[base + (long long)j * ld + d]) : 0.f);
+    }
+    m = mn;
+  }
+  const float il = 1.0f / l;
+#pragma unroll
+  for (int e = 0; e < VPL; ++e) {
+    const int d = lane + 32 * e;
+    if (d < hd) o[base + (long long)i * ld + d] = __float2bfloat16_rn(acc[e] * il);
+  }
+  if (lane == 0) lse[((long long)b * H + hh) * S + i] = m + logf(l);
+}
+
+// Dsum[b,h,i] = sum_d dO[i,d] * O[i,d]
+__global__ void attn_bwd_dsum(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
+                              float* __restrict__ dsum, int B, int S, int H, int hd, int ld) {
+  const long long total = (long long)B * H * S;
+  const long long gw = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (gw >= total) return;
+  const int lane = threadIdx.x & 31;
+  const int i = (int)(gw % S);
+  const int hh = (int)((gw / S) % H);
+  const int b = (int)(gw / ((long long)S * H));
+  const long long row = ((long long)b * S + i) * ld + (long long)hh * hd;
+  float s = 0.f;
+  for (int d = lane; d < hd; d += 32) s += bf(o[row + d]) * bf(dout[row + d]);
+  s = warp_sum(s);
+  if (lane == 0) dsum[((long long)b * H + hh) * S + i] = s;
+}
+
+// dQ_i = scale * sum_{j<=i} P_ij (dP_ij - D_i) K_j  (one warp per query row)
+template <int VPL>
+__global__ void attn_bwd_dq_generic(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
+                                    const __nv_bfloat16* __restrict__ v, const __nv_bfloat16* __restrict__ dout,
+                                    const float* __restrict__ lse, const float* __restrict__ dsum,
+                                    __nv_bfloat16* __restrict__ dq, int B, int S, int H, int hd, int ld,
+                                    float scale) {
+  const long long total = (long long)B * H * S;
+  const long long gw = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (gw >= total) return;
+  const int lane = threadIdx.x & 31;
+  const int i = (int)(gw % S);
+  const int hh = (int)((gw / S) % H);
+  const int b = (int)(gw / ((long long)S * H));
+  const long long base = (long long)b * S * ld + (long long)hh * hd;
+  const long long st = ((long long)b * H + hh) * S;
+  float qv[VPL], dov[VPL], acc[VPL];
+#pragma unroll
+  for (int e = 0; e < VPL; ++e) {
+    const int d = lane + 32 * e;
+    qv[e] = d < hd ? bf(q[base + (long long)i * ld + d]) : 0.f;
+    dov[e] = d < hd ? bf(dout[base + (long long)i * ld + d]) : 0.f;
+    acc[e] = 0.f;
+  }
+  const float L = lse[st + i], D = dsum[st + i];
+  for (int j = 0; j <= i; ++j) {
+    float s = 0.f, dp = 0.f;
+#pragma unroll
+    for (int e = 0; e < VPL; ++e) {
+      const int d = lane + 32 * e;
+      if (d < hd) {
+        s += qv[e] * bf(k[base + (long long)j * ld + d]);
+        dp += dov[e] * bf(v[base + (long long)j * ld + d]);
+      }
+    }
+    s = warp_sum(s) * scale;
+    dp = warp_sum(dp);
+    const float p = __expf(s - L);
+    const float ds = p * (dp - D) * scale;
+#pragma unroll
+    for (int e = 0; e < VPL; ++e) {
+      const int d = lane + 32 * e;
+      if (d < hd) acc[e] += ds * bf(k[base + (long long)j * ld + d]);
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < VPL; ++e) {
+    const int d = lane + 32 * e;
+    if (d < hd) dq[base + (long long)i * ld + d] = __float2bfloat16_rn(acc[e]);
+  }
+}
+
+// dV_j = sum_{i>=j} P_ij dO_i ; dK_j = scale * sum_{i>=j} P_ij (dP_ij - D_i) Q_i  (warp per key row)
+template <int VPL>
+__global__ void attn_bwd_dkv_generic(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
+                                     const __nv_bfloat16* __restrict__ v, const __nv_bfloat16* __restrict__ dout,
+                                     const float* __restrict__ lse, const float* __restrict__ dsum,
+                                     __nv_bfloat16* __restrict__ dk, __nv_bfloat16* __restrict__ dv, int B,
+                                     int S, int H, int hd, int ld, float scale) {
+  const long long total = (long long)B * H * S;
+  const long long gw = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (gw >= total) return;
+  const int lane = threadIdx.x & 31;
+  const int j = (int)(gw % S);
+  const int hh = (int)((gw / S) % H);
+  const int b = (int)(gw / ((long long)S * H));
+  const long long base = (long long)b * S * ld + (long long)hh * hd;
+  const long long st = ((long long)b * H + hh) * S;
+  float kv[VPL], vv[VPL], adk[VPL], adv[VPL];
+#pragma unroll
+  for (int e = 0; e < VPL; ++e) {
+    const int d = lane + 32 * e;
+    kv[e] = d < hd ? bf(k[base + (long long)j * ld + d]) : 0.f;
+    vv[e] = d < hd ? bf(v[base + (long long)j * ld + d]) : 0.f;
+    adk[e] = 0.f;
+    adv[e] = 0.f;
+  }
+  for (int i = j; i < S; ++i) {
+    float s = 0.f, dp = 0.f;
+    float qi[VPL], doi[VPL];
+#pragma unroll
+    for (int e = 0; e < VPL; ++e) {
+      const int d = lane + 32 * e;
+      qi[e] = d < hd ? bf(q[base + (long long)i * ld + d]) : 0.f;
+      doi[e] = d < hd ? bf(dout[base + (long long)i * ld + d]) : 0.f;
+      s += qi[e] * kv[e];
+      dp += doi[e] * vv[e];
+    }
+    s = warp_sum(s) * scale;
+    dp = warp_sum(dp);
+    const float p = __expf(s - lse[st + i]);
+    const float ds = p * (dp - dsum[st + i]) * scale;
+#pragma unroll
+    for (int e = 0; e < VPL; ++e) {
+      adv[e] += p * doi[e];
+      adk[e] += ds * qi[e];
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < VPL; ++e) {
+    const int d = lane + 32 * e;
+    if (d < hd) {
+      dk[base + (long long)j * ld + d] = __float2bfloat16_rn(adk[e]);
+      dv[base + (long long)j * ld + d] = __float2bfloat16_rn(adv[e]);
+    }
+  }
+}
+
+template <template <int> class K>
+struct Dummy {};
+
+}  // namespace
+
+// ====================================================================== launchers
+#define HLM_CHECK_LAUNCH() return cudaGetLastError() == cudaSuccess ? 0 : 1
+
+int hlm_ops_rmsnorm_fwd(const float* x, const void* scale, void* out, long long rows, int h, cudaStream_t s) {
+  rmsnorm_fwd_kernel<<<grid_for(rows, 8), 256, 0, s>>>(x, (const __nv_bfloat16*)scale, (__nv_bfloat16*)out, rows, h);
+  HLM_CHECK_LAUNCH();
+}
+
+int hlm_ops_rmsnorm_bwd(const float* x, const void* scale, const float* g, const float* resid, float* out,
+                        void* out_bf, float* inv_buf, float* partial, float* dscale, long long rows, int h,
+                        cudaStream_t s) {
+  rmsnorm_bwd_kernel<<<grid_for(rows, 8), 256, 0, s>>>(x, (const __nv_bfloat16*)scale, g, resid, out,
+                                                       (__nv_bfloat16*)out_bf, inv_buf, rows, h);
+  const int rpc = HLM_NORM_ROWS_PER_CHUNK;
+  const int chunks = (int)((rows + rpc - 1) / rpc);
+  dim3 grid((h + 255) / 256, chunks);
+  norm_scale_partial_kernel<<<grid, 256, 0, s>>>(x, g, inv_buf, partial, rows, h, rpc);
+  norm_scale_reduce_kernel<<<(h + 255) / 256, 256, 0, s>>>(partial, dscale, chunks, h);
+  HLM_CHECK_LAUNCH();
+}
+
+int hlm_ops_cast_bf16(const float* in, void* out, long long n, cudaStream_t s) {
+  cast_f32_bf16_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, s>>>(in, (__nv_bfloat16*)out, n);
+  HLM_CHECK_LAUNCH();
+}
+
+int hlm_ops_swiglu_fwd(const void* ug, void* act, long long n, cudaStream_t s) {
+  swiglu_fwd_kernel<<<grid_for(n / 8 + 1, 256), 256, 0, s>>>((const __nv_bfloat16*)ug, (__nv_bfloat16*)act, n);
+  HLM_CHECK_LAUNCH();
+}
+
+int hlm_ops_swiglu_bwd(const void* dact, const void* ug, void* dug, long long n, cudaStream_t s) {
+  swiglu_bwd_kernel<<<grid_for(n, 256), 256, 0, s>>>((const __nv_bfloat16*)dact, (const __nv_bfloat16*)ug,
+                                                    (__nv_bfloat16*)dug, n);
+  HLM_CHECK_LAUNCH();
+}
+
+int hlm_ops_rope(void* x, const float* cs, const float* sn, long long rows, int h, int hd, int S, int inverse,
+                 int nmats, long long mat_stride, cudaStream_t s) {
+  rope_kernel<<<grid_for(rows * (h / 2) * nmats, 256), 256, 0, s>>>((__nv_bfloat16*)x, cs, sn, rows, h, hd, S,
+                                                                     inverse, nmats, mat_stride);
+  HLM_CHECK_LAUNCH();
+}
+
+int hlm_ops_embed_fwd(const int32_t* tok, const void* table, float* out, long long rows, int h, int vocab,
+                      int* err, cudaStream_t s) {
+  embed_fwd_kernel<<<grid_for(rows * h, 256), 256, 0, s>>>(tok, (const __nv_bfloat16*)table, out, rows, h, vocab, err);
+  HLM_CHECK_LAUNCH();
+}
+
+int hlm_ops_embed_bwd(const int32_t* row_ptr, const int32_t* pos, const float* g, float* d_table, int vocab,
+                      int h, int accumulate, cudaStream_t s) {
+  embed_bwd_kernel<<<grid_for((long long)vocab * h, 256), 256, 0, s>>>(row_ptr, pos, g, d_table, vocab, h, accumulate);
+  HLM_CHECK_LAUNCH();
+}
+
+int hlm_ops_ce(const float* logits, long long ld_in, const int32_t* tgt, void* dl, long long ld_out,
+               float* loss_row, long long rows, int vocab, float inv_rows, int* err, cudaStream_t s) {
+  ce_kernel<512><<<(unsigned)rows, 512, 0, s>>>(logits, ld_in, tgt, (__nv_bfloat16*)dl, ld_out, loss_row, vocab,
+                                                inv_rows, err);
+  HLM_CHECK_LAUNCH();
+}
+
+namespace {
+template <int VPL>
+int attn_generic(const void* q, const void* k, const void* v, void* o, float* lse, int B, int S, int H, int hd,
+                 int ld, cudaStream_t s) {
+  const long long warps = (long long)B * H * S;
+  attn_fwd_generic<VPL><<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(
+      (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, (const __nv_bfloat16*)v, (__nv_bfloat16*)o, lse, B, S, H,
+      hd, ld, 1.0f / sqrtf((float)hd));
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+template <int VPL>
+int attn_bwd_generic(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                     const float* lse, float* dsum, void* dq, void* dk, void* dv, int B, int S, int H, int hd,
+                     int ld, cudaStream_t s) {
+  const long long warps = (long long)B * H * S;
+  const unsigned grid = (unsigned)((warps + 7) / 8);
+  const float scale = 1.0f / sqrtf((float)hd);
+  attn_bwd_dsum<<<grid, 256, 0, s>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, dsum, B, S, H, hd, ld);
+  attn_bwd_dq_generic<VPL><<<grid, 256, 0, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
+                                                (const __nv_bfloat16*)v, (const __nv_bfloat16*)dout, lse, dsum,
+                                                (__nv_bfloat16*)dq, B, S, H, hd, ld, scale);
+  attn_bwd_dkv_generic<VPL><<<grid, 256, 0, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
+                                                 (const __nv_bfloat16*)v, (const __nv_bfloat16*)dout, lse, dsum,
+                                                 (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, B, S, H, hd, ld, scale);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+}  // namespace
+
+int hlm_ops_attention_fwd_generic(const void* q, const void* k, const void* v, void* o, float* lse, int B, int S,
+                                  int H, int hd, int ld, cudaStream_t s) {
+  if (hd <= 32) return attn_generic<1>(q, k, v, o, lse, B, S, H, hd, ld, s);
+  if (hd <= 64) return attn_generic<2>(q, k, v, o, lse, B, S, H, hd, ld, s);
+  if (hd <= 128) return attn_generic<4>(q, k, v, o, lse, B, S, H, hd, ld, s);
+  if (hd <= 256) return attn_generic<8>(q, k, v, o, lse, B, S, H, hd, ld, s);
+  if (hd <= 512) return attn_generic<16>(q, k, v, o, lse, B, S, H, hd, ld, s);
+  if (hd <= 1024) return attn_generic<32>(q, k, v, o, lse, B, S, H, hd, ld, s);
+  return 2;
+}
+
+int hlm_ops_attention_bwd_generic(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                                  const float* lse, float* dsum, void* dq, void* dk, void* dv, int B, int S, int H,
+                                  int hd, int ld, cudaStream_t s) {
+  if (hd <= 32) return attn_bwd_generic<1>(q, k, v, o, dout, lse, dsum, dq, dk, dv, B, S, H, hd, ld, s);
+  if (hd <= 64) return attn_bwd_generic<2>(q, k, v, o, dout, lse, dsum, dq, dk, dv, B, S, H, hd, ld, s);
+  if (hd <= 128) return attn_bwd_generic<4>(q, k, v, o, dout, lse, dsum, dq, dk, dv, B, S, H, hd, ld, s);
+  if (hd <= 256) return attn_bwd_generic<8>(q, k, v, o, dout, lse, dsum, dq, dk, dv, B, S, H, hd, ld, s);
+  if (hd <= 512) return attn_bwd_generic<16>(q, k, v, o, dout, lse, dsum, dq, dk, dv, B, S, H, hd, ld, s);
+  if (hd <= 1024) return attn_bwd_generic<32>(q, k, v, o, dout, lse, dsum, dq, dk, dv, B, S, H, hd, ld, s);
+  return 2;
+}

@@ -1,0 +1,29 @@
+// Internal launchers of block_ops.cu (return 0 on a clean launch).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#define HLM_NORM_ROWS_PER_CHUNK 64
+
+int hlm_ops_rmsnorm_fwd(const float* x, const void* scale, void* out, long long rows, int h, cudaStream_t s);
+int hlm_ops_rmsnorm_bwd(const float* x, const void* scale, const float* g, const float* resid, float* out,
+                        void* out_bf, float* inv_buf, float* partial, float* dscale, long long rows, int h,
+                        cudaStream_t s);
+int hlm_ops_cast_bf16(const float* in, void* out, long long n, cudaStream_t s);
+int hlm_ops_swiglu_fwd(const void* ug, void* act, long long n, cudaStream_t s);
+int hlm_ops_swiglu_bwd(const void* dact, const void* ug, void* dug, long long n, cudaStream_t s);
+int hlm_ops_rope(void* x, const float* cs, const float* sn, long long rows, int h, int hd, int S, int inverse,
+                 int nmats, long long mat_stride, cudaStream_t s);
+int hlm_ops_embed_fwd(const int32_t* tok, const void* table, float* out, long long rows, int h, int vocab,
+                      int* err, cudaStream_t s);
+int hlm_ops_embed_bwd(const int32_t* row_ptr, const int32_t* pos, const float* g, float* d_table, int vocab,
+                      int h, int accumulate, cudaStream_t s);
+int hlm_ops_ce(const float* logits, long long ld_in, const int32_t* tgt, void* dl, long long ld_out,
+               float* loss_row, long long rows, int vocab, float inv_rows, int* err, cudaStream_t s);
+int hlm_ops_attention_fwd_generic(const void* q, const void* k, const void* v, void* o, float* lse, int B, int S,
+                                  int H, int hd, int ld, cudaStream_t s);
+int hlm_ops_attention_bwd_generic(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                                  const float* lse, float* dsum, void* dq, void* dk, void* dv, int B, int S, int H,
+                                  int hd, int ld, cudaStream_t s);
