@@ -1,0 +1,145 @@
+// Device memory of the B200 engine: ONE cudaMalloc sized by the footprint
+// formulas (footprint.hpp), carved into the reference's regions
+// (proj/include/hlm/device_arena.hpp:25-185): two weight stream buffers, a
+// LIFO activation stack (K block-activation slabs), checkpoint anchors and a
+// fixed workspace. Nothing is allocated after construction; every claim and
+// release goes through the exact ledger and over-claims throw ArenaOomError
+// naming the region.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "hlm/errors.hpp"
+#include "hlm/footprint.hpp"
+#include "hlm/model_config.hpp"
+
+namespace hlm {
+
+enum class Region : int { Stream0 = 0, Stream1 = 1, Stack = 2, Anchors = 3, Workspace = 4 };
+inline constexpr int kRegionCount = 5;
+const char* region_name(Region r);
+
+struct LedgerEvent {
+    int region;
+    i64 delta;
+};
+
+class ArenaLedger {
+public:
+    void init_region(Region r, i64 capacity) { cap_[static_cast<int>(r)] = capacity; }
+    void claim(Region r, i64 bytes);
+    void release(Region r, i64 bytes);
+    void begin_step();
+    i64 capacity(Region r) const { return cap_[static_cast<int>(r)]; }
+    i64 current(Region r) const { return cur_[static_cast<int>(r)]; }
+    i64 step_peak(Region r) const { return peak_[static_cast<int>(r)]; }
+    i64 total_capacity() const;
+    i64 total_current() const { return total_cur_; }
+    i64 step_peak_total() const { return total_peak_; }
+    i64 step_peak_non_anchor() const { return na_peak_; }
+    const std::vector<LedgerEvent>& events() const { return events_; }
+
+private:
+    std::array<i64, kRegionCount> cap_{}, cur_{}, peak_{};
+    i64 total_cur_ = 0, total_peak_ = 0, na_cur_ = 0, na_peak_ = 0;
+    std::vector<LedgerEvent> events_;
+};
+
+struct ArenaSnapshot {
+    struct RegionStat {
+        std::string name;
+        i64 capacity, current, step_peak;
+    };
+    std::vector<RegionStat> regions;
+    i64 committed_total = 0;
+    i64 committed_core = 0;
+    i64 step_peak_total = 0;
+    i64 step_peak_non_anchor = 0;
+};
+
+class DeviceArena {
+public:
+    // budget_cap: hard limit the footprint must fit (first region that does
+    // not fit is named in the ArenaOomError). device: CUDA ordinal.
+    DeviceArena(const ModelConfig& config, std::optional<i64> budget_cap = std::nullopt, int device = -1);
+    ~DeviceArena();
+    DeviceArena(const DeviceArena&) = delete;
+    DeviceArena& operator=(const DeviceArena&) = delete;
+
+    const ModelConfig& config() const { return cfg_; }
+    const ArenaFootprint& footprint() const { return fp_; }
+    int device() const { return device_; }
+    void begin_step();
+    ArenaSnapshot snapshot() const;
+    const ArenaLedger& ledger() const { return ledger_; }
+
+    // stream buffers: claim on H2D issue, release when its last reader finished
+    void* claim_buffer(int i, i64 layer_id, i64 bytes);
+    void release_buffer(int i);
+    i64 buffer_occupant(int i) const { return occupant_[i]; }
+    void* buffer(int i) const { return stream_[i]; }
+    i64 h2d_bytes() const { return h2d_bytes_; }
+    void add_h2d(i64 bytes) { h2d_bytes_ += bytes; }
+
+    // activation stack (LIFO, K slabs of A_max)
+    void* push_acts();
+    void pop_acts();
+    void* acts_at(i64 depth) const;
+    i64 stack_depth() const { return depth_; }
+
+    // anchors at multiples of K
+    float* anchor_checkpoint(i64 layer_index);     // claims the slot, returns it for writing
+    const float* load_checkpoint(i64 layer_index) const;
+    void release_checkpoint(i64 layer_index);
+
+    // workspace
+    void claim_workspace();
+    void release_workspace();
+    float* g_roll(int i) const { return g_roll_[i]; }
+    float* h_roll(int i) const { return h_roll_[i]; }
+    void* block_ws() const { return block_ws_; }
+    void* head_ws() const { return head_ws_; }
+    float* grad_out(int i) const { return grad_out_[i]; }
+    void* discard_acts() const { return discard_acts_; }
+    int32_t* tokens() const { return tokens_; }
+    int32_t* targets() const { return targets_; }
+    int32_t* csr_row_ptr() const { return row_ptr_; }
+    int32_t* csr_pos() const { return pos_; }
+    float* loss_rows() const { return loss_rows_; }
+    float* rope_cos() const { return rope_cos_; }
+    float* rope_sin() const { return rope_sin_; }
+    int* err_flag() const { return err_; }
+
+private:
+    float* anchor_slot(i64 layer_index) const;
+
+    ModelConfig cfg_;
+    ArenaFootprint fp_;
+    ArenaLedger ledger_;
+    int device_ = 0;
+    char* base_ = nullptr;
+    void* stream_[2] = {nullptr, nullptr};
+    i64 occupant_[2] = {-1, -1};
+    i64 occupant_bytes_[2] = {0, 0};
+    char* stack_base_ = nullptr;
+    i64 depth_ = 0;
+    char* anchors_base_ = nullptr;
+    std::vector<bool> anchor_live_;
+    bool ws_claimed_ = false;
+    float* g_roll_[2] = {nullptr, nullptr};
+    float* h_roll_[2] = {nullptr, nullptr};
+    void* block_ws_ = nullptr;
+    void* head_ws_ = nullptr;
+    float* grad_out_[2] = {nullptr, nullptr};
+    void* discard_acts_ = nullptr;
+    int32_t *tokens_ = nullptr, *targets_ = nullptr, *row_ptr_ = nullptr, *pos_ = nullptr;
+    float *loss_rows_ = nullptr, *rope_cos_ = nullptr, *rope_sin_ = nullptr;
+    int* err_ = nullptr;
+    i64 h2d_bytes_ = 0;
+};
+
+}  // namespace hlm

@@ -1,0 +1,165 @@
+// The B200 training engine: CPU-master / GPU-template layer streaming
+// (reference proj/include/hlm/engine.hpp:21-119, same public surface).
+//
+// Three CUDA streams — H2D weights, compute, D2H gradients — ordered only by
+// events (PAPER.md:326-342 protocol):
+//   weights-ready  : H2D of tile i into buffer b  ->  compute reading b
+//   buffer-free    : last compute reading b       ->  next H2D into b
+//   grad-ready     : backward of tile i           ->  D2H of its fp32 gradient
+//   grad-buf-free  : D2H of a gradient buffer     ->  next backward writing it
+// so layer i+1's weights stream in while layer i computes, and layer i's
+// gradient drains while layer i-1 computes. A host worker thread consumes
+// gradient slabs as their D2H completes and runs the fused host Adam per
+// tile (eager optimizer), overlapping the GPU backward.
+#pragma once
+
+#include <condition_variable>
+#include <cstdint>
+#include <deque>
+#include <exception>
+#include <memory>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "hlm/device_arena.hpp"
+#include "hlm/host_store.hpp"
+#include "hlm/trace.hpp"
+
+namespace hlm {
+
+struct Batch {
+    std::vector<std::int32_t> tokens;    // batch * seq
+    std::vector<std::int32_t> targets;   // batch * seq
+};
+
+struct EngineOptions {
+    bool eager_optim = false;      // per-tile Adam as gradients land
+    i64 n_slab = 12;
+    bool threaded_accum = false;   // consume slabs on a host worker thread
+    i64 accum_delay_us = 0;        // test hook, forces slab back-pressure
+    bool skip_optimizer = false;   // verification runs: leave gradients in the store
+    // B200 additions
+    bool fused_recompute = true;   // K == 1: recompute + backward share one weight H2D
+    bool record_trace = true;      // CUDA-event timestamps per op
+    int block_flags = 0;           // HLM_BLOCK_* (e.g. force the generic attention)
+};
+
+struct StepResult {
+    double loss = 0.0;
+    EventTrace trace;
+    ArenaSnapshot arena;
+    HostBytesReport host;
+    i64 h2d_bytes = 0;
+    i64 d2h_bytes = 0;
+    i64 recompute_forwards = 0;
+    double gpu_ms = 0.0;           // step-start to last GPU op, CUDA events
+};
+
+enum class Phase { Idle, Forward, Anchor, Backward, Optimize };
+
+class Engine {
+public:
+    Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper, EngineOptions opts = {});
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    StepResult train_step(const Batch& batch);
+
+    void begin_step(const Batch& batch);
+    void forward_streaming();
+    double anchor_loss();          // synchronises to return the loss (phase API, tests)
+    void backward_blockwise();
+    StepResult finish_step();
+
+    Phase phase() const { return phase_; }
+    // Rolling hidden state on the device; after forward_streaming it is h_L.
+    const float* debug_hidden_device() const { return h_cur_; }
+    std::vector<float> debug_hidden();   // copies h_L to the host
+    SlabPool& pool() { return *pool_; }
+    MasterStore& store() { return store_; }
+    DeviceArena& arena() { return arena_; }
+    const HyperParams& hyper() const { return hyper_; }
+    const EngineOptions& options() const { return opts_; }
+    void* compute_stream() const { return compute_; }
+
+private:
+    struct Pending {
+        i64 slab;
+        i64 layer;
+        i64 grad_op;
+    };
+    struct HostOpRecord {   // host-side Accum / OptStep, appended to the trace in finish_step
+        i64 slab, layer, grad_op;
+        double t0, t1;
+        bool opt;
+        double topt0, topt1;
+    };
+
+    void anchor_loss_async();
+    int stream_tile(i64 tile_id, i64* op_id);
+    void compute_wait_weights(int buf);
+    void compute_done_with(int buf, i64 op_id);
+    int next_grad_buf();
+    void evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op);
+    void consume(const Pending& p);          // READY -> ACCUMULATING -> FREE (+ Adam)
+    void process_oldest_inline();
+    void worker_loop();
+    void drain();
+    i64 op_begin(StreamOp op, void* stream);
+    void op_end(i64 id, void* stream);
+    void rethrow_worker_error();
+
+    MasterStore& store_;
+    DeviceArena& arena_;
+    HyperParams hyper_;
+    EngineOptions opts_;
+    std::unique_ptr<SlabPool> pool_;
+
+    void* h2d_ = nullptr;
+    void* compute_ = nullptr;
+    void* d2h_ = nullptr;
+    void* ev_w_ready_[2] = {};
+    void* ev_buf_free_[2] = {};
+    void* ev_grad_ready_[2] = {};
+    void* ev_gradbuf_free_[2] = {};
+    std::vector<void*> ev_slab_done_;
+    void* ev_step_start_ = nullptr;
+    void* ev_step_end_ = nullptr;
+    std::vector<void*> timing_events_;   // pairs per traced GPU op
+    std::vector<std::pair<i64, int>> op_events_;   // op id -> first timing event index
+    size_t timing_used_ = 0;
+    int32_t* loss_host_ = nullptr;       // pinned: loss rows (float bits) + error flag
+
+    Phase phase_ = Phase::Idle;
+    Batch batch_;
+    EventTrace trace_;
+    double host_t0_us_ = 0.0;
+    int next_buf_ = 0;
+    int next_gbuf_ = 0;
+    i64 last_reader_[2] = {-1, -1};
+    std::vector<i64> last_accum_op_;
+    const float* h_cur_ = nullptr;
+    int g_cur_ = 0;
+    i64 step_t_ = 0;
+    i64 d2h_base_ = 0;
+    i64 recompute_forwards_ = 0;
+    std::vector<i64> consumers_left_;
+    std::vector<HostOpRecord> host_ops_;   // guarded by mu_
+
+    // worker
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<Pending> pending_;
+    i64 in_process_ = 0;
+    bool stop_ = false;
+    std::exception_ptr worker_error_;
+    std::thread worker_;
+};
+
+// Deterministic synthetic data: random tokens echoed as their own targets
+// (reference proj/src/engine.cpp:434-441).
+Batch make_copy_task_batch(const ModelConfig& m, Rng& rng);
+
+}  // namespace hlm

@@ -150,6 +150,87 @@ int hlm_cuda_attention_bwd(const HlmBlockDims* d, const void* q, const void* k, 
                            const void* o, const void* d_o, const float* lse, float* dsum,
                            void* dq, void* dk, void* dv, int64_t ld, void* stream);
 
+
+/* ------------------------------------------------------------------ host engine
+ * Opaque handles over the C++ engine (include/hlm/ headers): the entry points a
+ * binding of the reference's Python / CLI surface (proj/python/bindings.cpp:79-96,
+ * tools/hlm_main.cpp:191-236) would call. Layout of HlmModelConfig matches
+ * oracle/oracle_abi.h OrcCfg. */
+typedef struct HlmModelConfig {
+  int64_t layers, hidden, ffn, vocab, seq, batch, k_ckpt;
+  int32_t tie_embeddings;
+  int32_t n_heads;     /* 1 = reference semantics */
+  double rope_theta;   /* 0 = no RoPE */
+} HlmModelConfig;
+
+typedef struct HlmHyper {
+  double lr, beta1, beta2, eps, weight_decay;
+} HlmHyper;
+
+typedef struct HlmEngineOptions {
+  int32_t eager_optim;
+  int32_t threaded_accum;
+  int64_t n_slab;
+  int64_t accum_delay_us;
+  int32_t skip_optimizer;
+  int32_t fused_recompute;
+  int32_t record_trace;
+  int32_t block_flags;
+} HlmEngineOptions;
+
+typedef struct HlmStepResult {
+  double loss;
+  int64_t h2d_bytes, d2h_bytes, recompute_forwards;
+  double gpu_ms;
+  int64_t arena_committed, arena_peak, host_total, slab_max_in_use;
+} HlmStepResult;
+
+typedef struct HlmStore HlmStore;
+typedef struct HlmArena HlmArena;
+typedef struct HlmEngine HlmEngine;
+
+enum HlmStoreField { HLM_FIELD_MASTER = 0, HLM_FIELD_M = 1, HLM_FIELD_V = 2, HLM_FIELD_GRADS = 3,
+                     HLM_FIELD_SHADOW = 4 };
+
+/* dtype: 0 = bf16 init (reference bf16-store values), 1 = fp32 init.
+ * init_mode: 0 = bit-identical to reference build_store, 1 = parallel. */
+int hlm_store_create(const HlmModelConfig* cfg, uint64_t seed, int dtype, int init_mode, int pin_shadow,
+                     HlmStore** out);
+void hlm_store_destroy(HlmStore* s);
+int64_t hlm_store_total_params(const HlmStore* s);
+int64_t hlm_store_adam_steps(const HlmStore* s);
+/* all physical tiles in store order, fp32 (shadow widened from bf16) */
+int hlm_store_export(const HlmStore* s, int field, float* out);
+int hlm_store_import_master(HlmStore* s, const float* w);   /* master := w, shadow re-packed */
+int hlm_store_bitwise_equal(const HlmStore* a, const HlmStore* b);
+/* Host Adam on every physical tile from caller gradients (store layout),
+ * step index t (reference adam_update_tile, host_store.cpp:334-362). */
+int hlm_store_adam_step(HlmStore* s, const float* grads, const HlmHyper* hp, int64_t t);
+
+int hlm_arena_create(const HlmModelConfig* cfg, int64_t budget_cap, int device, HlmArena** out);
+void hlm_arena_destroy(HlmArena* a);
+/* out[5] = stream_buf, anchor_slot, anchor_slots, stack, workspace (bytes) */
+int hlm_arena_footprint(const HlmModelConfig* cfg, int64_t* out);
+
+int hlm_engine_create(HlmStore* s, HlmArena* a, const HlmHyper* hp, const HlmEngineOptions* o,
+                      HlmEngine** out);
+void hlm_engine_destroy(HlmEngine* e);
+int hlm_engine_train_step(HlmEngine* e, const int32_t* tokens, const int32_t* targets, HlmStepResult* out);
+/* phase API (reference engine.hpp:62-66); out-of-order calls -> HLM_ERR_PROTOCOL */
+int hlm_engine_begin_step(HlmEngine* e, const int32_t* tokens, const int32_t* targets);
+int hlm_engine_forward(HlmEngine* e);
+int hlm_engine_anchor_loss(HlmEngine* e, double* loss);
+int hlm_engine_backward(HlmEngine* e);
+int hlm_engine_finish_step(HlmEngine* e, HlmStepResult* out);
+int hlm_engine_debug_hidden(HlmEngine* e, float* out);
+/* JSONL of the last step's measured trace; *needed = bytes incl. NUL */
+int hlm_engine_last_trace(HlmEngine* e, char* buf, size_t cap, size_t* needed);
+
+int hlm_make_copy_task_batch(const HlmModelConfig* cfg, uint64_t data_seed, int64_t skip, int32_t* tokens);
+/* run_training (trainer.hpp): store from seed, data seed+1, `steps` steps */
+int hlm_run_training(const HlmModelConfig* cfg, const HlmHyper* hp, uint64_t seed, int dtype, int64_t steps,
+                     const HlmEngineOptions* o, double* losses, HlmStepResult* last);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,773 @@
+// The B200 streaming engine (see include/hlm/engine.hpp). Control flow
+// follows reference proj/src/engine.cpp (begin_step :150-174, forward_impl
+// :176-216, anchor_loss_impl :227-269, backward_impl :279-368, finish_step
+// :379-424); the memcpy "transfers" and CPU kernels become async copies and
+// sm_100a kernels on three streams ordered by events.
+#include "hlm/engine.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <stdexcept>
+
+#include "hlm/flop_model.hpp"
+#include "hlm_cuda.h"
+
+namespace hlm {
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+void ck_hlm(int rc, const char* what) {
+    if (rc != HLM_OK) throw CudaError(std::string(what) + ": " + hlm_cuda_last_error());
+}
+cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+cudaEvent_t E(void* e) { return static_cast<cudaEvent_t>(e); }
+void* new_event(bool timing) {
+    cudaEvent_t e;
+    ck(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming), "cudaEventCreate");
+    return e;
+}
+double now_us() {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper, EngineOptions opts)
+    : store_(store), arena_(arena), hyper_(hyper), opts_(opts) {
+    const ModelConfig& m = store.config();
+    const ModelConfig& a = arena.config();
+    if (m.layers != a.layers || m.hidden != a.hidden || m.ffn != a.ffn || m.vocab != a.vocab || m.seq != a.seq ||
+        m.batch != a.batch || m.k_ckpt != a.k_ckpt || m.n_heads != a.n_heads)
+        throw ConfigError("engine: store and arena configs differ");
+    ck(cudaSetDevice(arena_.device()), "cudaSetDevice");
+    pool_ = std::make_unique<SlabPool>(opts_.n_slab, grad_buf_bytes(m), true);
+    cudaStream_t s;
+    ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+    h2d_ = s;
+    ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+    compute_ = s;
+    ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+    d2h_ = s;
+    for (int i = 0; i < 2; ++i) {
+        ev_w_ready_[i] = new_event(false);
+        ev_buf_free_[i] = new_event(false);
+        ev_grad_ready_[i] = new_event(false);
+        ev_gradbuf_free_[i] = new_event(false);
+        ck(cudaEventRecord(E(ev_buf_free_[i]), S(compute_)), "record");
+        ck(cudaEventRecord(E(ev_gradbuf_free_[i]), S(compute_)), "record");
+    }
+    for (i64 i = 0; i < pool_->size(); ++i) ev_slab_done_.push_back(new_event(false));
+    ev_step_start_ = new_event(true);
+    ev_step_end_ = new_event(true);
+    const i64 T = m.rows();
+    void* p = nullptr;
+    ck(cudaHostAlloc(&p, static_cast<size_t>(4 * (4 * T + m.vocab + 1 + 64)), cudaHostAllocPortable),
+       "cudaHostAlloc staging");
+    loss_host_ = static_cast<int32_t*>(p);
+    if (m.rope_theta > 0)
+        ck_hlm(hlm_cuda_rope_table(arena_.rope_cos(), arena_.rope_sin(), m.seq, m.head_dim(), m.rope_theta),
+               "rope table");
+    if (opts_.threaded_accum) worker_ = std::thread([this] { worker_loop(); });
+}
+
+Engine::~Engine() {
+    {
+        std::lock_guard<std::mutex> lk(mu_);
+        stop_ = true;
+    }
+    cv_.notify_all();
+    if (worker_.joinable()) worker_.join();
+    cudaStreamSynchronize(S(compute_));
+    cudaStreamSynchronize(S(h2d_));
+    cudaStreamSynchronize(S(d2h_));
+    cudaEventDestroy(E(ev_step_start_));
+    cudaEventDestroy(E(ev_step_end_));
+    for (int i = 0; i < 2; ++i) {
+        cudaEventDestroy(E(ev_w_ready_[i]));
+        cudaEventDestroy(E(ev_buf_free_[i]));
+        cudaEventDestroy(E(ev_grad_ready_[i]));
+        cudaEventDestroy(E(ev_gradbuf_free_[i]));
+    }
+    for (void* e : ev_slab_done_) cudaEventDestroy(E(e));
+    for (void* e : timing_events_) cudaEventDestroy(E(e));
+    cudaStreamDestroy(S(h2d_));
+    cudaStreamDestroy(S(compute_));
+    cudaStreamDestroy(S(d2h_));
+    if (loss_host_) cudaFreeHost(loss_host_);
+}
+
+// ------------------------------------------------------------------ trace helpers
+i64 Engine::op_begin(StreamOp op, void* stream) {
+    const i64 id = trace_.add(std::move(op));
+    if (opts_.record_trace && stream) {
+        if (timing_used_ + 2 > timing_events_.size()) {
+            timing_events_.push_back(new_event(true));
+            timing_events_.push_back(new_event(true));
+        }
+        ck(cudaEventRecord(E(timing_events_[timing_used_]), S(stream)), "record");
+        op_events_.push_back({id, static_cast<int>(timing_used_)});
+        timing_used_ += 2;
+    }
+    return id;
+}
+
+void Engine::op_end(i64 id, void* stream) {
+    if (!opts_.record_trace || !stream) return;
+    for (auto it = op_events_.rbegin(); it != op_events_.rend(); ++it)
+        if (it->first == id) {
+            ck(cudaEventRecord(E(timing_events_[static_cast<size_t>(it->second + 1)]), S(stream)), "record");
+            return;
+        }
+}
+
+// ------------------------------------------------------------------ streaming
+// reference engine.cpp:55-71: alternate buffers, release the old occupant,
+// H2D (here straight from the pinned bf16 shadow: no staging copy), with a
+// buffer-free dependency on the buffer's last reader.
+int Engine::stream_tile(i64 tile_id, i64* op_id) {
+    const int buf = next_buf_;
+    next_buf_ ^= 1;
+    if (arena_.buffer_occupant(buf) != -1) arena_.release_buffer(buf);
+    const LayerTile& tile = store_.tile(tile_id);
+    const i64 bytes = tile.weight_bytes();
+    void* dst = arena_.claim_buffer(buf, tile_id, bytes);
+    StreamOp op;
+    op.stream = StreamId::H2D;
+    op.kind = OpKind::WeightXfer;
+    op.layer = tile_id;
+    op.buf = buf;
+    op.bytes = bytes;
+    op.pinned = store_.shadow_pinned();
+    if (last_reader_[buf] >= 0) op.deps.push_back(last_reader_[buf]);
+    ck(cudaStreamWaitEvent(S(h2d_), E(ev_buf_free_[buf]), 0), "wait buf free");
+    const i64 id = op_begin(std::move(op), h2d_);
+    ck(cudaMemcpyAsync(dst, tile.shadow(), static_cast<size_t>(bytes), cudaMemcpyHostToDevice, S(h2d_)),
+       "H2D weights");
+    op_end(id, h2d_);
+    ck(cudaEventRecord(E(ev_w_ready_[buf]), S(h2d_)), "record w ready");
+    arena_.add_h2d(bytes);
+    *op_id = id;
+    return buf;
+}
+
+void Engine::compute_wait_weights(int buf) {
+    ck(cudaStreamWaitEvent(S(compute_), E(ev_w_ready_[buf]), 0), "wait weights");
+}
+
+void Engine::compute_done_with(int buf, i64 op_id) {
+    ck(cudaEventRecord(E(ev_buf_free_[buf]), S(compute_)), "record buf free");
+    last_reader_[buf] = op_id;
+}
+
+int Engine::next_grad_buf() {
+    const int gb = next_gbuf_;
+    next_gbuf_ ^= 1;
+    ck(cudaStreamWaitEvent(S(compute_), E(ev_gradbuf_free_[gb]), 0), "wait grad buf");
+    return gb;
+}
+
+// reference engine.cpp:103-121: acquire a slab (inline back-pressure
+// consumes the oldest READY slab), D2H the fp32 gradient, emit GradXfer.
+void Engine::evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op) {
+    ck(cudaEventRecord(E(ev_grad_ready_[gbuf]), S(compute_)), "record grad ready");
+    i64 slab = pool_->try_acquire();
+    while (slab < 0) {
+        if (opts_.threaded_accum) {
+            rethrow_worker_error();
+            slab = pool_->acquire_blocking();
+        } else {
+            process_oldest_inline();
+            slab = pool_->try_acquire();
+        }
+    }
+    const i64 bytes = 4 * n_params;
+    pool_->mark_in_flight(slab, tile_id, bytes);
+    StreamOp op;
+    op.stream = StreamId::D2H;
+    op.kind = OpKind::GradXfer;
+    op.layer = tile_id;
+    op.slab = slab;
+    op.bytes = bytes;
+    op.deps.push_back(lb_op);
+    if (last_accum_op_[static_cast<size_t>(slab)] >= 0) op.deps.push_back(last_accum_op_[static_cast<size_t>(slab)]);
+    ck(cudaStreamWaitEvent(S(d2h_), E(ev_grad_ready_[gbuf]), 0), "wait grad ready");
+    const i64 id = op_begin(std::move(op), d2h_);
+    ck(cudaMemcpyAsync(pool_->data(slab), arena_.grad_out(gbuf), static_cast<size_t>(bytes), cudaMemcpyDeviceToHost,
+                       S(d2h_)),
+       "D2H grads");
+    op_end(id, d2h_);
+    ck(cudaEventRecord(E(ev_slab_done_[static_cast<size_t>(slab)]), S(d2h_)), "record slab done");
+    ck(cudaEventRecord(E(ev_gradbuf_free_[gbuf]), S(d2h_)), "record grad buf free");
+    {
+        std::lock_guard<std::mutex> lk(mu_);
+        pending_.push_back({slab, tile_id, id});
+    }
+    cv_.notify_all();
+}
+
+// One slab: wait for its D2H, then accumulate / optimise (reference
+// host_store.cpp:254-284 and the eager hook engine.cpp:136-148). Numerics do
+// not depend on inline vs threaded consumption nor on the slab count.
+void Engine::consume(const Pending& p) {
+    ck(cudaEventSynchronize(E(ev_slab_done_[static_cast<size_t>(p.slab)])), "slab sync");
+    pool_->mark_ready(p.slab);
+    bool stop = false;
+    const i64 id = pool_->pop_ready_blocking(&stop);
+    if (id != p.slab) throw ProtocolError("slab FIFO order violated");
+    if (opts_.accum_delay_us > 0) std::this_thread::sleep_for(std::chrono::microseconds(opts_.accum_delay_us));
+    HostOpRecord rec{p.slab, p.layer, p.grad_op, now_us(), 0.0, false, 0.0, 0.0};
+    LayerTile& tile = store_.tile(p.layer);
+    const i64 phys = store_.physical_index(p.layer);
+    const bool optimise = opts_.eager_optim && !opts_.skip_optimizer;
+    if (optimise && store_.consumer_count(phys) == 1) {
+        // fused: the pinned slab IS the gradient; no store gradient region touched
+        rec.t1 = now_us();
+        rec.opt = true;
+        rec.topt0 = rec.t1;
+        adam_step_tile_from(tile, pool_->data(p.slab), hyper_, step_t_);
+        rec.topt1 = now_us();
+    } else {
+        accumulate_grads(tile, pool_->data(p.slab));
+        rec.t1 = now_us();
+        bool last = false;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            last = --consumers_left_[static_cast<size_t>(phys)] == 0;
+        }
+        if (optimise && last) {
+            rec.opt = true;
+            rec.topt0 = now_us();
+            adam_step_tile(store_, phys, hyper_, step_t_);
+            rec.topt1 = now_us();
+        }
+    }
+    pool_->release(p.slab);
+    std::lock_guard<std::mutex> lk(mu_);
+    host_ops_.push_back(rec);
+}
+
+void Engine::process_oldest_inline() {
+    Pending p;
+    {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (pending_.empty()) throw ProtocolError("slab pool exhausted with nothing to accumulate");
+        p = pending_.front();
+        pending_.pop_front();
+    }
+    consume(p);
+}
+
+void Engine::worker_loop() {
+    for (;;) {
+        Pending p;
+        {
+            std::unique_lock<std::mutex> lk(mu_);
+            cv_.wait(lk, [&] { return stop_ || !pending_.empty(); });
+            if (pending_.empty()) return;
+            p = pending_.front();
+            pending_.pop_front();
+            ++in_process_;
+        }
+        try {
+            consume(p);
+        } catch (...) {
+            std::lock_guard<std::mutex> lk(mu_);
+            if (!worker_error_) worker_error_ = std::current_exception();
+            // a failed slab must not wedge back-pressure
+            try {
+                pool_->release(p.slab);
+            } catch (...) {
+            }
+        }
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            --in_process_;
+        }
+        cv_.notify_all();
+    }
+}
+
+void Engine::rethrow_worker_error() {
+    std::exception_ptr e;
+    {
+        std::lock_guard<std::mutex> lk(mu_);
+        e = worker_error_;
+        worker_error_ = nullptr;
+    }
+    if (e) std::rethrow_exception(e);
+}
+
+void Engine::drain() {
+    if (opts_.threaded_accum) {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return pending_.empty() && in_process_ == 0; });
+    } else {
+        for (;;) {
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                if (pending_.empty()) break;
+            }
+            process_oldest_inline();
+        }
+    }
+    rethrow_worker_error();
+}
+
+// ------------------------------------------------------------------ phases
+void Engine::begin_step(const Batch& batch) {
+    if (phase_ != Phase::Idle) throw ProtocolError("begin_step outside Idle phase");
+    const ModelConfig& m = store_.config();
+    const i64 T = m.rows();
+    if (static_cast<i64>(batch.tokens.size()) != T || static_cast<i64>(batch.targets.size()) != T)
+        throw ConfigError("batch size does not match model config");
+    batch_ = batch;
+    arena_.begin_step();
+    arena_.claim_workspace();
+    trace_ = EventTrace{};
+    trace_.meta = TraceMeta{m.layers, 2, pool_->size(), m.embed_tile_id(), m.head_tile_id()};
+    op_events_.clear();
+    timing_used_ = 0;
+    next_buf_ = 0;
+    next_gbuf_ = 0;
+    g_cur_ = 0;
+    last_reader_[0] = last_reader_[1] = -1;
+    last_accum_op_.assign(static_cast<size_t>(pool_->size()), -1);
+    {
+        std::lock_guard<std::mutex> lk(mu_);
+        pending_.clear();
+        host_ops_.clear();
+        consumers_left_.assign(static_cast<size_t>(store_.physical_tiles()), 0);
+        for (i64 p = 0; p < store_.physical_tiles(); ++p)
+            consumers_left_[static_cast<size_t>(p)] = store_.consumer_count(p);
+    }
+    step_t_ = store_.adam_steps() + 1;
+    d2h_base_ = pool_->d2h_bytes();
+    recompute_forwards_ = 0;
+    host_t0_us_ = now_us();
+    ck(cudaEventRecord(E(ev_step_start_), S(compute_)), "record step start");
+    ck(cudaStreamWaitEvent(S(h2d_), E(ev_step_start_), 0), "wait");
+    ck(cudaStreamWaitEvent(S(d2h_), E(ev_step_start_), 0), "wait");
+    // batch -> device (pinned staging, compute stream orders it before use)
+    int32_t* st = loss_host_;
+    std::memcpy(st, batch.tokens.data(), static_cast<size_t>(T) * 4);
+    std::memcpy(st + T, batch.targets.data(), static_cast<size_t>(T) * 4);
+    ck(cudaMemcpyAsync(arena_.tokens(), st, static_cast<size_t>(T) * 4, cudaMemcpyHostToDevice, S(compute_)), "H2D tok");
+    ck(cudaMemcpyAsync(arena_.targets(), st + T, static_cast<size_t>(T) * 4, cudaMemcpyHostToDevice, S(compute_)),
+       "H2D tgt");
+    ck(cudaMemsetAsync(arena_.err_flag(), 0, 4, S(compute_)), "memset err");
+    phase_ = Phase::Forward;
+}
+
+// reference engine.cpp:176-216
+void Engine::forward_streaming() {
+    if (phase_ != Phase::Forward) throw ProtocolError("forward_streaming out of order");
+    const ModelConfig& m = store_.config();
+    const i64 T = m.rows();
+    for (i64 t = 0; t < T; ++t)
+        if (batch_.tokens[static_cast<size_t>(t)] < 0 || batch_.tokens[static_cast<size_t>(t)] >= m.vocab)
+            throw std::out_of_range("embed_fwd: token id out of range");
+    const HlmBlockDims dims = block_dims(m, opts_.block_flags);
+    const float* rc = m.rope_theta > 0 ? arena_.rope_cos() : nullptr;
+    const float* rs = m.rope_theta > 0 ? arena_.rope_sin() : nullptr;
+
+    i64 w_op = 0;
+    const int ebuf = stream_tile(m.embed_tile_id(), &w_op);
+    compute_wait_weights(ebuf);
+    float* h0 = arena_.anchor_checkpoint(0);
+    StreamOp op;
+    op.stream = StreamId::Compute;
+    op.kind = OpKind::Forward;
+    op.layer = m.embed_tile_id();
+    op.buf = ebuf;
+    op.flops = fwd_flops(m.embed_params(), T);
+    op.deps.push_back(w_op);
+    i64 id = op_begin(op, compute_);
+    ck_hlm(hlm_cuda_embed_fwd(arena_.tokens(), arena_.buffer(ebuf), h0, T, m.hidden, m.vocab, arena_.err_flag(),
+                              compute_),
+           "embed_fwd");
+    op_end(id, compute_);
+    compute_done_with(ebuf, id);
+    h_cur_ = h0;
+    int roll = 0;
+    for (i64 i = 1; i <= m.layers; ++i) {
+        const int buf = stream_tile(i, &w_op);
+        compute_wait_weights(buf);
+        float* out = (i % m.k_ckpt == 0) ? arena_.anchor_checkpoint(i) : arena_.h_roll(roll);
+        if (i % m.k_ckpt != 0) roll ^= 1;
+        StreamOp bo;
+        bo.stream = StreamId::Compute;
+        bo.kind = OpKind::Forward;
+        bo.layer = i;
+        bo.buf = buf;
+        bo.flops = fwd_flops(m.block_params(), T);
+        bo.deps.push_back(w_op);
+        id = op_begin(bo, compute_);
+        ck_hlm(hlm_cuda_block_fwd(&dims, arena_.buffer(buf), h_cur_, out, arena_.discard_acts(), arena_.block_ws(), rc,
+                                  rs, compute_),
+               "block_fwd");
+        op_end(id, compute_);
+        compute_done_with(buf, id);
+        h_cur_ = out;
+    }
+    phase_ = Phase::Anchor;
+}
+
+// reference engine.cpp:227-269: head fwd + CE + head bwd; g_L into the carry,
+// the head gradient straight to the outbound buffer and a slab.
+double Engine::anchor_loss() {
+    anchor_loss_async();
+    ck(cudaStreamSynchronize(S(compute_)), "sync loss");
+    const i64 T = store_.config().rows();
+    double loss = 0.0;
+    const float* lr = reinterpret_cast<const float*>(loss_host_ + 2 * T);
+    for (i64 r = 0; r < T; ++r) loss += static_cast<double>(lr[r]);
+    return loss;
+}
+
+void Engine::anchor_loss_async() {
+    if (phase_ != Phase::Anchor) throw ProtocolError("anchor_loss out of order");
+    const ModelConfig& m = store_.config();
+    const i64 T = m.rows();
+    for (i64 t = 0; t < T; ++t)
+        if (batch_.targets[static_cast<size_t>(t)] < 0 || batch_.targets[static_cast<size_t>(t)] >= m.vocab)
+            throw std::out_of_range("ce_loss_and_grad: target id out of range");
+    i64 w_op = 0;
+    const int buf = stream_tile(m.head_tile_id(), &w_op);
+    compute_wait_weights(buf);
+    const int gb = next_grad_buf();
+    StreamOp op;
+    op.stream = StreamId::Compute;
+    op.kind = OpKind::Forward;
+    op.layer = m.head_tile_id();
+    op.buf = buf;
+    op.flops = fwd_flops(m.embed_params(), T);
+    op.deps.push_back(w_op);
+    const i64 fid = op_begin(op, compute_);
+    ck_hlm(hlm_cuda_head_loss(T, m.hidden, m.vocab, arena_.buffer(buf), h_cur_, arena_.targets(),
+                              1.0f / static_cast<float>(T), arena_.g_roll(g_cur_), arena_.grad_out(gb), 0,
+                              arena_.loss_rows(), arena_.head_ws(), compute_),
+           "head_loss");
+    op_end(fid, compute_);
+    // the logical trace keeps the reference's separate Forward / LocalBackward ops
+    StreamOp lb;
+    lb.stream = StreamId::Compute;
+    lb.kind = OpKind::LocalBackward;
+    lb.layer = m.head_tile_id();
+    lb.buf = buf;
+    lb.flops = bwd_flops(m.embed_params(), T);
+    lb.deps.push_back(w_op);
+    const i64 lb_op = trace_.add(lb);
+    trace_.ops[static_cast<size_t>(lb_op)].t_start_us = -2.0;   // shares the fused launch's timing
+    compute_done_with(buf, lb_op);
+    ck(cudaMemcpyAsync(loss_host_ + 2 * T, arena_.loss_rows(), static_cast<size_t>(T) * 4, cudaMemcpyDeviceToHost,
+                       S(compute_)),
+       "D2H loss");
+    ck(cudaMemcpyAsync(loss_host_ + 3 * T, arena_.err_flag(), 4, cudaMemcpyDeviceToHost, S(compute_)), "D2H err");
+    evacuate(m.head_tile_id(), gb, m.embed_params(), lb_op);
+    if (m.layers % m.k_ckpt == 0) arena_.release_checkpoint(m.layers);
+    phase_ = Phase::Backward;
+}
+
+// reference engine.cpp:279-368 (K-block recompute onto the LIFO stack, then
+// reverse backward with immediate evacuation). With K == 1 and
+// fused_recompute, recompute and backward of a layer share one weight H2D.
+void Engine::backward_blockwise() {
+    if (phase_ != Phase::Backward) throw ProtocolError("backward_blockwise out of order");
+    const ModelConfig& m = store_.config();
+    const i64 T = m.rows(), K = m.k_ckpt, h = m.hidden;
+    const HlmBlockDims dims = block_dims(m, opts_.block_flags);
+    const float* rc = m.rope_theta > 0 ? arena_.rope_cos() : nullptr;
+    const float* rs = m.rope_theta > 0 ? arena_.rope_sin() : nullptr;
+    const i64 n_block = m.block_params();
+    const bool fused = opts_.fused_recompute && K == 1;
+    const size_t act_bytes = static_cast<size_t>(block_act_bytes(m));
+    (void)act_bytes;
+
+    for (i64 b = m.layers / K; b >= 0; --b) {
+        const i64 lo = b * K + 1, hi = std::min((b + 1) * K, m.layers);
+        if (lo > hi) continue;
+        const float* anchor = arena_.load_checkpoint(b * K);
+        std::vector<const float*> inputs(static_cast<size_t>(hi - lo + 1));
+        std::vector<void*> acts(static_cast<size_t>(hi - lo + 1));
+        if (fused) {
+            i64 w_op = 0;
+            const int buf = stream_tile(lo, &w_op);
+            compute_wait_weights(buf);
+            void* a = arena_.push_acts();
+            StreamOp rop;
+            rop.stream = StreamId::Compute;
+            rop.kind = OpKind::Recompute;
+            rop.layer = lo;
+            rop.buf = buf;
+            rop.flops = fwd_flops(n_block, T);
+            rop.deps.push_back(w_op);
+            i64 id = op_begin(rop, compute_);
+            ck_hlm(hlm_cuda_block_fwd(&dims, arena_.buffer(buf), anchor, arena_.h_roll(0), a, arena_.block_ws(), rc, rs,
+                                      compute_),
+                   "block_fwd (recompute)");
+            op_end(id, compute_);
+            ++recompute_forwards_;
+            const int gb = next_grad_buf();
+            StreamOp bop;
+            bop.stream = StreamId::Compute;
+            bop.kind = OpKind::LocalBackward;
+            bop.layer = lo;
+            bop.buf = buf;
+            bop.flops = bwd_flops(n_block, T);
+            bop.deps.push_back(w_op);
+            const i64 lb = op_begin(bop, compute_);
+            ck_hlm(hlm_cuda_block_bwd(&dims, arena_.buffer(buf), anchor, a, arena_.g_roll(g_cur_),
+                                      arena_.g_roll(g_cur_ ^ 1), arena_.grad_out(gb), arena_.block_ws(), rc, rs,
+                                      compute_),
+                   "block_bwd");
+            op_end(lb, compute_);
+            compute_done_with(buf, lb);
+            evacuate(lo, gb, n_block, lb);
+            arena_.pop_acts();
+            g_cur_ ^= 1;
+        } else {
+            // recompute lo..hi; each stack slab holds the layer's acts, inputs live
+            // in the anchor / rolling buffers (copied into h_roll pairs per layer)
+            const float* x = anchor;
+            std::vector<float*> saved(static_cast<size_t>(hi - lo + 1), nullptr);
+            for (i64 i = lo; i <= hi; ++i) {
+                i64 w_op = 0;
+                const int buf = stream_tile(i, &w_op);
+                compute_wait_weights(buf);
+                void* a = arena_.push_acts();
+                acts[static_cast<size_t>(i - lo)] = a;
+                inputs[static_cast<size_t>(i - lo)] = x;
+                // the block output becomes the next layer's input; keep one fp32 copy
+                // per layer inside the stack slab's tail (see footprint: stack slab
+                // = acts + (rows,h) fp32 input when K > 1)
+                float* out = reinterpret_cast<float*>(static_cast<char*>(a) + align256(block_act_bytes(m)));
+                StreamOp rop;
+                rop.stream = StreamId::Compute;
+                rop.kind = OpKind::Recompute;
+                rop.layer = i;
+                rop.buf = buf;
+                rop.flops = fwd_flops(n_block, T);
+                rop.deps.push_back(w_op);
+                const i64 id = op_begin(rop, compute_);
+                ck_hlm(hlm_cuda_block_fwd(&dims, arena_.buffer(buf), x, out, a, arena_.block_ws(), rc, rs, compute_),
+                       "block_fwd (recompute)");
+                op_end(id, compute_);
+                compute_done_with(buf, id);
+                ++recompute_forwards_;
+                saved[static_cast<size_t>(i - lo)] = out;
+                x = out;
+            }
+            for (i64 i = hi; i >= lo; --i) {
+                i64 w_op = 0;
+                const int buf = stream_tile(i, &w_op);
+                compute_wait_weights(buf);
+                const int gb = next_grad_buf();
+                StreamOp bop;
+                bop.stream = StreamId::Compute;
+                bop.kind = OpKind::LocalBackward;
+                bop.layer = i;
+                bop.buf = buf;
+                bop.flops = bwd_flops(n_block, T);
+                bop.deps.push_back(w_op);
+                const i64 lb = op_begin(bop, compute_);
+                ck_hlm(hlm_cuda_block_bwd(&dims, arena_.buffer(buf), inputs[static_cast<size_t>(i - lo)],
+                                          acts[static_cast<size_t>(i - lo)], arena_.g_roll(g_cur_),
+                                          arena_.g_roll(g_cur_ ^ 1), arena_.grad_out(gb), arena_.block_ws(), rc, rs,
+                                          compute_),
+                       "block_bwd");
+                op_end(lb, compute_);
+                compute_done_with(buf, lb);
+                evacuate(i, gb, n_block, lb);
+                arena_.pop_acts();
+                g_cur_ ^= 1;
+            }
+        }
+        arena_.release_checkpoint(b * K);
+    }
+    (void)h;
+    // embedding backward: deterministic scatter of g_0 by token id (kernels.hpp:396-408)
+    const i64 n_embed = m.embed_params();
+    int32_t* rp = loss_host_ + 3 * T + 16;
+    int32_t* pos = rp + m.vocab + 1;
+    // pos lives after row_ptr in the pinned staging (sized 4T + V + 1 + 64 ints)
+    if (hlm_embed_csr(batch_.tokens.data(), T, m.vocab, rp, pos) != HLM_OK)
+        throw std::out_of_range("embed_bwd: token id out of range");
+    ck(cudaMemcpyAsync(arena_.csr_row_ptr(), rp, static_cast<size_t>(m.vocab + 1) * 4, cudaMemcpyHostToDevice,
+                       S(compute_)),
+       "H2D csr");
+    ck(cudaMemcpyAsync(arena_.csr_pos(), pos, static_cast<size_t>(T) * 4, cudaMemcpyHostToDevice, S(compute_)),
+       "H2D csr pos");
+    const int gb = next_grad_buf();
+    StreamOp eop;
+    eop.stream = StreamId::Compute;
+    eop.kind = OpKind::LocalBackward;
+    eop.layer = m.embed_tile_id();
+    eop.flops = bwd_flops(n_embed, T);
+    const i64 lb = op_begin(eop, compute_);
+    ck_hlm(hlm_cuda_embed_bwd(arena_.csr_row_ptr(), arena_.csr_pos(), arena_.g_roll(g_cur_), arena_.grad_out(gb),
+                              m.vocab, m.hidden, 0, compute_),
+           "embed_bwd");
+    op_end(lb, compute_);
+    evacuate(m.embed_tile_id(), gb, n_embed, lb);
+    phase_ = Phase::Optimize;
+}
+
+// reference engine.cpp:379-424
+StepResult Engine::finish_step() {
+    if (phase_ != Phase::Optimize) throw ProtocolError("finish_step out of order");
+    const ModelConfig& m = store_.config();
+    const i64 T = m.rows();
+    ck(cudaEventRecord(E(ev_step_end_), S(compute_)), "record step end");
+    drain();
+    ck(cudaStreamSynchronize(S(compute_)), "sync compute");
+    ck(cudaStreamSynchronize(S(d2h_)), "sync d2h");
+    ck(cudaStreamSynchronize(S(h2d_)), "sync h2d");
+    const int err = loss_host_[3 * T];
+    if (err & 1) throw std::out_of_range("embed_fwd: token id out of range (device)");
+    if (err & 2) throw std::out_of_range("ce_loss_and_grad: target id out of range (device)");
+    double loss = 0.0;
+    const float* lr = reinterpret_cast<const float*>(loss_host_ + 2 * T);
+    for (i64 r = 0; r < T; ++r) loss += static_cast<double>(lr[r]);
+
+    // host ops into the trace, in consumption order
+    std::vector<i64> accum_ids;
+    for (const auto& rec : host_ops_) {
+        StreamOp op;
+        op.stream = StreamId::Host;
+        op.kind = OpKind::Accum;
+        op.layer = rec.layer;
+        op.slab = rec.slab;
+        op.params = store_.tile(rec.layer).n_params();
+        op.deps.push_back(rec.grad_op);
+        op.t_start_us = rec.t0 - host_t0_us_;
+        op.t_end_us = rec.t1 - host_t0_us_;
+        const i64 id = trace_.add(op);
+        last_accum_op_[static_cast<size_t>(rec.slab)] = id;
+        accum_ids.push_back(id);
+        if (rec.opt) {
+            StreamOp o;
+            o.stream = StreamId::Host;
+            o.kind = OpKind::OptStep;
+            o.layer = rec.layer;
+            o.params = store_.tile(rec.layer).n_params();
+            o.deps.push_back(id);
+            o.t_start_us = rec.topt0 - host_t0_us_;
+            o.t_end_us = rec.topt1 - host_t0_us_;
+            trace_.add(o);
+        }
+    }
+    if (!opts_.eager_optim && !opts_.skip_optimizer) {
+        const double t0 = now_us();
+        adam_step(store_, hyper_, step_t_);
+        StreamOp op;
+        op.stream = StreamId::Host;
+        op.kind = OpKind::OptStep;
+        op.params = store_.total_params();
+        op.deps = accum_ids;
+        op.t_start_us = t0 - host_t0_us_;
+        op.t_end_us = now_us() - host_t0_us_;
+        trace_.add(op);
+    }
+    if (!opts_.skip_optimizer) store_.set_adam_steps(step_t_);
+
+    // resolve GPU timestamps
+    float ms = 0.f;
+    for (const auto& oe : op_events_) {
+        StreamOp& op = trace_.ops[static_cast<size_t>(oe.first)];
+        float a = 0.f, b = 0.f;
+        if (cudaEventElapsedTime(&a, E(ev_step_start_), E(timing_events_[static_cast<size_t>(oe.second)])) ==
+                cudaSuccess &&
+            cudaEventElapsedTime(&b, E(ev_step_start_), E(timing_events_[static_cast<size_t>(oe.second + 1)])) ==
+                cudaSuccess) {
+            op.t_start_us = 1e3 * a;
+            op.t_end_us = 1e3 * b;
+        }
+    }
+    for (auto& op : trace_.ops)
+        if (op.t_start_us == -2.0) {   // fused head fwd/bwd: same launch as the preceding Forward
+            for (const auto& o2 : trace_.ops)
+                if (o2.layer == op.layer && o2.kind == OpKind::Forward) {
+                    op.t_start_us = o2.t_start_us;
+                    op.t_end_us = o2.t_end_us;
+                }
+        }
+    cudaEventElapsedTime(&ms, E(ev_step_start_), E(ev_step_end_));
+
+    for (int b = 0; b < 2; ++b)
+        if (arena_.buffer_occupant(b) != -1) arena_.release_buffer(b);
+    arena_.release_workspace();
+
+    StepResult r;
+    r.loss = loss;
+    r.trace = std::move(trace_);
+    r.arena = arena_.snapshot();
+    r.host.persistent = store_.persistent_bytes();
+    r.host.slabs = pool_->pool_bytes();
+    r.host.total = r.host.persistent + r.host.slabs;
+    r.h2d_bytes = arena_.h2d_bytes();
+    r.d2h_bytes = pool_->d2h_bytes() - d2h_base_;
+    r.recompute_forwards = recompute_forwards_;
+    r.gpu_ms = ms;
+    phase_ = Phase::Idle;
+    return r;
+}
+
+StepResult Engine::train_step(const Batch& batch) {
+    try {
+        begin_step(batch);
+        forward_streaming();
+        anchor_loss_async();
+        backward_blockwise();
+        return finish_step();
+    } catch (...) {
+        // leave the engine reusable: wait for in-flight work, reset protocol state
+        cudaStreamSynchronize(S(compute_));
+        cudaStreamSynchronize(S(h2d_));
+        cudaStreamSynchronize(S(d2h_));
+        try {
+            drain();
+        } catch (...) {
+        }
+        for (int b = 0; b < 2; ++b)
+            if (arena_.buffer_occupant(b) != -1) arena_.release_buffer(b);
+        while (arena_.stack_depth() > 0) arena_.pop_acts();
+        for (i64 i = 0; i <= store_.config().layers; i += store_.config().k_ckpt) {
+            try {
+                arena_.release_checkpoint(i);
+            } catch (...) {
+            }
+        }
+        try {
+            arena_.release_workspace();
+        } catch (...) {
+        }
+        phase_ = Phase::Idle;
+        throw;
+    }
+}
+
+std::vector<float> Engine::debug_hidden() {
+    const ModelConfig& m = store_.config();
+    std::vector<float> out(static_cast<size_t>(m.rows() * m.hidden));
+    ck(cudaStreamSynchronize(S(compute_)), "sync");
+    ck(cudaMemcpy(out.data(), h_cur_, out.size() * 4, cudaMemcpyDeviceToHost), "D2H hidden");
+    return out;
+}
+
+// reference engine.cpp:434-441
+Batch make_copy_task_batch(const ModelConfig& m, Rng& rng) {
+    Batch b;
+    const i64 n = m.rows();
+    b.tokens.resize(static_cast<size_t>(n));
+    for (auto& t : b.tokens) t = rng.uniform_int(static_cast<std::int32_t>(m.vocab));
+    b.targets = b.tokens;
+    return b;
+}
+
+}  // namespace hlm

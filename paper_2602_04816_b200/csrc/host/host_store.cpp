@@ -1,0 +1,506 @@
+// Host parameter store, gradient slabs and the fused host Adam.
+// See include/hlm/host_store.hpp for the design; reference counterparts in
+// proj/src/host_store.cpp are cited per function.
+#include "hlm/host_store.hpp"
+
+#include <cuda_runtime.h>
+#include <immintrin.h>
+#include <omp.h>
+#include <sys/mman.h>
+
+#include <cmath>
+#include <cstring>
+
+#include "hlm/bf16.hpp"
+
+namespace hlm {
+
+namespace {
+
+constexpr i64 kAlignElems = 1024;   // 4 KiB of fp32 / 2 KiB of bf16 per tile boundary
+
+i64 round_up(i64 x, i64 a) { return (x + a - 1) / a * a; }
+
+void* map_huge(size_t bytes) {
+    void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
+    if (p == MAP_FAILED) throw ConfigError("host store: cannot map " + std::to_string(bytes) + " bytes");
+    madvise(p, bytes, MADV_HUGEPAGE);
+    return p;
+}
+
+// Parallel first-touch zero fill (places pages and avoids faults inside Adam).
+void parallel_zero(void* p, size_t bytes) {
+    char* c = static_cast<char*>(p);
+    const i64 chunk = 1 << 24;
+    const i64 n = static_cast<i64>((bytes + chunk - 1) / chunk);
+#pragma omp parallel for schedule(static)
+    for (i64 i = 0; i < n; ++i) {
+        const size_t off = static_cast<size_t>(i) * chunk;
+        std::memset(c + off, 0, std::min<size_t>(chunk, bytes - off));
+    }
+}
+
+// RNE float -> bf16 for 16 lanes (bf16.hpp semantics incl. NaN quieting).
+inline __m256i bf16x16(__m512 x) {
+    const __m512i b = _mm512_castps_si512(x);
+    const __m512i lsb = _mm512_and_si512(_mm512_srli_epi32(b, 16), _mm512_set1_epi32(1));
+    const __m512i rounded = _mm512_srli_epi32(_mm512_add_epi32(_mm512_add_epi32(b, _mm512_set1_epi32(0x7FFF)), lsb), 16);
+    const __m512i hi = _mm512_srli_epi32(b, 16);
+    const __mmask16 special =
+        _mm512_cmpeq_epi32_mask(_mm512_and_si512(b, _mm512_set1_epi32(0x7F800000)), _mm512_set1_epi32(0x7F800000));
+    const __mmask16 nan = _mm512_mask_test_epi32_mask(special, b, _mm512_set1_epi32(0x7FFFFF));
+    __m512i r = _mm512_mask_mov_epi32(rounded, special, hi);
+    r = _mm512_mask_or_epi32(r, nan, r, _mm512_set1_epi32(0x40));
+    return _mm512_cvtepi32_epi16(r);
+}
+
+void pack_shadow(const float* src, std::uint16_t* dst, i64 n) {
+    const i64 chunk = 1 << 16;
+    const i64 nc = (n + chunk - 1) / chunk;
+#pragma omp parallel for schedule(static)
+    for (i64 c = 0; c < nc; ++c) {
+        const i64 b = c * chunk, e = std::min(n, b + chunk);
+        i64 i = b;
+        for (; i + 16 <= e; i += 16)
+            _mm256_storeu_si256(reinterpret_cast<__m256i*>(dst + i), bf16x16(_mm512_loadu_ps(src + i)));
+        for (; i < e; ++i) dst[i] = bf16_bits_from_f32(src[i]);
+    }
+}
+
+std::uint64_t mix64(std::uint64_t x) {   // splitmix64 finaliser
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ offset tables
+std::vector<NamedRegion> block_offset_table(i64 h, i64 f) {
+    std::vector<NamedRegion> t;
+    i64 off = 0;
+    auto add = [&](const char* name, std::vector<i64> shape) {
+        NamedRegion r{name, off, std::move(shape)};
+        off += r.numel();
+        t.push_back(std::move(r));
+    };
+    add("w_q", {h, h});
+    add("w_k", {h, h});
+    add("w_v", {h, h});
+    add("w_o", {h, h});
+    add("w_up", {h, f});
+    add("w_gate", {h, f});
+    add("w_down", {f, h});
+    add("norm1", {h});
+    add("norm2", {h});
+    return t;
+}
+
+std::vector<NamedRegion> table_offset_table(const std::string& name, i64 vocab, i64 h) {
+    return {NamedRegion{name, 0, {vocab, h}}};
+}
+
+// ------------------------------------------------------------------ LayerTile
+LayerTile::LayerTile(i64 layer_id, i64 n_params, std::vector<NamedRegion> offsets, float* state,
+                     std::uint16_t* shadow)
+    : layer_id_(layer_id), n_params_(n_params), offsets_(std::move(offsets)), state_(state), shadow_(shadow) {
+    i64 covered = 0;
+    for (const auto& r : offsets_) {
+        if (r.offset != covered) throw ProtocolError("tile offset table has a gap or overlap at '" + r.name + "'");
+        covered += r.numel();
+    }
+    if (covered != n_params) throw ProtocolError("tile offset table does not cover the tile");
+}
+
+const NamedRegion& LayerTile::region(const std::string& name) const {
+    for (const auto& r : offsets_)
+        if (r.name == name) return r;
+    throw ProtocolError("tile has no tensor named " + name);
+}
+
+float* LayerTile::grads() {
+    if (!grads_) {
+        grads_.reset(new float[static_cast<size_t>(n_params_)]);
+        parallel_zero(grads_.get(), static_cast<size_t>(n_params_) * 4);
+    }
+    return grads_.get();
+}
+
+void LayerTile::store_weight(i64 i, float v) {
+    state_[i] = v;
+    shadow_[i] = bf16_bits_from_f32(v);
+}
+
+// ------------------------------------------------------------------ MasterStore
+MasterStore::MasterStore(const ModelConfig& config, Dtype dtype, bool pin_shadow)
+    : config_(config), dtype_(dtype) {
+    config_.validate();
+    const i64 h = config_.hidden, f = config_.ffn, V = config_.vocab;
+    struct Spec {
+        i64 id, n;
+        std::vector<NamedRegion> off;
+    };
+    std::vector<Spec> specs;
+    specs.push_back({config_.embed_tile_id(), V * h, table_offset_table("embed", V, h)});
+    for (i64 l = 1; l <= config_.layers; ++l) specs.push_back({l, config_.block_params(), block_offset_table(h, f)});
+    if (!config_.tie_embeddings) specs.push_back({config_.head_tile_id(), V * h, table_offset_table("head", V, h)});
+
+    i64 state_elems = 0, shadow_elems = 0;
+    for (const auto& s : specs) {
+        state_elems += 3 * round_up(s.n, kAlignElems);
+        shadow_elems += round_up(s.n, kAlignElems);
+    }
+    state_bytes_ = static_cast<size_t>(state_elems) * 4;
+    shadow_bytes_ = static_cast<size_t>(shadow_elems) * 2;
+    state_base_ = static_cast<float*>(map_huge(state_bytes_));
+    parallel_zero(state_base_, state_bytes_);
+    if (pin_shadow) {
+        void* p = nullptr;
+        if (cudaHostAlloc(&p, shadow_bytes_, cudaHostAllocPortable) == cudaSuccess) {
+            shadow_base_ = static_cast<std::uint16_t*>(p);
+            pinned_ = true;
+        } else {
+            (void)cudaGetLastError();
+        }
+    }
+    if (!shadow_base_) shadow_base_ = static_cast<std::uint16_t*>(map_huge(shadow_bytes_));
+    parallel_zero(shadow_base_, shadow_bytes_);
+
+    i64 so = 0, sh = 0;
+    for (auto& s : specs) {
+        const i64 padded = round_up(s.n, kAlignElems);
+        tiles_.push_back(std::make_unique<LayerTile>(s.id, s.n, std::move(s.off), state_base_ + so, shadow_base_ + sh));
+        so += 3 * padded;
+        sh += padded;
+    }
+    // master, m, v are contiguous inside each tile's slot; the padding sits after v.
+    physical_of_.push_back(0);
+    for (i64 l = 1; l <= config_.layers; ++l) physical_of_.push_back(l);
+    physical_of_.push_back(config_.tie_embeddings ? 0 : config_.layers + 1);
+    for (const auto& t : tiles_) total_params_ += t->n_params();
+}
+
+MasterStore::~MasterStore() {
+    for (auto& t : tiles_) t.reset();
+    if (state_base_) munmap(state_base_, state_bytes_);
+    if (shadow_base_) {
+        if (pinned_)
+            cudaFreeHost(shadow_base_);
+        else
+            munmap(shadow_base_, shadow_bytes_);
+    }
+}
+
+i64 MasterStore::consumer_count(i64 physical_idx) const {
+    i64 n = 0;
+    for (i64 l = 0; l < logical_tiles(); ++l)
+        if (physical_of_[static_cast<size_t>(l)] == physical_idx) ++n;
+    return n;
+}
+
+i64 MasterStore::persistent_bytes() const {
+    i64 total = 0;
+    for (const auto& t : tiles_) {
+        total += t->n_params() * (12 + 2);
+        if (t->has_grads()) total += t->n_params() * 4;
+    }
+    return total;
+}
+
+bool MasterStore::bitwise_equal(const MasterStore& o) const {
+    if (physical_tiles() != o.physical_tiles()) return false;
+    for (i64 p = 0; p < physical_tiles(); ++p) {
+        const LayerTile& a = physical(p);
+        const LayerTile& b = o.physical(p);
+        if (a.n_params() != b.n_params()) return false;
+        const size_t n = static_cast<size_t>(a.n_params());
+        if (std::memcmp(a.master(), b.master(), 3 * n * 4) != 0) return false;
+        if (std::memcmp(a.shadow(), b.shadow(), n * 2) != 0) return false;
+    }
+    return true;
+}
+
+void MasterStore::repack_shadow() {
+    for (auto& t : tiles_) pack_shadow(t->master(), t->shadow(), t->n_params());
+}
+
+// reference host_store.cpp:141-156 (InitMode::Reference is bit-identical).
+std::unique_ptr<MasterStore> build_store(const ModelConfig& config, std::uint64_t seed, Dtype dtype, InitMode mode,
+                                         bool pin_shadow) {
+    auto store = std::make_unique<MasterStore>(config, dtype, pin_shadow);
+    const bool bf = dtype == Dtype::BF16;
+    if (mode == InitMode::Reference) {
+        Rng rng(seed);
+        for (i64 p = 0; p < store->physical_tiles(); ++p) {
+            LayerTile& t = store->physical(p);
+            float* w = t.master();
+            for (const auto& r : t.offset_table()) {
+                const bool norm = r.name == "norm1" || r.name == "norm2";
+                for (i64 i = 0; i < r.numel(); ++i) {
+                    const float v = norm ? 1.0f : rng.trunc_normal(0.02f);
+                    w[r.offset + i] = bf ? bf16_round(v) : v;
+                }
+            }
+        }
+    } else {
+        const i64 chunk = 1 << 16;
+        for (i64 p = 0; p < store->physical_tiles(); ++p) {
+            LayerTile& t = store->physical(p);
+            float* w = t.master();
+            const i64 n = t.n_params();
+            const i64 norm_begin = config.is_block_tile(t.layer_id()) ? config.block_matmul_params() : n;
+            const i64 nc = (n + chunk - 1) / chunk;
+#pragma omp parallel for schedule(dynamic, 16)
+            for (i64 c = 0; c < nc; ++c) {
+                Rng rng(mix64(seed ^ mix64(static_cast<std::uint64_t>(p) * 0x100000001B3ull + static_cast<std::uint64_t>(c))));
+                const i64 b = c * chunk, e = std::min(n, b + chunk);
+                for (i64 i = b; i < e; ++i) {
+                    const float v = i >= norm_begin ? 1.0f : rng.trunc_normal(0.02f);
+                    w[i] = bf ? bf16_round(v) : v;
+                }
+            }
+        }
+    }
+    store->repack_shadow();
+    return store;
+}
+
+// ------------------------------------------------------------------ SlabPool
+const char* slab_state_name(SlabState s) {
+    switch (s) {
+        case SlabState::FREE: return "FREE";
+        case SlabState::IN_FLIGHT: return "IN_FLIGHT";
+        case SlabState::READY: return "READY";
+        case SlabState::ACCUMULATING: return "ACCUMULATING";
+    }
+    return "?";
+}
+
+SlabPool::SlabPool(i64 n_slabs, i64 capacity_bytes, bool pinned) : capacity_(capacity_bytes), pinned_(pinned) {
+    if (n_slabs <= 0) throw ConfigError("slab pool needs at least one slab");
+    slabs_.resize(static_cast<size_t>(n_slabs));
+    for (auto& s : slabs_) {
+        void* p = nullptr;
+        if (pinned_ && cudaHostAlloc(&p, static_cast<size_t>(capacity_bytes), cudaHostAllocPortable) != cudaSuccess) {
+            (void)cudaGetLastError();
+            pinned_ = false;
+        }
+        if (!p) p = map_huge(static_cast<size_t>(capacity_bytes));
+        s.data = static_cast<float*>(p);
+    }
+}
+
+SlabPool::~SlabPool() {
+    for (auto& s : slabs_) {
+        if (!s.data) continue;
+        if (cudaFreeHost(s.data) != cudaSuccess) {
+            (void)cudaGetLastError();
+            munmap(s.data, static_cast<size_t>(capacity_));
+        }
+    }
+}
+
+SlabState SlabPool::state(i64 id) const {
+    std::lock_guard<std::mutex> lk(mu_);
+    return slabs_[static_cast<size_t>(id)].state;
+}
+
+i64 SlabPool::try_acquire() {
+    std::lock_guard<std::mutex> lk(mu_);
+    for (size_t i = 0; i < slabs_.size(); ++i)
+        if (slabs_[i].state == SlabState::FREE) {
+            slabs_[i].state = SlabState::IN_FLIGHT;
+            if (++in_use_ > max_in_use_) max_in_use_ = in_use_;
+            return static_cast<i64>(i);
+        }
+    return -1;
+}
+
+i64 SlabPool::acquire_blocking() {
+    std::unique_lock<std::mutex> lk(mu_);
+    for (;;) {
+        for (size_t i = 0; i < slabs_.size(); ++i)
+            if (slabs_[i].state == SlabState::FREE) {
+                slabs_[i].state = SlabState::IN_FLIGHT;
+                if (++in_use_ > max_in_use_) max_in_use_ = in_use_;
+                return static_cast<i64>(i);
+            }
+        cv_.wait(lk);
+    }
+}
+
+void SlabPool::mark_in_flight(i64 id, i64 layer_id, i64 bytes) {
+    std::lock_guard<std::mutex> lk(mu_);
+    Slab& s = slabs_[static_cast<size_t>(id)];
+    if (s.state != SlabState::IN_FLIGHT) throw ProtocolError(std::string("slab fill in state ") + slab_state_name(s.state));
+    if (bytes > capacity_) throw ProtocolError("slab payload exceeds slab capacity");
+    s.layer_id = layer_id;
+    s.bytes = bytes;
+}
+
+void SlabPool::mark_ready(i64 id) {
+    std::lock_guard<std::mutex> lk(mu_);
+    Slab& s = slabs_[static_cast<size_t>(id)];
+    if (s.state != SlabState::IN_FLIGHT) throw ProtocolError(std::string("slab ready in state ") + slab_state_name(s.state));
+    s.state = SlabState::READY;
+    ready_.push_back(id);
+    d2h_bytes_ += s.bytes;
+    cv_.notify_all();
+}
+
+i64 SlabPool::pop_ready_blocking(bool* stop) {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] { return !ready_.empty() || *stop; });
+    if (ready_.empty()) return -1;
+    const i64 id = ready_.front();
+    ready_.pop_front();
+    slabs_[static_cast<size_t>(id)].state = SlabState::ACCUMULATING;
+    return id;
+}
+
+void SlabPool::release(i64 id) {
+    std::lock_guard<std::mutex> lk(mu_);
+    Slab& s = slabs_[static_cast<size_t>(id)];
+    if (s.state != SlabState::ACCUMULATING && s.state != SlabState::IN_FLIGHT)
+        throw ProtocolError(std::string("slab release in state ") + slab_state_name(s.state));
+    s.state = SlabState::FREE;
+    s.layer_id = -1;
+    s.bytes = 0;
+    --in_use_;
+    cv_.notify_all();
+}
+
+void SlabPool::wait_all_free() {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] { return in_use_ == 0; });
+}
+
+// ------------------------------------------------------------------ Adam
+bool all_finite(const float* g, i64 n) {
+    int bad = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad)
+    for (i64 c = 0; c < (n + 65535) / 65536; ++c) {
+        const i64 b = c * 65536, e = std::min(n, b + 65536);
+        i64 i = b;
+        __mmask16 acc = 0;
+        for (; i + 16 <= e; i += 16) {
+            const __m512i x = _mm512_castps_si512(_mm512_loadu_ps(g + i));
+            acc |= _mm512_cmpeq_epi32_mask(_mm512_and_si512(x, _mm512_set1_epi32(0x7F800000)),
+                                           _mm512_set1_epi32(0x7F800000));
+        }
+        for (; i < e; ++i)
+            if (!std::isfinite(g[i])) acc = 1;
+        if (acc) bad = 1;
+    }
+    return bad == 0;
+}
+
+namespace {
+
+i64 first_non_finite(const float* g, i64 n) {
+    for (i64 i = 0; i < n; ++i)
+        if (!std::isfinite(g[i])) return i;
+    return -1;
+}
+
+// Reference host_store.cpp:342-361 in 16-wide lanes. Every operation is an
+// IEEE single op in the same order (this TU is compiled with
+// -ffp-contract=off), so lanes equal the scalar reference bit for bit.
+void adam_kernel(float* __restrict w, float* __restrict m, float* __restrict v, std::uint16_t* __restrict shadow,
+                 const float* __restrict g, i64 n, float lr, float b1, float b2, float eps, float wd, float bc1,
+                 float bc2, float* zero_after) {
+    const i64 chunk = 1 << 15;
+    const i64 nc = (n + chunk - 1) / chunk;
+    const float omb1 = 1.0f - b1, omb2 = 1.0f - b2;
+#pragma omp parallel for schedule(static)
+    for (i64 c = 0; c < nc; ++c) {
+        const i64 b = c * chunk, e = std::min(n, b + chunk);
+        const __m512 vb1 = _mm512_set1_ps(b1), vb2 = _mm512_set1_ps(b2), vo1 = _mm512_set1_ps(omb1),
+                     vo2 = _mm512_set1_ps(omb2), vbc1 = _mm512_set1_ps(bc1), vbc2 = _mm512_set1_ps(bc2),
+                     veps = _mm512_set1_ps(eps), vwd = _mm512_set1_ps(wd), vlr = _mm512_set1_ps(lr);
+        i64 i = b;
+        for (; i + 16 <= e; i += 16) {
+            const __m512 gg = _mm512_loadu_ps(g + i);
+            __m512 mm = _mm512_loadu_ps(m + i);
+            __m512 vv = _mm512_loadu_ps(v + i);
+            __m512 th = _mm512_loadu_ps(w + i);
+            mm = _mm512_add_ps(_mm512_mul_ps(vb1, mm), _mm512_mul_ps(vo1, gg));
+            vv = _mm512_add_ps(_mm512_mul_ps(vb2, vv), _mm512_mul_ps(_mm512_mul_ps(vo2, gg), gg));
+            const __m512 mhat = _mm512_div_ps(mm, vbc1);
+            const __m512 vhat = _mm512_div_ps(vv, vbc2);
+            const __m512 upd = _mm512_add_ps(_mm512_div_ps(mhat, _mm512_add_ps(_mm512_sqrt_ps(vhat), veps)),
+                                             _mm512_mul_ps(vwd, th));
+            th = _mm512_sub_ps(th, _mm512_mul_ps(vlr, upd));
+            _mm512_storeu_ps(m + i, mm);
+            _mm512_storeu_ps(v + i, vv);
+            _mm512_storeu_ps(w + i, th);
+            _mm256_storeu_si256(reinterpret_cast<__m256i*>(shadow + i), bf16x16(th));
+            if (zero_after) _mm512_storeu_ps(zero_after + i, _mm512_setzero_ps());
+        }
+        for (; i < e; ++i) {
+            const float gv = g[i];
+            m[i] = b1 * m[i] + (1.0f - b1) * gv;
+            v[i] = b2 * v[i] + (1.0f - b2) * gv * gv;
+            const float mhat = m[i] / bc1;
+            const float vhat = v[i] / bc2;
+            float th = w[i];
+            th -= lr * (mhat / (std::sqrt(vhat) + eps) + wd * th);
+            w[i] = th;
+            shadow[i] = bf16_bits_from_f32(th);
+            if (zero_after) zero_after[i] = 0.0f;
+        }
+    }
+}
+
+void adam_apply(LayerTile& tile, const float* grad, const HyperParams& hyper, i64 t, float* zero_after) {
+    if (t < 1) throw ProtocolError("adam step index must be >= 1");
+    if (!all_finite(grad, tile.n_params()))
+        throw NumericsError("non-finite gradient in layer " + std::to_string(tile.layer_id()) + " at element " +
+                            std::to_string(first_non_finite(grad, tile.n_params())) + "; step aborted");
+    const float lr = static_cast<float>(hyper.lr), b1 = static_cast<float>(hyper.beta1),
+                b2 = static_cast<float>(hyper.beta2), eps = static_cast<float>(hyper.eps),
+                wd = static_cast<float>(hyper.weight_decay);
+    const float bc1 = 1.0f - std::pow(b1, static_cast<float>(t));
+    const float bc2 = 1.0f - std::pow(b2, static_cast<float>(t));
+    adam_kernel(tile.master(), tile.moment_m(), tile.moment_v(), tile.shadow(), grad, tile.n_params(), lr, b1, b2,
+                eps, wd, bc1, bc2, zero_after);
+    tile.version.fetch_add(1, std::memory_order_release);
+}
+
+}  // namespace
+
+void adam_step_tile_from(LayerTile& tile, const float* grad, const HyperParams& hyper, i64 t) {
+    adam_apply(tile, grad, hyper, t, nullptr);
+}
+
+void adam_step_tile(MasterStore& store, i64 physical_idx, const HyperParams& hyper, i64 t) {
+    LayerTile& tile = store.physical(physical_idx);
+    float* g = tile.grads();
+    adam_apply(tile, g, hyper, t, g);
+}
+
+// reference host_store.cpp:371-385: validate everything before any mutation.
+void adam_step(MasterStore& store, const HyperParams& hyper, i64 t) {
+    if (t < 1) throw ProtocolError("adam step index must be >= 1");
+    for (i64 p = 0; p < store.physical_tiles(); ++p) {
+        LayerTile& tile = store.physical(p);
+        const float* g = tile.grads();
+        if (!all_finite(g, tile.n_params()))
+            throw NumericsError("non-finite gradient in layer " + std::to_string(tile.layer_id()) + " at element " +
+                                std::to_string(first_non_finite(g, tile.n_params())) + "; step aborted");
+    }
+    for (i64 p = 0; p < store.physical_tiles(); ++p) adam_step_tile(store, p, hyper, t);
+}
+
+void accumulate_grads(LayerTile& tile, const float* g) {
+    float* dst = tile.grads();
+    const i64 n = tile.n_params();
+#pragma omp parallel for schedule(static)
+    for (i64 c = 0; c < (n + 65535) / 65536; ++c) {
+        const i64 b = c * 65536, e = std::min(n, b + 65536);
+        for (i64 i = b; i < e; ++i) dst[i] = dst[i] + g[i];
+    }
+}
+
+}  // namespace hlm

@@ -1,0 +1,209 @@
+"""The streaming engine on the GPU through the C ABI, against the oracle
+(pinned bitwise to the reference) and the reference engine's own contracts
+(proj/tests/test_engine.cpp)."""
+import ast
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2602_04816_b200 import engine as E
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+REL_GRAD = 5e-2     # BF16-compute / FP32-accumulate bound on per-tensor relative L2
+REL_LOSS = 2e-3
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64); b = np.asarray(b, np.float64)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
+
+
+def ocfg(c):
+    return O.cfg(c.layers, c.hidden, c.ffn, c.vocab, c.seq, c.batch, c.k_ckpt,
+                 bool(c.tie_embeddings), c.n_heads, c.rope_theta)
+
+
+def tiles(c):
+    """(name, offset, size) of every logical gradient tile in store layout."""
+    V, h = c.vocab, c.hidden
+    out = [("embed", 0, V * h)]
+    o = V * h
+    for l in range(1, c.layers + 1):
+        out.append((f"block{l}", o, c.block_params())); o += c.block_params()
+    if not c.tie_embeddings:
+        out.append(("head", o, V * h))
+    return out
+
+
+def grad_step(c, seed, tokens, dtype="bf16", **opt):
+    s = E.Store(c, seed, dtype)
+    a = E.Arena(c)
+    e = E.Engine(s, a, E.HyperParams(), E.EngineOptions(skip_optimizer=True, **opt))
+    r = e.train_step(tokens)
+    return r, s.grads(), s
+
+
+CFGS = [
+    ("desk-K2", E.ModelConfig(4, 32, 64, 32, 16, 2, k_ckpt=2)),
+    ("desk-K1", E.ModelConfig(4, 32, 64, 32, 16, 2, k_ckpt=1)),
+    ("tied-K3", E.ModelConfig(4, 8, 24, 11, 8, 2, k_ckpt=3, tie_embeddings=True)),
+    ("c1-ref", E.ModelConfig(4, 256, 1024, 1024, 128, 4, k_ckpt=1)),
+    ("c1-qwen", E.ModelConfig(4, 256, 1024, 1024, 128, 4, k_ckpt=1, n_heads=2, rope_theta=1e6)),
+]
+
+
+@pytest.mark.parametrize("name,c", CFGS, ids=[n for n, _ in CFGS])
+def test_one_step_matches_oracle(name, c):
+    orc = O.Oracle()
+    seed = 1000 + c.layers
+    tok = E.make_copy_task_batch(c, seed + 1)
+    r, g, s = grad_step(c, seed, tok)
+    w = s.weights()
+    loss_ref, g_ref = orc.forward_backward(ocfg(c), w, tok)
+    assert abs(r.loss - loss_ref) / loss_ref < REL_LOSS, (r.loss, loss_ref)
+    errs = {n: rel_l2(g[o:o + k], g_ref[o:o + k]) for n, o, k in tiles(c)}
+    print(name, "loss", r.loss, loss_ref, {k: f"{v:.1e}" for k, v in errs.items()})
+    assert max(errs.values()) < REL_GRAD, errs
+
+
+def test_untrained_loss_near_ln_v_and_debug_hidden():
+    c = E.ModelConfig(4, 32, 64, 32, 16, 2, k_ckpt=2)
+    s = E.Store(c, 9)
+    e = E.Engine(s, E.Arena(c))
+    tok = E.make_copy_task_batch(c, 3)
+    e.begin_step(tok)
+    e.forward_streaming()
+    loss = e.anchor_loss()
+    assert abs(loss - np.log(32)) < 0.1
+    e.backward_blockwise()
+    e.finish_step()
+
+
+def test_zero_blocks_pass_embedding_through():
+    c = E.ModelConfig(2, 16, 32, 13, 4, 1)
+    s = E.Store(c, 5, "fp32")
+    w = s.weights()
+    nb = c.block_params()
+    w[13 * 16: 13 * 16 + 2 * nb] = 0.0
+    s.import_master(w)
+    e = E.Engine(s, E.Arena(c))
+    tok = E.make_copy_task_batch(c, 2)
+    e.begin_step(tok)
+    e.forward_streaming()
+    h = e.debug_hidden().reshape(-1, 16)
+    table = s.export(E.FIELD_SHADOW)[:13 * 16].reshape(13, 16)
+    assert np.array_equal(h, table[tok])
+    e.anchor_loss(); e.backward_blockwise(); e.finish_step()
+
+
+def test_phase_protocol_errors():
+    c = E.ModelConfig(2, 16, 32, 13, 4, 1)
+    e = E.Engine(E.Store(c, 1), E.Arena(c))
+    with pytest.raises(E.ProtocolError):
+        e.forward_streaming()
+    tok = E.make_copy_task_batch(c, 2)
+    e.begin_step(tok)
+    with pytest.raises(E.ProtocolError):
+        e.backward_blockwise()
+
+
+def test_out_of_range_ids_raise_and_engine_recovers():
+    c = E.ModelConfig(2, 16, 32, 13, 4, 1)
+    e = E.Engine(E.Store(c, 1), E.Arena(c))
+    bad = np.array([0, 1, 13, 2], np.int32)
+    with pytest.raises(IndexError, match="token id out of range"):
+        e.train_step(bad)
+    with pytest.raises(IndexError, match="target id out of range"):
+        e.train_step(np.array([0, 1, 2, 3], np.int32), np.array([0, -1, 2, 3], np.int32))
+    r = e.train_step(np.array([0, 1, 2, 3], np.int32))
+    assert np.isfinite(r.loss)
+
+
+def test_k_invariance_bitwise():
+    base = dict(layers=6, hidden=32, ffn=64, vocab=32, seq=16, batch=2)
+    tok = E.make_copy_task_batch(E.ModelConfig(**base), 21)
+    ref = None
+    for k in range(1, 7):
+        for fused in ([True, False] if k == 1 else [True]):
+            c = E.ModelConfig(**base, k_ckpt=k)
+            _, g, _ = grad_step(c, 42, tok, fused_recompute=fused)
+            if ref is None:
+                ref = g
+            else:
+                assert np.array_equal(g, ref), (k, fused)
+
+
+def test_byte_counters_match_formula():
+    c = E.ModelConfig(4, 32, 64, 32, 16, 2, k_ckpt=2)
+    s = E.Store(c, 3)
+    e = E.Engine(s, E.Arena(c))
+    r = e.train_step(E.make_copy_task_batch(c, 2))
+    n_table, n_blocks = c.vocab * c.hidden, c.layers * c.block_params()
+    assert r.h2d_bytes == 2 * (2 * n_table + 3 * n_blocks)     # reference 3-pass schedule (K=2)
+    assert r.d2h_bytes == 4 * (2 * n_table + n_blocks)         # fp32 gradients
+    c1 = E.ModelConfig(4, 32, 64, 32, 16, 2, k_ckpt=1)
+    e1 = E.Engine(E.Store(c1, 3), E.Arena(c1))
+    r1 = e1.train_step(E.make_copy_task_batch(c1, 2))
+    assert r1.h2d_bytes == 2 * (2 * n_table + 2 * n_blocks)    # fused K=1: two passes
+    assert r1.recompute_forwards == c1.layers
+
+
+def test_compute_schedule_L6_K3():
+    """proj/tests/test_engine.cpp:62-97 hand-enumerated compute order."""
+    c = E.ModelConfig(6, 8, 16, 11, 4, 1, k_ckpt=3)
+    e = E.Engine(E.Store(c, 3, "fp32"), E.Arena(c))
+    e.train_step(E.make_copy_task_batch(c, 1))
+    got = [(op["kind"], op["layer"]) for op in e.last_trace() if op["stream"] == "compute"]
+    F, R, B = "Forward", "Recompute", "LocalBackward"
+    expect = [(F, 0), (F, 1), (F, 2), (F, 3), (F, 4), (F, 5), (F, 6), (F, 7), (B, 7),
+              (R, 4), (R, 5), (R, 6), (B, 6), (B, 5), (B, 4),
+              (R, 1), (R, 2), (R, 3), (B, 3), (B, 2), (B, 1), (B, 0)]
+    assert got == expect
+    ops = e.last_trace()
+    assert all(op["t_end_us"] >= op["t_start_us"] >= 0 for op in ops if op["stream"] != "host")
+
+
+def _train(c, seed, steps, **opt):
+    s = E.Store(c, seed)
+    e = E.Engine(s, E.Arena(c), E.HyperParams(lr=2e-3), E.EngineOptions(**opt))
+    rng_tok = [E.make_copy_task_batch(c, 7, skip=i) for i in range(steps)]
+    for t in rng_tok:
+        e.train_step(t)
+    return s, e
+
+
+def test_eager_equals_lazy_and_threaded_equals_inline_and_slabs():
+    c = E.ModelConfig(4, 32, 64, 32, 16, 2, k_ckpt=2, tie_embeddings=True)
+    lazy, _ = _train(c, 55, 3)
+    eager, _ = _train(c, 55, 3, eager_optim=True)
+    assert lazy.bitwise_equal(eager)
+    threaded, _ = _train(c, 55, 3, eager_optim=True, threaded_accum=True, n_slab=2,
+                         accum_delay_us=500)
+    assert lazy.bitwise_equal(threaded)
+    one, e1 = _train(c, 55, 3, n_slab=1)
+    assert lazy.bitwise_equal(one)
+
+
+def test_no_device_state_persists_and_peak_settles():
+    c = E.ModelConfig(4, 32, 64, 32, 16, 2, k_ckpt=2)
+    e = E.Engine(E.Store(c, 3), E.Arena(c))
+    r = [e.train_step(E.make_copy_task_batch(c, 2, skip=i)) for i in range(3)]
+    assert r[1].arena_peak == r[2].arena_peak
+
+
+def test_training_tracks_oracle_mixed_precision():
+    """North-star numerics (FP32 master + Adam, BF16 shadow) for 20 steps vs
+    the oracle's mixed mode: per-step loss within 1 %."""
+    c = E.ModelConfig(4, 32, 64, 32, 16, 8, k_ckpt=2)
+    out = E.train({"model": dict(layers=4, hidden=32, ffn=64, vocab=32, seq=16, batch=8, k_ckpt=2),
+                   "hyper": {"lr": 3e-3}, "run": {"steps": 20, "seed": 1234, "dtype": "fp32",
+                                                  "eager_optim": True, "threaded_accum": True,
+                                                  "n_slab": 3}})
+    ref, _ = O.Oracle().train(ocfg(c), O.hyper(lr=3e-3), 1234, "mixed", 20)
+    l = np.array(out["losses"])
+    assert np.all(np.abs(l - ref) / ref < 1e-2), (l, ref)
+    assert l[-1] < 0.8 * l[0]

@@ -1,0 +1,107 @@
+"""Host-side C++ (libhlm_b200.so) on CPU only: store init, Adam, token
+stream, footprint formulas, C-ABI symbol surface. No GPU calls (pinning off)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2602_04816_b200 import _lib
+from paper_2602_04816_b200 import engine as E
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_every_declared_symbol_is_exported():
+    hdr = open(os.path.join(ROOT, "include", "hlm_cuda.h")).read()
+    names = set(re.findall(r"\b(hlm_[a-z0-9_]+)\s*\(", hdr))
+    lib = _lib.lib()
+    missing = [n for n in sorted(names) if not hasattr(lib, n)]
+    assert not missing, missing
+    assert len(names) > 30
+
+
+@pytest.mark.parametrize("name", ["tiny", "desk", "acc_tied"])
+def test_store_init_bitwise_reference(name):
+    z = np.load(os.path.join(GOLD, f"ref_{name}.npz"))
+    import ast
+    kw = ast.literal_eval(str(z["cfg_json"]))
+    c = E.ModelConfig(kw["layers"], kw["hidden"], kw["ffn"], kw["vocab"], kw["seq"], kw["batch"],
+                      kw["k_ckpt"], kw.get("tie", False))
+    seed = int(z["seed"])
+    assert np.array_equal(E.Store(c, seed, "bf16", pin=False).weights().view(np.uint32),
+                          z["w16"].view(np.uint32))
+    s32 = E.Store(c, seed, "fp32", pin=False)
+    assert np.array_equal(s32.weights().view(np.uint32), z["w32"].view(np.uint32))
+    # the transfer shadow is RNE(master), reference bf16.hpp semantics
+    assert np.array_equal(s32.export(E.FIELD_SHADOW), z["w16"])
+    assert np.array_equal(E.make_copy_task_batch(c, seed + 1), z["tokens"])
+
+
+def test_parallel_init_is_deterministic_and_trunc_normal():
+    c = E.ModelConfig(2, 64, 128, 512, 8, 2)
+    a = E.Store(c, 7, "fp32", init="parallel", pin=False).weights()
+    b = E.Store(c, 7, "fp32", init="parallel", pin=False).weights()
+    assert np.array_equal(a, b)
+    mats = a[:512 * 64]
+    assert abs(mats.mean()) < 1e-3 and 0.015 < mats.std() < 0.02 and np.abs(mats).max() <= 0.04
+    # norms are 1.0
+    blk = a[512 * 64: 512 * 64 + c.block_params()]
+    assert np.all(blk[-2 * 64:] == 1.0)
+
+
+def test_adam_bitwise_vs_oracle_and_known_answer():
+    c = E.ModelConfig(2, 16, 32, 13, 4, 1)
+    s = E.Store(c, 3, "fp32", pin=False)
+    orc = O.Oracle()
+    rng = np.random.default_rng(0)
+    w = s.weights().copy(); m = np.zeros_like(w); v = np.zeros_like(w)
+    for t in (1, 2, 3, 4):
+        g = (rng.standard_normal(w.size) * 1e-2).astype(np.float32)
+        s.adam_step(g, E.HyperParams(lr=3e-3, weight_decay=0.01), t)
+        orc.adam(O.hyper(lr=3e-3, weight_decay=0.01), t, w, g, m, v)
+    assert np.array_equal(s.weights(), w)
+    assert np.array_equal(s.export(E.FIELD_M), m)
+    assert np.array_equal(s.export(E.FIELD_V), v)
+    assert s.adam_steps == 4
+    # shadow tracks the master (RNE)
+    sh = s.export(E.FIELD_SHADOW)
+    assert np.array_equal(sh, (w.view(np.uint32) + 0x7FFF + ((w.view(np.uint32) >> 16) & 1) >> 16
+                               << 16).astype(np.uint32).view(np.float32))
+
+
+def test_adam_rejects_non_finite_gradient_without_mutation():
+    c = E.ModelConfig(2, 16, 32, 13, 4, 1)
+    s = E.Store(c, 3, "fp32", pin=False)
+    before = s.weights().copy()
+    g = np.zeros(s.total_params, np.float32)
+    g[5] = np.nan
+    with pytest.raises(E.NumericsError, match="non-finite gradient in layer 0 at element 5"):
+        s.adam_step(g, E.HyperParams(), 1)
+    assert np.array_equal(s.weights(), before)
+
+
+def test_config_validation():
+    with pytest.raises(E.HlmConfigError):
+        E.Store(E.ModelConfig(2, 12, 32, 13, 4, 1), 1, pin=False)        # hidden % 8
+    with pytest.raises(E.HlmConfigError):
+        E.Store(E.ModelConfig(2, 16, 32, 13, 4, 1, k_ckpt=3), 1, pin=False)  # K > L
+    with pytest.raises(E.HlmConfigError):
+        E.Store(E.ModelConfig(2, 16, 32, 13, 4, 1, n_heads=3), 1, pin=False)
+
+
+def test_footprint_is_depth_invariant_except_anchors():
+    a = E.arena_footprint(E.ModelConfig(4, 64, 128, 100, 16, 2))
+    b = E.arena_footprint(E.ModelConfig(40, 64, 128, 100, 16, 2))
+    assert a["stream_buf"] == b["stream_buf"] and a["stack"] == b["stack"]
+    assert a["workspace"] == b["workspace"]
+    assert b["anchor_slots"] == 41 and a["anchor_slots"] == 5
+    assert a["anchor_slot"] == 4 * 2 * 16 * 64
+
+
+def test_train_rejects_unknown_keys():
+    with pytest.raises(E.HlmConfigError):
+        E.train({"model": {}, "bogus": 1})
