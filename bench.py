@@ -1,0 +1,318 @@
+#!/usr/bin/env python
+"""Benchmark of the layer-streaming training step (BASELINE.json metric:
+train tokens/s & TFLOPS; H2D GB/s and overlap vs roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c2]
+
+Workload (N=1 default): BASELINE.json configs[1], the Qwen2.5-7B-shaped
+decoder — L28 h3584 f18944 V152064 S2048 B8 (T = 16384 tokens), 28 heads of
+128, RoPE theta 1e6, untied, K_ckpt = 1 — host-resident FP32 master + Adam
+(115 GB) with BF16 layer streaming, on 1 B200. One step = one full training
+step (forward, loss, recompute + backward, FP32 gradient D2H, host Adam on
+every parameter). Synthetic copy-task tokens, random-init weights.
+
+--impl reference times the reference's own CPU implementation of the same
+step (oracle/_ref, the reference library compiled from its sources) on a
+bounded sample: one block fwd + recompute + bwd and the head at full width on
+T = 4 tokens, extrapolated linearly in T and L (labelled an estimate).
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c1": dict(layers=4, hidden=256, ffn=1024, vocab=1024, seq=128, batch=4, n_heads=2),
+    "c2": dict(layers=28, hidden=3584, ffn=18944, vocab=152064, seq=2048, batch=8, n_heads=28),
+    "c3": dict(layers=64, hidden=5120, ffn=27648, vocab=152064, seq=2048, batch=8, n_heads=40),
+    "c4": dict(layers=80, hidden=8192, ffn=29568, vocab=152064, seq=2048, batch=8, n_heads=64),
+    "c5": dict(layers=48, hidden=12288, ffn=49152, vocab=201088, seq=4096, batch=8, n_heads=96),
+}
+NAMES = {"c1": "tiny-qwen-style-L4-d256-s128", "c2": "qwen2.5-7b-shaped-L28-d3584-s2048",
+         "c3": "qwen2.5-32b-shaped-L64-d5120-s2048", "c4": "qwen2.5-72b-shaped-L80-d8192-s2048",
+         "c5": "dense-120b-class-L48-d12288-s4096"}
+METRIC = "train_tokens_per_s"
+PCIE_ASSUMED_GBS = 55.0   # measured on the pool's box: pinned H2D 55.5 / D2H 55.8 GB/s
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["hbm_gbs"], d["bf16_tflops"], d["bf16_tflops_sustained"], "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+def model_numbers(m):
+    L, h, f, V, S, B = m["layers"], m["hidden"], m["ffn"], m["vocab"], m["seq"], m["batch"]
+    T = B * S
+    n_mm = 4 * h * h + 3 * h * f
+    n = n_mm + 2 * h
+    attn_fwd = 2.0 * B * S * S * h
+    model_flops = 6.0 * T * (L * n_mm + V * h) + 3.0 * L * attn_fwd
+    hw_flops = model_flops + L * (2.0 * n_mm * T + attn_fwd)
+    h2d = 2 * (2 * L * n + 2 * V * h)       # bf16 weights: forward + fused recompute/backward
+    d2h = 4 * (L * n + 2 * V * h)           # fp32 gradients
+    return dict(T=T, n=n, n_mm=n_mm, model_flops=model_flops, hw_flops=hw_flops, h2d=h2d, d2h=d2h,
+                params=(2 * V * h + L * n))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self):
+        self.rows, self.proc = [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for i, nme in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower().startswith("active"):
+                    reasons.add(nme)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), \
+        int(os.environ.get("LOCAL_RANK", 0))
+
+
+def reference_sample(m, steps, warmup):
+    """Reference CPU path: block fwd+recompute+bwd and head at full width, T=4."""
+    import oracle as O
+    ref = O.Reference()
+    Bs, Ss = 1, 4
+    ctx = ref.bench_create(Bs, Ss, m["hidden"], m["ffn"], m["vocab"])
+    try:
+        for _ in range(warmup):
+            ref.bench_run(ctx)
+        per = []
+        for _ in range(steps):
+            tb, th = ref.bench_run(ctx)
+            per.append(m["layers"] * tb + th)
+    finally:
+        ref.bench_destroy(ctx)
+    t_step = float(np.mean(per))            # estimated seconds for T=4 tokens through the model
+    tok_s = Bs * Ss / t_step
+    sample = (f"reference CPU kernels (oracle/_ref, -O3, 1 thread): one block fwd+recompute+bwd "
+              f"and head fwd+CE+bwd at h={m['hidden']} f={m['ffn']} V={m['vocab']} on T={Bs * Ss} "
+              f"tokens, x{m['layers']} blocks; estimate, linear in T and L")
+    return tok_s, t_step, sample
+
+
+def run_reference(args, m, name):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    steps = max(1, args.steps)
+    warmup = min(1, args.warmup)
+    tok_s, t_step, sample = reference_sample(m, steps, warmup)
+    nums = model_numbers(m)
+    line = {"metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": steps, "warmup": warmup, "ms_per_step": t_step * 1e3 * nums["T"] / 4,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": name, "global_batch": m["batch"], "seq_len": m["seq"],
+                       "parallelism": "cpu-1-thread"},
+            "tflops": nums["model_flops"] / nums["T"] * tok_s / 1e12,
+            "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": 1, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": tok_s, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, m, name):
+    from paper_2602_04816_b200 import _lib
+    from paper_2602_04816_b200 import engine as E
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    lib = _lib.blib()
+    import ctypes
+    lib.hlm_timer_record.argtypes = [ctypes.c_int]
+    lib.hlm_timer_elapsed_ms.restype = ctypes.c_double
+    lib.hlm_timer_elapsed_ms.argtypes = [ctypes.c_int, ctypes.c_int]
+    lib.hlm_cuda_launch_count.restype = ctypes.c_longlong
+    lib.hlm_cuda_bench_block_gemms.argtypes = [ctypes.POINTER(_lib.HlmBlockDims), ctypes.c_int] + \
+        [ctypes.POINTER(ctypes.c_double)] * 3
+
+    cfg = E.ModelConfig(m["layers"], m["hidden"], m["ffn"], m["vocab"], m["seq"], m["batch"],
+                        k_ckpt=1, n_heads=m["n_heads"], rope_theta=1e6)
+    nums = model_numbers(m)
+    t0 = time.time()
+    store = E.Store(cfg, 1234, "bf16", init="parallel")
+    arena = E.Arena(cfg, device=local)
+    opts = E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=args.slabs,
+                           record_trace=True)
+    eng = E.Engine(store, arena, E.HyperParams(lr=1e-4), opts)
+    setup_s = time.time() - t0
+    batches = [E.make_copy_task_batch(cfg, 1235, skip=i) for i in range(args.warmup + args.steps)]
+
+    for i in range(args.warmup):
+        eng.train_step(batches[i])
+    trace = eng.last_trace()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler()
+    clocks.start()
+    launches0 = lib.hlm_cuda_launch_count()
+    lib.hlm_timer_record(0)
+    wall0 = time.perf_counter()
+    losses, gpu_ms = [], []
+    for i in range(args.steps):
+        r = eng.train_step(batches[args.warmup + i])
+        losses.append(r.loss)
+        gpu_ms.append(r.gpu_ms)
+    lib.hlm_timer_record(1)
+    wall = time.perf_counter() - wall0
+    launches = (lib.hlm_cuda_launch_count() - launches0) // max(1, args.steps)
+    clk = clocks.stop()
+    dev_s = lib.hlm_timer_elapsed_ms(0, 1) / 1e3
+    if world > 1:
+        import torch
+        t = torch.tensor([dev_s])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_s = float(t.item())
+    step_s = dev_s / args.steps
+    value = world * nums["T"] * args.steps / dev_s
+    e2e = world * nums["T"] * args.steps / wall
+
+    # per-step overlap / bandwidth from the measured trace (last warm-up step)
+    h2d = [o for o in trace if o["stream"] == "h2d"]
+    d2h = [o for o in trace if o["stream"] == "d2h"]
+    comp = [o for o in trace if o["stream"] == "compute" and o["t_end_us"] > 0]
+    h2d_busy = sum(o["t_end_us"] - o["t_start_us"] for o in h2d)
+    d2h_busy = sum(o["t_end_us"] - o["t_start_us"] for o in d2h)
+    h2d_gbs = sum(o["bytes"] for o in h2d) / max(h2d_busy, 1e-9) / 1e3
+    d2h_gbs = sum(o["bytes"] for o in d2h) / max(d2h_busy, 1e-9) / 1e3
+    comp_iv = sorted((o["t_start_us"], o["t_end_us"]) for o in comp)
+
+    def covered(a, b):
+        tot = 0.0
+        for s, e in comp_iv:
+            lo, hi = max(a, s), min(b, e)
+            if hi > lo:
+                tot += hi - lo
+        return tot
+    xfer = sum(o["t_end_us"] - o["t_start_us"] for o in h2d + d2h)
+    hidden = sum(covered(o["t_start_us"], o["t_end_us"]) for o in h2d + d2h)
+    overlap = hidden / xfer if xfer > 0 else None
+    host_ops = [o for o in trace if o["stream"] == "host" and o["kind"] == "OptStep"]
+    adam_s = sum(o["t_end_us"] - o["t_start_us"] for o in host_ops) / 1e6
+    gpu_busy_s = float(np.mean(gpu_ms)) / 1e3
+
+    hbm, tf_burst, tf_sus, peak_kind = peaks()
+    # live roofline of the dominant kernel (tcgen05 GEMM) at the workload's block shapes
+    dims = _lib.HlmBlockDims(m["batch"], m["seq"], m["hidden"], m["ffn"], m["n_heads"], 0)
+    fl, ms_set, ms_launch = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    lib.hlm_cuda_bench_block_gemms(ctypes.byref(dims), 5, ctypes.byref(fl), ctypes.byref(ms_set),
+                                   ctypes.byref(ms_launch))
+    gemm_tflops = fl.value / (ms_set.value / 1e3) / 1e12
+
+    t_roof = max(nums["hw_flops"] / (tf_sus * 1e12), nums["h2d"] / (PCIE_ASSUMED_GBS * 1e9),
+                 nums["d2h"] / (PCIE_ASSUMED_GBS * 1e9))
+
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            tok_s, _, sample = reference_sample(m, 1, 0)
+            cpu_baseline = {"value": tok_s, "unit": "tokens/s", "cores": 1, "kind": "reference",
+                            "sample": sample}
+        except Exception as ex:   # reference lib absent -> say so
+            cpu_baseline = {"value": None, "unit": "tokens/s", "cores": 1, "kind": "reference",
+                            "sample": f"unavailable: {ex}"}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic copy-task tokens, random-init weights (parallel trunc-normal 0.02)",
+        "config": {"workload": name, "global_batch": m["batch"] * world, "seq_len": m["seq"],
+                   "tokens_per_step": nums["T"] * world, "params": nums["params"],
+                   "parallelism": f"dp{world}" if world > 1 else "single-gpu",
+                   "n_heads": m["n_heads"], "k_ckpt": 1, "l2": "inputs larger than L2 (weights "
+                   "streamed from host every step)"},
+        "tflops": nums["model_flops"] / step_s / 1e12,
+        "hw_tflops": nums["hw_flops"] / step_s / 1e12,
+        "e2e": {"value": e2e, "unit": "tokens/s",
+                "h2d_bytes_per_step": int(nums["h2d"] + 8 * nums["T"]),
+                "d2h_bytes_per_step": int(nums["d2h"] + 4 * nums["T"])},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "tensor", "kernel": "gemm_sm100 (tcgen05/TMA, 12 block launches)",
+                     "achieved": gemm_tflops, "peak": tf_burst, "unit": "TFLOP/s",
+                     "frac": gemm_tflops / tf_burst, "peak_kind": f"{peak_kind} burst",
+                     "traffic": None, "ms_per_launch": ms_launch.value},
+        "step_roofline": {"t_roof_s": t_roof, "t_step_s": step_s, "frac": t_roof / step_s,
+                          "def": "max(HW_FLOPS/sustained bf16, H2D/55GB/s, D2H/55GB/s)"},
+        "stream": {"h2d_gbs": h2d_gbs, "d2h_gbs": d2h_gbs, "overlap": overlap,
+                   "gpu_busy_s": gpu_busy_s, "host_adam_s": adam_s},
+        "clocks": clk, "cpu_baseline": cpu_baseline,
+        "loss": [float(x) for x in losses], "setup_s": setup_s,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--slabs", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    m = dict(CONFIGS[args.config])
+    if args.impl == "reference":
+        run_reference(args, m, NAMES[args.config])
+    else:
+        run_ours(args, m, NAMES[args.config])
+
+
+if __name__ == "__main__":
+    main()

@@ -49,6 +49,9 @@ enum HlmGemmErr {
 
 const char* hlm_cuda_last_error(void);
 
+/* Number of CUDA kernels this library has launched since it was loaded. */
+long long hlm_cuda_launch_count(void);
+
 /* ------------------------------------------------------------------ GEMM
  * C[g] = A[g] . B[g]  (bf16 operands, fp32 accumulation in TMEM)
  *   A element (m,k): a_mn ? A[k*lda + m] : A[m*lda + k]
@@ -144,6 +147,18 @@ int hlm_embed_csr(const int32_t* tokens, int64_t rows, int64_t vocab, int32_t* r
 
 /* ------------------------------------------------------------------ small ops */
 int hlm_cuda_cast_bf16(const float* in, void* out, int64_t n, void* stream);
+
+/* Device-event timer for harnesses: record(slot) synchronises the device and
+ * records an event on the legacy stream; elapsed_ms(a, b) between two slots. */
+int hlm_timer_record(int slot);
+double hlm_timer_elapsed_ms(int a, int b);
+
+/* Live roofline probe of the dominant kernel: the 12 tcgen05 GEMM launches of
+ * one block (4 forward, 8 backward: dgrad + wgrad) at the given dims, timed
+ * with CUDA events over `iters` repetitions on one stream. Outputs the
+ * algorithmic flops of the set, the mean ms per set and the per-launch mean. */
+int hlm_cuda_bench_block_gemms(const HlmBlockDims* d, int iters, double* flops, double* ms_per_set,
+                               double* ms_per_launch);
 int hlm_cuda_attention_fwd(const HlmBlockDims* d, const void* q, const void* k, const void* v,
                            void* o, float* lse, int64_t ld, void* stream);
 int hlm_cuda_attention_bwd(const HlmBlockDims* d, const void* q, const void* k, const void* v,

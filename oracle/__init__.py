@@ -200,6 +200,13 @@ class Reference(_Lib):
                                           ctypes.c_int64]
         L.ref_time_block.restype = ctypes.c_double
         L.ref_time_block.argtypes = [ctypes.c_int64] * 5
+        L.ref_bench_create.restype = ctypes.c_void_p
+        L.ref_bench_create.argtypes = [ctypes.c_int64] * 5
+        L.ref_bench_run.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
+                                    ctypes.POINTER(ctypes.c_double)]
+        L.ref_bench_destroy.argtypes = [ctypes.c_void_p]
+        L.ref_time_head.restype = ctypes.c_double
+        L.ref_time_head.argtypes = [ctypes.c_int64] * 4
 
     def grad_step(self, c, seed, bf16, tokens, targets=None):
         targets = tokens if targets is None else targets
@@ -230,6 +237,26 @@ class Reference(_Lib):
 
     def time_train_step(self, c, bf16=True, steps=3, warmup=1):
         t = self.lib.ref_time_train_step(ctypes.byref(c), int(bf16), steps, warmup)
+        if t < 0:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return t
+
+    def bench_create(self, B, S, h, f, V):
+        ctx = self.lib.ref_bench_create(B, S, h, f, V)
+        if not ctx:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return ctx
+
+    def bench_run(self, ctx):
+        b, hd = ctypes.c_double(), ctypes.c_double()
+        self._ok(self.lib.ref_bench_run(ctx, ctypes.byref(b), ctypes.byref(hd)))
+        return b.value, hd.value
+
+    def bench_destroy(self, ctx):
+        self.lib.ref_bench_destroy(ctx)
+
+    def time_head(self, rows, h, V, reps=1):
+        t = self.lib.ref_time_head(rows, h, V, reps)
         if t < 0:
             raise RuntimeError(self.lib.ref_last_error().decode())
         return t

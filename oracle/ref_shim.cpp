@@ -10,6 +10,7 @@
 //   block_forward/backward proj/include/hlm/kernels.hpp:313-383
 //   bf16_bits_from_f32     proj/include/hlm/bf16.hpp:15-25
 #include <chrono>
+#include <memory>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -328,5 +329,111 @@ double ref_time_block(int64_t B, int64_t S, int64_t h, int64_t f, int64_t reps) 
     return -1.0;
   }
 }
+
+// Wall-clock seconds of the head: head_fwd + ce_loss_and_grad + head_bwd
+// (kernels.hpp:410-446) at (rows, h, V) — the other half of the C2+ estimate.
+double ref_time_head(int64_t rows, int64_t h, int64_t V, int64_t reps) {
+  try {
+    std::vector<float> head(static_cast<std::size_t>(V * h)), x(static_cast<std::size_t>(rows * h)),
+        logits(static_cast<std::size_t>(rows * V)), dl(logits.size()), dx(x.size()), dhead(head.size(), 0.f);
+    Rng rng(11);
+    for (auto& v : head) v = rng.trunc_normal(0.02f);
+    for (auto& v : x) v = rng.normal();
+    std::vector<std::int32_t> tgt(static_cast<std::size_t>(rows));
+    for (auto& t : tgt) t = rng.uniform_int(static_cast<std::int32_t>(V));
+    PlainMat<float> hm{head.data(), V, h};
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int64_t r = 0; r < reps; ++r) {
+      head_fwd(x.data(), hm, logits.data(), rows, h, V);
+      (void)ce_loss_and_grad(logits.data(), tgt.data(), dl.data(), rows, V);
+      head_bwd(x.data(), dl.data(), hm, dx.data(), dhead.data(), rows, h, V);
+    }
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() /
+           static_cast<double>(reps);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1.0;
+  }
+}
+
+// Persistent context for the bench's reference arm: one block (fwd +
+// recompute + bwd) and the head (fwd + CE + bwd) at full width (h, f, V) on a
+// reduced token count T = B*S, run through the reference kernels. Weights are
+// filled with a cheap nonzero pattern (timing does not depend on values; the
+// zero-skip in matmul_grad_acc never triggers).
+struct RefBench {
+  int64_t B, S, h, f, V, T;
+  std::vector<float> w, grads, x, hout, g, gin, n1, y, n2, p, up, gate;
+  std::vector<float> head, xh, logits, dl, dx, dhead;
+  std::vector<std::int32_t> tgt;
+  std::unique_ptr<ScratchBuf<float>> scratch;
+};
+
+void* ref_bench_create(int64_t B, int64_t S, int64_t h, int64_t f, int64_t V) {
+  try {
+    auto* b = new RefBench{B, S, h, f, V, B * S, {}, {}, {}, {}, {}, {}, {}, {}, {}, {}, {}, {}, {}, {}, {}, {}, {}, {}, {}, nullptr};
+    const int64_t n = 4 * h * h + 3 * h * f + 2 * h, T = b->T;
+    uint32_t st = 12345u;
+    auto fill = [&](std::vector<float>& v, std::size_t sz, float scale) {
+      v.resize(sz);
+      for (auto& e : v) {
+        st = st * 1664525u + 1013904223u;
+        e = scale * (static_cast<float>((st >> 9) & 0x3FFF) / 8192.0f - 1.0f + 1e-3f);
+      }
+    };
+    fill(b->w, static_cast<std::size_t>(n), 0.02f);
+    b->grads.assign(static_cast<std::size_t>(n), 0.f);
+    fill(b->x, static_cast<std::size_t>(T * h), 1.0f);
+    fill(b->g, static_cast<std::size_t>(T * h), 1e-3f);
+    b->hout.resize(b->x.size()); b->gin.resize(b->x.size()); b->n1.resize(b->x.size());
+    b->y.resize(b->x.size()); b->n2.resize(b->x.size());
+    b->p.resize(static_cast<std::size_t>(B * S * S));
+    b->up.resize(static_cast<std::size_t>(T * f)); b->gate.resize(b->up.size());
+    fill(b->head, static_cast<std::size_t>(V * h), 0.02f);
+    fill(b->xh, static_cast<std::size_t>(T * h), 1.0f);
+    b->logits.resize(static_cast<std::size_t>(T * V)); b->dl.resize(b->logits.size());
+    b->dx.resize(b->xh.size()); b->dhead.assign(b->head.size(), 0.f);
+    b->tgt.resize(static_cast<std::size_t>(T));
+    for (auto& t : b->tgt) { st = st * 1664525u + 1013904223u; t = static_cast<std::int32_t>(st % static_cast<uint32_t>(V)); }
+    b->scratch = std::make_unique<ScratchBuf<float>>(B, S, h, f);
+    return b;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+// seconds of {block fwd, block recompute, block bwd} and of {head fwd+CE+bwd}
+int ref_bench_run(void* ctx, double* block_s, double* head_s) {
+  try {
+    auto* b = static_cast<RefBench*>(ctx);
+    const BlockDims d{b->B, b->S, b->h, b->f};
+    ActPtrs<float> acts{b->n1.data(), b->p.data(), b->y.data(), b->n2.data(), b->up.data(), b->gate.data()};
+    const auto bw = block_views(b->w.data(), b->h, b->f);
+    BlockGradPtrs<float> gp;
+    float* q = b->grads.data();
+    auto take = [&](int64_t k) { float* r = q; q += k; return r; };
+    const int64_t h = b->h, f = b->f;
+    gp.w_q = take(h * h); gp.w_k = take(h * h); gp.w_v = take(h * h); gp.w_o = take(h * h);
+    gp.w_up = take(h * f); gp.w_gate = take(h * f); gp.w_down = take(f * h);
+    gp.norm1 = take(h); gp.norm2 = take(h);
+    auto t0 = std::chrono::steady_clock::now();
+    block_forward(b->x.data(), bw, d, acts, b->hout.data(), b->scratch->view());
+    block_forward(b->x.data(), bw, d, acts, b->hout.data(), b->scratch->view());
+    block_backward(b->x.data(), bw, d, acts, b->g.data(), b->gin.data(), gp, b->scratch->view());
+    *block_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    PlainMat<float> hm{b->head.data(), b->V, b->h};
+    t0 = std::chrono::steady_clock::now();
+    head_fwd(b->xh.data(), hm, b->logits.data(), b->T, b->h, b->V);
+    (void)ce_loss_and_grad(b->logits.data(), b->tgt.data(), b->dl.data(), b->T, b->V);
+    head_bwd(b->xh.data(), b->dl.data(), hm, b->dx.data(), b->dhead.data(), b->T, b->h, b->V);
+    *head_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+void ref_bench_destroy(void* ctx) { delete static_cast<RefBench*>(ctx); }
 
 }  // extern "C"

@@ -172,6 +172,11 @@ void attention_bwd(const HlmBlockDims& d, const uint16_t* q, const uint16_t* k, 
   }
 }
 
+void** hlm_timer_events() {
+  static void* ev[16] = {};
+  return ev;
+}
+
 }  // namespace
 
 extern "C" {
@@ -409,6 +414,86 @@ int hlm_cuda_attention_bwd(const HlmBlockDims* d, const void* q, const void* k, 
     attention_bwd(*d, (const uint16_t*)q, (const uint16_t*)k, (const uint16_t*)v, (const uint16_t*)o,
                   (const uint16_t*)d_o, lse, dsum, (uint16_t*)dq, (uint16_t*)dk, (uint16_t*)dv, ld,
                   static_cast<cudaStream_t>(stream));
+  });
+}
+
+int hlm_timer_record(int slot) {
+  static cudaEvent_t ev[16] = {};
+  if (slot < 0 || slot >= 16) return HLM_ERR_ARGS;
+  if (!ev[slot]) cudaEventCreate(&ev[slot]);
+  cudaDeviceSynchronize();
+  cudaEventRecord(ev[slot], 0);
+  cudaEventSynchronize(ev[slot]);
+  hlm_timer_events()[slot] = ev[slot];
+  return HLM_OK;
+}
+
+double hlm_timer_elapsed_ms(int a, int b) {
+  float ms = -1.f;
+  cudaEventElapsedTime(&ms, static_cast<cudaEvent_t>(hlm_timer_events()[a]), static_cast<cudaEvent_t>(hlm_timer_events()[b]));
+  return ms;
+}
+
+int hlm_cuda_bench_block_gemms(const HlmBlockDims* d, int iters, double* flops, double* ms_per_set, double* ms_per_launch) {
+  return guarded([&] {
+    validate(d);
+    const i64 T = d->batch * d->seq, h = d->hidden, f = d->ffn;
+    const int Ti = (int)T, hi = (int)h, fi = (int)f;
+    cudaStream_t s;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    auto alloc = [](size_t bytes) {
+      void* p = nullptr;
+      if (cudaMalloc(&p, bytes) != cudaSuccess) throw Failure{"bench alloc failed", HLM_ERR_CUDA};
+      cudaMemset(p, 0, bytes);
+      return p;
+    };
+    const i64 n = 4 * h * h + 3 * h * f + 2 * h;
+    uint16_t* W = (uint16_t*)alloc(n * 2);
+    uint16_t* X = (uint16_t*)alloc(T * f * 2);      // activations (T,h) / (T,f)
+    uint16_t* X3 = (uint16_t*)alloc(3 * T * h * 2);
+    uint16_t* U = (uint16_t*)alloc(2 * T * f * 2);
+    float* Y = (float*)alloc(T * f * 4);
+    float* G = (float*)alloc(n * 4);
+    const TileOff off(h, f);
+    std::vector<HlmGemmDesc> set;
+    HlmGemmDesc g = gdesc(Ti, hi, hi, X, h, 0, W + off.q, h, 1, X3, h, HLM_EPI_BF16);
+    g.G = 3; g.b_grouped = 1; g.b_gstride = h * h; g.c_gstride = T * h; set.push_back(g);
+    set.push_back(gdesc(Ti, hi, hi, X, h, 0, W + off.o, h, 1, Y, h, HLM_EPI_F32));
+    g = gdesc(Ti, fi, hi, X, h, 0, W + off.up, f, 1, U, f, HLM_EPI_BF16);
+    g.G = 2; g.b_grouped = 1; g.b_gstride = h * f; g.c_gstride = T * f; set.push_back(g);
+    set.push_back(gdesc(Ti, hi, fi, X, f, 0, W + off.down, h, 1, Y, h, HLM_EPI_F32));
+    set.push_back(gdesc(fi, hi, Ti, X, f, 1, X, h, 1, G + off.down, h, HLM_EPI_F32));
+    set.push_back(gdesc(Ti, fi, hi, X, h, 0, W + off.down, h, 0, U, f, HLM_EPI_BF16));
+    g = gdesc(hi, fi, Ti, X, h, 1, U, f, 1, G + off.up, f, HLM_EPI_F32);
+    g.G = 2; g.b_grouped = 1; g.b_gstride = T * f; g.c_gstride = h * f; set.push_back(g);
+    g = gdesc(Ti, hi, fi, U, f, 0, W + off.up, f, 0, Y, h, HLM_EPI_F32);
+    g.G = 2; g.kgroup = 1; g.a_grouped = 1; g.a_gstride = T * f; g.b_grouped = 1; g.b_gstride = h * f; set.push_back(g);
+    set.push_back(gdesc(hi, hi, Ti, X, h, 1, X, h, 1, G + off.o, h, HLM_EPI_F32));
+    set.push_back(gdesc(Ti, hi, hi, X, h, 0, W + off.o, h, 0, X3, h, HLM_EPI_BF16));
+    g = gdesc(hi, hi, Ti, X, h, 1, X3, h, 1, G + off.q, h, HLM_EPI_F32);
+    g.G = 3; g.b_grouped = 1; g.b_gstride = T * h; g.c_gstride = h * h; set.push_back(g);
+    g = gdesc(Ti, hi, hi, X3, h, 0, W + off.q, h, 0, Y, h, HLM_EPI_F32);
+    g.G = 3; g.kgroup = 1; g.a_grouped = 1; g.a_gstride = T * h; g.b_grouped = 1; g.b_gstride = h * h; set.push_back(g);
+    double fl = 0;
+    for (const auto& q : set) fl += 2.0 * q.M * (double)q.N * q.K * (q.G > 1 ? q.G : 1);
+    for (const auto& q : set) chk_gemm(q, s, "bench warmup");
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+    for (int it = 0; it < iters; ++it)
+      for (const auto& q : set) chk_gemm(q, s, "bench");
+    cudaEventRecord(b, s);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    *flops = fl;
+    *ms_per_set = ms / iters;
+    *ms_per_launch = ms / iters / (double)set.size();
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    for (void* p : {(void*)W, (void*)X, (void*)X3, (void*)U, (void*)Y, (void*)G}) cudaFree(p);
+    cudaStreamDestroy(s);
   });
 }
 

@@ -6,6 +6,7 @@
 #include "capi_util.h"
 #include "hlm_cuda.h"
 #include "../kernels/gemm.h"
+#include "../kernels/block_ops.h"
 
 extern "C" int hlm_cuda_gemm(const HlmGemmDesc* desc, void* stream) {
   const int rc = hlm_gemm_launch(desc, static_cast<cudaStream_t>(stream));
@@ -17,3 +18,5 @@ extern "C" int hlm_cuda_gemm(const HlmGemmDesc* desc, void* stream) {
   }
   return rc;
 }
+
+extern "C" long long hlm_cuda_launch_count(void) { return hlm_launches_total(); }

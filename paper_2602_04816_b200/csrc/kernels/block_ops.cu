@@ -492,10 +492,16 @@ struct Dummy {};
 }  // namespace
 
 // ====================================================================== launchers
+#include <atomic>
+static std::atomic<long long> g_launches{0};
+void hlm_count_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+long long hlm_launches_total() { return g_launches.load(std::memory_order_relaxed); }
+
 #define HLM_CHECK_LAUNCH() return cudaGetLastError() == cudaSuccess ? 0 : 1
 
 int hlm_ops_rmsnorm_fwd(const float* x, const void* scale, void* out, long long rows, int h, cudaStream_t s) {
   rmsnorm_fwd_kernel<<<grid_for(rows, 8), 256, 0, s>>>(x, (const __nv_bfloat16*)scale, (__nv_bfloat16*)out, rows, h);
+  hlm_count_launches(1);
   HLM_CHECK_LAUNCH();
 }
 
@@ -509,22 +515,26 @@ int hlm_ops_rmsnorm_bwd(const float* x, const void* scale, const float* g, const
   dim3 grid((h + 255) / 256, chunks);
   norm_scale_partial_kernel<<<grid, 256, 0, s>>>(x, g, inv_buf, partial, rows, h, rpc);
   norm_scale_reduce_kernel<<<(h + 255) / 256, 256, 0, s>>>(partial, dscale, chunks, h);
+  hlm_count_launches(3);
   HLM_CHECK_LAUNCH();
 }
 
 int hlm_ops_cast_bf16(const float* in, void* out, long long n, cudaStream_t s) {
   cast_f32_bf16_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, s>>>(in, (__nv_bfloat16*)out, n);
+  hlm_count_launches(1);
   HLM_CHECK_LAUNCH();
 }
 
 int hlm_ops_swiglu_fwd(const void* ug, void* act, long long n, cudaStream_t s) {
   swiglu_fwd_kernel<<<grid_for(n / 8 + 1, 256), 256, 0, s>>>((const __nv_bfloat16*)ug, (__nv_bfloat16*)act, n);
+  hlm_count_launches(1);
   HLM_CHECK_LAUNCH();
 }
 
 int hlm_ops_swiglu_bwd(const void* dact, const void* ug, void* dug, long long n, cudaStream_t s) {
   swiglu_bwd_kernel<<<grid_for(n, 256), 256, 0, s>>>((const __nv_bfloat16*)dact, (const __nv_bfloat16*)ug,
                                                     (__nv_bfloat16*)dug, n);
+  hlm_count_launches(1);
   HLM_CHECK_LAUNCH();
 }
 
@@ -532,18 +542,21 @@ int hlm_ops_rope(void* x, const float* cs, const float* sn, long long rows, int 
                  int nmats, long long mat_stride, cudaStream_t s) {
   rope_kernel<<<grid_for(rows * (h / 2) * nmats, 256), 256, 0, s>>>((__nv_bfloat16*)x, cs, sn, rows, h, hd, S,
                                                                      inverse, nmats, mat_stride);
+  hlm_count_launches(1);
   HLM_CHECK_LAUNCH();
 }
 
 int hlm_ops_embed_fwd(const int32_t* tok, const void* table, float* out, long long rows, int h, int vocab,
                       int* err, cudaStream_t s) {
   embed_fwd_kernel<<<grid_for(rows * h, 256), 256, 0, s>>>(tok, (const __nv_bfloat16*)table, out, rows, h, vocab, err);
+  hlm_count_launches(1);
   HLM_CHECK_LAUNCH();
 }
 
 int hlm_ops_embed_bwd(const int32_t* row_ptr, const int32_t* pos, const float* g, float* d_table, int vocab,
                       int h, int accumulate, cudaStream_t s) {
   embed_bwd_kernel<<<grid_for((long long)vocab * h, 256), 256, 0, s>>>(row_ptr, pos, g, d_table, vocab, h, accumulate);
+  hlm_count_launches(1);
   HLM_CHECK_LAUNCH();
 }
 
@@ -551,6 +564,7 @@ int hlm_ops_ce(const float* logits, long long ld_in, const int32_t* tgt, void* d
                float* loss_row, long long rows, int vocab, float inv_rows, int* err, cudaStream_t s) {
   ce_kernel<512><<<(unsigned)rows, 512, 0, s>>>(logits, ld_in, tgt, (__nv_bfloat16*)dl, ld_out, loss_row, vocab,
                                                 inv_rows, err);
+  hlm_count_launches(5);
   HLM_CHECK_LAUNCH();
 }
 
@@ -559,6 +573,7 @@ template <int VPL>
 int attn_generic(const void* q, const void* k, const void* v, void* o, float* lse, int B, int S, int H, int hd,
                  int ld, cudaStream_t s) {
   const long long warps = (long long)B * H * S;
+  hlm_count_launches(1);
   attn_fwd_generic<VPL><<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(
       (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, (const __nv_bfloat16*)v, (__nv_bfloat16*)o, lse, B, S, H,
       hd, ld, 1.0f / sqrtf((float)hd));
@@ -571,6 +586,7 @@ int attn_bwd_generic(const void* q, const void* k, const void* v, const void* o,
   const long long warps = (long long)B * H * S;
   const unsigned grid = (unsigned)((warps + 7) / 8);
   const float scale = 1.0f / sqrtf((float)hd);
+  hlm_count_launches(3);
   attn_bwd_dsum<<<grid, 256, 0, s>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, dsum, B, S, H, hd, ld);
   attn_bwd_dq_generic<VPL><<<grid, 256, 0, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
                                                 (const __nv_bfloat16*)v, (const __nv_bfloat16*)dout, lse, dsum,

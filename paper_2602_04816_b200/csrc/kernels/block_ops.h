@@ -27,3 +27,7 @@ int hlm_ops_attention_fwd_generic(const void* q, const void* k, const void* v, v
 int hlm_ops_attention_bwd_generic(const void* q, const void* k, const void* v, const void* o, const void* dout,
                                   const float* lse, float* dsum, void* dq, void* dk, void* dv, int B, int S, int H,
                                   int hd, int ld, cudaStream_t s);
+
+// Kernel launches issued by this library since load (all launchers add to it).
+void hlm_count_launches(long long n);
+long long hlm_launches_total();

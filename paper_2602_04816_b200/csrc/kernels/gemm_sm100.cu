@@ -26,6 +26,7 @@
 
 #include "gemm.h"
 #include "sm100_ptx.cuh"
+#include "block_ops.h"
 
 using namespace hlm_sm100;
 
@@ -352,6 +353,7 @@ int launch(const HlmGemmDesc& d, cudaStream_t stream) {
   }
   const int grid = a.num_tiles < sm_count() ? a.num_tiles : sm_count();
   gemm_kernel<A_MN, B_MN><<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(ma, mb, a);
+  hlm_count_launches(1);
   attr_set = true;
   return cudaGetLastError() == cudaSuccess ? 0 : HLM_GEMM_ERR_LAUNCH;
 }
