@@ -441,10 +441,11 @@ int hlm_cuda_bench_block_gemms(const HlmBlockDims* d, int iters, double* flops, 
     const int Ti = (int)T, hi = (int)h, fi = (int)f;
     cudaStream_t s;
     cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
-    auto alloc = [](size_t bytes) {
+    auto alloc = [s](size_t bytes) {
       void* p = nullptr;
       if (cudaMalloc(&p, bytes) != cudaSuccess) throw Failure{"bench alloc failed", HLM_ERR_CUDA};
-      cudaMemset(p, 0, bytes);
+      // random bf16 bit patterns in [-1, 1) magnitude range: zero operands understate tensor-core power
+      hlm_ops_fill_random_bf16(p, static_cast<long long>(bytes / 2), 0x1234u, s);
       return p;
     };
     const i64 n = 4 * h * h + 3 * h * f + 2 * h;

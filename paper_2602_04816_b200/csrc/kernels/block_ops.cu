@@ -486,8 +486,14 @@ __global__ void attn_bwd_dkv_generic(const __nv_bfloat16* __restrict__ q, const 
   }
 }
 
-template <template <int> class K>
-struct Dummy {};
+__global__ void fill_random_bf16_kernel(__nv_bfloat16* p, long long n, unsigned seed) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    unsigned x = (unsigned)i * 2654435761u ^ seed;
+    x ^= x >> 16; x *= 0x7feb352du; x ^= x >> 15; x *= 0x846ca68bu; x ^= x >> 16;
+    p[i] = __float2bfloat16_rn(((float)(x >> 8) / 16777216.0f) * 2.0f - 1.0f);
+  }
+}
 
 }  // namespace
 
@@ -498,6 +504,11 @@ void hlm_count_launches(long long n) { g_launches.fetch_add(n, std::memory_order
 long long hlm_launches_total() { return g_launches.load(std::memory_order_relaxed); }
 
 #define HLM_CHECK_LAUNCH() return cudaGetLastError() == cudaSuccess ? 0 : 1
+
+int hlm_ops_fill_random_bf16(void* p, long long n, unsigned seed, cudaStream_t s) {
+  fill_random_bf16_kernel<<<grid_for(n, 256), 256, 0, s>>>((__nv_bfloat16*)p, n, seed);
+  HLM_CHECK_LAUNCH();
+}
 
 int hlm_ops_rmsnorm_fwd(const float* x, const void* scale, void* out, long long rows, int h, cudaStream_t s) {
   rmsnorm_fwd_kernel<<<grid_for(rows, 8), 256, 0, s>>>(x, (const __nv_bfloat16*)scale, (__nv_bfloat16*)out, rows, h);

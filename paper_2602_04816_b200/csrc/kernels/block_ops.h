@@ -31,3 +31,5 @@ int hlm_ops_attention_bwd_generic(const void* q, const void* k, const void* v, c
 // Kernel launches issued by this library since load (all launchers add to it).
 void hlm_count_launches(long long n);
 long long hlm_launches_total();
+// Deterministic pseudo-random bf16 fill (bench / probe inputs), |x| < 1.
+int hlm_ops_fill_random_bf16(void* p, long long n, unsigned seed, cudaStream_t s);
