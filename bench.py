@@ -60,7 +60,7 @@ def model_numbers(m):
     attn_fwd = 2.0 * B * S * S * h
     model_flops = 6.0 * T * (L * n_mm + V * h) + 3.0 * L * attn_fwd
     hw_flops = model_flops + L * (2.0 * n_mm * T + attn_fwd)
-    h2d = 2 * (2 * L * n + 2 * V * h)       # bf16 weights: forward + fused recompute/backward
+    h2d = 2 * (2 * L * n + 2 * V * h)       # bf16 weights: forward + fused recompute/backward (no cache)
     d2h = 4 * (L * n + 2 * V * h)           # fp32 gradients
     return dict(T=T, n=n, n_mm=n_mm, model_flops=model_flops, hw_flops=hw_flops, h2d=h2d, d2h=d2h,
                 params=(2 * V * h + L * n))
@@ -180,7 +180,10 @@ def run_ours(args, m, name):
     nums = model_numbers(m)
     t0 = time.time()
     store = E.Store(cfg, 1234, "bf16", init="parallel")
-    arena = E.Arena(cfg, device=local)
+    # HBM weight cache for the backward turnaround: all blocks when they fit next to the arena
+    blk = (2 * nums["n"] + 255) // 256 * 256
+    cache = min(m["layers"], int(args.cache_gb * 1e9) // blk) * blk
+    arena = E.Arena(cfg, device=local, weight_cache_bytes=cache)
     opts = E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=args.slabs,
                            record_trace=True)
     eng = E.Engine(store, arena, E.HyperParams(lr=1e-4), opts)
@@ -305,6 +308,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--slabs", type=int, default=3)
+    ap.add_argument("--cache-gb", type=float, default=60.0,
+                    help="HBM weight cache (block tiles resident between forward and backward)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     m = dict(CONFIGS[args.config])

@@ -19,8 +19,8 @@
 
 namespace hlm {
 
-enum class Region : int { Stream0 = 0, Stream1 = 1, Stack = 2, Anchors = 3, Workspace = 4 };
-inline constexpr int kRegionCount = 5;
+enum class Region : int { Stream0 = 0, Stream1 = 1, Stack = 2, Anchors = 3, Workspace = 4, WeightCache = 5 };
+inline constexpr int kRegionCount = 6;
 const char* region_name(Region r);
 
 struct LedgerEvent {
@@ -65,7 +65,10 @@ class DeviceArena {
 public:
     // budget_cap: hard limit the footprint must fit (first region that does
     // not fit is named in the ArenaOomError). device: CUDA ordinal.
-    DeviceArena(const ModelConfig& config, std::optional<i64> budget_cap = std::nullopt, int device = -1);
+    // weight_cache_bytes: optional HBM region that keeps forward-streamed block
+    // weights resident for the backward turnaround (one H2D pass per cached layer).
+    DeviceArena(const ModelConfig& config, std::optional<i64> budget_cap = std::nullopt, int device = -1,
+                i64 weight_cache_bytes = 0);
     ~DeviceArena();
     DeviceArena(const DeviceArena&) = delete;
     DeviceArena& operator=(const DeviceArena&) = delete;
@@ -84,6 +87,12 @@ public:
     void* buffer(int i) const { return stream_[i]; }
     i64 h2d_bytes() const { return h2d_bytes_; }
     void add_h2d(i64 bytes) { h2d_bytes_ += bytes; }
+
+    // weight cache: `cache_slots()` block-sized slots
+    i64 cache_slots() const { return cache_slots_; }
+    void* cache_slot(i64 s) const { return cache_base_ + s * fp_.stream_buf_block; }
+    void claim_cache_slot(i64 s);
+    void release_cache_slots();
 
     // activation stack (LIFO, K slabs of A_max)
     void* push_acts();
@@ -126,6 +135,9 @@ private:
     i64 occupant_[2] = {-1, -1};
     i64 occupant_bytes_[2] = {0, 0};
     char* stack_base_ = nullptr;
+    char* cache_base_ = nullptr;
+    i64 cache_slots_ = 0;
+    std::vector<bool> cache_live_;
     i64 depth_ = 0;
     char* anchors_base_ = nullptr;
     std::vector<bool> anchor_live_;

@@ -98,7 +98,11 @@ private:
     };
 
     void anchor_loss_async();
-    int stream_tile(i64 tile_id, i64* op_id);
+    // Returns a weight "buffer" id: 0/1 = stream buffers, 2+s = weight-cache slot s.
+    // forward_pass: a cacheable block streams into its cache slot; later passes
+    // of the same step reuse the resident copy without any H2D.
+    int stream_tile(i64 tile_id, i64* op_id, bool forward_pass = false);
+    void* weights_ptr(int buf) const;
     void compute_wait_weights(int buf);
     void compute_done_with(int buf, i64 op_id);
     int next_grad_buf();
@@ -147,6 +151,9 @@ private:
     i64 recompute_forwards_ = 0;
     std::vector<i64> consumers_left_;
     std::vector<HostOpRecord> host_ops_;   // guarded by mu_
+    std::vector<i64> cache_slot_of_;       // per logical tile, -1 when not cached
+    std::vector<i64> cache_xfer_op_;       // per slot: this step's WeightXfer op, -1 if not resident
+    std::vector<void*> ev_cache_ready_;
 
     // worker
     std::mutex mu_;

@@ -74,18 +74,24 @@ inline WorkspaceLayout workspace_layout(const ModelConfig& m) {
 
 struct ArenaFootprint {
     i64 stream_buf = 0;    // per buffer
+    i64 stream_buf_block = 0;   // one block tile in bf16 (a weight-cache slot)
+    i64 weight_cache = 0;  // optional HBM weight cache (multiple of stream_buf_block)
     i64 anchor_slot = 0;   // per anchor
     i64 anchor_slots = 0;  // ceil(L/K) + 1
     i64 stack = 0;         // K x (A_max + fp32 block output)
     i64 workspace = 0;
     i64 anchors_total() const { return anchor_slots * anchor_slot; }
-    i64 core_total() const { return 2 * stream_buf + stack + workspace; }
+    i64 core_total() const { return 2 * stream_buf + stack + workspace + weight_cache; }
     i64 total() const { return core_total() + anchors_total(); }
 };
 
-inline ArenaFootprint arena_footprint(const ModelConfig& m) {
+inline ArenaFootprint arena_footprint(const ModelConfig& m, i64 weight_cache_bytes = 0) {
     ArenaFootprint fp;
     fp.stream_buf = stream_buf_bytes(m);
+    fp.stream_buf_block = (2 * m.block_params() + 255) / 256 * 256;
+    i64 slots = weight_cache_bytes / fp.stream_buf_block;
+    if (slots > m.layers) slots = m.layers;
+    fp.weight_cache = slots * fp.stream_buf_block;
     fp.anchor_slot = align256(anchor_slot_bytes(m));
     fp.anchor_slots = m.anchor_capacity();
     // each stack slab: the block's activations + its fp32 output (the next

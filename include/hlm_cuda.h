@@ -223,6 +223,10 @@ int hlm_store_bitwise_equal(const HlmStore* a, const HlmStore* b);
 int hlm_store_adam_step(HlmStore* s, const float* grads, const HlmHyper* hp, int64_t t);
 
 int hlm_arena_create(const HlmModelConfig* cfg, int64_t budget_cap, int device, HlmArena** out);
+/* + an HBM weight cache of weight_cache_bytes (block tiles resident between the
+ * forward and the backward of a step: one H2D pass for every cached layer) */
+int hlm_arena_create_ex(const HlmModelConfig* cfg, int64_t budget_cap, int device, int64_t weight_cache_bytes,
+                        HlmArena** out);
 void hlm_arena_destroy(HlmArena* a);
 /* out[5] = stream_buf, anchor_slot, anchor_slots, stack, workspace (bytes) */
 int hlm_arena_footprint(const HlmModelConfig* cfg, int64_t* out);

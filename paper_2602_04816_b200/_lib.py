@@ -47,7 +47,7 @@ def lib():
             raise RuntimeError(
                 f"{LIB_PATH} is missing: run __graft_entry__.build() (make -C "
                 "paper_2602_04816_b200/csrc). The CUDA path has no fallback.")
-        _lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+        _lib = ctypes.CDLL(LIB_PATH)
         _lib.hlm_cuda_last_error.restype = ctypes.c_char_p
         _lib.hlm_cuda_gemm.argtypes = [ctypes.POINTER(HlmGemmDesc), ctypes.c_void_p]
     return _lib

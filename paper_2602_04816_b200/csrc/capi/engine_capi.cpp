@@ -204,6 +204,17 @@ int hlm_arena_create(const HlmModelConfig* cfg, int64_t budget_cap, int device, 
     });
 }
 
+int hlm_arena_create_ex(const HlmModelConfig* cfg, int64_t budget_cap, int device, int64_t weight_cache_bytes,
+                        HlmArena** out) {
+    return guarded([&] {
+        auto a = std::make_unique<HlmArena>();
+        std::optional<hlm::i64> cap;
+        if (budget_cap > 0) cap = budget_cap;
+        a->a = std::make_unique<hlm::DeviceArena>(to_model(cfg), cap, device, weight_cache_bytes);
+        *out = a.release();
+    });
+}
+
 void hlm_arena_destroy(HlmArena* a) { delete a; }
 
 int hlm_arena_footprint(const HlmModelConfig* cfg, int64_t* out) {

@@ -73,6 +73,14 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
     if (m.rope_theta > 0)
         ck_hlm(hlm_cuda_rope_table(arena_.rope_cos(), arena_.rope_sin(), m.seq, m.head_dim(), m.rope_theta),
                "rope table");
+    // weight cache: the last `slots` blocks stay resident between forward and backward
+    cache_slot_of_.assign(static_cast<size_t>(m.tile_count()), -1);
+    const i64 slots = arena_.cache_slots();
+    for (i64 s = 0; s < slots; ++s) {
+        cache_slot_of_[static_cast<size_t>(m.layers - slots + 1 + s)] = s;
+        ev_cache_ready_.push_back(new_event(false));
+    }
+    cache_xfer_op_.assign(static_cast<size_t>(slots), -1);
     if (opts_.threaded_accum) worker_ = std::thread([this] { worker_loop(); });
 }
 
@@ -95,6 +103,7 @@ Engine::~Engine() {
         cudaEventDestroy(E(ev_gradbuf_free_[i]));
     }
     for (void* e : ev_slab_done_) cudaEventDestroy(E(e));
+    for (void* e : ev_cache_ready_) cudaEventDestroy(E(e));
     for (void* e : timing_events_) cudaEventDestroy(E(e));
     cudaStreamDestroy(S(h2d_));
     cudaStreamDestroy(S(compute_));
@@ -130,7 +139,40 @@ void Engine::op_end(i64 id, void* stream) {
 // reference engine.cpp:55-71: alternate buffers, release the old occupant,
 // H2D (here straight from the pinned bf16 shadow: no staging copy), with a
 // buffer-free dependency on the buffer's last reader.
-int Engine::stream_tile(i64 tile_id, i64* op_id) {
+void* Engine::weights_ptr(int buf) const {
+    return buf >= 2 ? arena_.cache_slot(buf - 2) : arena_.buffer(buf);
+}
+
+int Engine::stream_tile(i64 tile_id, i64* op_id, bool forward_pass) {
+    const i64 slot = cache_slot_of_[static_cast<size_t>(tile_id)];
+    if (slot >= 0) {
+        if (cache_xfer_op_[static_cast<size_t>(slot)] >= 0) {   // resident since this step's forward
+            *op_id = cache_xfer_op_[static_cast<size_t>(slot)];
+            return 2 + static_cast<int>(slot);
+        }
+        if (forward_pass) {
+            const LayerTile& tile = store_.tile(tile_id);
+            const i64 bytes = tile.weight_bytes();
+            arena_.claim_cache_slot(slot);
+            StreamOp op;
+            op.stream = StreamId::H2D;
+            op.kind = OpKind::WeightXfer;
+            op.layer = tile_id;
+            op.buf = 2 + slot;
+            op.bytes = bytes;
+            op.pinned = store_.shadow_pinned();
+            const i64 id = op_begin(std::move(op), h2d_);
+            ck(cudaMemcpyAsync(arena_.cache_slot(slot), tile.shadow(), static_cast<size_t>(bytes),
+                               cudaMemcpyHostToDevice, S(h2d_)),
+               "H2D weights (cache)");
+            op_end(id, h2d_);
+            ck(cudaEventRecord(E(ev_cache_ready_[static_cast<size_t>(slot)]), S(h2d_)), "record cache ready");
+            arena_.add_h2d(bytes);
+            cache_xfer_op_[static_cast<size_t>(slot)] = id;
+            *op_id = id;
+            return 2 + static_cast<int>(slot);
+        }
+    }
     const int buf = next_buf_;
     next_buf_ ^= 1;
     if (arena_.buffer_occupant(buf) != -1) arena_.release_buffer(buf);
@@ -157,10 +199,12 @@ int Engine::stream_tile(i64 tile_id, i64* op_id) {
 }
 
 void Engine::compute_wait_weights(int buf) {
-    ck(cudaStreamWaitEvent(S(compute_), E(ev_w_ready_[buf]), 0), "wait weights");
+    void* ev = buf >= 2 ? ev_cache_ready_[static_cast<size_t>(buf - 2)] : ev_w_ready_[buf];
+    ck(cudaStreamWaitEvent(S(compute_), E(ev), 0), "wait weights");
 }
 
 void Engine::compute_done_with(int buf, i64 op_id) {
+    if (buf >= 2) return;   // cache slots are rewritten only by the next step's forward
     ck(cudaEventRecord(E(ev_buf_free_[buf]), S(compute_)), "record buf free");
     last_reader_[buf] = op_id;
 }
@@ -346,6 +390,7 @@ void Engine::begin_step(const Batch& batch) {
         for (i64 p = 0; p < store_.physical_tiles(); ++p)
             consumers_left_[static_cast<size_t>(p)] = store_.consumer_count(p);
     }
+    std::fill(cache_xfer_op_.begin(), cache_xfer_op_.end(), -1);
     step_t_ = store_.adam_steps() + 1;
     d2h_base_ = pool_->d2h_bytes();
     recompute_forwards_ = 0;
@@ -388,7 +433,7 @@ void Engine::forward_streaming() {
     op.flops = fwd_flops(m.embed_params(), T);
     op.deps.push_back(w_op);
     i64 id = op_begin(op, compute_);
-    ck_hlm(hlm_cuda_embed_fwd(arena_.tokens(), arena_.buffer(ebuf), h0, T, m.hidden, m.vocab, arena_.err_flag(),
+    ck_hlm(hlm_cuda_embed_fwd(arena_.tokens(), weights_ptr(ebuf), h0, T, m.hidden, m.vocab, arena_.err_flag(),
                               compute_),
            "embed_fwd");
     op_end(id, compute_);
@@ -396,7 +441,7 @@ void Engine::forward_streaming() {
     h_cur_ = h0;
     int roll = 0;
     for (i64 i = 1; i <= m.layers; ++i) {
-        const int buf = stream_tile(i, &w_op);
+        const int buf = stream_tile(i, &w_op, true);
         compute_wait_weights(buf);
         float* out = (i % m.k_ckpt == 0) ? arena_.anchor_checkpoint(i) : arena_.h_roll(roll);
         if (i % m.k_ckpt != 0) roll ^= 1;
@@ -408,7 +453,7 @@ void Engine::forward_streaming() {
         bo.flops = fwd_flops(m.block_params(), T);
         bo.deps.push_back(w_op);
         id = op_begin(bo, compute_);
-        ck_hlm(hlm_cuda_block_fwd(&dims, arena_.buffer(buf), h_cur_, out, arena_.discard_acts(), arena_.block_ws(), rc,
+        ck_hlm(hlm_cuda_block_fwd(&dims, weights_ptr(buf), h_cur_, out, arena_.discard_acts(), arena_.block_ws(), rc,
                                   rs, compute_),
                "block_fwd");
         op_end(id, compute_);
@@ -449,7 +494,7 @@ void Engine::anchor_loss_async() {
     op.flops = fwd_flops(m.embed_params(), T);
     op.deps.push_back(w_op);
     const i64 fid = op_begin(op, compute_);
-    ck_hlm(hlm_cuda_head_loss(T, m.hidden, m.vocab, arena_.buffer(buf), h_cur_, arena_.targets(),
+    ck_hlm(hlm_cuda_head_loss(T, m.hidden, m.vocab, weights_ptr(buf), h_cur_, arena_.targets(),
                               1.0f / static_cast<float>(T), arena_.g_roll(g_cur_), arena_.grad_out(gb), 0,
                               arena_.loss_rows(), arena_.head_ws(), compute_),
            "head_loss");
@@ -508,7 +553,7 @@ void Engine::backward_blockwise() {
             rop.flops = fwd_flops(n_block, T);
             rop.deps.push_back(w_op);
             i64 id = op_begin(rop, compute_);
-            ck_hlm(hlm_cuda_block_fwd(&dims, arena_.buffer(buf), anchor, arena_.h_roll(0), a, arena_.block_ws(), rc, rs,
+            ck_hlm(hlm_cuda_block_fwd(&dims, weights_ptr(buf), anchor, arena_.h_roll(0), a, arena_.block_ws(), rc, rs,
                                       compute_),
                    "block_fwd (recompute)");
             op_end(id, compute_);
@@ -522,7 +567,7 @@ void Engine::backward_blockwise() {
             bop.flops = bwd_flops(n_block, T);
             bop.deps.push_back(w_op);
             const i64 lb = op_begin(bop, compute_);
-            ck_hlm(hlm_cuda_block_bwd(&dims, arena_.buffer(buf), anchor, a, arena_.g_roll(g_cur_),
+            ck_hlm(hlm_cuda_block_bwd(&dims, weights_ptr(buf), anchor, a, arena_.g_roll(g_cur_),
                                       arena_.g_roll(g_cur_ ^ 1), arena_.grad_out(gb), arena_.block_ws(), rc, rs,
                                       compute_),
                    "block_bwd");
@@ -555,7 +600,7 @@ void Engine::backward_blockwise() {
                 rop.flops = fwd_flops(n_block, T);
                 rop.deps.push_back(w_op);
                 const i64 id = op_begin(rop, compute_);
-                ck_hlm(hlm_cuda_block_fwd(&dims, arena_.buffer(buf), x, out, a, arena_.block_ws(), rc, rs, compute_),
+                ck_hlm(hlm_cuda_block_fwd(&dims, weights_ptr(buf), x, out, a, arena_.block_ws(), rc, rs, compute_),
                        "block_fwd (recompute)");
                 op_end(id, compute_);
                 compute_done_with(buf, id);
@@ -576,7 +621,7 @@ void Engine::backward_blockwise() {
                 bop.flops = bwd_flops(n_block, T);
                 bop.deps.push_back(w_op);
                 const i64 lb = op_begin(bop, compute_);
-                ck_hlm(hlm_cuda_block_bwd(&dims, arena_.buffer(buf), inputs[static_cast<size_t>(i - lo)],
+                ck_hlm(hlm_cuda_block_bwd(&dims, weights_ptr(buf), inputs[static_cast<size_t>(i - lo)],
                                           acts[static_cast<size_t>(i - lo)], arena_.g_roll(g_cur_),
                                           arena_.g_roll(g_cur_ ^ 1), arena_.grad_out(gb), arena_.block_ws(), rc, rs,
                                           compute_),
@@ -701,6 +746,7 @@ StepResult Engine::finish_step() {
 
     for (int b = 0; b < 2; ++b)
         if (arena_.buffer_occupant(b) != -1) arena_.release_buffer(b);
+    arena_.release_cache_slots();
     arena_.release_workspace();
 
     StepResult r;
@@ -736,6 +782,8 @@ StepResult Engine::train_step(const Batch& batch) {
         }
         for (int b = 0; b < 2; ++b)
             if (arena_.buffer_occupant(b) != -1) arena_.release_buffer(b);
+        arena_.release_cache_slots();
+        std::fill(cache_xfer_op_.begin(), cache_xfer_op_.end(), -1);
         while (arena_.stack_depth() > 0) arena_.pop_acts();
         for (i64 i = 0; i <= store_.config().layers; i += store_.config().k_ckpt) {
             try {

@@ -435,7 +435,11 @@ void adam_kernel(float* __restrict w, float* __restrict m, float* __restrict v, 
             _mm512_storeu_ps(m + i, mm);
             _mm512_storeu_ps(v + i, vv);
             _mm512_storeu_ps(w + i, th);
-            _mm256_storeu_si256(reinterpret_cast<__m256i*>(shadow + i), bf16x16(th));
+            // the shadow is only read by the next H2D DMA: stream it past the cache (no RFO)
+            if ((reinterpret_cast<uintptr_t>(shadow + i) & 31) == 0)
+                _mm256_stream_si256(reinterpret_cast<__m256i*>(shadow + i), bf16x16(th));
+            else
+                _mm256_storeu_si256(reinterpret_cast<__m256i*>(shadow + i), bf16x16(th));
             if (zero_after) _mm512_storeu_ps(zero_after + i, _mm512_setzero_ps());
         }
         for (; i < e; ++i) {
@@ -450,6 +454,7 @@ void adam_kernel(float* __restrict w, float* __restrict m, float* __restrict v, 
             shadow[i] = bf16_bits_from_f32(th);
             if (zero_after) zero_after[i] = 0.0f;
         }
+        _mm_sfence();
     }
 }
 

@@ -125,6 +125,8 @@ def _L():
         L.hlm_store_bitwise_equal.argtypes = [_vp, _vp]
         L.hlm_store_adam_step.argtypes = [_vp, _f32p, P(HyperParams), ctypes.c_int64]
         L.hlm_arena_create.argtypes = [P(ModelConfig), ctypes.c_int64, ctypes.c_int, P(_vp)]
+        L.hlm_arena_create_ex.argtypes = [P(ModelConfig), ctypes.c_int64, ctypes.c_int,
+                                          ctypes.c_int64, P(_vp)]
         L.hlm_arena_destroy.argtypes = [_vp]
         L.hlm_arena_footprint.argtypes = [P(ModelConfig), np.ctypeslib.ndpointer(np.int64)]
         L.hlm_engine_create.argtypes = [_vp, _vp, P(HyperParams), P(EngineOptions), P(_vp)]
@@ -201,11 +203,13 @@ def arena_footprint(cfg):
 
 
 class Arena:
-    """Device arena: one cudaMalloc carved into the reference regions."""
+    """Device arena: one cudaMalloc carved into the reference regions (+ an
+    optional HBM weight cache of `weight_cache_bytes`)."""
 
-    def __init__(self, cfg, budget_cap=0, device=-1):
+    def __init__(self, cfg, budget_cap=0, device=-1, weight_cache_bytes=0):
         h = _vp()
-        _check(_L().hlm_arena_create(ctypes.byref(cfg), budget_cap, device, ctypes.byref(h)))
+        _check(_L().hlm_arena_create_ex(ctypes.byref(cfg), budget_cap, device, weight_cache_bytes,
+                                        ctypes.byref(h)))
         self.h = h
 
     def __del__(self):

@@ -207,3 +207,26 @@ def test_training_tracks_oracle_mixed_precision():
     l = np.array(out["losses"])
     assert np.all(np.abs(l - ref) / ref < 1e-2), (l, ref)
     assert l[-1] < 0.8 * l[0]
+
+
+def test_weight_cache_is_bitwise_neutral_and_halves_h2d():
+    """HBM weight cache: cached blocks cross PCIe once per step; gradients and
+    the optimizer trajectory are bitwise unchanged."""
+    c = E.ModelConfig(4, 32, 64, 32, 16, 2, k_ckpt=1)
+    tok = [E.make_copy_task_batch(c, 7, skip=i) for i in range(3)]
+    s0 = E.Store(c, 5)
+    e0 = E.Engine(s0, E.Arena(c), E.HyperParams(lr=2e-3), E.EngineOptions(eager_optim=True))
+    r0 = [e0.train_step(t) for t in tok]
+    blk = 2 * c.block_params()
+    for cache_layers in (2, 4):
+        s1 = E.Store(c, 5)
+        a1 = E.Arena(c, weight_cache_bytes=cache_layers * ((blk + 255) // 256 * 256))
+        e1 = E.Engine(s1, a1, E.HyperParams(lr=2e-3), E.EngineOptions(eager_optim=True))
+        r1 = [e1.train_step(t) for t in tok]
+        assert s0.bitwise_equal(s1)
+        assert [x.loss for x in r0] == [x.loss for x in r1]
+        assert r0[-1].h2d_bytes - r1[-1].h2d_bytes == cache_layers * blk
+        ops = e1.last_trace()
+        xfer_layers = [o["layer"] for o in ops if o["kind"] == "WeightXfer"]
+        for l in range(c.layers - cache_layers + 1, c.layers + 1):
+            assert xfer_layers.count(l) == 1
