@@ -185,7 +185,8 @@ def run_ours(args, m, name):
     cache = min(m["layers"], int(args.cache_gb * 1e9) // blk) * blk
     arena = E.Arena(cfg, device=local, weight_cache_bytes=cache)
     opts = E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=args.slabs,
-                           record_trace=True)
+                           record_trace=True, overlap_optimizer_tail=args.tail_blocks >= 0,
+                           tail_blocks=max(0, args.tail_blocks))
     eng = E.Engine(store, arena, E.HyperParams(lr=1e-4), opts)
     setup_s = time.time() - t0
     batches = [E.make_copy_task_batch(cfg, 1235, skip=i) for i in range(args.warmup + args.steps)]
@@ -205,6 +206,7 @@ def run_ours(args, m, name):
         r = eng.train_step(batches[args.warmup + i])
         losses.append(r.loss)
         gpu_ms.append(r.gpu_ms)
+    eng.sync()   # the last step's optimizer tail is inside the timed region
     lib.hlm_timer_record(1)
     wall = time.perf_counter() - wall0
     launches = (lib.hlm_cuda_launch_count() - launches0) // max(1, args.steps)
@@ -307,7 +309,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--slabs", type=int, default=3)
+    ap.add_argument("--slabs", type=int, default=5)
+    ap.add_argument("--tail-blocks", type=int, default=2,
+                    help="blocks optimised after the embedding, overlapping the next forward (-1: off)")
     ap.add_argument("--cache-gb", type=float, default=60.0,
                     help="HBM weight cache (block tiles resident between forward and backward)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

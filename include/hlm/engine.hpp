@@ -43,6 +43,12 @@ struct EngineOptions {
     bool fused_recompute = true;   // K == 1: recompute + backward share one weight H2D
     bool record_trace = true;      // CUDA-event timestamps per op
     int block_flags = 0;           // HLM_BLOCK_* (e.g. force the generic attention)
+    // Cross-step overlap (eager + threaded only): the head and the top `tail_blocks`
+    // blocks are optimised after the embedding (the order the next forward needs
+    // them), train_step returns once every other tile is updated, and the next
+    // step's H2D of each tile waits for that tile's update. Numerics unchanged.
+    bool overlap_optimizer_tail = false;
+    i64 tail_blocks = 2;
 };
 
 struct StepResult {
@@ -66,6 +72,9 @@ public:
     Engine& operator=(const Engine&) = delete;
 
     StepResult train_step(const Batch& batch);
+    // Waits until every pending host optimizer update has been applied (the
+    // store is consistent); a no-op unless overlap_optimizer_tail is on.
+    void sync();
 
     void begin_step(const Batch& batch);
     void forward_streaming();
@@ -89,6 +98,7 @@ private:
         i64 slab;
         i64 layer;
         i64 grad_op;
+        i64 step = 0;
     };
     struct HostOpRecord {   // host-side Accum / OptStep, appended to the trace in finish_step
         i64 slab, layer, grad_op;
@@ -111,6 +121,8 @@ private:
     void process_oldest_inline();
     void worker_loop();
     void drain();
+    bool eligible(const Pending& p) const;   // mu_ held
+    void wait_tile_current(i64 tile_id);
     i64 op_begin(StreamOp op, void* stream);
     void op_end(i64 id, void* stream);
     void rethrow_worker_error();
@@ -154,6 +166,10 @@ private:
     std::vector<i64> cache_slot_of_;       // per logical tile, -1 when not cached
     std::vector<i64> cache_xfer_op_;       // per slot: this step's WeightXfer op, -1 if not resident
     std::vector<void*> ev_cache_ready_;
+    std::vector<char> deferred_;           // per logical tile: optimised in the tail
+    std::vector<i64> target_version_;      // per physical tile: version the next H2D needs
+    bool tail_open_ = true;                // embed of the current step processed (mu_)
+    i64 step_index_ = 0;
 
     // worker
     std::mutex mu_;

@@ -191,6 +191,8 @@ typedef struct HlmEngineOptions {
   int32_t fused_recompute;
   int32_t record_trace;
   int32_t block_flags;
+  int32_t overlap_optimizer_tail; /* head + top tail_blocks optimised while the next step starts */
+  int32_t tail_blocks;
 } HlmEngineOptions;
 
 typedef struct HlmStepResult {
@@ -235,6 +237,8 @@ int hlm_engine_create(HlmStore* s, HlmArena* a, const HlmHyper* hp, const HlmEng
                       HlmEngine** out);
 void hlm_engine_destroy(HlmEngine* e);
 int hlm_engine_train_step(HlmEngine* e, const int32_t* tokens, const int32_t* targets, HlmStepResult* out);
+/* wait for every pending host optimizer update (store consistent afterwards) */
+int hlm_engine_sync(HlmEngine* e);
 /* phase API (reference engine.hpp:62-66); out-of-order calls -> HLM_ERR_PROTOCOL */
 int hlm_engine_begin_step(HlmEngine* e, const int32_t* tokens, const int32_t* targets);
 int hlm_engine_forward(HlmEngine* e);

@@ -97,6 +97,8 @@ hlm::EngineOptions to_opts(const HlmEngineOptions* o) {
         e.fused_recompute = o->fused_recompute != 0;
         e.record_trace = o->record_trace != 0;
         e.block_flags = o->block_flags;
+        e.overlap_optimizer_tail = o->overlap_optimizer_tail != 0;
+        e.tail_blocks = o->tail_blocks;
     }
     return e;
 }
@@ -244,6 +246,10 @@ int hlm_engine_train_step(HlmEngine* e, const int32_t* tokens, const int32_t* ta
         e->last_trace = hlm::trace_to_jsonl(r.trace);
         fill_result(r, *e->e, out);
     });
+}
+
+int hlm_engine_sync(HlmEngine* e) {
+    return guarded([&] { e->e->sync(); });
 }
 
 int hlm_engine_begin_step(HlmEngine* e, const int32_t* tokens, const int32_t* targets) {

@@ -81,13 +81,28 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
         ev_cache_ready_.push_back(new_event(false));
     }
     cache_xfer_op_.assign(static_cast<size_t>(slots), -1);
+    if (!(opts_.threaded_accum && opts_.eager_optim && !opts_.skip_optimizer)) opts_.overlap_optimizer_tail = false;
+    deferred_.assign(static_cast<size_t>(m.tile_count()), 0);
+    if (opts_.overlap_optimizer_tail) {
+        // a tied head shares the embedding's tile (two consumers): nothing to defer
+        if (!m.tie_embeddings) deferred_[static_cast<size_t>(m.head_tile_id())] = 1;
+        for (i64 l = std::max<i64>(1, m.layers - opts_.tail_blocks + 1); l <= m.layers; ++l)
+            deferred_[static_cast<size_t>(l)] = 1;
+    }
+    for (i64 p = 0; p < store_.physical_tiles(); ++p)
+        target_version_.push_back(store_.physical(p).version.load(std::memory_order_acquire));
     if (opts_.threaded_accum) worker_ = std::thread([this] { worker_loop(); });
 }
 
 Engine::~Engine() {
+    try {
+        sync();
+    } catch (...) {
+    }
     {
         std::lock_guard<std::mutex> lk(mu_);
         stop_ = true;
+        tail_open_ = true;
     }
     cv_.notify_all();
     if (worker_.joinable()) worker_.join();
@@ -143,8 +158,22 @@ void* Engine::weights_ptr(int buf) const {
     return buf >= 2 ? arena_.cache_slot(buf - 2) : arena_.buffer(buf);
 }
 
+void Engine::wait_tile_current(i64 tile_id) {
+    if (!opts_.overlap_optimizer_tail) return;
+    const i64 p = store_.physical_index(tile_id);
+    const LayerTile& tile = store_.physical(p);
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] {
+        return tile.version.load(std::memory_order_acquire) >= target_version_[static_cast<size_t>(p)] ||
+               worker_error_ != nullptr;
+    });
+    lk.unlock();
+    rethrow_worker_error();
+}
+
 int Engine::stream_tile(i64 tile_id, i64* op_id, bool forward_pass) {
     const i64 slot = cache_slot_of_[static_cast<size_t>(tile_id)];
+    if (!(slot >= 0 && cache_xfer_op_[static_cast<size_t>(slot)] >= 0)) wait_tile_current(tile_id);
     if (slot >= 0) {
         if (cache_xfer_op_[static_cast<size_t>(slot)] >= 0) {   // resident since this step's forward
             *op_id = cache_xfer_op_[static_cast<size_t>(slot)];
@@ -250,7 +279,7 @@ void Engine::evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op) {
     ck(cudaEventRecord(E(ev_gradbuf_free_[gbuf]), S(d2h_)), "record grad buf free");
     {
         std::lock_guard<std::mutex> lk(mu_);
-        pending_.push_back({slab, tile_id, id});
+        pending_.push_back({slab, tile_id, id, step_index_});
     }
     cv_.notify_all();
 }
@@ -294,6 +323,11 @@ void Engine::consume(const Pending& p) {
     pool_->release(p.slab);
     std::lock_guard<std::mutex> lk(mu_);
     host_ops_.push_back(rec);
+    if (p.layer == store_.config().embed_tile_id() && p.step == step_index_) tail_open_ = true;
+}
+
+bool Engine::eligible(const Pending& p) const {
+    return !deferred_[static_cast<size_t>(p.layer)] || tail_open_ || p.step < step_index_ || stop_;
 }
 
 void Engine::process_oldest_inline() {
@@ -312,10 +346,21 @@ void Engine::worker_loop() {
         Pending p;
         {
             std::unique_lock<std::mutex> lk(mu_);
-            cv_.wait(lk, [&] { return stop_ || !pending_.empty(); });
-            if (pending_.empty()) return;
-            p = pending_.front();
-            pending_.pop_front();
+            auto pick = [&]() -> bool {
+                for (auto it = pending_.begin(); it != pending_.end(); ++it)
+                    if (eligible(*it)) {
+                        p = *it;
+                        pending_.erase(it);
+                        return true;
+                    }
+                return false;
+            };
+            bool got = false;
+            cv_.wait(lk, [&] {
+                got = pick();
+                return got || (stop_ && pending_.empty());
+            });
+            if (!got) return;
             ++in_process_;
         }
         try {
@@ -347,8 +392,22 @@ void Engine::rethrow_worker_error() {
     if (e) std::rethrow_exception(e);
 }
 
+void Engine::sync() {
+    if (!opts_.threaded_accum) return;
+    {
+        std::unique_lock<std::mutex> lk(mu_);
+        tail_open_ = true;
+        cv_.notify_all();
+        cv_.wait(lk, [&] { return pending_.empty() && in_process_ == 0; });
+    }
+    rethrow_worker_error();
+}
+
 void Engine::drain() {
-    if (opts_.threaded_accum) {
+    if (opts_.threaded_accum && opts_.overlap_optimizer_tail) {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return tail_open_ || worker_error_ != nullptr; });
+    } else if (opts_.threaded_accum) {
         std::unique_lock<std::mutex> lk(mu_);
         cv_.wait(lk, [&] { return pending_.empty() && in_process_ == 0; });
     } else {
@@ -382,9 +441,12 @@ void Engine::begin_step(const Batch& batch) {
     g_cur_ = 0;
     last_reader_[0] = last_reader_[1] = -1;
     last_accum_op_.assign(static_cast<size_t>(pool_->size()), -1);
+    rethrow_worker_error();
     {
         std::lock_guard<std::mutex> lk(mu_);
-        pending_.clear();
+        ++step_index_;
+        tail_open_ = !opts_.overlap_optimizer_tail;
+        if (!opts_.overlap_optimizer_tail) pending_.clear();
         host_ops_.clear();
         consumers_left_.assign(static_cast<size_t>(store_.physical_tiles()), 0);
         for (i64 p = 0; p < store_.physical_tiles(); ++p)
@@ -720,6 +782,8 @@ StepResult Engine::finish_step() {
         trace_.add(op);
     }
     if (!opts_.skip_optimizer) store_.set_adam_steps(step_t_);
+    if (opts_.overlap_optimizer_tail)
+        for (auto& tv : target_version_) ++tv;
 
     // resolve GPU timestamps
     float ms = 0.f;

@@ -337,6 +337,7 @@ void SlabPool::mark_in_flight(i64 id, i64 layer_id, i64 bytes) {
     if (bytes > capacity_) throw ProtocolError("slab payload exceeds slab capacity");
     s.layer_id = layer_id;
     s.bytes = bytes;
+    d2h_bytes_ += bytes;   // counted when the copy is issued
 }
 
 void SlabPool::mark_ready(i64 id) {
@@ -345,7 +346,6 @@ void SlabPool::mark_ready(i64 id) {
     if (s.state != SlabState::IN_FLIGHT) throw ProtocolError(std::string("slab ready in state ") + slab_state_name(s.state));
     s.state = SlabState::READY;
     ready_.push_back(id);
-    d2h_bytes_ += s.bytes;
     cv_.notify_all();
 }
 

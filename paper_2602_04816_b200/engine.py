@@ -88,12 +88,15 @@ class EngineOptions(ctypes.Structure):
     _fields_ = [("eager_optim", ctypes.c_int32), ("threaded_accum", ctypes.c_int32),
                 ("n_slab", ctypes.c_int64), ("accum_delay_us", ctypes.c_int64),
                 ("skip_optimizer", ctypes.c_int32), ("fused_recompute", ctypes.c_int32),
-                ("record_trace", ctypes.c_int32), ("block_flags", ctypes.c_int32)]
+                ("record_trace", ctypes.c_int32), ("block_flags", ctypes.c_int32),
+                ("overlap_optimizer_tail", ctypes.c_int32), ("tail_blocks", ctypes.c_int32)]
 
     def __init__(self, eager_optim=False, threaded_accum=False, n_slab=12, accum_delay_us=0,
-                 skip_optimizer=False, fused_recompute=True, record_trace=True, block_flags=0):
+                 skip_optimizer=False, fused_recompute=True, record_trace=True, block_flags=0,
+                 overlap_optimizer_tail=False, tail_blocks=2):
         super().__init__(int(eager_optim), int(threaded_accum), n_slab, accum_delay_us,
-                         int(skip_optimizer), int(fused_recompute), int(record_trace), block_flags)
+                         int(skip_optimizer), int(fused_recompute), int(record_trace), block_flags,
+                         int(overlap_optimizer_tail), tail_blocks)
 
 
 class StepResult(ctypes.Structure):
@@ -132,6 +135,7 @@ def _L():
         L.hlm_engine_create.argtypes = [_vp, _vp, P(HyperParams), P(EngineOptions), P(_vp)]
         L.hlm_engine_destroy.argtypes = [_vp]
         L.hlm_engine_train_step.argtypes = [_vp, _i32p, _i32p, P(StepResult)]
+        L.hlm_engine_sync.argtypes = [_vp]
         L.hlm_engine_begin_step.argtypes = [_vp, _i32p, _i32p]
         L.hlm_engine_forward.argtypes = [_vp]
         L.hlm_engine_anchor_loss.argtypes = [_vp, P(ctypes.c_double)]
@@ -241,6 +245,9 @@ class Engine:
         _check(_L().hlm_engine_train_step(self.h, self._arr(tokens), self._arr(targets),
                                           ctypes.byref(r)))
         return r
+
+    def sync(self):
+        _check(_L().hlm_engine_sync(self.h))
 
     def begin_step(self, tokens, targets=None):
         targets = tokens if targets is None else targets

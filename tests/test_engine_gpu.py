@@ -230,3 +230,19 @@ def test_weight_cache_is_bitwise_neutral_and_halves_h2d():
         xfer_layers = [o["layer"] for o in ops if o["kind"] == "WeightXfer"]
         for l in range(c.layers - cache_layers + 1, c.layers + 1):
             assert xfer_layers.count(l) == 1
+
+
+def test_optimizer_tail_overlap_is_bitwise_neutral():
+    c = E.ModelConfig(6, 32, 64, 32, 16, 2, k_ckpt=1)
+    tok = [E.make_copy_task_batch(c, 9, skip=i) for i in range(4)]
+    ref = E.Store(c, 3)
+    e0 = E.Engine(ref, E.Arena(c), E.HyperParams(lr=2e-3), E.EngineOptions(eager_optim=True))
+    l0 = [e0.train_step(t).loss for t in tok]
+    s = E.Store(c, 3)
+    e = E.Engine(s, E.Arena(c), E.HyperParams(lr=2e-3),
+                 E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=5,
+                                 overlap_optimizer_tail=True, tail_blocks=3, accum_delay_us=300))
+    l1 = [e.train_step(t).loss for t in tok]
+    e.sync()
+    assert l0 == l1
+    assert ref.bitwise_equal(s)
