@@ -98,7 +98,8 @@ private:
         i64 slab;
         i64 layer;
         i64 grad_op;
-        i64 step = 0;
+        i64 step = 0;   // engine step index (tail eligibility)
+        i64 t = 0;      // Adam step index of the gradient (bias correction)
     };
     struct HostOpRecord {   // host-side Accum / OptStep, appended to the trace in finish_step
         i64 slab, layer, grad_op;

@@ -83,6 +83,9 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
     cache_xfer_op_.assign(static_cast<size_t>(slots), -1);
     if (!(opts_.threaded_accum && opts_.eager_optim && !opts_.skip_optimizer)) opts_.overlap_optimizer_tail = false;
     deferred_.assign(static_cast<size_t>(m.tile_count()), 0);
+    // deferred tiles hold their slabs until the tail opens: keep two slabs for the rest
+    if (opts_.overlap_optimizer_tail) opts_.tail_blocks = std::min(opts_.tail_blocks, pool_->size() - 3);
+    if (opts_.overlap_optimizer_tail && opts_.tail_blocks < 0) opts_.overlap_optimizer_tail = false;
     if (opts_.overlap_optimizer_tail) {
         // a tied head shares the embedding's tile (two consumers): nothing to defer
         if (!m.tie_embeddings) deferred_[static_cast<size_t>(m.head_tile_id())] = 1;
@@ -253,6 +256,13 @@ void Engine::evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op) {
     while (slab < 0) {
         if (opts_.threaded_accum) {
             rethrow_worker_error();
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                bool any = in_process_ > 0;
+                for (const auto& q : pending_) any = any || eligible(q);
+                if (!any && !pending_.empty()) tail_open_ = true;   // never wedge on deferred slabs
+            }
+            cv_.notify_all();
             slab = pool_->acquire_blocking();
         } else {
             process_oldest_inline();
@@ -279,7 +289,7 @@ void Engine::evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op) {
     ck(cudaEventRecord(E(ev_gradbuf_free_[gbuf]), S(d2h_)), "record grad buf free");
     {
         std::lock_guard<std::mutex> lk(mu_);
-        pending_.push_back({slab, tile_id, id, step_index_});
+        pending_.push_back({slab, tile_id, id, step_index_, step_t_});
     }
     cv_.notify_all();
 }
@@ -303,7 +313,7 @@ void Engine::consume(const Pending& p) {
         rec.t1 = now_us();
         rec.opt = true;
         rec.topt0 = rec.t1;
-        adam_step_tile_from(tile, pool_->data(p.slab), hyper_, step_t_);
+        adam_step_tile_from(tile, pool_->data(p.slab), hyper_, p.t);
         rec.topt1 = now_us();
     } else {
         accumulate_grads(tile, pool_->data(p.slab));
@@ -316,7 +326,7 @@ void Engine::consume(const Pending& p) {
         if (optimise && last) {
             rec.opt = true;
             rec.topt0 = now_us();
-            adam_step_tile(store_, phys, hyper_, step_t_);
+            adam_step_tile(store_, phys, hyper_, p.t);
             rec.topt1 = now_us();
         }
     }
@@ -744,7 +754,12 @@ StepResult Engine::finish_step() {
 
     // host ops into the trace, in consumption order
     std::vector<i64> accum_ids;
-    for (const auto& rec : host_ops_) {
+    std::vector<HostOpRecord> recs;
+    {
+        std::lock_guard<std::mutex> lk(mu_);
+        recs = host_ops_;
+    }
+    for (const auto& rec : recs) {
         StreamOp op;
         op.stream = StreamId::Host;
         op.kind = OpKind::Accum;
