@@ -194,6 +194,10 @@ def run_ours(args, m, name):
     for i in range(args.warmup):
         eng.train_step(batches[i])
     trace = eng.last_trace()
+    if args.dump_trace:
+        with open(args.dump_trace, "w") as f:
+            for op in trace:
+                f.write(json.dumps(op) + "\n")
     if world > 1:
         dist.barrier()
     clocks = ClockSampler()
@@ -315,6 +319,7 @@ def main():
     ap.add_argument("--cache-gb", type=float, default=60.0,
                     help="HBM weight cache (block tiles resident between forward and backward)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dump-trace", default="", help="write the last warm-up step's measured trace (JSONL)")
     args = ap.parse_args()
     m = dict(CONFIGS[args.config])
     if args.impl == "reference":
