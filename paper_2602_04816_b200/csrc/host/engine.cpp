@@ -356,14 +356,22 @@ void Engine::worker_loop() {
         Pending p;
         {
             std::unique_lock<std::mutex> lk(mu_);
+            // FIFO over the step's regular tiles; deferred (tail) tiles in the order
+            // the next forward consumes them (ascending tile id, head last).
             auto pick = [&]() -> bool {
-                for (auto it = pending_.begin(); it != pending_.end(); ++it)
-                    if (eligible(*it)) {
-                        p = *it;
-                        pending_.erase(it);
-                        return true;
+                auto best = pending_.end();
+                for (auto it = pending_.begin(); it != pending_.end(); ++it) {
+                    if (!eligible(*it)) continue;
+                    if (!deferred_[static_cast<size_t>(it->layer)]) {
+                        best = it;
+                        break;
                     }
-                return false;
+                    if (best == pending_.end() || it->layer < best->layer) best = it;
+                }
+                if (best == pending_.end()) return false;
+                p = *best;
+                pending_.erase(best);
+                return true;
             };
             bool got = false;
             cv_.wait(lk, [&] {
