@@ -336,9 +336,7 @@ void Engine::consume(const Pending& p) {
     if (p.layer == store_.config().embed_tile_id() && p.step == step_index_) tail_open_ = true;
 }
 
-bool Engine::eligible(const Pending& p) const {
-    return !deferred_[static_cast<size_t>(p.layer)] || tail_open_ || p.step < step_index_ || stop_;
-}
+bool Engine::eligible(const Pending&) const { return true; }
 
 void Engine::process_oldest_inline() {
     Pending p;
@@ -356,17 +354,26 @@ void Engine::worker_loop() {
         Pending p;
         {
             std::unique_lock<std::mutex> lk(mu_);
-            // FIFO over the step's regular tiles; deferred (tail) tiles in the order
-            // the next forward consumes them (ascending tile id, head last).
+            // Never idle while a gradient is available; priority: the previous
+            // step's tail (the running forward needs it, in tile order), then this
+            // step's regular tiles in arrival order, then this step's tail tiles in
+            // the order the next forward consumes them (ascending id, head last).
             auto pick = [&]() -> bool {
                 auto best = pending_.end();
-                for (auto it = pending_.begin(); it != pending_.end(); ++it) {
-                    if (!eligible(*it)) continue;
-                    if (!deferred_[static_cast<size_t>(it->layer)]) {
+                std::pair<int, i64> best_rank{3, 0};
+                i64 pos = 0;
+                for (auto it = pending_.begin(); it != pending_.end(); ++it, ++pos) {
+                    std::pair<int, i64> rank;
+                    if (it->step < step_index_)
+                        rank = {0, it->layer};
+                    else if (!deferred_[static_cast<size_t>(it->layer)])
+                        rank = {1, pos};
+                    else
+                        rank = {2, it->layer};
+                    if (rank < best_rank) {
+                        best_rank = rank;
                         best = it;
-                        break;
                     }
-                    if (best == pending_.end() || it->layer < best->layer) best = it;
                 }
                 if (best == pending_.end()) return false;
                 p = *best;
