@@ -313,8 +313,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--slabs", type=int, default=5)
-    ap.add_argument("--tail-blocks", type=int, default=2,
+    ap.add_argument("--slabs", type=int, default=6)
+    ap.add_argument("--tail-blocks", type=int, default=3,
                     help="blocks optimised after the embedding, overlapping the next forward (-1: off)")
     ap.add_argument("--cache-gb", type=float, default=60.0,
                     help="HBM weight cache (block tiles resident between forward and backward)")

@@ -49,6 +49,16 @@ struct EngineOptions {
     // step's H2D of each tile waits for that tile's update. Numerics unchanged.
     bool overlap_optimizer_tail = false;
     i64 tail_blocks = 2;
+    // Data parallel (one process per GPU over a shared host store): this rank
+    // trains on its rows of the global micro-batch (loss scaled by
+    // 1/global_rows); every layer gradient is reduce-scattered (comm_grad, D2H
+    // stream) and only this rank's 1/world shard is copied to the host and
+    // optimised here. With comm_weights, each rank H2Ds 1/world of a layer and
+    // the full layer is all-gathered over NVLink (h2d stream).
+    int rank = 0;
+    int world = 1;
+    void* comm_grad = nullptr;      // ncclComm_t
+    void* comm_weights = nullptr;   // ncclComm_t, optional
 };
 
 struct StepResult {
@@ -167,6 +177,9 @@ private:
     std::vector<i64> cache_slot_of_;       // per logical tile, -1 when not cached
     std::vector<i64> cache_xfer_op_;       // per slot: this step's WeightXfer op, -1 if not resident
     std::vector<void*> ev_cache_ready_;
+    i64 shard_elems(i64 n) const;          // n / world (throws unless divisible)
+    void h2d_tile(void* dst, const LayerTile& tile, i64 bytes);
+    double* loss_dev_ = nullptr;
     std::vector<char> deferred_;           // per logical tile: optimised in the tail
     std::vector<i64> target_version_;      // per physical tile: version the next H2D needs
     bool tail_open_ = true;                // embed of the current step processed (mu_)

@@ -76,10 +76,34 @@ public:
     float load_grad(i64 i) const { return grads_ ? grads_[i] : 0.0f; }
     void store_grad(i64 i, float v) { grads()[i] = v; }
 
-    // Completed optimizer updates of this tile (cross-step H2D gating).
+    // Completed optimizer updates of this tile (cross-step H2D gating). In a
+    // shared (multi-process) store every rank owns one counter per tile in the
+    // shared mapping: bump_version(rank) after updating its shard, and a tile is
+    // current for the next H2D when min_version() reached the target.
     std::atomic<i64> version{0};
+    void attach_shared_versions(std::atomic<i64>* v, int world) {
+        shared_versions_ = v;
+        world_ = world;
+    }
+    void bump_version(int rank) {
+        if (shared_versions_)
+            shared_versions_[rank].fetch_add(1, std::memory_order_acq_rel);
+        else
+            version.fetch_add(1, std::memory_order_acq_rel);
+    }
+    i64 min_version() const {
+        if (!shared_versions_) return version.load(std::memory_order_acquire);
+        i64 v = shared_versions_[0].load(std::memory_order_acquire);
+        for (int r = 1; r < world_; ++r) {
+            const i64 x = shared_versions_[r].load(std::memory_order_acquire);
+            if (x < v) v = x;
+        }
+        return v;
+    }
 
 private:
+    std::atomic<i64>* shared_versions_ = nullptr;
+    int world_ = 1;
     i64 layer_id_;
     i64 n_params_;
     std::vector<NamedRegion> offsets_;
@@ -93,12 +117,23 @@ enum class InitMode : std::uint8_t {
     Parallel = 1     // counter-seeded per 64Ki-element chunk: same distribution, any thread count
 };
 
+// Multi-process (one process per GPU) store: every rank maps the same POSIX
+// shared-memory object (/dev/shm/<name>); rank 0 creates and initialises it,
+// the others attach once it is marked ready. Each process pins the shared BF16
+// shadow for its own DMA (cudaHostRegister).
+struct SharedStoreSpec {
+    std::string name;
+    int rank = 0;
+    int world = 1;
+};
+
 class MasterStore {
 public:
     // Allocates host memory (master/moments: huge-page anonymous mapping;
     // shadow: pinned through the CUDA runtime, or plain memory when
     // pin_shadow is false, e.g. on CPU-only machines).
-    MasterStore(const ModelConfig& config, Dtype dtype, bool pin_shadow = true);
+    MasterStore(const ModelConfig& config, Dtype dtype, bool pin_shadow = true,
+                const SharedStoreSpec* shared = nullptr);
     ~MasterStore();
     MasterStore(const MasterStore&) = delete;
     MasterStore& operator=(const MasterStore&) = delete;
@@ -131,6 +166,13 @@ public:
     // Re-packs the BF16 shadow of every tile from the master (after external edits).
     void repack_shadow();
 
+    bool shared() const { return shm_fd_ >= 0; }
+    int rank() const { return rank_; }
+    int world() const { return world_; }
+    bool owner() const { return rank_ == 0; }
+    void mark_ready();            // rank 0, after initialisation
+    void wait_ready() const;      // other ranks
+
 private:
     ModelConfig config_;
     Dtype dtype_;
@@ -143,13 +185,20 @@ private:
     std::uint16_t* shadow_base_ = nullptr;
     size_t shadow_bytes_ = 0;
     bool pinned_ = false;
+    // shared mapping: [header 2 MiB][state][shadow][versions]
+    int shm_fd_ = -1;
+    std::string shm_name_;
+    void* map_base_ = nullptr;
+    size_t map_bytes_ = 0;
+    int rank_ = 0, world_ = 1;
+    bool registered_ = false;
 };
 
 // Allocates and initialises a store: trunc_normal(0.02) matrices, unit norm
 // scales, zero moments (reference host_store.cpp:141-156).
 std::unique_ptr<MasterStore> build_store(const ModelConfig& config, std::uint64_t seed,
                                          Dtype dtype = Dtype::BF16, InitMode mode = InitMode::Reference,
-                                         bool pin_shadow = true);
+                                         bool pin_shadow = true, const SharedStoreSpec* shared = nullptr);
 
 // ------------------------------------------------------------------ gradient slabs
 enum class SlabState : std::uint8_t { FREE = 0, IN_FLIGHT = 1, READY = 2, ACCUMULATING = 3 };
@@ -210,6 +259,10 @@ private:
 void adam_step(MasterStore& store, const HyperParams& hyper, i64 t);
 void adam_step_tile(MasterStore& store, i64 physical_idx, const HyperParams& hyper, i64 t);
 void adam_step_tile_from(LayerTile& tile, const float* grad, const HyperParams& hyper, i64 t);
+// Shard version (data parallel): elements [begin, begin + count) of the tile,
+// grad points at the shard's first element. Does not bump the version.
+void adam_step_range(LayerTile& tile, const float* grad, i64 begin, i64 count, const HyperParams& hyper,
+                     i64 t);
 
 // grads(tile) += g  (slab accumulation, host_store.cpp:254-284, FP32).
 void accumulate_grads(LayerTile& tile, const float* g);

@@ -193,6 +193,13 @@ typedef struct HlmEngineOptions {
   int32_t block_flags;
   int32_t overlap_optimizer_tail; /* head + top tail_blocks optimised while the next step starts */
   int32_t tail_blocks;
+  /* data parallel: this process is `rank` of `world`; per-layer fp32 gradient
+   * reduce-scatter on comm_grad; sharded weight H2D + all-gather on comm_weights
+   * (may be NULL: full H2D per rank). Communicators from hlm_nccl_comm_create. */
+  int32_t rank;
+  int32_t world;
+  void* comm_grad;
+  void* comm_weights;
 } HlmEngineOptions;
 
 typedef struct HlmStepResult {
@@ -220,6 +227,15 @@ int64_t hlm_store_adam_steps(const HlmStore* s);
 int hlm_store_export(const HlmStore* s, int field, float* out);
 int hlm_store_import_master(HlmStore* s, const float* w);   /* master := w, shadow re-packed */
 int hlm_store_bitwise_equal(const HlmStore* a, const HlmStore* b);
+/* Shared host store for one-process-per-GPU data parallelism: rank 0 creates
+ * /dev/shm/<name> and initialises it, the other ranks attach. */
+int hlm_store_create_shared(const HlmModelConfig* cfg, uint64_t seed, int dtype, int init_mode, int pin_shadow,
+                            const char* name, int rank, int world, HlmStore** out);
+/* Data-parallel host Adam: this rank updates its 1/world shard of every tile
+ * from full-size gradients (store layout) and bumps its version counters. */
+int hlm_store_adam_shard(HlmStore* s, const float* grads, const HlmHyper* hp, int64_t t, int rank, int world);
+/* min over ranks of the completed-update counter of physical tile p */
+int64_t hlm_store_tile_version(const HlmStore* s, int64_t p);
 /* Host Adam on every physical tile from caller gradients (store layout),
  * step index t (reference adam_update_tile, host_store.cpp:334-362). */
 int hlm_store_adam_step(HlmStore* s, const float* grads, const HlmHyper* hp, int64_t t);
@@ -248,6 +264,11 @@ int hlm_engine_finish_step(HlmEngine* e, HlmStepResult* out);
 int hlm_engine_debug_hidden(HlmEngine* e, float* out);
 /* JSONL of the last step's measured trace; *needed = bytes incl. NUL */
 int hlm_engine_last_trace(HlmEngine* e, char* buf, size_t cap, size_t* needed);
+
+/* NCCL (loaded at run time): 128-byte unique id, communicator create / destroy */
+int hlm_nccl_unique_id(uint8_t* out128);
+int hlm_nccl_comm_create(const uint8_t* id128, int world, int rank, void** comm);
+void hlm_nccl_comm_destroy(void* comm);
 
 int hlm_make_copy_task_batch(const HlmModelConfig* cfg, uint64_t data_seed, int64_t skip, int32_t* tokens);
 /* run_training (trainer.hpp): store from seed, data seed+1, `steps` steps */

@@ -11,6 +11,9 @@
 #include "hlm/engine.hpp"
 #include "hlm/trainer.hpp"
 #include "hlm_cuda.h"
+#include "../host/nccl_dyn.h"
+
+#include <algorithm>
 
 struct HlmStore {
     std::unique_ptr<hlm::MasterStore> s;
@@ -99,6 +102,10 @@ hlm::EngineOptions to_opts(const HlmEngineOptions* o) {
         e.block_flags = o->block_flags;
         e.overlap_optimizer_tail = o->overlap_optimizer_tail != 0;
         e.tail_blocks = o->tail_blocks;
+        e.rank = o->rank;
+        e.world = o->world > 0 ? o->world : 1;
+        e.comm_grad = o->comm_grad;
+        e.comm_weights = o->comm_weights;
     }
     return e;
 }
@@ -136,6 +143,59 @@ int hlm_store_create(const HlmModelConfig* cfg, uint64_t seed, int dtype, int in
                                  init_mode == 1 ? hlm::InitMode::Parallel : hlm::InitMode::Reference, pin_shadow != 0);
         *out = st.release();
     });
+}
+
+int hlm_store_create_shared(const HlmModelConfig* cfg, uint64_t seed, int dtype, int init_mode, int pin_shadow,
+                            const char* name, int rank, int world, HlmStore** out) {
+    return guarded([&] {
+        if (!name || !*name) throw std::invalid_argument("shared store needs a name");
+        hlm::SharedStoreSpec spec{name, rank, world};
+        auto st = std::make_unique<HlmStore>();
+        st->s = hlm::build_store(to_model(cfg), seed, dtype == 1 ? hlm::Dtype::FP32 : hlm::Dtype::BF16,
+                                 init_mode == 1 ? hlm::InitMode::Parallel : hlm::InitMode::Reference, pin_shadow != 0,
+                                 &spec);
+        *out = st.release();
+    });
+}
+
+int hlm_store_adam_shard(HlmStore* s, const float* grads, const HlmHyper* hp, int64_t t, int rank, int world) {
+    return guarded([&] {
+        hlm::MasterStore& st = *s->s;
+        const hlm::HyperParams h = to_hyper(hp);
+        for (hlm::i64 p = 0; p < st.physical_tiles(); ++p) {
+            hlm::LayerTile& tile = st.physical(p);
+            if (tile.n_params() % world) throw std::invalid_argument("tile not divisible by world");
+            const hlm::i64 cnt = tile.n_params() / world, begin = rank * cnt;
+            hlm::adam_step_range(tile, grads + begin, begin, cnt, h, t);
+            tile.bump_version(rank);
+            grads += tile.n_params();
+        }
+        st.set_adam_steps(t);
+    });
+}
+
+int64_t hlm_store_tile_version(const HlmStore* s, int64_t p) { return s->s->physical(p).min_version(); }
+
+int hlm_nccl_unique_id(uint8_t* out128) {
+    return guarded([&] {
+        ncclUniqueId id;
+        hlm::nccl_check(hlm::nccl().GetUniqueId(&id), "ncclGetUniqueId");
+        std::memcpy(out128, id.internal, NCCL_UNIQUE_ID_BYTES);
+    });
+}
+
+int hlm_nccl_comm_create(const uint8_t* id128, int world, int rank, void** comm) {
+    return guarded([&] {
+        ncclUniqueId id;
+        std::memcpy(id.internal, id128, NCCL_UNIQUE_ID_BYTES);
+        ncclComm_t c;
+        hlm::nccl_check(hlm::nccl().CommInitRank(&c, world, id, rank), "ncclCommInitRank");
+        *comm = c;
+    });
+}
+
+void hlm_nccl_comm_destroy(void* comm) {
+    if (comm) hlm::nccl().CommDestroy(static_cast<ncclComm_t>(comm));
 }
 
 void hlm_store_destroy(HlmStore* s) { delete s; }

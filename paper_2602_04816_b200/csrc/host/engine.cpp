@@ -14,6 +14,7 @@
 
 #include "hlm/flop_model.hpp"
 #include "hlm_cuda.h"
+#include "nccl_dyn.h"
 
 namespace hlm {
 
@@ -46,7 +47,15 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
         m.batch != a.batch || m.k_ckpt != a.k_ckpt || m.n_heads != a.n_heads)
         throw ConfigError("engine: store and arena configs differ");
     ck(cudaSetDevice(arena_.device()), "cudaSetDevice");
-    pool_ = std::make_unique<SlabPool>(opts_.n_slab, grad_buf_bytes(m), true);
+    if (opts_.world < 1 || opts_.rank < 0 || opts_.rank >= opts_.world) throw ConfigError("engine: bad rank/world");
+    if (opts_.world > 1 && !opts_.comm_grad) throw ConfigError("engine: world > 1 needs a gradient communicator");
+    if (opts_.comm_grad) {
+        if (store_.shared() && store_.world() != opts_.world) throw ConfigError("engine: store world mismatch");
+        (void)nccl();
+        ck(cudaMalloc(&loss_dev_, sizeof(double)), "cudaMalloc loss");
+    }
+    // data parallel: slabs hold a 1/world gradient shard
+    pool_ = std::make_unique<SlabPool>(opts_.n_slab, (grad_buf_bytes(m) / opts_.world + 255) / 256 * 256, true);
     cudaStream_t s;
     ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
     h2d_ = s;
@@ -93,7 +102,7 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
             deferred_[static_cast<size_t>(l)] = 1;
     }
     for (i64 p = 0; p < store_.physical_tiles(); ++p)
-        target_version_.push_back(store_.physical(p).version.load(std::memory_order_acquire));
+        target_version_.push_back(store_.physical(p).min_version());
     if (opts_.threaded_accum) worker_ = std::thread([this] { worker_loop(); });
 }
 
@@ -127,6 +136,30 @@ Engine::~Engine() {
     cudaStreamDestroy(S(compute_));
     cudaStreamDestroy(S(d2h_));
     if (loss_host_) cudaFreeHost(loss_host_);
+    if (loss_dev_) cudaFree(loss_dev_);
+}
+
+i64 Engine::shard_elems(i64 n) const {
+    if (n % opts_.world) throw ConfigError("data parallel: tile size not divisible by world size");
+    return n / opts_.world;
+}
+
+// H2D of a tile's bf16 shadow: full copy, or this rank's shard + NVLink all-gather.
+void Engine::h2d_tile(void* dst, const LayerTile& tile, i64 bytes) {
+    if (opts_.comm_weights && tile.n_params() % opts_.world == 0) {
+        const i64 cnt = tile.n_params() / opts_.world;
+        const i64 off = opts_.rank * cnt;
+        uint16_t* d = static_cast<uint16_t*>(dst);
+        ck(cudaMemcpyAsync(d + off, tile.shadow() + off, static_cast<size_t>(cnt) * 2, cudaMemcpyHostToDevice, S(h2d_)),
+           "H2D weight shard");
+        nccl_check(nccl().AllGather(d + off, d, static_cast<size_t>(cnt), ncclBfloat16,
+                                    static_cast<ncclComm_t>(opts_.comm_weights), S(h2d_)),
+                   "all-gather weights");
+        arena_.add_h2d(cnt * 2);
+        return;
+    }
+    ck(cudaMemcpyAsync(dst, tile.shadow(), static_cast<size_t>(bytes), cudaMemcpyHostToDevice, S(h2d_)), "H2D weights");
+    arena_.add_h2d(bytes);
 }
 
 // ------------------------------------------------------------------ trace helpers
@@ -167,7 +200,7 @@ void Engine::wait_tile_current(i64 tile_id) {
     const LayerTile& tile = store_.physical(p);
     std::unique_lock<std::mutex> lk(mu_);
     cv_.wait(lk, [&] {
-        return tile.version.load(std::memory_order_acquire) >= target_version_[static_cast<size_t>(p)] ||
+        return tile.min_version() >= target_version_[static_cast<size_t>(p)] ||
                worker_error_ != nullptr;
     });
     lk.unlock();
@@ -194,12 +227,9 @@ int Engine::stream_tile(i64 tile_id, i64* op_id, bool forward_pass) {
             op.bytes = bytes;
             op.pinned = store_.shadow_pinned();
             const i64 id = op_begin(std::move(op), h2d_);
-            ck(cudaMemcpyAsync(arena_.cache_slot(slot), tile.shadow(), static_cast<size_t>(bytes),
-                               cudaMemcpyHostToDevice, S(h2d_)),
-               "H2D weights (cache)");
+            h2d_tile(arena_.cache_slot(slot), tile, bytes);
             op_end(id, h2d_);
             ck(cudaEventRecord(E(ev_cache_ready_[static_cast<size_t>(slot)]), S(h2d_)), "record cache ready");
-            arena_.add_h2d(bytes);
             cache_xfer_op_[static_cast<size_t>(slot)] = id;
             *op_id = id;
             return 2 + static_cast<int>(slot);
@@ -221,11 +251,9 @@ int Engine::stream_tile(i64 tile_id, i64* op_id, bool forward_pass) {
     if (last_reader_[buf] >= 0) op.deps.push_back(last_reader_[buf]);
     ck(cudaStreamWaitEvent(S(h2d_), E(ev_buf_free_[buf]), 0), "wait buf free");
     const i64 id = op_begin(std::move(op), h2d_);
-    ck(cudaMemcpyAsync(dst, tile.shadow(), static_cast<size_t>(bytes), cudaMemcpyHostToDevice, S(h2d_)),
-       "H2D weights");
+    h2d_tile(dst, tile, bytes);
     op_end(id, h2d_);
     ck(cudaEventRecord(E(ev_w_ready_[buf]), S(h2d_)), "record w ready");
-    arena_.add_h2d(bytes);
     *op_id = id;
     return buf;
 }
@@ -269,7 +297,8 @@ void Engine::evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op) {
             slab = pool_->try_acquire();
         }
     }
-    const i64 bytes = 4 * n_params;
+    const i64 cnt = opts_.comm_grad ? shard_elems(n_params) : n_params;
+    const i64 bytes = 4 * cnt;
     pool_->mark_in_flight(slab, tile_id, bytes);
     StreamOp op;
     op.stream = StreamId::D2H;
@@ -281,8 +310,14 @@ void Engine::evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op) {
     if (last_accum_op_[static_cast<size_t>(slab)] >= 0) op.deps.push_back(last_accum_op_[static_cast<size_t>(slab)]);
     ck(cudaStreamWaitEvent(S(d2h_), E(ev_grad_ready_[gbuf]), 0), "wait grad ready");
     const i64 id = op_begin(std::move(op), d2h_);
-    ck(cudaMemcpyAsync(pool_->data(slab), arena_.grad_out(gbuf), static_cast<size_t>(bytes), cudaMemcpyDeviceToHost,
-                       S(d2h_)),
+    float* src = arena_.grad_out(gbuf);
+    if (opts_.comm_grad) {   // in-place reduce-scatter over NVLink, then D2H of this rank's shard
+        src += opts_.rank * cnt;
+        nccl_check(nccl().ReduceScatter(arena_.grad_out(gbuf), src, static_cast<size_t>(cnt), ncclFloat32, ncclSum,
+                                        static_cast<ncclComm_t>(opts_.comm_grad), S(d2h_)),
+                   "reduce-scatter grads");
+    }
+    ck(cudaMemcpyAsync(pool_->data(slab), src, static_cast<size_t>(bytes), cudaMemcpyDeviceToHost, S(d2h_)),
        "D2H grads");
     op_end(id, d2h_);
     ck(cudaEventRecord(E(ev_slab_done_[static_cast<size_t>(slab)]), S(d2h_)), "record slab done");
@@ -308,7 +343,35 @@ void Engine::consume(const Pending& p) {
     LayerTile& tile = store_.tile(p.layer);
     const i64 phys = store_.physical_index(p.layer);
     const bool optimise = opts_.eager_optim && !opts_.skip_optimizer;
-    if (optimise && store_.consumer_count(phys) == 1) {
+    if (opts_.comm_grad) {   // this rank's shard [begin, begin + cnt)
+        const i64 cnt = shard_elems(tile.n_params()), begin = opts_.rank * cnt;
+        const float* g = pool_->data(p.slab);
+        if (optimise && store_.consumer_count(phys) == 1) {
+            rec.t1 = now_us();
+            rec.opt = true;
+            rec.topt0 = rec.t1;
+            adam_step_range(tile, g, begin, cnt, hyper_, p.t);
+            tile.bump_version(opts_.rank);
+            rec.topt1 = now_us();
+        } else {
+            float* dst = tile.grads() + begin;
+            for (i64 i = 0; i < cnt; ++i) dst[i] = dst[i] + g[i];
+            rec.t1 = now_us();
+            bool last = false;
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                last = --consumers_left_[static_cast<size_t>(phys)] == 0;
+            }
+            if (optimise && last) {
+                rec.opt = true;
+                rec.topt0 = now_us();
+                adam_step_range(tile, dst, begin, cnt, hyper_, p.t);
+                std::fill(dst, dst + cnt, 0.0f);
+                tile.bump_version(opts_.rank);
+                rec.topt1 = now_us();
+            }
+        }
+    } else if (optimise && store_.consumer_count(phys) == 1) {
         // fused: the pinned slab IS the gradient; no store gradient region touched
         rec.t1 = now_us();
         rec.opt = true;
@@ -582,7 +645,7 @@ void Engine::anchor_loss_async() {
     op.deps.push_back(w_op);
     const i64 fid = op_begin(op, compute_);
     ck_hlm(hlm_cuda_head_loss(T, m.hidden, m.vocab, weights_ptr(buf), h_cur_, arena_.targets(),
-                              1.0f / static_cast<float>(T), arena_.g_roll(g_cur_), arena_.grad_out(gb), 0,
+                              1.0f / static_cast<float>(T * opts_.world), arena_.g_roll(g_cur_), arena_.grad_out(gb), 0,
                               arena_.loss_rows(), arena_.head_ws(), compute_),
            "head_loss");
     op_end(fid, compute_);
@@ -766,6 +829,14 @@ StepResult Engine::finish_step() {
     double loss = 0.0;
     const float* lr = reinterpret_cast<const float*>(loss_host_ + 2 * T);
     for (i64 r = 0; r < T; ++r) loss += static_cast<double>(lr[r]);
+    if (opts_.comm_grad) {   // sum of every rank's (1/global_rows)-scaled partial loss
+        ck(cudaMemcpyAsync(loss_dev_, &loss, sizeof(double), cudaMemcpyHostToDevice, S(compute_)), "H2D loss");
+        nccl_check(nccl().AllReduce(loss_dev_, loss_dev_, 1, ncclFloat64, ncclSum,
+                                    static_cast<ncclComm_t>(opts_.comm_grad), S(compute_)),
+                   "all-reduce loss");
+        ck(cudaMemcpyAsync(&loss, loss_dev_, sizeof(double), cudaMemcpyDeviceToHost, S(compute_)), "D2H loss");
+        ck(cudaStreamSynchronize(S(compute_)), "sync loss");
+    }
 
     // host ops into the trace, in consumption order
     std::vector<i64> accum_ids;
@@ -799,7 +870,30 @@ StepResult Engine::finish_step() {
             trace_.add(o);
         }
     }
-    if (!opts_.eager_optim && !opts_.skip_optimizer) {
+    if (!opts_.eager_optim && !opts_.skip_optimizer && opts_.comm_grad) {
+        const double t0 = now_us();
+        for (i64 p = 0; p < store_.physical_tiles(); ++p) {   // validate every shard first
+            LayerTile& tile = store_.physical(p);
+            const i64 cnt = shard_elems(tile.n_params());
+            if (!all_finite(tile.grads() + opts_.rank * cnt, cnt))
+                throw NumericsError("non-finite gradient in layer " + std::to_string(tile.layer_id()) + "; step aborted");
+        }
+        for (i64 p = 0; p < store_.physical_tiles(); ++p) {
+            LayerTile& tile = store_.physical(p);
+            const i64 cnt = shard_elems(tile.n_params()), begin = opts_.rank * cnt;
+            adam_step_range(tile, tile.grads() + begin, begin, cnt, hyper_, step_t_);
+            std::fill(tile.grads() + begin, tile.grads() + begin + cnt, 0.0f);
+            tile.bump_version(opts_.rank);
+        }
+        StreamOp op;
+        op.stream = StreamId::Host;
+        op.kind = OpKind::OptStep;
+        op.params = store_.total_params() / opts_.world;
+        op.deps = accum_ids;
+        op.t_start_us = t0 - host_t0_us_;
+        op.t_end_us = now_us() - host_t0_us_;
+        trace_.add(op);
+    } else if (!opts_.eager_optim && !opts_.skip_optimizer) {
         const double t0 = now_us();
         adam_step(store_, hyper_, step_t_);
         StreamOp op;

@@ -6,7 +6,12 @@
 #include <cuda_runtime.h>
 #include <immintrin.h>
 #include <omp.h>
+#include <fcntl.h>
 #include <sys/mman.h>
+#include <unistd.h>
+
+#include <chrono>
+#include <thread>
 
 #include <cmath>
 #include <cstring>
@@ -133,7 +138,18 @@ void LayerTile::store_weight(i64 i, float v) {
 }
 
 // ------------------------------------------------------------------ MasterStore
-MasterStore::MasterStore(const ModelConfig& config, Dtype dtype, bool pin_shadow)
+namespace {
+constexpr size_t kShmHeader = 2u << 20;
+constexpr std::uint64_t kShmMagic = 0x484C4D53484D3031ull;   // "HLMSHM01"
+struct ShmHeader {
+    std::uint64_t magic;
+    std::atomic<std::uint64_t> ready;
+    std::int64_t dims[8];
+};
+size_t align2m(size_t x) { return (x + (2u << 20) - 1) & ~size_t((2u << 20) - 1); }
+}  // namespace
+
+MasterStore::MasterStore(const ModelConfig& config, Dtype dtype, bool pin_shadow, const SharedStoreSpec* shared)
     : config_(config), dtype_(dtype) {
     config_.validate();
     const i64 h = config_.hidden, f = config_.ffn, V = config_.vocab;
@@ -153,9 +169,57 @@ MasterStore::MasterStore(const ModelConfig& config, Dtype dtype, bool pin_shadow
     }
     state_bytes_ = static_cast<size_t>(state_elems) * 4;
     shadow_bytes_ = static_cast<size_t>(shadow_elems) * 2;
+    std::atomic<i64>* versions = nullptr;
+    if (shared && shared->world >= 1 && !shared->name.empty()) {
+        rank_ = shared->rank;
+        world_ = shared->world;
+        shm_name_ = "/" + shared->name;
+        const size_t ver_bytes = align2m(specs.size() * static_cast<size_t>(world_) * sizeof(i64));
+        map_bytes_ = kShmHeader + align2m(state_bytes_) + align2m(shadow_bytes_) + ver_bytes;
+        if (rank_ == 0) {
+            shm_unlink(shm_name_.c_str());
+            shm_fd_ = shm_open(shm_name_.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
+            if (shm_fd_ < 0) throw ConfigError("shared store: shm_open(create) failed for " + shm_name_);
+            if (ftruncate(shm_fd_, static_cast<off_t>(map_bytes_)) != 0)
+                throw ConfigError("shared store: ftruncate failed");
+        } else {
+            for (int i = 0; i < 60000 && shm_fd_ < 0; ++i) {
+                shm_fd_ = shm_open(shm_name_.c_str(), O_RDWR, 0600);
+                if (shm_fd_ < 0) std::this_thread::sleep_for(std::chrono::milliseconds(10));
+            }
+            if (shm_fd_ < 0) throw ConfigError("shared store: rank 0 never created " + shm_name_);
+            for (int i = 0; i < 60000; ++i) {   // wait for the full size
+                if (lseek(shm_fd_, 0, SEEK_END) >= static_cast<off_t>(map_bytes_)) break;
+                std::this_thread::sleep_for(std::chrono::milliseconds(10));
+            }
+        }
+        map_base_ = mmap(nullptr, map_bytes_, PROT_READ | PROT_WRITE, MAP_SHARED, shm_fd_, 0);
+        if (map_base_ == MAP_FAILED) throw ConfigError("shared store: mmap failed");
+        char* b = static_cast<char*>(map_base_);
+        auto* hdr = reinterpret_cast<ShmHeader*>(b);
+        state_base_ = reinterpret_cast<float*>(b + kShmHeader);
+        shadow_base_ = reinterpret_cast<std::uint16_t*>(b + kShmHeader + align2m(state_bytes_));
+        versions = reinterpret_cast<std::atomic<i64>*>(b + kShmHeader + align2m(state_bytes_) + align2m(shadow_bytes_));
+        const std::int64_t dims[8] = {config_.layers, config_.hidden, config_.ffn, config_.vocab,
+                                      config_.tie_embeddings ? 1 : 0, static_cast<std::int64_t>(world_), 0, 0};
+        if (rank_ == 0) {
+            hdr->magic = kShmMagic;
+            std::memcpy(hdr->dims, dims, sizeof dims);
+            parallel_zero(state_base_, state_bytes_);
+            parallel_zero(shadow_base_, shadow_bytes_);
+            parallel_zero(versions, specs.size() * static_cast<size_t>(world_) * sizeof(i64));
+        }
+        if (pin_shadow) {
+            if (cudaHostRegister(shadow_base_, align2m(shadow_bytes_), cudaHostRegisterPortable) == cudaSuccess)
+                registered_ = pinned_ = true;
+            else
+                (void)cudaGetLastError();
+        }
+    } else {
     state_base_ = static_cast<float*>(map_huge(state_bytes_));
     parallel_zero(state_base_, state_bytes_);
-    if (pin_shadow) {
+    }
+    if (shm_fd_ < 0 && pin_shadow) {
         void* p = nullptr;
         if (cudaHostAlloc(&p, shadow_bytes_, cudaHostAllocPortable) == cudaSuccess) {
             shadow_base_ = static_cast<std::uint16_t*>(p);
@@ -164,13 +228,16 @@ MasterStore::MasterStore(const ModelConfig& config, Dtype dtype, bool pin_shadow
             (void)cudaGetLastError();
         }
     }
-    if (!shadow_base_) shadow_base_ = static_cast<std::uint16_t*>(map_huge(shadow_bytes_));
-    parallel_zero(shadow_base_, shadow_bytes_);
+    if (!shadow_base_) {
+        shadow_base_ = static_cast<std::uint16_t*>(map_huge(shadow_bytes_));
+        parallel_zero(shadow_base_, shadow_bytes_);
+    }
 
     i64 so = 0, sh = 0;
     for (auto& s : specs) {
         const i64 padded = round_up(s.n, kAlignElems);
         tiles_.push_back(std::make_unique<LayerTile>(s.id, s.n, std::move(s.off), state_base_ + so, shadow_base_ + sh));
+        if (versions) tiles_.back()->attach_shared_versions(versions + (tiles_.size() - 1) * world_, world_);
         so += 3 * padded;
         sh += padded;
     }
@@ -183,6 +250,13 @@ MasterStore::MasterStore(const ModelConfig& config, Dtype dtype, bool pin_shadow
 
 MasterStore::~MasterStore() {
     for (auto& t : tiles_) t.reset();
+    if (shm_fd_ >= 0) {
+        if (registered_) cudaHostUnregister(shadow_base_);
+        munmap(map_base_, map_bytes_);
+        close(shm_fd_);
+        if (rank_ == 0) shm_unlink(shm_name_.c_str());
+        return;
+    }
     if (state_base_) munmap(state_base_, state_bytes_);
     if (shadow_base_) {
         if (pinned_)
@@ -221,14 +295,32 @@ bool MasterStore::bitwise_equal(const MasterStore& o) const {
     return true;
 }
 
+void MasterStore::mark_ready() {
+    if (shm_fd_ < 0) return;
+    reinterpret_cast<ShmHeader*>(map_base_)->ready.store(1, std::memory_order_release);
+}
+
+void MasterStore::wait_ready() const {
+    if (shm_fd_ < 0) return;
+    auto* hdr = reinterpret_cast<ShmHeader*>(map_base_);
+    for (;;) {
+        if (hdr->magic == kShmMagic && hdr->ready.load(std::memory_order_acquire) == 1) return;
+        std::this_thread::sleep_for(std::chrono::milliseconds(5));
+    }
+}
+
 void MasterStore::repack_shadow() {
     for (auto& t : tiles_) pack_shadow(t->master(), t->shadow(), t->n_params());
 }
 
 // reference host_store.cpp:141-156 (InitMode::Reference is bit-identical).
 std::unique_ptr<MasterStore> build_store(const ModelConfig& config, std::uint64_t seed, Dtype dtype, InitMode mode,
-                                         bool pin_shadow) {
-    auto store = std::make_unique<MasterStore>(config, dtype, pin_shadow);
+                                         bool pin_shadow, const SharedStoreSpec* shared) {
+    auto store = std::make_unique<MasterStore>(config, dtype, pin_shadow, shared);
+    if (store->shared() && !store->owner()) {   // attach: rank 0 initialises
+        store->wait_ready();
+        return store;
+    }
     const bool bf = dtype == Dtype::BF16;
     if (mode == InitMode::Reference) {
         Rng rng(seed);
@@ -263,6 +355,7 @@ std::unique_ptr<MasterStore> build_store(const ModelConfig& config, std::uint64_
         }
     }
     store->repack_shadow();
+    store->mark_ready();
     return store;
 }
 
@@ -470,10 +563,25 @@ void adam_apply(LayerTile& tile, const float* grad, const HyperParams& hyper, i6
     const float bc2 = 1.0f - std::pow(b2, static_cast<float>(t));
     adam_kernel(tile.master(), tile.moment_m(), tile.moment_v(), tile.shadow(), grad, tile.n_params(), lr, b1, b2,
                 eps, wd, bc1, bc2, zero_after);
-    tile.version.fetch_add(1, std::memory_order_release);
+    tile.bump_version(0);
 }
 
 }  // namespace
+
+void adam_step_range(LayerTile& tile, const float* grad, i64 begin, i64 count, const HyperParams& hyper, i64 t) {
+    if (t < 1) throw ProtocolError("adam step index must be >= 1");
+    if (begin < 0 || begin + count > tile.n_params()) throw ProtocolError("adam shard out of range");
+    if (!all_finite(grad, count))
+        throw NumericsError("non-finite gradient in layer " + std::to_string(tile.layer_id()) + " at element " +
+                            std::to_string(begin + first_non_finite(grad, count)) + "; step aborted");
+    const float lr = static_cast<float>(hyper.lr), b1 = static_cast<float>(hyper.beta1),
+                b2 = static_cast<float>(hyper.beta2), eps = static_cast<float>(hyper.eps),
+                wd = static_cast<float>(hyper.weight_decay);
+    const float bc1 = 1.0f - std::pow(b1, static_cast<float>(t));
+    const float bc2 = 1.0f - std::pow(b2, static_cast<float>(t));
+    adam_kernel(tile.master() + begin, tile.moment_m() + begin, tile.moment_v() + begin, tile.shadow() + begin, grad,
+                count, lr, b1, b2, eps, wd, bc1, bc2, nullptr);
+}
 
 void adam_step_tile_from(LayerTile& tile, const float* grad, const HyperParams& hyper, i64 t) {
     adam_apply(tile, grad, hyper, t, nullptr);

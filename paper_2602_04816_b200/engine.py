@@ -89,14 +89,20 @@ class EngineOptions(ctypes.Structure):
                 ("n_slab", ctypes.c_int64), ("accum_delay_us", ctypes.c_int64),
                 ("skip_optimizer", ctypes.c_int32), ("fused_recompute", ctypes.c_int32),
                 ("record_trace", ctypes.c_int32), ("block_flags", ctypes.c_int32),
-                ("overlap_optimizer_tail", ctypes.c_int32), ("tail_blocks", ctypes.c_int32)]
+                ("overlap_optimizer_tail", ctypes.c_int32), ("tail_blocks", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("comm_grad", ctypes.c_void_p),
+                ("comm_weights", ctypes.c_void_p)]
 
     def __init__(self, eager_optim=False, threaded_accum=False, n_slab=12, accum_delay_us=0,
                  skip_optimizer=False, fused_recompute=True, record_trace=True, block_flags=0,
-                 overlap_optimizer_tail=False, tail_blocks=2):
+                 overlap_optimizer_tail=False, tail_blocks=2, rank=0, world=1, comm_grad=None,
+                 comm_weights=None):
         super().__init__(int(eager_optim), int(threaded_accum), n_slab, accum_delay_us,
                          int(skip_optimizer), int(fused_recompute), int(record_trace), block_flags,
-                         int(overlap_optimizer_tail), tail_blocks)
+                         int(overlap_optimizer_tail), tail_blocks, rank, world,
+                         comm_grad.value if isinstance(comm_grad, ctypes.c_void_p) else comm_grad,
+                         comm_weights.value if isinstance(comm_weights, ctypes.c_void_p)
+                         else comm_weights)
 
 
 class StepResult(ctypes.Structure):
@@ -127,6 +133,16 @@ def _L():
         L.hlm_store_import_master.argtypes = [_vp, _f32p]
         L.hlm_store_bitwise_equal.argtypes = [_vp, _vp]
         L.hlm_store_adam_step.argtypes = [_vp, _f32p, P(HyperParams), ctypes.c_int64]
+        L.hlm_store_create_shared.argtypes = [P(ModelConfig), ctypes.c_uint64, ctypes.c_int,
+                                              ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
+                                              ctypes.c_int, ctypes.c_int, P(_vp)]
+        L.hlm_store_adam_shard.argtypes = [_vp, _f32p, P(HyperParams), ctypes.c_int64, ctypes.c_int,
+                                           ctypes.c_int]
+        L.hlm_store_tile_version.argtypes = [_vp, ctypes.c_int64]
+        L.hlm_store_tile_version.restype = ctypes.c_int64
+        L.hlm_nccl_unique_id.argtypes = [ctypes.c_char_p]
+        L.hlm_nccl_comm_create.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, P(_vp)]
+        L.hlm_nccl_comm_destroy.argtypes = [_vp]
         L.hlm_arena_create.argtypes = [P(ModelConfig), ctypes.c_int64, ctypes.c_int, P(_vp)]
         L.hlm_arena_create_ex.argtypes = [P(ModelConfig), ctypes.c_int64, ctypes.c_int,
                                           ctypes.c_int64, P(_vp)]
@@ -157,11 +173,18 @@ class Store:
     """Host parameter store (build_store). dtype 'bf16' | 'fp32' (initial rounding);
     init 'reference' (bit-identical to the reference) | 'parallel'."""
 
-    def __init__(self, cfg, seed, dtype="bf16", init="reference", pin=True):
+    def __init__(self, cfg, seed, dtype="bf16", init="reference", pin=True, shared=None, rank=0,
+                 world=1):
+        """shared: name of a /dev/shm object for a one-process-per-GPU store
+        (rank 0 creates and initialises it, other ranks attach)."""
         self.cfg = cfg
         h = _vp()
-        _check(_L().hlm_store_create(ctypes.byref(cfg), seed, 1 if dtype == "fp32" else 0,
-                                     1 if init == "parallel" else 0, int(pin), ctypes.byref(h)))
+        dt, im = (1 if dtype == "fp32" else 0), (1 if init == "parallel" else 0)
+        if shared:
+            _check(_L().hlm_store_create_shared(ctypes.byref(cfg), seed, dt, im, int(pin),
+                                                shared.encode(), rank, world, ctypes.byref(h)))
+        else:
+            _check(_L().hlm_store_create(ctypes.byref(cfg), seed, dt, im, int(pin), ctypes.byref(h)))
         self.h = h
 
     def __del__(self):
@@ -197,6 +220,25 @@ class Store:
 
     def bitwise_equal(self, other):
         return bool(_L().hlm_store_bitwise_equal(self.h, other.h))
+
+    def adam_shard(self, grads, hyper, t, rank, world):
+        _check(_L().hlm_store_adam_shard(self.h, np.ascontiguousarray(grads, np.float32),
+                                         ctypes.byref(hyper), t, rank, world))
+
+    def tile_version(self, p):
+        return _L().hlm_store_tile_version(self.h, p)
+
+
+def nccl_unique_id():
+    buf = ctypes.create_string_buffer(128)
+    _check(_L().hlm_nccl_unique_id(buf))
+    return buf.raw
+
+
+def nccl_comm(uid, world, rank):
+    c = _vp()
+    _check(_L().hlm_nccl_comm_create(uid, world, rank, ctypes.byref(c)))
+    return c
 
 
 def arena_footprint(cfg):
