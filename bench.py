@@ -159,10 +159,15 @@ def run_reference(args, m, name):
 
 
 def run_ours(args, m, name):
+    rank, world, local = dist_env()
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    if world > 1 and "OMP_NUM_THREADS" not in os.environ:
+        # ranks share the host cores for their shard of the Adam
+        os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or 16) // local_world))
     from paper_2602_04816_b200 import _lib
     from paper_2602_04816_b200 import engine as E
 
-    rank, world, local = dist_env()
+    dp = world > 1 or args.force_dp
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo")
@@ -172,6 +177,7 @@ def run_ours(args, m, name):
     lib.hlm_timer_elapsed_ms.restype = ctypes.c_double
     lib.hlm_timer_elapsed_ms.argtypes = [ctypes.c_int, ctypes.c_int]
     lib.hlm_cuda_launch_count.restype = ctypes.c_longlong
+    lib.hlm_nccl_comm_destroy.argtypes = [ctypes.c_void_p]
     lib.hlm_cuda_bench_block_gemms.argtypes = [ctypes.POINTER(_lib.HlmBlockDims), ctypes.c_int] + \
         [ctypes.POINTER(ctypes.c_double)] * 3
 
@@ -179,17 +185,32 @@ def run_ours(args, m, name):
                         k_ckpt=1, n_heads=m["n_heads"], rope_theta=1e6)
     nums = model_numbers(m)
     t0 = time.time()
-    store = E.Store(cfg, 1234, "bf16", init="parallel")
+    comm_g = comm_w = None
+    if dp:
+        uids = [E.nccl_unique_id(), E.nccl_unique_id()] if rank == 0 else [None, None]
+        if world > 1:
+            dist.broadcast_object_list(uids, src=0)
+        comm_g = E.nccl_comm(uids[0], world, rank)
+        comm_w = E.nccl_comm(uids[1], world, rank)
+        shm = f"hlm_bench_{os.environ.get('MASTER_PORT', os.getpid())}"
+        store = E.Store(cfg, 1234, "bf16", init="parallel", shared=shm, rank=rank, world=world)
+    else:
+        store = E.Store(cfg, 1234, "bf16", init="parallel")
     # HBM weight cache for the backward turnaround: all blocks when they fit next to the arena
     blk = (2 * nums["n"] + 255) // 256 * 256
     cache = min(m["layers"], int(args.cache_gb * 1e9) // blk) * blk
     arena = E.Arena(cfg, device=local, weight_cache_bytes=cache)
     opts = E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=args.slabs,
                            record_trace=True, overlap_optimizer_tail=args.tail_blocks >= 0,
-                           tail_blocks=max(0, args.tail_blocks))
+                           tail_blocks=max(0, args.tail_blocks), rank=rank, world=world,
+                           comm_grad=comm_g, comm_weights=comm_w)
     eng = E.Engine(store, arena, E.HyperParams(lr=1e-4), opts)
     setup_s = time.time() - t0
-    batches = [E.make_copy_task_batch(cfg, 1235, skip=i) for i in range(args.warmup + args.steps)]
+    # one global token stream (reference RNG, global batch = world x local), sliced by rank
+    gcfg = E.ModelConfig(m["layers"], m["hidden"], m["ffn"], m["vocab"], m["seq"], m["batch"] * world)
+    rows = m["batch"] * m["seq"]
+    batches = [E.make_copy_task_batch(gcfg, 1235, skip=i)[rank * rows:(rank + 1) * rows]
+               for i in range(args.warmup + args.steps)]
 
     for i in range(args.warmup):
         eng.train_step(batches[i])
@@ -273,6 +294,10 @@ def run_ours(args, m, name):
     if rank != 0:
         if world > 1:
             dist.barrier()
+        del eng
+        for c in (comm_g, comm_w):
+            if c is not None:
+                lib.hlm_nccl_comm_destroy(c)
         return
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -304,6 +329,10 @@ def run_ours(args, m, name):
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
+    del eng
+    for c in (comm_g, comm_w):
+        if c is not None:
+            lib.hlm_nccl_comm_destroy(c)
 
 
 def main():
@@ -319,6 +348,8 @@ def main():
     ap.add_argument("--cache-gb", type=float, default=60.0,
                     help="HBM weight cache (block tiles resident between forward and backward)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-dp", action="store_true",
+                    help="use the data-parallel code path (NCCL, shared store) even at world 1")
     ap.add_argument("--dump-trace", default="", help="write the last warm-up step's measured trace (JSONL)")
     args = ap.parse_args()
     m = dict(CONFIGS[args.config])
