@@ -180,6 +180,8 @@ private:
     i64 shard_elems(i64 n) const;          // n / world (throws unless divisible)
     void h2d_tile(void* dst, const LayerTile& tile, i64 bytes);
     double* loss_dev_ = nullptr;
+    unsigned long long* nf_dev_ = nullptr;    // per slab: first non-finite index (device)
+    unsigned long long* nf_host_ = nullptr;   // pinned mirror
     std::vector<char> deferred_;           // per logical tile: optimised in the tail
     std::vector<i64> target_version_;      // per physical tile: version the next H2D needs
     bool tail_open_ = true;                // embed of the current step processed (mu_)

@@ -258,11 +258,14 @@ private:
 //   adam_step_tile_from: gradients from an external FP32 buffer (a slab).
 void adam_step(MasterStore& store, const HyperParams& hyper, i64 t);
 void adam_step_tile(MasterStore& store, i64 physical_idx, const HyperParams& hyper, i64 t);
-void adam_step_tile_from(LayerTile& tile, const float* grad, const HyperParams& hyper, i64 t);
+// prechecked: the caller already verified every gradient is finite (the engine
+// does it on the GPU before the D2H), so the host skips its validation read.
+void adam_step_tile_from(LayerTile& tile, const float* grad, const HyperParams& hyper, i64 t,
+                         bool prechecked = false);
 // Shard version (data parallel): elements [begin, begin + count) of the tile,
 // grad points at the shard's first element. Does not bump the version.
 void adam_step_range(LayerTile& tile, const float* grad, i64 begin, i64 count, const HyperParams& hyper,
-                     i64 t);
+                     i64 t, bool prechecked = false);
 
 // grads(tile) += g  (slab accumulation, host_store.cpp:254-284, FP32).
 void accumulate_grads(LayerTile& tile, const float* g);

@@ -147,6 +147,8 @@ int hlm_embed_csr(const int32_t* tokens, int64_t rows, int64_t vocab, int32_t* r
 
 /* ------------------------------------------------------------------ small ops */
 int hlm_cuda_cast_bf16(const float* in, void* out, int64_t n, void* stream);
+/* *first (device u64) := smallest index of a non-finite element of g, ~0 when all finite */
+int hlm_cuda_nonfinite(const float* g, int64_t n, unsigned long long* first, void* stream);
 
 /* Device-event timer for harnesses: record(slot) synchronises the device and
  * records an event on the legacy stream; elapsed_ms(a, b) between two slots. */

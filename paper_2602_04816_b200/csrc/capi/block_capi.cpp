@@ -393,6 +393,10 @@ int hlm_embed_csr(const int32_t* tokens, int64_t rows, int64_t vocab, int32_t* r
 }
 
 // ------------------------------------------------------------------ small ops
+int hlm_cuda_nonfinite(const float* g, int64_t n, unsigned long long* first, void* stream) {
+  return guarded([&] { chk(hlm_ops_nonfinite(g, n, first, static_cast<cudaStream_t>(stream)), "nonfinite"); });
+}
+
 int hlm_cuda_cast_bf16(const float* in, void* out, int64_t n, void* stream) {
   return guarded([&] { chk(hlm_ops_cast_bf16(in, out, n, static_cast<cudaStream_t>(stream)), "cast"); });
 }

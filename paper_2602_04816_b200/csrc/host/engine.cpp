@@ -72,6 +72,10 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
         ck(cudaEventRecord(E(ev_gradbuf_free_[i]), S(compute_)), "record");
     }
     for (i64 i = 0; i < pool_->size(); ++i) ev_slab_done_.push_back(new_event(false));
+    ck(cudaMalloc(&nf_dev_, static_cast<size_t>(pool_->size()) * 8), "cudaMalloc nf");
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&nf_host_), static_cast<size_t>(pool_->size()) * 8,
+                     cudaHostAllocPortable),
+       "cudaHostAlloc nf");
     ev_step_start_ = new_event(true);
     ev_step_end_ = new_event(true);
     const i64 T = m.rows();
@@ -137,6 +141,8 @@ Engine::~Engine() {
     cudaStreamDestroy(S(d2h_));
     if (loss_host_) cudaFreeHost(loss_host_);
     if (loss_dev_) cudaFree(loss_dev_);
+    if (nf_dev_) cudaFree(nf_dev_);
+    if (nf_host_) cudaFreeHost(nf_host_);
 }
 
 i64 Engine::shard_elems(i64 n) const {
@@ -317,8 +323,11 @@ void Engine::evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op) {
                                         static_cast<ncclComm_t>(opts_.comm_grad), S(d2h_)),
                    "reduce-scatter grads");
     }
+    // the reference's "all gradients finite before any mutation" check, on the GPU
+    ck_hlm(hlm_cuda_nonfinite(src, cnt, nf_dev_ + slab, d2h_), "nonfinite scan");
     ck(cudaMemcpyAsync(pool_->data(slab), src, static_cast<size_t>(bytes), cudaMemcpyDeviceToHost, S(d2h_)),
        "D2H grads");
+    ck(cudaMemcpyAsync(nf_host_ + slab, nf_dev_ + slab, 8, cudaMemcpyDeviceToHost, S(d2h_)), "D2H nf flag");
     op_end(id, d2h_);
     ck(cudaEventRecord(E(ev_slab_done_[static_cast<size_t>(slab)]), S(d2h_)), "record slab done");
     ck(cudaEventRecord(E(ev_gradbuf_free_[gbuf]), S(d2h_)), "record grad buf free");
@@ -343,6 +352,12 @@ void Engine::consume(const Pending& p) {
     LayerTile& tile = store_.tile(p.layer);
     const i64 phys = store_.physical_index(p.layer);
     const bool optimise = opts_.eager_optim && !opts_.skip_optimizer;
+    const unsigned long long bad = nf_host_[p.slab];
+    if (bad != ~0ull && optimise) {
+        const i64 base = opts_.comm_grad ? opts_.rank * shard_elems(tile.n_params()) : 0;
+        throw NumericsError("non-finite gradient in layer " + std::to_string(tile.layer_id()) + " at element " +
+                            std::to_string(base + static_cast<i64>(bad)) + "; step aborted");
+    }
     if (opts_.comm_grad) {   // this rank's shard [begin, begin + cnt)
         const i64 cnt = shard_elems(tile.n_params()), begin = opts_.rank * cnt;
         const float* g = pool_->data(p.slab);
@@ -350,7 +365,7 @@ void Engine::consume(const Pending& p) {
             rec.t1 = now_us();
             rec.opt = true;
             rec.topt0 = rec.t1;
-            adam_step_range(tile, g, begin, cnt, hyper_, p.t);
+            adam_step_range(tile, g, begin, cnt, hyper_, p.t, /*prechecked=*/true);
             tile.bump_version(opts_.rank);
             rec.topt1 = now_us();
         } else {
@@ -376,7 +391,7 @@ void Engine::consume(const Pending& p) {
         rec.t1 = now_us();
         rec.opt = true;
         rec.topt0 = rec.t1;
-        adam_step_tile_from(tile, pool_->data(p.slab), hyper_, p.t);
+        adam_step_tile_from(tile, pool_->data(p.slab), hyper_, p.t, /*prechecked=*/true);
         rec.topt1 = now_us();
     } else {
         accumulate_grads(tile, pool_->data(p.slab));

@@ -551,9 +551,10 @@ void adam_kernel(float* __restrict w, float* __restrict m, float* __restrict v, 
     }
 }
 
-void adam_apply(LayerTile& tile, const float* grad, const HyperParams& hyper, i64 t, float* zero_after) {
+void adam_apply(LayerTile& tile, const float* grad, const HyperParams& hyper, i64 t, float* zero_after,
+                bool prechecked = false) {
     if (t < 1) throw ProtocolError("adam step index must be >= 1");
-    if (!all_finite(grad, tile.n_params()))
+    if (!prechecked && !all_finite(grad, tile.n_params()))
         throw NumericsError("non-finite gradient in layer " + std::to_string(tile.layer_id()) + " at element " +
                             std::to_string(first_non_finite(grad, tile.n_params())) + "; step aborted");
     const float lr = static_cast<float>(hyper.lr), b1 = static_cast<float>(hyper.beta1),
@@ -568,10 +569,11 @@ void adam_apply(LayerTile& tile, const float* grad, const HyperParams& hyper, i6
 
 }  // namespace
 
-void adam_step_range(LayerTile& tile, const float* grad, i64 begin, i64 count, const HyperParams& hyper, i64 t) {
+void adam_step_range(LayerTile& tile, const float* grad, i64 begin, i64 count, const HyperParams& hyper, i64 t,
+                     bool prechecked) {
     if (t < 1) throw ProtocolError("adam step index must be >= 1");
     if (begin < 0 || begin + count > tile.n_params()) throw ProtocolError("adam shard out of range");
-    if (!all_finite(grad, count))
+    if (!prechecked && !all_finite(grad, count))
         throw NumericsError("non-finite gradient in layer " + std::to_string(tile.layer_id()) + " at element " +
                             std::to_string(begin + first_non_finite(grad, count)) + "; step aborted");
     const float lr = static_cast<float>(hyper.lr), b1 = static_cast<float>(hyper.beta1),
@@ -583,8 +585,8 @@ void adam_step_range(LayerTile& tile, const float* grad, i64 begin, i64 count, c
                 count, lr, b1, b2, eps, wd, bc1, bc2, nullptr);
 }
 
-void adam_step_tile_from(LayerTile& tile, const float* grad, const HyperParams& hyper, i64 t) {
-    adam_apply(tile, grad, hyper, t, nullptr);
+void adam_step_tile_from(LayerTile& tile, const float* grad, const HyperParams& hyper, i64 t, bool prechecked) {
+    adam_apply(tile, grad, hyper, t, nullptr, prechecked);
 }
 
 void adam_step_tile(MasterStore& store, i64 physical_idx, const HyperParams& hyper, i64 t) {

@@ -308,6 +308,26 @@ __global__ void __launch_bounds__(THREADS) ce_kernel(const float* __restrict__ l
   }
 }
 
+// ------------------------------------------------------------------ finiteness
+// first[0] = min index of a non-finite element (INT64 max when none): the
+// reference's "validate before any mutation" check (host_store.cpp:340-345),
+// run at HBM speed before the gradient leaves the GPU.
+__global__ void nonfinite_kernel(const float* __restrict__ g, long long n, unsigned long long* first) {
+  const long long stride = (long long)gridDim.x * blockDim.x * 4;
+  for (long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < n; i += stride) {
+    if (i + 4 <= n) {
+      const float4 v = *reinterpret_cast<const float4*>(g + i);
+      const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (!isfinite(e[k])) atomicMin(first, (unsigned long long)(i + k));
+    } else {
+      for (long long k = i; k < n; ++k)
+        if (!isfinite(g[k])) atomicMin(first, (unsigned long long)k);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ generic attention
 // Causal softmax attention for any head_dim <= 32*VPL: one warp per
 // (batch, head, query row), online softmax over keys j <= i in fp32.
@@ -507,6 +527,13 @@ long long hlm_launches_total() { return g_launches.load(std::memory_order_relaxe
 
 int hlm_ops_fill_random_bf16(void* p, long long n, unsigned seed, cudaStream_t s) {
   fill_random_bf16_kernel<<<grid_for(n, 256), 256, 0, s>>>((__nv_bfloat16*)p, n, seed);
+  HLM_CHECK_LAUNCH();
+}
+
+int hlm_ops_nonfinite(const float* g, long long n, unsigned long long* first, cudaStream_t s) {
+  cudaMemsetAsync(first, 0xFF, sizeof(unsigned long long), s);
+  nonfinite_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, s>>>(g, n, first);
+  hlm_count_launches(1);
   HLM_CHECK_LAUNCH();
 }
 

@@ -33,3 +33,5 @@ void hlm_count_launches(long long n);
 long long hlm_launches_total();
 // Deterministic pseudo-random bf16 fill (bench / probe inputs), |x| < 1.
 int hlm_ops_fill_random_bf16(void* p, long long n, unsigned seed, cudaStream_t s);
+// first[0] := smallest index of a non-finite element of g[0..n), ~0ull when none.
+int hlm_ops_nonfinite(const float* g, long long n, unsigned long long* first, cudaStream_t s);

@@ -246,3 +246,16 @@ def test_optimizer_tail_overlap_is_bitwise_neutral():
     e.sync()
     assert l0 == l1
     assert ref.bitwise_equal(s)
+
+
+def test_non_finite_gradient_aborts_naming_the_layer():
+    """A NaN weight poisons the gradients; the eager optimizer must refuse the
+    update (host_store.cpp:371-382 contract, checked on the GPU before D2H)."""
+    c = E.ModelConfig(2, 16, 32, 13, 4, 1)
+    s = E.Store(c, 5, "fp32")
+    w = s.weights()
+    w[-1] = np.nan   # head tile, last element
+    s.import_master(w)
+    e = E.Engine(s, E.Arena(c), E.HyperParams(), E.EngineOptions(eager_optim=True))
+    with pytest.raises(E.NumericsError, match="non-finite gradient in layer"):
+        e.train_step(E.make_copy_task_batch(c, 2))
