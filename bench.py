@@ -231,6 +231,7 @@ def run_ours(args, m, name):
         r = eng.train_step(batches[args.warmup + i])
         losses.append(r.loss)
         gpu_ms.append(r.gpu_ms)
+        h2d_step = r.h2d_bytes
     eng.sync()   # the last step's optimizer tail is inside the timed region
     lib.hlm_timer_record(1)
     wall = time.perf_counter() - wall0
@@ -246,26 +247,11 @@ def run_ours(args, m, name):
     value = world * nums["T"] * args.steps / dev_s
     e2e = world * nums["T"] * args.steps / wall
 
-    # per-step overlap / bandwidth from the measured trace (last warm-up step)
-    h2d = [o for o in trace if o["stream"] == "h2d"]
-    d2h = [o for o in trace if o["stream"] == "d2h"]
-    comp = [o for o in trace if o["stream"] == "compute" and o["t_end_us"] > 0]
-    h2d_busy = sum(o["t_end_us"] - o["t_start_us"] for o in h2d)
-    d2h_busy = sum(o["t_end_us"] - o["t_start_us"] for o in d2h)
-    h2d_gbs = sum(o["bytes"] for o in h2d) / max(h2d_busy, 1e-9) / 1e3
-    d2h_gbs = sum(o["bytes"] for o in d2h) / max(d2h_busy, 1e-9) / 1e3
-    comp_iv = sorted((o["t_start_us"], o["t_end_us"]) for o in comp)
-
-    def covered(a, b):
-        tot = 0.0
-        for s, e in comp_iv:
-            lo, hi = max(a, s), min(b, e)
-            if hi > lo:
-                tot += hi - lo
-        return tot
-    xfer = sum(o["t_end_us"] - o["t_start_us"] for o in h2d + d2h)
-    hidden = sum(covered(o["t_start_us"], o["t_end_us"]) for o in h2d + d2h)
-    overlap = hidden / xfer if xfer > 0 else None
+    # per-step overlap / bandwidth / protocol check from the measured trace (last warm-up step)
+    from paper_2602_04816_b200.trace import overlap_report, validate_trace
+    rep = overlap_report(trace)
+    h2d_gbs, d2h_gbs, overlap = rep["h2d_gbs"], rep["d2h_gbs"], rep["overlap"]
+    violations = validate_trace(trace, m["layers"])
     host_ops = [o for o in trace if o["stream"] == "host" and o["kind"] == "OptStep"]
     adam_s = sum(o["t_end_us"] - o["t_start_us"] for o in host_ops) / 1e6
     gpu_busy_s = float(np.mean(gpu_ms)) / 1e3
@@ -312,7 +298,7 @@ def run_ours(args, m, name):
         "tflops": nums["model_flops"] / step_s / 1e12,
         "hw_tflops": nums["hw_flops"] / step_s / 1e12,
         "e2e": {"value": e2e, "unit": "tokens/s",
-                "h2d_bytes_per_step": int(nums["h2d"] + 8 * nums["T"]),
+                "h2d_bytes_per_step": int(h2d_step + 8 * nums["T"]),
                 "d2h_bytes_per_step": int(nums["d2h"] + 4 * nums["T"])},
         "gpu_launches": int(launches),
         "roofline": {"bound": "tensor", "kernel": "gemm_sm100 (tcgen05/TMA, 12 block launches)",
@@ -322,7 +308,8 @@ def run_ours(args, m, name):
         "step_roofline": {"t_roof_s": t_roof, "t_step_s": step_s, "frac": t_roof / step_s,
                           "def": "max(HW_FLOPS/sustained bf16, H2D/55GB/s, D2H/55GB/s)"},
         "stream": {"h2d_gbs": h2d_gbs, "d2h_gbs": d2h_gbs, "overlap": overlap,
-                   "gpu_busy_s": gpu_busy_s, "host_adam_s": adam_s},
+                   "gpu_busy_s": gpu_busy_s, "host_adam_s": adam_s,
+                   "h2d_bytes_measured": int(h2d_step), "trace_violations": len(violations)},
         "clocks": clk, "cpu_baseline": cpu_baseline,
         "loss": [float(x) for x in losses], "setup_s": setup_s,
     }

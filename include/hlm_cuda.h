@@ -267,13 +267,22 @@ int hlm_engine_debug_hidden(HlmEngine* e, float* out);
 /* JSONL of the last step's measured trace; *needed = bytes incl. NUL */
 int hlm_engine_last_trace(HlmEngine* e, char* buf, size_t cap, size_t* needed);
 
+/* HLM2 checkpoint of the host store (master, m, v, Adam step count); load
+ * re-derives the BF16 shadow and rejects mismatched geometry (HLM_ERR_CONFIG). */
+int hlm_store_save(const HlmStore* s, const char* path);
+int hlm_store_load(HlmStore* s, const char* path);
+
 /* NCCL (loaded at run time): 128-byte unique id, communicator create / destroy */
 int hlm_nccl_unique_id(uint8_t* out128);
 int hlm_nccl_comm_create(const uint8_t* id128, int world, int rank, void** comm);
 void hlm_nccl_comm_destroy(void* comm);
 
 int hlm_make_copy_task_batch(const HlmModelConfig* cfg, uint64_t data_seed, int64_t skip, int32_t* tokens);
-/* run_training (trainer.hpp): store from seed, data seed+1, `steps` steps */
+/* run_training (trainer.hpp): store from seed, data seed+1, `steps` steps;
+ * hlm_run_training_store continues an existing store (resume: the data stream
+ * is replayed past store->adam_steps batches). */
+int hlm_run_training_store(HlmStore* s, const HlmHyper* hp, uint64_t seed, int64_t steps,
+                           const HlmEngineOptions* o, double* losses);
 int hlm_run_training(const HlmModelConfig* cfg, const HlmHyper* hp, uint64_t seed, int dtype, int64_t steps,
                      const HlmEngineOptions* o, double* losses, HlmStepResult* last);
 

@@ -8,6 +8,7 @@
 
 #include "capi_util.h"
 #include "hlm/bf16.hpp"
+#include "hlm/checkpoint.hpp"
 #include "hlm/engine.hpp"
 #include "hlm/trainer.hpp"
 #include "hlm_cuda.h"
@@ -175,6 +176,32 @@ int hlm_store_adam_shard(HlmStore* s, const float* grads, const HlmHyper* hp, in
 }
 
 int64_t hlm_store_tile_version(const HlmStore* s, int64_t p) { return s->s->physical(p).min_version(); }
+
+int hlm_store_save(const HlmStore* s, const char* path) {
+    return guarded([&] { hlm::save_checkpoint(*s->s, path); });
+}
+
+int hlm_store_load(HlmStore* s, const char* path) {
+    return guarded([&] { hlm::load_checkpoint(*s->s, path); });
+}
+
+int hlm_run_training_store(HlmStore* s, const HlmHyper* hp, uint64_t seed, int64_t steps,
+                           const HlmEngineOptions* o, double* losses) {
+    return guarded([&] {
+        hlm::RunConfig rc;
+        rc.model = s->s->config();
+        rc.hyper = to_hyper(hp);
+        rc.run.steps = steps;
+        rc.run.seed = seed;
+        const hlm::EngineOptions eo = to_opts(o);
+        rc.run.eager_optim = eo.eager_optim;
+        rc.run.n_slab = eo.n_slab;
+        rc.run.threaded_accum = eo.threaded_accum;
+        hlm::DeviceArena arena(rc.model);
+        const hlm::TrainOutput out = hlm::run_training(rc, *s->s, arena, {}, eo);
+        for (size_t i = 0; i < out.steps.size(); ++i) losses[i] = out.steps[i].loss;
+    });
+}
 
 int hlm_nccl_unique_id(uint8_t* out128) {
     return guarded([&] {

@@ -140,6 +140,10 @@ def _L():
                                            ctypes.c_int]
         L.hlm_store_tile_version.argtypes = [_vp, ctypes.c_int64]
         L.hlm_store_tile_version.restype = ctypes.c_int64
+        L.hlm_store_save.argtypes = [_vp, ctypes.c_char_p]
+        L.hlm_store_load.argtypes = [_vp, ctypes.c_char_p]
+        L.hlm_run_training_store.argtypes = [_vp, P(HyperParams), ctypes.c_uint64, ctypes.c_int64,
+                                             P(EngineOptions), _f64p]
         L.hlm_nccl_unique_id.argtypes = [ctypes.c_char_p]
         L.hlm_nccl_comm_create.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, P(_vp)]
         L.hlm_nccl_comm_destroy.argtypes = [_vp]
@@ -220,6 +224,19 @@ class Store:
 
     def bitwise_equal(self, other):
         return bool(_L().hlm_store_bitwise_equal(self.h, other.h))
+
+    def save(self, path):
+        _check(_L().hlm_store_save(self.h, str(path).encode()))
+
+    def load(self, path):
+        _check(_L().hlm_store_load(self.h, str(path).encode()))
+
+    def run_training(self, hyper, seed, steps, options=None):
+        """run_training on this store (resume-aware: replays the data stream)."""
+        losses = np.empty(steps, np.float64)
+        _check(_L().hlm_run_training_store(self.h, ctypes.byref(hyper), seed, steps,
+                                           ctypes.byref(options or EngineOptions()), losses))
+        return losses
 
     def adam_shard(self, grads, hyper, t, rank, world):
         _check(_L().hlm_store_adam_shard(self.h, np.ascontiguousarray(grads, np.float32),

@@ -259,3 +259,39 @@ def test_non_finite_gradient_aborts_naming_the_layer():
     e = E.Engine(s, E.Arena(c), E.HyperParams(), E.EngineOptions(eager_optim=True))
     with pytest.raises(E.NumericsError, match="non-finite gradient in layer"):
         e.train_step(E.make_copy_task_batch(c, 2))
+
+
+def test_save_load_resume_is_bitwise(tmp_path):
+    """reference test_engine.cpp:376-407: 3 steps + save + load into a
+    differently seeded store + 3 steps == 6 uninterrupted steps."""
+    c = E.ModelConfig(4, 32, 64, 32, 16, 2, k_ckpt=2)
+    hp = E.HyperParams(lr=2e-3)
+    opts = E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=3)
+    full = E.Store(c, 77)
+    lf = full.run_training(hp, 77, 6, opts)
+    part = E.Store(c, 77)
+    l1 = part.run_training(hp, 77, 3, opts)
+    part.save(tmp_path / "ck.hlm2")
+    resumed = E.Store(c, 1)
+    resumed.load(tmp_path / "ck.hlm2")
+    l2 = resumed.run_training(hp, 77, 3, opts)
+    assert resumed.bitwise_equal(full)
+    assert list(l1) + list(l2) == list(lf)
+
+
+@pytest.mark.parametrize("kw", [dict(k=1), dict(k=3), dict(k=1, cache=2), dict(k=1, tail=True),
+                                dict(k=2, fused=False)])
+def test_measured_traces_validate(kw):
+    from paper_2602_04816_b200.trace import validate_trace
+    c = E.ModelConfig(6, 32, 64, 32, 16, 2, k_ckpt=kw.get("k", 1))
+    blk = (2 * c.block_params() + 255) // 256 * 256
+    a = E.Arena(c, weight_cache_bytes=kw.get("cache", 0) * blk)
+    opts = E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=6,
+                           overlap_optimizer_tail=kw.get("tail", False), tail_blocks=2,
+                           fused_recompute=kw.get("fused", True))
+    e = E.Engine(E.Store(c, 3), a, E.HyperParams(), opts)
+    for i in range(3):
+        e.train_step(E.make_copy_task_batch(c, 1, skip=i))
+    e.sync()
+    v = validate_trace(e.last_trace(), c.layers)
+    assert v == [], v[:5]

@@ -105,3 +105,21 @@ def test_footprint_is_depth_invariant_except_anchors():
 def test_train_rejects_unknown_keys():
     with pytest.raises(E.HlmConfigError):
         E.train({"model": {}, "bogus": 1})
+
+
+def test_checkpoint_roundtrip_and_geometry_checks(tmp_path):
+    c = E.ModelConfig(2, 16, 32, 13, 4, 1)
+    s = E.Store(c, 3, "fp32", pin=False)
+    rng = np.random.default_rng(0)
+    for t in (1, 2):
+        s.adam_step((rng.standard_normal(s.total_params) * 1e-2).astype(np.float32), E.HyperParams(), t)
+    p = tmp_path / "a.hlm2"
+    s.save(p)
+    r = E.Store(c, 99, "bf16", pin=False)
+    r.load(p)
+    assert r.bitwise_equal(s) and r.adam_steps == 2
+    with pytest.raises(E.HlmConfigError, match="geometry"):
+        E.Store(E.ModelConfig(3, 16, 32, 13, 4, 1), 1, pin=False).load(p)
+    (tmp_path / "bad").write_bytes(b"HLM1xxxxxxxx")
+    with pytest.raises(E.HlmConfigError, match="not an HLM2"):
+        r.load(tmp_path / "bad")
