@@ -320,16 +320,29 @@ int hlm_cuda_rope_table(float* dev_cos, float* dev_sin, int64_t seq, int64_t hea
 // ------------------------------------------------------------------ head + loss
 static i64 padded_vocab(i64 V) { return (V + 7) / 8 * 8; }
 
+// Rows per head chunk: logits (fp32) + d_logits (bf16) of one chunk fit in
+// ~kHeadChunkBytes, so the (T, V) buffers of the reference never exist whole.
+static const int64_t kHeadChunkBytes = 2ll << 30;
+static i64 head_chunk_rows(i64 rows, i64 vocab) {
+  i64 r = kHeadChunkBytes / (6 * padded_vocab(vocab));
+  r = r / 128 * 128;
+  if (r < 128) r = 128;
+  return r < rows ? r : rows;
+}
+
 size_t hlm_cuda_head_ws_bytes(int64_t rows, int64_t hidden, int64_t vocab) {
   Carver c(nullptr);
-  const i64 ldv = padded_vocab(vocab);
+  const i64 ldv = padded_vocab(vocab), cr = head_chunk_rows(rows, vocab);
   c.take<uint16_t>(rows * hidden);
-  c.take<float>(rows * ldv);
-  c.take<uint16_t>(rows * ldv);
+  c.take<float>(cr * ldv);
+  c.take<uint16_t>(cr * ldv);
   c.take<int>(4);
   return c.off;
 }
 
+// Chunked over rows: per chunk, logits = x_c . head^T (fp32), CE -> d_logits_c
+// (bf16), d_x_c = d_logits_c . head, d_head (+)= d_logits_c^T . x_c (the first
+// chunk stores or accumulates per the caller, later chunks accumulate).
 int hlm_cuda_head_loss(int64_t rows, int64_t hidden, int64_t vocab, const void* head, const float* x,
                        const int32_t* targets, float inv_rows, float* d_x, float* d_head, int accumulate_d_head,
                        float* loss_rows, void* ws, void* stream) {
@@ -337,24 +350,29 @@ int hlm_cuda_head_loss(int64_t rows, int64_t hidden, int64_t vocab, const void* 
     if (rows <= 0 || hidden <= 0 || vocab <= 0 || hidden % 8)
       throw Failure{"head: bad dims (hidden must be a multiple of 8)", HLM_ERR_CONFIG};
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const i64 ldv = padded_vocab(vocab);
+    const i64 ldv = padded_vocab(vocab), cr = head_chunk_rows(rows, vocab);
     Carver c(ws);
     uint16_t* x_bf = c.take<uint16_t>(rows * hidden);
-    float* logits = c.take<float>(rows * ldv);
-    uint16_t* dl = c.take<uint16_t>(rows * ldv);
+    float* logits = c.take<float>(cr * ldv);
+    uint16_t* dl = c.take<uint16_t>(cr * ldv);
     int* err = c.take<int>(4);
-    const int R = (int)rows, Hh = (int)hidden, V = (int)vocab;
+    const int Hh = (int)hidden, V = (int)vocab;
     chk(hlm_ops_cast_bf16(x, x_bf, rows * hidden, s), "cast x");
-    chk_gemm(gdesc(R, V, Hh, x_bf, hidden, 0, head, hidden, 0, logits, ldv, HLM_EPI_F32), s, "head fwd");
-    chk(hlm_ops_ce(logits, ldv, targets, dl, ldv, loss_rows, rows, V, inv_rows, err, s), "cross entropy");
-    chk_gemm(gdesc(R, Hh, V, dl, ldv, 0, head, hidden, 1, d_x, hidden, HLM_EPI_F32), s, "head dgrad");
-    HlmGemmDesc g = gdesc(V, Hh, R, dl, ldv, 1, x_bf, hidden, 1, d_head, hidden,
-                          accumulate_d_head ? HLM_EPI_F32_ADD : HLM_EPI_F32);
-    if (accumulate_d_head) {
-      g.R = d_head;
-      g.ldr = hidden;
+    for (i64 r0 = 0; r0 < rows; r0 += cr) {
+      const i64 n = rows - r0 < cr ? rows - r0 : cr;
+      const int R = (int)n;
+      const uint16_t* xc = x_bf + r0 * hidden;
+      chk_gemm(gdesc(R, V, Hh, xc, hidden, 0, head, hidden, 0, logits, ldv, HLM_EPI_F32), s, "head fwd");
+      chk(hlm_ops_ce(logits, ldv, targets + r0, dl, ldv, loss_rows + r0, n, V, inv_rows, err, s), "cross entropy");
+      chk_gemm(gdesc(R, Hh, V, dl, ldv, 0, head, hidden, 1, d_x + r0 * hidden, hidden, HLM_EPI_F32), s, "head dgrad");
+      const bool acc = accumulate_d_head || r0 > 0;
+      HlmGemmDesc g = gdesc(V, Hh, R, dl, ldv, 1, xc, hidden, 1, d_head, hidden, acc ? HLM_EPI_F32_ADD : HLM_EPI_F32);
+      if (acc) {
+        g.R = d_head;
+        g.ldr = hidden;
+      }
+      chk_gemm(g, s, "head wgrad");
     }
-    chk_gemm(g, s, "head wgrad");
   });
 }
 

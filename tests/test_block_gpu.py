@@ -155,3 +155,30 @@ def test_head_loss_and_embedding_match_oracle():
     assert abs(loss - loss_ref) / loss_ref < 1e-3
     assert rel_l2(dhead.cpu().numpy().ravel(), g_ref[off + nb:]) < REL_GRAD
     assert rel_l2(dtab.cpu().numpy().ravel(), g_ref[:off]) < REL_GRAD
+
+
+def test_head_loss_is_chunked_and_matches_torch():
+    """T*V large enough for several row chunks (2 GiB of logits + d_logits per
+    chunk): loss, d_x and the chunk-accumulated d_head vs an fp32 torch reference."""
+    Lb = L.blib()
+    dev = "cuda"
+    T, h, V = 8192, 256, 152064
+    torch.manual_seed(0)
+    x = torch.randn(T, h, device=dev)
+    head = (torch.randn(V, h, device=dev) * 0.02).bfloat16()
+    tgt = torch.randint(0, V, (T,), device=dev, dtype=torch.int32)
+    ws = torch.empty(Lb.hlm_cuda_head_ws_bytes(T, h, V), dtype=torch.uint8, device=dev)
+    assert ws.numel() < 3 * (1 << 30)      # never the whole (T, V) fp32 + bf16 pair (7.5 GB)
+    dx = torch.empty(T, h, device=dev)
+    dhead = torch.empty(V, h, device=dev)
+    loss_rows = torch.empty(T, device=dev)
+    L.check(Lb.hlm_cuda_head_loss(T, h, V, vp(head), vp(x), vp(tgt), 1.0 / T, vp(dx), vp(dhead), 0,
+                                  vp(loss_rows), vp(ws), None))
+    torch.cuda.synchronize()
+    xb = x.bfloat16().float().requires_grad_(True)
+    hf = head.float().requires_grad_(True)
+    loss = torch.nn.functional.cross_entropy(xb @ hf.t(), tgt.long())
+    loss.backward()
+    assert abs(loss_rows.double().sum().item() - loss.item()) < 1e-3 * loss.item()
+    assert rel_l2(dx.cpu().numpy(), xb.grad.cpu().numpy()) < 2e-2
+    assert rel_l2(dhead.cpu().numpy(), hf.grad.cpu().numpy()) < 2e-2
