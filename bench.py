@@ -266,6 +266,13 @@ def run_ours(args, m, name):
 
     t_roof = max(nums["hw_flops"] / (tf_sus * 1e12), nums["h2d"] / (PCIE_ASSUMED_GBS * 1e9),
                  nums["d2h"] / (PCIE_ASSUMED_GBS * 1e9))
+    # host DRAM roofline: every parameter moves 30 B through the host Adam (g, w, m, v in;
+    # w, m, v, bf16 shadow out) + 4 B of gradient DMA written + 2 B per weight DMA pass read
+    lib.hlm_host_triad_gbs.restype = ctypes.c_double
+    lib.hlm_host_triad_gbs.argtypes = [ctypes.c_int64, ctypes.c_int]
+    host_bw = lib.hlm_host_triad_gbs(1 << 30, 3) if rank == 0 else None
+    host_bytes = nums["params"] * 34 + h2d_step
+    t_host = host_bytes / (host_bw * 1e9) if host_bw else None
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -307,6 +314,10 @@ def run_ours(args, m, name):
                      "traffic": None, "ms_per_launch": ms_launch.value},
         "step_roofline": {"t_roof_s": t_roof, "t_step_s": step_s, "frac": t_roof / step_s,
                           "def": "max(HW_FLOPS/sustained bf16, H2D/55GB/s, D2H/55GB/s)"},
+        "host_roofline": {"host_bytes_per_step": int(host_bytes), "triad_gbs": host_bw,
+                          "t_host_s": t_host, "frac": (t_host / step_s) if t_host else None,
+                          "def": "(34 B/param host Adam + gradient DMA, + weight DMA bytes) / "
+                                 "measured 16-thread STREAM triad"},
         "stream": {"h2d_gbs": h2d_gbs, "d2h_gbs": d2h_gbs, "overlap": overlap,
                    "gpu_busy_s": gpu_busy_s, "host_adam_s": adam_s,
                    "h2d_bytes_measured": int(h2d_step), "trace_violations": len(violations)},

@@ -270,6 +270,9 @@ void adam_step_range(LayerTile& tile, const float* grad, i64 begin, i64 count, c
 // grads(tile) += g  (slab accumulation, host_store.cpp:254-284, FP32).
 void accumulate_grads(LayerTile& tile, const float* g);
 
+// Anonymous huge-page-advised mapping (throws on failure).
+void* map_huge_public(size_t bytes);
+
 // True when every element is finite (parallel scan).
 bool all_finite(const float* g, i64 n);
 

@@ -267,6 +267,10 @@ int hlm_engine_debug_hidden(HlmEngine* e, float* out);
 /* JSONL of the last step's measured trace; *needed = bytes incl. NUL */
 int hlm_engine_last_trace(HlmEngine* e, char* buf, size_t cap, size_t* needed);
 
+/* Host DRAM bandwidth probe (all OpenMP threads): STREAM triad a = b + s*c over
+ * three arrays of `bytes_per_array`, best of `reps`; GB/s counting 3 arrays. */
+double hlm_host_triad_gbs(int64_t bytes_per_array, int reps);
+
 /* HLM2 checkpoint of the host store (master, m, v, Adam step count); load
  * re-derives the BF16 shadow and rejects mismatched geometry (HLM_ERR_CONFIG). */
 int hlm_store_save(const HlmStore* s, const char* path);

@@ -81,6 +81,8 @@ std::uint64_t mix64(std::uint64_t x) {   // splitmix64 finaliser
 
 }  // namespace
 
+void* map_huge_public(size_t bytes) { return map_huge(bytes); }
+
 // ------------------------------------------------------------------ offset tables
 std::vector<NamedRegion> block_offset_table(i64 h, i64 f) {
     std::vector<NamedRegion> t;
@@ -619,3 +621,28 @@ void accumulate_grads(LayerTile& tile, const float* g) {
 }
 
 }  // namespace hlm
+
+extern "C" double hlm_host_triad_gbs(int64_t bytes_per_array, int reps) {
+    const hlm::i64 n = bytes_per_array / 4;
+    float* a = static_cast<float*>(hlm::map_huge_public(static_cast<size_t>(n) * 4));
+    float* b = static_cast<float*>(hlm::map_huge_public(static_cast<size_t>(n) * 4));
+    float* c = static_cast<float*>(hlm::map_huge_public(static_cast<size_t>(n) * 4));
+#pragma omp parallel for schedule(static)
+    for (hlm::i64 i = 0; i < n; ++i) {
+        a[i] = 0.f;
+        b[i] = 1.f;
+        c[i] = 2.f;
+    }
+    double best = 0;
+    for (int r = 0; r < reps; ++r) {
+        const auto t0 = std::chrono::steady_clock::now();
+#pragma omp parallel for schedule(static)
+        for (hlm::i64 i = 0; i < n; ++i) a[i] = b[i] + 0.5f * c[i];
+        const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        best = std::max(best, 3.0 * static_cast<double>(n) * 4 / dt / 1e9);
+    }
+    munmap(a, static_cast<size_t>(n) * 4);
+    munmap(b, static_cast<size_t>(n) * 4);
+    munmap(c, static_cast<size_t>(n) * 4);
+    return best;
+}
