@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "attention.h"
 #include "block_ops.h"
@@ -573,6 +574,13 @@ bool hlm_flash_supported(int head_dim, int seq) { return (head_dim == 64 || head
 
 int hlm_flash_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int B, int S, int H, int hd,
                   int ld, cudaStream_t s) {
+  // tcgen05 path unless HLM_ATTN_MMA_SYNC=1 (A/B comparisons)
+  static int mma_sync = -1;
+  if (mma_sync < 0) {
+    const char* e = getenv("HLM_ATTN_MMA_SYNC");
+    mma_sync = (e && *e == '1') ? 1 : 0;
+  }
+  if (!mma_sync && hlm_flash_tc_supported(hd, S, ld)) return hlm_flash_fwd_tc(q, k, v, o, lse, B, S, H, ld, s);
   if (hd == 128) return fwd_impl<128>(q, k, v, o, lse, B, S, H, ld, s);
   if (hd == 64) return fwd_impl<64>(q, k, v, o, lse, B, S, H, ld, s);
   return 2;

@@ -1,0 +1,27 @@
+"""Causal attention forward / backward timing at the C2 shape (B8 S2048 H28 hd128)."""
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2602_04816_b200 import _lib as L
+Lb = L.blib()
+B, S, H, hd = 8, 2048, 28, 128
+h, T = H * hd, B * S
+dev = "cuda"
+q, k, v, do = (torch.randn(T, h, device=dev).bfloat16() for _ in range(4))
+o = torch.empty_like(q); lse = torch.empty(B * H * S, device=dev)
+dq, dk, dv = (torch.empty_like(q) for _ in range(3)); ds = torch.empty_like(lse)
+d = L.HlmBlockDims(B, S, h, 8, H, 0)
+vp = lambda t: ctypes.c_void_p(t.data_ptr())
+fwd = lambda: L.check(Lb.hlm_cuda_attention_fwd(ctypes.byref(d), vp(q), vp(k), vp(v), vp(o), vp(lse), h, None))
+bwd = lambda: L.check(Lb.hlm_cuda_attention_bwd(ctypes.byref(d), vp(q), vp(k), vp(v), vp(o), vp(do), vp(lse), vp(ds), vp(dq), vp(dk), vp(dv), h, None))
+def t(fn, it=10):
+    for _ in range(3): fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(True), torch.cuda.Event(True)
+    a.record()
+    for _ in range(it): fn()
+    b.record(); torch.cuda.synchronize()
+    return a.elapsed_time(b) / it
+fl = 2.0 * B * S * S * h   # causal fwd: QK^T and PV over the lower triangle
+tf = t(fwd); tb = t(bwd)
+print(f"fwd {tf:.3f} ms = {fl/tf/1e9:.0f} TFLOP/s ; bwd {tb:.3f} ms = {2.5*fl/tb/1e9:.0f} TFLOP/s (2.5x fwd flops)")
