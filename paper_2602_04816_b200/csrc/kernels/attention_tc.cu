@@ -30,11 +30,11 @@ namespace {
 constexpr int TQ = 128, TK = 128, HD = 128;
 constexpr int TILE_BYTES = TQ * HD * 2;            // 32 KiB
 constexpr int ATOM_BYTES = 128 * 64 * 2;           // 16 KiB: 128 rows x 64 cols
-constexpr int SMEM_BYTES = TILE_BYTES * 6 + 1024 + 512;   // Q, K0 V0 K1 V1, P
+constexpr int SMEM_BYTES = TILE_BYTES * 7 + 1024 + 256;   // Q, K0 V0 K1 V1, P0 P1
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct Bars {
-  uint64_t q_full, kv_full[2], kv_empty[2], s_full[2], s_free[2], p_full, o_full[2], o_free[2];
+  uint64_t q_full, kv_full[2], kv_empty[2], s_full[2], s_free[2], p_full[2], o_full[2], o_free[2];
   uint32_t tmem;
 };
 
@@ -65,8 +65,8 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* sQ = smem;
   uint8_t* sK[2] = {smem + TILE_BYTES, smem + 3 * TILE_BYTES};
   uint8_t* sV[2] = {smem + 2 * TILE_BYTES, smem + 4 * TILE_BYTES};
-  uint8_t* sP = smem + 5 * TILE_BYTES;
-  Bars* bars = reinterpret_cast<Bars*>(smem + 6 * TILE_BYTES);
+  uint8_t* sP[2] = {smem + 5 * TILE_BYTES, smem + 6 * TILE_BYTES};
+  Bars* bars = reinterpret_cast<Bars*>(smem + 7 * TILE_BYTES);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int qt = (int)(gridDim.x - 1 - blockIdx.x);   // long (late) query tiles first
@@ -87,8 +87,8 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&bars->s_free[i], 4);
       mbar_init(&bars->o_full[i], 1);
       mbar_init(&bars->o_free[i], 4);
+      mbar_init(&bars->p_full[i], 4);
     }
-    mbar_init(&bars->p_full, 4);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(&bars->tmem);
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp == 1) {
     constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false, false);
     constexpr uint32_t idesc_o = make_idesc_bf16(128, 128, false, true);
-    const uint32_t q_base = smem_u32(sQ), p_base = smem_u32(sP);
+    const uint32_t q_base = smem_u32(sQ);
     mbar_wait(&bars->q_full, 0);
     auto issue_s = [&](int j) {
       const int st = j & 1;
@@ -136,11 +136,12 @@ __global__ void __launch_bounds__(256, 1)
     for (int j = 0; j < n_tiles; ++j) {
       const int st = j & 1;
       if (j + 1 < n_tiles) issue_s(j + 1);
-      mbar_wait(&bars->p_full, j & 1);
+      mbar_wait(&bars->p_full[st], (j >> 1) & 1);
       mbar_wait(&bars->o_free[st], ((j >> 1) & 1) ^ 1);
       tc_fence_after();
       if (lane == 0) {
         const uint32_t v_base = smem_u32(sV[st]);
+        const uint32_t p_base = smem_u32(sP[st]);
 #pragma unroll
         for (int kk = 0; kk < TK / 16; ++kk)
           umma_bf16(tmem + 256 + st * 128, kmajor_desc(p_base, kk), mnmajor_desc(v_base, kk), idesc_o, kk ? 1u : 0u);
@@ -157,8 +158,24 @@ __global__ void __launch_bounds__(256, 1)
     float oacc[HD];
 #pragma unroll
     for (int i = 0; i < HD; ++i) oacc[i] = 0.f;
-    float m = -INFINITY, l = 0.f;
-    uint8_t* prow = sP + r * 128;
+    float m = -INFINITY, l = 0.f, alpha_prev = 1.f;
+    // O_acc <- alpha * O_acc + O_j (TMEM O[jj % 2]), then release that O buffer
+    auto fold = [&](int jj, float alpha) {
+      const int so = jj & 1;
+      mbar_wait(&bars->o_full[so], (jj >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32(tmem + 256 + so * 128 + c * 32 + lane_off, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) oacc[c * 32 + e] = oacc[c * 32 + e] * alpha + __uint_as_float(v[e]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->o_free[so]);
+    };
     for (int j = 0; j < n_tiles; ++j) {
       const int st = j & 1;
       const bool diag = j == qt;
@@ -179,8 +196,9 @@ __global__ void __launch_bounds__(256, 1)
       }
       const float alpha = exp2f(m - mx);
       m = mx;
-      // the previous P must have been consumed by PV_{j-1} before it is overwritten
-      if (j > 0) mbar_wait(&bars->o_full[(j - 1) & 1], ((j - 1) >> 1) & 1);
+      // P[st] was last read by PV_{j-2}
+      if (j >= 2) mbar_wait(&bars->o_full[st], ((j - 2) >> 1) & 1);
+      uint8_t* prow = sP[st] + r * 128;
       // pass 2: p = exp2(s - m), row sum, bf16 P into the swizzled K-major tile
       float rs = 0.f;
 #pragma unroll 1
@@ -198,8 +216,7 @@ __global__ void __launch_bounds__(256, 1)
           rs += p0 + p1;
           pk[e / 2] = pack_bf16x2(p0, p1);
         }
-        // keys c*32 .. c*32+31: atom (c/2), 16-byte chunks (c%2)*4 .. +3
-        const int atom = c >> 1;
+        const int atom = c >> 1;   // keys c*32 .. c*32+31: atom (c/2), 16-byte chunks (c%2)*4 .. +3
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) {
           const int chunk = (c & 1) * 4 + q4;
@@ -213,23 +230,13 @@ __global__ void __launch_bounds__(256, 1)
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&bars->s_free[st]);
-        mbar_arrive(&bars->p_full);
+        mbar_arrive(&bars->p_full[st]);
       }
-      // O_acc = alpha * O_acc + P_j V_j
-      mbar_wait(&bars->o_full[st], (j >> 1) & 1);
-      tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < HD / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32(tmem + 256 + st * 128 + c * 32 + lane_off, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 32; ++e) oacc[c * 32 + e] = oacc[c * 32 + e] * alpha + __uint_as_float(v[e]);
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars->o_free[st]);
+      // fold the previous tile while PV_j runs on the tensor core
+      if (j >= 1) fold(j - 1, alpha_prev);
+      alpha_prev = alpha;
     }
+    fold(n_tiles - 1, alpha_prev);
     const float il = 1.f / l;
     __nv_bfloat16* orow = o + (long long)(row0 + qpos) * ld + col0;
 #pragma unroll
