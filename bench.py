@@ -172,6 +172,7 @@ def run_ours(args, m, name):
         import torch.distributed as dist
         dist.init_process_group("gloo")
     lib = _lib.blib()
+    E.set_device(local)   # before pinning, communicators and the arena
     import ctypes
     lib.hlm_timer_record.argtypes = [ctypes.c_int]
     lib.hlm_timer_elapsed_ms.restype = ctypes.c_double

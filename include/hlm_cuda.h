@@ -49,6 +49,9 @@ enum HlmGemmErr {
 
 const char* hlm_cuda_last_error(void);
 
+/* Select this process's GPU (call before creating stores, communicators or arenas). */
+int hlm_cuda_set_device(int device);
+
 /* Number of CUDA kernels this library has launched since it was loaded. */
 long long hlm_cuda_launch_count(void);
 

@@ -20,3 +20,12 @@ extern "C" int hlm_cuda_gemm(const HlmGemmDesc* desc, void* stream) {
 }
 
 extern "C" long long hlm_cuda_launch_count(void) { return hlm_launches_total(); }
+
+extern "C" int hlm_cuda_set_device(int device) {
+  const cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    hlm_capi::set_error(std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    return HLM_ERR_CUDA;
+  }
+  return HLM_OK;
+}

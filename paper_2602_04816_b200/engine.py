@@ -246,6 +246,12 @@ class Store:
         return _L().hlm_store_tile_version(self.h, p)
 
 
+def set_device(device):
+    """Bind this process to a GPU; call first in every data-parallel rank."""
+    _L().hlm_cuda_set_device.argtypes = [ctypes.c_int]
+    _check(_L().hlm_cuda_set_device(device))
+
+
 def nccl_unique_id():
     buf = ctypes.create_string_buffer(128)
     _check(_L().hlm_nccl_unique_id(buf))
