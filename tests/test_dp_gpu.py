@@ -33,3 +33,52 @@ def test_dp_world1_nccl_paths_match_single_process_engine():
     assert l0 == l1
     assert ref.bitwise_equal(s)
     del e1
+
+
+def _dp_rank(rank, world, port, name, out_dir):
+    import torch.distributed as dist
+    from paper_2602_04816_b200 import engine as E
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    E.set_device(rank)
+    uids = [E.nccl_unique_id(), E.nccl_unique_id()] if rank == 0 else [None, None]
+    dist.broadcast_object_list(uids, src=0)
+    cg, cw = E.nccl_comm(uids[0], world, rank), E.nccl_comm(uids[1], world, rank)
+    c = E.ModelConfig(3, 64, 128, 96, 32, 2, n_heads=1)               # local micro-batch
+    g = E.ModelConfig(3, 64, 128, 96, 32, 2 * world, n_heads=1)       # global batch
+    s = E.Store(c, 11, shared=name, rank=rank, world=world)
+    e = E.Engine(s, E.Arena(c, device=rank), E.HyperParams(lr=2e-3),
+                 E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=4, rank=rank,
+                                 world=world, comm_grad=cg, comm_weights=cw))
+    rows = c.rows
+    losses = [e.train_step(E.make_copy_task_batch(g, 5, skip=i)[rank * rows:(rank + 1) * rows]).loss
+              for i in range(3)]
+    e.sync()
+    dist.barrier()
+    if rank == 0:
+        np.save(os.path.join(out_dir, "w.npy"), s.weights())
+        np.save(os.path.join(out_dir, "l.npy"), np.array(losses))
+    dist.barrier()
+    del e
+
+
+@pytest.mark.skipif(not __import__("torch").cuda.is_available() or
+                    __import__("torch").cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_dp_two_gpus_matches_global_batch():
+    """2 ranks x local batch == 1 process x global batch (loss scaled by 1/global rows,
+    gradients reduce-scattered): losses within fp32 summation-order tolerance."""
+    import socket
+    import tempfile
+    import torch.multiprocessing as mp
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    out = tempfile.mkdtemp()
+    mp.start_processes(_dp_rank, args=(2, port, f"hlm_dp2_{os.getpid()}", out), nprocs=2,
+                       start_method="spawn")
+    g = E.ModelConfig(3, 64, 128, 96, 32, 4, n_heads=1)
+    ref = E.Store(g, 11)
+    e = E.Engine(ref, E.Arena(g), E.HyperParams(lr=2e-3), E.EngineOptions(eager_optim=True))
+    l_ref = [e.train_step(E.make_copy_task_batch(g, 5, skip=i)).loss for i in range(3)]
+    l_dp = np.load(os.path.join(out, "l.npy"))
+    assert np.allclose(l_dp, l_ref, rtol=1e-4)
+    w = np.load(os.path.join(out, "w.npy"))
+    assert np.linalg.norm(w - ref.weights()) / np.linalg.norm(ref.weights()) < 1e-3
