@@ -161,9 +161,8 @@ def run_reference(args, m, name):
 def run_ours(args, m, name):
     rank, world, local = dist_env()
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
-    if world > 1 and "OMP_NUM_THREADS" not in os.environ:
-        # ranks share the host cores for their shard of the Adam
-        os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or 16) // local_world))
+    # ranks on one host split its cores for their shard of the Adam (init keeps all cores)
+    adam_threads = max(1, (os.cpu_count() or 16) // local_world) if world > 1 else 0
     from paper_2602_04816_b200 import _lib
     from paper_2602_04816_b200 import engine as E
 
@@ -204,7 +203,7 @@ def run_ours(args, m, name):
     opts = E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=args.slabs,
                            record_trace=True, overlap_optimizer_tail=args.tail_blocks >= 0,
                            tail_blocks=max(0, args.tail_blocks), rank=rank, world=world,
-                           comm_grad=comm_g, comm_weights=comm_w)
+                           comm_grad=comm_g, comm_weights=comm_w, host_threads=adam_threads)
     eng = E.Engine(store, arena, E.HyperParams(lr=1e-4), opts)
     setup_s = time.time() - t0
     # one global token stream (reference RNG, global batch = world x local), sliced by rank

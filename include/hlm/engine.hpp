@@ -59,6 +59,9 @@ struct EngineOptions {
     int world = 1;
     void* comm_grad = nullptr;      // ncclComm_t
     void* comm_weights = nullptr;   // ncclComm_t, optional
+    // OpenMP threads of the host optimizer worker (0 = OpenMP default). Ranks sharing
+    // a host split its cores; initialisation elsewhere keeps every core.
+    int host_threads = 0;
 };
 
 struct StepResult {

@@ -205,6 +205,7 @@ typedef struct HlmEngineOptions {
   int32_t world;
   void* comm_grad;
   void* comm_weights;
+  int32_t host_threads;  /* OpenMP threads of the optimizer worker (0 = default) */
 } HlmEngineOptions;
 
 typedef struct HlmStepResult {

@@ -107,6 +107,7 @@ hlm::EngineOptions to_opts(const HlmEngineOptions* o) {
         e.world = o->world > 0 ? o->world : 1;
         e.comm_grad = o->comm_grad;
         e.comm_weights = o->comm_weights;
+        e.host_threads = o->host_threads;
     }
     return e;
 }

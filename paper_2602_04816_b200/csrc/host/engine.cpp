@@ -6,6 +6,7 @@
 #include "hlm/engine.hpp"
 
 #include <cuda_runtime.h>
+#include <omp.h>
 
 #include <algorithm>
 #include <chrono>
@@ -428,6 +429,7 @@ void Engine::process_oldest_inline() {
 }
 
 void Engine::worker_loop() {
+    if (opts_.host_threads > 0) omp_set_num_threads(opts_.host_threads);
     for (;;) {
         Pending p;
         {
