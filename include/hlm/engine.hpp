@@ -62,6 +62,15 @@ struct EngineOptions {
     // OpenMP threads of the host optimizer worker (0 = OpenMP default). Ranks sharing
     // a host split its cores; initialisation elsewhere keeps every core.
     int host_threads = 0;
+    // HBM-resident optimizer tiles (eager, K == 1, single process, untied): the
+    // embedding (resident_embed) and blocks 1..resident_blocks keep FP32 master, m, v
+    // and their BF16 weights in device memory for the engine's lifetime. Their
+    // weights are never streamed and their gradients never leave the GPU (finiteness
+    // scan + device Adam, bit-identical to the host Adam, right after the backward).
+    // These are the tiles the next forward needs first and the host Adam would
+    // finish last. sync() (and the destructor) copies them back into the store.
+    i64 resident_blocks = 0;
+    bool resident_embed = false;
 };
 
 struct StepResult {
@@ -180,6 +189,21 @@ private:
     std::vector<i64> cache_slot_of_;       // per logical tile, -1 when not cached
     std::vector<i64> cache_xfer_op_;       // per slot: this step's WeightXfer op, -1 if not resident
     std::vector<void*> ev_cache_ready_;
+    struct Resident {
+        i64 tile;          // logical tile id
+        i64 n;
+        float* state;      // device [master | m | v]
+        uint16_t* w16;     // device bf16 weights
+    };
+    std::vector<i64> resident_of_;         // per logical tile: index into residents_ or -1
+    std::vector<Resident> residents_;
+    void* resident_mem_ = nullptr;
+    unsigned long long* resident_bad_ = nullptr;   // device: per resident tile, first non-finite index
+    unsigned long long* resident_bad_host_ = nullptr;
+    bool resident_dirty_ = false;
+    bool is_resident(i64 tile) const { return resident_of_[static_cast<size_t>(tile)] >= 0; }
+    void resident_update(i64 tile, int gbuf, i64 dep_op);   // device finiteness scan + Adam
+    void sync_resident();
     i64 shard_elems(i64 n) const;          // n / world (throws unless divisible)
     void h2d_tile(void* dst, const LayerTile& tile, i64 bytes);
     double* loss_dev_ = nullptr;

@@ -150,6 +150,11 @@ int hlm_embed_csr(const int32_t* tokens, int64_t rows, int64_t vocab, int32_t* r
 
 /* ------------------------------------------------------------------ small ops */
 int hlm_cuda_cast_bf16(const float* in, void* out, int64_t n, void* stream);
+/* Adam on HBM-resident optimizer state (w, m, v fp32, w16 bf16 out) — bit-identical
+ * to the host Adam; skipped when *bad (device, from hlm_cuda_nonfinite) != ~0. */
+struct HlmHyper;
+int hlm_cuda_adam(float* w, float* m, float* v, void* w16, const float* g, int64_t n,
+                  const unsigned long long* bad, const struct HlmHyper* hp, int64_t t, void* stream);
 /* *first (device u64) := smallest index of a non-finite element of g, ~0 when all finite */
 int hlm_cuda_nonfinite(const float* g, int64_t n, unsigned long long* first, void* stream);
 
@@ -206,6 +211,10 @@ typedef struct HlmEngineOptions {
   void* comm_grad;
   void* comm_weights;
   int32_t host_threads;  /* OpenMP threads of the optimizer worker (0 = default) */
+  /* HBM-resident optimizer tiles: embedding + blocks 1..resident_blocks keep FP32
+   * master / m / v and BF16 weights on the GPU (device Adam, no streaming) */
+  int32_t resident_embed;
+  int64_t resident_blocks;
 } HlmEngineOptions;
 
 typedef struct HlmStepResult {

@@ -411,6 +411,19 @@ int hlm_embed_csr(const int32_t* tokens, int64_t rows, int64_t vocab, int32_t* r
 }
 
 // ------------------------------------------------------------------ small ops
+int hlm_cuda_adam(float* w, float* m, float* v, void* w16, const float* g, int64_t n, const unsigned long long* bad,
+                  const HlmHyper* hp, int64_t t, void* stream) {
+  return guarded([&] {
+    if (t < 1) throw Failure{"adam step index must be >= 1", HLM_ERR_PROTOCOL};
+    const float lr = (float)hp->lr, b1 = (float)hp->beta1, b2 = (float)hp->beta2, eps = (float)hp->eps,
+                wd = (float)hp->weight_decay;
+    const float bc1 = 1.0f - std::pow(b1, static_cast<float>(t));   // as the host (host_store.cpp)
+    const float bc2 = 1.0f - std::pow(b2, static_cast<float>(t));
+    chk(hlm_ops_adam_device(w, m, v, w16, g, n, bad, lr, b1, b2, eps, wd, bc1, bc2, static_cast<cudaStream_t>(stream)),
+        "adam device");
+  });
+}
+
 int hlm_cuda_nonfinite(const float* g, int64_t n, unsigned long long* first, void* stream) {
   return guarded([&] { chk(hlm_ops_nonfinite(g, n, first, static_cast<cudaStream_t>(stream)), "nonfinite"); });
 }

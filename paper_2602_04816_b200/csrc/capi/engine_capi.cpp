@@ -108,6 +108,8 @@ hlm::EngineOptions to_opts(const HlmEngineOptions* o) {
         e.comm_grad = o->comm_grad;
         e.comm_weights = o->comm_weights;
         e.host_threads = o->host_threads;
+        e.resident_embed = o->resident_embed != 0;
+        e.resident_blocks = o->resident_blocks;
     }
     return e;
 }

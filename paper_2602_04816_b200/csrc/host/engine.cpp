@@ -108,6 +108,34 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
     }
     for (i64 p = 0; p < store_.physical_tiles(); ++p)
         target_version_.push_back(store_.physical(p).min_version());
+    // HBM-resident optimizer tiles
+    resident_of_.assign(static_cast<size_t>(m.tile_count()), -1);
+    const bool resident_ok = opts_.eager_optim && !opts_.skip_optimizer && opts_.world == 1 && !opts_.comm_grad &&
+                             !m.tie_embeddings && m.k_ckpt == 1 && opts_.fused_recompute;
+    if (resident_ok && (opts_.resident_embed || opts_.resident_blocks > 0)) {
+        std::vector<i64> ids;
+        if (opts_.resident_embed) ids.push_back(m.embed_tile_id());
+        for (i64 l = 1; l <= std::min(opts_.resident_blocks, m.layers); ++l) ids.push_back(l);
+        size_t bytes = 0;
+        for (i64 id : ids) bytes += static_cast<size_t>((store_.tile(id).n_params() * 14 + 255) / 256 * 256);
+        ck(cudaMalloc(&resident_mem_, bytes), "cudaMalloc resident optimizer tiles");
+        ck(cudaMalloc(&resident_bad_, ids.size() * 8), "cudaMalloc resident flags");
+        ck(cudaHostAlloc(reinterpret_cast<void**>(&resident_bad_host_), ids.size() * 8, cudaHostAllocPortable),
+           "cudaHostAlloc resident flags");
+        char* q = static_cast<char*>(resident_mem_);
+        for (i64 id : ids) {
+            LayerTile& t = store_.tile(id);
+            Resident r{id, t.n_params(), reinterpret_cast<float*>(q),
+                       reinterpret_cast<uint16_t*>(q + 12 * t.n_params())};
+            ck(cudaMemcpy(r.state, t.master(), static_cast<size_t>(12 * r.n), cudaMemcpyHostToDevice),
+               "upload resident state");
+            ck(cudaMemcpy(r.w16, t.shadow(), static_cast<size_t>(2 * r.n), cudaMemcpyHostToDevice),
+               "upload resident weights");
+            resident_of_[static_cast<size_t>(id)] = static_cast<i64>(residents_.size());
+            residents_.push_back(r);
+            q += (t.n_params() * 14 + 255) / 256 * 256;
+        }
+    }
     if (opts_.threaded_accum) worker_ = std::thread([this] { worker_loop(); });
 }
 
@@ -116,6 +144,9 @@ Engine::~Engine() {
         sync();
     } catch (...) {
     }
+    if (resident_mem_) cudaFree(resident_mem_);
+    if (resident_bad_) cudaFree(resident_bad_);
+    if (resident_bad_host_) cudaFreeHost(resident_bad_host_);
     {
         std::lock_guard<std::mutex> lk(mu_);
         stop_ = true;
@@ -417,6 +448,28 @@ void Engine::consume(const Pending& p) {
 
 bool Engine::eligible(const Pending&) const { return true; }
 
+// Gradient of a resident tile: GPU finiteness scan, then the device Adam (no-op
+// on a flagged gradient; finish_step raises NumericsError). Stream-ordered on
+// the compute stream before any later reader of the tile's weights.
+void Engine::resident_update(i64 tile, int gbuf, i64 dep_op) {
+    const i64 ri = resident_of_[static_cast<size_t>(tile)];
+    const Resident& r = residents_[static_cast<size_t>(ri)];
+    StreamOp op;
+    op.stream = StreamId::Compute;
+    op.kind = OpKind::OptStep;
+    op.layer = tile;
+    op.params = r.n;
+    op.deps.push_back(dep_op);
+    const i64 id = op_begin(op, compute_);
+    ck_hlm(hlm_cuda_nonfinite(arena_.grad_out(gbuf), r.n, resident_bad_ + ri, compute_), "nonfinite (resident)");
+    HlmHyper hp{hyper_.lr, hyper_.beta1, hyper_.beta2, hyper_.eps, hyper_.weight_decay};
+    ck_hlm(hlm_cuda_adam(r.state, r.state + r.n, r.state + 2 * r.n, r.w16, arena_.grad_out(gbuf), r.n,
+                         resident_bad_ + ri, &hp, step_t_, compute_),
+           "device adam");
+    op_end(id, compute_);
+    resident_dirty_ = true;
+}
+
 void Engine::process_oldest_inline() {
     Pending p;
     {
@@ -497,7 +550,19 @@ void Engine::rethrow_worker_error() {
     if (e) std::rethrow_exception(e);
 }
 
+void Engine::sync_resident() {
+    if (!resident_dirty_) return;
+    ck(cudaStreamSynchronize(S(compute_)), "sync compute");
+    for (const auto& r : residents_) {
+        LayerTile& t = store_.tile(r.tile);
+        ck(cudaMemcpy(t.master(), r.state, static_cast<size_t>(12 * r.n), cudaMemcpyDeviceToHost), "download state");
+        ck(cudaMemcpy(t.shadow(), r.w16, static_cast<size_t>(2 * r.n), cudaMemcpyDeviceToHost), "download weights");
+    }
+    resident_dirty_ = false;
+}
+
 void Engine::sync() {
+    sync_resident();
     if (!opts_.threaded_accum) return;
     {
         std::unique_lock<std::mutex> lk(mu_);
@@ -588,28 +653,34 @@ void Engine::forward_streaming() {
     const float* rc = m.rope_theta > 0 ? arena_.rope_cos() : nullptr;
     const float* rs = m.rope_theta > 0 ? arena_.rope_sin() : nullptr;
 
-    i64 w_op = 0;
-    const int ebuf = stream_tile(m.embed_tile_id(), &w_op);
-    compute_wait_weights(ebuf);
+    i64 w_op = -1;
+    const bool embed_res = is_resident(m.embed_tile_id());
+    const int ebuf = embed_res ? -2 : stream_tile(m.embed_tile_id(), &w_op);
+    if (!embed_res) compute_wait_weights(ebuf);
     float* h0 = arena_.anchor_checkpoint(0);
     StreamOp op;
     op.stream = StreamId::Compute;
     op.kind = OpKind::Forward;
     op.layer = m.embed_tile_id();
-    op.buf = ebuf;
+    op.buf = ebuf;   // -2: HBM-resident weights
     op.flops = fwd_flops(m.embed_params(), T);
-    op.deps.push_back(w_op);
+    if (w_op >= 0) op.deps.push_back(w_op);
     i64 id = op_begin(op, compute_);
-    ck_hlm(hlm_cuda_embed_fwd(arena_.tokens(), weights_ptr(ebuf), h0, T, m.hidden, m.vocab, arena_.err_flag(),
-                              compute_),
+    const void* etab = embed_res ? static_cast<const void*>(residents_[static_cast<size_t>(resident_of_[0])].w16)
+                                 : weights_ptr(ebuf);
+    ck_hlm(hlm_cuda_embed_fwd(arena_.tokens(), etab, h0, T, m.hidden, m.vocab, arena_.err_flag(), compute_),
            "embed_fwd");
     op_end(id, compute_);
-    compute_done_with(ebuf, id);
+    if (!embed_res) compute_done_with(ebuf, id);
     h_cur_ = h0;
     int roll = 0;
     for (i64 i = 1; i <= m.layers; ++i) {
-        const int buf = stream_tile(i, &w_op, true);
-        compute_wait_weights(buf);
+        const bool res = is_resident(i);
+        w_op = -1;
+        const int buf = res ? -2 : stream_tile(i, &w_op, true);
+        if (!res) compute_wait_weights(buf);
+        const void* wptr = res ? static_cast<const void*>(residents_[static_cast<size_t>(resident_of_[static_cast<size_t>(i)])].w16)
+                               : weights_ptr(buf);
         float* out = (i % m.k_ckpt == 0) ? arena_.anchor_checkpoint(i) : arena_.h_roll(roll);
         if (i % m.k_ckpt != 0) roll ^= 1;
         StreamOp bo;
@@ -618,13 +689,13 @@ void Engine::forward_streaming() {
         bo.layer = i;
         bo.buf = buf;
         bo.flops = fwd_flops(m.block_params(), T);
-        bo.deps.push_back(w_op);
+        if (w_op >= 0) bo.deps.push_back(w_op);
         id = op_begin(bo, compute_);
-        ck_hlm(hlm_cuda_block_fwd(&dims, weights_ptr(buf), h_cur_, out, arena_.discard_acts(), arena_.block_ws(), rc,
-                                  rs, compute_),
+        ck_hlm(hlm_cuda_block_fwd(&dims, wptr, h_cur_, out, arena_.discard_acts(), arena_.block_ws(), rc, rs,
+                                  compute_),
                "block_fwd");
         op_end(id, compute_);
-        compute_done_with(buf, id);
+        if (!res) compute_done_with(buf, id);
         h_cur_ = out;
     }
     phase_ = Phase::Anchor;
@@ -708,20 +779,22 @@ void Engine::backward_blockwise() {
         std::vector<const float*> inputs(static_cast<size_t>(hi - lo + 1));
         std::vector<void*> acts(static_cast<size_t>(hi - lo + 1));
         if (fused) {
-            i64 w_op = 0;
-            const int buf = stream_tile(lo, &w_op);
-            compute_wait_weights(buf);
+            i64 w_op = -1;
+            const bool res = is_resident(lo);
+            const int buf = res ? -2 : stream_tile(lo, &w_op);
+            if (!res) compute_wait_weights(buf);
+            const void* wptr = res ? static_cast<const void*>(residents_[static_cast<size_t>(resident_of_[static_cast<size_t>(lo)])].w16)
+                                   : weights_ptr(buf);
             void* a = arena_.push_acts();
             StreamOp rop;
             rop.stream = StreamId::Compute;
             rop.kind = OpKind::Recompute;
             rop.layer = lo;
-            rop.buf = buf;
+            rop.buf = buf;   // -2: HBM-resident weights
             rop.flops = fwd_flops(n_block, T);
-            rop.deps.push_back(w_op);
+            if (w_op >= 0) rop.deps.push_back(w_op);
             i64 id = op_begin(rop, compute_);
-            ck_hlm(hlm_cuda_block_fwd(&dims, weights_ptr(buf), anchor, arena_.h_roll(0), a, arena_.block_ws(), rc, rs,
-                                      compute_),
+            ck_hlm(hlm_cuda_block_fwd(&dims, wptr, anchor, arena_.h_roll(0), a, arena_.block_ws(), rc, rs, compute_),
                    "block_fwd (recompute)");
             op_end(id, compute_);
             ++recompute_forwards_;
@@ -732,15 +805,18 @@ void Engine::backward_blockwise() {
             bop.layer = lo;
             bop.buf = buf;
             bop.flops = bwd_flops(n_block, T);
-            bop.deps.push_back(w_op);
+            if (w_op >= 0) bop.deps.push_back(w_op);
             const i64 lb = op_begin(bop, compute_);
-            ck_hlm(hlm_cuda_block_bwd(&dims, weights_ptr(buf), anchor, a, arena_.g_roll(g_cur_),
-                                      arena_.g_roll(g_cur_ ^ 1), arena_.grad_out(gb), arena_.block_ws(), rc, rs,
-                                      compute_),
+            ck_hlm(hlm_cuda_block_bwd(&dims, wptr, anchor, a, arena_.g_roll(g_cur_), arena_.g_roll(g_cur_ ^ 1),
+                                      arena_.grad_out(gb), arena_.block_ws(), rc, rs, compute_),
                    "block_bwd");
             op_end(lb, compute_);
-            compute_done_with(buf, lb);
-            evacuate(lo, gb, n_block, lb);
+            if (res) {
+                resident_update(lo, gb, lb);
+            } else {
+                compute_done_with(buf, lb);
+                evacuate(lo, gb, n_block, lb);
+            }
             arena_.pop_acts();
             g_cur_ ^= 1;
         } else {
@@ -826,7 +902,10 @@ void Engine::backward_blockwise() {
                               m.vocab, m.hidden, 0, compute_),
            "embed_bwd");
     op_end(lb, compute_);
-    evacuate(m.embed_tile_id(), gb, n_embed, lb);
+    if (is_resident(m.embed_tile_id()))
+        resident_update(m.embed_tile_id(), gb, lb);
+    else
+        evacuate(m.embed_tile_id(), gb, n_embed, lb);
     phase_ = Phase::Optimize;
 }
 
@@ -840,6 +919,14 @@ StepResult Engine::finish_step() {
     ck(cudaStreamSynchronize(S(compute_)), "sync compute");
     ck(cudaStreamSynchronize(S(d2h_)), "sync d2h");
     ck(cudaStreamSynchronize(S(h2d_)), "sync h2d");
+    if (!residents_.empty()) {
+        ck(cudaMemcpy(resident_bad_host_, resident_bad_, residents_.size() * 8, cudaMemcpyDeviceToHost),
+           "D2H resident flags");
+        for (size_t i = 0; i < residents_.size(); ++i)
+            if (resident_bad_host_[i] != ~0ull)
+                throw NumericsError("non-finite gradient in layer " + std::to_string(residents_[i].tile) +
+                                    " at element " + std::to_string(resident_bad_host_[i]) + "; step aborted");
+    }
     const int err = loss_host_[3 * T];
     if (err & 1) throw std::out_of_range("embed_fwd: token id out of range (device)");
     if (err & 2) throw std::out_of_range("ce_loss_and_grad: target id out of range (device)");

@@ -328,6 +328,33 @@ __global__ void nonfinite_kernel(const float* __restrict__ g, long long n, unsig
   }
 }
 
+// ------------------------------------------------------------------ device Adam
+// Reference adam_update_tile (host_store.cpp:334-362) for HBM-resident optimizer
+// tiles: every operation an IEEE-rounded intrinsic in the host kernel's order (no
+// FMA contraction), so results equal the host Adam bit for bit. Skipped entirely
+// when the gradient scan flagged a non-finite element (no mutation, as the host).
+__global__ void adam_device_kernel(float* __restrict__ w, float* __restrict__ m, float* __restrict__ v,
+                                   __nv_bfloat16* __restrict__ w16, const float* __restrict__ g, long long n,
+                                   const unsigned long long* __restrict__ bad, float lr, float b1, float b2,
+                                   float omb1, float omb2, float eps, float wd, float bc1, float bc2) {
+  if (*bad != ~0ull) return;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float gv = g[i];
+    const float mm = __fadd_rn(__fmul_rn(b1, m[i]), __fmul_rn(omb1, gv));
+    const float vv = __fadd_rn(__fmul_rn(b2, v[i]), __fmul_rn(__fmul_rn(omb2, gv), gv));
+    const float mhat = __fdiv_rn(mm, bc1);
+    const float vhat = __fdiv_rn(vv, bc2);
+    float th = w[i];
+    const float upd = __fadd_rn(__fdiv_rn(mhat, __fadd_rn(__fsqrt_rn(vhat), eps)), __fmul_rn(wd, th));
+    th = __fsub_rn(th, __fmul_rn(lr, upd));
+    m[i] = mm;
+    v[i] = vv;
+    w[i] = th;
+    w16[i] = __float2bfloat16_rn(th);
+  }
+}
+
 // ------------------------------------------------------------------ generic attention
 // Causal softmax attention for any head_dim <= 32*VPL: one warp per
 // (batch, head, query row), online softmax over keys j <= i in fp32.
@@ -533,6 +560,15 @@ int hlm_ops_fill_random_bf16(void* p, long long n, unsigned seed, cudaStream_t s
 int hlm_ops_nonfinite(const float* g, long long n, unsigned long long* first, cudaStream_t s) {
   cudaMemsetAsync(first, 0xFF, sizeof(unsigned long long), s);
   nonfinite_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, s>>>(g, n, first);
+  hlm_count_launches(1);
+  HLM_CHECK_LAUNCH();
+}
+
+int hlm_ops_adam_device(float* w, float* m, float* v, void* w16, const float* g, long long n,
+                        const unsigned long long* bad, float lr, float b1, float b2, float eps, float wd, float bc1,
+                        float bc2, cudaStream_t s) {
+  adam_device_kernel<<<grid_for(n, 256), 256, 0, s>>>(w, m, v, (__nv_bfloat16*)w16, g, n, bad, lr, b1, b2, 1.0f - b1,
+                                                       1.0f - b2, eps, wd, bc1, bc2);
   hlm_count_launches(1);
   HLM_CHECK_LAUNCH();
 }

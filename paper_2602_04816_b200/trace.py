@@ -28,6 +28,8 @@ GPU_STREAMS = ("h2d", "compute", "d2h")
 
 
 def _consumes_weights(op, embed_tile):
+    if op["buf"] == -2:          # HBM-resident optimizer tile: weights never streamed
+        return False
     if op["kind"] in ("Forward", "Recompute"):
         return True
     return op["kind"] == "LocalBackward" and op["layer"] != embed_tile
@@ -88,7 +90,7 @@ def validate_trace(ops, n_layers, embed_tile=0, head_tile=None, n_stream_buffers
                     out.append(Violation(op["id"], "buffer-free",
                                          f"missing dependency on buffer_free[{b}] (reader op {reader[b]})"))
             into[b], reader[b], consumed[b] = op["id"], -1, False
-        elif 0 <= b < n_stream_buffers and op["stream"] == "compute":
+        elif 0 <= b < n_stream_buffers and op["stream"] == "compute" and op["kind"] != "OptStep":
             reader[b], consumed[b] = op["id"], True
 
     group, used = [], 0

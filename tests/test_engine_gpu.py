@@ -295,3 +295,29 @@ def test_measured_traces_validate(kw):
     e.sync()
     v = validate_trace(e.last_trace(), c.layers)
     assert v == [], v[:5]
+
+
+@pytest.mark.parametrize("res", [dict(resident_embed=True, resident_blocks=2),
+                                 dict(resident_blocks=6), dict(resident_embed=True)])
+def test_hbm_resident_optimizer_tiles_are_bitwise_neutral(res):
+    """Embedding / first blocks optimised on the GPU from HBM-resident FP32 state:
+    same losses and, after sync(), the same store bit for bit as the host Adam."""
+    from paper_2602_04816_b200.trace import validate_trace
+    c = E.ModelConfig(6, 32, 64, 32, 16, 2, k_ckpt=1, n_heads=2, rope_theta=1e4)
+    toks = [E.make_copy_task_batch(c, 4, skip=i) for i in range(3)]
+    ref = E.Store(c, 8)
+    e0 = E.Engine(ref, E.Arena(c), E.HyperParams(lr=2e-3, weight_decay=0.01),
+                  E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=4))
+    l0 = [e0.train_step(t).loss for t in toks]
+    s = E.Store(c, 8)
+    e1 = E.Engine(s, E.Arena(c), E.HyperParams(lr=2e-3, weight_decay=0.01),
+                  E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=4,
+                                  overlap_optimizer_tail=True, tail_blocks=1, **res))
+    l1 = [e1.train_step(t) for t in toks]
+    assert validate_trace(e1.last_trace(), c.layers) == []
+    e1.sync()
+    assert l0 == [r.loss for r in l1]
+    assert ref.bitwise_equal(s)
+    streamed = 2 * (c.vocab * c.hidden * (0 if res.get("resident_embed") else 1) +
+                    c.vocab * c.hidden + 2 * (c.layers - res.get("resident_blocks", 0)) * c.block_params())
+    assert l1[-1].h2d_bytes == streamed
