@@ -211,7 +211,8 @@ private:
     unsigned long long* nf_host_ = nullptr;   // pinned mirror
     std::vector<char> deferred_;           // per logical tile: optimised in the tail
     std::vector<i64> target_version_;      // per physical tile: version the next H2D needs
-    bool tail_open_ = true;                // embed of the current step processed (mu_)
+    bool tail_open_ = true;                // every regular tile of this step processed (mu_)
+    i64 regular_left_ = 0;                 // host (non-deferred, non-resident) tiles still to consume (mu_)
     i64 step_index_ = 0;
 
     // worker

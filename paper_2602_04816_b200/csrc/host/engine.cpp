@@ -443,7 +443,7 @@ void Engine::consume(const Pending& p) {
     pool_->release(p.slab);
     std::lock_guard<std::mutex> lk(mu_);
     host_ops_.push_back(rec);
-    if (p.layer == store_.config().embed_tile_id() && p.step == step_index_) tail_open_ = true;
+    if (p.step == step_index_ && !deferred_[static_cast<size_t>(p.layer)] && --regular_left_ == 0) tail_open_ = true;
 }
 
 bool Engine::eligible(const Pending&) const { return true; }
@@ -615,7 +615,10 @@ void Engine::begin_step(const Batch& batch) {
     {
         std::lock_guard<std::mutex> lk(mu_);
         ++step_index_;
-        tail_open_ = !opts_.overlap_optimizer_tail;
+        regular_left_ = 0;
+        for (i64 t = 0; t < m.tile_count(); ++t)
+            if (!deferred_[static_cast<size_t>(t)] && resident_of_[static_cast<size_t>(t)] < 0) ++regular_left_;
+        tail_open_ = !opts_.overlap_optimizer_tail || regular_left_ == 0;
         if (!opts_.overlap_optimizer_tail) pending_.clear();
         host_ops_.clear();
         consumers_left_.assign(static_cast<size_t>(store_.physical_tiles()), 0);
