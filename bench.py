@@ -203,7 +203,8 @@ def run_ours(args, m, name):
     opts = E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=args.slabs,
                            record_trace=True, overlap_optimizer_tail=args.tail_blocks >= 0,
                            tail_blocks=max(0, args.tail_blocks), rank=rank, world=world,
-                           comm_grad=comm_g, comm_weights=comm_w, host_threads=adam_threads)
+                           comm_grad=comm_g, comm_weights=comm_w, host_threads=adam_threads,
+                           resident_embed=args.resident_embed, resident_blocks=args.resident_blocks)
     eng = E.Engine(store, arena, E.HyperParams(lr=1e-4), opts)
     setup_s = time.time() - t0
     # one global token stream (reference RNG, global batch = world x local), sliced by rank
@@ -305,7 +306,9 @@ def run_ours(args, m, name):
                    "tokens_per_step": nums["T"] * world, "params": nums["params"],
                    "parallelism": f"dp{world}" if world > 1 else "single-gpu",
                    "n_heads": m["n_heads"], "k_ckpt": 1, "l2": "inputs larger than L2 (weights "
-                   "streamed from host every step)"},
+                   "streamed from host every step)",
+                   "hbm_resident_optimizer": {"embed": bool(args.resident_embed),
+                                              "blocks": args.resident_blocks}},
         "tflops": nums["model_flops"] / step_s / 1e12,
         "hw_tflops": nums["hw_flops"] / step_s / 1e12,
         "e2e": {"value": e2e, "unit": "tokens/s",
@@ -351,6 +354,10 @@ def main():
     ap.add_argument("--cache-gb", type=float, default=60.0,
                     help="HBM weight cache (block tiles resident between forward and backward)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--resident-blocks", type=int, default=0,
+                    help="blocks 1..N keep FP32 master + Adam state in HBM (device Adam, no streaming)")
+    ap.add_argument("--resident-embed", action="store_true",
+                    help="the embedding table keeps FP32 master + Adam state in HBM")
     ap.add_argument("--force-dp", action="store_true",
                     help="use the data-parallel code path (NCCL, shared store) even at world 1")
     ap.add_argument("--dump-trace", default="", help="write the last warm-up step's measured trace (JSONL)")
