@@ -94,9 +94,12 @@ public:
     Engine& operator=(const Engine&) = delete;
 
     StepResult train_step(const Batch& batch);
-    // Waits until every pending host optimizer update has been applied (the
-    // store is consistent); a no-op unless overlap_optimizer_tail is on.
+    // Waits until every pending host optimizer update has been applied and copies
+    // HBM-resident optimizer tiles back into the store: the store is consistent.
     void sync();
+    // Waits for the host optimizer only (no resident write-back): the end of a
+    // training step's work when timing.
+    void wait_optimizer();
 
     void begin_step(const Batch& batch);
     void forward_streaming();

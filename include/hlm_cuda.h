@@ -268,8 +268,11 @@ int hlm_engine_create(HlmStore* s, HlmArena* a, const HlmHyper* hp, const HlmEng
                       HlmEngine** out);
 void hlm_engine_destroy(HlmEngine* e);
 int hlm_engine_train_step(HlmEngine* e, const int32_t* tokens, const int32_t* targets, HlmStepResult* out);
-/* wait for every pending host optimizer update (store consistent afterwards) */
+/* wait for every pending host optimizer update and copy HBM-resident optimizer
+ * tiles back (store consistent afterwards) */
 int hlm_engine_sync(HlmEngine* e);
+/* wait for the host optimizer only (end of the training work; no write-back) */
+int hlm_engine_wait_optimizer(HlmEngine* e);
 /* phase API (reference engine.hpp:62-66); out-of-order calls -> HLM_ERR_PROTOCOL */
 int hlm_engine_begin_step(HlmEngine* e, const int32_t* tokens, const int32_t* targets);
 int hlm_engine_forward(HlmEngine* e);

@@ -342,6 +342,10 @@ int hlm_engine_sync(HlmEngine* e) {
     return guarded([&] { e->e->sync(); });
 }
 
+int hlm_engine_wait_optimizer(HlmEngine* e) {
+    return guarded([&] { e->e->wait_optimizer(); });
+}
+
 int hlm_engine_begin_step(HlmEngine* e, const int32_t* tokens, const int32_t* targets) {
     return guarded([&] { e->e->begin_step(to_batch(e->e->store().config(), tokens, targets)); });
 }

@@ -562,7 +562,11 @@ void Engine::sync_resident() {
 }
 
 void Engine::sync() {
+    wait_optimizer();
     sync_resident();
+}
+
+void Engine::wait_optimizer() {
     if (!opts_.threaded_accum) return;
     {
         std::unique_lock<std::mutex> lk(mu_);

@@ -157,6 +157,7 @@ def _L():
         L.hlm_engine_destroy.argtypes = [_vp]
         L.hlm_engine_train_step.argtypes = [_vp, _i32p, _i32p, P(StepResult)]
         L.hlm_engine_sync.argtypes = [_vp]
+        L.hlm_engine_wait_optimizer.argtypes = [_vp]
         L.hlm_engine_begin_step.argtypes = [_vp, _i32p, _i32p]
         L.hlm_engine_forward.argtypes = [_vp]
         L.hlm_engine_anchor_loss.argtypes = [_vp, P(ctypes.c_double)]
@@ -313,7 +314,12 @@ class Engine:
         return r
 
     def sync(self):
+        """Host optimizer drained + HBM-resident tiles written back: store consistent."""
         _check(_L().hlm_engine_sync(self.h))
+
+    def wait_optimizer(self):
+        """Host optimizer drained (the end of the training work of the last step)."""
+        _check(_L().hlm_engine_wait_optimizer(self.h))
 
     def begin_step(self, tokens, targets=None):
         targets = tokens if targets is None else targets
