@@ -14,3 +14,5 @@ int hlm_flash_bwd(const void* q, const void* k, const void* v, const void* o, co
 bool hlm_flash_tc_supported(int head_dim, int seq, int ld);
 int hlm_flash_fwd_tc(const void* q, const void* k, const void* v, void* o, float* lse, int B, int S, int H, int ld,
                      cudaStream_t s);
+int hlm_flash_bwd_tc(const void* q, const void* k, const void* v, const void* d_o, const float* lse,
+                     const float* dsum, void* dq, void* dk, void* dv, int B, int S, int H, int ld, cudaStream_t s);

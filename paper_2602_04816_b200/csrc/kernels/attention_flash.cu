@@ -524,6 +524,16 @@ __global__ void dsum_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bflo
   if (lane == 0) dsum[((long long)b * H + hh) * S + i] = s;
 }
 
+// tcgen05 kernels (attention_tc.cu) unless HLM_ATTN_MMA_SYNC=1 (A/B comparisons)
+bool use_tc() {
+  static int mma_sync = -1;
+  if (mma_sync < 0) {
+    const char* e = getenv("HLM_ATTN_MMA_SYNC");
+    mma_sync = (e && *e == '1') ? 1 : 0;
+  }
+  return !mma_sync;
+}
+
 template <int HD>
 int fwd_impl(const void* q, const void* k, const void* v, void* o, float* lse, int B, int S, int H, int ld,
              cudaStream_t s) {
@@ -556,6 +566,10 @@ int bwd_impl(const void* q, const void* k, const void* v, const void* o, const v
   const long long warps = (long long)B * H * S;
   dsum_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dout,
                                                           dsum, B, S, H, HD, ld);
+  if (use_tc() && hlm_flash_tc_supported(HD, S, ld)) {
+    hlm_count_launches(1);
+    return hlm_flash_bwd_tc(q, k, v, dout, lse, dsum, dq, dk, dv, B, S, H, ld, s);
+  }
   dim3 grid(S / BR, B * H);
   flash_bwd_dq<HD><<<grid, NW * 32, smem_dq, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
                                                   (const __nv_bfloat16*)v, (const __nv_bfloat16*)dout, lse, dsum,
@@ -574,13 +588,7 @@ bool hlm_flash_supported(int head_dim, int seq) { return (head_dim == 64 || head
 
 int hlm_flash_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int B, int S, int H, int hd,
                   int ld, cudaStream_t s) {
-  // tcgen05 path unless HLM_ATTN_MMA_SYNC=1 (A/B comparisons)
-  static int mma_sync = -1;
-  if (mma_sync < 0) {
-    const char* e = getenv("HLM_ATTN_MMA_SYNC");
-    mma_sync = (e && *e == '1') ? 1 : 0;
-  }
-  if (!mma_sync && hlm_flash_tc_supported(hd, S, ld)) return hlm_flash_fwd_tc(q, k, v, o, lse, B, S, H, ld, s);
+  if (use_tc() && hlm_flash_tc_supported(hd, S, ld)) return hlm_flash_fwd_tc(q, k, v, o, lse, B, S, H, ld, s);
   if (hd == 128) return fwd_impl<128>(q, k, v, o, lse, B, S, H, ld, s);
   if (hd == 64) return fwd_impl<64>(q, k, v, o, lse, B, S, H, ld, s);
   return 2;

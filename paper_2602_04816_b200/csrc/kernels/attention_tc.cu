@@ -254,6 +254,333 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+
+// ------------------------------------------------------------------ backward
+// Shared pieces: a 128-row bf16 tile written by 128 threads (thread = row) into
+// the K-major SW128 layout the MMA A operand expects (two 64-column atoms).
+__device__ __forceinline__ void store_row_kmajor(uint8_t* tile, int r, int c, const uint32_t (&pk)[16]) {
+  // columns c*32 .. c*32+31 of row r: atom c/2, 16-byte chunks (c%2)*4 .. +3
+  uint8_t* row = tile + (c >> 1) * ATOM_BYTES + r * 128;
+#pragma unroll
+  for (int q4 = 0; q4 < 4; ++q4) {
+    const int chunk = (c & 1) * 4 + q4;
+    *reinterpret_cast<uint4*>(row + ((chunk ^ (r & 7)) << 4)) =
+        make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
+  }
+}
+
+__device__ __forceinline__ void store_acc_row(__nv_bfloat16* dst, uint32_t taddr, float scale) {
+#pragma unroll 1
+  for (int c = 0; c < HD / 32; ++c) {
+    uint32_t v[32];
+    tmem_ld_32x32(taddr + c * 32, v);
+    tmem_ld_wait();
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      reinterpret_cast<uint4*>(dst + c * 32)[q] =
+          make_uint4(pack_bf16x2(__uint_as_float(v[8 * q]) * scale, __uint_as_float(v[8 * q + 1]) * scale),
+                     pack_bf16x2(__uint_as_float(v[8 * q + 2]) * scale, __uint_as_float(v[8 * q + 3]) * scale),
+                     pack_bf16x2(__uint_as_float(v[8 * q + 4]) * scale, __uint_as_float(v[8 * q + 5]) * scale),
+                     pack_bf16x2(__uint_as_float(v[8 * q + 6]) * scale, __uint_as_float(v[8 * q + 7]) * scale));
+  }
+}
+
+// dK, dV for one 128-key tile: loop over query tiles i >= kt.
+//   TMEM: S^T [0,128) dP^T [128,256) dV [256,384) dK [384,512)
+//   smem: K, V (fixed), Q_i, dO_i, P^T, dS^T (bf16, K-major), lse2/D of tile i
+struct BwdKVBars {
+  uint64_t kv_full, qd_full, qd_empty, s_full, p_full, acc_full;
+  uint32_t tmem;
+};
+constexpr int BWD_KV_SMEM = TILE_BYTES * 6 + 1024 + 1024 + 256;
+
+__global__ void __launch_bounds__(256, 1)
+    flash_bwd_dkv_tc(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                     const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do,
+                     const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dk,
+                     __nv_bfloat16* __restrict__ dv, int S, int H, int ld, float scale, float scale_log2) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sK = smem, *sV = smem + TILE_BYTES, *sQ = smem + 2 * TILE_BYTES, *sdO = smem + 3 * TILE_BYTES,
+          *sPT = smem + 4 * TILE_BYTES, *sdST = smem + 5 * TILE_BYTES;
+  float* sL = reinterpret_cast<float*>(smem + 6 * TILE_BYTES);
+  float* sD = sL + 128;
+  BwdKVBars* bars = reinterpret_cast<BwdKVBars*>(smem + 6 * TILE_BYTES + 1024);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int kt = (int)blockIdx.x;        // key tile (early tiles have the longest loops: launched first)
+  const int nq = S / TQ;
+  const int bh = blockIdx.y, b = bh / H, hh = bh % H;
+  const int row0 = b * S, col0 = hh * HD;
+  if (threadIdx.x == 0) {
+    tma_prefetch(&map_q);
+    tma_prefetch(&map_k);
+    tma_prefetch(&map_v);
+    tma_prefetch(&map_do);
+    mbar_init(&bars->kv_full, 1);
+    mbar_init(&bars->qd_full, 1);
+    mbar_init(&bars->qd_empty, 1);
+    mbar_init(&bars->s_full, 1);
+    mbar_init(&bars->p_full, 4);
+    mbar_init(&bars->acc_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(&bars->tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&bars->kv_full, 2 * TILE_BYTES);
+      tma_load_2d(sK, &map_k, &bars->kv_full, col0, row0 + kt * TK);
+      tma_load_2d(sK + ATOM_BYTES, &map_k, &bars->kv_full, col0 + 64, row0 + kt * TK);
+      tma_load_2d(sV, &map_v, &bars->kv_full, col0, row0 + kt * TK);
+      tma_load_2d(sV + ATOM_BYTES, &map_v, &bars->kv_full, col0 + 64, row0 + kt * TK);
+      for (int i = kt; i < nq; ++i) {
+        const int it = i - kt;
+        mbar_wait(&bars->qd_empty, (it & 1) ^ 1);
+        mbar_arrive_expect_tx(&bars->qd_full, 2 * TILE_BYTES);
+        const int r = row0 + i * TQ;
+        tma_load_2d(sQ, &map_q, &bars->qd_full, col0, r);
+        tma_load_2d(sQ + ATOM_BYTES, &map_q, &bars->qd_full, col0 + 64, r);
+        tma_load_2d(sdO, &map_do, &bars->qd_full, col0, r);
+        tma_load_2d(sdO + ATOM_BYTES, &map_do, &bars->qd_full, col0 + 64, r);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_kk = make_idesc_bf16(128, 128, false, false);   // A K-major, B K-major
+    constexpr uint32_t idesc_kmn = make_idesc_bf16(128, 128, false, true);   // A K-major, B MN-major
+    const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV), q_base = smem_u32(sQ), do_base = smem_u32(sdO),
+                   pt_base = smem_u32(sPT), dst_base = smem_u32(sdST);
+    mbar_wait(&bars->kv_full, 0);
+    for (int i = kt; i < nq; ++i) {
+      const int it = i - kt;
+      mbar_wait(&bars->qd_full, it & 1);
+      tc_fence_after();
+      if (lane == 0) {
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          umma_bf16(tmem, kmajor_desc(k_base, kk), kmajor_desc(q_base, kk), idesc_kk, kk ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          umma_bf16(tmem + 128, kmajor_desc(v_base, kk), kmajor_desc(do_base, kk), idesc_kk, kk ? 1u : 0u);
+        umma_commit(&bars->s_full);
+      }
+      __syncwarp();
+      mbar_wait(&bars->p_full, it & 1);
+      tc_fence_after();
+      if (lane == 0) {
+#pragma unroll
+        for (int kk = 0; kk < TQ / 16; ++kk)
+          umma_bf16(tmem + 256, kmajor_desc(pt_base, kk), mnmajor_desc(do_base, kk), idesc_kmn,
+                    (it > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < TQ / 16; ++kk)
+          umma_bf16(tmem + 384, kmajor_desc(dst_base, kk), mnmajor_desc(q_base, kk), idesc_kmn,
+                    (it > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&bars->qd_empty);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) umma_commit(&bars->acc_full);
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int ew = warp - 4, r = ew * 32 + lane;   // key row within the tile
+    const int key = kt * TK + r;
+    const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
+    const float* L = lse + (long long)bh * S;
+    const float* Dr = dsum + (long long)bh * S;
+    for (int i = kt; i < nq; ++i) {
+      const int it = i - kt;
+      // lse (log2 units) and D of this query tile; the previous tile's readers are done
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      sL[r] = L[i * TQ + r] * kLog2e;
+      sD[r] = Dr[i * TQ + r];
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      mbar_wait(&bars->s_full, it & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < TQ / 32; ++c) {
+        uint32_t sv[32], dpv[32];
+        tmem_ld_32x32(tmem + c * 32 + lane_off, sv);
+        tmem_ld_32x32(tmem + 128 + c * 32 + lane_off, dpv);
+        tmem_ld_wait();
+        uint32_t pk[16], dk16[16];
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          float p[2], ds[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int qc = c * 32 + e + u, qpos = i * TQ + qc;
+            float pv = exp2f(__uint_as_float(sv[e + u]) * scale_log2 - sL[qc]);
+            if (key > qpos) pv = 0.f;
+            p[u] = pv;
+            ds[u] = pv * (__uint_as_float(dpv[e + u]) - sD[qc]);
+          }
+          pk[e / 2] = pack_bf16x2(p[0], p[1]);
+          dk16[e / 2] = pack_bf16x2(ds[0], ds[1]);
+        }
+        store_row_kmajor(sPT, r, c, pk);
+        store_row_kmajor(sdST, r, c, dk16);
+      }
+      tc_fence_before();
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->p_full);
+    }
+    mbar_wait(&bars->acc_full, 0);
+    tc_fence_after();
+    store_acc_row(dv + (long long)(row0 + key) * ld + col0, tmem + 256 + lane_off, 1.0f);
+    store_acc_row(dk + (long long)(row0 + key) * ld + col0, tmem + 384 + lane_off, scale);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+// dQ for one 128-query tile: loop over key tiles j <= qt (K/V double-buffered).
+//   TMEM: S [0,128) dP [128,256) dQ [256,384)
+struct BwdQBars {
+  uint64_t q_full, kv_full[2], kv_empty[2], s_full, ds_full, acc_full;
+  uint32_t tmem;
+};
+constexpr int BWD_Q_SMEM = TILE_BYTES * 7 + 1024 + 256;
+
+__global__ void __launch_bounds__(256, 1)
+    flash_bwd_dq_tc(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                    const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do,
+                    const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dq,
+                    int S, int H, int ld, float scale, float scale_log2) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sQ = smem, *sdO = smem + TILE_BYTES, *sdS = smem + 6 * TILE_BYTES;
+  // stage st: K at (2 + 2 st) tiles, V at (3 + 2 st) tiles
+  auto sK = [&](int st) { return smem + (2 + 2 * st) * TILE_BYTES; };
+  auto sV = [&](int st) { return smem + (3 + 2 * st) * TILE_BYTES; };
+  BwdQBars* bars = reinterpret_cast<BwdQBars*>(smem + 7 * TILE_BYTES);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int qt = (int)(gridDim.x - 1 - blockIdx.x);
+  const int bh = blockIdx.y, b = bh / H, hh = bh % H;
+  const int row0 = b * S, col0 = hh * HD;
+  const int n_tiles = qt + 1;
+  if (threadIdx.x == 0) {
+    tma_prefetch(&map_q);
+    tma_prefetch(&map_k);
+    tma_prefetch(&map_v);
+    tma_prefetch(&map_do);
+    mbar_init(&bars->q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars->kv_full[i], 1);
+      mbar_init(&bars->kv_empty[i], 1);
+    }
+    mbar_init(&bars->s_full, 1);
+    mbar_init(&bars->ds_full, 4);
+    mbar_init(&bars->acc_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(&bars->tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&bars->q_full, 2 * TILE_BYTES);
+      tma_load_2d(sQ, &map_q, &bars->q_full, col0, row0 + qt * TQ);
+      tma_load_2d(sQ + ATOM_BYTES, &map_q, &bars->q_full, col0 + 64, row0 + qt * TQ);
+      tma_load_2d(sdO, &map_do, &bars->q_full, col0, row0 + qt * TQ);
+      tma_load_2d(sdO + ATOM_BYTES, &map_do, &bars->q_full, col0 + 64, row0 + qt * TQ);
+      for (int j = 0; j < n_tiles; ++j) {
+        const int st = j & 1;
+        mbar_wait(&bars->kv_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&bars->kv_full[st], 2 * TILE_BYTES);
+        const int r = row0 + j * TK;
+        tma_load_2d(sK(st), &map_k, &bars->kv_full[st], col0, r);
+        tma_load_2d(sK(st) + ATOM_BYTES, &map_k, &bars->kv_full[st], col0 + 64, r);
+        tma_load_2d(sV(st), &map_v, &bars->kv_full[st], col0, r);
+        tma_load_2d(sV(st) + ATOM_BYTES, &map_v, &bars->kv_full[st], col0 + 64, r);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_kk = make_idesc_bf16(128, 128, false, false);
+    constexpr uint32_t idesc_kmn = make_idesc_bf16(128, 128, false, true);
+    const uint32_t q_base = smem_u32(sQ), do_base = smem_u32(sdO), ds_base = smem_u32(sdS);
+    mbar_wait(&bars->q_full, 0);
+    for (int j = 0; j < n_tiles; ++j) {
+      const int st = j & 1;
+      mbar_wait(&bars->kv_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t k_base = smem_u32(sK(st)), v_base = smem_u32(sV(st));
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          umma_bf16(tmem, kmajor_desc(q_base, kk), kmajor_desc(k_base, kk), idesc_kk, kk ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          umma_bf16(tmem + 128, kmajor_desc(do_base, kk), kmajor_desc(v_base, kk), idesc_kk, kk ? 1u : 0u);
+        umma_commit(&bars->s_full);
+      }
+      __syncwarp();
+      mbar_wait(&bars->ds_full, j & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t k_base = smem_u32(sK(st));
+#pragma unroll
+        for (int kk = 0; kk < TK / 16; ++kk)
+          umma_bf16(tmem + 256, kmajor_desc(ds_base, kk), mnmajor_desc(k_base, kk), idesc_kmn,
+                    (j > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&bars->kv_empty[st]);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) umma_commit(&bars->acc_full);
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int ew = warp - 4, r = ew * 32 + lane;   // query row within the tile
+    const int qpos = qt * TQ + r;
+    const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
+    const float l2 = lse[(long long)bh * S + qpos] * kLog2e;
+    const float D = dsum[(long long)bh * S + qpos];
+    for (int j = 0; j < n_tiles; ++j) {
+      const bool diag = j == qt;
+      mbar_wait(&bars->s_full, j & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < TK / 32; ++c) {
+        uint32_t sv[32], dpv[32];
+        tmem_ld_32x32(tmem + c * 32 + lane_off, sv);
+        tmem_ld_32x32(tmem + 128 + c * 32 + lane_off, dpv);
+        tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          float ds[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            float pv = exp2f(__uint_as_float(sv[e + u]) * scale_log2 - l2);
+            if (diag && c * 32 + e + u > r) pv = 0.f;
+            ds[u] = pv * (__uint_as_float(dpv[e + u]) - D);
+          }
+          pk[e / 2] = pack_bf16x2(ds[0], ds[1]);
+        }
+        store_row_kmajor(sdS, r, c, pk);
+      }
+      tc_fence_before();
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->ds_full);
+    }
+    mbar_wait(&bars->acc_full, 0);
+    tc_fence_after();
+    store_acc_row(dq + (long long)(row0 + qpos) * ld + col0, tmem + 256 + lane_off, scale);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -297,5 +624,29 @@ int hlm_flash_fwd_tc(const void* q, const void* k, const void* v, void* o, float
   flash_fwd_tc<<<grid, 256, SMEM_BYTES, s>>>(mq, mk, mv, (__nv_bfloat16*)o, lse, S, H, ld,
                                              (1.0f / sqrtf((float)HD)) * kLog2e);
   hlm_count_launches(1);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+// D (rowsum dO . O) comes from the caller (dsum, computed by dsum_kernel in attention_flash.cu).
+int hlm_flash_bwd_tc(const void* q, const void* k, const void* v, const void* d_o, const float* lse,
+                     const float* dsum, void* dq, void* dk, void* dv, int B, int S, int H, int ld, cudaStream_t s) {
+  CUtensorMap mq, mk, mv, mdo;
+  const long long rows = (long long)B * S;
+  if (!make_map_2d(&mq, q, rows, ld) || !make_map_2d(&mk, k, rows, ld) || !make_map_2d(&mv, v, rows, ld) ||
+      !make_map_2d(&mdo, d_o, rows, ld))
+    return 3;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(flash_bwd_dkv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_KV_SMEM);
+    cudaFuncSetAttribute(flash_bwd_dq_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_Q_SMEM);
+    attr = true;
+  }
+  const float scale = 1.0f / sqrtf((float)HD);
+  dim3 grid(S / TQ, B * H);
+  flash_bwd_dkv_tc<<<grid, 256, BWD_KV_SMEM, s>>>(mq, mk, mv, mdo, lse, dsum, (__nv_bfloat16*)dk,
+                                                   (__nv_bfloat16*)dv, S, H, ld, scale, scale * kLog2e);
+  flash_bwd_dq_tc<<<grid, 256, BWD_Q_SMEM, s>>>(mq, mk, mv, mdo, lse, dsum, (__nv_bfloat16*)dq, S, H, ld, scale,
+                                                 scale * kLog2e);
+  hlm_count_launches(2);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }

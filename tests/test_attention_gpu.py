@@ -31,7 +31,7 @@ def rel(a, b):
     return ((a.float() - b.float()).norm() / b.float().norm()).item()
 
 
-@pytest.mark.parametrize("hd,H,S,B", [(128, 2, 256, 2), (64, 4, 128, 1), (128, 1, 64, 3), (32, 2, 64, 1)])
+@pytest.mark.parametrize("hd,H,S,B", [(128, 2, 256, 2), (128, 3, 640, 2), (64, 4, 128, 1), (128, 1, 64, 3), (32, 2, 64, 1)])
 @pytest.mark.parametrize("generic", [0, 1])
 def test_attention_fwd_bwd(hd, H, S, B, generic):
     torch.manual_seed(hd + S + generic)
