@@ -44,6 +44,39 @@ METRIC = "train_tokens_per_s"
 PCIE_ASSUMED_GBS = 55.0   # measured on the pool's box: pinned H2D 55.5 / D2H 55.8 GB/s
 
 
+
+def _mem_available():
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return None
+
+
+def pick_slabs(args, m, nums, world, local_world):
+    """Gradient slab count and optimizer tail. The host never idles while a
+    gradient is in flight, so the pool should hold a whole step's backlog of
+    block gradients (layers + 4 slabs: two widest-tile slabs for the embedding /
+    head, the rest block-sized), capped by the host memory left after the
+    store (16 GB reserve); the tail then covers every block."""
+    n_slab = args.slabs
+    if n_slab <= 0:
+        block = 4 * nums["n"] // world
+        wide = 4 * m["vocab"] * m["hidden"] // world
+        avail = _mem_available()
+        n_slab = m["layers"] + 4
+        if avail is not None:
+            budget = (avail - 16e9) / max(1, local_world) - 2 * max(wide, block)
+            n_slab = min(n_slab, 2 + int(budget // block))
+        n_slab = max(6, n_slab)
+    tail = args.tail_blocks
+    if tail == -2:
+        tail = min(m["layers"], n_slab - 3)
+    return n_slab, tail
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -200,9 +233,10 @@ def run_ours(args, m, name):
     blk = (2 * nums["n"] + 255) // 256 * 256
     cache = min(m["layers"], int(args.cache_gb * 1e9) // blk) * blk
     arena = E.Arena(cfg, device=local, weight_cache_bytes=cache)
-    opts = E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=args.slabs,
-                           record_trace=True, overlap_optimizer_tail=args.tail_blocks >= 0,
-                           tail_blocks=max(0, args.tail_blocks), rank=rank, world=world,
+    n_slab, tail = pick_slabs(args, m, nums, world, local_world)
+    opts = E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=n_slab,
+                           record_trace=True, overlap_optimizer_tail=tail >= 0,
+                           tail_blocks=max(0, tail), rank=rank, world=world,
                            comm_grad=comm_g, comm_weights=comm_w, host_threads=adam_threads,
                            resident_embed=args.resident_embed, resident_blocks=args.resident_blocks)
     eng = E.Engine(store, arena, E.HyperParams(lr=1e-4), opts)
@@ -255,7 +289,7 @@ def run_ours(args, m, name):
     violations = validate_trace(trace, m["layers"])
     host_ops = [o for o in trace if o["stream"] == "host" and o["kind"] == "OptStep"]
     adam_s = sum(o["t_end_us"] - o["t_start_us"] for o in host_ops) / 1e6
-    gpu_busy_s = float(np.mean(gpu_ms)) / 1e3
+    gpu_span_s = float(np.mean(gpu_ms)) / 1e3   # step-start .. step-end events on the compute stream
 
     hbm, tf_burst, tf_sus, peak_kind = peaks()
     # live roofline of the dominant kernel (tcgen05 GEMM) at the workload's block shapes
@@ -264,6 +298,15 @@ def run_ours(args, m, name):
     lib.hlm_cuda_bench_block_gemms(ctypes.byref(dims), 5, ctypes.byref(fl), ctypes.byref(ms_set),
                                    ctypes.byref(ms_launch))
     gemm_tflops = fl.value / (ms_set.value / 1e3) / 1e12
+    # DRAM bytes per launch of the same 12 GEMMs from the committed ncu --set full capture
+    tp = os.path.join(ROOT, "profiles", "r01_gemm_probe_traffic.json")
+    gemm_traffic = json.load(open(tp)) if os.path.exists(tp) and m["hidden"] == 3584 else {}
+    # elementwise / norm kernels: achieved HBM GB/s at the workload shape (HBM-bound)
+    ew_names = ("rmsnorm_fwd", "rmsnorm_bwd", "swiglu_fwd", "swiglu_bwd", "rope", "cast_bf16")
+    ew_gbs, ew_ms = (ctypes.c_double * 6)(), (ctypes.c_double * 6)()
+    lib.hlm_cuda_bench_block_ops(ctypes.byref(dims), 10, ew_gbs, ew_ms)
+    elementwise = {k: {"gbs": ew_gbs[i], "ms": ew_ms[i], "frac": ew_gbs[i] / hbm}
+                   for i, k in enumerate(ew_names)}
 
     t_roof = max(nums["hw_flops"] / (tf_sus * 1e12), nums["h2d"] / (PCIE_ASSUMED_GBS * 1e9),
                  nums["d2h"] / (PCIE_ASSUMED_GBS * 1e9))
@@ -307,6 +350,7 @@ def run_ours(args, m, name):
                    "parallelism": f"dp{world}" if world > 1 else "single-gpu",
                    "n_heads": m["n_heads"], "k_ckpt": 1, "l2": "inputs larger than L2 (weights "
                    "streamed from host every step)",
+                   "gradient_slabs": n_slab, "optimizer_tail_blocks": tail,
                    "hbm_resident_optimizer": {"embed": bool(args.resident_embed),
                                               "blocks": args.resident_blocks}},
         "tflops": nums["model_flops"] / step_s / 1e12,
@@ -318,7 +362,11 @@ def run_ours(args, m, name):
         "roofline": {"bound": "tensor", "kernel": "gemm_sm100 (tcgen05/TMA, 12 block launches)",
                      "achieved": gemm_tflops, "peak": tf_burst, "unit": "TFLOP/s",
                      "frac": gemm_tflops / tf_burst, "peak_kind": f"{peak_kind} burst",
-                     "traffic": None, "ms_per_launch": ms_launch.value},
+                     "traffic": gemm_traffic.get("dram_bytes_per_launch"),
+                     "algorithmic_bytes_per_launch": gemm_traffic.get("algorithmic_bytes_per_launch"),
+                     "traffic_source": gemm_traffic.get("source"), "ms_per_launch": ms_launch.value},
+        "elementwise_roofline": {"peak_gbs": hbm, "unit": "GB/s", "kernels": elementwise,
+                                 "def": "algorithmic bytes (each tensor read/written once) / CUDA-event time"},
         "step_roofline": {"t_roof_s": t_roof, "t_step_s": step_s, "frac": t_roof / step_s,
                           "def": "max(HW_FLOPS/sustained bf16, H2D/55GB/s, D2H/55GB/s)"},
         "host_roofline": {"host_bytes_per_step": int(host_bytes), "triad_gbs": host_bw,
@@ -327,7 +375,8 @@ def run_ours(args, m, name):
                           "def": "(30 B/param host Adam + 4 B/param gradient DMA + weight DMA bytes)"
                                  " / (4/3 x measured 16-thread STREAM triad = raw DRAM bandwidth)"},
         "stream": {"h2d_gbs": h2d_gbs, "d2h_gbs": d2h_gbs, "overlap": overlap,
-                   "gpu_busy_s": gpu_busy_s, "host_adam_s": adam_s,
+                   "gpu_span_s": gpu_span_s, "compute_busy_s": rep["compute_busy_ms"] / 1e3,
+                   "host_adam_s": adam_s,
                    "h2d_bytes_measured": int(h2d_step), "trace_violations": len(violations)},
         "clocks": clk, "cpu_baseline": cpu_baseline,
         "loss": [float(x) for x in losses], "setup_s": setup_s,
@@ -348,9 +397,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--slabs", type=int, default=6)
-    ap.add_argument("--tail-blocks", type=int, default=3,
-                    help="blocks optimised after the embedding, overlapping the next forward (-1: off)")
+    ap.add_argument("--slabs", type=int, default=0,
+                    help="pinned gradient slabs (0: auto = layers + 4, capped by free host memory)")
+    ap.add_argument("--tail-blocks", type=int, default=-2,
+                    help="blocks optimised after the embedding, overlapping the next forward "
+                         "(-1: off, -2: auto = every block the slab pool can hold)")
     ap.add_argument("--cache-gb", type=float, default=60.0,
                     help="HBM weight cache (block tiles resident between forward and backward)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

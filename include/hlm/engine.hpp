@@ -127,7 +127,7 @@ private:
         i64 t = 0;      // Adam step index of the gradient (bias correction)
     };
     struct HostOpRecord {   // host-side Accum / OptStep, appended to the trace in finish_step
-        i64 slab, layer, grad_op;
+        i64 slab, layer, grad_op, step;   // step: the gradient's step (an earlier one for a tail tile)
         double t0, t1;
         bool opt;
         double topt0, topt1;

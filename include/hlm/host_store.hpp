@@ -210,21 +210,25 @@ const char* slab_state_name(SlabState s);
 class SlabPool {
 public:
     SlabPool(i64 n_slabs, i64 slab_capacity_bytes, bool pinned = true);
+    // Mixed capacities: acquire(bytes) takes the smallest FREE slab that fits
+    // (two widest-tile slabs for the embedding/head, the rest block-sized).
+    explicit SlabPool(const std::vector<i64>& capacities, bool pinned = true);
     ~SlabPool();
     SlabPool(const SlabPool&) = delete;
     SlabPool& operator=(const SlabPool&) = delete;
 
     i64 size() const { return static_cast<i64>(slabs_.size()); }
-    i64 slab_capacity() const { return capacity_; }
-    i64 pool_bytes() const { return size() * capacity_; }
+    i64 slab_capacity() const { return capacity_; }   // the largest slab
+    i64 capacity_of(i64 id) const { return slabs_[static_cast<size_t>(id)].capacity; }
+    i64 pool_bytes() const { return pool_bytes_; }
     SlabState state(i64 id) const;
     float* data(i64 id) { return slabs_[static_cast<size_t>(id)].data; }
     i64 layer_of(i64 id) const { return slabs_[static_cast<size_t>(id)].layer_id; }
     i64 d2h_bytes() const { return d2h_bytes_; }
     i64 max_in_use() const { return max_in_use_; }
 
-    i64 try_acquire();                       // FREE -> IN_FLIGHT, -1 if none
-    i64 acquire_blocking();                  // waits for a FREE slab
+    i64 try_acquire(i64 bytes = 0);          // FREE -> IN_FLIGHT, -1 if none fits
+    i64 acquire_blocking(i64 bytes = 0);     // waits for a FREE slab that fits
     void mark_in_flight(i64 id, i64 layer_id, i64 bytes);
     void mark_ready(i64 id);                 // IN_FLIGHT -> READY (+ FIFO)
     i64 pop_ready_blocking(bool* stop);      // oldest READY -> ACCUMULATING, -1 when stopped
@@ -234,12 +238,14 @@ public:
 private:
     struct Slab {
         float* data = nullptr;
+        i64 capacity = 0;
+        bool pinned = false;
         SlabState state = SlabState::FREE;
         i64 layer_id = -1;
         i64 bytes = 0;
     };
-    i64 capacity_;
-    bool pinned_;
+    i64 pick_free_locked(i64 bytes);
+    i64 capacity_ = 0, pool_bytes_ = 0;
     std::vector<Slab> slabs_;
     std::deque<i64> ready_;
     mutable std::mutex mu_;

@@ -169,6 +169,10 @@ double hlm_timer_elapsed_ms(int a, int b);
  * algorithmic flops of the set, the mean ms per set and the per-launch mean. */
 int hlm_cuda_bench_block_gemms(const HlmBlockDims* d, int iters, double* flops, double* ms_per_set,
                                double* ms_per_launch);
+/* Achieved HBM GB/s (algorithmic bytes / CUDA-event time) of the block's
+ * elementwise and norm kernels at the workload shape; gbs[6], ms[6] (ms may be
+ * NULL) in the order rmsnorm_fwd, rmsnorm_bwd, swiglu_fwd, swiglu_bwd, rope, cast. */
+int hlm_cuda_bench_block_ops(const HlmBlockDims* d, int iters, double* gbs, double* ms);
 int hlm_cuda_attention_fwd(const HlmBlockDims* d, const void* q, const void* k, const void* v,
                            void* o, float* lse, int64_t ld, void* stream);
 int hlm_cuda_attention_bwd(const HlmBlockDims* d, const void* q, const void* k, const void* v,

@@ -533,4 +533,78 @@ int hlm_cuda_bench_block_gemms(const HlmBlockDims* d, int iters, double* flops, 
   });
 }
 
+// Achieved HBM bandwidth of the block's elementwise / norm kernels at the
+// workload shape (random data, CUDA events, `iters` back-to-back launches).
+// Algorithmic bytes per call (each tensor read / written once):
+//   0 rmsnorm_fwd  x f32 -> bf16              6 B x T*h
+//   1 rmsnorm_bwd  x, g, resid f32 -> f32 + bf16 (+ scale grad)   18 B x T*h
+//   2 swiglu_fwd   up, gate bf16 -> act       6 B x T*f
+//   3 swiglu_bwd   d_act, up, gate -> d_up, d_gate   10 B x T*f
+//   4 rope         q, k bf16 in place         8 B x T*h
+//   5 cast         f32 -> bf16                6 B x T*h
+int hlm_cuda_bench_block_ops(const HlmBlockDims* d, int iters, double* gbs, double* ms_out) {
+  return guarded([&] {
+    validate(d);
+    const i64 T = d->batch * d->seq, h = d->hidden, f = d->ffn;
+    const int hd = (int)(h / d->n_heads);
+    cudaStream_t s;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    std::vector<void*> bufs;
+    auto alloc = [&](size_t bytes) {
+      void* p = nullptr;
+      if (cudaMalloc(&p, bytes) != cudaSuccess) throw Failure{"bench alloc failed", HLM_ERR_CUDA};
+      hlm_ops_fill_random_bf16(p, static_cast<long long>(bytes / 2), 0x9e37u, s);
+      bufs.push_back(p);
+      return p;
+    };
+    float* x = (float*)alloc(T * h * 4);
+    float* g = (float*)alloc(T * h * 4);
+    float* resid = (float*)alloc(T * h * 4);
+    float* out = (float*)alloc(T * h * 4);
+    void* out_bf = alloc(T * h * 2);
+    void* scale = alloc(h * 2);
+    float* inv = (float*)alloc(T * 4);
+    float* partial = (float*)alloc(((T + HLM_NORM_ROWS_PER_CHUNK - 1) / HLM_NORM_ROWS_PER_CHUNK) * h * 4);
+    float* dscale = (float*)alloc(h * 4);
+    void* ug = alloc(2 * T * f * 2);
+    void* act = alloc(T * f * 2);
+    void* dug = alloc(2 * T * f * 2);
+    void* qk = alloc(2 * T * h * 2);
+    float* cs = (float*)alloc(d->seq * (hd / 2) * 4);
+    float* sn = (float*)alloc(d->seq * (hd / 2) * 4);
+    const double bytes[6] = {6.0 * T * h, 18.0 * T * h, 6.0 * T * f, 10.0 * T * f, 8.0 * T * h, 6.0 * T * h};
+    auto run = [&](int k) {
+      switch (k) {
+        case 0: chk(hlm_ops_rmsnorm_fwd(x, scale, out_bf, T, (int)h, s), "rmsnorm fwd"); break;
+        case 1:
+          chk(hlm_ops_rmsnorm_bwd(x, scale, g, resid, out, out_bf, inv, partial, dscale, T, (int)h, s), "rmsnorm bwd");
+          break;
+        case 2: chk(hlm_ops_swiglu_fwd(ug, act, T * f, s), "swiglu fwd"); break;
+        case 3: chk(hlm_ops_swiglu_bwd(act, ug, dug, T * f, s), "swiglu bwd"); break;
+        case 4: chk(hlm_ops_rope(qk, cs, sn, T, (int)h, hd, (int)d->seq, 0, 2, T * h, s), "rope"); break;
+        default: chk(hlm_ops_cast_bf16(x, out_bf, T * h, s), "cast"); break;
+      }
+    };
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    for (int k = 0; k < 6; ++k) {
+      run(k);
+      cudaEventRecord(a, s);
+      for (int it = 0; it < iters; ++it) run(k);
+      cudaEventRecord(b, s);
+      cudaEventSynchronize(b);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, a, b);
+      const double per = ms / iters;
+      if (ms_out) ms_out[k] = per;
+      gbs[k] = bytes[k] / (per * 1e-3) / 1e9;
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    for (void* p : bufs) cudaFree(p);
+    cudaStreamDestroy(s);
+  });
+}
+
 }  // extern "C"

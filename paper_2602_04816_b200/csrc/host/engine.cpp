@@ -56,7 +56,16 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
         ck(cudaMalloc(&loss_dev_, sizeof(double)), "cudaMalloc loss");
     }
     // data parallel: slabs hold a 1/world gradient shard
-    pool_ = std::make_unique<SlabPool>(opts_.n_slab, (grad_buf_bytes(m) / opts_.world + 255) / 256 * 256, true);
+    {
+        // two widest-tile slabs (embedding / head gradients), the rest block-sized
+        auto round = [](i64 b) { return (b + 255) / 256 * 256; };
+        const i64 widest = round(grad_buf_bytes(m) / opts_.world);
+        const i64 block = round(4 * m.block_params() / opts_.world);
+        std::vector<i64> caps(static_cast<size_t>(std::max<i64>(opts_.n_slab, 1)), widest);
+        if (opts_.n_slab >= 4 && block < widest)
+            for (size_t i = 2; i < caps.size(); ++i) caps[i] = block;
+        pool_ = std::make_unique<SlabPool>(caps, true);
+    }
     cudaStream_t s;
     ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
     h2d_ = s;
@@ -318,7 +327,9 @@ int Engine::next_grad_buf() {
 // consumes the oldest READY slab), D2H the fp32 gradient, emit GradXfer.
 void Engine::evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op) {
     ck(cudaEventRecord(E(ev_grad_ready_[gbuf]), S(compute_)), "record grad ready");
-    i64 slab = pool_->try_acquire();
+    const i64 cnt = opts_.comm_grad ? shard_elems(n_params) : n_params;
+    const i64 bytes = 4 * cnt;
+    i64 slab = pool_->try_acquire(bytes);
     while (slab < 0) {
         if (opts_.threaded_accum) {
             rethrow_worker_error();
@@ -329,14 +340,12 @@ void Engine::evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op) {
                 if (!any && !pending_.empty()) tail_open_ = true;   // never wedge on deferred slabs
             }
             cv_.notify_all();
-            slab = pool_->acquire_blocking();
+            slab = pool_->acquire_blocking(bytes);
         } else {
             process_oldest_inline();
-            slab = pool_->try_acquire();
+            slab = pool_->try_acquire(bytes);
         }
     }
-    const i64 cnt = opts_.comm_grad ? shard_elems(n_params) : n_params;
-    const i64 bytes = 4 * cnt;
     pool_->mark_in_flight(slab, tile_id, bytes);
     StreamOp op;
     op.stream = StreamId::D2H;
@@ -380,7 +389,7 @@ void Engine::consume(const Pending& p) {
     const i64 id = pool_->pop_ready_blocking(&stop);
     if (id != p.slab) throw ProtocolError("slab FIFO order violated");
     if (opts_.accum_delay_us > 0) std::this_thread::sleep_for(std::chrono::microseconds(opts_.accum_delay_us));
-    HostOpRecord rec{p.slab, p.layer, p.grad_op, now_us(), 0.0, false, 0.0, 0.0};
+    HostOpRecord rec{p.slab, p.layer, p.grad_op, p.step, now_us(), 0.0, false, 0.0, 0.0};
     LayerTile& tile = store_.tile(p.layer);
     const i64 phys = store_.physical_index(p.layer);
     const bool optimise = opts_.eager_optim && !opts_.skip_optimizer;
@@ -487,15 +496,21 @@ void Engine::worker_loop() {
         Pending p;
         {
             std::unique_lock<std::mutex> lk(mu_);
-            // Never idle while a gradient is available; priority: the previous
-            // step's tail (the running forward needs it, in tile order), then this
-            // step's regular tiles in arrival order, then this step's tail tiles in
-            // the order the next forward consumes them (ascending id, head last).
+            // Never idle while a gradient is available. Among slabs whose D2H has
+            // landed: the previous step's tail first (the running forward needs
+            // it, in tile order), then this step's regular tiles in arrival order,
+            // then this step's tail tiles in the order the next forward consumes
+            // them (ascending id, head last). With none landed, the oldest entry
+            // (the D2H stream completes in issue order).
             auto pick = [&]() -> bool {
+                if (pending_.empty()) return false;
                 auto best = pending_.end();
                 std::pair<int, i64> best_rank{3, 0};
                 i64 pos = 0;
                 for (auto it = pending_.begin(); it != pending_.end(); ++it, ++pos) {
+                    const cudaError_t q = cudaEventQuery(E(ev_slab_done_[static_cast<size_t>(it->slab)]));
+                    if (q == cudaErrorNotReady) continue;
+                    if (q != cudaSuccess) (void)cudaGetLastError();   // surfaced by consume's synchronize
                     std::pair<int, i64> rank;
                     if (it->step < step_index_)
                         rank = {0, it->layer};
@@ -508,7 +523,7 @@ void Engine::worker_loop() {
                         best = it;
                     }
                 }
-                if (best == pending_.end()) return false;
+                if (best == pending_.end()) best = pending_.begin();
                 p = *best;
                 pending_.erase(best);
                 return true;
@@ -963,7 +978,7 @@ StepResult Engine::finish_step() {
         op.layer = rec.layer;
         op.slab = rec.slab;
         op.params = store_.tile(rec.layer).n_params();
-        op.deps.push_back(rec.grad_op);
+        if (rec.step == step_index_) op.deps.push_back(rec.grad_op);   // earlier step: op ids of another trace
         op.t_start_us = rec.t0 - host_t0_us_;
         op.t_end_us = rec.t1 - host_t0_us_;
         const i64 id = trace_.add(op);

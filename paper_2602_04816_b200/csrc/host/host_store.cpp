@@ -372,16 +372,24 @@ const char* slab_state_name(SlabState s) {
     return "?";
 }
 
-SlabPool::SlabPool(i64 n_slabs, i64 capacity_bytes, bool pinned) : capacity_(capacity_bytes), pinned_(pinned) {
-    if (n_slabs <= 0) throw ConfigError("slab pool needs at least one slab");
-    slabs_.resize(static_cast<size_t>(n_slabs));
-    for (auto& s : slabs_) {
+SlabPool::SlabPool(i64 n_slabs, i64 capacity_bytes, bool pinned)
+    : SlabPool(std::vector<i64>(static_cast<size_t>(std::max<i64>(n_slabs, 0)), capacity_bytes), pinned) {}
+
+SlabPool::SlabPool(const std::vector<i64>& capacities, bool pinned) {
+    if (capacities.empty()) throw ConfigError("slab pool needs at least one slab");
+    slabs_.resize(capacities.size());
+    for (size_t i = 0; i < capacities.size(); ++i) {
+        Slab& s = slabs_[i];
+        s.capacity = capacities[i];
+        capacity_ = std::max(capacity_, s.capacity);
+        pool_bytes_ += s.capacity;
         void* p = nullptr;
-        if (pinned_ && cudaHostAlloc(&p, static_cast<size_t>(capacity_bytes), cudaHostAllocPortable) != cudaSuccess) {
+        if (pinned && cudaHostAlloc(&p, static_cast<size_t>(s.capacity), cudaHostAllocPortable) == cudaSuccess) {
+            s.pinned = true;
+        } else {
             (void)cudaGetLastError();
-            pinned_ = false;
+            p = map_huge(static_cast<size_t>(s.capacity));
         }
-        if (!p) p = map_huge(static_cast<size_t>(capacity_bytes));
         s.data = static_cast<float*>(p);
     }
 }
@@ -389,10 +397,10 @@ SlabPool::SlabPool(i64 n_slabs, i64 capacity_bytes, bool pinned) : capacity_(cap
 SlabPool::~SlabPool() {
     for (auto& s : slabs_) {
         if (!s.data) continue;
-        if (cudaFreeHost(s.data) != cudaSuccess) {
-            (void)cudaGetLastError();
-            munmap(s.data, static_cast<size_t>(capacity_));
-        }
+        if (s.pinned)
+            cudaFreeHost(s.data);
+        else
+            munmap(s.data, static_cast<size_t>(s.capacity));
     }
 }
 
@@ -401,26 +409,33 @@ SlabState SlabPool::state(i64 id) const {
     return slabs_[static_cast<size_t>(id)].state;
 }
 
-i64 SlabPool::try_acquire() {
-    std::lock_guard<std::mutex> lk(mu_);
-    for (size_t i = 0; i < slabs_.size(); ++i)
-        if (slabs_[i].state == SlabState::FREE) {
-            slabs_[i].state = SlabState::IN_FLIGHT;
-            if (++in_use_ > max_in_use_) max_in_use_ = in_use_;
-            return static_cast<i64>(i);
-        }
-    return -1;
+// smallest FREE slab with capacity >= bytes (first such in index order on ties)
+i64 SlabPool::pick_free_locked(i64 bytes) {
+    i64 best = -1;
+    for (size_t i = 0; i < slabs_.size(); ++i) {
+        const Slab& s = slabs_[i];
+        if (s.state != SlabState::FREE || s.capacity < bytes) continue;
+        if (best < 0 || s.capacity < slabs_[static_cast<size_t>(best)].capacity) best = static_cast<i64>(i);
+    }
+    if (best >= 0) {
+        slabs_[static_cast<size_t>(best)].state = SlabState::IN_FLIGHT;
+        if (++in_use_ > max_in_use_) max_in_use_ = in_use_;
+    }
+    return best;
 }
 
-i64 SlabPool::acquire_blocking() {
+i64 SlabPool::try_acquire(i64 bytes) {
+    std::lock_guard<std::mutex> lk(mu_);
+    if (bytes > capacity_) throw ProtocolError("slab request exceeds the largest slab");
+    return pick_free_locked(bytes);
+}
+
+i64 SlabPool::acquire_blocking(i64 bytes) {
     std::unique_lock<std::mutex> lk(mu_);
+    if (bytes > capacity_) throw ProtocolError("slab request exceeds the largest slab");
     for (;;) {
-        for (size_t i = 0; i < slabs_.size(); ++i)
-            if (slabs_[i].state == SlabState::FREE) {
-                slabs_[i].state = SlabState::IN_FLIGHT;
-                if (++in_use_ > max_in_use_) max_in_use_ = in_use_;
-                return static_cast<i64>(i);
-            }
+        const i64 id = pick_free_locked(bytes);
+        if (id >= 0) return id;
         cv_.wait(lk);
     }
 }
@@ -429,7 +444,7 @@ void SlabPool::mark_in_flight(i64 id, i64 layer_id, i64 bytes) {
     std::lock_guard<std::mutex> lk(mu_);
     Slab& s = slabs_[static_cast<size_t>(id)];
     if (s.state != SlabState::IN_FLIGHT) throw ProtocolError(std::string("slab fill in state ") + slab_state_name(s.state));
-    if (bytes > capacity_) throw ProtocolError("slab payload exceeds slab capacity");
+    if (bytes > s.capacity) throw ProtocolError("slab payload exceeds slab capacity");
     s.layer_id = layer_id;
     s.bytes = bytes;
     d2h_bytes_ += bytes;   // counted when the copy is issued

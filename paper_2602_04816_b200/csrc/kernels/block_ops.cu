@@ -84,10 +84,22 @@ __global__ void rmsnorm_bwd_kernel(const float* __restrict__ x, const __nv_bfloa
     const float* xr = x + r * h;
     const float* gr = g + r * h;
     float ss = 0.f, dot = 0.f;
-    for (int j = lane; j < h; j += 32) {
-      const float xv = xr[j];
-      ss += xv * xv;
-      dot += gr[j] * bf(scale[j]) * xv;
+    if ((h & 3) == 0) {
+      for (int j = lane * 4; j < h; j += 128) {
+        const float4 xv = *reinterpret_cast<const float4*>(xr + j);
+        const float4 gv = *reinterpret_cast<const float4*>(gr + j);
+        const uint2 sp = *reinterpret_cast<const uint2*>(scale + j);
+        const float2 s01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sp.x));
+        const float2 s23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sp.y));
+        ss += xv.x * xv.x + xv.y * xv.y + xv.z * xv.z + xv.w * xv.w;
+        dot += gv.x * s01.x * xv.x + gv.y * s01.y * xv.y + gv.z * s23.x * xv.z + gv.w * s23.y * xv.w;
+      }
+    } else {
+      for (int j = lane; j < h; j += 32) {
+        const float xv = xr[j];
+        ss += xv * xv;
+        dot += gr[j] * bf(scale[j]) * xv;
+      }
     }
     ss = warp_sum(ss);
     dot = warp_sum(dot);
@@ -95,11 +107,38 @@ __global__ void rmsnorm_bwd_kernel(const float* __restrict__ x, const __nv_bfloa
     const float c = inv * inv * inv * dot / (float)h;
     if (lane == 0) inv_out[r] = inv;
     const float* rr = resid ? resid + r * h : nullptr;
-    for (int j = lane; j < h; j += 32) {
-      float v = gr[j] * bf(scale[j]) * inv - c * xr[j];
-      if (rr) v += rr[j];
-      out[r * h + j] = v;
-      if (out_bf) out_bf[r * h + j] = __float2bfloat16_rn(v);
+    if ((h & 3) == 0) {
+      for (int j = lane * 4; j < h; j += 128) {
+        const float4 xv = *reinterpret_cast<const float4*>(xr + j);
+        const float4 gv = *reinterpret_cast<const float4*>(gr + j);
+        const uint2 sp = *reinterpret_cast<const uint2*>(scale + j);
+        const float2 s01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sp.x));
+        const float2 s23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sp.y));
+        float4 v = make_float4(gv.x * s01.x * inv - c * xv.x, gv.y * s01.y * inv - c * xv.y,
+                               gv.z * s23.x * inv - c * xv.z, gv.w * s23.y * inv - c * xv.w);
+        if (rr) {
+          const float4 q = *reinterpret_cast<const float4*>(rr + j);
+          v.x += q.x;
+          v.y += q.y;
+          v.z += q.z;
+          v.w += q.w;
+        }
+        *reinterpret_cast<float4*>(out + r * h + j) = v;
+        if (out_bf) {
+          __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+          uint2 pk;
+          pk.x = *reinterpret_cast<uint32_t*>(&a);
+          pk.y = *reinterpret_cast<uint32_t*>(&b);
+          *reinterpret_cast<uint2*>(out_bf + r * h + j) = pk;
+        }
+      }
+    } else {
+      for (int j = lane; j < h; j += 32) {
+        float v = gr[j] * bf(scale[j]) * inv - c * xr[j];
+        if (rr) v += rr[j];
+        out[r * h + j] = v;
+        if (out_bf) out_bf[r * h + j] = __float2bfloat16_rn(v);
+      }
     }
   }
 }
@@ -176,11 +215,35 @@ __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ ug, __nv_bfl
 __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ dact, const __nv_bfloat16* __restrict__ ug,
                                   __nv_bfloat16* __restrict__ dug, long long n) {
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const float da = bf(dact[i]), u = bf(ug[i]), z = bf(ug[n + i]);
-    const float s = 1.0f / (1.0f + __expf(-z));
-    dug[i] = __float2bfloat16_rn(da * z * s);
-    dug[n + i] = __float2bfloat16_rn(da * u * (s * (1.0f + z * (1.0f - s))));
+  for (long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 8; i < n; i += stride * 8) {
+    if (i + 8 <= n) {
+      const uint4 dv = *reinterpret_cast<const uint4*>(dact + i);
+      const uint4 uv = *reinterpret_cast<const uint4*>(ug + i);
+      const uint4 zv = *reinterpret_cast<const uint4*>(ug + n + i);
+      const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&dv);
+      const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&uv);
+      const __nv_bfloat162* z2 = reinterpret_cast<const __nv_bfloat162*>(&zv);
+      uint4 ou, og;
+      __nv_bfloat162* ou2 = reinterpret_cast<__nv_bfloat162*>(&ou);
+      __nv_bfloat162* og2 = reinterpret_cast<__nv_bfloat162*>(&og);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 da = __bfloat1622float2(d2[k]), u = __bfloat1622float2(u2[k]), z = __bfloat1622float2(z2[k]);
+        const float sx = 1.0f / (1.0f + __expf(-z.x)), sy = 1.0f / (1.0f + __expf(-z.y));
+        ou2[k] = __floats2bfloat162_rn(da.x * z.x * sx, da.y * z.y * sy);
+        og2[k] = __floats2bfloat162_rn(da.x * u.x * (sx * (1.0f + z.x * (1.0f - sx))),
+                                       da.y * u.y * (sy * (1.0f + z.y * (1.0f - sy))));
+      }
+      *reinterpret_cast<uint4*>(dug + i) = ou;
+      *reinterpret_cast<uint4*>(dug + n + i) = og;
+    } else {
+      for (long long k = i; k < n; ++k) {
+        const float da = bf(dact[k]), u = bf(ug[k]), z = bf(ug[n + k]);
+        const float sg = 1.0f / (1.0f + __expf(-z));
+        dug[k] = __float2bfloat16_rn(da * z * sg);
+        dug[n + k] = __float2bfloat16_rn(da * u * (sg * (1.0f + z * (1.0f - sg))));
+      }
+    }
   }
 }
 
@@ -210,6 +273,46 @@ __global__ void rope_kernel(__nv_bfloat16* __restrict__ x, const float* __restri
       v[i] = __float2bfloat16_rn(a * c + b * s);
       v[i + half] = __float2bfloat16_rn(b * c - a * s);
     }
+  }
+}
+
+// 8 rotation pairs per thread: 16-byte loads of x[i..i+8) and x[i+half..), two
+// float4 loads of cos / sin each (hd % 16 == 0, h % 8 == 0).
+__global__ void rope8_kernel(__nv_bfloat16* __restrict__ x, const float* __restrict__ cs,
+                             const float* __restrict__ sn, int rows, int h, int hd, int S, int inverse,
+                             int nmats, long long mat_stride) {
+  const int half = hd >> 1, cph = half >> 3;
+  const int per_row = (h / hd) * cph;
+  const long long per_mat = (long long)rows * per_row;
+  const long long total = per_mat * nmats;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+    const int m = (int)(t / per_mat);
+    const long long p = t - (long long)m * per_mat;
+    const int r = (int)(p / per_row);
+    const int k = (int)(p - (long long)r * per_row);
+    const int head = k / cph, i = (k - head * cph) * 8;
+    const int pos = r % S;
+    __nv_bfloat16* v = x + m * mat_stride + (long long)r * h + head * hd + i;
+    uint4 ua = *reinterpret_cast<const uint4*>(v);
+    uint4 ub = *reinterpret_cast<const uint4*>(v + half);
+    const float4* cp = reinterpret_cast<const float4*>(cs + (long long)pos * half + i);
+    const float4* sp = reinterpret_cast<const float4*>(sn + (long long)pos * half + i);
+    const float4 c0 = cp[0], c1 = cp[1], s0 = sp[0], s1 = sp[1];
+    const float c[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    const float sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+    __nv_bfloat162* a2 = reinterpret_cast<__nv_bfloat162*>(&ua);
+    __nv_bfloat162* b2 = reinterpret_cast<__nv_bfloat162*>(&ub);
+    const float sg = inverse ? -1.0f : 1.0f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 a = __bfloat1622float2(a2[q]), b = __bfloat1622float2(b2[q]);
+      const float cx = c[2 * q], cy = c[2 * q + 1], sx = sg * sv[2 * q], sy = sg * sv[2 * q + 1];
+      a2[q] = __floats2bfloat162_rn(a.x * cx - b.x * sx, a.y * cy - b.y * sy);
+      b2[q] = __floats2bfloat162_rn(b.x * cx + a.x * sx, b.y * cy + a.y * sy);
+    }
+    *reinterpret_cast<uint4*>(v) = ua;
+    *reinterpret_cast<uint4*>(v + half) = ub;
   }
 }
 
@@ -606,7 +709,7 @@ int hlm_ops_swiglu_fwd(const void* ug, void* act, long long n, cudaStream_t s) {
 }
 
 int hlm_ops_swiglu_bwd(const void* dact, const void* ug, void* dug, long long n, cudaStream_t s) {
-  swiglu_bwd_kernel<<<grid_for(n, 256), 256, 0, s>>>((const __nv_bfloat16*)dact, (const __nv_bfloat16*)ug,
+  swiglu_bwd_kernel<<<grid_for(n / 8 + 1, 256), 256, 0, s>>>((const __nv_bfloat16*)dact, (const __nv_bfloat16*)ug,
                                                     (__nv_bfloat16*)dug, n);
   hlm_count_launches(1);
   HLM_CHECK_LAUNCH();
@@ -614,8 +717,12 @@ int hlm_ops_swiglu_bwd(const void* dact, const void* ug, void* dug, long long n,
 
 int hlm_ops_rope(void* x, const float* cs, const float* sn, long long rows, int h, int hd, int S, int inverse,
                  int nmats, long long mat_stride, cudaStream_t s) {
-  rope_kernel<<<grid_for(rows * (h / 2) * nmats, 256), 256, 0, s>>>((__nv_bfloat16*)x, cs, sn, rows, h, hd, S,
-                                                                     inverse, nmats, mat_stride);
+  if (hd % 16 == 0 && h % 8 == 0 && rows < (1LL << 31))
+    rope8_kernel<<<grid_for(rows * (h / 16) * nmats, 256), 256, 0, s>>>((__nv_bfloat16*)x, cs, sn, (int)rows, h, hd,
+                                                                         S, inverse, nmats, mat_stride);
+  else
+    rope_kernel<<<grid_for(rows * (h / 2) * nmats, 256), 256, 0, s>>>((__nv_bfloat16*)x, cs, sn, rows, h, hd, S,
+                                                                       inverse, nmats, mat_stride);
   hlm_count_launches(1);
   HLM_CHECK_LAUNCH();
 }

@@ -143,15 +143,16 @@ def _union(intervals):
 
 def overlap_report(ops):
     """Per-step transfer/compute overlap from a measured trace: the fraction of
-    H2D + D2H busy time during which the compute stream was also busy, plus the
-    achieved copy bandwidths (GB/s over the streams' busy time)."""
+    H2D + D2H busy time during which the compute stream was also busy, the
+    achieved copy bandwidths (GB/s over the streams' busy time) and the compute
+    stream's busy time (union of its op intervals)."""
     comp = _union([(o["t_start_us"], o["t_end_us"]) for o in ops
                    if o["stream"] == "compute" and o["t_end_us"] > o["t_start_us"] >= 0])
 
     def covered(a, b):
         return sum(max(0.0, min(b, e) - max(a, s)) for s, e in comp)
 
-    rep = {}
+    rep = {"compute_busy_ms": sum(e - s for s, e in comp) / 1e3}
     for st in ("h2d", "d2h"):
         xs = [o for o in ops if o["stream"] == st and o["t_end_us"] > o["t_start_us"] >= 0]
         busy = sum(o["t_end_us"] - o["t_start_us"] for o in xs)

@@ -49,7 +49,10 @@ cases = [
   ("wgrad up|gate [N-grp2]", desc(h, f, T, X, dUG, dW2, 1, 1, G=2, bg=1, epi=L.EPI_F32), 2*T*h*f*2, None),
   ("wgrad down", desc(f, h, T, Act, X, dWd, 1, 1, epi=L.EPI_F32), 2*T*h*f, lambda: torch.matmul(Act.t(), X)),
 ]
+only = os.environ.get("GEMM_CASE")   # substring filter, e.g. GEMM_CASE="wgrad down"
 for name, d, flops, ref in cases:
+    if only and only not in name:
+        continue
     t = timeit(lambda: L.gemm(d))
     line = f"{name:26s} {t*1e3:8.3f} ms  {flops/t/1e12:7.1f} TFLOP/s"
     if ref is not None:
