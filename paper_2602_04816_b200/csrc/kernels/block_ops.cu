@@ -5,12 +5,15 @@
 //   embed gather / scatter-add       kernels.hpp:385-408
 //   cross entropy + d_logits         kernels.hpp:423-446
 //   RoPE (extension, Qwen2 rotate-half)
-// All HBM-bound: 16-byte vector accesses, one warp per row for row
-// reductions, fixed-order (deterministic) reductions everywhere.
+// All HBM-bound: 16-byte vector accesses; RMSNorm keeps a chunk's rows in
+// registers between the row reduction and the output pass (one HBM read of each
+// input); fixed-order (deterministic) reductions everywhere. Achieved GB/s at
+// the workload shape: hlm_cuda_bench_block_ops (bench.py elementwise_roofline).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "block_ops.h"
 
@@ -68,6 +71,64 @@ __global__ void rmsnorm_fwd_kernel(const float* __restrict__ x, const __nv_bfloa
       }
     } else {
       for (int j = lane; j < h; j += 32) o[j] = __float2bfloat16_rn(xr[j] * inv * bf(scale[j]));
+    }
+  }
+}
+
+// Register-resident forward: one block per chunk of rows, thread owns float4
+// columns q = tid + k*THREADS; x read once, scale loaded once per block.
+template <int THREADS, int V>
+__global__ void __launch_bounds__(THREADS)
+    rmsnorm_fwd_reg_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ scale,
+                           __nv_bfloat16* __restrict__ out, long long rows, int h, int rows_per_block) {
+  constexpr int NW = THREADS / 32;
+  __shared__ float red[2][NW];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nv = h >> 2;
+  float4 sc[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const int q = tid + k * THREADS;
+    sc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (q < nv) {
+      const uint2 spk = *reinterpret_cast<const uint2*>(scale + 4 * q);
+      const float2 s01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&spk.x));
+      const float2 s23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&spk.y));
+      sc[k] = make_float4(s01.x, s01.y, s23.x, s23.y);
+    }
+  }
+  const long long r0 = (long long)blockIdx.x * rows_per_block;
+  const long long r1 = r0 + rows_per_block < rows ? r0 + rows_per_block : rows;
+  int par = 0;
+  for (long long r = r0; r < r1; ++r, par ^= 1) {
+    float4 xv[V];
+    float ss = 0.f;
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      const int q = tid + k * THREADS;
+      if (q < nv) {
+        xv[k] = reinterpret_cast<const float4*>(x + r * h)[q];
+        ss += xv[k].x * xv[k].x + xv[k].y * xv[k].y + xv[k].z * xv[k].z + xv[k].w * xv[k].w;
+      }
+    }
+    ss = warp_sum(ss);
+    if (lane == 0) red[par][warp] = ss;
+    __syncthreads();
+    ss = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) ss += red[par][w];
+    const float inv = 1.0f / sqrtf(ss / (float)h + kEps);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      const int q = tid + k * THREADS;
+      if (q < nv) {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(xv[k].x * inv * sc[k].x, xv[k].y * inv * sc[k].y);
+        __nv_bfloat162 hi = __floats2bfloat162_rn(xv[k].z * inv * sc[k].z, xv[k].w * inv * sc[k].w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+        reinterpret_cast<uint2*>(out + r * h)[q] = pk;
+      }
     }
   }
 }
@@ -143,6 +204,101 @@ __global__ void rmsnorm_bwd_kernel(const float* __restrict__ x, const __nv_bfloa
   }
 }
 
+// Register-resident variant: one block per chunk of rows_per_chunk rows; each
+// thread owns float4 columns q = tid + k*THREADS (k < V) and keeps the row's x,
+// g and its scale in registers between the reduction and the output pass, so x
+// and g are read from HBM once. The scale-gradient partial of the chunk
+// (sum over its rows of g*x*inv, row order) accumulates in registers too.
+// Deterministic: fixed-order warp and block reductions.
+template <int THREADS, int V, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB)
+    rmsnorm_bwd_reg_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ scale,
+                           const float* __restrict__ g, const float* __restrict__ resid, float* __restrict__ out,
+                           __nv_bfloat16* __restrict__ out_bf, float* __restrict__ inv_out,
+                           float* __restrict__ partial, long long rows, int h, int rows_per_chunk) {
+  constexpr int NW = THREADS / 32;
+  __shared__ float red[2][2][NW];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nv = h >> 2;
+  float4 sc[V], acc[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const int q = tid + k * THREADS;
+    acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    sc[k] = acc[k];
+    if (q < nv) {
+      const uint2 spk = *reinterpret_cast<const uint2*>(scale + 4 * q);
+      const float2 s01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&spk.x));
+      const float2 s23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&spk.y));
+      sc[k] = make_float4(s01.x, s01.y, s23.x, s23.y);
+    }
+  }
+  const long long r0 = (long long)blockIdx.x * rows_per_chunk;
+  const long long r1 = r0 + rows_per_chunk < rows ? r0 + rows_per_chunk : rows;
+  int par = 0;
+  for (long long r = r0; r < r1; ++r, par ^= 1) {
+    float4 xv[V], gv[V], rv[V];
+    float ss = 0.f, dot = 0.f;
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      const int q = tid + k * THREADS;
+      rv[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (q < nv) {
+        xv[k] = __ldcs(reinterpret_cast<const float4*>(x + r * h) + q);
+        gv[k] = __ldcs(reinterpret_cast<const float4*>(g + r * h) + q);
+        if (resid) rv[k] = __ldcs(reinterpret_cast<const float4*>(resid + r * h) + q);
+        ss += xv[k].x * xv[k].x + xv[k].y * xv[k].y + xv[k].z * xv[k].z + xv[k].w * xv[k].w;
+        dot += gv[k].x * sc[k].x * xv[k].x + gv[k].y * sc[k].y * xv[k].y + gv[k].z * sc[k].z * xv[k].z +
+               gv[k].w * sc[k].w * xv[k].w;
+      }
+    }
+    ss = warp_sum(ss);
+    dot = warp_sum(dot);
+    if (lane == 0) {
+      red[par][0][warp] = ss;
+      red[par][1][warp] = dot;
+    }
+    __syncthreads();   // red[par] complete; red[par ^ 1] (last row) no longer read
+    ss = 0.f;
+    dot = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      ss += red[par][0][w];
+      dot += red[par][1][w];
+    }
+    const float inv = 1.0f / sqrtf(ss / (float)h + kEps);
+    const float c = inv * inv * inv * dot / (float)h;
+    if (tid == 0) inv_out[r] = inv;
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      const int q = tid + k * THREADS;
+      if (q < nv) {
+        const float4 v = make_float4(gv[k].x * sc[k].x * inv - c * xv[k].x + rv[k].x,
+                                     gv[k].y * sc[k].y * inv - c * xv[k].y + rv[k].y,
+                                     gv[k].z * sc[k].z * inv - c * xv[k].z + rv[k].z,
+                                     gv[k].w * sc[k].w * inv - c * xv[k].w + rv[k].w);
+        __stcs(reinterpret_cast<float4*>(out + r * h) + q, v);
+        if (out_bf) {
+          __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+          uint2 pk;
+          pk.x = *reinterpret_cast<uint32_t*>(&lo);
+          pk.y = *reinterpret_cast<uint32_t*>(&hi);
+          reinterpret_cast<uint2*>(out_bf + r * h)[q] = pk;
+        }
+        acc[k].x += gv[k].x * xv[k].x * inv;
+        acc[k].y += gv[k].y * xv[k].y * inv;
+        acc[k].z += gv[k].z * xv[k].z * inv;
+        acc[k].w += gv[k].w * xv[k].w * inv;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const int q = tid + k * THREADS;
+    if (q < nv) reinterpret_cast<float4*>(partial + (long long)blockIdx.x * h)[q] = acc[k];
+  }
+}
+
 // partial[c][j] = sum_{r in chunk c} g[r][j] * x[r][j] * inv[r]   (columns across threads)
 __global__ void norm_scale_partial_kernel(const float* __restrict__ x, const float* __restrict__ g,
                                           const float* __restrict__ inv, float* __restrict__ partial,
@@ -157,13 +313,25 @@ __global__ void norm_scale_partial_kernel(const float* __restrict__ x, const flo
   partial[(long long)c * h + j] = acc;
 }
 
-__global__ void norm_scale_reduce_kernel(const float* __restrict__ partial, float* __restrict__ out,
-                                         int chunks, int h) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= h) return;
+// out[j] = sum_c partial[c][j]: 32 columns x 8 chunk groups per block; group k
+// sums chunks k, k+8, ... in order, then the 8 group sums are added in group
+// order (fixed, deterministic), coalesced 128-byte rows of partial.
+__global__ void __launch_bounds__(256) norm_scale_reduce_kernel(const float* __restrict__ partial,
+                                                                float* __restrict__ out, int chunks, int h) {
+  __shared__ float red[8][33];
+  const int col = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + col;
   float acc = 0.f;
-  for (int c = 0; c < chunks; ++c) acc += partial[(long long)c * h + j];
-  out[j] = acc;
+  if (j < h)
+    for (int c = grp; c < chunks; c += 8) acc += partial[(long long)c * h + j];
+  red[grp][col] = acc;
+  __syncthreads();
+  if (grp == 0 && j < h) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += red[k][col];
+    out[j] = t;
+  }
 }
 
 // ------------------------------------------------------------------ casts
@@ -677,7 +845,17 @@ int hlm_ops_adam_device(float* w, float* m, float* v, void* w16, const float* g,
 }
 
 int hlm_ops_rmsnorm_fwd(const float* x, const void* scale, void* out, long long rows, int h, cudaStream_t s) {
-  rmsnorm_fwd_kernel<<<grid_for(rows, 8), 256, 0, s>>>(x, (const __nv_bfloat16*)scale, (__nv_bfloat16*)out, rows, h);
+  constexpr int rpb = 8;
+  const unsigned blocks = (unsigned)((rows + rpb - 1) / rpb);
+  if (h % 4 == 0 && h <= 4 * 256 * 4)
+    rmsnorm_fwd_reg_kernel<256, 4><<<blocks, 256, 0, s>>>(x, (const __nv_bfloat16*)scale, (__nv_bfloat16*)out, rows,
+                                                          h, rpb);
+  else if (h % 4 == 0 && h <= 4 * 512 * 6)
+    rmsnorm_fwd_reg_kernel<512, 6><<<blocks, 512, 0, s>>>(x, (const __nv_bfloat16*)scale, (__nv_bfloat16*)out, rows,
+                                                          h, rpb);
+  else
+    rmsnorm_fwd_kernel<<<grid_for(rows, 8), 256, 0, s>>>(x, (const __nv_bfloat16*)scale, (__nv_bfloat16*)out, rows,
+                                                         h);
   hlm_count_launches(1);
   HLM_CHECK_LAUNCH();
 }
@@ -685,14 +863,23 @@ int hlm_ops_rmsnorm_fwd(const float* x, const void* scale, void* out, long long 
 int hlm_ops_rmsnorm_bwd(const float* x, const void* scale, const float* g, const float* resid, float* out,
                         void* out_bf, float* inv_buf, float* partial, float* dscale, long long rows, int h,
                         cudaStream_t s) {
-  rmsnorm_bwd_kernel<<<grid_for(rows, 8), 256, 0, s>>>(x, (const __nv_bfloat16*)scale, g, resid, out,
-                                                       (__nv_bfloat16*)out_bf, inv_buf, rows, h);
   const int rpc = HLM_NORM_ROWS_PER_CHUNK;
   const int chunks = (int)((rows + rpc - 1) / rpc);
-  dim3 grid((h + 255) / 256, chunks);
-  norm_scale_partial_kernel<<<grid, 256, 0, s>>>(x, g, inv_buf, partial, rows, h, rpc);
-  norm_scale_reduce_kernel<<<(h + 255) / 256, 256, 0, s>>>(partial, dscale, chunks, h);
-  hlm_count_launches(3);
+  if (h % 4 == 0 && h <= 4 * 256 * 4) {
+    rmsnorm_bwd_reg_kernel<256, 4, 3><<<chunks, 256, 0, s>>>(x, (const __nv_bfloat16*)scale, g, resid, out,
+                                                             (__nv_bfloat16*)out_bf, inv_buf, partial, rows, h, rpc);
+  } else if (h % 4 == 0 && h <= 4 * 512 * 6) {
+    rmsnorm_bwd_reg_kernel<512, 6, 1><<<chunks, 512, 0, s>>>(x, (const __nv_bfloat16*)scale, g, resid, out,
+                                                             (__nv_bfloat16*)out_bf, inv_buf, partial, rows, h, rpc);
+  } else {
+    rmsnorm_bwd_kernel<<<grid_for(rows, 8), 256, 0, s>>>(x, (const __nv_bfloat16*)scale, g, resid, out,
+                                                         (__nv_bfloat16*)out_bf, inv_buf, rows, h);
+    dim3 grid((h + 255) / 256, chunks);
+    norm_scale_partial_kernel<<<grid, 256, 0, s>>>(x, g, inv_buf, partial, rows, h, rpc);
+    hlm_count_launches(1);
+  }
+  norm_scale_reduce_kernel<<<(h + 31) / 32, 256, 0, s>>>(partial, dscale, chunks, h);
+  hlm_count_launches(2);
   HLM_CHECK_LAUNCH();
 }
 

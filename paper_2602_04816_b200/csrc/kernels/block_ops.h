@@ -5,7 +5,7 @@
 
 #include <cstdint>
 
-#define HLM_NORM_ROWS_PER_CHUNK 64
+#define HLM_NORM_ROWS_PER_CHUNK 8
 
 int hlm_ops_rmsnorm_fwd(const float* x, const void* scale, void* out, long long rows, int h, cudaStream_t s);
 int hlm_ops_rmsnorm_bwd(const float* x, const void* scale, const float* g, const float* resid, float* out,
