@@ -8,6 +8,7 @@
 #include <omp.h>
 #include <fcntl.h>
 #include <sys/mman.h>
+#include <sys/statvfs.h>
 #include <unistd.h>
 
 #include <chrono>
@@ -179,6 +180,16 @@ MasterStore::MasterStore(const ModelConfig& config, Dtype dtype, bool pin_shadow
         const size_t ver_bytes = align2m(specs.size() * static_cast<size_t>(world_) * sizeof(i64));
         map_bytes_ = kShmHeader + align2m(state_bytes_) + align2m(shadow_bytes_) + ver_bytes;
         if (rank_ == 0) {
+            // tmpfs pages are allocated on first touch: a store larger than the free space of
+            // /dev/shm would die of SIGBUS mid-initialisation, so refuse it up front
+            struct statvfs vs {};
+            if (statvfs("/dev/shm", &vs) == 0) {
+                const double avail = static_cast<double>(vs.f_bavail) * static_cast<double>(vs.f_frsize);
+                if (avail < static_cast<double>(map_bytes_))
+                    throw ConfigError("shared store: " + std::to_string(map_bytes_ >> 20) + " MiB needed but /dev/shm has " +
+                                      std::to_string(static_cast<long long>(avail) >> 20) +
+                                      " MiB free (remount /dev/shm larger or use fewer / smaller tiles)");
+            }
             shm_unlink(shm_name_.c_str());
             shm_fd_ = shm_open(shm_name_.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
             if (shm_fd_ < 0) throw ConfigError("shared store: shm_open(create) failed for " + shm_name_);
