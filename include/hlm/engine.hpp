@@ -125,6 +125,8 @@ private:
         i64 grad_op;
         i64 step = 0;   // engine step index (tail eligibility)
         i64 t = 0;      // Adam step index of the gradient (bias correction)
+        i64 count = 0;  // fp32 elements copied into the slab (the tile, or this rank's shard)
+        i64 pieces = 1; // D2H pieces, each with its own event (the optimizer starts on piece 0)
     };
     struct HostOpRecord {   // host-side Accum / OptStep, appended to the trace in finish_step
         i64 slab, layer, grad_op, step;   // step: the gradient's step (an earlier one for a tail tile)
@@ -167,6 +169,23 @@ private:
     void* ev_grad_ready_[2] = {};
     void* ev_gradbuf_free_[2] = {};
     std::vector<void*> ev_slab_done_;
+    // Large gradients land in pieces of kPieceElems: per slab, an event after the
+    // finiteness flag and one per piece, so the host Adam starts on the first piece
+    // instead of waiting for the whole tile (the head gradient is 2.2 GB at C2).
+    static constexpr i64 kPieceElems = i64(64) << 20;
+    i64 max_pieces_ = 1;
+    std::vector<void*> ev_slab_flag_;    // per slab
+    std::vector<void*> ev_piece_;        // per slab x max_pieces_
+    // The head tile is prefetched into a stream buffer during the forward, before
+    // block head_prefetch_at_ is issued: the first block from which every block is
+    // cached or HBM-resident (never touches a stream buffer). The optimizer worker
+    // orders the previous step's head right before that block, so the last tile the
+    // forward waits for is block L, not the 2 GB head.
+    bool head_prefetch_ = false;
+    i64 head_prefetch_at_ = 0;
+    int head_buf_ = -1;
+    i64 head_wop_ = -1;
+    i64 tail_key(i64 layer) const;      // forward-need order of a tile (optimizer priority)
     void* ev_step_start_ = nullptr;
     void* ev_step_end_ = nullptr;
     std::vector<void*> timing_events_;   // pairs per traced GPU op

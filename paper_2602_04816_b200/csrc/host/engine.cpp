@@ -82,6 +82,11 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
         ck(cudaEventRecord(E(ev_gradbuf_free_[i]), S(compute_)), "record");
     }
     for (i64 i = 0; i < pool_->size(); ++i) ev_slab_done_.push_back(new_event(false));
+    max_pieces_ = std::max<i64>(1, (pool_->slab_capacity() / 4 + kPieceElems - 1) / kPieceElems);
+    for (i64 i = 0; i < pool_->size(); ++i) {
+        ev_slab_flag_.push_back(new_event(false));
+        for (i64 k = 0; k < max_pieces_; ++k) ev_piece_.push_back(new_event(false));
+    }
     ck(cudaMalloc(&nf_dev_, static_cast<size_t>(pool_->size()) * 8), "cudaMalloc nf");
     ck(cudaHostAlloc(reinterpret_cast<void**>(&nf_host_), static_cast<size_t>(pool_->size()) * 8,
                      cudaHostAllocPortable),
@@ -145,7 +150,28 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
             q += (t.n_params() * 14 + 255) / 256 * 256;
         }
     }
+    // head prefetch: as early as possible, such that no block after the prefetch point
+    // uses a stream buffer (cached or HBM-resident), and at the latest before block L - 1
+    if (opts_.overlap_optimizer_tail && !m.tie_embeddings && m.k_ckpt == 1 && opts_.fused_recompute &&
+        m.layers >= 2) {
+        i64 at = m.layers + 1;
+        while (at > 1 && (cache_slot_of_[static_cast<size_t>(at - 1)] >= 0 ||
+                          resident_of_[static_cast<size_t>(at - 1)] >= 0))
+            --at;
+        if (at <= m.layers - 1) {
+            head_prefetch_ = true;
+            head_prefetch_at_ = at;
+        }
+    }
     if (opts_.threaded_accum) worker_ = std::thread([this] { worker_loop(); });
+}
+
+// Order in which the next forward needs the tiles (embedding, blocks, head); with
+// the head prefetch the head is needed right after block L - 2.
+i64 Engine::tail_key(i64 layer) const {
+    const ModelConfig& m = store_.config();
+    if (layer == m.head_tile_id() && head_prefetch_) return 2 * (head_prefetch_at_ - 1) + 1;
+    return 2 * layer;
 }
 
 Engine::~Engine() {
@@ -175,6 +201,8 @@ Engine::~Engine() {
         cudaEventDestroy(E(ev_gradbuf_free_[i]));
     }
     for (void* e : ev_slab_done_) cudaEventDestroy(E(e));
+    for (void* e : ev_slab_flag_) cudaEventDestroy(E(e));
+    for (void* e : ev_piece_) cudaEventDestroy(E(e));
     for (void* e : ev_cache_ready_) cudaEventDestroy(E(e));
     for (void* e : timing_events_) cudaEventDestroy(E(e));
     cudaStreamDestroy(S(h2d_));
@@ -364,17 +392,25 @@ void Engine::evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op) {
                                         static_cast<ncclComm_t>(opts_.comm_grad), S(d2h_)),
                    "reduce-scatter grads");
     }
-    // the reference's "all gradients finite before any mutation" check, on the GPU
+    // the reference's "all gradients finite before any mutation" check, on the GPU;
+    // its flag lands first, then the gradient in pieces (the optimizer starts on piece 0)
     ck_hlm(hlm_cuda_nonfinite(src, cnt, nf_dev_ + slab, d2h_), "nonfinite scan");
-    ck(cudaMemcpyAsync(pool_->data(slab), src, static_cast<size_t>(bytes), cudaMemcpyDeviceToHost, S(d2h_)),
-       "D2H grads");
     ck(cudaMemcpyAsync(nf_host_ + slab, nf_dev_ + slab, 8, cudaMemcpyDeviceToHost, S(d2h_)), "D2H nf flag");
+    ck(cudaEventRecord(E(ev_slab_flag_[static_cast<size_t>(slab)]), S(d2h_)), "record slab flag");
+    const i64 pieces = (cnt + kPieceElems - 1) / kPieceElems;
+    for (i64 k = 0; k < pieces; ++k) {
+        const i64 off = k * kPieceElems, len = std::min(kPieceElems, cnt - off);
+        ck(cudaMemcpyAsync(pool_->data(slab) + off, src + off, static_cast<size_t>(len) * 4, cudaMemcpyDeviceToHost,
+                           S(d2h_)),
+           "D2H grads");
+        ck(cudaEventRecord(E(ev_piece_[static_cast<size_t>(slab * max_pieces_ + k)]), S(d2h_)), "record piece");
+    }
     op_end(id, d2h_);
     ck(cudaEventRecord(E(ev_slab_done_[static_cast<size_t>(slab)]), S(d2h_)), "record slab done");
     ck(cudaEventRecord(E(ev_gradbuf_free_[gbuf]), S(d2h_)), "record grad buf free");
     {
         std::lock_guard<std::mutex> lk(mu_);
-        pending_.push_back({slab, tile_id, id, step_index_, step_t_});
+        pending_.push_back({slab, tile_id, id, step_index_, step_t_, cnt, pieces});
     }
     cv_.notify_all();
 }
@@ -383,32 +419,46 @@ void Engine::evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op) {
 // host_store.cpp:254-284 and the eager hook engine.cpp:136-148). Numerics do
 // not depend on inline vs threaded consumption nor on the slab count.
 void Engine::consume(const Pending& p) {
-    ck(cudaEventSynchronize(E(ev_slab_done_[static_cast<size_t>(p.slab)])), "slab sync");
+    LayerTile& tile = store_.tile(p.layer);
+    const i64 phys = store_.physical_index(p.layer);
+    const bool optimise = opts_.eager_optim && !opts_.skip_optimizer;
+    // fused (slab IS the gradient, one consumer): wait for the finiteness flag, then
+    // optimise piece by piece as the D2H lands; otherwise wait for the whole slab
+    const bool piecewise = optimise && store_.consumer_count(phys) == 1;
+    ck(cudaEventSynchronize(E(piecewise ? ev_slab_flag_[static_cast<size_t>(p.slab)]
+                                        : ev_slab_done_[static_cast<size_t>(p.slab)])),
+       "slab sync");
     pool_->mark_ready(p.slab);
     bool stop = false;
     const i64 id = pool_->pop_ready_blocking(&stop);
     if (id != p.slab) throw ProtocolError("slab FIFO order violated");
     if (opts_.accum_delay_us > 0) std::this_thread::sleep_for(std::chrono::microseconds(opts_.accum_delay_us));
     HostOpRecord rec{p.slab, p.layer, p.grad_op, p.step, now_us(), 0.0, false, 0.0, 0.0};
-    LayerTile& tile = store_.tile(p.layer);
-    const i64 phys = store_.physical_index(p.layer);
-    const bool optimise = opts_.eager_optim && !opts_.skip_optimizer;
     const unsigned long long bad = nf_host_[p.slab];
     if (bad != ~0ull && optimise) {
         const i64 base = opts_.comm_grad ? opts_.rank * shard_elems(tile.n_params()) : 0;
         throw NumericsError("non-finite gradient in layer " + std::to_string(tile.layer_id()) + " at element " +
                             std::to_string(base + static_cast<i64>(bad)) + "; step aborted");
     }
+    // fused piecewise Adam over [base, base + count): the tile, or this rank's shard
+    auto adam_pieces = [&](i64 base) {
+        rec.t1 = now_us();
+        rec.opt = true;
+        rec.topt0 = rec.t1;
+        const float* g = pool_->data(p.slab);
+        for (i64 k = 0; k < p.pieces; ++k) {
+            const i64 off = k * kPieceElems, len = std::min(kPieceElems, p.count - off);
+            ck(cudaEventSynchronize(E(ev_piece_[static_cast<size_t>(p.slab * max_pieces_ + k)])), "piece sync");
+            adam_step_range(tile, g + off, base + off, len, hyper_, p.t, /*prechecked=*/true);
+        }
+        tile.bump_version(opts_.rank);
+        rec.topt1 = now_us();
+    };
     if (opts_.comm_grad) {   // this rank's shard [begin, begin + cnt)
         const i64 cnt = shard_elems(tile.n_params()), begin = opts_.rank * cnt;
         const float* g = pool_->data(p.slab);
-        if (optimise && store_.consumer_count(phys) == 1) {
-            rec.t1 = now_us();
-            rec.opt = true;
-            rec.topt0 = rec.t1;
-            adam_step_range(tile, g, begin, cnt, hyper_, p.t, /*prechecked=*/true);
-            tile.bump_version(opts_.rank);
-            rec.topt1 = now_us();
+        if (piecewise) {
+            adam_pieces(begin);
         } else {
             float* dst = tile.grads() + begin;
             for (i64 i = 0; i < cnt; ++i) dst[i] = dst[i] + g[i];
@@ -427,13 +477,9 @@ void Engine::consume(const Pending& p) {
                 rec.topt1 = now_us();
             }
         }
-    } else if (optimise && store_.consumer_count(phys) == 1) {
+    } else if (piecewise) {
         // fused: the pinned slab IS the gradient; no store gradient region touched
-        rec.t1 = now_us();
-        rec.opt = true;
-        rec.topt0 = rec.t1;
-        adam_step_tile_from(tile, pool_->data(p.slab), hyper_, p.t, /*prechecked=*/true);
-        rec.topt1 = now_us();
+        adam_pieces(0);
     } else {
         accumulate_grads(tile, pool_->data(p.slab));
         rec.t1 = now_us();
@@ -508,16 +554,16 @@ void Engine::worker_loop() {
                 std::pair<int, i64> best_rank{3, 0};
                 i64 pos = 0;
                 for (auto it = pending_.begin(); it != pending_.end(); ++it, ++pos) {
-                    const cudaError_t q = cudaEventQuery(E(ev_slab_done_[static_cast<size_t>(it->slab)]));
+                    const cudaError_t q = cudaEventQuery(E(ev_slab_flag_[static_cast<size_t>(it->slab)]));
                     if (q == cudaErrorNotReady) continue;
                     if (q != cudaSuccess) (void)cudaGetLastError();   // surfaced by consume's synchronize
                     std::pair<int, i64> rank;
                     if (it->step < step_index_)
-                        rank = {0, it->layer};
+                        rank = {0, tail_key(it->layer)};
                     else if (!deferred_[static_cast<size_t>(it->layer)])
                         rank = {1, pos};
                     else
-                        rank = {2, it->layer};
+                        rank = {2, tail_key(it->layer)};
                     if (rank < best_rank) {
                         best_rank = rank;
                         best = it;
@@ -627,6 +673,7 @@ void Engine::begin_step(const Batch& batch) {
     timing_used_ = 0;
     next_buf_ = 0;
     next_gbuf_ = 0;
+    head_buf_ = -1;
     g_cur_ = 0;
     last_reader_[0] = last_reader_[1] = -1;
     last_accum_op_.assign(static_cast<size_t>(pool_->size()), -1);
@@ -697,6 +744,7 @@ void Engine::forward_streaming() {
     h_cur_ = h0;
     int roll = 0;
     for (i64 i = 1; i <= m.layers; ++i) {
+        if (head_prefetch_ && i == head_prefetch_at_) head_buf_ = stream_tile(m.head_tile_id(), &head_wop_);
         const bool res = is_resident(i);
         w_op = -1;
         const int buf = res ? -2 : stream_tile(i, &w_op, true);
@@ -743,7 +791,13 @@ void Engine::anchor_loss_async() {
         if (batch_.targets[static_cast<size_t>(t)] < 0 || batch_.targets[static_cast<size_t>(t)] >= m.vocab)
             throw std::out_of_range("ce_loss_and_grad: target id out of range");
     i64 w_op = 0;
-    const int buf = stream_tile(m.head_tile_id(), &w_op);
+    int buf = head_buf_;
+    if (buf >= 0) {   // prefetched during the forward
+        w_op = head_wop_;
+        head_buf_ = -1;
+    } else {
+        buf = stream_tile(m.head_tile_id(), &w_op);
+    }
     compute_wait_weights(buf);
     const int gb = next_grad_buf();
     StreamOp op;
@@ -1098,6 +1152,7 @@ StepResult Engine::train_step(const Batch& batch) {
             if (arena_.buffer_occupant(b) != -1) arena_.release_buffer(b);
         arena_.release_cache_slots();
         std::fill(cache_xfer_op_.begin(), cache_xfer_op_.end(), -1);
+        head_buf_ = -1;
         while (arena_.stack_depth() > 0) arena_.pop_acts();
         for (i64 i = 0; i <= store_.config().layers; i += store_.config().k_ckpt) {
             try {
