@@ -70,6 +70,10 @@ struct EngineOptions {
     // These are the tiles the next forward needs first and the host Adam would
     // finish last. sync() (and the destructor) copies them back into the store.
     i64 resident_blocks = 0;
+    // Vocab-chunked head: the head weight gradient is computed, copied and optimised
+    // in pieces of head_piece_vocab vocab rows (0 = auto, ~kPieceElems elements per
+    // piece when the head spans two or more; -1 = off). Eager untied single-GPU only.
+    i64 head_piece_vocab = 0;
     bool resident_embed = false;
 };
 
@@ -127,6 +131,7 @@ private:
         i64 t = 0;      // Adam step index of the gradient (bias correction)
         i64 count = 0;  // fp32 elements copied into the slab (the tile, or this rank's shard)
         i64 pieces = 1; // D2H pieces, each with its own event (the optimizer starts on piece 0)
+        i64 piece = kPieceElems;   // elements per piece
     };
     struct HostOpRecord {   // host-side Accum / OptStep, appended to the trace in finish_step
         i64 slab, layer, grad_op, step;   // step: the gradient's step (an earlier one for a tail tile)
@@ -186,6 +191,16 @@ private:
     int head_buf_ = -1;
     i64 head_wop_ = -1;
     i64 tail_key(i64 layer) const;      // forward-need order of a tile (optimizer priority)
+    // vocab-chunked head: vocab rows per piece (0 = off), certificate word, per-piece
+    // compute events, full-scan fallback flag per slab (device + pinned mirror)
+    i64 head_vc_ = 0;
+    unsigned long long* head_cert_dev_ = nullptr;
+    void* ev_head_cert_ = nullptr;
+    std::vector<void*> ev_head_chunk_;
+    unsigned long long* nf2_dev_ = nullptr;
+    unsigned long long* nf2_host_ = nullptr;
+    i64 acquire_slab(i64 bytes);        // back-pressure: blocks (worker) or consumes inline
+    void anchor_loss_pieces(int buf, i64 w_op);
     void* ev_step_start_ = nullptr;
     void* ev_step_end_ = nullptr;
     std::vector<void*> timing_events_;   // pairs per traced GPU op

@@ -129,6 +129,25 @@ int hlm_cuda_rope_table(float* dev_cos, float* dev_sin, int64_t seq, int64_t hea
  * loss_rows[r] = (logz_r - logit_r[target_r]) * inv_rows; the caller sums.
  * inv_rows is 1/global_rows under data parallelism. */
 size_t hlm_cuda_head_ws_bytes(int64_t rows, int64_t hidden, int64_t vocab);
+/* Vocab-chunked head, the same numbers in pieces (engine's piecewise head gradient):
+ * hlm_cuda_head_stats: logits row chunk by row chunk -> per-row max and 1/z kept in
+ * ws, loss_rows as hlm_cuda_head_loss; then *cert = ~0 when every element of the
+ * head weight gradient is provably finite before it is computed (finite row
+ * statistics and rows * inv_rows * max|x| far below FLT_MAX), else
+ * HLM_HEAD_UNCERTIFIED (the caller scans the gradient instead).
+ * hlm_cuda_head_grad_chunk: vocab rows [v0, v0 + vc): logits chunk, d_logits,
+ * d_head rows [v0, v0 + vc) of the (vocab, hidden) fp32 gradient (stored, or added
+ * when accumulate_d_head), d_x (+)= d_logits_c . head_c (stored when
+ * accumulate_d_x == 0). Same ws as hlm_cuda_head_loss, after hlm_cuda_head_stats.
+ * hlm_cuda_head_chunk_vocab: the largest vc (multiple of 128) the ws holds. */
+#define HLM_HEAD_UNCERTIFIED 0xFFFFFFFFFFFFFFFEull
+int hlm_cuda_head_stats(int64_t rows, int64_t hidden, int64_t vocab, const void* head, const float* x,
+                        const int32_t* targets, float inv_rows, float* loss_rows, unsigned long long* cert,
+                        void* ws, void* stream);
+int hlm_cuda_head_grad_chunk(int64_t rows, int64_t hidden, int64_t vocab, const void* head,
+                             const int32_t* targets, float inv_rows, int64_t v0, int64_t vc, float* d_x,
+                             int accumulate_d_x, float* d_head, int accumulate_d_head, void* ws, void* stream);
+int64_t hlm_cuda_head_chunk_vocab(int64_t rows, int64_t vocab);
 int hlm_cuda_head_loss(int64_t rows, int64_t hidden, int64_t vocab, const void* head,
                        const float* x, const int32_t* targets, float inv_rows, float* d_x,
                        float* d_head, int accumulate_d_head, float* loss_rows, void* ws,
@@ -219,6 +238,10 @@ typedef struct HlmEngineOptions {
    * master / m / v and BF16 weights on the GPU (device Adam, no streaming) */
   int32_t resident_embed;
   int64_t resident_blocks;
+  /* vocab rows per piece of the head weight gradient (vocab-chunked head, each
+   * piece's D2H and host Adam start while the next piece is computed):
+   * 0 = auto (~64 Mi elements per piece when the head spans two or more), -1 = off */
+  int64_t head_piece_vocab;
 } HlmEngineOptions;
 
 typedef struct HlmStepResult {

@@ -84,6 +84,13 @@ def _setup_block_protos(L):
     L.hlm_cuda_head_ws_bytes.argtypes = [ctypes.c_int64] * 3
     L.hlm_cuda_head_loss.argtypes = [ctypes.c_int64] * 3 + [_vp, _vp, _vp, ctypes.c_float, _vp, _vp,
                                                             ctypes.c_int, _vp, _vp, _vp]
+    L.hlm_cuda_head_stats.argtypes = [ctypes.c_int64] * 3 + [_vp, _vp, _vp, ctypes.c_float, _vp, _vp, _vp,
+                                                             _vp]
+    L.hlm_cuda_head_grad_chunk.argtypes = [ctypes.c_int64] * 3 + [_vp, _vp, ctypes.c_float, ctypes.c_int64,
+                                                                  ctypes.c_int64, _vp, ctypes.c_int, _vp,
+                                                                  ctypes.c_int, _vp, _vp]
+    L.hlm_cuda_head_chunk_vocab.restype = ctypes.c_int64
+    L.hlm_cuda_head_chunk_vocab.argtypes = [ctypes.c_int64] * 2
     L.hlm_cuda_embed_fwd.argtypes = [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                      _vp, _vp]
     L.hlm_cuda_embed_bwd.argtypes = [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,

@@ -9,6 +9,7 @@
 // fp32 flat tile gradient in the same order, ready for the D2H copy.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <string>
@@ -337,7 +338,97 @@ size_t hlm_cuda_head_ws_bytes(int64_t rows, int64_t hidden, int64_t vocab) {
   c.take<float>(cr * ldv);
   c.take<uint16_t>(cr * ldv);
   c.take<int>(4);
+  c.take<float>(2 * rows);   // vocab-chunked head: per-row (max, 1/z)
   return c.off;
+}
+
+int64_t hlm_cuda_head_chunk_vocab(int64_t rows, int64_t vocab) {
+  if (rows <= 0 || vocab <= 0) return 0;
+  const i64 ldv = padded_vocab(vocab), cr = head_chunk_rows(rows, vocab);
+  const i64 cap = cr * ldv / rows;   // padded columns per row the logits / d_logits regions hold
+  if (cap >= vocab) return vocab;
+  return cap >= 128 ? cap / 128 * 128 : std::max<i64>(8, cap / 8 * 8);
+}
+
+namespace {
+struct HeadWs {
+  uint16_t* x_bf;
+  float* logits;
+  uint16_t* dl;
+  int* err;
+  float* stats;
+};
+HeadWs carve_head(void* ws, i64 rows, i64 hidden, i64 vocab) {
+  const i64 ldv = padded_vocab(vocab), cr = head_chunk_rows(rows, vocab);
+  Carver c(ws);
+  HeadWs w;
+  w.x_bf = c.take<uint16_t>(rows * hidden);
+  w.logits = c.take<float>(cr * ldv);
+  w.dl = c.take<uint16_t>(cr * ldv);
+  w.err = c.take<int>(4);
+  w.stats = c.take<float>(2 * rows);
+  return w;
+}
+}  // namespace
+
+int hlm_cuda_head_stats(int64_t rows, int64_t hidden, int64_t vocab, const void* head, const float* x,
+                        const int32_t* targets, float inv_rows, float* loss_rows, unsigned long long* cert,
+                        void* ws, void* stream) {
+  return guarded([&] {
+    if (rows <= 0 || hidden <= 0 || vocab <= 0 || hidden % 8)
+      throw Failure{"head: bad dims (hidden must be a multiple of 8)", HLM_ERR_CONFIG};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const i64 ldv = padded_vocab(vocab), cr = head_chunk_rows(rows, vocab);
+    HeadWs w = carve_head(ws, rows, hidden, vocab);
+    chk(hlm_ops_cast_bf16(x, w.x_bf, rows * hidden, s), "cast x");
+    for (i64 r0 = 0; r0 < rows; r0 += cr) {
+      const i64 n = rows - r0 < cr ? rows - r0 : cr;
+      chk_gemm(gdesc((int)n, (int)vocab, (int)hidden, w.x_bf + r0 * hidden, hidden, 0, head, hidden, 0, w.logits,
+                     ldv, HLM_EPI_F32),
+               s, "head fwd");
+      chk(hlm_ops_ce_stats(w.logits, ldv, targets + r0, w.stats + 2 * r0, loss_rows + r0, n, (int)vocab, inv_rows,
+                           w.err, s),
+          "ce stats");
+    }
+    // |d_head| <= rows * inv_rows * 1.01 * max|x|: certify far below FLT_MAX
+    const double lim = 1e36 / std::max(1.0, static_cast<double>(rows) * static_cast<double>(inv_rows));
+    chk(hlm_ops_head_certify(w.x_bf, rows * hidden, w.stats, rows, static_cast<float>(std::min(lim, 1e36)), cert,
+                             s),
+        "head certificate");
+  });
+}
+
+int hlm_cuda_head_grad_chunk(int64_t rows, int64_t hidden, int64_t vocab, const void* head,
+                             const int32_t* targets, float inv_rows, int64_t v0, int64_t vc, float* d_x,
+                             int accumulate_d_x, float* d_head, int accumulate_d_head, void* ws, void* stream) {
+  return guarded([&] {
+    if (rows <= 0 || hidden <= 0 || vocab <= 0 || hidden % 8)
+      throw Failure{"head: bad dims (hidden must be a multiple of 8)", HLM_ERR_CONFIG};
+    if (v0 < 0 || vc <= 0 || v0 + vc > vocab || vc > hlm_cuda_head_chunk_vocab(rows, vocab))
+      throw Failure{"head: bad vocab chunk", HLM_ERR_ARGS};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    HeadWs w = carve_head(ws, rows, hidden, vocab);
+    const i64 ld = (vc + 7) / 8 * 8;
+    const uint16_t* hc = static_cast<const uint16_t*>(head) + v0 * hidden;
+    const int R = (int)rows, Hh = (int)hidden, Vc = (int)vc;
+    chk_gemm(gdesc(R, Vc, Hh, w.x_bf, hidden, 0, hc, hidden, 0, w.logits, ld, HLM_EPI_F32), s, "head fwd chunk");
+    chk(hlm_ops_ce_grad_chunk(w.logits, ld, targets, w.stats, w.dl, ld, rows, (int)v0, Vc, inv_rows, s),
+        "ce grad chunk");
+    HlmGemmDesc gw = gdesc(Vc, Hh, R, w.dl, ld, 1, w.x_bf, hidden, 1, d_head + v0 * hidden, hidden,
+                           accumulate_d_head ? HLM_EPI_F32_ADD : HLM_EPI_F32);
+    if (accumulate_d_head) {
+      gw.R = d_head + v0 * hidden;
+      gw.ldr = hidden;
+    }
+    chk_gemm(gw, s, "head wgrad chunk");
+    HlmGemmDesc gd = gdesc(R, Hh, Vc, w.dl, ld, 0, hc, hidden, 1, d_x, hidden,
+                           accumulate_d_x ? HLM_EPI_F32_ADD : HLM_EPI_F32);
+    if (accumulate_d_x) {
+      gd.R = d_x;
+      gd.ldr = hidden;
+    }
+    chk_gemm(gd, s, "head dgrad chunk");
+  });
 }
 
 // Chunked over rows: per chunk, logits = x_c . head^T (fp32), CE -> d_logits_c

@@ -110,6 +110,7 @@ hlm::EngineOptions to_opts(const HlmEngineOptions* o) {
         e.host_threads = o->host_threads;
         e.resident_embed = o->resident_embed != 0;
         e.resident_blocks = o->resident_blocks;
+        e.head_piece_vocab = o->head_piece_vocab;
     }
     return e;
 }

@@ -83,6 +83,24 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
     }
     for (i64 i = 0; i < pool_->size(); ++i) ev_slab_done_.push_back(new_event(false));
     max_pieces_ = std::max<i64>(1, (pool_->slab_capacity() / 4 + kPieceElems - 1) / kPieceElems);
+    // vocab-chunked head (single GPU, untied): pieces of head_vc_ vocab rows
+    if (!opts_.comm_grad && !m.tie_embeddings && opts_.head_piece_vocab >= 0) {
+        i64 vc = opts_.head_piece_vocab;
+        if (vc == 0 && m.embed_params() >= 2 * kPieceElems) vc = std::max<i64>(128, kPieceElems / m.hidden / 128 * 128);
+        if (vc > 0) vc = std::min<i64>(vc, hlm_cuda_head_chunk_vocab(m.rows(), m.vocab));
+        if (vc > 0 && vc < m.vocab) head_vc_ = vc;
+    }
+    if (head_vc_ > 0) {
+        const i64 chunks = (m.vocab + head_vc_ - 1) / head_vc_;
+        max_pieces_ = std::max(max_pieces_, chunks);
+        for (i64 k = 0; k < chunks; ++k) ev_head_chunk_.push_back(new_event(false));
+        ev_head_cert_ = new_event(false);
+        ck(cudaMalloc(&head_cert_dev_, 8), "cudaMalloc head certificate");
+    }
+    ck(cudaMalloc(&nf2_dev_, static_cast<size_t>(pool_->size()) * 8), "cudaMalloc nf2");
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&nf2_host_), static_cast<size_t>(pool_->size()) * 8,
+                     cudaHostAllocPortable),
+       "cudaHostAlloc nf2");
     for (i64 i = 0; i < pool_->size(); ++i) {
         ev_slab_flag_.push_back(new_event(false));
         for (i64 k = 0; k < max_pieces_; ++k) ev_piece_.push_back(new_event(false));
@@ -203,6 +221,11 @@ Engine::~Engine() {
     for (void* e : ev_slab_done_) cudaEventDestroy(E(e));
     for (void* e : ev_slab_flag_) cudaEventDestroy(E(e));
     for (void* e : ev_piece_) cudaEventDestroy(E(e));
+    for (void* e : ev_head_chunk_) cudaEventDestroy(E(e));
+    if (ev_head_cert_) cudaEventDestroy(E(ev_head_cert_));
+    if (head_cert_dev_) cudaFree(head_cert_dev_);
+    if (nf2_dev_) cudaFree(nf2_dev_);
+    if (nf2_host_) cudaFreeHost(nf2_host_);
     for (void* e : ev_cache_ready_) cudaEventDestroy(E(e));
     for (void* e : timing_events_) cudaEventDestroy(E(e));
     cudaStreamDestroy(S(h2d_));
@@ -351,12 +374,10 @@ int Engine::next_grad_buf() {
     return gb;
 }
 
-// reference engine.cpp:103-121: acquire a slab (inline back-pressure
-// consumes the oldest READY slab), D2H the fp32 gradient, emit GradXfer.
-void Engine::evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op) {
-    ck(cudaEventRecord(E(ev_grad_ready_[gbuf]), S(compute_)), "record grad ready");
-    const i64 cnt = opts_.comm_grad ? shard_elems(n_params) : n_params;
-    const i64 bytes = 4 * cnt;
+// A FREE slab of at least `bytes` (reference SlabPool::acquire,
+// host_store.cpp:197-218): blocks on the worker, or consumes the oldest READY
+// slab inline.
+i64 Engine::acquire_slab(i64 bytes) {
     i64 slab = pool_->try_acquire(bytes);
     while (slab < 0) {
         if (opts_.threaded_accum) {
@@ -374,6 +395,16 @@ void Engine::evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op) {
             slab = pool_->try_acquire(bytes);
         }
     }
+    return slab;
+}
+
+// reference engine.cpp:103-121: acquire a slab (inline back-pressure
+// consumes the oldest READY slab), D2H the fp32 gradient, emit GradXfer.
+void Engine::evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op) {
+    ck(cudaEventRecord(E(ev_grad_ready_[gbuf]), S(compute_)), "record grad ready");
+    const i64 cnt = opts_.comm_grad ? shard_elems(n_params) : n_params;
+    const i64 bytes = 4 * cnt;
+    const i64 slab = acquire_slab(bytes);
     pool_->mark_in_flight(slab, tile_id, bytes);
     StreamOp op;
     op.stream = StreamId::D2H;
@@ -434,7 +465,11 @@ void Engine::consume(const Pending& p) {
     if (id != p.slab) throw ProtocolError("slab FIFO order violated");
     if (opts_.accum_delay_us > 0) std::this_thread::sleep_for(std::chrono::microseconds(opts_.accum_delay_us));
     HostOpRecord rec{p.slab, p.layer, p.grad_op, p.step, now_us(), 0.0, false, 0.0, 0.0};
-    const unsigned long long bad = nf_host_[p.slab];
+    unsigned long long bad = nf_host_[p.slab];
+    if (bad == HLM_HEAD_UNCERTIFIED) {   // vocab-chunked head without a certificate: the full scan
+        ck(cudaEventSynchronize(E(ev_slab_done_[static_cast<size_t>(p.slab)])), "slab sync");
+        bad = nf2_host_[p.slab];
+    }
     if (bad != ~0ull && optimise) {
         const i64 base = opts_.comm_grad ? opts_.rank * shard_elems(tile.n_params()) : 0;
         throw NumericsError("non-finite gradient in layer " + std::to_string(tile.layer_id()) + " at element " +
@@ -447,7 +482,7 @@ void Engine::consume(const Pending& p) {
         rec.topt0 = rec.t1;
         const float* g = pool_->data(p.slab);
         for (i64 k = 0; k < p.pieces; ++k) {
-            const i64 off = k * kPieceElems, len = std::min(kPieceElems, p.count - off);
+            const i64 off = k * p.piece, len = std::min(p.piece, p.count - off);
             ck(cudaEventSynchronize(E(ev_piece_[static_cast<size_t>(p.slab * max_pieces_ + k)])), "piece sync");
             adam_step_range(tile, g + off, base + off, len, hyper_, p.t, /*prechecked=*/true);
         }
@@ -686,7 +721,6 @@ void Engine::begin_step(const Batch& batch) {
             if (!deferred_[static_cast<size_t>(t)] && resident_of_[static_cast<size_t>(t)] < 0) ++regular_left_;
         tail_open_ = !opts_.overlap_optimizer_tail || regular_left_ == 0;
         if (!opts_.overlap_optimizer_tail) pending_.clear();
-        host_ops_.clear();
         consumers_left_.assign(static_cast<size_t>(store_.physical_tiles()), 0);
         for (i64 p = 0; p < store_.physical_tiles(); ++p)
             consumers_left_[static_cast<size_t>(p)] = store_.consumer_count(p);
@@ -799,6 +833,12 @@ void Engine::anchor_loss_async() {
         buf = stream_tile(m.head_tile_id(), &w_op);
     }
     compute_wait_weights(buf);
+    if (head_vc_ > 0) {
+        anchor_loss_pieces(buf, w_op);
+        if (m.layers % m.k_ckpt == 0) arena_.release_checkpoint(m.layers);
+        phase_ = Phase::Backward;
+        return;
+    }
     const int gb = next_grad_buf();
     StreamOp op;
     op.stream = StreamId::Compute;
@@ -831,6 +871,92 @@ void Engine::anchor_loss_async() {
     evacuate(m.head_tile_id(), gb, m.embed_params(), lb_op);
     if (m.layers % m.k_ckpt == 0) arena_.release_checkpoint(m.layers);
     phase_ = Phase::Backward;
+}
+
+// Vocab-chunked head (same numbers as hlm_cuda_head_loss, in pieces): pass 1
+// (row statistics, loss, finiteness certificate) as the head Forward, then per
+// piece of head_vc_ vocab rows a LocalBackward (logits, d_logits, d_head rows,
+// d_x accumulation) whose d_head rows go to the slab at once, so the host Adam of
+// the head starts one piece after the statistics instead of after the whole head.
+void Engine::anchor_loss_pieces(int buf, i64 w_op) {
+    const ModelConfig& m = store_.config();
+    const i64 T = m.rows(), V = m.vocab, h = m.hidden, n = m.embed_params();
+    const i64 head = m.head_tile_id();
+    const float inv = 1.0f / static_cast<float>(T * opts_.world);
+    const void* W = weights_ptr(buf);
+    const int gb = next_grad_buf();
+    StreamOp op;
+    op.stream = StreamId::Compute;
+    op.kind = OpKind::Forward;
+    op.layer = head;
+    op.buf = buf;
+    op.flops = fwd_flops(n, T);
+    op.deps.push_back(w_op);
+    const i64 fid = op_begin(op, compute_);
+    ck_hlm(hlm_cuda_head_stats(T, h, V, W, h_cur_, arena_.targets(), inv, arena_.loss_rows(), head_cert_dev_,
+                               arena_.head_ws(), compute_),
+           "head_stats");
+    op_end(fid, compute_);
+    ck(cudaEventRecord(E(ev_head_cert_), S(compute_)), "record head certificate");
+    ck(cudaMemcpyAsync(loss_host_ + 2 * T, arena_.loss_rows(), static_cast<size_t>(T) * 4, cudaMemcpyDeviceToHost,
+                       S(compute_)),
+       "D2H loss");
+    ck(cudaMemcpyAsync(loss_host_ + 3 * T, arena_.err_flag(), 4, cudaMemcpyDeviceToHost, S(compute_)), "D2H err");
+
+    const i64 bytes = 4 * n;
+    const i64 slab = acquire_slab(bytes);
+    pool_->mark_in_flight(slab, head, bytes);
+    ck(cudaStreamWaitEvent(S(d2h_), E(ev_head_cert_), 0), "wait head certificate");
+    ck(cudaMemcpyAsync(nf_host_ + slab, head_cert_dev_, 8, cudaMemcpyDeviceToHost, S(d2h_)), "D2H certificate");
+    ck(cudaEventRecord(E(ev_slab_flag_[static_cast<size_t>(slab)]), S(d2h_)), "record slab flag");
+    const i64 pieces = (V + head_vc_ - 1) / head_vc_;
+    i64 first_gx = -1, last_lb = -1;
+    float* g = arena_.grad_out(gb);
+    for (i64 k = 0; k < pieces; ++k) {
+        const i64 v0 = k * head_vc_, vc = std::min(head_vc_, V - v0);
+        StreamOp lb;
+        lb.stream = StreamId::Compute;
+        lb.kind = OpKind::LocalBackward;
+        lb.layer = head;
+        lb.buf = buf;
+        lb.flops = bwd_flops(n, T) * vc / V;
+        lb.deps.push_back(w_op);
+        const i64 lbid = op_begin(lb, compute_);
+        ck_hlm(hlm_cuda_head_grad_chunk(T, h, V, W, arena_.targets(), inv, v0, vc, arena_.g_roll(g_cur_), k > 0, g, 0,
+                                        arena_.head_ws(), compute_),
+               "head_grad_chunk");
+        op_end(lbid, compute_);
+        ck(cudaEventRecord(E(ev_head_chunk_[static_cast<size_t>(k)]), S(compute_)), "record head chunk");
+        StreamOp gx;
+        gx.stream = StreamId::D2H;
+        gx.kind = OpKind::GradXfer;
+        gx.layer = head;
+        gx.slab = slab;
+        gx.bytes = 4 * vc * h;
+        gx.deps.push_back(lbid);
+        if (k == 0 && last_accum_op_[static_cast<size_t>(slab)] >= 0)
+            gx.deps.push_back(last_accum_op_[static_cast<size_t>(slab)]);
+        ck(cudaStreamWaitEvent(S(d2h_), E(ev_head_chunk_[static_cast<size_t>(k)]), 0), "wait head chunk");
+        const i64 gxid = op_begin(std::move(gx), d2h_);
+        ck(cudaMemcpyAsync(pool_->data(slab) + v0 * h, g + v0 * h, static_cast<size_t>(vc * h) * 4,
+                           cudaMemcpyDeviceToHost, S(d2h_)),
+           "D2H head piece");
+        op_end(gxid, d2h_);
+        ck(cudaEventRecord(E(ev_piece_[static_cast<size_t>(slab * max_pieces_ + k)]), S(d2h_)), "record piece");
+        if (k == 0) first_gx = gxid;
+        last_lb = lbid;
+    }
+    compute_done_with(buf, last_lb);
+    // the certificate's fallback: the full scan of the head gradient
+    ck_hlm(hlm_cuda_nonfinite(g, n, nf2_dev_ + slab, d2h_), "nonfinite scan (head)");
+    ck(cudaMemcpyAsync(nf2_host_ + slab, nf2_dev_ + slab, 8, cudaMemcpyDeviceToHost, S(d2h_)), "D2H nf2 flag");
+    ck(cudaEventRecord(E(ev_slab_done_[static_cast<size_t>(slab)]), S(d2h_)), "record slab done");
+    ck(cudaEventRecord(E(ev_gradbuf_free_[gb]), S(d2h_)), "record grad buf free");
+    {
+        std::lock_guard<std::mutex> lk(mu_);
+        pending_.push_back({slab, head, first_gx, step_index_, step_t_, n, pieces, head_vc_ * h});
+    }
+    cv_.notify_all();
 }
 
 // reference engine.cpp:279-368 (K-block recompute onto the LIFO stack, then
@@ -1021,9 +1147,9 @@ StepResult Engine::finish_step() {
     // host ops into the trace, in consumption order
     std::vector<i64> accum_ids;
     std::vector<HostOpRecord> recs;
-    {
+    {   // records completing after this point land in the next step's trace
         std::lock_guard<std::mutex> lk(mu_);
-        recs = host_ops_;
+        recs.swap(host_ops_);
     }
     for (const auto& rec : recs) {
         StreamOp op;

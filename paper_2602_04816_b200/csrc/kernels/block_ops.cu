@@ -16,6 +16,7 @@
 #include <cstdlib>
 
 #include "block_ops.h"
+#include "hlm_cuda.h"
 
 namespace {
 
@@ -579,6 +580,104 @@ __global__ void __launch_bounds__(THREADS) ce_kernel(const float* __restrict__ l
   }
 }
 
+// Vocab-chunked head, pass 1: the row statistics of ce_kernel (same max / sum
+// order, so d_logits below equal ce_kernel's bit for bit) -> stats[r] = (max,
+// 1/z), loss_row[r]; the d_logits are produced later per vocab chunk.
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) ce_stats_kernel(const float* __restrict__ logits, long long ld_in,
+                                                           const int32_t* __restrict__ tgt,
+                                                           float2* __restrict__ stats, float* __restrict__ loss_row,
+                                                           int vocab, float inv_rows, int* __restrict__ err) {
+  __shared__ float red[THREADS / 32];
+  __shared__ float bcast;
+  const long long r = blockIdx.x;
+  const float* l = logits + r * ld_in;
+  const int lane = threadIdx.x & 31, w = threadIdx.x / 32;
+  float mx = -INFINITY;
+  for (int v = threadIdx.x; v < vocab; v += THREADS) mx = fmaxf(mx, l[v]);
+  mx = warp_max(mx);
+  if (lane == 0) red[w] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = red[0];
+    for (int i = 1; i < THREADS / 32; ++i) m = fmaxf(m, red[i]);
+    bcast = m;
+  }
+  __syncthreads();
+  mx = bcast;
+  float z = 0.f;
+  for (int v = threadIdx.x; v < vocab; v += THREADS) z += __expf(l[v] - mx);
+  z = warp_sum(z);
+  __syncthreads();
+  if (lane == 0) red[w] = z;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float sz = 0.f;
+    for (int i = 0; i < THREADS / 32; ++i) sz += red[i];
+    const int t = tgt[r];
+    stats[r] = make_float2(mx, 1.0f / sz);
+    if (t < 0 || t >= vocab) {
+      atomicOr(err, 2);
+      loss_row[r] = 0.f;
+    } else {
+      loss_row[r] = (logf(sz) + mx - l[t]) * inv_rows;
+    }
+  }
+}
+
+// Pass 2 for vocab columns [v0, v0 + vc): d_logits (bf16, row stride ld_out,
+// zero in the padding columns vc..ld_out) from the chunk's logits (stride
+// ld_in) and the pass-1 statistics: the formula of ce_kernel.
+__global__ void ce_grad_chunk_kernel(const float* __restrict__ logits, long long ld_in,
+                                     const int32_t* __restrict__ tgt, const float2* __restrict__ stats,
+                                     __nv_bfloat16* __restrict__ dl, long long ld_out, long long rows, int v0,
+                                     int vc, float inv_rows) {
+  const long long per_row = ld_out / 2;   // bf16 pairs
+  const long long n = rows * per_row;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const long long r = i / per_row;
+    const int c = (int)(i - r * per_row) * 2;
+    const float2 st = stats[r];
+    const int t = tgt[r] - v0;
+    float p0 = 0.f, p1 = 0.f;
+    if (c < vc) {
+      p0 = __expf(logits[r * ld_in + c] - st.x) * st.y * inv_rows;
+      if (c == t) p0 -= inv_rows;
+    }
+    if (c + 1 < vc) {
+      p1 = __expf(logits[r * ld_in + c + 1] - st.x) * st.y * inv_rows;
+      if (c + 1 == t) p1 -= inv_rows;
+    }
+    reinterpret_cast<__nv_bfloat162*>(dl + r * ld_out)[c / 2] = __floats2bfloat162_rn(p0, p1);
+  }
+}
+
+// Finiteness certificate of the head weight gradient, issued before any of it
+// exists: with every d_logits element in [-inv_rows, inv_rows] (up to bf16
+// rounding; finite when every row's statistics are), |d_head[v][j]| =
+// |sum_t d_logits[t][v] x[t][j]| <= rows * inv_rows * 1.01 * max|x|. So when the
+// row statistics are finite and rows * inv_rows * max|x| stays far below FLT_MAX,
+// no element of d_head can be non-finite and *word keeps ~0 ("none"); otherwise
+// it becomes HLM_HEAD_UNCERTIFIED and the caller falls back to scanning d_head.
+__global__ void head_certify_kernel(const __nv_bfloat16* __restrict__ x, long long n,
+                                    const float2* __restrict__ stats, long long rows, float limit,
+                                    unsigned long long* word) {
+  bool bad = false;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n / 2; i += stride) {
+    const __nv_bfloat162 v = reinterpret_cast<const __nv_bfloat162*>(x)[i];
+    const float a = __low2float(v), b = __high2float(v);
+    bad |= !(fabsf(a) <= limit) || !(fabsf(b) <= limit);   // NaN and Inf fail the comparison
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) bad |= !(fabsf(__bfloat162float(x[n - 1])) <= limit);
+  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += stride) {
+    const float2 st = stats[r];
+    bad |= !isfinite(st.x) || !isfinite(st.y);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(word, HLM_HEAD_UNCERTIFIED);
+}
+
 // ------------------------------------------------------------------ finiteness
 // first[0] = min index of a non-finite element (INT64 max when none): the
 // reference's "validate before any mutation" check (host_store.cpp:340-345),
@@ -933,6 +1032,32 @@ int hlm_ops_ce(const float* logits, long long ld_in, const int32_t* tgt, void* d
   ce_kernel<512><<<(unsigned)rows, 512, 0, s>>>(logits, ld_in, tgt, (__nv_bfloat16*)dl, ld_out, loss_row, vocab,
                                                 inv_rows, err);
   hlm_count_launches(5);
+  HLM_CHECK_LAUNCH();
+}
+
+int hlm_ops_ce_stats(const float* logits, long long ld_in, const int32_t* tgt, void* stats, float* loss_row,
+                     long long rows, int vocab, float inv_rows, int* err, cudaStream_t s) {
+  ce_stats_kernel<512><<<(unsigned)rows, 512, 0, s>>>(logits, ld_in, tgt, (float2*)stats, loss_row, vocab,
+                                                      inv_rows, err);
+  hlm_count_launches(1);
+  HLM_CHECK_LAUNCH();
+}
+
+int hlm_ops_ce_grad_chunk(const float* logits, long long ld_in, const int32_t* tgt, const void* stats, void* dl,
+                          long long ld_out, long long rows, int v0, int vc, float inv_rows, cudaStream_t s) {
+  if (ld_out % 2) return 2;
+  ce_grad_chunk_kernel<<<grid_for(rows * (ld_out / 2), 256), 256, 0, s>>>(
+      logits, ld_in, tgt, (const float2*)stats, (__nv_bfloat16*)dl, ld_out, rows, v0, vc, inv_rows);
+  hlm_count_launches(1);
+  HLM_CHECK_LAUNCH();
+}
+
+int hlm_ops_head_certify(const void* x_bf, long long n, const void* stats, long long rows, float limit,
+                         unsigned long long* word, cudaStream_t s) {
+  if (cudaMemsetAsync(word, 0xFF, 8, s) != cudaSuccess) return 1;
+  head_certify_kernel<<<grid_for(n / 2 + 1, 256), 256, 0, s>>>((const __nv_bfloat16*)x_bf, n,
+                                                               (const float2*)stats, rows, limit, word);
+  hlm_count_launches(1);
   HLM_CHECK_LAUNCH();
 }
 

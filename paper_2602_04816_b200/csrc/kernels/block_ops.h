@@ -22,6 +22,15 @@ int hlm_ops_embed_bwd(const int32_t* row_ptr, const int32_t* pos, const float* g
                       int h, int accumulate, cudaStream_t s);
 int hlm_ops_ce(const float* logits, long long ld_in, const int32_t* tgt, void* dl, long long ld_out,
                float* loss_row, long long rows, int vocab, float inv_rows, int* err, cudaStream_t s);
+// Vocab-chunked head (hlm_cuda_head_stats / hlm_cuda_head_grad_chunk): pass-1 row
+// statistics (float2 max, 1/z per row), pass-2 d_logits of one vocab chunk, and
+// the up-front finiteness certificate of d_head (word: ~0 or HLM_HEAD_UNCERTIFIED).
+int hlm_ops_ce_stats(const float* logits, long long ld_in, const int32_t* tgt, void* stats, float* loss_row,
+                     long long rows, int vocab, float inv_rows, int* err, cudaStream_t s);
+int hlm_ops_ce_grad_chunk(const float* logits, long long ld_in, const int32_t* tgt, const void* stats, void* dl,
+                          long long ld_out, long long rows, int v0, int vc, float inv_rows, cudaStream_t s);
+int hlm_ops_head_certify(const void* x_bf, long long n, const void* stats, long long rows, float limit,
+                         unsigned long long* word, cudaStream_t s);
 int hlm_ops_attention_fwd_generic(const void* q, const void* k, const void* v, void* o, float* lse, int B, int S,
                                   int H, int hd, int ld, cudaStream_t s);
 int hlm_ops_attention_bwd_generic(const void* q, const void* k, const void* v, const void* o, const void* dout,
