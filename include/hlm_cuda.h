@@ -141,6 +141,16 @@ size_t hlm_cuda_head_ws_bytes(int64_t rows, int64_t hidden, int64_t vocab);
  * accumulate_d_x == 0). Same ws as hlm_cuda_head_loss, after hlm_cuda_head_stats.
  * hlm_cuda_head_chunk_vocab: the largest vc (multiple of 128) the ws holds. */
 #define HLM_HEAD_UNCERTIFIED 0xFFFFFFFFFFFFFFFEull
+
+/* ------------------------------------------------------------------ kernel timer
+ * Per-launch CUDA-event timing of the hot kernels inside a timed region (the
+ * bench's roofline.achieved): when enabled, every GEMM / attention launch is
+ * bracketed by an event pair on its own stream and its algorithmic flops kept.
+ * collect() sums one kind (synchronises on its events); reset() recycles them. */
+enum { HLM_KTIMER_GEMM = 0, HLM_KTIMER_ATTN_FWD = 1, HLM_KTIMER_ATTN_BWD = 2 };
+int hlm_ktimer_enable(int on);
+int hlm_ktimer_collect(int kind, double* ms, double* flops, int64_t* launches);
+int hlm_ktimer_reset(void);
 int hlm_cuda_head_stats(int64_t rows, int64_t hidden, int64_t vocab, const void* head, const float* x,
                         const int32_t* targets, float inv_rows, float* loss_rows, unsigned long long* cert,
                         void* ws, void* stream);

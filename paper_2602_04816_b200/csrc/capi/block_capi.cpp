@@ -118,7 +118,9 @@ struct Failure {
 };
 
 void chk_gemm(const HlmGemmDesc& g, cudaStream_t s, const char* what) {
+  const int tk = hlm_capi::ktimer_begin(s);
   const int rc = hlm_gemm_launch(&g, s);
+  hlm_capi::ktimer_end(tk, s, HLM_KTIMER_GEMM, 2.0 * g.M * g.N * (double)g.K * (g.G > 0 ? g.G : 1));
   if (rc) throw Failure{std::string("gemm ") + what + " failed (code " + std::to_string(rc) + ")", HLM_ERR_CUDA};
 }
 void chk(int rc, const char* what) {
@@ -150,6 +152,13 @@ int guarded(F&& fn) {
 void attention_fwd(const HlmBlockDims& d, const uint16_t* q, const uint16_t* k, const uint16_t* v, uint16_t* o,
                    float* lse, i64 ld, cudaStream_t s) {
   const int hd = static_cast<int>(d.hidden / d.n_heads);
+  // causal attention flops: 2 * B * S^2 * h forward
+  const double fl = 2.0 * d.batch * (double)d.seq * d.seq * d.hidden;
+  const int tk = hlm_capi::ktimer_begin(s);
+  struct End {
+    int tk; cudaStream_t s; double fl;
+    ~End() { hlm_capi::ktimer_end(tk, s, HLM_KTIMER_ATTN_FWD, fl); }
+  } end{tk, s, fl};
   if (!(d.flags & HLM_BLOCK_GENERIC_ATTENTION) && hlm_flash_supported(hd, static_cast<int>(d.seq))) {
     chk(hlm_flash_fwd(q, k, v, o, lse, (int)d.batch, (int)d.seq, (int)d.n_heads, hd, (int)ld, s), "flash fwd");
   } else {
@@ -162,6 +171,13 @@ void attention_bwd(const HlmBlockDims& d, const uint16_t* q, const uint16_t* k, 
                    const uint16_t* o, const uint16_t* d_o, const float* lse, float* dsum, uint16_t* dq,
                    uint16_t* dk, uint16_t* dv, i64 ld, cudaStream_t s) {
   const int hd = static_cast<int>(d.hidden / d.n_heads);
+  // backward = 2.5 x forward flops (dV, dP, dQ, dK: 4 + 1 recomputed S per tile pair, causal)
+  const double fl = 2.5 * 2.0 * d.batch * (double)d.seq * d.seq * d.hidden;
+  const int tk = hlm_capi::ktimer_begin(s);
+  struct End {
+    int tk; cudaStream_t s; double fl;
+    ~End() { hlm_capi::ktimer_end(tk, s, HLM_KTIMER_ATTN_BWD, fl); }
+  } end{tk, s, fl};
   if (!(d.flags & HLM_BLOCK_GENERIC_ATTENTION) && hlm_flash_supported(hd, static_cast<int>(d.seq))) {
     chk(hlm_flash_bwd(q, k, v, o, d_o, lse, dsum, dq, dk, dv, (int)d.batch, (int)d.seq, (int)d.n_heads, hd,
                       (int)ld, s),
