@@ -10,9 +10,14 @@
 //           operand, P from shared memory); S_{j+1} is issued before PV_j so the
 //           tensor core overlaps the softmax of tile j
 //   warp 2  TMEM allocator (512 columns: S0 S1 O0 O1)
-//   warps 4-7 softmax: thread = query row; two TMEM passes over S (row max,
-//           then exp2 + row sum + bf16 P written to swizzled smem), then the
-//           online rescale O_acc = alpha * O_acc + O_j in registers.
+//   warps 4-11 softmax, 384 threads in all: warp w owns TMEM lanes 32*(w%4)..
+//           (thread = query row) and column half (w-4)/4 of S and O (64 keys /
+//           64 head dims). Per tile: ONE TMEM load of its 64 S columns (kept in
+//           registers), the row max exchanged with the partner warp of the other
+//           half through smem, exp2 + row sum + bf16 P written to its swizzled
+//           smem atom, then the online rescale O_acc = alpha * O_acc + O_j of its
+//           64 O columns in registers (one TMEM load). Two warps per scheduler and
+//           one exposed TMEM latency per pass instead of four.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -30,7 +35,8 @@ namespace {
 constexpr int TQ = 128, TK = 128, HD = 128;
 constexpr int TILE_BYTES = TQ * HD * 2;            // 32 KiB
 constexpr int ATOM_BYTES = 128 * 64 * 2;           // 16 KiB: 128 rows x 64 cols
-constexpr int SMEM_BYTES = TILE_BYTES * 7 + 1024 + 256;   // Q, K0 V0 K1 V1, P0 P1
+constexpr int FWD_THREADS = 384;
+constexpr int SMEM_BYTES = TILE_BYTES * 7 + 1024 + 128 + 1024;   // Q, K0 V0 K1 V1, P0 P1, barriers, row exchange
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct Bars {
@@ -46,6 +52,13 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// the two softmax warps sharing TMEM lanes 32q..32q+31 (named barrier 1 + q, 64 threads)
+__device__ __forceinline__ void pair_sync(int q) { asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory"); }
 
 // K-major SW128 descriptor for K step kk (16 elements) of a 128 x 128 tile stored as two atoms.
 __device__ __forceinline__ uint64_t kmajor_desc(uint32_t base, int kk) {
@@ -56,7 +69,7 @@ __device__ __forceinline__ uint64_t mnmajor_desc(uint32_t base, int kk) {
   return make_sw128_desc(base + kk * 2048, ATOM_BYTES, 1024);
 }
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(FWD_THREADS, 1)
     flash_fwd_tc(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                  const __grid_constant__ CUtensorMap map_v, __nv_bfloat16* __restrict__ o, float* __restrict__ lse,
                  int S, int H, int ld, float scale_log2) {
@@ -67,6 +80,7 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* sV[2] = {smem + 2 * TILE_BYTES, smem + 4 * TILE_BYTES};
   uint8_t* sP[2] = {smem + 5 * TILE_BYTES, smem + 6 * TILE_BYTES};
   Bars* bars = reinterpret_cast<Bars*>(smem + 7 * TILE_BYTES);
+  float* xch = reinterpret_cast<float*>(smem + 7 * TILE_BYTES + 128);   // [2 halves][128 rows]
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int qt = (int)(gridDim.x - 1 - blockIdx.x);   // long (late) query tiles first
@@ -84,10 +98,10 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&bars->kv_full[i], 1);
       mbar_init(&bars->kv_empty[i], 1);
       mbar_init(&bars->s_full[i], 1);
-      mbar_init(&bars->s_free[i], 4);
+      mbar_init(&bars->s_free[i], 8);
       mbar_init(&bars->o_full[i], 1);
-      mbar_init(&bars->o_free[i], 4);
-      mbar_init(&bars->p_full[i], 4);
+      mbar_init(&bars->o_free[i], 8);
+      mbar_init(&bars->p_full[i], 8);
     }
     fence_barrier_init();
   }
@@ -151,26 +165,29 @@ __global__ void __launch_bounds__(256, 1)
       __syncwarp();
     }
   } else if (warp >= 4) {
-    const int ew = warp - 4;
-    const int r = ew * 32 + lane;                 // query row within the tile
+    const int half = (warp - 4) >> 2;             // S / O columns [64*half, 64*half + 64)
+    const int quarter = warp & 3;                 // TMEM lanes 32*quarter .. +31
+    const int r = quarter * 32 + lane;            // query row within the tile
     const int qpos = qt * TQ + r;
-    const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
-    float oacc[HD];
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const int cb = half * 64;
+    float oacc[64];
 #pragma unroll
-    for (int i = 0; i < HD; ++i) oacc[i] = 0.f;
+    for (int i = 0; i < 64; ++i) oacc[i] = 0.f;
     float m = -INFINITY, l = 0.f, alpha_prev = 1.f;
-    // O_acc <- alpha * O_acc + O_j (TMEM O[jj % 2]), then release that O buffer
+    // O_acc <- alpha * O_acc + O_j (this half's 64 columns of TMEM O[jj % 2]), then release it
     auto fold = [&](int jj, float alpha) {
       const int so = jj & 1;
       mbar_wait(&bars->o_full[so], (jj >> 1) & 1);
       tc_fence_after();
+      uint32_t v0[32], v1[32];
+      tmem_ld_32x32(tmem + 256 + so * 128 + cb + lane_off, v0);
+      tmem_ld_32x32(tmem + 256 + so * 128 + cb + 32 + lane_off, v1);
+      tmem_ld_wait();
 #pragma unroll
-      for (int c = 0; c < HD / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32(tmem + 256 + so * 128 + c * 32 + lane_off, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 32; ++e) oacc[c * 32 + e] = oacc[c * 32 + e] * alpha + __uint_as_float(v[e]);
+      for (int e = 0; e < 32; ++e) {
+        oacc[e] = oacc[e] * alpha + __uint_as_float(v0[e]);
+        oacc[32 + e] = oacc[32 + e] * alpha + __uint_as_float(v1[e]);
       }
       tc_fence_before();
       __syncwarp();
@@ -181,48 +198,46 @@ __global__ void __launch_bounds__(256, 1)
       const bool diag = j == qt;
       mbar_wait(&bars->s_full[st], (j >> 1) & 1);
       tc_fence_after();
-      // pass 1: row max
-      float mx = m;
-#pragma unroll 1
-      for (int c = 0; c < TK / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32(tmem + st * 128 + c * 32 + lane_off, v);
-        tmem_ld_wait();
+      uint32_t s0[32], s1[32];
+      tmem_ld_32x32(tmem + st * 128 + cb + lane_off, s0);
+      tmem_ld_32x32(tmem + st * 128 + cb + 32 + lane_off, s1);
+      tmem_ld_wait();
+      float sv[64];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const float sv = __uint_as_float(v[e]) * scale_log2;
-          if (!diag || c * 32 + e <= r) mx = fmaxf(mx, sv);
-        }
+      for (int e = 0; e < 32; ++e) {
+        sv[e] = __uint_as_float(s0[e]) * scale_log2;
+        sv[32 + e] = __uint_as_float(s1[e]) * scale_log2;
       }
-      const float alpha = exp2f(m - mx);
+      if (diag) {
+#pragma unroll
+        for (int e = 0; e < 64; ++e)
+          if (cb + e > r) sv[e] = -INFINITY;
+      }
+      float mx = m;
+#pragma unroll
+      for (int e = 0; e < 64; ++e) mx = fmaxf(mx, sv[e]);
+      // row max across the two column halves
+      xch[half * 128 + r] = mx;
+      pair_sync(quarter);
+      mx = fmaxf(xch[r], xch[128 + r]);
+      pair_sync(quarter);                         // both read before the next tile's write
+      const float alpha = ex2(m - mx);
       m = mx;
       // P[st] was last read by PV_{j-2}
       if (j >= 2) mbar_wait(&bars->o_full[st], ((j - 2) >> 1) & 1);
-      uint8_t* prow = sP[st] + r * 128;
-      // pass 2: p = exp2(s - m), row sum, bf16 P into the swizzled K-major tile
+      uint8_t* prow = sP[st] + half * ATOM_BYTES + r * 128;   // keys 64*half.. = swizzle atom `half`
       float rs = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < TK / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32(tmem + st * 128 + c * 32 + lane_off, v);
-        tmem_ld_wait();
-        uint32_t pk[16];
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          float p0 = exp2f(__uint_as_float(v[e]) * scale_log2 - m);
-          float p1 = exp2f(__uint_as_float(v[e + 1]) * scale_log2 - m);
-          if (diag && c * 32 + e > r) p0 = 0.f;
-          if (diag && c * 32 + e + 1 > r) p1 = 0.f;
+      for (int cc = 0; cc < 8; ++cc) {               // 16-byte chunk = 8 keys
+        uint32_t pk[4];
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) {
+          const float p0 = ex2(sv[cc * 8 + e] - m);
+          const float p1 = ex2(sv[cc * 8 + e + 1] - m);
           rs += p0 + p1;
           pk[e / 2] = pack_bf16x2(p0, p1);
         }
-        const int atom = c >> 1;   // keys c*32 .. c*32+31: atom (c/2), 16-byte chunks (c%2)*4 .. +3
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const int chunk = (c & 1) * 4 + q4;
-          uint4 val = make_uint4(pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
-          *reinterpret_cast<uint4*>(prow + atom * ATOM_BYTES + ((chunk ^ (r & 7)) << 4)) = val;
-        }
+        *reinterpret_cast<uint4*>(prow + ((cc ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
       }
       l = l * alpha + rs;
       tc_fence_before();
@@ -237,17 +252,20 @@ __global__ void __launch_bounds__(256, 1)
       alpha_prev = alpha;
     }
     fold(n_tiles - 1, alpha_prev);
-    const float il = 1.f / l;
-    __nv_bfloat16* orow = o + (long long)(row0 + qpos) * ld + col0;
+    xch[half * 128 + r] = l;
+    pair_sync(quarter);
+    const float lt = xch[r] + xch[128 + r];
+    const float il = 1.f / lt;
+    __nv_bfloat16* orow = o + (long long)(row0 + qpos) * ld + col0 + cb;
 #pragma unroll
-    for (int c = 0; c < HD / 8; ++c) {
+    for (int c = 0; c < 8; ++c) {
       uint4 val = make_uint4(pack_bf16x2(oacc[8 * c] * il, oacc[8 * c + 1] * il),
                              pack_bf16x2(oacc[8 * c + 2] * il, oacc[8 * c + 3] * il),
                              pack_bf16x2(oacc[8 * c + 4] * il, oacc[8 * c + 5] * il),
                              pack_bf16x2(oacc[8 * c + 6] * il, oacc[8 * c + 7] * il));
       reinterpret_cast<uint4*>(orow)[c] = val;
     }
-    lse[(long long)bh * S + qpos] = (m + log2f(l)) / kLog2e;
+    if (half == 0) lse[(long long)bh * S + qpos] = (m + log2f(lt)) / kLog2e;
   }
   tc_fence_before();
   __syncthreads();
@@ -269,9 +287,10 @@ __device__ __forceinline__ void store_row_kmajor(uint8_t* tile, int r, int c, co
   }
 }
 
-__device__ __forceinline__ void store_acc_row(__nv_bfloat16* dst, uint32_t taddr, float scale) {
+// 64 accumulator columns (one half) of a row: TMEM -> scaled bf16 in global memory
+__device__ __forceinline__ void store_acc_half(__nv_bfloat16* dst, uint32_t taddr, float scale) {
 #pragma unroll 1
-  for (int c = 0; c < HD / 32; ++c) {
+  for (int c = 0; c < 2; ++c) {
     uint32_t v[32];
     tmem_ld_32x32(taddr + c * 32, v);
     tmem_ld_wait();
@@ -294,7 +313,7 @@ struct BwdKVBars {
 };
 constexpr int BWD_KV_SMEM = TILE_BYTES * 6 + 1024 + 1024 + 256;
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(FWD_THREADS, 1)
     flash_bwd_dkv_tc(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                      const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do,
                      const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dk,
@@ -320,7 +339,7 @@ __global__ void __launch_bounds__(256, 1)
     mbar_init(&bars->qd_full, 1);
     mbar_init(&bars->qd_empty, 1);
     mbar_init(&bars->s_full, 1);
-    mbar_init(&bars->p_full, 4);
+    mbar_init(&bars->p_full, 8);
     mbar_init(&bars->acc_full, 1);
     fence_barrier_init();
   }
@@ -386,22 +405,28 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) umma_commit(&bars->acc_full);
     __syncwarp();
   } else if (warp >= 4) {
-    const int ew = warp - 4, r = ew * 32 + lane;   // key row within the tile
+    // warp w: key rows 32*(w%4).. (its TMEM lanes), query columns [64*half, +64)
+    const int half = (warp - 4) >> 2, quarter = warp & 3;
+    const int r = quarter * 32 + lane;             // key row within the tile
     const int key = kt * TK + r;
-    const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
+    const int tid = (warp - 4) * 32 + lane;        // 0..255
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float* L = lse + (long long)bh * S;
     const float* Dr = dsum + (long long)bh * S;
     for (int i = kt; i < nq; ++i) {
       const int it = i - kt;
       // lse (log2 units) and D of this query tile; the previous tile's readers are done
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      sL[r] = L[i * TQ + r] * kLog2e;
-      sD[r] = Dr[i * TQ + r];
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (tid < 128)
+        sL[tid] = L[i * TQ + tid] * kLog2e;
+      else
+        sD[tid - 128] = Dr[i * TQ + tid - 128];
+      asm volatile("bar.sync 1, 256;" ::: "memory");
       mbar_wait(&bars->s_full, it & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < TQ / 32; ++c) {
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int c = half * 2 + h2;               // 32-column chunk of the 128 query columns
         uint32_t sv[32], dpv[32];
         tmem_ld_32x32(tmem + c * 32 + lane_off, sv);
         tmem_ld_32x32(tmem + 128 + c * 32 + lane_off, dpv);
@@ -413,7 +438,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             const int qc = c * 32 + e + u, qpos = i * TQ + qc;
-            float pv = exp2f(__uint_as_float(sv[e + u]) * scale_log2 - sL[qc]);
+            float pv = ex2(__uint_as_float(sv[e + u]) * scale_log2 - sL[qc]);
             if (key > qpos) pv = 0.f;
             p[u] = pv;
             ds[u] = pv * (__uint_as_float(dpv[e + u]) - sD[qc]);
@@ -431,8 +456,8 @@ __global__ void __launch_bounds__(256, 1)
     }
     mbar_wait(&bars->acc_full, 0);
     tc_fence_after();
-    store_acc_row(dv + (long long)(row0 + key) * ld + col0, tmem + 256 + lane_off, 1.0f);
-    store_acc_row(dk + (long long)(row0 + key) * ld + col0, tmem + 384 + lane_off, scale);
+    store_acc_half(dv + (long long)(row0 + key) * ld + col0 + half * 64, tmem + 256 + half * 64 + lane_off, 1.0f);
+    store_acc_half(dk + (long long)(row0 + key) * ld + col0 + half * 64, tmem + 384 + half * 64 + lane_off, scale);
   }
   tc_fence_before();
   __syncthreads();
@@ -447,7 +472,7 @@ struct BwdQBars {
 };
 constexpr int BWD_Q_SMEM = TILE_BYTES * 7 + 1024 + 256;
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(FWD_THREADS, 1)
     flash_bwd_dq_tc(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                     const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do,
                     const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dq,
@@ -475,7 +500,7 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&bars->kv_empty[i], 1);
     }
     mbar_init(&bars->s_full, 1);
-    mbar_init(&bars->ds_full, 4);
+    mbar_init(&bars->ds_full, 8);
     mbar_init(&bars->acc_full, 1);
     fence_barrier_init();
   }
@@ -538,9 +563,11 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) umma_commit(&bars->acc_full);
     __syncwarp();
   } else if (warp >= 4) {
-    const int ew = warp - 4, r = ew * 32 + lane;   // query row within the tile
+    // warp w: query rows 32*(w%4).. (its TMEM lanes), key columns [64*half, +64)
+    const int half = (warp - 4) >> 2, quarter = warp & 3;
+    const int r = quarter * 32 + lane;             // query row within the tile
     const int qpos = qt * TQ + r;
-    const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float l2 = lse[(long long)bh * S + qpos] * kLog2e;
     const float D = dsum[(long long)bh * S + qpos];
     for (int j = 0; j < n_tiles; ++j) {
@@ -548,7 +575,8 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(&bars->s_full, j & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < TK / 32; ++c) {
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int c = half * 2 + h2;
         uint32_t sv[32], dpv[32];
         tmem_ld_32x32(tmem + c * 32 + lane_off, sv);
         tmem_ld_32x32(tmem + 128 + c * 32 + lane_off, dpv);
@@ -559,7 +587,7 @@ __global__ void __launch_bounds__(256, 1)
           float ds[2];
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
-            float pv = exp2f(__uint_as_float(sv[e + u]) * scale_log2 - l2);
+            float pv = ex2(__uint_as_float(sv[e + u]) * scale_log2 - l2);
             if (diag && c * 32 + e + u > r) pv = 0.f;
             ds[u] = pv * (__uint_as_float(dpv[e + u]) - D);
           }
@@ -574,7 +602,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     mbar_wait(&bars->acc_full, 0);
     tc_fence_after();
-    store_acc_row(dq + (long long)(row0 + qpos) * ld + col0, tmem + 256 + lane_off, scale);
+    store_acc_half(dq + (long long)(row0 + qpos) * ld + col0 + half * 64, tmem + 256 + half * 64 + lane_off, scale);
   }
   tc_fence_before();
   __syncthreads();
@@ -621,7 +649,7 @@ int hlm_flash_fwd_tc(const void* q, const void* k, const void* v, void* o, float
     attr = true;
   }
   dim3 grid(S / TQ, B * H);
-  flash_fwd_tc<<<grid, 256, SMEM_BYTES, s>>>(mq, mk, mv, (__nv_bfloat16*)o, lse, S, H, ld,
+  flash_fwd_tc<<<grid, FWD_THREADS, SMEM_BYTES, s>>>(mq, mk, mv, (__nv_bfloat16*)o, lse, S, H, ld,
                                              (1.0f / sqrtf((float)HD)) * kLog2e);
   hlm_count_launches(1);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
@@ -643,9 +671,9 @@ int hlm_flash_bwd_tc(const void* q, const void* k, const void* v, const void* d_
   }
   const float scale = 1.0f / sqrtf((float)HD);
   dim3 grid(S / TQ, B * H);
-  flash_bwd_dkv_tc<<<grid, 256, BWD_KV_SMEM, s>>>(mq, mk, mv, mdo, lse, dsum, (__nv_bfloat16*)dk,
+  flash_bwd_dkv_tc<<<grid, FWD_THREADS, BWD_KV_SMEM, s>>>(mq, mk, mv, mdo, lse, dsum, (__nv_bfloat16*)dk,
                                                    (__nv_bfloat16*)dv, S, H, ld, scale, scale * kLog2e);
-  flash_bwd_dq_tc<<<grid, 256, BWD_Q_SMEM, s>>>(mq, mk, mv, mdo, lse, dsum, (__nv_bfloat16*)dq, S, H, ld, scale,
+  flash_bwd_dq_tc<<<grid, FWD_THREADS, BWD_Q_SMEM, s>>>(mq, mk, mv, mdo, lse, dsum, (__nv_bfloat16*)dq, S, H, ld, scale,
                                                  scale * kLog2e);
   hlm_count_launches(2);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
