@@ -36,11 +36,12 @@ constexpr int TQ = 128, TK = 128, HD = 128;
 constexpr int TILE_BYTES = TQ * HD * 2;            // 32 KiB
 constexpr int ATOM_BYTES = 128 * 64 * 2;           // 16 KiB: 128 rows x 64 cols
 constexpr int FWD_THREADS = 384;
-constexpr int SMEM_BYTES = TILE_BYTES * 7 + 1024 + 128 + 1024;   // Q, K0 V0 K1 V1, P0 P1, barriers, row exchange
+constexpr int SMEM_BYTES = TILE_BYTES * 7 + 1024 + 256 + 1024;   // Q, K0 V0 K1 V1, P0 P1, barriers, row exchange
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct Bars {
-  uint64_t q_full, kv_full[2], kv_empty[2], s_full[2], s_free[2], p_full[2], o_full[2], o_free[2];
+  uint64_t q_full, k_full[2], k_empty[2], s_full[2], s_free[2], p_full[2], o_full[2], o_free[2];
+  uint64_t v_full[2], v_empty[2];
   uint32_t tmem;
 };
 
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   uint8_t* sV[2] = {smem + 2 * TILE_BYTES, smem + 4 * TILE_BYTES};
   uint8_t* sP[2] = {smem + 5 * TILE_BYTES, smem + 6 * TILE_BYTES};
   Bars* bars = reinterpret_cast<Bars*>(smem + 7 * TILE_BYTES);
-  float* xch = reinterpret_cast<float*>(smem + 7 * TILE_BYTES + 128);   // [2 halves][128 rows]
+  float* xch = reinterpret_cast<float*>(smem + 7 * TILE_BYTES + 256);   // [2 halves][128 rows]
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int qt = (int)(gridDim.x - 1 - blockIdx.x);   // long (late) query tiles first
@@ -95,8 +96,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     tma_prefetch(&map_v);
     mbar_init(&bars->q_full, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&bars->kv_full[i], 1);
-      mbar_init(&bars->kv_empty[i], 1);
+      mbar_init(&bars->k_full[i], 1);
+      mbar_init(&bars->k_empty[i], 1);
+      mbar_init(&bars->v_full[i], 1);
+      mbar_init(&bars->v_empty[i], 1);
       mbar_init(&bars->s_full[i], 1);
       mbar_init(&bars->s_free[i], 8);
       mbar_init(&bars->o_full[i], 1);
@@ -116,15 +119,18 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       mbar_arrive_expect_tx(&bars->q_full, TILE_BYTES);
       tma_load_2d(sQ, &map_q, &bars->q_full, col0, row0 + qt * TQ);
       tma_load_2d(sQ + ATOM_BYTES, &map_q, &bars->q_full, col0 + 64, row0 + qt * TQ);
+      // K_j is released by S_j, V_j by PV_j: the next K streams in while the softmax runs
       for (int j = 0; j < n_tiles; ++j) {
         const int st = j & 1;
-        mbar_wait(&bars->kv_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&bars->kv_full[st], 2 * TILE_BYTES);
         const int r = row0 + j * TK;
-        tma_load_2d(sK[st], &map_k, &bars->kv_full[st], col0, r);
-        tma_load_2d(sK[st] + ATOM_BYTES, &map_k, &bars->kv_full[st], col0 + 64, r);
-        tma_load_2d(sV[st], &map_v, &bars->kv_full[st], col0, r);
-        tma_load_2d(sV[st] + ATOM_BYTES, &map_v, &bars->kv_full[st], col0 + 64, r);
+        mbar_wait(&bars->k_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&bars->k_full[st], TILE_BYTES);
+        tma_load_2d(sK[st], &map_k, &bars->k_full[st], col0, r);
+        tma_load_2d(sK[st] + ATOM_BYTES, &map_k, &bars->k_full[st], col0 + 64, r);
+        mbar_wait(&bars->v_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&bars->v_full[st], TILE_BYTES);
+        tma_load_2d(sV[st], &map_v, &bars->v_full[st], col0, r);
+        tma_load_2d(sV[st] + ATOM_BYTES, &map_v, &bars->v_full[st], col0 + 64, r);
       }
     }
   } else if (warp == 1) {
@@ -134,7 +140,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     mbar_wait(&bars->q_full, 0);
     auto issue_s = [&](int j) {
       const int st = j & 1;
-      mbar_wait(&bars->kv_full[st], (j >> 1) & 1);
+      mbar_wait(&bars->k_full[st], (j >> 1) & 1);
       mbar_wait(&bars->s_free[st], ((j >> 1) & 1) ^ 1);
       tc_fence_after();
       if (lane == 0) {
@@ -143,6 +149,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         for (int kk = 0; kk < HD / 16; ++kk)
           umma_bf16(tmem + st * 128, kmajor_desc(q_base, kk), kmajor_desc(k_base, kk), idesc_s, kk ? 1u : 0u);
         umma_commit(&bars->s_full[st]);
+        umma_commit(&bars->k_empty[st]);
       }
       __syncwarp();
     };
@@ -152,6 +159,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       if (j + 1 < n_tiles) issue_s(j + 1);
       mbar_wait(&bars->p_full[st], (j >> 1) & 1);
       mbar_wait(&bars->o_free[st], ((j >> 1) & 1) ^ 1);
+      mbar_wait(&bars->v_full[st], (j >> 1) & 1);
       tc_fence_after();
       if (lane == 0) {
         const uint32_t v_base = smem_u32(sV[st]);
@@ -160,7 +168,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         for (int kk = 0; kk < TK / 16; ++kk)
           umma_bf16(tmem + 256 + st * 128, kmajor_desc(p_base, kk), mnmajor_desc(v_base, kk), idesc_o, kk ? 1u : 0u);
         umma_commit(&bars->o_full[st]);
-        umma_commit(&bars->kv_empty[st]);
+        umma_commit(&bars->v_empty[st]);
       }
       __syncwarp();
     }
@@ -307,11 +315,13 @@ __device__ __forceinline__ void store_acc_half(__nv_bfloat16* dst, uint32_t tadd
 // dK, dV for one 128-key tile: loop over query tiles i >= kt.
 //   TMEM: S^T [0,128) dP^T [128,256) dV [256,384) dK [384,512)
 //   smem: K, V (fixed), Q_i, dO_i, P^T, dS^T (bf16, K-major), lse2/D of tile i
+//   Q is double-buffered (released by the dK MMA), dO single (released by the dV
+//   MMA, issued first): the next Q / dO stream in under this tile's MMAs.
 struct BwdKVBars {
-  uint64_t kv_full, qd_full, qd_empty, s_full, p_full, acc_full;
+  uint64_t kv_full, q_full[2], q_empty[2], do_full, do_empty, s_full, p_full, acc_full;
   uint32_t tmem;
 };
-constexpr int BWD_KV_SMEM = TILE_BYTES * 6 + 1024 + 1024 + 256;
+constexpr int BWD_KV_SMEM = TILE_BYTES * 7 + 1024 + 1024 + 256;
 
 __global__ void __launch_bounds__(FWD_THREADS, 1)
     flash_bwd_dkv_tc(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
@@ -320,11 +330,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
                      __nv_bfloat16* __restrict__ dv, int S, int H, int ld, float scale, float scale_log2) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t *sK = smem, *sV = smem + TILE_BYTES, *sQ = smem + 2 * TILE_BYTES, *sdO = smem + 3 * TILE_BYTES,
-          *sPT = smem + 4 * TILE_BYTES, *sdST = smem + 5 * TILE_BYTES;
-  float* sL = reinterpret_cast<float*>(smem + 6 * TILE_BYTES);
+  uint8_t *sK = smem, *sV = smem + TILE_BYTES, *sdO = smem + 3 * TILE_BYTES, *sPT = smem + 4 * TILE_BYTES,
+          *sdST = smem + 5 * TILE_BYTES;
+  uint8_t* sQ[2] = {smem + 2 * TILE_BYTES, smem + 6 * TILE_BYTES};
+  float* sL = reinterpret_cast<float*>(smem + 7 * TILE_BYTES);
   float* sD = sL + 128;
-  BwdKVBars* bars = reinterpret_cast<BwdKVBars*>(smem + 6 * TILE_BYTES + 1024);
+  BwdKVBars* bars = reinterpret_cast<BwdKVBars*>(smem + 7 * TILE_BYTES + 1024);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int kt = (int)blockIdx.x;        // key tile (early tiles have the longest loops: launched first)
   const int nq = S / TQ;
@@ -336,8 +347,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     tma_prefetch(&map_v);
     tma_prefetch(&map_do);
     mbar_init(&bars->kv_full, 1);
-    mbar_init(&bars->qd_full, 1);
-    mbar_init(&bars->qd_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars->q_full[i], 1);
+      mbar_init(&bars->q_empty[i], 1);
+    }
+    mbar_init(&bars->do_full, 1);
+    mbar_init(&bars->do_empty, 1);
     mbar_init(&bars->s_full, 1);
     mbar_init(&bars->p_full, 8);
     mbar_init(&bars->acc_full, 1);
@@ -358,29 +373,39 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       tma_load_2d(sV + ATOM_BYTES, &map_v, &bars->kv_full, col0 + 64, row0 + kt * TK);
       for (int i = kt; i < nq; ++i) {
         const int it = i - kt;
-        mbar_wait(&bars->qd_empty, (it & 1) ^ 1);
-        mbar_arrive_expect_tx(&bars->qd_full, 2 * TILE_BYTES);
+        const int qs = it & 1;
         const int r = row0 + i * TQ;
-        tma_load_2d(sQ, &map_q, &bars->qd_full, col0, r);
-        tma_load_2d(sQ + ATOM_BYTES, &map_q, &bars->qd_full, col0 + 64, r);
-        tma_load_2d(sdO, &map_do, &bars->qd_full, col0, r);
-        tma_load_2d(sdO + ATOM_BYTES, &map_do, &bars->qd_full, col0 + 64, r);
+        mbar_wait(&bars->q_empty[qs], ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&bars->q_full[qs], TILE_BYTES);
+        tma_load_2d(sQ[qs], &map_q, &bars->q_full[qs], col0, r);
+        tma_load_2d(sQ[qs] + ATOM_BYTES, &map_q, &bars->q_full[qs], col0 + 64, r);
+        mbar_wait(&bars->do_empty, (it & 1) ^ 1);
+        mbar_arrive_expect_tx(&bars->do_full, TILE_BYTES);
+        tma_load_2d(sdO, &map_do, &bars->do_full, col0, r);
+        tma_load_2d(sdO + ATOM_BYTES, &map_do, &bars->do_full, col0 + 64, r);
       }
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc_kk = make_idesc_bf16(128, 128, false, false);   // A K-major, B K-major
     constexpr uint32_t idesc_kmn = make_idesc_bf16(128, 128, false, true);   // A K-major, B MN-major
-    const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV), q_base = smem_u32(sQ), do_base = smem_u32(sdO),
+    const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV), do_base = smem_u32(sdO),
                    pt_base = smem_u32(sPT), dst_base = smem_u32(sdST);
     mbar_wait(&bars->kv_full, 0);
     for (int i = kt; i < nq; ++i) {
       const int it = i - kt;
-      mbar_wait(&bars->qd_full, it & 1);
+      const int qs = it & 1;
+      const uint32_t q_base = smem_u32(sQ[qs]);
+      mbar_wait(&bars->q_full[qs], (it >> 1) & 1);
       tc_fence_after();
       if (lane == 0) {
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk)
           umma_bf16(tmem, kmajor_desc(k_base, kk), kmajor_desc(q_base, kk), idesc_kk, kk ? 1u : 0u);
+      }
+      __syncwarp();
+      mbar_wait(&bars->do_full, it & 1);
+      tc_fence_after();
+      if (lane == 0) {
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk)
           umma_bf16(tmem + 128, kmajor_desc(v_base, kk), kmajor_desc(do_base, kk), idesc_kk, kk ? 1u : 0u);
@@ -394,11 +419,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         for (int kk = 0; kk < TQ / 16; ++kk)
           umma_bf16(tmem + 256, kmajor_desc(pt_base, kk), mnmajor_desc(do_base, kk), idesc_kmn,
                     (it > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&bars->do_empty);
 #pragma unroll
         for (int kk = 0; kk < TQ / 16; ++kk)
           umma_bf16(tmem + 384, kmajor_desc(dst_base, kk), mnmajor_desc(q_base, kk), idesc_kmn,
                     (it > 0 || kk > 0) ? 1u : 0u);
-        umma_commit(&bars->qd_empty);
+        umma_commit(&bars->q_empty[qs]);
       }
       __syncwarp();
     }
