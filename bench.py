@@ -402,6 +402,11 @@ def run_ours(args, m, name):
                           "def": "(30 B/param host Adam + 4 B/param gradient DMA + weight DMA bytes)"
                                  " / (4/3 x measured 16-thread STREAM triad = raw DRAM bandwidth)"},
         "stream": {"h2d_gbs": h2d_gbs, "d2h_gbs": d2h_gbs, "overlap": overlap,
+                   "h2d_overlap": rep["h2d_overlap"], "h2d_exposed_s": rep["h2d_exposed_ms"] / 1e3,
+                   "compute_idle_s": rep["compute_idle_ms"] / 1e3,
+                   "overlap_def": "overlap: share of H2D + D2H busy time with the compute stream busy; "
+                                  "h2d_overlap: 1 - (compute idle while a weight transfer it waits on "
+                                  "is in flight) / H2D busy time",
                    "gpu_span_s": gpu_span_s, "compute_busy_s": rep["compute_busy_ms"] / 1e3,
                    "host_adam_s": adam_s,
                    "h2d_bytes_measured": int(h2d_step), "trace_violations": len(violations)},

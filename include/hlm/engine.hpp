@@ -74,6 +74,8 @@ struct EngineOptions {
     // in pieces of head_piece_vocab vocab rows (0 = auto, ~kPieceElems elements per
     // piece when the head spans two or more; -1 = off). Eager untied single-GPU only.
     i64 head_piece_vocab = 0;
+    // Elements per D2H / optimizer / forward-H2D piece (0 = 64 Mi = 256 MB of fp32).
+    i64 piece_elems = 0;
     bool resident_embed = false;
 };
 
@@ -131,7 +133,7 @@ private:
         i64 t = 0;      // Adam step index of the gradient (bias correction)
         i64 count = 0;  // fp32 elements copied into the slab (the tile, or this rank's shard)
         i64 pieces = 1; // D2H pieces, each with its own event (the optimizer starts on piece 0)
-        i64 piece = kPieceElems;   // elements per piece
+        i64 piece = 0;  // elements per piece
     };
     struct HostOpRecord {   // host-side Accum / OptStep, appended to the trace in finish_step
         i64 slab, layer, grad_op, step;   // step: the gradient's step (an earlier one for a tail tile)
@@ -178,6 +180,7 @@ private:
     // finiteness flag and one per piece, so the host Adam starts on the first piece
     // instead of waiting for the whole tile (the head gradient is 2.2 GB at C2).
     static constexpr i64 kPieceElems = i64(64) << 20;
+    i64 piece_elems_ = kPieceElems;     // EngineOptions::piece_elems (tests use small pieces)
     i64 max_pieces_ = 1;
     std::vector<void*> ev_slab_flag_;    // per slab
     std::vector<void*> ev_piece_;        // per slab x max_pieces_
@@ -191,6 +194,10 @@ private:
     int head_buf_ = -1;
     i64 head_wop_ = -1;
     i64 tail_key(i64 layer) const;      // forward-need order of a tile (optimizer priority)
+    // Per physical tile: leading elements whose running Adam update is done (mu_).
+    // A forward H2D into a cache slot copies piece by piece behind the optimizer.
+    std::vector<i64> progress_;
+    bool wait_elems_current(i64 tile_id, i64 end);   // false: whole tile current
     // vocab-chunked head: vocab rows per piece (0 = off), certificate word, per-piece
     // compute events, full-scan fallback flag per slab (device + pinned mirror)
     i64 head_vc_ = 0;

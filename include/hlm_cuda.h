@@ -252,6 +252,8 @@ typedef struct HlmEngineOptions {
    * piece's D2H and host Adam start while the next piece is computed):
    * 0 = auto (~64 Mi elements per piece when the head spans two or more), -1 = off */
   int64_t head_piece_vocab;
+  /* elements per gradient D2H / host Adam / forward weight H2D piece (0 = 64 Mi) */
+  int64_t piece_elems;
 } HlmEngineOptions;
 
 typedef struct HlmStepResult {

@@ -111,6 +111,7 @@ hlm::EngineOptions to_opts(const HlmEngineOptions* o) {
         e.resident_embed = o->resident_embed != 0;
         e.resident_blocks = o->resident_blocks;
         e.head_piece_vocab = o->head_piece_vocab;
+        e.piece_elems = o->piece_elems;
     }
     return e;
 }

@@ -82,11 +82,13 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
         ck(cudaEventRecord(E(ev_gradbuf_free_[i]), S(compute_)), "record");
     }
     for (i64 i = 0; i < pool_->size(); ++i) ev_slab_done_.push_back(new_event(false));
-    max_pieces_ = std::max<i64>(1, (pool_->slab_capacity() / 4 + kPieceElems - 1) / kPieceElems);
+    if (opts_.piece_elems > 0) piece_elems_ = opts_.piece_elems;
+    max_pieces_ = std::max<i64>(1, (pool_->slab_capacity() / 4 + piece_elems_ - 1) / piece_elems_);
     // vocab-chunked head (single GPU, untied): pieces of head_vc_ vocab rows
     if (!opts_.comm_grad && !m.tie_embeddings && opts_.head_piece_vocab >= 0) {
         i64 vc = opts_.head_piece_vocab;
-        if (vc == 0 && m.embed_params() >= 2 * kPieceElems) vc = std::max<i64>(128, kPieceElems / m.hidden / 128 * 128);
+        if (vc == 0 && m.embed_params() >= 2 * piece_elems_)
+            vc = std::max<i64>(128, piece_elems_ / m.hidden / 128 * 128);
         if (vc > 0) vc = std::min<i64>(vc, hlm_cuda_head_chunk_vocab(m.rows(), m.vocab));
         if (vc > 0 && vc < m.vocab) head_vc_ = vc;
     }
@@ -140,6 +142,7 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
     }
     for (i64 p = 0; p < store_.physical_tiles(); ++p)
         target_version_.push_back(store_.physical(p).min_version());
+    progress_.assign(static_cast<size_t>(store_.physical_tiles()), 0);
     // HBM-resident optimizer tiles
     resident_of_.assign(static_cast<size_t>(m.tile_count()), -1);
     const bool resident_ok = opts_.eager_optim && !opts_.skip_optimizer && opts_.world == 1 && !opts_.comm_grad &&
@@ -305,9 +308,57 @@ void Engine::wait_tile_current(i64 tile_id) {
     rethrow_worker_error();
 }
 
+// Wait until elements [0, end) of the tile hold the update the next H2D needs;
+// returns false when the whole tile is current (the rest need not be waited for).
+bool Engine::wait_elems_current(i64 tile_id, i64 end) {
+    const i64 p = store_.physical_index(tile_id);
+    const LayerTile& tile = store_.physical(p);
+    bool whole = false;
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] {
+        whole = tile.min_version() >= target_version_[static_cast<size_t>(p)];
+        return whole || progress_[static_cast<size_t>(p)] >= end || worker_error_ != nullptr;
+    });
+    lk.unlock();
+    rethrow_worker_error();
+    return !whole;
+}
+
 int Engine::stream_tile(i64 tile_id, i64* op_id, bool forward_pass) {
     const i64 slot = cache_slot_of_[static_cast<size_t>(tile_id)];
-    if (!(slot >= 0 && cache_xfer_op_[static_cast<size_t>(slot)] >= 0)) wait_tile_current(tile_id);
+    // forward into a cache slot, single GPU: copy piece by piece behind the optimizer
+    const bool piecewise = slot >= 0 && forward_pass && cache_xfer_op_[static_cast<size_t>(slot)] < 0 &&
+                           opts_.overlap_optimizer_tail && opts_.world == 1 && !opts_.comm_weights;
+    if (!piecewise && !(slot >= 0 && cache_xfer_op_[static_cast<size_t>(slot)] >= 0)) wait_tile_current(tile_id);
+    if (piecewise) {
+        const LayerTile& tile = store_.tile(tile_id);
+        const i64 n = tile.n_params();
+        arena_.claim_cache_slot(slot);
+        uint16_t* dst = static_cast<uint16_t*>(arena_.cache_slot(slot));
+        bool waiting = true;
+        i64 id = -1;
+        for (i64 off = 0; off < n; off += piece_elems_) {
+            const i64 len = std::min(piece_elems_, n - off);
+            if (waiting) waiting = wait_elems_current(tile_id, off + len);
+            StreamOp op;
+            op.stream = StreamId::H2D;
+            op.kind = OpKind::WeightXfer;
+            op.layer = tile_id;
+            op.buf = 2 + slot;
+            op.bytes = 2 * len;
+            op.pinned = store_.shadow_pinned();
+            id = op_begin(std::move(op), h2d_);
+            ck(cudaMemcpyAsync(dst + off, tile.shadow() + off, static_cast<size_t>(len) * 2, cudaMemcpyHostToDevice,
+                               S(h2d_)),
+               "H2D weight piece");
+            arena_.add_h2d(2 * len);
+            op_end(id, h2d_);
+        }
+        ck(cudaEventRecord(E(ev_cache_ready_[static_cast<size_t>(slot)]), S(h2d_)), "record cache ready");
+        cache_xfer_op_[static_cast<size_t>(slot)] = id;
+        *op_id = id;
+        return 2 + static_cast<int>(slot);
+    }
     if (slot >= 0) {
         if (cache_xfer_op_[static_cast<size_t>(slot)] >= 0) {   // resident since this step's forward
             *op_id = cache_xfer_op_[static_cast<size_t>(slot)];
@@ -428,9 +479,9 @@ void Engine::evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op) {
     ck_hlm(hlm_cuda_nonfinite(src, cnt, nf_dev_ + slab, d2h_), "nonfinite scan");
     ck(cudaMemcpyAsync(nf_host_ + slab, nf_dev_ + slab, 8, cudaMemcpyDeviceToHost, S(d2h_)), "D2H nf flag");
     ck(cudaEventRecord(E(ev_slab_flag_[static_cast<size_t>(slab)]), S(d2h_)), "record slab flag");
-    const i64 pieces = (cnt + kPieceElems - 1) / kPieceElems;
+    const i64 pieces = (cnt + piece_elems_ - 1) / piece_elems_;
     for (i64 k = 0; k < pieces; ++k) {
-        const i64 off = k * kPieceElems, len = std::min(kPieceElems, cnt - off);
+        const i64 off = k * piece_elems_, len = std::min(piece_elems_, cnt - off);
         ck(cudaMemcpyAsync(pool_->data(slab) + off, src + off, static_cast<size_t>(len) * 4, cudaMemcpyDeviceToHost,
                            S(d2h_)),
            "D2H grads");
@@ -441,7 +492,7 @@ void Engine::evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op) {
     ck(cudaEventRecord(E(ev_gradbuf_free_[gbuf]), S(d2h_)), "record grad buf free");
     {
         std::lock_guard<std::mutex> lk(mu_);
-        pending_.push_back({slab, tile_id, id, step_index_, step_t_, cnt, pieces});
+        pending_.push_back({slab, tile_id, id, step_index_, step_t_, cnt, pieces, piece_elems_});
     }
     cv_.notify_all();
 }
@@ -481,12 +532,23 @@ void Engine::consume(const Pending& p) {
         rec.opt = true;
         rec.topt0 = rec.t1;
         const float* g = pool_->data(p.slab);
+        const size_t pi = static_cast<size_t>(phys);
         for (i64 k = 0; k < p.pieces; ++k) {
             const i64 off = k * p.piece, len = std::min(p.piece, p.count - off);
             ck(cudaEventSynchronize(E(ev_piece_[static_cast<size_t>(p.slab * max_pieces_ + k)])), "piece sync");
             adam_step_range(tile, g + off, base + off, len, hyper_, p.t, /*prechecked=*/true);
+            if (opts_.world == 1) {   // a forward H2D may copy this piece now
+                std::lock_guard<std::mutex> lk(mu_);
+                progress_[pi] = off + len;
+            }
+            if (opts_.world == 1) cv_.notify_all();
         }
-        tile.bump_version(opts_.rank);
+        {   // the version now covers the whole tile; progress counts the next update
+            std::lock_guard<std::mutex> lk(mu_);
+            tile.bump_version(opts_.rank);
+            progress_[pi] = 0;
+        }
+        cv_.notify_all();
         rec.topt1 = now_us();
     };
     if (opts_.comm_grad) {   // this rank's shard [begin, begin + cnt)

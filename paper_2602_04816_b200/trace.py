@@ -161,4 +161,36 @@ def overlap_report(ops):
         rep[f"{st}_hidden_ms"] = sum(covered(o["t_start_us"], o["t_end_us"]) for o in xs) / 1e3
     total = rep["h2d_busy_ms"] + rep["d2h_busy_ms"]
     rep["overlap"] = (rep["h2d_hidden_ms"] + rep["d2h_hidden_ms"]) / total if total > 0 else None
+    rep.update(exposed_weights(ops))
     return rep
+
+
+def exposed_weights(ops):
+    """Where the compute stream idles, and why: for every idle gap before a
+    compute op, the part during which a weight transfer that op depends on was
+    in flight is EXPOSED TRANSFER; the rest of the gap is waiting for the
+    transfer to be issued at all (the host optimizer had not finished that tile)
+    or for other work. h2d_overlap = 1 - exposed / H2D busy time: the per-layer
+    compute/transfer overlap of the north-star target, separated from host-paced
+    idling."""
+    by_id = {o["id"]: o for o in ops}
+    comp = sorted((o for o in ops if o["stream"] == "compute" and o["t_end_us"] > o["t_start_us"] >= 0),
+                  key=lambda o: o["t_start_us"])
+    prev, idle, exposed = None, 0.0, 0.0
+    for c in comp:
+        if prev is not None and c["t_start_us"] > prev:
+            g0, g1 = prev, c["t_start_us"]
+            idle += g1 - g0
+            spans = []
+            for d in c["deps"]:
+                x = by_id.get(d)
+                if x and x["stream"] == "h2d" and x["t_end_us"] > x["t_start_us"] >= 0:
+                    lo, hi = max(g0, x["t_start_us"]), min(g1, x["t_end_us"])
+                    if hi > lo:
+                        spans.append((lo, hi))
+            exposed += sum(e - s for s, e in _union(spans))
+        prev = c["t_end_us"] if prev is None else max(prev, c["t_end_us"])
+    busy = sum(o["t_end_us"] - o["t_start_us"] for o in ops
+               if o["stream"] == "h2d" and o["t_end_us"] > o["t_start_us"] >= 0)
+    return {"compute_idle_ms": idle / 1e3, "h2d_exposed_ms": exposed / 1e3,
+            "h2d_overlap": 1.0 - exposed / busy if busy > 0 else None}

@@ -321,3 +321,31 @@ def test_hbm_resident_optimizer_tiles_are_bitwise_neutral(res):
     streamed = 2 * (c.vocab * c.hidden * (0 if res.get("resident_embed") else 1) +
                     c.vocab * c.hidden + 2 * (c.layers - res.get("resident_blocks", 0)) * c.block_params())
     assert l1[-1].h2d_bytes == streamed
+
+
+@pytest.mark.parametrize("pieces", [dict(piece_elems=1000), dict(piece_elems=4096, head_piece_vocab=8)])
+def test_piecewise_transfers_are_bitwise_neutral(pieces):
+    """Gradients landing in pieces with the host Adam piece by piece, and the
+    forward H2D of cached blocks copied piece by piece behind the optimizer:
+    the same losses and store, bit for bit, as whole-tile transfers."""
+    from paper_2602_04816_b200.trace import validate_trace
+    c = E.ModelConfig(6, 32, 64, 40, 16, 2, k_ckpt=1, n_heads=2, rope_theta=1e4)
+    toks = [E.make_copy_task_batch(c, 6, skip=i) for i in range(4)]
+    blk = (2 * c.block_params() + 255) // 256 * 256
+    hp = E.HyperParams(lr=2e-3)
+    res = []
+    for kw in (dict(head_piece_vocab=-1), pieces):
+        s = E.Store(c, 12)
+        e = E.Engine(s, E.Arena(c, weight_cache_bytes=c.layers * blk), hp,
+                     E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=c.layers + 4,
+                                     overlap_optimizer_tail=True, tail_blocks=c.layers, **kw))
+        losses = [e.train_step(t).loss for t in toks]
+        assert validate_trace(e.last_trace(), c.layers) == []
+        e.sync()
+        res.append((losses, s))
+    if "head_piece_vocab" in pieces:     # vocab-chunked head: d_x summed in another order
+        assert res[0][0][0] == res[1][0][0]
+        assert np.allclose(res[0][0], res[1][0], rtol=1e-4)
+    else:
+        assert res[0][0] == res[1][0]
+        assert res[0][1].bitwise_equal(res[1][1])
