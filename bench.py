@@ -280,10 +280,10 @@ def run_ours(args, m, name):
     clk = clocks.stop()
     lib.hlm_ktimer_enable(0)
     kt = {}
-    for kind, name in ((0, "gemm"), (1, "attn_fwd"), (2, "attn_bwd")):
+    for kind, kname in ((0, "gemm"), (1, "attn_fwd"), (2, "attn_bwd")):
         ms_k, fl_k, n_k = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
         lib.hlm_ktimer_collect(kind, ctypes.byref(ms_k), ctypes.byref(fl_k), ctypes.byref(n_k))
-        kt[name] = {"ms": ms_k.value, "flops": fl_k.value, "launches": n_k.value,
+        kt[kname] = {"ms": ms_k.value, "flops": fl_k.value, "launches": n_k.value,
                     "tflops": fl_k.value / (ms_k.value / 1e3) / 1e12 if ms_k.value > 0 else None}
     lib.hlm_ktimer_reset()
     dev_s = lib.hlm_timer_elapsed_ms(0, 1) / 1e3
@@ -444,12 +444,19 @@ def main():
     ap.add_argument("--force-dp", action="store_true",
                     help="use the data-parallel code path (NCCL, shared store) even at world 1")
     ap.add_argument("--dump-trace", default="", help="write the last warm-up step's measured trace (JSONL)")
+    ap.add_argument("--layers", type=int, default=0,
+                    help="partial depth of the config's full-width decoder (C3-C5 do not fit a 196 GB "
+                         "host at full depth); the workload name says so")
     args = ap.parse_args()
     m = dict(CONFIGS[args.config])
+    name = NAMES[args.config]
+    if args.layers > 0 and args.layers != m["layers"]:
+        name = f"{name}-first{args.layers}of{m['layers']}layers"
+        m["layers"] = args.layers
     if args.impl == "reference":
-        run_reference(args, m, NAMES[args.config])
+        run_reference(args, m, name)
     else:
-        run_ours(args, m, NAMES[args.config])
+        run_ours(args, m, name)
 
 
 if __name__ == "__main__":
