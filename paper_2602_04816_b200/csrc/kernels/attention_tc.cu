@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "attention.h"
 #include "block_ops.h"
@@ -280,6 +281,261 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+
+// ------------------------------------------------------------------ forward, ping-pong
+// Two 128-query tiles per CTA (A = 2p, B = 2p + 1) share every K / V tile, and the
+// softmax of one tile runs while the tensor core works on the other.
+//   TMEM: S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512).
+//   P (bf16) overwrites the first 64 columns of its S region (tcgen05.st) and the PV
+//   MMA reads it straight from TMEM (A operand in TMEM); O accumulates in TMEM.
+//   The running row max is raised only when a tile's max exceeds it by more than
+//   2^8 (then the owning warp rescales its O rows and l in place); otherwise P <= 256,
+//   exact in the fp32 accumulators. No O traffic through registers per tile.
+//   warp 0 TMA producer (Q_A, Q_B once; K / V 2-slot rings released separately),
+//   warp 1 MMA issuer + TMEM allocator, warps 2-9 softmax: tile (w-2)/4, TMEM lane
+//   quarter w%4, thread = query row, all 128 key columns in registers. (A 16-warp
+//   variant with 64 columns per thread and a smem row-max exchange measured slower:
+//   0.49 vs 0.38 ms at C2 — spills at 96 registers and the extra barriers.)
+struct PPBars {
+  uint64_t q_full, k_full[2], k_empty[2], v_full[2], v_empty[2];
+  uint64_t s_full[2], p_full[2], o_final[2];
+  uint32_t tmem;
+};
+constexpr int PP_THREADS = 320;
+constexpr int PP_SMEM = TILE_BYTES * 6 + 1024 + 256;
+constexpr float kRescaleLog2 = 8.0f;
+
+__device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tmem_st_32x32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]) : "memory");
+}
+__device__ __forceinline__ void tmem_st_32x16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]) : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__global__ void __launch_bounds__(PP_THREADS, 1)
+    flash_fwd_pp(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                 const __grid_constant__ CUtensorMap map_v, __nv_bfloat16* __restrict__ o, float* __restrict__ lse,
+                 int S, int H, int ld, float scale_log2) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ[2] = {smem, smem + TILE_BYTES};
+  uint8_t* sK[2] = {smem + 2 * TILE_BYTES, smem + 3 * TILE_BYTES};
+  uint8_t* sV[2] = {smem + 4 * TILE_BYTES, smem + 5 * TILE_BYTES};
+  PPBars* bars = reinterpret_cast<PPBars*>(smem + 6 * TILE_BYTES);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int pair = (int)(gridDim.x - 1 - blockIdx.x);   // long (late) query tiles first
+  const int qtile[2] = {2 * pair, 2 * pair + 1};
+  const int ntile[2] = {2 * pair + 1, 2 * pair + 2};
+  const int bh = blockIdx.y, b = bh / H, hh = bh % H;
+  const int row0 = b * S;
+  const int col0 = hh * HD;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&map_q);
+    tma_prefetch(&map_k);
+    tma_prefetch(&map_v);
+    mbar_init(&bars->q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars->k_full[i], 1);
+      mbar_init(&bars->k_empty[i], 1);
+      mbar_init(&bars->v_full[i], 1);
+      mbar_init(&bars->v_empty[i], 1);
+      mbar_init(&bars->s_full[i], 1);
+      mbar_init(&bars->p_full[i], 4);
+      mbar_init(&bars->o_final[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&bars->tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&bars->q_full, 2 * TILE_BYTES);
+      for (int t = 0; t < 2; ++t) {
+        tma_load_2d(sQ[t], &map_q, &bars->q_full, col0, row0 + qtile[t] * TQ);
+        tma_load_2d(sQ[t] + ATOM_BYTES, &map_q, &bars->q_full, col0 + 64, row0 + qtile[t] * TQ);
+      }
+      for (int j = 0; j < ntile[1]; ++j) {
+        const int st = j & 1;
+        const int r = row0 + j * TK;
+        mbar_wait(&bars->k_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&bars->k_full[st], TILE_BYTES);
+        tma_load_2d(sK[st], &map_k, &bars->k_full[st], col0, r);
+        tma_load_2d(sK[st] + ATOM_BYTES, &map_k, &bars->k_full[st], col0 + 64, r);
+        mbar_wait(&bars->v_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&bars->v_full[st], TILE_BYTES);
+        tma_load_2d(sV[st], &map_v, &bars->v_full[st], col0, r);
+        tma_load_2d(sV[st] + ATOM_BYTES, &map_v, &bars->v_full[st], col0 + 64, r);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false, false);
+    constexpr uint32_t idesc_o = make_idesc_bf16(128, 128, false, true);
+    mbar_wait(&bars->q_full, 0);
+    // S_t = Q_t K_j^T; K_j is released by tile B's S (B uses every K tile, after A)
+    auto issue_s = [&](int t, int j) {
+      const int st = j & 1;
+      mbar_wait(&bars->k_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t q_base = smem_u32(sQ[t]), k_base = smem_u32(sK[st]);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          umma_bf16(tmem + t * 128, kmajor_desc(q_base, kk), kmajor_desc(k_base, kk), idesc_s, kk ? 1u : 0u);
+        umma_commit(&bars->s_full[t]);
+        if (t == 1) umma_commit(&bars->k_empty[st]);
+      }
+      __syncwarp();
+    };
+    // O_t += P_t V_j with P_t in TMEM (the first 64 columns of S_t); V_j released by tile B's PV
+    auto issue_pv = [&](int t, int j) {
+      const int st = j & 1;
+      mbar_wait(&bars->p_full[t], j & 1);
+      mbar_wait(&bars->v_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t v_base = smem_u32(sV[st]);
+#pragma unroll
+        for (int kk = 0; kk < TK / 16; ++kk)
+          umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, mnmajor_desc(v_base, kk), idesc_o,
+                       (j > 0 || kk > 0) ? 1u : 0u);
+        if (t == 1) umma_commit(&bars->v_empty[st]);
+      }
+      __syncwarp();
+    };
+    issue_s(0, 0);
+    issue_s(1, 0);
+    for (int j = 0; j < ntile[1]; ++j) {
+      if (j < ntile[0]) {
+        issue_pv(0, j);
+        if (j + 1 < ntile[0]) {
+          issue_s(0, j + 1);
+        } else {
+          if (lane == 0) umma_commit(&bars->o_final[0]);
+          __syncwarp();
+        }
+      }
+      issue_pv(1, j);
+      if (j + 1 < ntile[1]) {
+        issue_s(1, j + 1);
+      } else {
+        if (lane == 0) umma_commit(&bars->o_final[1]);
+        __syncwarp();
+      }
+    }
+  } else {
+    const int t = (warp - 2) >> 2;                 // query tile A (0) or B (1)
+    const int quarter = warp & 3;                  // TMEM lanes 32*quarter ..
+    const int r = quarter * 32 + lane;             // query row within the tile
+    const int qt = qtile[t], n = ntile[t];
+    const int qpos = qt * TQ + r;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const uint32_t s_addr = tmem + t * 128 + lane_off, o_addr = tmem + 256 + t * 128 + lane_off;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < n; ++j) {
+      mbar_wait(&bars->s_full[t], j & 1);
+      tc_fence_after();
+      uint32_t sv[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld_32x32(s_addr + c * 32, sv[c]);
+      tmem_ld_wait();
+      if (j == qt) {   // diagonal tile (warp-uniform): mask keys above the row
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (c * 32 + e > r) sv[c][e] = __float_as_uint(-INFINITY);
+      }
+      // max of the raw scores (scale_log2 > 0 commutes with max); 8 independent chains
+      float mx8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) mx8[u] = fmaxf(__uint_as_float(sv[0][u]), __uint_as_float(sv[0][u + 8]));
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int e = (c == 0 ? 16 : 0); e < 32; e += 2)
+          mx8[e & 7] = fmaxf(mx8[e & 7], fmaxf(__uint_as_float(sv[c][e]), __uint_as_float(sv[c][e + 1])));
+      const float mx = scale_log2 * fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                          fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+      if (j == 0) {
+        m = mx;
+      } else if (__any_sync(0xffffffffu, mx > m + kRescaleLog2)) {
+        // O_t holds P V of tiles < j: S_t(j) was issued after PV_t(j-1), so its
+        // completion implies theirs. Rescale this warp's 32 rows in TMEM.
+        const float mn = fmaxf(m, mx);
+        const float alpha = ex2(m - mn);
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t ov[32];
+          tmem_ld_32x32(o_addr + c * 32, ov);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+          tmem_st_32x32(o_addr + c * 32, ov);
+        }
+        l *= alpha;
+        m = mn;
+      }
+      // P = 2^(s * scale_log2 - m) <= 2^8 as bf16 pairs into S_t columns [0, 64)
+      const float negm = -m;
+      float l8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float p0 = ex2(fmaf(__uint_as_float(sv[c][2 * e]), scale_log2, negm));
+          const float p1 = ex2(fmaf(__uint_as_float(sv[c][2 * e + 1]), scale_log2, negm));
+          l8[e & 7] += p0 + p1;
+          pk[e] = pack_bf16x2(p0, p1);
+        }
+        tmem_st_32x16(s_addr + c * 16, pk);
+      }
+      l += ((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7]));
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->p_full[t]);
+    }
+    mbar_wait(&bars->o_final[t], 0);
+    tc_fence_after();
+    const float il = 1.f / l;
+    __nv_bfloat16* orow = o + (long long)(row0 + qpos) * ld + col0;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t ov[32];
+      tmem_ld_32x32(o_addr + c * 32, ov);
+      tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        reinterpret_cast<uint4*>(orow + c * 32)[q] =
+            make_uint4(pack_bf16x2(__uint_as_float(ov[8 * q]) * il, __uint_as_float(ov[8 * q + 1]) * il),
+                       pack_bf16x2(__uint_as_float(ov[8 * q + 2]) * il, __uint_as_float(ov[8 * q + 3]) * il),
+                       pack_bf16x2(__uint_as_float(ov[8 * q + 4]) * il, __uint_as_float(ov[8 * q + 5]) * il),
+                       pack_bf16x2(__uint_as_float(ov[8 * q + 6]) * il, __uint_as_float(ov[8 * q + 7]) * il));
+    }
+    lse[(long long)bh * S + qpos] = (m + log2f(l)) / kLog2e;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
 
 // ------------------------------------------------------------------ backward
 // Shared pieces: a 128-row bf16 tile written by 128 threads (thread = row) into
@@ -673,6 +929,19 @@ int hlm_flash_fwd_tc(const void* q, const void* k, const void* v, void* o, float
   if (!attr) {
     cudaFuncSetAttribute(flash_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     attr = true;
+  }
+  static const bool pp = std::getenv("HLM_ATTN_FWD_V1") == nullptr;
+  if (pp && S % (2 * TQ) == 0) {   // two query tiles per CTA
+    static bool attr_pp = false;
+    if (!attr_pp) {
+      cudaFuncSetAttribute(flash_fwd_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, PP_SMEM);
+      attr_pp = true;
+    }
+    dim3 grid(S / (2 * TQ), B * H);
+    flash_fwd_pp<<<grid, PP_THREADS, PP_SMEM, s>>>(mq, mk, mv, (__nv_bfloat16*)o, lse, S, H, ld,
+                                                   (1.0f / sqrtf((float)HD)) * kLog2e);
+    hlm_count_launches(1);
+    return cudaGetLastError() == cudaSuccess ? 0 : 1;
   }
   dim3 grid(S / TQ, B * H);
   flash_fwd_tc<<<grid, FWD_THREADS, SMEM_BYTES, s>>>(mq, mk, mv, (__nv_bfloat16*)o, lse, S, H, ld,
