@@ -24,6 +24,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "attention.h"
 #include "block_ops.h"
@@ -700,7 +701,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
       // lse (log2 units) and D of this query tile; the previous tile's readers are done
       asm volatile("bar.sync 1, 256;" ::: "memory");
       if (tid < 128)
-        sL[tid] = L[i * TQ + tid] * kLog2e;
+        sL[tid] = -L[i * TQ + tid] * kLog2e;   // negated: exp argument is one FFMA
       else
         sD[tid - 128] = Dr[i * TQ + tid - 128];
       asm volatile("bar.sync 1, 256;" ::: "memory");
@@ -714,20 +715,34 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         tmem_ld_32x32(tmem + 128 + c * 32 + lane_off, dpv);
         tmem_ld_wait();
         uint32_t pk[16], dk16[16];
+        const float4* L4 = reinterpret_cast<const float4*>(sL + c * 32);
+        const float4* D4 = reinterpret_cast<const float4*>(sD + c * 32);
+        // only the diagonal tile (i == kt, warp-uniform) has keys above its queries
+        auto body = [&](auto diag_tag) {
+          constexpr bool kDiag = decltype(diag_tag)::value;
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          float p[2], ds[2];
+          for (int e4 = 0; e4 < 8; ++e4) {
+            const float4 lv = L4[e4], dv4 = D4[e4];
+            const float ln[4] = {lv.x, lv.y, lv.z, lv.w}, dn[4] = {dv4.x, dv4.y, dv4.z, dv4.w};
+            float p[4], ds[4];
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int qc = c * 32 + e + u, qpos = i * TQ + qc;
-            float pv = ex2(__uint_as_float(sv[e + u]) * scale_log2 - sL[qc]);
-            if (key > qpos) pv = 0.f;
-            p[u] = pv;
-            ds[u] = pv * (__uint_as_float(dpv[e + u]) - sD[qc]);
+            for (int u = 0; u < 4; ++u) {
+              const int e = e4 * 4 + u;
+              float pv = ex2(fmaf(__uint_as_float(sv[e]), scale_log2, ln[u]));
+              if (kDiag && r > c * 32 + e) pv = 0.f;
+              p[u] = pv;
+              ds[u] = pv * (__uint_as_float(dpv[e]) - dn[u]);
+            }
+            pk[e4 * 2] = pack_bf16x2(p[0], p[1]);
+            pk[e4 * 2 + 1] = pack_bf16x2(p[2], p[3]);
+            dk16[e4 * 2] = pack_bf16x2(ds[0], ds[1]);
+            dk16[e4 * 2 + 1] = pack_bf16x2(ds[2], ds[3]);
           }
-          pk[e / 2] = pack_bf16x2(p[0], p[1]);
-          dk16[e / 2] = pack_bf16x2(ds[0], ds[1]);
-        }
+        };
+        if (i == kt)
+          body(std::true_type{});
+        else
+          body(std::false_type{});
         store_row_kmajor(sPT, r, c, pk);
         store_row_kmajor(sdST, r, c, dk16);
       }
@@ -850,7 +865,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     const int r = quarter * 32 + lane;             // query row within the tile
     const int qpos = qt * TQ + r;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    const float l2 = lse[(long long)bh * S + qpos] * kLog2e;
+    const float neg_l2 = -lse[(long long)bh * S + qpos] * kLog2e;
     const float D = dsum[(long long)bh * S + qpos];
     for (int j = 0; j < n_tiles; ++j) {
       const bool diag = j == qt;
@@ -864,17 +879,24 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         tmem_ld_32x32(tmem + 128 + c * 32 + lane_off, dpv);
         tmem_ld_wait();
         uint32_t pk[16];
+        auto body = [&](auto diag_tag) {
+          constexpr bool kDiag = decltype(diag_tag)::value;
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          float ds[2];
+          for (int e = 0; e < 32; e += 2) {
+            float ds[2];
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            float pv = ex2(__uint_as_float(sv[e + u]) * scale_log2 - l2);
-            if (diag && c * 32 + e + u > r) pv = 0.f;
-            ds[u] = pv * (__uint_as_float(dpv[e + u]) - D);
+            for (int u = 0; u < 2; ++u) {
+              float pv = ex2(fmaf(__uint_as_float(sv[e + u]), scale_log2, neg_l2));
+              if (kDiag && c * 32 + e + u > r) pv = 0.f;
+              ds[u] = pv * (__uint_as_float(dpv[e + u]) - D);
+            }
+            pk[e / 2] = pack_bf16x2(ds[0], ds[1]);
           }
-          pk[e / 2] = pack_bf16x2(ds[0], ds[1]);
-        }
+        };
+        if (diag)   // warp-uniform: only the diagonal tile masks
+          body(std::true_type{});
+        else
+          body(std::false_type{});
         store_row_kmajor(sdS, r, c, pk);
       }
       tc_fence_before();
