@@ -147,9 +147,12 @@ size_t hlm_cuda_head_ws_bytes(int64_t rows, int64_t hidden, int64_t vocab);
  * bench's roofline.achieved): when enabled, every GEMM / attention launch is
  * bracketed by an event pair on its own stream and its algorithmic flops kept.
  * collect() sums one kind (synchronises on its events); reset() recycles them. */
-enum { HLM_KTIMER_GEMM = 0, HLM_KTIMER_ATTN_FWD = 1, HLM_KTIMER_ATTN_BWD = 2 };
+enum { HLM_KTIMER_GEMM = 0, HLM_KTIMER_ATTN_FWD = 1, HLM_KTIMER_ATTN_BWD = 2,
+       /* HBM-bound kernels: work = algorithmic bytes (each tensor read / written once) */
+       HLM_KTIMER_RMSNORM_FWD = 3, HLM_KTIMER_RMSNORM_BWD = 4, HLM_KTIMER_SWIGLU_FWD = 5,
+       HLM_KTIMER_SWIGLU_BWD = 6, HLM_KTIMER_ROPE = 7, HLM_KTIMER_CAST = 8 };
 int hlm_ktimer_enable(int on);
-int hlm_ktimer_collect(int kind, double* ms, double* flops, int64_t* launches);
+int hlm_ktimer_collect(int kind, double* ms, double* work, int64_t* launches);
 int hlm_ktimer_reset(void);
 int hlm_cuda_head_stats(int64_t rows, int64_t hidden, int64_t vocab, const void* head, const float* x,
                         const int32_t* targets, float inv_rows, float* loss_rows, unsigned long long* cert,

@@ -129,6 +129,13 @@ void chk(int rc, const char* what) {
     throw Failure{std::string(what) + " launch failed: " + cudaGetErrorString(e), HLM_ERR_CUDA};
   }
 }
+// An HBM-bound launch timed by the kernel timer (work = algorithmic bytes).
+template <typename F>
+void timed(int kind, double bytes, cudaStream_t s, F&& launch) {
+  const int tk = hlm_capi::ktimer_begin(s);
+  launch();
+  hlm_capi::ktimer_end(tk, s, kind, bytes);
+}
 
 void validate(const HlmBlockDims* d) {
   if (!d || d->batch <= 0 || d->seq <= 0 || d->hidden <= 0 || d->ffn <= 0 || d->n_heads <= 0)
@@ -222,7 +229,7 @@ int hlm_cuda_block_fwd(const HlmBlockDims* d, const void* w_tile, const float* h
     const uint16_t* W = static_cast<const uint16_t*>(w_tile);
     BlockActs a = carve_acts(*d, acts, nullptr);
 
-    chk(hlm_ops_rmsnorm_fwd(h_in, W + off.norm1, a.n1, T, hi, s), "rmsnorm1");
+    timed(HLM_KTIMER_RMSNORM_FWD, 6.0 * T * h, s, [&] { chk(hlm_ops_rmsnorm_fwd(h_in, W + off.norm1, a.n1, T, hi, s), "rmsnorm1"); });
     HlmGemmDesc g = gdesc(Ti, hi, hi, a.n1, h, 0, W + off.q, h, 1, a.qkv, h, HLM_EPI_BF16);
     g.G = 3;
     g.b_grouped = 1;
@@ -230,20 +237,22 @@ int hlm_cuda_block_fwd(const HlmBlockDims* d, const void* w_tile, const float* h
     g.c_gstride = T * h;
     chk_gemm(g, s, "qkv");
     if (rope_cos)
-      chk(hlm_ops_rope(a.qkv, rope_cos, rope_sin, T, hi, hi / d->n_heads, (int)d->seq, 0, 2, T * h, s), "rope");
+      timed(HLM_KTIMER_ROPE, 8.0 * T * h, s, [&] {
+        chk(hlm_ops_rope(a.qkv, rope_cos, rope_sin, T, hi, hi / d->n_heads, (int)d->seq, 0, 2, T * h, s), "rope");
+      });
     attention_fwd(*d, a.qkv, a.qkv + T * h, a.qkv + 2 * T * h, a.o, a.lse, h, s);
     g = gdesc(Ti, hi, hi, a.o, h, 0, W + off.o, h, 1, a.y, h, HLM_EPI_F32_ADD);
     g.R = h_in;
     g.ldr = h;
     chk_gemm(g, s, "o-proj");
-    chk(hlm_ops_rmsnorm_fwd(a.y, W + off.norm2, a.n2, T, hi, s), "rmsnorm2");
+    timed(HLM_KTIMER_RMSNORM_FWD, 6.0 * T * h, s, [&] { chk(hlm_ops_rmsnorm_fwd(a.y, W + off.norm2, a.n2, T, hi, s), "rmsnorm2"); });
     g = gdesc(Ti, fi, hi, a.n2, h, 0, W + off.up, f, 1, a.ug, f, HLM_EPI_BF16);
     g.G = 2;
     g.b_grouped = 1;
     g.b_gstride = h * f;
     g.c_gstride = T * f;
     chk_gemm(g, s, "up|gate");
-    chk(hlm_ops_swiglu_fwd(a.ug, a.act, T * f, s), "swiglu");
+    timed(HLM_KTIMER_SWIGLU_FWD, 6.0 * T * f, s, [&] { chk(hlm_ops_swiglu_fwd(a.ug, a.act, T * f, s), "swiglu"); });
     g = gdesc(Ti, hi, fi, a.act, f, 0, W + off.down, h, 1, h_out, h, HLM_EPI_F32_ADD);
     g.R = a.y;
     g.ldr = h;
@@ -266,10 +275,10 @@ int hlm_cuda_block_bwd(const HlmBlockDims* d, const void* w_tile, const float* h
     float* G = grad_tile;
 
     // MLP branch
-    chk(hlm_ops_cast_bf16(g_out, w.g_bf, T * h, s), "cast g_out");
+    timed(HLM_KTIMER_CAST, 6.0 * T * h, s, [&] { chk(hlm_ops_cast_bf16(g_out, w.g_bf, T * h, s), "cast g_out"); });
     chk_gemm(gdesc(fi, hi, Ti, a.act, f, 1, w.g_bf, h, 1, G + off.down, h, HLM_EPI_F32), s, "wgrad down");
     chk_gemm(gdesc(Ti, fi, hi, w.g_bf, h, 0, W + off.down, h, 0, w.d_act, f, HLM_EPI_BF16), s, "dgrad down");
-    chk(hlm_ops_swiglu_bwd(w.d_act, a.ug, w.dug, T * f, s), "swiglu bwd");
+    timed(HLM_KTIMER_SWIGLU_BWD, 10.0 * T * f, s, [&] { chk(hlm_ops_swiglu_bwd(w.d_act, a.ug, w.dug, T * f, s), "swiglu bwd"); });
     HlmGemmDesc g = gdesc(hi, fi, Ti, a.n2, h, 1, w.dug, f, 1, G + off.up, f, HLM_EPI_F32);
     g.G = 2;
     g.b_grouped = 1;
@@ -284,17 +293,21 @@ int hlm_cuda_block_bwd(const HlmBlockDims* d, const void* w_tile, const float* h
     g.b_grouped = 1;
     g.b_gstride = h * f;
     chk_gemm(g, s, "dgrad up|gate");
-    chk(hlm_ops_rmsnorm_bwd(a.y, W + off.norm2, w.d_n, g_out, w.d_y, w.d_y_bf, w.inv, w.partial, G + off.norm2,
-                            T, hi, s),
-        "rmsnorm2 bwd");
+    timed(HLM_KTIMER_RMSNORM_BWD, 18.0 * T * h, s, [&] {
+      chk(hlm_ops_rmsnorm_bwd(a.y, W + off.norm2, w.d_n, g_out, w.d_y, w.d_y_bf, w.inv, w.partial, G + off.norm2,
+                              T, hi, s),
+          "rmsnorm2 bwd");
+    });
     // attention branch
     chk_gemm(gdesc(hi, hi, Ti, a.o, h, 1, w.d_y_bf, h, 1, G + off.o, h, HLM_EPI_F32), s, "wgrad o");
     chk_gemm(gdesc(Ti, hi, hi, w.d_y_bf, h, 0, W + off.o, h, 0, w.d_o, h, HLM_EPI_BF16), s, "dgrad o");
     attention_bwd(*d, a.qkv, a.qkv + T * h, a.qkv + 2 * T * h, a.o, w.d_o, a.lse, w.dsum, w.dqkv, w.dqkv + T * h,
                   w.dqkv + 2 * T * h, h, s);
     if (rope_cos)
-      chk(hlm_ops_rope(w.dqkv, rope_cos, rope_sin, T, hi, hi / d->n_heads, (int)d->seq, 1, 2, T * h, s),
-          "rope bwd");
+      timed(HLM_KTIMER_ROPE, 8.0 * T * h, s, [&] {
+        chk(hlm_ops_rope(w.dqkv, rope_cos, rope_sin, T, hi, hi / d->n_heads, (int)d->seq, 1, 2, T * h, s),
+            "rope bwd");
+      });
     g = gdesc(hi, hi, Ti, a.n1, h, 1, w.dqkv, h, 1, G + off.q, h, HLM_EPI_F32);
     g.G = 3;
     g.b_grouped = 1;
@@ -309,9 +322,11 @@ int hlm_cuda_block_bwd(const HlmBlockDims* d, const void* w_tile, const float* h
     g.b_grouped = 1;
     g.b_gstride = h * h;
     chk_gemm(g, s, "dgrad qkv");
-    chk(hlm_ops_rmsnorm_bwd(h_in, W + off.norm1, w.d_n, w.d_y, g_in, nullptr, w.inv, w.partial, G + off.norm1, T,
-                            hi, s),
-        "rmsnorm1 bwd");
+    timed(HLM_KTIMER_RMSNORM_BWD, 16.0 * T * h, s, [&] {
+      chk(hlm_ops_rmsnorm_bwd(h_in, W + off.norm1, w.d_n, w.d_y, g_in, nullptr, w.inv, w.partial, G + off.norm1,
+                              T, hi, s),
+          "rmsnorm1 bwd");
+    });
   });
 }
 
