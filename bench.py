@@ -234,13 +234,15 @@ def run_hybrid(args, m, nums, E, lib, store, arena, holder, opts, batches, trace
     k = int(min(L, max(0, np.ceil(need / t_blk) + 1)))
     free, _ = torch.cuda.mem_get_info()
     per_blk, per_emb = 14 * nums["n"], 14 * m["vocab"] * m["hidden"]
-    k = int(max(0, min(k, (free - 4e9 - per_emb) // per_blk)))
+    extra = max(0, opts.grad_buffers - 2) * 4 * max(nums["n"], m["vocab"] * m["hidden"])
+    k = int(max(0, min(k, (free - 4e9 - per_emb - extra) // per_blk)))
     eng = holder.pop()
     eng.sync()
     del eng
     import gc
     gc.collect()
     o2 = E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=opts.n_slab, record_trace=True,
+                         grad_buffers=opts.grad_buffers,
                          overlap_optimizer_tail=True, tail_blocks=opts.tail_blocks, resident_embed=True,
                          resident_blocks=k)
     eng2 = E.Engine(store, arena, E.HyperParams(lr=1e-4), o2)
@@ -314,6 +316,7 @@ def run_ours(args, m, name):
     arena = E.Arena(cfg, device=local, weight_cache_bytes=cache)
     n_slab, tail = pick_slabs(args, m, nums, world, local_world)
     opts = E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=n_slab,
+                           grad_buffers=args.grad_buffers,
                            record_trace=True, overlap_optimizer_tail=tail >= 0,
                            tail_blocks=max(0, tail), rank=rank, world=world,
                            comm_grad=comm_g, comm_weights=comm_w, host_threads=adam_threads,
@@ -535,6 +538,9 @@ def main():
     ap.add_argument("--cache-gb", type=float, default=60.0,
                     help="HBM weight cache (block tiles resident between forward and backward)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--grad-buffers", type=int, default=8,
+                    help="device fp32 gradient buffers (2 = the arena's; more let the backward run "
+                         "ahead of a slow D2H)")
     ap.add_argument("--no-hybrid", action="store_true",
                     help="skip the measured HBM-resident-optimizer variant reported beside the headline")
     ap.add_argument("--resident-blocks", type=int, default=0,

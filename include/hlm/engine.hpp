@@ -76,6 +76,9 @@ struct EngineOptions {
     i64 head_piece_vocab = 0;
     // Elements per D2H / optimizer / forward-H2D piece (0 = 64 Mi = 256 MB of fp32).
     i64 piece_elems = 0;
+    // Outbound fp32 gradient buffers on the device (>= 2; the arena holds two, the engine
+    // allocates the rest, each the widest tile).
+    i64 grad_buffers = 2;
     bool resident_embed = false;
 };
 
@@ -173,8 +176,14 @@ private:
     void* d2h_ = nullptr;
     void* ev_w_ready_[2] = {};
     void* ev_buf_free_[2] = {};
-    void* ev_grad_ready_[2] = {};
-    void* ev_gradbuf_free_[2] = {};
+    // outbound fp32 gradient buffers: the arena's two (reference footprint) plus
+    // EngineOptions.grad_buffers - 2 engine-owned ones, so the backward runs ahead of a
+    // slow D2H instead of waiting for the buffer two layers back
+    std::vector<float*> gbuf_;
+    void* gbuf_mem_ = nullptr;
+    std::vector<void*> ev_grad_ready_;
+    std::vector<void*> ev_gradbuf_free_;
+    float* grad_buf(int i) const { return gbuf_[static_cast<size_t>(i)]; }
     std::vector<void*> ev_slab_done_;
     // Large gradients land in pieces of kPieceElems: per slab, an event after the
     // finiteness flag and one per piece, so the host Adam starts on the first piece

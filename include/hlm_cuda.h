@@ -257,6 +257,8 @@ typedef struct HlmEngineOptions {
   int64_t head_piece_vocab;
   /* elements per gradient D2H / host Adam / forward weight H2D piece (0 = 64 Mi) */
   int64_t piece_elems;
+  /* outbound fp32 gradient buffers on the device (<= 2: the arena's two) */
+  int64_t grad_buffers;
 } HlmEngineOptions;
 
 typedef struct HlmStepResult {

@@ -112,6 +112,7 @@ hlm::EngineOptions to_opts(const HlmEngineOptions* o) {
         e.resident_blocks = o->resident_blocks;
         e.head_piece_vocab = o->head_piece_vocab;
         e.piece_elems = o->piece_elems;
+        e.grad_buffers = o->grad_buffers > 2 ? o->grad_buffers : 2;
     }
     return e;
 }

@@ -76,10 +76,22 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
     for (int i = 0; i < 2; ++i) {
         ev_w_ready_[i] = new_event(false);
         ev_buf_free_[i] = new_event(false);
-        ev_grad_ready_[i] = new_event(false);
-        ev_gradbuf_free_[i] = new_event(false);
         ck(cudaEventRecord(E(ev_buf_free_[i]), S(compute_)), "record");
-        ck(cudaEventRecord(E(ev_gradbuf_free_[i]), S(compute_)), "record");
+    }
+    {
+        const i64 n_gb = std::max<i64>(2, opts_.grad_buffers);
+        gbuf_ = {arena_.grad_out(0), arena_.grad_out(1)};
+        if (n_gb > 2) {
+            const size_t each = static_cast<size_t>((grad_buf_bytes(m) + 255) / 256 * 256);
+            ck(cudaMalloc(&gbuf_mem_, each * static_cast<size_t>(n_gb - 2)), "cudaMalloc gradient buffers");
+            for (i64 i = 0; i < n_gb - 2; ++i)
+                gbuf_.push_back(reinterpret_cast<float*>(static_cast<char*>(gbuf_mem_) + each * static_cast<size_t>(i)));
+        }
+        for (i64 i = 0; i < n_gb; ++i) {
+            ev_grad_ready_.push_back(new_event(false));
+            ev_gradbuf_free_.push_back(new_event(false));
+            ck(cudaEventRecord(E(ev_gradbuf_free_.back()), S(compute_)), "record");
+        }
     }
     for (i64 i = 0; i < pool_->size(); ++i) ev_slab_done_.push_back(new_event(false));
     if (opts_.piece_elems > 0) piece_elems_ = opts_.piece_elems;
@@ -218,11 +230,12 @@ Engine::~Engine() {
     for (int i = 0; i < 2; ++i) {
         cudaEventDestroy(E(ev_w_ready_[i]));
         cudaEventDestroy(E(ev_buf_free_[i]));
-        cudaEventDestroy(E(ev_grad_ready_[i]));
-        cudaEventDestroy(E(ev_gradbuf_free_[i]));
     }
     for (void* e : ev_slab_done_) cudaEventDestroy(E(e));
     for (void* e : ev_slab_flag_) cudaEventDestroy(E(e));
+    for (void* e : ev_grad_ready_) cudaEventDestroy(E(e));
+    for (void* e : ev_gradbuf_free_) cudaEventDestroy(E(e));
+    if (gbuf_mem_) cudaFree(gbuf_mem_);
     for (void* e : ev_piece_) cudaEventDestroy(E(e));
     for (void* e : ev_head_chunk_) cudaEventDestroy(E(e));
     if (ev_head_cert_) cudaEventDestroy(E(ev_head_cert_));
@@ -420,7 +433,7 @@ void Engine::compute_done_with(int buf, i64 op_id) {
 
 int Engine::next_grad_buf() {
     const int gb = next_gbuf_;
-    next_gbuf_ ^= 1;
+    next_gbuf_ = (next_gbuf_ + 1) % static_cast<int>(gbuf_.size());
     ck(cudaStreamWaitEvent(S(compute_), E(ev_gradbuf_free_[gb]), 0), "wait grad buf");
     return gb;
 }
@@ -467,10 +480,10 @@ void Engine::evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op) {
     if (last_accum_op_[static_cast<size_t>(slab)] >= 0) op.deps.push_back(last_accum_op_[static_cast<size_t>(slab)]);
     ck(cudaStreamWaitEvent(S(d2h_), E(ev_grad_ready_[gbuf]), 0), "wait grad ready");
     const i64 id = op_begin(std::move(op), d2h_);
-    float* src = arena_.grad_out(gbuf);
+    float* src = grad_buf(gbuf);
     if (opts_.comm_grad) {   // in-place reduce-scatter over NVLink, then D2H of this rank's shard
         src += opts_.rank * cnt;
-        nccl_check(nccl().ReduceScatter(arena_.grad_out(gbuf), src, static_cast<size_t>(cnt), ncclFloat32, ncclSum,
+        nccl_check(nccl().ReduceScatter(grad_buf(gbuf), src, static_cast<size_t>(cnt), ncclFloat32, ncclSum,
                                         static_cast<ncclComm_t>(opts_.comm_grad), S(d2h_)),
                    "reduce-scatter grads");
     }
@@ -613,9 +626,9 @@ void Engine::resident_update(i64 tile, int gbuf, i64 dep_op) {
     op.params = r.n;
     op.deps.push_back(dep_op);
     const i64 id = op_begin(op, compute_);
-    ck_hlm(hlm_cuda_nonfinite(arena_.grad_out(gbuf), r.n, resident_bad_ + ri, compute_), "nonfinite (resident)");
+    ck_hlm(hlm_cuda_nonfinite(grad_buf(gbuf), r.n, resident_bad_ + ri, compute_), "nonfinite (resident)");
     HlmHyper hp{hyper_.lr, hyper_.beta1, hyper_.beta2, hyper_.eps, hyper_.weight_decay};
-    ck_hlm(hlm_cuda_adam(r.state, r.state + r.n, r.state + 2 * r.n, r.w16, arena_.grad_out(gbuf), r.n,
+    ck_hlm(hlm_cuda_adam(r.state, r.state + r.n, r.state + 2 * r.n, r.w16, grad_buf(gbuf), r.n,
                          resident_bad_ + ri, &hp, step_t_, compute_),
            "device adam");
     op_end(id, compute_);
@@ -911,7 +924,7 @@ void Engine::anchor_loss_async() {
     op.deps.push_back(w_op);
     const i64 fid = op_begin(op, compute_);
     ck_hlm(hlm_cuda_head_loss(T, m.hidden, m.vocab, weights_ptr(buf), h_cur_, arena_.targets(),
-                              1.0f / static_cast<float>(T * opts_.world), arena_.g_roll(g_cur_), arena_.grad_out(gb), 0,
+                              1.0f / static_cast<float>(T * opts_.world), arena_.g_roll(g_cur_), grad_buf(gb), 0,
                               arena_.loss_rows(), arena_.head_ws(), compute_),
            "head_loss");
     op_end(fid, compute_);
@@ -973,7 +986,7 @@ void Engine::anchor_loss_pieces(int buf, i64 w_op) {
     ck(cudaEventRecord(E(ev_slab_flag_[static_cast<size_t>(slab)]), S(d2h_)), "record slab flag");
     const i64 pieces = (V + head_vc_ - 1) / head_vc_;
     i64 first_gx = -1, last_lb = -1;
-    float* g = arena_.grad_out(gb);
+    float* g = grad_buf(gb);
     for (i64 k = 0; k < pieces; ++k) {
         const i64 v0 = k * head_vc_, vc = std::min(head_vc_, V - v0);
         StreamOp lb;
@@ -1072,7 +1085,7 @@ void Engine::backward_blockwise() {
             if (w_op >= 0) bop.deps.push_back(w_op);
             const i64 lb = op_begin(bop, compute_);
             ck_hlm(hlm_cuda_block_bwd(&dims, wptr, anchor, a, arena_.g_roll(g_cur_), arena_.g_roll(g_cur_ ^ 1),
-                                      arena_.grad_out(gb), arena_.block_ws(), rc, rs, compute_),
+                                      grad_buf(gb), arena_.block_ws(), rc, rs, compute_),
                    "block_bwd");
             op_end(lb, compute_);
             if (res) {
@@ -1130,7 +1143,7 @@ void Engine::backward_blockwise() {
                 const i64 lb = op_begin(bop, compute_);
                 ck_hlm(hlm_cuda_block_bwd(&dims, weights_ptr(buf), inputs[static_cast<size_t>(i - lo)],
                                           acts[static_cast<size_t>(i - lo)], arena_.g_roll(g_cur_),
-                                          arena_.g_roll(g_cur_ ^ 1), arena_.grad_out(gb), arena_.block_ws(), rc, rs,
+                                          arena_.g_roll(g_cur_ ^ 1), grad_buf(gb), arena_.block_ws(), rc, rs,
                                           compute_),
                        "block_bwd");
                 op_end(lb, compute_);
@@ -1162,7 +1175,7 @@ void Engine::backward_blockwise() {
     eop.layer = m.embed_tile_id();
     eop.flops = bwd_flops(n_embed, T);
     const i64 lb = op_begin(eop, compute_);
-    ck_hlm(hlm_cuda_embed_bwd(arena_.csr_row_ptr(), arena_.csr_pos(), arena_.g_roll(g_cur_), arena_.grad_out(gb),
+    ck_hlm(hlm_cuda_embed_bwd(arena_.csr_row_ptr(), arena_.csr_pos(), arena_.g_roll(g_cur_), grad_buf(gb),
                               m.vocab, m.hidden, 0, compute_),
            "embed_bwd");
     op_end(lb, compute_);

@@ -323,7 +323,8 @@ def test_hbm_resident_optimizer_tiles_are_bitwise_neutral(res):
     assert l1[-1].h2d_bytes == streamed
 
 
-@pytest.mark.parametrize("pieces", [dict(piece_elems=1000), dict(piece_elems=4096, head_piece_vocab=8)])
+@pytest.mark.parametrize("pieces", [dict(piece_elems=1000), dict(piece_elems=4096, head_piece_vocab=8),
+                                    dict(piece_elems=1000, grad_buffers=5)])
 def test_piecewise_transfers_are_bitwise_neutral(pieces):
     """Gradients landing in pieces with the host Adam piece by piece, and the
     forward H2D of cached blocks copied piece by piece behind the optimizer:
