@@ -38,13 +38,14 @@ constexpr int A_STAGE = BM * BK * 2;   // 16 KiB
 constexpr int B_STAGE = BN * BK * 2;   // 32 KiB
 constexpr int ATOM = 64 * BK * 2;      // one 64-wide MN atom of a MN-major stage: 8 KiB
 constexpr int NUM_THREADS = 256;
-constexpr int GROUP_M = 16;            // raster: 16 M-tiles share each B panel in L2
+constexpr int GROUP_M = 16;            // raster: 16 M-tiles share each B panel in L2 (default)
 constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + 1024 /*align*/ + 256 /*barriers*/;
 
 struct KArgs {
   int M, N, K, G;
   int kgroup, a_grouped, b_grouped;
   int tiles_m, tiles_n, kblocks, num_tiles;
+  int group_m;   // raster group (M-tiles sharing a B panel)
   void* C;
   long long ldc, c_gstride;
   const float* R;
@@ -56,10 +57,10 @@ __device__ __forceinline__ void tile_coords(const KArgs& a, int t, int& g, int& 
   const int per_group = a.tiles_m * a.tiles_n;
   g = a.kgroup ? 0 : t / per_group;
   const int rem = t - g * per_group;
-  const int per_panel = GROUP_M * a.tiles_n;
+  const int per_panel = a.group_m * a.tiles_n;
   const int panel = rem / per_panel;
-  const int first_m = panel * GROUP_M;
-  const int gm = min(a.tiles_m - first_m, GROUP_M);
+  const int first_m = panel * a.group_m;
+  const int gm = min(a.tiles_m - first_m, a.group_m);
   const int r = rem - panel * per_panel;
   m = first_m + r % gm;
   n = r / gm;
@@ -481,13 +482,15 @@ int sm_count() {
 // HLM_GEMM_1SM=1 forces the 1-CTA kernel (A/B comparisons); otherwise the
 // 2-CTA kernel serves every non-K-grouped problem with M > 128.
 bool use_2sm(int M, int kgroup) {
-  static int force1 = -1;
+  static int force1 = -1, kgroup2 = -1;
   if (force1 < 0) {
     const char* e = std::getenv("HLM_GEMM_1SM");
     force1 = (e && *e == '1') ? 1 : 0;
+    const char* k = std::getenv("HLM_GEMM_KGROUP_2SM");
+    kgroup2 = (k && *k == '1') ? 1 : 0;
   }
   // measured (r01, C2 shapes): the K-grouped dgrads run faster on 1-CTA tiles
-  return !force1 && M > 128 && !kgroup;
+  return !force1 && M > 128 && (!kgroup || kgroup2);
 }
 
 template <bool A_MN, bool B_MN>
@@ -520,6 +523,14 @@ int launch(const HlmGemmDesc& d, cudaStream_t stream) {
   a.tiles_n = (d.N + BN - 1) / BN;
   a.kblocks = (d.K + BK - 1) / BK;
   a.num_tiles = a.tiles_m * a.tiles_n * (d.kgroup ? 1 : a.G);
+  {
+    static int gm_env = -1;
+    if (gm_env < 0) {
+      const char* e = std::getenv("HLM_GEMM_GROUP_M");
+      gm_env = e ? std::atoi(e) : 0;
+    }
+    a.group_m = gm_env > 0 ? gm_env : GROUP_M;
+  }
   a.C = d.C;
   a.ldc = d.ldc;
   a.c_gstride = d.c_gstride;
