@@ -240,6 +240,7 @@ private:
         float* data = nullptr;
         i64 capacity = 0;
         bool pinned = false;
+        bool registered = false;   // huge-page mapping pinned with cudaHostRegister
         SlabState state = SlabState::FREE;
         i64 layer_id = -1;
         i64 bytes = 0;

@@ -84,6 +84,40 @@ std::uint64_t mix64(std::uint64_t x) {   // splitmix64 finaliser
 
 void* map_huge_public(size_t bytes) { return map_huge(bytes); }
 
+namespace {
+size_t align_2m(size_t x) { return (x + (2u << 20) - 1) & ~size_t((2u << 20) - 1); }
+}  // namespace
+
+// Pinned host memory on transparent huge pages: a 2 MiB-aligned anonymous mapping,
+// touched in parallel (huge pages fault in), then page-locked with cudaHostRegister.
+// The host Adam streams gradients and shadows through these buffers; 2 MiB pages
+// keep its page walks short. Opt-in (HLM_PIN_HUGE=1): measured at C2 on the pool's box
+// it changes the step by less than the box's run-to-run noise (8.85 vs 9.0 k tok/s over
+// 2 + 2 runs) while cutting store + slab setup from ~31 s to ~12 s.
+bool pin_huge_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = std::getenv("HLM_PIN_HUGE");
+        on = (e && *e == '1') ? 1 : 0;
+    }
+    return on == 1;
+}
+void* alloc_pinned_huge(size_t bytes) {
+    const size_t b = align_2m(bytes);
+    void* p = map_huge(b);
+    parallel_zero(p, b);
+    if (cudaHostRegister(p, b, cudaHostRegisterPortable) != cudaSuccess) {
+        (void)cudaGetLastError();
+        munmap(p, b);
+        return nullptr;
+    }
+    return p;
+}
+void free_pinned_huge(void* p, size_t bytes) {
+    cudaHostUnregister(p);
+    munmap(p, align_2m(bytes));
+}
+
 // ------------------------------------------------------------------ offset tables
 std::vector<NamedRegion> block_offset_table(i64 h, i64 f) {
     std::vector<NamedRegion> t;
@@ -232,7 +266,13 @@ MasterStore::MasterStore(const ModelConfig& config, Dtype dtype, bool pin_shadow
     state_base_ = static_cast<float*>(map_huge(state_bytes_));
     parallel_zero(state_base_, state_bytes_);
     }
-    if (shm_fd_ < 0 && pin_shadow) {
+    if (shm_fd_ < 0 && pin_shadow && pin_huge_enabled()) {
+        if (void* p = alloc_pinned_huge(static_cast<size_t>(shadow_bytes_))) {
+            shadow_base_ = static_cast<std::uint16_t*>(p);
+            pinned_ = registered_ = true;
+        }
+    }
+    if (shm_fd_ < 0 && pin_shadow && !shadow_base_) {
         void* p = nullptr;
         if (cudaHostAlloc(&p, shadow_bytes_, cudaHostAllocPortable) == cudaSuccess) {
             shadow_base_ = static_cast<std::uint16_t*>(p);
@@ -272,7 +312,9 @@ MasterStore::~MasterStore() {
     }
     if (state_base_) munmap(state_base_, state_bytes_);
     if (shadow_base_) {
-        if (pinned_)
+        if (registered_)
+            free_pinned_huge(shadow_base_, static_cast<size_t>(shadow_bytes_));
+        else if (pinned_)
             cudaFreeHost(shadow_base_);
         else
             munmap(shadow_base_, shadow_bytes_);
@@ -395,7 +437,9 @@ SlabPool::SlabPool(const std::vector<i64>& capacities, bool pinned) {
         capacity_ = std::max(capacity_, s.capacity);
         pool_bytes_ += s.capacity;
         void* p = nullptr;
-        if (pinned && cudaHostAlloc(&p, static_cast<size_t>(s.capacity), cudaHostAllocPortable) == cudaSuccess) {
+        if (pinned && pin_huge_enabled() && (p = alloc_pinned_huge(static_cast<size_t>(s.capacity))) != nullptr) {
+            s.pinned = s.registered = true;
+        } else if (pinned && cudaHostAlloc(&p, static_cast<size_t>(s.capacity), cudaHostAllocPortable) == cudaSuccess) {
             s.pinned = true;
         } else {
             (void)cudaGetLastError();
@@ -408,7 +452,9 @@ SlabPool::SlabPool(const std::vector<i64>& capacities, bool pinned) {
 SlabPool::~SlabPool() {
     for (auto& s : slabs_) {
         if (!s.data) continue;
-        if (s.pinned)
+        if (s.registered)
+            free_pinned_huge(s.data, static_cast<size_t>(s.capacity));
+        else if (s.pinned)
             cudaFreeHost(s.data);
         else
             munmap(s.data, static_cast<size_t>(s.capacity));
