@@ -93,3 +93,27 @@ def test_forward_pointing_dependency_is_malformed(ops):
     m = _mut(ops, lambda m: m[tgt["id"]]["deps"].append(len(m) - 1))
     v = validate_trace(m, 28)
     assert any(x.op_id == tgt["id"] and x.rule == "malformed" for x in v)
+
+
+def test_exposed_weights_counts_only_waits_on_inflight_transfers():
+    """h2d_overlap: compute idle while a weight transfer its op depends on is in
+    flight is exposed; idle before the transfer even started (host-paced) is not."""
+    from paper_2602_04816_b200.trace import exposed_weights
+    ops = [
+        {"id": 0, "stream": "compute", "kind": "Forward", "layer": 0, "deps": [], "t_start_us": 0.0, "t_end_us": 100.0,
+         "bytes": 0},
+        # host-paced: the transfer starts 400 us after compute went idle, runs 100 us
+        {"id": 1, "stream": "h2d", "kind": "WeightXfer", "layer": 1, "deps": [], "t_start_us": 500.0,
+         "t_end_us": 600.0, "bytes": 1000},
+        {"id": 2, "stream": "compute", "kind": "Forward", "layer": 1, "deps": [1], "t_start_us": 600.0,
+         "t_end_us": 700.0, "bytes": 0},
+        # fully hidden transfer
+        {"id": 3, "stream": "h2d", "kind": "WeightXfer", "layer": 2, "deps": [], "t_start_us": 600.0,
+         "t_end_us": 650.0, "bytes": 1000},
+        {"id": 4, "stream": "compute", "kind": "Forward", "layer": 2, "deps": [3], "t_start_us": 700.0,
+         "t_end_us": 800.0, "bytes": 0},
+    ]
+    r = exposed_weights(ops)
+    assert abs(r["compute_idle_ms"] - 0.5) < 1e-9        # 100 -> 600
+    assert abs(r["h2d_exposed_ms"] - 0.1) < 1e-9         # only 500 -> 600 had the transfer in flight
+    assert abs(r["h2d_overlap"] - (1 - 100.0 / 150.0)) < 1e-9
