@@ -412,6 +412,14 @@ def run_ours(args, m, name):
 
     t_roof = max(nums["hw_flops"] / (tf_sus * 1e12), nums["h2d"] / (PCIE_ASSUMED_GBS * 1e9),
                  nums["d2h"] / (PCIE_ASSUMED_GBS * 1e9))
+    # stricter per-phase roofline: forward max(flops, weight H2D) + backward
+    # max(recompute + backward flops, gradient D2H); with the HBM weight cache the backward
+    # streams no weights
+    attn_fwd = 2.0 * m["batch"] * m["seq"] ** 2 * m["hidden"]
+    fl_fwd = m["layers"] * (2.0 * nums["n_mm"] * nums["T"] + attn_fwd) + 2.0 * nums["T"] * m["vocab"] * m["hidden"]
+    fl_bwd = nums["hw_flops"] - fl_fwd
+    t_fwd = max(fl_fwd / (tf_sus * 1e12), h2d_step / (PCIE_ASSUMED_GBS * 1e9))
+    t_bwd = max(fl_bwd / (tf_sus * 1e12), nums["d2h"] / (PCIE_ASSUMED_GBS * 1e9))
     # host DRAM roofline: every parameter moves 30 B through the host Adam (g, w, m, v in;
     # w, m, v, bf16 shadow out) + 4 B of gradient DMA written + 2 B per weight DMA pass read
     lib.hlm_host_triad_gbs.restype = ctypes.c_double
@@ -497,6 +505,10 @@ def run_ours(args, m, name):
                                         "launches at the workload shape after the steps"},
         "step_roofline": {"t_roof_s": t_roof, "t_step_s": step_s, "frac": t_roof / step_s,
                           "def": "max(HW_FLOPS/sustained bf16, H2D/55GB/s, D2H/55GB/s)"},
+        "phase_roofline": {"t_fwd_s": t_fwd, "t_bwd_s": t_bwd, "t_roof_s": t_fwd + t_bwd,
+                           "frac": (t_fwd + t_bwd) / step_s,
+                           "def": "max(fwd flops/sustained bf16, measured weight H2D bytes/55GB/s) + "
+                                  "max(recompute+bwd flops/sustained bf16, D2H bytes/55GB/s)"},
         "host_roofline": {"host_bytes_per_step": int(host_bytes), "triad_gbs": host_bw,
                           "raw_dram_gbs": raw_bw, "t_host_s": t_host,
                           "frac": (t_host / step_s) if t_host else None,
