@@ -1,0 +1,113 @@
+"""One transformer block at the C2 (Qwen2.5-7B-shaped) width — h 3584, f 18944,
+28 heads of 128, RoPE theta 1e6 — through the C ABI (hlm_cuda_block_fwd / _bwd:
+the 2-CTA and K-grouped tcgen05 GEMMs, the ping-pong flash attention, the fused
+RMSNorm / RoPE / SwiGLU kernels at production shapes), against a plain PyTorch fp32
+autograd restatement of the same block (oracle/hlm_oracle.cpp block_forward /
+block_backward semantics: pre-RMSNorm eps 1e-6, x.W with W (in, out), rotate-half
+RoPE, causal softmax(q k^T / sqrt(hd)), SwiGLU down(up * silu(gate)), residuals).
+Tolerance: BF16 GEMM operands / FP32 accumulation — relative L2 1e-2 on the output,
+5e-2 on every gradient (w_q / w_k: 1e-1, their gradients are tiny at init)."""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2602_04816_b200 import _lib as L
+
+pytestmark = pytest.mark.gpu
+
+
+def vp(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def rel(a, b):
+    a, b = a.double(), b.double()
+    return ((a - b).norm() / b.norm().clamp_min(1e-30)).item()
+
+
+def torch_block(x, W, h, f, H, S, theta, eps=1e-6):
+    hd = h // H
+    o = 0
+    def take(n, shape):
+        nonlocal o
+        t = W[o:o + n].view(*shape); o += n
+        return t
+    wq, wk, wv, wo = (take(h * h, (h, h)) for _ in range(4))
+    wup, wgate = take(h * f, (h, f)), take(h * f, (h, f))
+    wdown = take(f * h, (f, h))
+    n1w, n2w = take(h, (h,)), take(h, (h,))
+    T = x.shape[0]
+    B = T // S
+
+    def rms(v, s):
+        return v * torch.rsqrt((v * v).mean(-1, keepdim=True) + eps) * s
+
+    half = hd // 2
+    i = torch.arange(half, device=x.device, dtype=torch.float64)
+    pos = torch.arange(S, device=x.device, dtype=torch.float64)
+    ang = pos[:, None] * theta ** (-2.0 * i / hd)
+    cos, sin = ang.cos().float(), ang.sin().float()
+
+    def rope(v):
+        v = v.view(B, S, H, hd)
+        a, b = v[..., :half], v[..., half:]
+        c, s_ = cos[None, :, None, :], sin[None, :, None, :]
+        return torch.cat([a * c - b * s_, b * c + a * s_], -1).view(T, h)
+
+    n1 = rms(x, n1w)
+    q, k, v = rope(n1 @ wq), rope(n1 @ wk), n1 @ wv
+    qh, kh, vh = (t.view(B, S, H, hd).permute(0, 2, 1, 3) for t in (q, k, v))
+    sc = qh @ kh.transpose(-1, -2) / hd ** 0.5
+    sc = sc.masked_fill(torch.triu(torch.ones(S, S, dtype=torch.bool, device=x.device), 1), float("-inf"))
+    att = (torch.softmax(sc, -1) @ vh).permute(0, 2, 1, 3).reshape(T, h)
+    y = x + att @ wo
+    n2 = rms(y, n2w)
+    act = (n2 @ wup) * torch.nn.functional.silu(n2 @ wgate)
+    return y + act @ wdown
+
+
+@pytest.mark.parametrize("B,S", [(2, 1024)])
+def test_c2_width_block_matches_torch_fp32(B, S):
+    h, f, H, theta = 3584, 18944, 28, 1e6
+    T = B * S
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(7)
+    n_mm = 4 * h * h + 3 * h * f
+    Wb = (torch.randn(n_mm, device=dev, generator=g) * 0.02).clamp(-0.04, 0.04)
+    Wb = torch.cat([Wb, 1.0 + 0.1 * torch.randn(2 * h, device=dev, generator=g)]).bfloat16()
+    x = torch.randn(T, h, device=dev, generator=g)
+    g_out = torch.randn(T, h, device=dev, generator=g) * 1e-2
+
+    Lb = L.blib()
+    d = L.HlmBlockDims(B, S, h, f, H, 0)
+    y = torch.empty_like(x)
+    acts = torch.empty(Lb.hlm_cuda_block_acts_bytes(ctypes.byref(d)), dtype=torch.uint8, device=dev)
+    ws = torch.empty(Lb.hlm_cuda_block_ws_bytes(ctypes.byref(d)), dtype=torch.uint8, device=dev)
+    hd = h // H
+    cs = torch.empty(S * hd // 2, device=dev); sn = torch.empty_like(cs)
+    L.check(Lb.hlm_cuda_rope_table(vp(cs), vp(sn), S, hd, theta))
+    L.check(Lb.hlm_cuda_block_fwd(ctypes.byref(d), vp(Wb), vp(x), vp(y), vp(acts), vp(ws), vp(cs), vp(sn), None))
+    g_in = torch.empty_like(x)
+    grad = torch.full((Wb.numel(),), float("nan"), device=dev)
+    L.check(Lb.hlm_cuda_block_bwd(ctypes.byref(d), vp(Wb), vp(x), vp(acts), vp(g_out), vp(g_in), vp(grad),
+                                  vp(ws), vp(cs), vp(sn), None))
+    torch.cuda.synchronize()
+
+    W = Wb.float().requires_grad_(True)
+    xr = x.clone().requires_grad_(True)
+    y_ref = torch_block(xr, W, h, f, H, S, theta)
+    y_ref.backward(g_out)
+    errs = {"out": rel(y, y_ref.detach()), "g_in": rel(g_in, xr.grad)}
+    assert errs["out"] < 1e-2
+    assert errs["g_in"] < 5e-2
+    assert not torch.isnan(grad).any()
+    o = 0
+    for name, n in (("w_q", h * h), ("w_k", h * h), ("w_v", h * h), ("w_o", h * h), ("w_up", h * f),
+                    ("w_gate", h * f), ("w_down", f * h), ("norm1", h), ("norm2", h)):
+        e = rel(grad[o:o + n], W.grad[o:o + n])
+        errs[name] = e
+        assert e < (1e-1 if name in ("w_q", "w_k") else 5e-2), (name, e)
+        o += n
+    print("c2-width block rel-L2:", {k: f"{v:.1e}" for k, v in errs.items()})
