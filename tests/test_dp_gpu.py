@@ -13,7 +13,8 @@ from paper_2602_04816_b200 import engine as E
 pytestmark = pytest.mark.gpu
 
 
-def test_dp_world1_nccl_paths_match_single_process_engine():
+@pytest.mark.parametrize("extra", [dict(), dict(piece_elems=1000, grad_buffers=4)])
+def test_dp_world1_nccl_paths_match_single_process_engine(extra):
     c = E.ModelConfig(4, 64, 128, 96, 32, 2, k_ckpt=1, n_heads=1)
     toks = [E.make_copy_task_batch(c, 5, skip=i) for i in range(3)]
     ref = E.Store(c, 11)
@@ -27,7 +28,7 @@ def test_dp_world1_nccl_paths_match_single_process_engine():
     e1 = E.Engine(s, E.Arena(c), E.HyperParams(lr=2e-3),
                   E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=4,
                                   overlap_optimizer_tail=True, tail_blocks=1, rank=0, world=1,
-                                  comm_grad=comm_g, comm_weights=comm_w))
+                                  comm_grad=comm_g, comm_weights=comm_w, **extra))
     l1 = [e1.train_step(t).loss for t in toks]
     e1.sync()
     assert l0 == l1
