@@ -189,6 +189,8 @@ private:
     // finiteness flag and one per piece, so the host Adam starts on the first piece
     // instead of waiting for the whole tile (the head gradient is 2.2 GB at C2).
     static constexpr i64 kPieceElems = i64(64) << 20;
+    // the host Adam publishes progress (and a forward H2D copies) in 16 Mi-element steps
+    static constexpr i64 kPublishElems = i64(16) << 20;
     i64 piece_elems_ = kPieceElems;     // EngineOptions::piece_elems (tests use small pieces)
     i64 max_pieces_ = 1;
     std::vector<void*> ev_slab_flag_;    // per slab

@@ -350,8 +350,9 @@ int Engine::stream_tile(i64 tile_id, i64* op_id, bool forward_pass) {
         uint16_t* dst = static_cast<uint16_t*>(arena_.cache_slot(slot));
         bool waiting = true;
         i64 id = -1;
-        for (i64 off = 0; off < n; off += piece_elems_) {
-            const i64 len = std::min(piece_elems_, n - off);
+        const i64 hp = std::min(piece_elems_, kPublishElems);
+        for (i64 off = 0; off < n; off += hp) {
+            const i64 len = std::min(hp, n - off);
             if (waiting) waiting = wait_elems_current(tile_id, off + len);
             StreamOp op;
             op.stream = StreamId::H2D;
@@ -549,12 +550,18 @@ void Engine::consume(const Pending& p) {
         for (i64 k = 0; k < p.pieces; ++k) {
             const i64 off = k * p.piece, len = std::min(p.piece, p.count - off);
             ck(cudaEventSynchronize(E(ev_piece_[static_cast<size_t>(p.slab * max_pieces_ + k)])), "piece sync");
-            adam_step_range(tile, g + off, base + off, len, hyper_, p.t, /*prechecked=*/true);
-            if (opts_.world == 1) {   // a forward H2D may copy this piece now
-                std::lock_guard<std::mutex> lk(mu_);
-                progress_[pi] = off + len;
+            // optimise in sub-pieces and publish each: a forward H2D copies right behind
+            for (i64 so = 0; so < len; so += kPublishElems) {
+                const i64 sl = std::min(kPublishElems, len - so);
+                adam_step_range(tile, g + off + so, base + off + so, sl, hyper_, p.t, /*prechecked=*/true);
+                if (opts_.world == 1) {
+                    {
+                        std::lock_guard<std::mutex> lk(mu_);
+                        progress_[pi] = off + so + sl;
+                    }
+                    cv_.notify_all();
+                }
             }
-            if (opts_.world == 1) cv_.notify_all();
         }
         {   // the version now covers the whole tile; progress counts the next update
             std::lock_guard<std::mutex> lk(mu_);

@@ -176,9 +176,9 @@ def exposed_weights(ops):
     by_id = {o["id"]: o for o in ops}
     comp = sorted((o for o in ops if o["stream"] == "compute" and o["t_end_us"] > o["t_start_us"] >= 0),
                   key=lambda o: o["t_start_us"])
-    prev, idle, exposed = None, 0.0, 0.0
+    prev, idle, exposed = 0.0, 0.0, 0.0   # timestamps are relative to the step-start event
     for c in comp:
-        if prev is not None and c["t_start_us"] > prev:
+        if c["t_start_us"] > prev:
             g0, g1 = prev, c["t_start_us"]
             idle += g1 - g0
             spans = []
@@ -189,7 +189,7 @@ def exposed_weights(ops):
                     if hi > lo:
                         spans.append((lo, hi))
             exposed += sum(e - s for s, e in _union(spans))
-        prev = c["t_end_us"] if prev is None else max(prev, c["t_end_us"])
+        prev = max(prev, c["t_end_us"])
     busy = sum(o["t_end_us"] - o["t_start_us"] for o in ops
                if o["stream"] == "h2d" and o["t_end_us"] > o["t_start_us"] >= 0)
     return {"compute_idle_ms": idle / 1e3, "h2d_exposed_ms": exposed / 1e3,
