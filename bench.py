@@ -322,7 +322,7 @@ def run_ours(args, m, name):
     arena = E.Arena(cfg, device=local, weight_cache_bytes=cache)
     n_slab, tail = pick_slabs(args, m, nums, world, local_world)
     opts = E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=n_slab,
-                           grad_buffers=args.grad_buffers,
+                           grad_buffers=args.grad_buffers, sparse_embed_grad=not args.dense_embed_grad,
                            record_trace=True, overlap_optimizer_tail=tail >= 0,
                            tail_blocks=max(0, tail), rank=rank, world=world,
                            comm_grad=comm_g, comm_weights=comm_w, host_threads=adam_threads,
@@ -358,6 +358,7 @@ def run_ours(args, m, name):
         losses.append(r.loss)
         gpu_ms.append(r.gpu_ms)
         h2d_step = r.h2d_bytes
+        d2h_step = r.d2h_bytes
     eng.wait_optimizer()   # the last step's host optimizer tail is inside the timed region
     lib.hlm_timer_record(1)
     wall = time.perf_counter() - wall0
@@ -431,7 +432,9 @@ def run_ours(args, m, name):
     lib.hlm_host_triad_gbs.restype = ctypes.c_double
     lib.hlm_host_triad_gbs.argtypes = [ctypes.c_int64, ctypes.c_int]
     host_bw = lib.hlm_host_triad_gbs(1 << 30, 3) if rank == 0 else None
-    host_bytes = nums["params"] * 34 + h2d_step
+    # 26 B/param of Adam state traffic (w, m, v read + written, bf16 shadow written) + the
+    # gradient bytes twice (DMA write, Adam read) + the weight DMA read
+    host_bytes = nums["params"] * 26 + 2 * d2h_step + h2d_step
     # STREAM counts 3 arrays for a triad but the DRAM also serves the write-allocate read of
     # `a`: raw bandwidth = 4/3 x triad. Our traffic is raw (non-temporal shadow stores, DMA
     # writes whole lines, w/m/v are read before written).
@@ -486,7 +489,7 @@ def run_ours(args, m, name):
         "hw_tflops": nums["hw_flops"] / step_s / 1e12,
         "e2e": {"value": e2e, "unit": "tokens/s",
                 "h2d_bytes_per_step": int(h2d_step + 8 * nums["T"]),
-                "d2h_bytes_per_step": int(nums["d2h"] + 4 * nums["T"])},
+                "d2h_bytes_per_step": int(d2h_step + 4 * nums["T"])},
         "gpu_launches": int(launches),
         "roofline": {"bound": "tensor", "kernel": "gemm_sm100 (tcgen05/TMA): every GEMM launch of the timed "
                                                   "steps (block fwd / recompute / dgrad / wgrad, head)",
@@ -522,8 +525,9 @@ def run_ours(args, m, name):
         "host_roofline": {"host_bytes_per_step": int(host_bytes), "triad_gbs": host_bw,
                           "raw_dram_gbs": raw_bw, "t_host_s": t_host,
                           "frac": (t_host / step_s) if t_host else None,
-                          "def": "(30 B/param host Adam + 4 B/param gradient DMA + weight DMA bytes)"
-                                 " / (4/3 x measured 16-thread STREAM triad = raw DRAM bandwidth)"},
+                          "def": "(26 B/param host Adam state + gradient bytes x 2 (DMA write, Adam read) + "
+                                 "weight DMA bytes) / (4/3 x measured 16-thread STREAM triad = raw DRAM "
+                                 "bandwidth)"},
         "stream": {"h2d_gbs": h2d_gbs, "d2h_gbs": d2h_gbs, "overlap": overlap,
                    "h2d_overlap": rep["h2d_overlap"], "h2d_exposed_s": rep["h2d_exposed_ms"] / 1e3,
                    "compute_idle_s": rep["compute_idle_ms"] / 1e3,
@@ -563,6 +567,8 @@ def main():
     ap.add_argument("--grad-buffers", type=int, default=8,
                     help="device fp32 gradient buffers (2 = the arena's; more let the backward run "
                          "ahead of a slow D2H)")
+    ap.add_argument("--dense-embed-grad", action="store_true",
+                    help="ship the whole (V, h) embedding gradient (default: only the batch's token rows)")
     ap.add_argument("--no-hybrid", action="store_true",
                     help="skip the measured HBM-resident-optimizer variant reported beside the headline")
     ap.add_argument("--resident-blocks", type=int, default=0,

@@ -79,6 +79,10 @@ struct EngineOptions {
     // Outbound fp32 gradient buffers on the device (>= 2; the arena holds two, the engine
     // allocates the rest, each the widest tile).
     i64 grad_buffers = 2;
+    // Row-sparse embedding gradient: only the rows of the batch's tokens are computed,
+    // copied and read by the host Adam (the other rows' gradient is exactly zero; their
+    // Adam update runs without reading one). Single GPU, untied, eager optimizer.
+    bool sparse_embed_grad = false;
     bool resident_embed = false;
 };
 
@@ -137,6 +141,7 @@ private:
         i64 count = 0;  // fp32 elements copied into the slab (the tile, or this rank's shard)
         i64 pieces = 1; // D2H pieces, each with its own event (the optimizer starts on piece 0)
         i64 piece = 0;  // elements per piece
+        bool sparse_rows = false;   // row-compact embedding gradient (embed_row_map_)
     };
     struct HostOpRecord {   // host-side Accum / OptStep, appended to the trace in finish_step
         i64 slab, layer, grad_op, step;   // step: the gradient's step (an earlier one for a tail tile)
@@ -154,7 +159,7 @@ private:
     void compute_wait_weights(int buf);
     void compute_done_with(int buf, i64 op_id);
     int next_grad_buf();
-    void evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op);
+    void evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op, bool sparse_rows = false);
     void consume(const Pending& p);          // READY -> ACCUMULATING -> FREE (+ Adam)
     void process_oldest_inline();
     void worker_loop();
@@ -218,6 +223,12 @@ private:
     unsigned long long* nf2_dev_ = nullptr;
     unsigned long long* nf2_host_ = nullptr;
     i64 acquire_slab(i64 bytes);        // back-pressure: blocks (worker) or consumes inline
+    // row-sparse embedding gradient state of the running step
+    bool sparse_embed_ = false;
+    int32_t* embed_rows_host_ = nullptr;   // pinned: touched rows, ascending
+    int32_t* embed_rows_dev_ = nullptr;
+    std::vector<int32_t> embed_row_map_;   // row -> compact index or -1
+    i64 embed_rows_n_ = 0;
     void anchor_loss_pieces(int buf, i64 w_op);
     void* ev_step_start_ = nullptr;
     void* ev_step_end_ = nullptr;

@@ -276,6 +276,12 @@ void adam_step_range(LayerTile& tile, const float* grad, i64 begin, i64 count, c
 
 // grads(tile) += g  (slab accumulation, host_store.cpp:254-284, FP32).
 void accumulate_grads(LayerTile& tile, const float* g);
+// Adam over a (rows x width) tile whose gradient is zero except on the rows with
+// row_map[r] >= 0, whose gradient row is compact[row_map[r] * width ...]: the zero
+// rows are optimised without reading a gradient. Bit-identical to adam_step_tile_from
+// on the dense gradient (same per-element IEEE operations).
+void adam_step_rows_sparse(LayerTile& tile, i64 rows, i64 width, const std::int32_t* row_map, const float* compact,
+                           const HyperParams& hyper, i64 t);
 
 // Anonymous huge-page-advised mapping (throws on failure).
 void* map_huge_public(size_t bytes);

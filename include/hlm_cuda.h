@@ -142,6 +142,13 @@ size_t hlm_cuda_head_ws_bytes(int64_t rows, int64_t hidden, int64_t vocab);
  * hlm_cuda_head_chunk_vocab: the largest vc (multiple of 128) the ws holds. */
 #define HLM_HEAD_UNCERTIFIED 0xFFFFFFFFFFFFFFFEull
 
+/* Row-compact embedding gradient (reference embed_bwd_acc, kernels.hpp:396-408, for
+ * the touched rows only): out[c] = sum of g rows at the positions of token rows[c]
+ * (CSR from hlm_embed_csr; rows ascending) — equal to hlm_cuda_embed_bwd's row
+ * rows[c] bit for bit; the (vocab - n_rows) untouched rows are exactly zero there. */
+int hlm_cuda_embed_bwd_compact(const int32_t* row_ptr, const int32_t* pos, const int32_t* rows, int64_t n_rows,
+                               const float* g, float* out, int64_t hidden, void* stream);
+
 /* ------------------------------------------------------------------ kernel timer
  * Per-launch CUDA-event timing of the hot kernels inside a timed region (the
  * bench's roofline.achieved): when enabled, every GEMM / attention launch is
@@ -259,6 +266,9 @@ typedef struct HlmEngineOptions {
   int64_t piece_elems;
   /* outbound fp32 gradient buffers on the device (<= 2: the arena's two) */
   int64_t grad_buffers;
+  /* row-sparse embedding gradient (only the batch's token rows computed, copied and
+   * read by the host Adam; bit-identical results) */
+  int32_t sparse_embed_grad;
 } HlmEngineOptions;
 
 typedef struct HlmStepResult {

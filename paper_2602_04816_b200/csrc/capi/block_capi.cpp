@@ -517,6 +517,15 @@ int hlm_cuda_embed_bwd(const int32_t* row_ptr, const int32_t* pos, const float* 
   });
 }
 
+int hlm_cuda_embed_bwd_compact(const int32_t* row_ptr, const int32_t* pos, const int32_t* rows, int64_t n_rows,
+                               const float* g, float* out, int64_t hidden, void* stream) {
+  return guarded([&] {
+    chk(hlm_ops_embed_bwd_compact(row_ptr, pos, rows, (int)n_rows, g, out, (int)hidden,
+                                  static_cast<cudaStream_t>(stream)),
+        "embed bwd compact");
+  });
+}
+
 int hlm_embed_csr(const int32_t* tokens, int64_t rows, int64_t vocab, int32_t* row_ptr, int32_t* pos) {
   for (int64_t v = 0; v <= vocab; ++v) row_ptr[v] = 0;
   for (int64_t t = 0; t < rows; ++t) {

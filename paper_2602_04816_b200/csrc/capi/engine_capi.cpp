@@ -113,6 +113,7 @@ hlm::EngineOptions to_opts(const HlmEngineOptions* o) {
         e.head_piece_vocab = o->head_piece_vocab;
         e.piece_elems = o->piece_elems;
         e.grad_buffers = o->grad_buffers > 2 ? o->grad_buffers : 2;
+        e.sparse_embed_grad = o->sparse_embed_grad != 0;
     }
     return e;
 }

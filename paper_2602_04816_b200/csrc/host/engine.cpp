@@ -183,6 +183,15 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
             q += (t.n_params() * 14 + 255) / 256 * 256;
         }
     }
+    sparse_embed_ = opts_.sparse_embed_grad && !m.tie_embeddings && resident_of_[0] < 0 && opts_.world == 1 &&
+                    !opts_.comm_grad && opts_.eager_optim && !opts_.skip_optimizer;
+    if (sparse_embed_) {
+        ck(cudaHostAlloc(reinterpret_cast<void**>(&embed_rows_host_), static_cast<size_t>(m.vocab) * 4,
+                         cudaHostAllocPortable),
+           "cudaHostAlloc embed rows");
+        ck(cudaMalloc(&embed_rows_dev_, static_cast<size_t>(m.vocab) * 4), "cudaMalloc embed rows");
+        embed_row_map_.assign(static_cast<size_t>(m.vocab), -1);
+    }
     // head prefetch: as early as possible, such that no block after the prefetch point
     // uses a stream buffer (cached or HBM-resident), and at the latest before block L - 1
     if (opts_.overlap_optimizer_tail && !m.tie_embeddings && m.k_ckpt == 1 && opts_.fused_recompute &&
@@ -236,6 +245,8 @@ Engine::~Engine() {
     for (void* e : ev_grad_ready_) cudaEventDestroy(E(e));
     for (void* e : ev_gradbuf_free_) cudaEventDestroy(E(e));
     if (gbuf_mem_) cudaFree(gbuf_mem_);
+    if (embed_rows_host_) cudaFreeHost(embed_rows_host_);
+    if (embed_rows_dev_) cudaFree(embed_rows_dev_);
     for (void* e : ev_piece_) cudaEventDestroy(E(e));
     for (void* e : ev_head_chunk_) cudaEventDestroy(E(e));
     if (ev_head_cert_) cudaEventDestroy(E(ev_head_cert_));
@@ -465,7 +476,7 @@ i64 Engine::acquire_slab(i64 bytes) {
 
 // reference engine.cpp:103-121: acquire a slab (inline back-pressure
 // consumes the oldest READY slab), D2H the fp32 gradient, emit GradXfer.
-void Engine::evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op) {
+void Engine::evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op, bool sparse_rows) {
     ck(cudaEventRecord(E(ev_grad_ready_[gbuf]), S(compute_)), "record grad ready");
     const i64 cnt = opts_.comm_grad ? shard_elems(n_params) : n_params;
     const i64 bytes = 4 * cnt;
@@ -506,7 +517,7 @@ void Engine::evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op) {
     ck(cudaEventRecord(E(ev_gradbuf_free_[gbuf]), S(d2h_)), "record grad buf free");
     {
         std::lock_guard<std::mutex> lk(mu_);
-        pending_.push_back({slab, tile_id, id, step_index_, step_t_, cnt, pieces, piece_elems_});
+        pending_.push_back({slab, tile_id, id, step_index_, step_t_, cnt, pieces, piece_elems_, sparse_rows});
     }
     cv_.notify_all();
 }
@@ -520,7 +531,7 @@ void Engine::consume(const Pending& p) {
     const bool optimise = opts_.eager_optim && !opts_.skip_optimizer;
     // fused (slab IS the gradient, one consumer): wait for the finiteness flag, then
     // optimise piece by piece as the D2H lands; otherwise wait for the whole slab
-    const bool piecewise = optimise && store_.consumer_count(phys) == 1;
+    const bool piecewise = optimise && store_.consumer_count(phys) == 1 && !p.sparse_rows;
     ck(cudaEventSynchronize(E(piecewise ? ev_slab_flag_[static_cast<size_t>(p.slab)]
                                         : ev_slab_done_[static_cast<size_t>(p.slab)])),
        "slab sync");
@@ -534,6 +545,12 @@ void Engine::consume(const Pending& p) {
     if (bad == HLM_HEAD_UNCERTIFIED) {   // vocab-chunked head without a certificate: the full scan
         ck(cudaEventSynchronize(E(ev_slab_done_[static_cast<size_t>(p.slab)])), "slab sync");
         bad = nf2_host_[p.slab];
+    }
+    if (bad != ~0ull && optimise && p.sparse_rows) {   // compact index -> table element
+        const i64 h = store_.config().hidden;
+        const i64 c = static_cast<i64>(bad) / h, j = static_cast<i64>(bad) % h;
+        throw NumericsError("non-finite gradient in layer " + std::to_string(tile.layer_id()) + " at element " +
+                            std::to_string(static_cast<i64>(embed_rows_host_[c]) * h + j) + "; step aborted");
     }
     if (bad != ~0ull && optimise) {
         const i64 base = opts_.comm_grad ? opts_.rank * shard_elems(tile.n_params()) : 0;
@@ -594,6 +611,14 @@ void Engine::consume(const Pending& p) {
                 rec.topt1 = now_us();
             }
         }
+    } else if (p.sparse_rows) {
+        // row-compact embedding gradient: untouched rows optimised with a zero gradient
+        rec.t1 = now_us();
+        rec.opt = true;
+        rec.topt0 = rec.t1;
+        const ModelConfig& m = store_.config();
+        adam_step_rows_sparse(tile, m.vocab, m.hidden, embed_row_map_.data(), pool_->data(p.slab), hyper_, p.t);
+        rec.topt1 = now_us();
     } else if (piecewise) {
         // fused: the pinned slab IS the gradient; no store gradient region touched
         adam_pieces(0);
@@ -1181,13 +1206,32 @@ void Engine::backward_blockwise() {
     eop.kind = OpKind::LocalBackward;
     eop.layer = m.embed_tile_id();
     eop.flops = bwd_flops(n_embed, T);
+    if (sparse_embed_) {   // the batch's distinct tokens, ascending (CSR order)
+        i64 n = 0;
+        for (i64 v = 0; v < m.vocab; ++v) {
+            const bool touched = rp[v + 1] > rp[v];
+            embed_row_map_[static_cast<size_t>(v)] = touched ? static_cast<int32_t>(n) : -1;
+            if (touched) embed_rows_host_[n++] = static_cast<int32_t>(v);
+        }
+        embed_rows_n_ = n;
+        ck(cudaMemcpyAsync(embed_rows_dev_, embed_rows_host_, static_cast<size_t>(std::max<i64>(n, 1)) * 4,
+                           cudaMemcpyHostToDevice, S(compute_)),
+           "H2D embed rows");
+    }
     const i64 lb = op_begin(eop, compute_);
-    ck_hlm(hlm_cuda_embed_bwd(arena_.csr_row_ptr(), arena_.csr_pos(), arena_.g_roll(g_cur_), grad_buf(gb),
-                              m.vocab, m.hidden, 0, compute_),
-           "embed_bwd");
+    if (sparse_embed_)
+        ck_hlm(hlm_cuda_embed_bwd_compact(arena_.csr_row_ptr(), arena_.csr_pos(), embed_rows_dev_, embed_rows_n_,
+                                          arena_.g_roll(g_cur_), grad_buf(gb), m.hidden, compute_),
+               "embed_bwd_compact");
+    else
+        ck_hlm(hlm_cuda_embed_bwd(arena_.csr_row_ptr(), arena_.csr_pos(), arena_.g_roll(g_cur_), grad_buf(gb),
+                                  m.vocab, m.hidden, 0, compute_),
+               "embed_bwd");
     op_end(lb, compute_);
     if (is_resident(m.embed_tile_id()))
         resident_update(m.embed_tile_id(), gb, lb);
+    else if (sparse_embed_)
+        evacuate(m.embed_tile_id(), gb, std::max<i64>(embed_rows_n_, 1) * m.hidden, lb, true);
     else
         evacuate(m.embed_tile_id(), gb, n_embed, lb);
     phase_ = Phase::Optimize;

@@ -659,6 +659,60 @@ void adam_step_range(LayerTile& tile, const float* grad, i64 begin, i64 count, c
                 count, lr, b1, b2, eps, wd, bc1, bc2, nullptr);
 }
 
+void adam_step_rows_sparse(LayerTile& tile, i64 rows, i64 width, const std::int32_t* row_map, const float* compact,
+                           const HyperParams& hyper, i64 t) {
+    if (t < 1) throw ProtocolError("adam step index must be >= 1");
+    if (rows * width != tile.n_params()) throw ProtocolError("sparse adam: geometry mismatch");
+    const float lr = static_cast<float>(hyper.lr), b1 = static_cast<float>(hyper.beta1),
+                b2 = static_cast<float>(hyper.beta2), eps = static_cast<float>(hyper.eps),
+                wd = static_cast<float>(hyper.weight_decay);
+    const float bc1 = 1.0f - std::pow(b1, static_cast<float>(t));
+    const float bc2 = 1.0f - std::pow(b2, static_cast<float>(t));
+    const float omb1 = 1.0f - b1, omb2 = 1.0f - b2;
+    float* W = tile.master();
+    float* M = tile.moment_m();
+    float* Vv = tile.moment_v();
+    std::uint16_t* SH = tile.shadow();
+#pragma omp parallel for schedule(static, 16)
+    for (i64 r = 0; r < rows; ++r) {
+        const i64 b = r * width, e = b + width;
+        const float* g = row_map[r] >= 0 ? compact + static_cast<i64>(row_map[r]) * width - b : nullptr;
+        const __m512 vb1 = _mm512_set1_ps(b1), vb2 = _mm512_set1_ps(b2), vo1 = _mm512_set1_ps(omb1),
+                     vo2 = _mm512_set1_ps(omb2), vbc1 = _mm512_set1_ps(bc1), vbc2 = _mm512_set1_ps(bc2),
+                     veps = _mm512_set1_ps(eps), vwd = _mm512_set1_ps(wd), vlr = _mm512_set1_ps(lr);
+        i64 i = b;
+        for (; i + 16 <= e; i += 16) {   // adam_kernel's lane sequence; a zero gradient is not read
+            const __m512 gg = g ? _mm512_loadu_ps(g + i) : _mm512_setzero_ps();
+            __m512 mm = _mm512_loadu_ps(M + i);
+            __m512 vv = _mm512_loadu_ps(Vv + i);
+            __m512 th = _mm512_loadu_ps(W + i);
+            mm = _mm512_add_ps(_mm512_mul_ps(vb1, mm), _mm512_mul_ps(vo1, gg));
+            vv = _mm512_add_ps(_mm512_mul_ps(vb2, vv), _mm512_mul_ps(_mm512_mul_ps(vo2, gg), gg));
+            const __m512 mhat = _mm512_div_ps(mm, vbc1);
+            const __m512 vhat = _mm512_div_ps(vv, vbc2);
+            const __m512 upd = _mm512_add_ps(_mm512_div_ps(mhat, _mm512_add_ps(_mm512_sqrt_ps(vhat), veps)),
+                                             _mm512_mul_ps(vwd, th));
+            th = _mm512_sub_ps(th, _mm512_mul_ps(vlr, upd));
+            _mm512_storeu_ps(M + i, mm);
+            _mm512_storeu_ps(Vv + i, vv);
+            _mm512_storeu_ps(W + i, th);
+            _mm256_storeu_si256(reinterpret_cast<__m256i*>(SH + i), bf16x16(th));
+        }
+        for (; i < e; ++i) {
+            const float gv = g ? g[i] : 0.0f;
+            M[i] = b1 * M[i] + (1.0f - b1) * gv;
+            Vv[i] = b2 * Vv[i] + (1.0f - b2) * gv * gv;
+            const float mhat = M[i] / bc1;
+            const float vhat = Vv[i] / bc2;
+            float th = W[i];
+            th -= lr * (mhat / (std::sqrt(vhat) + eps) + wd * th);
+            W[i] = th;
+            SH[i] = bf16_bits_from_f32(th);
+        }
+    }
+    tile.bump_version(0);
+}
+
 void adam_step_tile_from(LayerTile& tile, const float* grad, const HyperParams& hyper, i64 t, bool prechecked) {
     adam_apply(tile, grad, hyper, t, nullptr, prechecked);
 }

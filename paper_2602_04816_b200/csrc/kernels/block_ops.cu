@@ -521,6 +521,24 @@ __global__ void embed_bwd_kernel(const int32_t* __restrict__ row_ptr, const int3
   }
 }
 
+// Row-compact embedding gradient: out[c][j] = sum over the positions of token
+// rows[c] (ascending, the CSR order of embed_bwd_kernel, so each touched row equals
+// embed_bwd_kernel's bit for bit) of g[p][j]. Untouched rows are not materialised.
+__global__ void embed_bwd_compact_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ pos,
+                                         const int32_t* __restrict__ rows, int n_rows, const float* __restrict__ g,
+                                         float* __restrict__ out, int h) {
+  const long long n = (long long)n_rows * h;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int c = (int)(i / h);
+    const int j = (int)(i - (long long)c * h);
+    const int v = rows[c];
+    float acc = 0.f;
+    for (int k = row_ptr[v]; k < row_ptr[v + 1]; ++k) acc += g[(long long)pos[k] * h + j];
+    out[i] = acc;
+  }
+}
+
 // ------------------------------------------------------------------ cross entropy
 // One CTA per row. loss_row[r] = (logz - l[tgt]) * inv_rows ;
 // d_logits = (softmax - onehot) * inv_rows (bf16, row stride ld).
@@ -1016,6 +1034,15 @@ int hlm_ops_rope(void* x, const float* cs, const float* sn, long long rows, int 
 int hlm_ops_embed_fwd(const int32_t* tok, const void* table, float* out, long long rows, int h, int vocab,
                       int* err, cudaStream_t s) {
   embed_fwd_kernel<<<grid_for(rows * h, 256), 256, 0, s>>>(tok, (const __nv_bfloat16*)table, out, rows, h, vocab, err);
+  hlm_count_launches(1);
+  HLM_CHECK_LAUNCH();
+}
+
+int hlm_ops_embed_bwd_compact(const int32_t* row_ptr, const int32_t* pos, const int32_t* rows, int n_rows,
+                              const float* g, float* out, int h, cudaStream_t s) {
+  if (n_rows <= 0) return 0;
+  embed_bwd_compact_kernel<<<grid_for((long long)n_rows * h, 256), 256, 0, s>>>(row_ptr, pos, rows, n_rows, g, out,
+                                                                                 h);
   hlm_count_launches(1);
   HLM_CHECK_LAUNCH();
 }

@@ -20,6 +20,8 @@ int hlm_ops_embed_fwd(const int32_t* tok, const void* table, float* out, long lo
                       int* err, cudaStream_t s);
 int hlm_ops_embed_bwd(const int32_t* row_ptr, const int32_t* pos, const float* g, float* d_table, int vocab,
                       int h, int accumulate, cudaStream_t s);
+int hlm_ops_embed_bwd_compact(const int32_t* row_ptr, const int32_t* pos, const int32_t* rows, int n_rows,
+                              const float* g, float* out, int h, cudaStream_t s);
 int hlm_ops_ce(const float* logits, long long ld_in, const int32_t* tgt, void* dl, long long ld_out,
                float* loss_row, long long rows, int vocab, float inv_rows, int* err, cudaStream_t s);
 // Vocab-chunked head (hlm_cuda_head_stats / hlm_cuda_head_grad_chunk): pass-1 row

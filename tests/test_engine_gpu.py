@@ -324,7 +324,8 @@ def test_hbm_resident_optimizer_tiles_are_bitwise_neutral(res):
 
 
 @pytest.mark.parametrize("pieces", [dict(piece_elems=1000), dict(piece_elems=4096, head_piece_vocab=8),
-                                    dict(piece_elems=1000, grad_buffers=5)])
+                                    dict(piece_elems=1000, grad_buffers=5), dict(sparse_embed_grad=True),
+                                    dict(sparse_embed_grad=True, piece_elems=700, grad_buffers=3)])
 def test_piecewise_transfers_are_bitwise_neutral(pieces):
     """Gradients landing in pieces with the host Adam piece by piece, and the
     forward H2D of cached blocks copied piece by piece behind the optimizer:
@@ -350,3 +351,15 @@ def test_piecewise_transfers_are_bitwise_neutral(pieces):
     else:
         assert res[0][0] == res[1][0]
         assert res[0][1].bitwise_equal(res[1][1])
+
+
+def test_sparse_embedding_gradient_non_finite_names_the_table_element():
+    c = E.ModelConfig(2, 16, 32, 13, 4, 1)
+    s = E.Store(c, 5, "fp32")
+    w = s.weights()
+    tok = E.make_copy_task_batch(c, 2)
+    w[int(tok[0]) * c.hidden + 3] = np.inf   # an embedding row the batch reads
+    s.import_master(w)
+    e = E.Engine(s, E.Arena(c), E.HyperParams(), E.EngineOptions(eager_optim=True, sparse_embed_grad=True))
+    with pytest.raises(E.NumericsError, match="non-finite gradient in layer"):
+        e.train_step(tok)
