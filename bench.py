@@ -323,6 +323,7 @@ def run_ours(args, m, name):
     n_slab, tail = pick_slabs(args, m, nums, world, local_world)
     opts = E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=n_slab,
                            grad_buffers=args.grad_buffers, sparse_embed_grad=not args.dense_embed_grad,
+                           embed_gather_host=not args.dense_embed_grad,
                            record_trace=True, overlap_optimizer_tail=tail >= 0,
                            tail_blocks=max(0, tail), rank=rank, world=world,
                            comm_grad=comm_g, comm_weights=comm_w, host_threads=adam_threads,
@@ -568,7 +569,8 @@ def main():
                     help="device fp32 gradient buffers (2 = the arena's; more let the backward run "
                          "ahead of a slow D2H)")
     ap.add_argument("--dense-embed-grad", action="store_true",
-                    help="ship the whole (V, h) embedding gradient (default: only the batch's token rows)")
+                    help="stream the whole (V, h) embedding table / gradient (default: only the batch's "
+                         "token rows: zero-copy gather in the forward, row-sparse gradient)")
     ap.add_argument("--no-hybrid", action="store_true",
                     help="skip the measured HBM-resident-optimizer variant reported beside the headline")
     ap.add_argument("--resident-blocks", type=int, default=0,

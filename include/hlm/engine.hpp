@@ -83,6 +83,10 @@ struct EngineOptions {
     // copied and read by the host Adam (the other rows' gradient is exactly zero; their
     // Adam update runs without reading one). Single GPU, untied, eager optimizer.
     bool sparse_embed_grad = false;
+    // Forward embedding lookup reads the batch's rows straight from the pinned host BF16
+    // shadow (zero-copy over PCIe: T x h x 2 bytes) instead of streaming the (V, h) table.
+    // Single GPU, untied, host-resident embedding.
+    bool embed_gather_host = false;
     bool resident_embed = false;
 };
 
@@ -229,6 +233,7 @@ private:
     int32_t* embed_rows_dev_ = nullptr;
     std::vector<int32_t> embed_row_map_;   // row -> compact index or -1
     i64 embed_rows_n_ = 0;
+    const void* embed_host_dev_ = nullptr;   // device alias of the embedding's pinned shadow (zero-copy)
     void anchor_loss_pieces(int buf, i64 w_op);
     void* ev_step_start_ = nullptr;
     void* ev_step_end_ = nullptr;

@@ -269,6 +269,8 @@ typedef struct HlmEngineOptions {
   /* row-sparse embedding gradient (only the batch's token rows computed, copied and
    * read by the host Adam; bit-identical results) */
   int32_t sparse_embed_grad;
+  /* forward embedding rows gathered zero-copy from the pinned host shadow (no table H2D) */
+  int32_t embed_gather_host;
 } HlmEngineOptions;
 
 typedef struct HlmStepResult {

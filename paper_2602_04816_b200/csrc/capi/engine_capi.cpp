@@ -114,6 +114,7 @@ hlm::EngineOptions to_opts(const HlmEngineOptions* o) {
         e.piece_elems = o->piece_elems;
         e.grad_buffers = o->grad_buffers > 2 ? o->grad_buffers : 2;
         e.sparse_embed_grad = o->sparse_embed_grad != 0;
+        e.embed_gather_host = o->embed_gather_host != 0;
     }
     return e;
 }

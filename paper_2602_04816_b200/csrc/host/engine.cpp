@@ -192,6 +192,15 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
         ck(cudaMalloc(&embed_rows_dev_, static_cast<size_t>(m.vocab) * 4), "cudaMalloc embed rows");
         embed_row_map_.assign(static_cast<size_t>(m.vocab), -1);
     }
+    if (opts_.embed_gather_host && !m.tie_embeddings && resident_of_[0] < 0 && opts_.world == 1 &&
+        !opts_.comm_weights && store_.shadow_pinned()) {
+        void* dp = nullptr;
+        if (cudaHostGetDevicePointer(&dp, const_cast<uint16_t*>(store_.tile(m.embed_tile_id()).shadow()), 0) ==
+            cudaSuccess)
+            embed_host_dev_ = dp;
+        else
+            (void)cudaGetLastError();   // not mapped: stream the table as usual
+    }
     // head prefetch: as early as possible, such that no block after the prefetch point
     // uses a stream buffer (cached or HBM-resident), and at the latest before block L - 1
     if (opts_.overlap_optimizer_tail && !m.tie_embeddings && m.k_ckpt == 1 && opts_.fused_recompute &&
@@ -865,23 +874,29 @@ void Engine::forward_streaming() {
 
     i64 w_op = -1;
     const bool embed_res = is_resident(m.embed_tile_id());
-    const int ebuf = embed_res ? -2 : stream_tile(m.embed_tile_id(), &w_op);
-    if (!embed_res) compute_wait_weights(ebuf);
+    const bool embed_zc = !embed_res && embed_host_dev_ != nullptr;
+    if (embed_zc) {   // zero-copy gather: only the table version must be current
+        wait_tile_current(m.embed_tile_id());
+        arena_.add_h2d(T * m.hidden * 2);
+    }
+    const int ebuf = embed_res ? -2 : embed_zc ? -3 : stream_tile(m.embed_tile_id(), &w_op);
+    if (!embed_res && !embed_zc) compute_wait_weights(ebuf);
     float* h0 = arena_.anchor_checkpoint(0);
     StreamOp op;
     op.stream = StreamId::Compute;
     op.kind = OpKind::Forward;
     op.layer = m.embed_tile_id();
-    op.buf = ebuf;   // -2: HBM-resident weights
+    op.buf = ebuf;   // -2: HBM-resident weights, -3: rows gathered zero-copy from the host shadow
     op.flops = fwd_flops(m.embed_params(), T);
     if (w_op >= 0) op.deps.push_back(w_op);
     i64 id = op_begin(op, compute_);
-    const void* etab = embed_res ? static_cast<const void*>(residents_[static_cast<size_t>(resident_of_[0])].w16)
-                                 : weights_ptr(ebuf);
+    const void* etab = embed_res  ? static_cast<const void*>(residents_[static_cast<size_t>(resident_of_[0])].w16)
+                       : embed_zc ? embed_host_dev_
+                                  : weights_ptr(ebuf);
     ck_hlm(hlm_cuda_embed_fwd(arena_.tokens(), etab, h0, T, m.hidden, m.vocab, arena_.err_flag(), compute_),
            "embed_fwd");
     op_end(id, compute_);
-    if (!embed_res) compute_done_with(ebuf, id);
+    if (!embed_res && !embed_zc) compute_done_with(ebuf, id);
     h_cur_ = h0;
     int roll = 0;
     for (i64 i = 1; i <= m.layers; ++i) {

@@ -504,6 +504,32 @@ __global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, const __nv_bfl
   }
 }
 
+// h % 8 == 0: 16-byte reads of the table (a zero-copy table in pinned host memory is
+// read over PCIe in full 16-byte pieces), two float4 writes.
+__global__ void embed_fwd_vec8_kernel(const int32_t* __restrict__ tok, const uint4* __restrict__ table,
+                                      float4* __restrict__ out, long long rows, int h8, int vocab,
+                                      int* __restrict__ err) {
+  const long long n = rows * h8;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const long long r = i / h8;
+    const int j = (int)(i - r * h8);
+    const int id = tok[r];
+    if (id < 0 || id >= vocab) {
+      if (j == 0) atomicOr(err, 1);
+      out[2 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      out[2 * i + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+      continue;
+    }
+    const uint4 v = table[(long long)id * h8 + j];
+    const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v);
+    const float2 a = __bfloat1622float2(p[0]), b = __bfloat1622float2(p[1]), c = __bfloat1622float2(p[2]),
+                 d = __bfloat1622float2(p[3]);
+    out[2 * i] = make_float4(a.x, a.y, b.x, b.y);
+    out[2 * i + 1] = make_float4(c.x, c.y, d.x, d.y);
+  }
+}
+
 // d_table[v][j] = sum over positions p of token v (ascending) of g[p][j]:
 // the reference's in-order scatter-add (kernels.hpp:396-408) without atomics,
 // driven by a host-built CSR (row_ptr[V+1], pos[]) of the batch tokens.
@@ -1033,7 +1059,12 @@ int hlm_ops_rope(void* x, const float* cs, const float* sn, long long rows, int 
 
 int hlm_ops_embed_fwd(const int32_t* tok, const void* table, float* out, long long rows, int h, int vocab,
                       int* err, cudaStream_t s) {
-  embed_fwd_kernel<<<grid_for(rows * h, 256), 256, 0, s>>>(tok, (const __nv_bfloat16*)table, out, rows, h, vocab, err);
+  if (h % 8 == 0 && (reinterpret_cast<uintptr_t>(table) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0)
+    embed_fwd_vec8_kernel<<<grid_for(rows * (h / 8), 256), 256, 0, s>>>(tok, (const uint4*)table, (float4*)out, rows,
+                                                                        h / 8, vocab, err);
+  else
+    embed_fwd_kernel<<<grid_for(rows * h, 256), 256, 0, s>>>(tok, (const __nv_bfloat16*)table, out, rows, h, vocab,
+                                                             err);
   hlm_count_launches(1);
   HLM_CHECK_LAUNCH();
 }

@@ -28,7 +28,7 @@ GPU_STREAMS = ("h2d", "compute", "d2h")
 
 
 def _consumes_weights(op, embed_tile):
-    if op["buf"] == -2:          # HBM-resident optimizer tile: weights never streamed
+    if op["buf"] in (-2, -3):    # HBM-resident optimizer tile / rows gathered zero-copy from host
         return False
     if op["kind"] in ("Forward", "Recompute"):
         return True

@@ -325,7 +325,8 @@ def test_hbm_resident_optimizer_tiles_are_bitwise_neutral(res):
 
 @pytest.mark.parametrize("pieces", [dict(piece_elems=1000), dict(piece_elems=4096, head_piece_vocab=8),
                                     dict(piece_elems=1000, grad_buffers=5), dict(sparse_embed_grad=True),
-                                    dict(sparse_embed_grad=True, piece_elems=700, grad_buffers=3)])
+                                    dict(sparse_embed_grad=True, piece_elems=700, grad_buffers=3),
+                                    dict(embed_gather_host=True, sparse_embed_grad=True)])
 def test_piecewise_transfers_are_bitwise_neutral(pieces):
     """Gradients landing in pieces with the host Adam piece by piece, and the
     forward H2D of cached blocks copied piece by piece behind the optimizer:
