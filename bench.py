@@ -280,6 +280,8 @@ def run_ours(args, m, name):
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
     # ranks on one host split its cores for their shard of the Adam (init keeps all cores)
     adam_threads = max(1, (os.cpu_count() or 16) // local_world) if world > 1 else 0
+    if args.host_threads > 0:
+        adam_threads = args.host_threads
     from paper_2602_04816_b200 import _lib
     from paper_2602_04816_b200 import engine as E
 
@@ -323,7 +325,7 @@ def run_ours(args, m, name):
     n_slab, tail = pick_slabs(args, m, nums, world, local_world)
     opts = E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=n_slab,
                            grad_buffers=args.grad_buffers, sparse_embed_grad=not args.dense_embed_grad,
-                           embed_gather_host=not args.dense_embed_grad,
+                           embed_gather_host=not args.dense_embed_grad, pin_threads=not args.no_pin,
                            record_trace=True, overlap_optimizer_tail=tail >= 0,
                            tail_blocks=max(0, tail), rank=rank, world=world,
                            comm_grad=comm_g, comm_weights=comm_w, host_threads=adam_threads,
@@ -571,6 +573,9 @@ def main():
     ap.add_argument("--dense-embed-grad", action="store_true",
                     help="stream the whole (V, h) embedding table / gradient (default: only the batch's "
                          "token rows: zero-copy gather in the forward, row-sparse gradient)")
+    ap.add_argument("--host-threads", type=int, default=0,
+                    help="OpenMP threads of the host optimizer (0: all cores / cores per local rank)")
+    ap.add_argument("--no-pin", action="store_true", help="leave the host optimizer threads unpinned")
     ap.add_argument("--no-hybrid", action="store_true",
                     help="skip the measured HBM-resident-optimizer variant reported beside the headline")
     ap.add_argument("--resident-blocks", type=int, default=0,

@@ -87,6 +87,8 @@ struct EngineOptions {
     // shadow (zero-copy over PCIe: T x h x 2 bytes) instead of streaming the (V, h) table.
     // Single GPU, untied, host-resident embedding.
     bool embed_gather_host = false;
+    // Pin the host optimizer's OpenMP team to cores (scheduling only).
+    bool pin_threads = true;
     bool resident_embed = false;
 };
 

@@ -271,6 +271,8 @@ typedef struct HlmEngineOptions {
   int32_t sparse_embed_grad;
   /* forward embedding rows gathered zero-copy from the pinned host shadow (no table H2D) */
   int32_t embed_gather_host;
+  /* 1: leave the host optimizer's OpenMP team unpinned (default: pinned to cores) */
+  int32_t no_pin_threads;
 } HlmEngineOptions;
 
 typedef struct HlmStepResult {

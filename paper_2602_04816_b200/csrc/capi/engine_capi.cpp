@@ -115,6 +115,7 @@ hlm::EngineOptions to_opts(const HlmEngineOptions* o) {
         e.grad_buffers = o->grad_buffers > 2 ? o->grad_buffers : 2;
         e.sparse_embed_grad = o->sparse_embed_grad != 0;
         e.embed_gather_host = o->embed_gather_host != 0;
+        e.pin_threads = o->no_pin_threads == 0;
     }
     return e;
 }
