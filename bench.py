@@ -434,7 +434,7 @@ def run_ours(args, m, name):
     # w, m, v, bf16 shadow out) + 4 B of gradient DMA written + 2 B per weight DMA pass read
     lib.hlm_host_triad_gbs.restype = ctypes.c_double
     lib.hlm_host_triad_gbs.argtypes = [ctypes.c_int64, ctypes.c_int]
-    host_bw = lib.hlm_host_triad_gbs(1 << 30, 3) if rank == 0 else None
+    host_bw = lib.hlm_host_triad_gbs(1 << 30, 5) if rank == 0 else None
     # 26 B/param of Adam state traffic (w, m, v read + written, bf16 shadow written) + the
     # gradient bytes twice (DMA write, Adam read) + the weight DMA read
     host_bytes = nums["params"] * 26 + 2 * d2h_step + h2d_step

@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <immintrin.h>
 #include <omp.h>
+#include <sched.h>
+#include <pthread.h>
 #include <fcntl.h>
 #include <sys/mman.h>
 #include <sys/statvfs.h>
@@ -748,7 +750,39 @@ void accumulate_grads(LayerTile& tile, const float* g) {
 
 }  // namespace hlm
 
+namespace hlm {
+double triad_gbs_impl(int64_t bytes_per_array, int reps);
+}
+
+// STREAM triad on a thread of its own with a team pinned like the optimizer's (one
+// thread per allowed CPU), so the roofline denominator sees the same placement.
 extern "C" double hlm_host_triad_gbs(int64_t bytes_per_array, int reps) {
+    double best = 0.0;
+    std::thread th([&] {
+        cpu_set_t allowed;
+        CPU_ZERO(&allowed);
+        std::vector<int> cpus;
+        if (sched_getaffinity(0, sizeof(allowed), &allowed) == 0)
+            for (int c = 0; c < CPU_SETSIZE; ++c)
+                if (CPU_ISSET(c, &allowed)) cpus.push_back(c);
+        if (!cpus.empty()) {
+            omp_set_num_threads(static_cast<int>(cpus.size()));
+#pragma omp parallel
+            {
+                cpu_set_t one;
+                CPU_ZERO(&one);
+                CPU_SET(cpus[static_cast<size_t>(omp_get_thread_num()) % cpus.size()], &one);
+                pthread_setaffinity_np(pthread_self(), sizeof(one), &one);
+            }
+        }
+        best = hlm::triad_gbs_impl(bytes_per_array, reps);
+    });
+    th.join();
+    return best;
+}
+
+namespace hlm {
+double triad_gbs_impl(int64_t bytes_per_array, int reps) {
     const hlm::i64 n = bytes_per_array / 4;
     float* a = static_cast<float*>(hlm::map_huge_public(static_cast<size_t>(n) * 4));
     float* b = static_cast<float*>(hlm::map_huge_public(static_cast<size_t>(n) * 4));
@@ -772,3 +806,4 @@ extern "C" double hlm_host_triad_gbs(int64_t bytes_per_array, int reps) {
     munmap(c, static_cast<size_t>(n) * 4);
     return best;
 }
+}  // namespace hlm
