@@ -569,6 +569,33 @@ __device__ __forceinline__ void store_acc_half(__nv_bfloat16* dst, uint32_t tadd
   }
 }
 
+// 32 lanes x 16 columns of 32-bit
+__device__ __forceinline__ void tmem_ld_32x16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]) : "r"(taddr));
+}
+// 16 columns (c16-th group of 16 along the 128) of row r of a K-major SW128 bf16 tile
+__device__ __forceinline__ void store_row16_kmajor(uint8_t* tile, int r, int c16, const uint32_t (&pk)[8]) {
+  uint8_t* row = tile + (c16 >> 2) * ATOM_BYTES + r * 128;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int chunk = (c16 & 3) * 2 + q;
+    *reinterpret_cast<uint4*>(row + ((chunk ^ (r & 7)) << 4)) =
+        make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+  }
+}
+// 32 accumulator columns of a row: TMEM -> scaled bf16 in global memory
+__device__ __forceinline__ void store_acc_32(__nv_bfloat16* dst, uint32_t taddr, float scale) {
+  uint32_t v[32];
+  tmem_ld_32x32(taddr, v);
+  tmem_ld_wait();
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    reinterpret_cast<uint4*>(dst)[q] =
+        make_uint4(pack_bf16x2(__uint_as_float(v[8 * q]) * scale, __uint_as_float(v[8 * q + 1]) * scale),
+                   pack_bf16x2(__uint_as_float(v[8 * q + 2]) * scale, __uint_as_float(v[8 * q + 3]) * scale),
+                   pack_bf16x2(__uint_as_float(v[8 * q + 4]) * scale, __uint_as_float(v[8 * q + 5]) * scale),
+                   pack_bf16x2(__uint_as_float(v[8 * q + 6]) * scale, __uint_as_float(v[8 * q + 7]) * scale));
+}
 // dK, dV for one 128-key tile: loop over query tiles i >= kt.
 //   TMEM: S^T [0,128) dP^T [128,256) dV [256,384) dK [384,512)
 //   smem: K, V (fixed), Q_i, dO_i, P^T, dS^T (bf16, K-major), lse2/D of tile i
@@ -579,8 +606,9 @@ struct BwdKVBars {
   uint32_t tmem;
 };
 constexpr int BWD_KV_SMEM = TILE_BYTES * 7 + 1024 + 1024 + 256;
+constexpr int BWD_KV_THREADS = 640;   // 4 control warps + 16 elementwise warps (4 column quarters)
 
-__global__ void __launch_bounds__(FWD_THREADS, 1)
+__global__ void __launch_bounds__(BWD_KV_THREADS, 1)
     flash_bwd_dkv_tc(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                      const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do,
                      const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dk,
@@ -611,7 +639,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     mbar_init(&bars->do_full, 1);
     mbar_init(&bars->do_empty, 1);
     mbar_init(&bars->s_full, 1);
-    mbar_init(&bars->p_full, 8);
+    mbar_init(&bars->p_full, 16);
     mbar_init(&bars->acc_full, 1);
     fence_barrier_init();
   }
@@ -688,40 +716,40 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     if (lane == 0) umma_commit(&bars->acc_full);
     __syncwarp();
   } else if (warp >= 4) {
-    // warp w: key rows 32*(w%4).. (its TMEM lanes), query columns [64*half, +64)
-    const int half = (warp - 4) >> 2, quarter = warp & 3;
+    // warp w: key rows 32*(w%4).. (its TMEM lanes), query columns [32*cq, +32), cq = (w-4)/4:
+    // sixteen elementwise warps, four per scheduler, two 16-column rounds each
+    const int cq = (warp - 4) >> 2, quarter = warp & 3;
     const int r = quarter * 32 + lane;             // key row within the tile
     const int key = kt * TK + r;
-    const int tid = (warp - 4) * 32 + lane;        // 0..255
+    const int tid = (warp - 4) * 32 + lane;        // 0..511
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float* L = lse + (long long)bh * S;
     const float* Dr = dsum + (long long)bh * S;
     for (int i = kt; i < nq; ++i) {
       const int it = i - kt;
       // lse (log2 units) and D of this query tile; the previous tile's readers are done
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      asm volatile("bar.sync 1, 512;" ::: "memory");
       if (tid < 128)
         sL[tid] = -L[i * TQ + tid] * kLog2e;   // negated: exp argument is one FFMA
-      else
+      else if (tid < 256)
         sD[tid - 128] = Dr[i * TQ + tid - 128];
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      asm volatile("bar.sync 1, 512;" ::: "memory");
       mbar_wait(&bars->s_full, it & 1);
       tc_fence_after();
 #pragma unroll 1
       for (int h2 = 0; h2 < 2; ++h2) {
-        const int c = half * 2 + h2;               // 32-column chunk of the 128 query columns
-        uint32_t sv[32], dpv[32];
-        tmem_ld_32x32(tmem + c * 32 + lane_off, sv);
-        tmem_ld_32x32(tmem + 128 + c * 32 + lane_off, dpv);
+        const int c16 = cq * 2 + h2;               // 16-column group of the 128 query columns
+        uint32_t sv[16], dpv[16];
+        tmem_ld_32x16(tmem + c16 * 16 + lane_off, sv);
+        tmem_ld_32x16(tmem + 128 + c16 * 16 + lane_off, dpv);
         tmem_ld_wait();
-        uint32_t pk[16], dk16[16];
-        const float4* L4 = reinterpret_cast<const float4*>(sL + c * 32);
-        const float4* D4 = reinterpret_cast<const float4*>(sD + c * 32);
-        // only the diagonal tile (i == kt, warp-uniform) has keys above its queries
+        uint32_t pk[8], dk8[8];
+        const float4* L4 = reinterpret_cast<const float4*>(sL + c16 * 16);
+        const float4* D4 = reinterpret_cast<const float4*>(sD + c16 * 16);
         auto body = [&](auto diag_tag) {
           constexpr bool kDiag = decltype(diag_tag)::value;
 #pragma unroll
-          for (int e4 = 0; e4 < 8; ++e4) {
+          for (int e4 = 0; e4 < 4; ++e4) {
             const float4 lv = L4[e4], dv4 = D4[e4];
             const float ln[4] = {lv.x, lv.y, lv.z, lv.w}, dn[4] = {dv4.x, dv4.y, dv4.z, dv4.w};
             float p[4], ds[4];
@@ -729,22 +757,22 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
             for (int u = 0; u < 4; ++u) {
               const int e = e4 * 4 + u;
               float pv = ex2(fmaf(__uint_as_float(sv[e]), scale_log2, ln[u]));
-              if (kDiag && r > c * 32 + e) pv = 0.f;
+              if (kDiag && r > c16 * 16 + e) pv = 0.f;
               p[u] = pv;
               ds[u] = pv * (__uint_as_float(dpv[e]) - dn[u]);
             }
             pk[e4 * 2] = pack_bf16x2(p[0], p[1]);
             pk[e4 * 2 + 1] = pack_bf16x2(p[2], p[3]);
-            dk16[e4 * 2] = pack_bf16x2(ds[0], ds[1]);
-            dk16[e4 * 2 + 1] = pack_bf16x2(ds[2], ds[3]);
+            dk8[e4 * 2] = pack_bf16x2(ds[0], ds[1]);
+            dk8[e4 * 2 + 1] = pack_bf16x2(ds[2], ds[3]);
           }
         };
         if (i == kt)
           body(std::true_type{});
         else
           body(std::false_type{});
-        store_row_kmajor(sPT, r, c, pk);
-        store_row_kmajor(sdST, r, c, dk16);
+        store_row16_kmajor(sPT, r, c16, pk);
+        store_row16_kmajor(sdST, r, c16, dk8);
       }
       tc_fence_before();
       fence_proxy_async();
@@ -753,8 +781,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     }
     mbar_wait(&bars->acc_full, 0);
     tc_fence_after();
-    store_acc_half(dv + (long long)(row0 + key) * ld + col0 + half * 64, tmem + 256 + half * 64 + lane_off, 1.0f);
-    store_acc_half(dk + (long long)(row0 + key) * ld + col0 + half * 64, tmem + 384 + half * 64 + lane_off, scale);
+    store_acc_32(dv + (long long)(row0 + key) * ld + col0 + cq * 32, tmem + 256 + cq * 32 + lane_off, 1.0f);
+    store_acc_32(dk + (long long)(row0 + key) * ld + col0 + cq * 32, tmem + 384 + cq * 32 + lane_off, scale);
   }
   tc_fence_before();
   __syncthreads();
@@ -988,7 +1016,7 @@ int hlm_flash_bwd_tc(const void* q, const void* k, const void* v, const void* d_
   }
   const float scale = 1.0f / sqrtf((float)HD);
   dim3 grid(S / TQ, B * H);
-  flash_bwd_dkv_tc<<<grid, FWD_THREADS, BWD_KV_SMEM, s>>>(mq, mk, mv, mdo, lse, dsum, (__nv_bfloat16*)dk,
+  flash_bwd_dkv_tc<<<grid, BWD_KV_THREADS, BWD_KV_SMEM, s>>>(mq, mk, mv, mdo, lse, dsum, (__nv_bfloat16*)dk,
                                                    (__nv_bfloat16*)dv, S, H, ld, scale, scale * kLog2e);
   flash_bwd_dq_tc<<<grid, FWD_THREADS, BWD_Q_SMEM, s>>>(mq, mk, mv, mdo, lse, dsum, (__nv_bfloat16*)dq, S, H, ld, scale,
                                                  scale * kLog2e);
