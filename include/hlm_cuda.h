@@ -312,6 +312,12 @@ int64_t hlm_store_tile_version(const HlmStore* s, int64_t p);
 /* Host Adam on every physical tile from caller gradients (store layout),
  * step index t (reference adam_update_tile, host_store.cpp:334-362). */
 int hlm_store_adam_step(HlmStore* s, const float* grads, const HlmHyper* hp, int64_t t);
+/* Host Adam on the embedding tile from a row-compact gradient: rows[c] (ascending,
+ * n_rows of them) carry compact[c * hidden ...], every other row a zero gradient that
+ * is not read (the engine's sparse_embed_grad path); bit-identical to hlm_store_adam_step
+ * on the dense gradient for that tile. */
+int hlm_store_adam_embed_rows(HlmStore* s, const int32_t* rows, int64_t n_rows, const float* compact,
+                              const HlmHyper* hp, int64_t t);
 
 int hlm_arena_create(const HlmModelConfig* cfg, int64_t budget_cap, int device, HlmArena** out);
 /* + an HBM weight cache of weight_cache_bytes (block tiles resident between the

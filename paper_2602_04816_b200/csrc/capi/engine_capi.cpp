@@ -1,5 +1,6 @@
 // extern "C" surface over the C++ host engine. Exceptions become HlmStatus
 // codes (reference errors.hpp:13-50 / hlm_main.cpp:418-430 mapping).
+#include <vector>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -278,6 +279,22 @@ int hlm_store_import_master(HlmStore* s, const float* w) {
 }
 
 int hlm_store_bitwise_equal(const HlmStore* a, const HlmStore* b) { return a->s->bitwise_equal(*b->s) ? 1 : 0; }
+
+int hlm_store_adam_embed_rows(HlmStore* s, const int32_t* rows, int64_t n_rows, const float* compact,
+                              const HlmHyper* hp, int64_t t) {
+    return guarded([&] {
+        hlm::MasterStore& st = *s->s;
+        const hlm::ModelConfig& m = st.config();
+        std::vector<int32_t> map(static_cast<size_t>(m.vocab), -1);
+        for (int64_t c = 0; c < n_rows; ++c) {
+            if (rows[c] < 0 || rows[c] >= m.vocab || (c && rows[c] <= rows[c - 1]))
+                throw std::invalid_argument("embedding rows must be ascending ids in [0, vocab)");
+            map[static_cast<size_t>(rows[c])] = static_cast<int32_t>(c);
+        }
+        hlm::adam_step_rows_sparse(st.tile(m.embed_tile_id()), m.vocab, m.hidden, map.data(), compact,
+                                   to_hyper(hp), t);
+    });
+}
 
 int hlm_store_adam_step(HlmStore* s, const float* grads, const HlmHyper* hp, int64_t t) {
     return guarded([&] {

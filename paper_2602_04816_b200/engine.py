@@ -141,6 +141,8 @@ def _L():
         L.hlm_store_import_master.argtypes = [_vp, _f32p]
         L.hlm_store_bitwise_equal.argtypes = [_vp, _vp]
         L.hlm_store_adam_step.argtypes = [_vp, _f32p, P(HyperParams), ctypes.c_int64]
+        L.hlm_store_adam_embed_rows.argtypes = [_vp, np.ctypeslib.ndpointer(np.int32), ctypes.c_int64, _f32p,
+                                                P(HyperParams), ctypes.c_int64]
         L.hlm_store_create_shared.argtypes = [P(ModelConfig), ctypes.c_uint64, ctypes.c_int,
                                               ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
                                               ctypes.c_int, ctypes.c_int, P(_vp)]
@@ -230,6 +232,12 @@ class Store:
     def adam_step(self, grads, hyper, t):
         _check(_L().hlm_store_adam_step(self.h, np.ascontiguousarray(grads, np.float32),
                                         ctypes.byref(hyper), t))
+
+    def adam_embed_rows(self, rows, compact, hyper, t):
+        rows = np.ascontiguousarray(rows, np.int32)
+        _check(_L().hlm_store_adam_embed_rows(self.h, rows, len(rows),
+                                              np.ascontiguousarray(compact, np.float32).ravel(),
+                                              ctypes.byref(hyper), t))
 
     def bitwise_equal(self, other):
         return bool(_L().hlm_store_bitwise_equal(self.h, other.h))
