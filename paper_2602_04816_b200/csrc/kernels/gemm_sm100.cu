@@ -487,9 +487,11 @@ bool use_2sm(int M, int kgroup) {
     const char* e = std::getenv("HLM_GEMM_1SM");
     force1 = (e && *e == '1') ? 1 : 0;
     const char* k = std::getenv("HLM_GEMM_KGROUP_2SM");
-    kgroup2 = (k && *k == '1') ? 1 : 0;
+    kgroup2 = (k && *k == '0') ? 0 : 1;
   }
-  // measured (r01, C2 shapes): the K-grouped dgrads run faster on 1-CTA tiles
+  // measured in isolation (late r01, C2 shapes): K-grouped dgrad qkv 1425 TFLOP/s on pair
+  // tiles vs 1348 on 1-CTA tiles, dgrad up|gate within noise (1340-1405 either way);
+  // HLM_GEMM_KGROUP_2SM=0 routes K-grouped problems to 1-CTA tiles
   return !force1 && M > 128 && (!kgroup || kgroup2);
 }
 
