@@ -364,3 +364,26 @@ def test_sparse_embedding_gradient_non_finite_names_the_table_element():
     e = E.Engine(s, E.Arena(c), E.HyperParams(), E.EngineOptions(eager_optim=True, sparse_embed_grad=True))
     with pytest.raises(E.NumericsError, match="non-finite gradient in layer"):
         e.train_step(tok)
+
+
+def test_bench_feature_set_tracks_oracle_for_20_steps():
+    """Every scheduling feature the bench turns on — gradient / weight pieces, the
+    vocab-chunked head, row-sparse embedding gradient, zero-copy embedding gather, extra
+    gradient buffers, the optimizer tail over every block, the weight cache, pinned
+    optimizer threads — over 20 training steps of the Qwen-style config (2 heads, RoPE)
+    against the oracle's mixed-precision trajectory (per-step loss within 1 %)."""
+    c = E.ModelConfig(4, 64, 128, 96, 32, 4, k_ckpt=1, n_heads=2, rope_theta=1e4)
+    s = E.Store(c, 1234)
+    blk = (2 * c.block_params() + 255) // 256 * 256
+    e = E.Engine(s, E.Arena(c, weight_cache_bytes=c.layers * blk), E.HyperParams(lr=3e-3),
+                 E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=c.layers + 4,
+                                 overlap_optimizer_tail=True, tail_blocks=c.layers, piece_elems=5000,
+                                 head_piece_vocab=16, sparse_embed_grad=True, embed_gather_host=True,
+                                 grad_buffers=6))
+    toks = [E.make_copy_task_batch(c, 1235, skip=i) for i in range(20)]   # run_training's data stream
+    losses = [e.train_step(t).loss for t in toks]
+    e.sync()
+    ref, _ = O.Oracle().train(ocfg(c), O.hyper(lr=3e-3), 1234, "mixed", 20)
+    l = np.array(losses)
+    assert np.all(np.abs(l - ref) / ref < 1e-2), (l, ref)
+    assert l[-1] < 0.9 * l[0]
