@@ -249,7 +249,10 @@ def run_hybrid(args, m, nums, E, lib, store, arena, holder, opts, batches, trace
     o2 = E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=opts.n_slab, record_trace=True,
                          grad_buffers=opts.grad_buffers,
                          overlap_optimizer_tail=True, tail_blocks=opts.tail_blocks, resident_embed=True,
-                         resident_blocks=k)
+                         resident_blocks=k,
+                         # GPU-bound here: skip the vocab-chunked head's extra head GEMM (it only
+                         # serves to start the host Adam of the head earlier)
+                         head_piece_vocab=-1)
     eng2 = E.Engine(store, arena, E.HyperParams(lr=1e-4), o2)
     try:
         for i in range(args.warmup):
