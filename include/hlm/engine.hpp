@@ -185,6 +185,8 @@ private:
     void* h2d_ = nullptr;
     void* compute_ = nullptr;
     void* d2h_ = nullptr;
+    void* opt_ = nullptr;            // device Adam of HBM-resident tiles, beside the backward
+    void* ev_res_grad_ = nullptr;    // a resident tile's gradient is complete (compute -> opt_)
     void* ev_w_ready_[2] = {};
     void* ev_buf_free_[2] = {};
     // outbound fp32 gradient buffers: the arena's two (reference footprint) plus

@@ -75,6 +75,9 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
     compute_ = s;
     ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
     d2h_ = s;
+    ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+    opt_ = s;
+    ev_res_grad_ = new_event(false);
     for (int i = 0; i < 2; ++i) {
         ev_w_ready_[i] = new_event(false);
         ev_buf_free_[i] = new_event(false);
@@ -245,6 +248,8 @@ Engine::~Engine() {
     cudaStreamSynchronize(S(compute_));
     cudaStreamSynchronize(S(h2d_));
     cudaStreamSynchronize(S(d2h_));
+    cudaStreamSynchronize(S(opt_));
+    cudaEventDestroy(E(ev_res_grad_));
     cudaEventDestroy(E(ev_step_start_));
     cudaEventDestroy(E(ev_step_end_));
     for (int i = 0; i < 2; ++i) {
@@ -269,6 +274,7 @@ Engine::~Engine() {
     cudaStreamDestroy(S(h2d_));
     cudaStreamDestroy(S(compute_));
     cudaStreamDestroy(S(d2h_));
+    cudaStreamDestroy(S(opt_));
     if (loss_host_) cudaFreeHost(loss_host_);
     if (loss_dev_) cudaFree(loss_dev_);
     if (nf_dev_) cudaFree(nf_dev_);
@@ -657,24 +663,29 @@ void Engine::consume(const Pending& p) {
 bool Engine::eligible(const Pending&) const { return true; }
 
 // Gradient of a resident tile: GPU finiteness scan, then the device Adam (no-op
-// on a flagged gradient; finish_step raises NumericsError). Stream-ordered on
-// the compute stream before any later reader of the tile's weights.
+// on a flagged gradient; finish_step raises NumericsError). HBM-bound, so it runs on
+// its own stream beside the compute-bound backward of the layers below; nothing in
+// this step reads the tile's weights again, the next step starts after finish_step
+// synchronised that stream, and the gradient buffer is released when the Adam is done.
 void Engine::resident_update(i64 tile, int gbuf, i64 dep_op) {
     const i64 ri = resident_of_[static_cast<size_t>(tile)];
     const Resident& r = residents_[static_cast<size_t>(ri)];
+    ck(cudaEventRecord(E(ev_res_grad_), S(compute_)), "record resident grad");
+    ck(cudaStreamWaitEvent(S(opt_), E(ev_res_grad_), 0), "wait resident grad");
     StreamOp op;
-    op.stream = StreamId::Compute;
+    op.stream = StreamId::Compute;   // trace schema: a GPU op of the step (on the optimizer stream)
     op.kind = OpKind::OptStep;
     op.layer = tile;
     op.params = r.n;
     op.deps.push_back(dep_op);
-    const i64 id = op_begin(op, compute_);
-    ck_hlm(hlm_cuda_nonfinite(grad_buf(gbuf), r.n, resident_bad_ + ri, compute_), "nonfinite (resident)");
+    const i64 id = op_begin(op, opt_);
+    ck_hlm(hlm_cuda_nonfinite(grad_buf(gbuf), r.n, resident_bad_ + ri, opt_), "nonfinite (resident)");
     HlmHyper hp{hyper_.lr, hyper_.beta1, hyper_.beta2, hyper_.eps, hyper_.weight_decay};
     ck_hlm(hlm_cuda_adam(r.state, r.state + r.n, r.state + 2 * r.n, r.w16, grad_buf(gbuf), r.n,
-                         resident_bad_ + ri, &hp, step_t_, compute_),
+                         resident_bad_ + ri, &hp, step_t_, opt_),
            "device adam");
-    op_end(id, compute_);
+    op_end(id, opt_);
+    ck(cudaEventRecord(E(ev_gradbuf_free_[gbuf]), S(opt_)), "record grad buf free (resident)");
     resident_dirty_ = true;
 }
 
@@ -794,6 +805,7 @@ void Engine::rethrow_worker_error() {
 void Engine::sync_resident() {
     if (!resident_dirty_) return;
     ck(cudaStreamSynchronize(S(compute_)), "sync compute");
+    ck(cudaStreamSynchronize(S(opt_)), "sync optimizer stream");
     for (const auto& r : residents_) {
         LayerTile& t = store_.tile(r.tile);
         ck(cudaMemcpy(t.master(), r.state, static_cast<size_t>(12 * r.n), cudaMemcpyDeviceToHost), "download state");
@@ -1286,11 +1298,16 @@ StepResult Engine::finish_step() {
     if (phase_ != Phase::Optimize) throw ProtocolError("finish_step out of order");
     const ModelConfig& m = store_.config();
     const i64 T = m.rows();
+    if (resident_dirty_) {   // the step's GPU span includes the device Adam of the resident tiles
+        ck(cudaEventRecord(E(ev_res_grad_), S(opt_)), "record optimizer stream done");
+        ck(cudaStreamWaitEvent(S(compute_), E(ev_res_grad_), 0), "wait optimizer stream");
+    }
     ck(cudaEventRecord(E(ev_step_end_), S(compute_)), "record step end");
     drain();
     ck(cudaStreamSynchronize(S(compute_)), "sync compute");
     ck(cudaStreamSynchronize(S(d2h_)), "sync d2h");
     ck(cudaStreamSynchronize(S(h2d_)), "sync h2d");
+    ck(cudaStreamSynchronize(S(opt_)), "sync optimizer stream");
     if (!residents_.empty()) {
         ck(cudaMemcpy(resident_bad_host_, resident_bad_, residents_.size() * 8, cudaMemcpyDeviceToHost),
            "D2H resident flags");
@@ -1440,6 +1457,7 @@ StepResult Engine::train_step(const Batch& batch) {
         cudaStreamSynchronize(S(compute_));
         cudaStreamSynchronize(S(h2d_));
         cudaStreamSynchronize(S(d2h_));
+        cudaStreamSynchronize(S(opt_));
         try {
             drain();
         } catch (...) {
