@@ -240,7 +240,11 @@ def run_hybrid(args, m, nums, E, lib, store, arena, holder, opts, batches, trace
     free, _ = torch.cuda.mem_get_info()
     per_blk, per_emb = 14 * nums["n"], 14 * m["vocab"] * m["hidden"]
     extra = max(0, opts.grad_buffers - 2) * 4 * max(nums["n"], m["vocab"] * m["hidden"])
-    k = int(max(0, min(k, (free - 4e9 - per_emb - extra) // per_blk)))
+    room = free - 6e9 - extra
+    if room < per_emb:
+        return {"error": f"not enough free HBM for the resident embedding ({per_emb / 1e9:.1f} GB needed, "
+                         f"{room / 1e9:.1f} GB free after the arena)"}
+    k = int(max(0, min(k, (room - per_emb) // per_blk)))
     eng = holder.pop()
     eng.sync()
     del eng
