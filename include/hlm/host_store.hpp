@@ -160,6 +160,11 @@ public:
 
     i64 adam_steps() const { return adam_steps_; }
     void set_adam_steps(i64 t) { adam_steps_ = t; }
+    // Engines holding HBM-resident tiles whose optimizer state is newer than this
+    // store's (between a resident Adam and Engine::sync()). save_checkpoint refuses
+    // while the count is non-zero: the file would silently hold stale tiles.
+    void add_device_newer(int d) { device_newer_.fetch_add(d); }
+    int device_newer() const { return device_newer_.load(); }
 
     bool bitwise_equal(const MasterStore& other) const;   // master, moments, shadow
 
@@ -192,6 +197,7 @@ private:
     size_t map_bytes_ = 0;
     int rank_ = 0, world_ = 1;
     bool registered_ = false;
+    std::atomic<int> device_newer_{0};
 };
 
 // Allocates and initialises a store: trunc_normal(0.02) matrices, unit norm

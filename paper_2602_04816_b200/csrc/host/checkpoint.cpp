@@ -32,6 +32,9 @@ void fill_dims(const ModelConfig& m, std::int64_t* d) {
 }  // namespace
 
 void save_checkpoint(const MasterStore& store, const std::string& path) {
+    if (store.device_newer() > 0)
+        throw ProtocolError("save_checkpoint: an engine holds HBM-resident tiles newer than the store; "
+                            "call Engine::sync() first");
     Header h{};
     std::memcpy(h.magic, kMagic, 4);
     h.version = kVersion;

@@ -686,6 +686,7 @@ void Engine::resident_update(i64 tile, int gbuf, i64 dep_op) {
            "device adam");
     op_end(id, opt_);
     ck(cudaEventRecord(E(ev_gradbuf_free_[gbuf]), S(opt_)), "record grad buf free (resident)");
+    if (!resident_dirty_) store_.add_device_newer(1);
     resident_dirty_ = true;
 }
 
@@ -812,6 +813,7 @@ void Engine::sync_resident() {
         ck(cudaMemcpy(t.shadow(), r.w16, static_cast<size_t>(2 * r.n), cudaMemcpyDeviceToHost), "download weights");
     }
     resident_dirty_ = false;
+    store_.add_device_newer(-1);
 }
 
 void Engine::sync() {

@@ -299,7 +299,7 @@ def test_measured_traces_validate(kw):
 
 @pytest.mark.parametrize("res", [dict(resident_embed=True, resident_blocks=2),
                                  dict(resident_blocks=6), dict(resident_embed=True)])
-def test_hbm_resident_optimizer_tiles_are_bitwise_neutral(res):
+def test_hbm_resident_optimizer_tiles_are_bitwise_neutral(res, tmp_path):
     """Embedding / first blocks optimised on the GPU from HBM-resident FP32 state:
     same losses and, after sync(), the same store bit for bit as the host Adam."""
     from paper_2602_04816_b200.trace import validate_trace
@@ -315,7 +315,11 @@ def test_hbm_resident_optimizer_tiles_are_bitwise_neutral(res):
                                   overlap_optimizer_tail=True, tail_blocks=1, **res))
     l1 = [e1.train_step(t) for t in toks]
     assert validate_trace(e1.last_trace(), c.layers) == []
+    ck = str(tmp_path / "stale.hlm2")
+    with pytest.raises(Exception, match="sync"):
+        s.save(ck)          # the store's resident tiles are stale until sync()
     e1.sync()
+    s.save(ck)
     assert l0 == [r.loss for r in l1]
     assert ref.bitwise_equal(s)
     streamed = 2 * (c.vocab * c.hidden * (0 if res.get("resident_embed") else 1) +
