@@ -319,6 +319,15 @@ int hlm_store_adam_step(HlmStore* s, const float* grads, const HlmHyper* hp, int
 int hlm_store_adam_embed_rows(HlmStore* s, const int32_t* rows, int64_t n_rows, const float* compact,
                               const HlmHyper* hp, int64_t t);
 
+/* CPUs a data-parallel rank's optimizer team is pinned to (the engine's own
+ * placement rule, exposed for testing): rank's share of the CPUs of its GPU's NUMA
+ * node, split among the ranks on that node. gpu_nodes[world] = node of each rank's
+ * GPU (-1 unknown); allowed[n_allowed] = the process affinity (ascending); online =
+ * host CPU count; node_of_cpu[n_cpus] = node of each CPU id. Writes up to out_cap
+ * CPU ids to out and returns how many (negative on error). */
+int hlm_rank_cpu_slice(int rank, const int* gpu_nodes, int world, const int* allowed, int n_allowed, int online,
+                       const int* node_of_cpu, int n_cpus, int* out, int out_cap);
+
 int hlm_arena_create(const HlmModelConfig* cfg, int64_t budget_cap, int device, HlmArena** out);
 /* + an HBM weight cache of weight_cache_bytes (block tiles resident between the
  * forward and the backward of a step: one H2D pass for every cached layer) */

@@ -11,6 +11,7 @@
 #include "hlm/bf16.hpp"
 #include "hlm/checkpoint.hpp"
 #include "hlm/engine.hpp"
+#include "hlm/numa_place.hpp"
 #include "hlm/trainer.hpp"
 #include "hlm_cuda.h"
 #include "../host/nccl_dyn.h"
@@ -294,6 +295,23 @@ int hlm_store_adam_embed_rows(HlmStore* s, const int32_t* rows, int64_t n_rows, 
         hlm::adam_step_rows_sparse(st.tile(m.embed_tile_id()), m.vocab, m.hidden, map.data(), compact,
                                    to_hyper(hp), t);
     });
+}
+
+int hlm_rank_cpu_slice(int rank, const int* gpu_nodes, int world, const int* allowed, int n_allowed, int online,
+                       const int* node_of_cpu, int n_cpus, int* out, int out_cap) {
+    if (world < 1 || rank < 0 || rank >= world || n_allowed < 0 || n_cpus < 0 || out_cap < 0) return -1;
+    std::vector<std::vector<int>> of_node;
+    for (int c = 0; c < n_cpus; ++c) {
+        const int n = node_of_cpu[c];
+        if (n < 0) continue;
+        if (static_cast<size_t>(n) >= of_node.size()) of_node.resize(static_cast<size_t>(n) + 1);
+        of_node[static_cast<size_t>(n)].push_back(c);
+    }
+    const std::vector<int> cpus = hlm::rank_cpu_slice(rank, std::vector<int>(gpu_nodes, gpu_nodes + world),
+                                                      std::vector<int>(allowed, allowed + n_allowed), online, of_node);
+    const int n = static_cast<int>(std::min<size_t>(cpus.size(), static_cast<size_t>(out_cap)));
+    std::copy(cpus.begin(), cpus.begin() + n, out);
+    return static_cast<int>(cpus.size());
 }
 
 int hlm_store_adam_step(HlmStore* s, const float* grads, const HlmHyper* hp, int64_t t) {

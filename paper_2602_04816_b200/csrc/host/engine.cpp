@@ -4,6 +4,9 @@
 // :379-424); the memcpy "transfers" and CPU kernels become async copies and
 // sm_100a kernels on three streams ordered by events.
 #include "hlm/engine.hpp"
+#include "hlm/numa_place.hpp"
+
+#include <unistd.h>
 
 #include <cuda_runtime.h>
 #include <omp.h>
@@ -701,35 +704,39 @@ void Engine::process_oldest_inline() {
     consume(p);
 }
 
-// Pin the optimizer's OpenMP team, thread i to the i-th allowed CPU (offset by rank x
-// team size, so ranks sharing a host take disjoint cores). Unpinned, the team's threads
+// Pin the optimizer's OpenMP team one thread per CPU. Unpinned, the team's threads
 // migrate and collide with the issue / CUDA threads: measured at C2, 8.2-8.6 k tok/s
-// unpinned vs 8.7-9.3 k pinned on the same boxes. Without an explicit thread count the
-// team leaves one CPU to the thread issuing the GPU work (15 of 16: 9.1-9.2 k, steadier
-// than 16). Scheduling only; results unchanged.
-void pin_optimizer_team(int rank, bool default_team) {
-    cpu_set_t allowed;
-    CPU_ZERO(&allowed);
-    if (sched_getaffinity(0, sizeof(allowed), &allowed) != 0) return;
-    std::vector<int> cpus;
-    for (int c = 0; c < CPU_SETSIZE; ++c)
-        if (CPU_ISSET(c, &allowed)) cpus.push_back(c);
-    if (cpus.empty()) return;
-    if (default_team && cpus.size() >= 8) omp_set_num_threads(static_cast<int>(cpus.size()) - 1);
-    const int team = omp_get_max_threads();
-    const size_t offset = static_cast<size_t>(rank) * static_cast<size_t>(team) % cpus.size();
+// unpinned vs 8.7-9.3 k pinned on the same boxes. One rank: every allowed CPU but one,
+// left to the thread issuing the GPU work (15 of 16: 9.1-9.2 k, steadier than 16). Data
+// parallel: the rank's slice of its GPU's NUMA node, shared evenly with the other ranks
+// on that node, so N ranks on one host never stack N pinned teams on the same cores.
+// Scheduling only; results unchanged.
+void pin_optimizer_team(int rank, int world, bool default_team) {
+    const std::vector<int> allowed = allowed_cpus();
+    if (allowed.empty()) return;
+    std::vector<int> cpus = allowed;
+    if (world > 1) {
+        std::vector<std::vector<int>> of_node(static_cast<size_t>(numa_node_count()));
+        for (size_t n = 0; n < of_node.size(); ++n) of_node[n] = node_cpus(static_cast<int>(n));
+        cpus = rank_cpu_slice(rank, rank_gpu_nodes(world), allowed, static_cast<int>(sysconf(_SC_NPROCESSORS_ONLN)),
+                              of_node);
+    }
+    if (default_team) {
+        const int n = static_cast<int>(cpus.size());
+        omp_set_num_threads(world == 1 && n >= 8 ? n - 1 : std::max(1, n));
+    }
 #pragma omp parallel
     {
         cpu_set_t one;
         CPU_ZERO(&one);
-        CPU_SET(cpus[(offset + static_cast<size_t>(omp_get_thread_num())) % cpus.size()], &one);
+        CPU_SET(cpus[static_cast<size_t>(omp_get_thread_num()) % cpus.size()], &one);
         pthread_setaffinity_np(pthread_self(), sizeof(one), &one);
     }
 }
 
 void Engine::worker_loop() {
     if (opts_.host_threads > 0) omp_set_num_threads(opts_.host_threads);
-    if (opts_.pin_threads) pin_optimizer_team(opts_.rank, opts_.host_threads <= 0);
+    if (opts_.pin_threads) pin_optimizer_team(opts_.rank, opts_.world, opts_.host_threads <= 0);
     for (;;) {
         Pending p;
         {

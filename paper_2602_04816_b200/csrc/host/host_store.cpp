@@ -2,6 +2,7 @@
 // See include/hlm/host_store.hpp for the design; reference counterparts in
 // proj/src/host_store.cpp are cited per function.
 #include "hlm/host_store.hpp"
+#include "hlm/numa_place.hpp"
 
 #include <cuda_runtime.h>
 #include <immintrin.h>
@@ -254,6 +255,26 @@ MasterStore::MasterStore(const ModelConfig& config, Dtype dtype, bool pin_shadow
         if (rank_ == 0) {
             hdr->magic = kShmMagic;
             std::memcpy(hdr->dims, dims, sizeof dims);
+            if (world_ > 1 && numa_node_count() > 1) {
+                // multi-socket host: each rank's shard of every tile (master, m, v, shadow)
+                // in the DRAM of its GPU's socket, where its Adam team and its DMA run
+                const std::vector<int> nodes = rank_gpu_nodes(world_);
+                i64 so = 0, sh = 0;
+                for (const auto& sp : specs) {
+                    const i64 cnt = sp.n / world_;
+                    for (int r = 0; r < world_; ++r)
+                        for (int a = 0; a < 4; ++a) {
+                            if (a < 3)
+                                prefer_node(state_base_ + so + a * sp.n + r * cnt, static_cast<size_t>(cnt) * 4,
+                                            nodes[static_cast<size_t>(r)]);
+                            else
+                                prefer_node(shadow_base_ + sh + r * cnt, static_cast<size_t>(cnt) * 2,
+                                            nodes[static_cast<size_t>(r)]);
+                        }
+                    so += 3 * round_up(sp.n, kAlignElems);
+                    sh += round_up(sp.n, kAlignElems);
+                }
+            }
             parallel_zero(state_base_, state_bytes_);
             parallel_zero(shadow_base_, shadow_bytes_);
             parallel_zero(versions, specs.size() * static_cast<size_t>(world_) * sizeof(i64));

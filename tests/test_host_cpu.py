@@ -147,3 +147,34 @@ def test_sparse_embedding_adam_is_bitwise_the_dense_adam():
     for field in (E.FIELD_MASTER, E.FIELD_M, E.FIELD_V, E.FIELD_SHADOW):
         a, b = dense.export(field)[:n_tab], sparse.export(field)[:n_tab]
         assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), field
+
+
+def _cpu_slice(rank, gpu_nodes, allowed, online, node_of_cpu):
+    lib = _lib.lib()
+    I = ctypes.c_int
+    arr = lambda xs: (I * max(1, len(xs)))(*xs)
+    out = (I * 256)()
+    n = lib.hlm_rank_cpu_slice(I(rank), arr(gpu_nodes), I(len(gpu_nodes)), arr(allowed), I(len(allowed)), I(online),
+                               arr(node_of_cpu), I(len(node_of_cpu)), out, I(256))
+    assert n >= 0
+    return list(out[:n])
+
+
+def test_rank_cpu_slices_follow_gpu_numa_nodes_and_never_overlap():
+    """N data-parallel ranks on one host split the optimizer CPUs: each rank takes
+    its share of its GPU's socket; unknown topology splits the whole set; a process
+    the launcher already bound, or a single rank, keeps its affinity."""
+    node_of = [0] * 8 + [1] * 8
+    two_socket = [_cpu_slice(r, [0, 0, 1, 1], list(range(16)), 16, node_of) for r in range(4)]
+    assert two_socket == [[0, 1, 2, 3], [4, 5, 6, 7], [8, 9, 10, 11], [12, 13, 14, 15]]
+    # 8 ranks, GPUs 0-3 on socket 0 and 4-7 on socket 1, hyperthreads numbered after cores
+    node_of = ([0] * 4 + [1] * 4) * 2
+    sl = [_cpu_slice(r, [0] * 4 + [1] * 4, list(range(16)), 16, node_of) for r in range(8)]
+    assert all(len(s) == 2 and all(node_of[c] == (r >= 4) for c in s) for r, s in enumerate(sl))
+    assert sorted(c for s in sl for c in s) == list(range(16))
+    unknown = [_cpu_slice(r, [-1, -1], list(range(16)), 16, []) for r in range(2)]
+    assert unknown == [list(range(8)), list(range(8, 16))]
+    assert _cpu_slice(1, [0, 1], [2, 3, 4], 16, [0] * 8 + [1] * 8) == [2, 3, 4]   # launcher-bound
+    assert _cpu_slice(0, [0], list(range(16)), 16, [0] * 16) == list(range(16))
+    # a node with no allowed CPU (memory-only node) falls back to the whole set
+    assert _cpu_slice(0, [2, 2], list(range(4)), 4, [0] * 4) == [0, 1]
