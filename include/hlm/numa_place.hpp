@@ -36,4 +36,17 @@ std::vector<int> rank_gpu_nodes(int world);
 // false when the kernel refused the policy.
 bool prefer_node(void* addr, std::size_t bytes, int node);
 
+// While alive, new pages faulted by this thread prefer `node` (the rank's pinned
+// gradient slabs are allocated under it). No-op for node < 0 or one node.
+class ScopedPreferNode {
+public:
+    explicit ScopedPreferNode(int node);
+    ~ScopedPreferNode();
+    ScopedPreferNode(const ScopedPreferNode&) = delete;
+    ScopedPreferNode& operator=(const ScopedPreferNode&) = delete;
+
+private:
+    bool active_ = false;
+};
+
 }  // namespace hlm

@@ -60,8 +60,9 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
         (void)nccl();
         ck(cudaMalloc(&loss_dev_, sizeof(double)), "cudaMalloc loss");
     }
-    // data parallel: slabs hold a 1/world gradient shard
+    // data parallel: slabs hold a 1/world gradient shard, in the DRAM of this GPU's socket
     {
+        const ScopedPreferNode local(opts_.world > 1 ? gpu_numa_node(arena_.device()) : -1);
         // two widest-tile slabs (embedding / head gradients), the rest block-sized
         auto round = [](i64 b) { return (b + 255) / 256 * 256; };
         const i64 widest = round(grad_buf_bytes(m) / opts_.world);

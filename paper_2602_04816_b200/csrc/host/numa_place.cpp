@@ -135,4 +135,14 @@ bool prefer_node(void* addr, std::size_t bytes, int node) {
     return syscall(SYS_mbind, lo, hi - lo, kMpolPreferred, &mask, sizeof(mask) * 8, 0) == 0;
 }
 
+ScopedPreferNode::ScopedPreferNode(int node) {
+    if (node < 0 || node >= 64 || numa_node_count() < 2) return;
+    unsigned long mask = 1UL << node;
+    active_ = syscall(SYS_set_mempolicy, kMpolPreferred, &mask, sizeof(mask) * 8) == 0;
+}
+
+ScopedPreferNode::~ScopedPreferNode() {
+    if (active_) (void)syscall(SYS_set_mempolicy, 0 /* MPOL_DEFAULT */, nullptr, 0);
+}
+
 }  // namespace hlm
