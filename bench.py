@@ -285,8 +285,9 @@ def run_hybrid(args, m, nums, E, lib, store, arena, holder, opts, batches, trace
 def run_ours(args, m, name):
     rank, world, local = dist_env()
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
-    # ranks on one host split its cores for their shard of the Adam (init keeps all cores)
-    adam_threads = max(1, (os.cpu_count() or 16) // local_world) if world > 1 else 0
+    # ranks on one host split its cores for their shard of the Adam (init keeps all cores);
+    # pinned, the engine sizes each rank's team from its NUMA-local CPU slice itself
+    adam_threads = max(1, (os.cpu_count() or 16) // local_world) if world > 1 and args.no_pin else 0
     if args.host_threads > 0:
         adam_threads = args.host_threads
     from paper_2602_04816_b200 import _lib

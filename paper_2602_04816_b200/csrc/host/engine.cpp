@@ -707,10 +707,11 @@ void Engine::process_oldest_inline() {
 
 // Pin the optimizer's OpenMP team one thread per CPU. Unpinned, the team's threads
 // migrate and collide with the issue / CUDA threads: measured at C2, 8.2-8.6 k tok/s
-// unpinned vs 8.7-9.3 k pinned on the same boxes. One rank: every allowed CPU but one,
-// left to the thread issuing the GPU work (15 of 16: 9.1-9.2 k, steadier than 16). Data
+// unpinned vs 8.7-9.3 k pinned on the same boxes. One rank: every allowed CPU; data
 // parallel: the rank's slice of its GPU's NUMA node, shared evenly with the other ranks
 // on that node, so N ranks on one host never stack N pinned teams on the same cores.
+// Without an explicit thread count the team leaves one CPU of a slice of 8 or more to
+// the thread issuing the GPU work (15 of 16: 9.1-9.2 k, steadier than 16).
 // Scheduling only; results unchanged.
 void pin_optimizer_team(int rank, int world, bool default_team) {
     const std::vector<int> allowed = allowed_cpus();
@@ -724,7 +725,7 @@ void pin_optimizer_team(int rank, int world, bool default_team) {
     }
     if (default_team) {
         const int n = static_cast<int>(cpus.size());
-        omp_set_num_threads(world == 1 && n >= 8 ? n - 1 : std::max(1, n));
+        omp_set_num_threads(n >= 8 ? n - 1 : std::max(1, n));
     }
 #pragma omp parallel
     {
