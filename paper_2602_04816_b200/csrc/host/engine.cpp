@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 
@@ -75,7 +76,13 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
     cudaStream_t s;
     ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
     h2d_ = s;
-    ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+    // The critical path gets the block scheduler first: the finiteness scans (D2H stream)
+    // and the resident tiles' device Adam (optimizer stream) fill the SMs it leaves idle
+    // instead of stealing them from the next layer's GEMMs and attention waves.
+    int prio_least = 0, prio_greatest = 0;
+    ck(cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest), "stream priority range");
+    const bool flat = std::getenv("HLM_FLAT_STREAM_PRIORITY") != nullptr;   // A/B switch
+    ck(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, flat ? prio_least : prio_greatest), "stream");
     compute_ = s;
     ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
     d2h_ = s;
