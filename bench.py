@@ -349,7 +349,8 @@ def run_ours(args, m, name):
                            record_trace=True, overlap_optimizer_tail=tail >= 0,
                            tail_blocks=max(0, tail), rank=rank, world=world,
                            comm_grad=comm_g, comm_weights=comm_w, host_threads=adam_threads,
-                           resident_embed=args.resident_embed, resident_blocks=args.resident_blocks)
+                           resident_embed=args.resident_embed, resident_blocks=args.resident_blocks,
+                           transit_blocks=args.transit_blocks)
     eng = E.Engine(store, arena, E.HyperParams(lr=1e-4), opts)
     setup_s = time.time() - t0
     # one global token stream (reference RNG, global batch = world x local), sliced by rank
@@ -594,6 +595,8 @@ def main():
     ap.add_argument("--no-pin", action="store_true", help="leave the host optimizer threads unpinned")
     ap.add_argument("--no-hybrid", action="store_true",
                     help="skip the measured HBM-resident-optimizer variant reported beside the headline")
+    ap.add_argument("--transit-blocks", type=int, default=0,
+                    help="top blocks whose host FP32 state is streamed through HBM for a device Adam")
     ap.add_argument("--resident-blocks", type=int, default=0,
                     help="blocks 1..N keep FP32 master + Adam state in HBM (device Adam, no streaming)")
     ap.add_argument("--resident-embed", action="store_true",

@@ -327,6 +327,38 @@ def test_hbm_resident_optimizer_tiles_are_bitwise_neutral(res, tmp_path):
     assert l1[-1].h2d_bytes == streamed
 
 
+@pytest.mark.parametrize("opts", [dict(transit_blocks=2), dict(transit_blocks=6),
+                                  dict(transit_blocks=3, resident_blocks=4, resident_embed=True),
+                                  dict(transit_blocks=1, tail_blocks=0, sparse_embed_grad=True, grad_buffers=4)])
+def test_transit_tiles_are_bitwise_neutral(opts):
+    """Top blocks' host FP32 state streamed through HBM for a device Adam each step:
+    same losses and, without any sync(), the same store bit for bit as the host Adam
+    (the state and weights are back on the host at the end of every step)."""
+    from paper_2602_04816_b200.trace import validate_trace
+    c = E.ModelConfig(6, 32, 64, 32, 16, 2, k_ckpt=1, n_heads=2, rope_theta=1e4)
+    toks = [E.make_copy_task_batch(c, 4, skip=i) for i in range(4)]
+    hp = E.HyperParams(lr=2e-3, weight_decay=0.01)
+    ref = E.Store(c, 8)
+    e0 = E.Engine(ref, E.Arena(c), hp, E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=4))
+    l0 = [e0.train_step(t).loss for t in toks]
+    e0.sync()
+    s = E.Store(c, 8)
+    o = dict(eager_optim=True, threaded_accum=True, n_slab=4, overlap_optimizer_tail=True, tail_blocks=1)
+    o.update(opts)
+    e1 = E.Engine(s, E.Arena(c), hp, E.EngineOptions(**o))
+    l1 = [e1.train_step(t) for t in toks]
+    assert validate_trace(e1.last_trace(), c.layers) == []
+    assert l0 == [r.loss for r in l1]
+    if not opts.get("resident_blocks"):
+        e1.wait_optimizer()   # host tiles only: no device write-back needed for the transit ones
+        assert ref.bitwise_equal(s)
+    e1.sync()
+    assert ref.bitwise_equal(s)
+    k = min(opts["transit_blocks"], c.layers - opts.get("resident_blocks", 0))
+    # the transit tiles' state comes in (12 B/param) and goes back with the weights (14 B/param)
+    assert l1[-1].d2h_bytes >= 14 * k * c.block_params()
+
+
 @pytest.mark.parametrize("pieces", [dict(piece_elems=1000), dict(piece_elems=4096, head_piece_vocab=8),
                                     dict(piece_elems=1000, grad_buffers=5), dict(sparse_embed_grad=True),
                                     dict(sparse_embed_grad=True, piece_elems=700, grad_buffers=3),
