@@ -330,15 +330,15 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
                  int S, int H, int ld, float scale_log2) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ[2] = {smem, smem + TILE_BYTES};
-  uint8_t* sK[2] = {smem + 2 * TILE_BYTES, smem + 3 * TILE_BYTES};
-  uint8_t* sV[2] = {smem + 4 * TILE_BYTES, smem + 5 * TILE_BYTES};
+  // tile t / ring slot st as arithmetic, not runtime-indexed arrays (those live on the stack)
+  auto sQ = [&](int t) { return smem + t * TILE_BYTES; };
+  auto sK = [&](int st) { return smem + (2 + st) * TILE_BYTES; };
+  auto sV = [&](int st) { return smem + (4 + st) * TILE_BYTES; };
   PPBars* bars = reinterpret_cast<PPBars*>(smem + 6 * TILE_BYTES);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int pair = (int)(gridDim.x - 1 - blockIdx.x);   // long (late) query tiles first
-  const int qtile[2] = {2 * pair, 2 * pair + 1};
-  const int ntile[2] = {2 * pair + 1, 2 * pair + 2};
+  const int ntile_b = 2 * pair + 2;                     // key tiles of query tile B (A: one fewer)
   const int bh = blockIdx.y, b = bh / H, hh = bh % H;
   const int row0 = b * S;
   const int col0 = hh * HD;
@@ -369,20 +369,20 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
     if (lane == 0) {
       mbar_arrive_expect_tx(&bars->q_full, 2 * TILE_BYTES);
       for (int t = 0; t < 2; ++t) {
-        tma_load_2d(sQ[t], &map_q, &bars->q_full, col0, row0 + qtile[t] * TQ);
-        tma_load_2d(sQ[t] + ATOM_BYTES, &map_q, &bars->q_full, col0 + 64, row0 + qtile[t] * TQ);
+        tma_load_2d(sQ(t), &map_q, &bars->q_full, col0, row0 + (2 * pair + t) * TQ);
+        tma_load_2d(sQ(t) + ATOM_BYTES, &map_q, &bars->q_full, col0 + 64, row0 + (2 * pair + t) * TQ);
       }
-      for (int j = 0; j < ntile[1]; ++j) {
+      for (int j = 0; j < ntile_b; ++j) {
         const int st = j & 1;
         const int r = row0 + j * TK;
         mbar_wait(&bars->k_empty[st], ((j >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&bars->k_full[st], TILE_BYTES);
-        tma_load_2d(sK[st], &map_k, &bars->k_full[st], col0, r);
-        tma_load_2d(sK[st] + ATOM_BYTES, &map_k, &bars->k_full[st], col0 + 64, r);
+        tma_load_2d(sK(st), &map_k, &bars->k_full[st], col0, r);
+        tma_load_2d(sK(st) + ATOM_BYTES, &map_k, &bars->k_full[st], col0 + 64, r);
         mbar_wait(&bars->v_empty[st], ((j >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&bars->v_full[st], TILE_BYTES);
-        tma_load_2d(sV[st], &map_v, &bars->v_full[st], col0, r);
-        tma_load_2d(sV[st] + ATOM_BYTES, &map_v, &bars->v_full[st], col0 + 64, r);
+        tma_load_2d(sV(st), &map_v, &bars->v_full[st], col0, r);
+        tma_load_2d(sV(st) + ATOM_BYTES, &map_v, &bars->v_full[st], col0 + 64, r);
       }
     }
   } else if (warp == 1) {
@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       mbar_wait(&bars->k_full[st], (j >> 1) & 1);
       tc_fence_after();
       if (lane == 0) {
-        const uint32_t q_base = smem_u32(sQ[t]), k_base = smem_u32(sK[st]);
+        const uint32_t q_base = smem_u32(sQ(t)), k_base = smem_u32(sK(st));
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk)
           umma_bf16(tmem + t * 128, kmajor_desc(q_base, kk), kmajor_desc(k_base, kk), idesc_s, kk ? 1u : 0u);
@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       mbar_wait(&bars->v_full[st], (j >> 1) & 1);
       tc_fence_after();
       if (lane == 0) {
-        const uint32_t v_base = smem_u32(sV[st]);
+        const uint32_t v_base = smem_u32(sV(st));
 #pragma unroll
         for (int kk = 0; kk < TK / 16; ++kk)
           umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, mnmajor_desc(v_base, kk), idesc_o,
@@ -422,10 +422,10 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
     };
     issue_s(0, 0);
     issue_s(1, 0);
-    for (int j = 0; j < ntile[1]; ++j) {
-      if (j < ntile[0]) {
+    for (int j = 0; j < ntile_b; ++j) {
+      if (j < ntile_b - 1) {
         issue_pv(0, j);
-        if (j + 1 < ntile[0]) {
+        if (j + 1 < ntile_b - 1) {
           issue_s(0, j + 1);
         } else {
           if (lane == 0) umma_commit(&bars->o_final[0]);
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         }
       }
       issue_pv(1, j);
-      if (j + 1 < ntile[1]) {
+      if (j + 1 < ntile_b) {
         issue_s(1, j + 1);
       } else {
         if (lane == 0) umma_commit(&bars->o_final[1]);
@@ -444,7 +444,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
     const int t = (warp - 2) >> 2;                 // query tile A (0) or B (1)
     const int quarter = warp & 3;                  // TMEM lanes 32*quarter ..
     const int r = quarter * 32 + lane;             // query row within the tile
-    const int qt = qtile[t], n = ntile[t];
+    const int qt = 2 * pair + t, n = qt + 1;
     const int qpos = qt * TQ + r;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const uint32_t s_addr = tmem + t * 128 + lane_off, o_addr = tmem + 256 + t * 128 + lane_off;
