@@ -55,6 +55,25 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// Blackwell packed fp32 (two lanes per instruction, each rounded like FFMA / FADD)
+// and the three-input max: fewer issue slots per score in the softmax loop.
+__device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b, float c) {
+  asm("{\n.reg .b64 ra, rb, rc, rd;\n"
+      "mov.b64 ra, {%2, %3};\nmov.b64 rb, {%4, %4};\nmov.b64 rc, {%5, %5};\n"
+      "fma.rn.f32x2 rd, ra, rb, rc;\nmov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b), "f"(c));
+}
+__device__ __forceinline__ void fadd2(float& d0, float& d1, float a0, float a1) {
+  asm("{\n.reg .b64 ra, rd;\n"
+      "mov.b64 ra, {%2, %3};\nmov.b64 rd, {%0, %1};\n"
+      "add.rn.f32x2 rd, rd, ra;\nmov.b64 {%0, %1}, rd;\n}"
+      : "+f"(d0), "+f"(d1) : "f"(a0), "f"(a1));
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -471,7 +490,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       for (int c = 0; c < 4; ++c)
 #pragma unroll
         for (int e = (c == 0 ? 16 : 0); e < 32; e += 2)
-          mx8[e & 7] = fmaxf(mx8[e & 7], fmaxf(__uint_as_float(sv[c][e]), __uint_as_float(sv[c][e + 1])));
+          mx8[e & 7] = fmax3(mx8[e & 7], __uint_as_float(sv[c][e]), __uint_as_float(sv[c][e + 1]));
       const float mx = scale_log2 * fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                                           fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       if (j == 0) {
@@ -501,9 +520,10 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          const float p0 = ex2(fmaf(__uint_as_float(sv[c][2 * e]), scale_log2, negm));
-          const float p1 = ex2(fmaf(__uint_as_float(sv[c][2 * e + 1]), scale_log2, negm));
-          l8[e & 7] += p0 + p1;
+          float a0, a1;
+          ffma2(a0, a1, __uint_as_float(sv[c][2 * e]), __uint_as_float(sv[c][2 * e + 1]), scale_log2, negm);
+          const float p0 = ex2(a0), p1 = ex2(a1);
+          fadd2(l8[2 * (e & 3)], l8[2 * (e & 3) + 1], p0, p1);
           pk[e] = pack_bf16x2(p0, p1);
         }
         tmem_st_32x16(s_addr + c * 16, pk);
@@ -982,14 +1002,15 @@ int hlm_flash_fwd_tc(const void* q, const void* k, const void* v, void* o, float
   }
   static const bool pp = std::getenv("HLM_ATTN_FWD_V1") == nullptr;
   if (pp && S % (2 * TQ) == 0) {   // two query tiles per CTA
+    auto kern = flash_fwd_pp;
     static bool attr_pp = false;
     if (!attr_pp) {
-      cudaFuncSetAttribute(flash_fwd_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, PP_SMEM);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PP_SMEM);
       attr_pp = true;
     }
     dim3 grid(S / (2 * TQ), B * H);
-    flash_fwd_pp<<<grid, PP_THREADS, PP_SMEM, s>>>(mq, mk, mv, (__nv_bfloat16*)o, lse, S, H, ld,
-                                                   (1.0f / sqrtf((float)HD)) * kLog2e);
+    kern<<<grid, PP_THREADS, PP_SMEM, s>>>(mq, mk, mv, (__nv_bfloat16*)o, lse, S, H, ld,
+                                           (1.0f / sqrtf((float)HD)) * kLog2e);
     hlm_count_launches(1);
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
   }
