@@ -69,6 +69,21 @@ __device__ __forceinline__ void fadd2(float& d0, float& d1, float a0, float a1) 
       "add.rn.f32x2 rd, rd, ra;\nmov.b64 {%0, %1}, rd;\n}"
       : "+f"(d0), "+f"(d1) : "f"(a0), "f"(a1));
 }
+// general two-lane forms (per-lane operands), each lane rounded like the scalar op
+__device__ __forceinline__ void fma2v(float& d0, float& d1, float a0, float a1, float b0, float b1, float c0, float c1) {
+  asm("{\n.reg .b64 ra, rb, rc, rd;\n"
+      "mov.b64 ra, {%2, %3};\nmov.b64 rb, {%4, %5};\nmov.b64 rc, {%6, %7};\n"
+      "fma.rn.f32x2 rd, ra, rb, rc;\nmov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+// (a - b) * p per lane: the dS = P (dP - D) of the attention backward
+__device__ __forceinline__ void submul2(float& d0, float& d1, float a0, float a1, float b0, float b1, float p0,
+                                        float p1) {
+  asm("{\n.reg .b64 ra, rb, rp, rd;\n"
+      "mov.b64 ra, {%2, %3};\nmov.b64 rb, {%4, %5};\nmov.b64 rp, {%6, %7};\n"
+      "sub.rn.f32x2 rd, ra, rb;\nmul.rn.f32x2 rd, rp, rd;\nmov.b64 {%0, %1}, rd;\n}"
+      : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(p0), "f"(p1));
+}
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float d;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
@@ -774,12 +789,18 @@ __global__ void __launch_bounds__(BWD_KV_THREADS, 1)
             const float ln[4] = {lv.x, lv.y, lv.z, lv.w}, dn[4] = {dv4.x, dv4.y, dv4.z, dv4.w};
             float p[4], ds[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < 4; u += 2) {
               const int e = e4 * 4 + u;
-              float pv = ex2(fmaf(__uint_as_float(sv[e]), scale_log2, ln[u]));
-              if (kDiag && r > c16 * 16 + e) pv = 0.f;
-              p[u] = pv;
-              ds[u] = pv * (__uint_as_float(dpv[e]) - dn[u]);
+              float x0, x1;
+              fma2v(x0, x1, __uint_as_float(sv[e]), __uint_as_float(sv[e + 1]), scale_log2, scale_log2, ln[u],
+                    ln[u + 1]);
+              float p0 = ex2(x0), p1 = ex2(x1);
+              if (kDiag && r > c16 * 16 + e) p0 = 0.f;
+              if (kDiag && r > c16 * 16 + e + 1) p1 = 0.f;
+              p[u] = p0;
+              p[u + 1] = p1;
+              submul2(ds[u], ds[u + 1], __uint_as_float(dpv[e]), __uint_as_float(dpv[e + 1]), dn[u], dn[u + 1], p0,
+                      p1);
             }
             pk[e4 * 2] = pack_bf16x2(p[0], p[1]);
             pk[e4 * 2 + 1] = pack_bf16x2(p[2], p[3]);
@@ -931,13 +952,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
           constexpr bool kDiag = decltype(diag_tag)::value;
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
-            float ds[2];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              float pv = ex2(fmaf(__uint_as_float(sv[e + u]), scale_log2, neg_l2));
-              if (kDiag && c * 32 + e + u > r) pv = 0.f;
-              ds[u] = pv * (__uint_as_float(dpv[e + u]) - D);
-            }
+            float ds[2], x0, x1;
+            fma2v(x0, x1, __uint_as_float(sv[e]), __uint_as_float(sv[e + 1]), scale_log2, scale_log2, neg_l2, neg_l2);
+            float p0 = ex2(x0), p1 = ex2(x1);
+            if (kDiag && c * 32 + e > r) p0 = 0.f;
+            if (kDiag && c * 32 + e + 1 > r) p1 = 0.f;
+            submul2(ds[0], ds[1], __uint_as_float(dpv[e]), __uint_as_float(dpv[e + 1]), D, D, p0, p1);
             pk[e / 2] = pack_bf16x2(ds[0], ds[1]);
           }
         };
