@@ -99,16 +99,39 @@ def model_numbers(m):
                 params=(2 * V * h + L * n))
 
 
-class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+def smi_gpu_id(local):
+    """nvidia-smi id (UUID, else PCI bus id) of this rank's CUDA device, or None."""
+    try:
+        import torch
+        p = torch.cuda.get_device_properties(local)
+        u = str(getattr(p, "uuid", "") or "")
+        cands = ([u if u.startswith("GPU-") else "GPU-" + u] if u else []) + \
+            ["%08X:%02X:%02X.0" % (p.pci_domain_id, p.pci_bus_id, p.pci_device_id)]
+    except Exception:
+        return None
+    for c in cands:
+        try:
+            r = subprocess.run(["nvidia-smi", "-i", c, "--query-gpu=index", "--format=csv,noheader"],
+                               capture_output=True, text=True, timeout=20)
+            if r.returncode == 0 and r.stdout.strip():
+                return c
+        except (OSError, subprocess.TimeoutExpired):
+            return None
+    return None
 
-    def __init__(self):
-        self.rows, self.proc = [], None
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons of this rank's GPU, sampled during the timed
+    region (other GPUs of the node, idle at low clocks, would skew the median)."""
+
+    def __init__(self, gpu_id=None):
+        self.rows, self.proc, self.gpu_id = [], None, gpu_id
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,"
+                ["nvidia-smi"] + (["-i", self.gpu_id] if self.gpu_id else []) +
+                ["--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,"
                  "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
                  "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
@@ -299,6 +322,7 @@ def run_ours(args, m, name):
         dist.init_process_group("gloo")
     lib = _lib.blib()
     E.set_device(local)   # before pinning, communicators and the arena
+    smi_id = smi_gpu_id(local)
     import ctypes
     lib.hlm_timer_record.argtypes = [ctypes.c_int]
     lib.hlm_timer_elapsed_ms.restype = ctypes.c_double
@@ -371,7 +395,7 @@ def run_ours(args, m, name):
     # per-launch CUDA events around every GEMM / attention launch of the timed steps
     lib.hlm_ktimer_reset()
     lib.hlm_ktimer_enable(1)
-    clocks = ClockSampler()
+    clocks = ClockSampler(smi_id)
     clocks.start()
     launches0 = lib.hlm_cuda_launch_count()
     lib.hlm_timer_record(0)
@@ -388,6 +412,14 @@ def run_ours(args, m, name):
     wall = time.perf_counter() - wall0
     launches = (lib.hlm_cuda_launch_count() - launches0) // max(1, args.steps)
     clk = clocks.stop()
+    if world > 1:   # every rank sampled its own GPU: median of the ranks' medians, union of reasons
+        per = [None] * world
+        dist.all_gather_object(per, clk)
+        meds = [c["sm_mhz"] for c in per if c.get("sm_mhz") is not None]
+        clk = {"sm_mhz": float(np.median(meds)) if meds else None,
+               "sm_max_mhz": max((c["sm_max_mhz"] for c in per if c.get("sm_max_mhz")), default=None),
+               "reasons": sorted(set(r for c in per for r in c["reasons"])),
+               "samples": sum(c["samples"] for c in per), "per_rank_sm_mhz": [c.get("sm_mhz") for c in per]}
     lib.hlm_ktimer_enable(0)
     kt = {}
     for kind, kname in ((0, "gemm"), (1, "attn_fwd"), (2, "attn_bwd")):
