@@ -359,6 +359,33 @@ def test_transit_tiles_are_bitwise_neutral(opts):
     assert l1[-1].d2h_bytes >= 14 * k * c.block_params()
 
 
+def test_transit_checkpoint_mid_run_resumes_bitwise(tmp_path):
+    """The transit tiles' state is back in the store at the end of every step: a
+    checkpoint taken without sync() (host optimizer drained only) resumes bit for bit."""
+    c = E.ModelConfig(6, 32, 64, 32, 16, 2, k_ckpt=1, n_heads=2, rope_theta=1e4)
+    toks = [E.make_copy_task_batch(c, 4, skip=i) for i in range(5)]
+    hp = E.HyperParams(lr=2e-3, weight_decay=0.01)
+    o = dict(eager_optim=True, threaded_accum=True, n_slab=4, overlap_optimizer_tail=True, tail_blocks=1,
+             transit_blocks=3)
+    ref = E.Store(c, 8)
+    e0 = E.Engine(ref, E.Arena(c), hp, E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=4))
+    l0 = [e0.train_step(t).loss for t in toks]
+    e0.sync()
+    s = E.Store(c, 8)
+    e1 = E.Engine(s, E.Arena(c), hp, E.EngineOptions(**o))
+    l1 = [e1.train_step(t).loss for t in toks[:2]]
+    e1.wait_optimizer()
+    s.save(tmp_path / "mid.hlm2")
+    del e1
+    r = E.Store(c, 1)
+    r.load(tmp_path / "mid.hlm2")
+    e2 = E.Engine(r, E.Arena(c), hp, E.EngineOptions(**o))
+    l2 = [e2.train_step(t).loss for t in toks[2:]]
+    e2.sync()
+    assert l1 + l2 == l0
+    assert r.bitwise_equal(ref)
+
+
 @pytest.mark.parametrize("pieces", [dict(piece_elems=1000), dict(piece_elems=4096, head_piece_vocab=8),
                                     dict(piece_elems=1000, grad_buffers=5), dict(sparse_embed_grad=True),
                                     dict(sparse_embed_grad=True, piece_elems=700, grad_buffers=3),
