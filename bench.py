@@ -268,6 +268,13 @@ def run_hybrid(args, m, nums, E, lib, store, arena, holder, opts, batches, trace
         return {"error": f"not enough free HBM for the resident embedding ({per_emb / 1e9:.1f} GB needed, "
                          f"{room / 1e9:.1f} GB free after the arena)"}
     k = int(max(0, min(k, (room - per_emb) // per_blk)))
+    # HBM left after the resident state keeps the top blocks' forward activations for their
+    # backward (no recompute: bit-identical, less GPU time in this GPU-bound variant)
+    from paper_2602_04816_b200 import _lib as _L
+    dims = _L.HlmBlockDims(m["batch"], m["seq"], m["hidden"], m["ffn"], m["n_heads"], 0)
+    act = (int(lib.hlm_cuda_block_acts_bytes(ctypes.byref(dims))) + 255) // 256 * 256
+    saved = 0 if args.no_saved_acts else \
+        int(max(0, min(L, (room - per_emb - k * per_blk - 2e9) // act)))
     eng = holder.pop()
     eng.sync()
     del eng
@@ -276,7 +283,7 @@ def run_hybrid(args, m, nums, E, lib, store, arena, holder, opts, batches, trace
     o2 = E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=opts.n_slab, record_trace=True,
                          grad_buffers=opts.grad_buffers,
                          overlap_optimizer_tail=True, tail_blocks=opts.tail_blocks, resident_embed=True,
-                         resident_blocks=k,
+                         resident_blocks=k, saved_act_layers=saved,
                          # GPU-bound here: skip the vocab-chunked head's extra head GEMM (it only
                          # serves to start the host Adam of the head earlier)
                          head_piece_vocab=-1)
@@ -298,11 +305,13 @@ def run_hybrid(args, m, nums, E, lib, store, arena, holder, opts, batches, trace
     return {"value": nums["T"] * args.steps / dev_s, "unit": "tokens/s", "ms_per_step": dev_s / args.steps * 1e3,
             "e2e": nums["T"] * args.steps / wall, "resident_embed": True, "resident_blocks": k,
             "resident_params": int(m["vocab"] * m["hidden"] + k * nums["n"]),
+            "saved_act_layers": saved, "saved_act_bytes": saved * act,
             "balance": {"host_adam_s": t_host, "gpu_busy_s": t_gpu, "host_adam_per_block_s": t_blk,
                         "k_balance": k_balance},
             "def": "not the headline: embedding + blocks 1..k keep FP32 master/m/v in HBM (device Adam, "
                    "bit-identical), the rest host-resident as in the headline; k = k_balance + 6 "
-                   "(k_balance: where host Adam time would equal GPU busy time), capped by free HBM"}
+                   "(k_balance: where host Adam time would equal GPU busy time), capped by free HBM; the "
+                   "HBM left keeps the top saved_act_layers blocks' forward activations (no recompute)"}
 
 
 def run_ours(args, m, name):
@@ -374,7 +383,7 @@ def run_ours(args, m, name):
                            tail_blocks=max(0, tail), rank=rank, world=world,
                            comm_grad=comm_g, comm_weights=comm_w, host_threads=adam_threads,
                            resident_embed=args.resident_embed, resident_blocks=args.resident_blocks,
-                           transit_blocks=args.transit_blocks)
+                           transit_blocks=args.transit_blocks, saved_act_layers=args.saved_act_layers)
     eng = E.Engine(store, arena, E.HyperParams(lr=1e-4), opts)
     setup_s = time.time() - t0
     # one global token stream (reference RNG, global batch = world x local), sliced by rank
@@ -627,6 +636,10 @@ def main():
     ap.add_argument("--no-pin", action="store_true", help="leave the host optimizer threads unpinned")
     ap.add_argument("--no-hybrid", action="store_true",
                     help="skip the measured HBM-resident-optimizer variant reported beside the headline")
+    ap.add_argument("--no-saved-acts", action="store_true",
+                    help="variant: recompute every block instead of keeping spare-HBM activations")
+    ap.add_argument("--saved-act-layers", type=int, default=0,
+                    help="top blocks whose forward activations stay in HBM (no recompute)")
     ap.add_argument("--transit-blocks", type=int, default=0,
                     help="top blocks whose host FP32 state is streamed through HBM for a device Adam")
     ap.add_argument("--resident-blocks", type=int, default=0,

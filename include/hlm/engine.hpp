@@ -99,6 +99,11 @@ struct EngineOptions {
     // the GPU, idle in a host-bound step, absorbs part of the optimizer while PCIe
     // has headroom. Blocks that are HBM-resident are never transit.
     i64 transit_blocks = 0;
+    // Blocks L - saved_act_layers + 1 .. L (K == 1, fused recompute) keep the activations
+    // their forward computed in HBM until their backward, which then skips the recompute
+    // (the same kernels on the same inputs and weights would reproduce them bit for bit).
+    // Trades HBM (one block's activations each) for GPU time where the GPU is the bound.
+    i64 saved_act_layers = 0;
 };
 
 struct StepResult {
@@ -288,6 +293,8 @@ private:
     bool is_resident(i64 tile) const { return resident_of_[static_cast<size_t>(tile)] >= 0; }
     void resident_update(i64 tile, int gbuf, i64 dep_op);   // device finiteness scan + Adam
     void sync_resident();
+    std::vector<void*> saved_acts_;        // per logical tile: HBM activations kept from the forward
+    void* saved_mem_ = nullptr;
     // transit tiles (EngineOptions::transit_blocks)
     static constexpr int kTransitSlots = 2;
     std::vector<i64> transit_of_;          // per logical tile: index into transits_ or -1

@@ -277,6 +277,9 @@ typedef struct HlmEngineOptions {
    * in the host store, streamed through HBM each step for a device Adam (bit-identical
    * to the host Adam) instead of their gradient going to the host optimizer */
   int64_t transit_blocks;
+  /* blocks L - saved_act_layers + 1 .. L keep their forward activations in HBM until
+   * their backward (no recompute; bit-identical: the recompute would reproduce them) */
+  int64_t saved_act_layers;
 } HlmEngineOptions;
 
 typedef struct HlmStepResult {

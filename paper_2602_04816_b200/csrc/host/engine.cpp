@@ -199,6 +199,15 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
             q += (t.n_params() * 14 + 255) / 256 * 256;
         }
     }
+    // saved activations: the top blocks' forward activations stay in HBM for their backward
+    saved_acts_.assign(static_cast<size_t>(m.tile_count()), nullptr);
+    if (opts_.saved_act_layers > 0 && m.k_ckpt == 1 && opts_.fused_recompute) {
+        const i64 n = std::min(opts_.saved_act_layers, m.layers);
+        const size_t bytes = static_cast<size_t>(align256(block_act_bytes(m)));
+        ck(cudaMalloc(&saved_mem_, static_cast<size_t>(n) * bytes), "cudaMalloc saved activations");
+        for (i64 k = 0; k < n; ++k)
+            saved_acts_[static_cast<size_t>(m.layers - k)] = static_cast<char*>(saved_mem_) + static_cast<size_t>(k) * bytes;
+    }
     // transit tiles: the top blocks, host state streamed through two HBM slots
     transit_of_.assign(static_cast<size_t>(m.tile_count()), -1);
     if (opts_.transit_blocks > 0) {
@@ -340,6 +349,7 @@ Engine::~Engine() {
     }
     for (void* p : transit_registered_) cudaHostUnregister(p);
     if (transit_mem_) cudaFree(transit_mem_);
+    if (saved_mem_) cudaFree(saved_mem_);
     if (transit_bad_) cudaFree(transit_bad_);
     if (transit_bad_host_) cudaFreeHost(transit_bad_host_);
     if (loss_host_) cudaFreeHost(loss_host_);
@@ -1103,9 +1113,8 @@ void Engine::forward_streaming() {
         bo.flops = fwd_flops(m.block_params(), T);
         if (w_op >= 0) bo.deps.push_back(w_op);
         id = op_begin(bo, compute_);
-        ck_hlm(hlm_cuda_block_fwd(&dims, wptr, h_cur_, out, arena_.discard_acts(), arena_.block_ws(), rc, rs,
-                                  compute_),
-               "block_fwd");
+        void* acts = saved_acts_[static_cast<size_t>(i)] ? saved_acts_[static_cast<size_t>(i)] : arena_.discard_acts();
+        ck_hlm(hlm_cuda_block_fwd(&dims, wptr, h_cur_, out, acts, arena_.block_ws(), rc, rs, compute_), "block_fwd");
         op_end(id, compute_);
         if (!res) compute_done_with(buf, id);
         h_cur_ = out;
@@ -1297,19 +1306,23 @@ void Engine::backward_blockwise() {
             if (!res) compute_wait_weights(buf);
             const void* wptr = res ? static_cast<const void*>(residents_[static_cast<size_t>(resident_of_[static_cast<size_t>(lo)])].w16)
                                    : weights_ptr(buf);
-            void* a = arena_.push_acts();
+            void* saved = saved_acts_[static_cast<size_t>(lo)];
+            void* a = saved ? saved : arena_.push_acts();
             StreamOp rop;
             rop.stream = StreamId::Compute;
             rop.kind = OpKind::Recompute;
             rop.layer = lo;
             rop.buf = buf;   // -2: HBM-resident weights
-            rop.flops = fwd_flops(n_block, T);
+            rop.flops = saved ? 0 : fwd_flops(n_block, T);   // saved: the forward's activations, no kernel
             if (w_op >= 0) rop.deps.push_back(w_op);
             i64 id = op_begin(rop, compute_);
-            ck_hlm(hlm_cuda_block_fwd(&dims, wptr, anchor, arena_.h_roll(0), a, arena_.block_ws(), rc, rs, compute_),
-                   "block_fwd (recompute)");
+            if (!saved) {
+                ck_hlm(hlm_cuda_block_fwd(&dims, wptr, anchor, arena_.h_roll(0), a, arena_.block_ws(), rc, rs,
+                                          compute_),
+                       "block_fwd (recompute)");
+                ++recompute_forwards_;
+            }
             op_end(id, compute_);
-            ++recompute_forwards_;
             const int gb = next_grad_buf();
             StreamOp bop;
             bop.stream = StreamId::Compute;
@@ -1332,7 +1345,7 @@ void Engine::backward_blockwise() {
                 compute_done_with(buf, lb);
                 evacuate(lo, gb, n_block, lb);
             }
-            arena_.pop_acts();
+            if (!saved) arena_.pop_acts();
             g_cur_ ^= 1;
         } else {
             // recompute lo..hi; each stack slab holds the layer's acts, inputs live

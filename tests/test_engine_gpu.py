@@ -359,6 +359,32 @@ def test_transit_tiles_are_bitwise_neutral(opts):
     assert l1[-1].d2h_bytes >= 14 * k * c.block_params()
 
 
+@pytest.mark.parametrize("opts", [dict(saved_act_layers=2), dict(saved_act_layers=6),
+                                  dict(saved_act_layers=3, resident_blocks=4, resident_embed=True),
+                                  dict(saved_act_layers=2, transit_blocks=3)])
+def test_saved_activations_are_bitwise_neutral(opts):
+    """Top blocks' forward activations kept in HBM (no recompute in their backward):
+    the same losses and store bit for bit, and that many fewer recompute forwards."""
+    from paper_2602_04816_b200.trace import validate_trace
+    c = E.ModelConfig(6, 32, 64, 32, 16, 2, k_ckpt=1, n_heads=2, rope_theta=1e4)
+    toks = [E.make_copy_task_batch(c, 4, skip=i) for i in range(3)]
+    hp = E.HyperParams(lr=2e-3, weight_decay=0.01)
+    ref = E.Store(c, 8)
+    e0 = E.Engine(ref, E.Arena(c), hp, E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=4))
+    l0 = [e0.train_step(t).loss for t in toks]
+    e0.sync()
+    s = E.Store(c, 8)
+    o = dict(eager_optim=True, threaded_accum=True, n_slab=4, overlap_optimizer_tail=True, tail_blocks=1)
+    o.update(opts)
+    e1 = E.Engine(s, E.Arena(c), hp, E.EngineOptions(**o))
+    l1 = [e1.train_step(t) for t in toks]
+    assert validate_trace(e1.last_trace(), c.layers) == []
+    e1.sync()
+    assert l0 == [r.loss for r in l1]
+    assert ref.bitwise_equal(s)
+    assert l1[-1].recompute_forwards == c.layers - opts["saved_act_layers"]
+
+
 def test_transit_checkpoint_mid_run_resumes_bitwise(tmp_path):
     """The transit tiles' state is back in the store at the end of every step: a
     checkpoint taken without sync() (host optimizer drained only) resumes bit for bit."""
