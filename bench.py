@@ -254,12 +254,13 @@ def run_hybrid(args, m, nums, E, lib, store, arena, holder, opts, batches, trace
     t_host = sum(dur(o) for o in opt)
     t_gpu = rep["compute_busy_ms"] / 1e3
     # the balance point (host Adam time = GPU busy time, from the headline trace) is a lower
-    # bound: a host paced by the GPU idles in the gaps. Measured at C2 on one box: k = 12:
-    # 14.2 k tok/s, 16-24: 15.5 k (plateau, GPU-bound), 28: 15.3 k (device Adam of every
-    # block adds GPU time); so k_balance + 6, capped by free HBM
+    # bound: a host paced by the GPU idles in the gaps. With the HBM left after the resident
+    # state holding saved activations, measured at C2 on one box (k_balance 13-15): slack 2:
+    # 15.7 k tok/s, 4: 16.1 k, 6: 16.7 k, 9: 17.2 k (twice), 12: 17.0 k, 14: 16.7 k; so
+    # k_balance + 9 (--resident-slack), capped by free HBM
     need = t_host - (emb[0] if emb else 0.0) - t_gpu
     k_balance = int(min(L, max(0, np.ceil(need / t_blk))))
-    k = min(L, k_balance + 6)
+    k = min(L, k_balance + args.resident_slack)
     free, _ = torch.cuda.mem_get_info()
     per_blk, per_emb = 14 * nums["n"], 14 * m["vocab"] * m["hidden"]
     extra = max(0, opts.grad_buffers - 2) * 4 * max(nums["n"], m["vocab"] * m["hidden"])
@@ -309,7 +310,7 @@ def run_hybrid(args, m, nums, E, lib, store, arena, holder, opts, batches, trace
             "balance": {"host_adam_s": t_host, "gpu_busy_s": t_gpu, "host_adam_per_block_s": t_blk,
                         "k_balance": k_balance},
             "def": "not the headline: embedding + blocks 1..k keep FP32 master/m/v in HBM (device Adam, "
-                   "bit-identical), the rest host-resident as in the headline; k = k_balance + 6 "
+                   "bit-identical), the rest host-resident as in the headline; k = k_balance + 9 "
                    "(k_balance: where host Adam time would equal GPU busy time), capped by free HBM; the "
                    "HBM left keeps the top saved_act_layers blocks' forward activations (no recompute)"}
 
@@ -636,6 +637,8 @@ def main():
     ap.add_argument("--no-pin", action="store_true", help="leave the host optimizer threads unpinned")
     ap.add_argument("--no-hybrid", action="store_true",
                     help="skip the measured HBM-resident-optimizer variant reported beside the headline")
+    ap.add_argument("--resident-slack", type=int, default=9,
+                    help="variant: resident blocks beyond the host/GPU balance point")
     ap.add_argument("--no-saved-acts", action="store_true",
                     help="variant: recompute every block instead of keeping spare-HBM activations")
     ap.add_argument("--saved-act-layers", type=int, default=0,
