@@ -455,6 +455,24 @@ def test_sparse_embedding_gradient_non_finite_names_the_table_element():
         e.train_step(tok)
 
 
+def test_transit_tile_non_finite_gradient_raises_and_keeps_state():
+    """A non-finite gradient in a transit tile: the device Adam is a no-op for it, the
+    (unchanged) state still returns to the store, and finish_step raises."""
+    c = E.ModelConfig(3, 16, 32, 13, 4, 1, k_ckpt=1)
+    s = E.Store(c, 5, "fp32")
+    w = s.weights()
+    lo = c.vocab * c.hidden + (c.layers - 1) * c.block_params()   # block L: the transit tile
+    w[lo + 7] = np.inf
+    s.import_master(w)
+    before = s.weights()[lo:lo + c.block_params()].copy()
+    e = E.Engine(s, E.Arena(c), E.HyperParams(),
+                 E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=4, transit_blocks=1))
+    with pytest.raises(E.NumericsError, match="non-finite gradient in layer"):
+        e.train_step(E.make_copy_task_batch(c, 2))
+    after = s.weights()[lo:lo + c.block_params()]
+    assert np.array_equal(before, after, equal_nan=True)
+
+
 def test_bench_feature_set_tracks_oracle_for_20_steps():
     """Every scheduling feature the bench turns on — gradient / weight pieces, the
     vocab-chunked head, row-sparse embedding gradient, zero-copy embedding gather, extra
