@@ -833,7 +833,7 @@ __global__ void __launch_bounds__(BWD_KV_THREADS, 1)
 // dQ for one 128-query tile: loop over key tiles j <= qt (K/V double-buffered).
 //   TMEM: S [0,128) dP [128,256) dQ [256,384)
 struct BwdQBars {
-  uint64_t q_full, kv_full[2], kv_empty[2], s_full, ds_full, acc_full;
+  uint64_t q_full, kv_full[2], kv_empty[2], s_full, ds_full, ds_free, acc_full;
   uint32_t tmem;
 };
 constexpr int BWD_Q_SMEM = TILE_BYTES * 7 + 1024 + 256;
@@ -867,6 +867,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     }
     mbar_init(&bars->s_full, 1);
     mbar_init(&bars->ds_full, 8);
+    mbar_init(&bars->ds_free, 1);
     mbar_init(&bars->acc_full, 1);
     fence_barrier_init();
   }
@@ -898,8 +899,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
     constexpr uint32_t idesc_kk = make_idesc_bf16(128, 128, false, false);
     constexpr uint32_t idesc_kmn = make_idesc_bf16(128, 128, false, true);
     const uint32_t q_base = smem_u32(sQ), do_base = smem_u32(sdO), ds_base = smem_u32(sdS);
-    mbar_wait(&bars->q_full, 0);
-    for (int j = 0; j < n_tiles; ++j) {
+    // S_j, dP_j into TMEM [0,256)
+    auto issue_sdp = [&](int j) {
       const int st = j & 1;
       mbar_wait(&bars->kv_full[st], (j >> 1) & 1);
       tc_fence_after();
@@ -914,7 +915,15 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
         umma_commit(&bars->s_full);
       }
       __syncwarp();
+    };
+    mbar_wait(&bars->q_full, 0);
+    issue_sdp(0);
+    for (int j = 0; j < n_tiles; ++j) {
+      const int st = j & 1;
       mbar_wait(&bars->ds_full, j & 1);
+      // S / dP of the next key tile first (the elementwise warps are done reading TMEM),
+      // so they compute under this tile's dQ MMA; dS_j's smem is released by ds_free
+      if (j + 1 < n_tiles) issue_sdp(j + 1);
       tc_fence_after();
       if (lane == 0) {
         const uint32_t k_base = smem_u32(sK(st));
@@ -923,6 +932,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
           umma_bf16(tmem + 256, kmajor_desc(ds_base, kk), mnmajor_desc(k_base, kk), idesc_kmn,
                     (j > 0 || kk > 0) ? 1u : 0u);
         umma_commit(&bars->kv_empty[st]);
+        umma_commit(&bars->ds_free);
       }
       __syncwarp();
     }
@@ -965,6 +975,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
           body(std::true_type{});
         else
           body(std::false_type{});
+        if (h2 == 0 && j > 0) mbar_wait(&bars->ds_free, (j - 1) & 1);   // dQ_{j-1} has read dS
         store_row_kmajor(sdS, r, c, pk);
       }
       tc_fence_before();
