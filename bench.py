@@ -192,6 +192,60 @@ def reference_sample(m, steps, warmup):
     return tok_s, t_step, sample
 
 
+def host_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+C1_REF = dict(layers=4, hidden=256, ffn=1024, vocab=1024, seq=128, batch=4, n_heads=1)
+
+
+def measured_c1_reference(steps=3, warmup=1):
+    """SURVEY §8d: the reference's full Engine::train_step (proj/src/engine.cpp:426-432),
+    bf16-store, measured wall clock at C1 in reference semantics (1 head, no RoPE) on one
+    core — the reference step is single-threaded. Measured, not extrapolated."""
+    import oracle as O
+    m = C1_REF
+    c = O.cfg(m["layers"], m["hidden"], m["ffn"], m["vocab"], m["seq"], m["batch"], 1, False, 1, 0.0)
+    s = O.Reference().time_train_step(c, True, steps, warmup)
+    T = m["batch"] * m["seq"]
+    return {"workload": "C1 " + NAMES["c1"].replace("qwen-style", "reference-mode"),
+            "shape": m, "steps": steps, "warmup": warmup, "s_per_step": s, "tokens_per_s": T / s,
+            "cores": 1, "kind": "reference", **host_info(),
+            "def": "oracle/_ref (the reference library, its sources compiled with its Release flags): "
+                   "hlm::Engine::train_step in bf16-store mode, wall clock per step"}
+
+
+def measured_c1_ours(E, steps=3, warmup=2):
+    """Our step on the same C1 workload through the public API (host tokens in, loss out,
+    host Adam included), wall clock per step — beside the measured reference step."""
+    m = C1_REF
+    c = E.ModelConfig(m["layers"], m["hidden"], m["ffn"], m["vocab"], m["seq"], m["batch"], k_ckpt=1)
+    store = E.Store(c, 1234, "bf16")
+    eng = E.Engine(store, E.Arena(c), E.HyperParams(lr=3e-3),
+                   E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=4))
+    toks = [E.make_copy_task_batch(c, 1235, skip=i) for i in range(warmup + steps)]
+    for i in range(warmup):
+        eng.train_step(toks[i])
+    t0 = time.perf_counter()
+    for i in range(steps):
+        eng.train_step(toks[warmup + i])
+    eng.wait_optimizer()
+    s = (time.perf_counter() - t0) / steps
+    del eng
+    T = m["batch"] * m["seq"]
+    return {"s_per_step": s, "tokens_per_s": T / s,
+            "def": "Engine.train_step (C ABI) wall clock incl. token H2D, loss D2H and the host Adam"}
+
+
 def _reference_worker(a):
     m, steps, warmup = a
     sys.path.insert(0, ROOT)
@@ -221,6 +275,10 @@ def run_reference(args, m, name):
     t_step = float(np.mean([r[1] for r in res]))
     sample = res[0][2].replace("1 thread", f"{cores} single-threaded replicas, one per core")
     nums = model_numbers(m)
+    try:
+        mc1 = measured_c1_reference()
+    except Exception as ex:
+        mc1 = {"error": f"{type(ex).__name__}: {ex}"}
     line = {"metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": steps, "warmup": warmup, "ms_per_step": nums["T"] / tok_s * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
@@ -229,7 +287,8 @@ def run_reference(args, m, name):
                        "parallelism": f"cpu-{cores}-replicas"},
             "tflops": nums["model_flops"] / nums["T"] * tok_s / 1e12,
             "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": cores, "kind": "reference",
-                             "sample": sample, "per_replica_step_s_for_4_tokens": t_step},
+                             "sample": sample, "per_replica_step_s_for_4_tokens": t_step,
+                             "estimate": True, **host_info(), "measured_c1": mc1},
             "e2e": {"value": tok_s, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -516,6 +575,17 @@ def run_ours(args, m, name):
         except Exception as ex:
             hybrid = {"error": f"{type(ex).__name__}: {ex}"}
 
+    if cpu_baseline is not None:
+        cpu_baseline.update(estimate=True, **host_info())
+        try:   # the reference's full train_step measured at C1 beside ours
+            ref_c1 = measured_c1_reference()
+            ours_c1 = measured_c1_ours(E)
+            ref_c1["ours"] = ours_c1
+            ref_c1["speedup_e2e"] = ref_c1["s_per_step"] / ours_c1["s_per_step"]
+            cpu_baseline["measured_c1"] = ref_c1
+        except Exception as ex:
+            cpu_baseline["measured_c1"] = {"error": f"{type(ex).__name__}: {ex}"}
+
     if hybrid and "ms_per_step" in hybrid:
         hs = hybrid["ms_per_step"] / 1e3
         hybrid["step_roofline_frac"] = t_roof / hs
@@ -602,13 +672,76 @@ def run_ours(args, m, name):
         "clocks": clk, "cpu_baseline": cpu_baseline, "hbm_resident_variant": hybrid,
         "loss": [float(x) for x in losses], "setup_s": setup_s,
     }
-    print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
     del eng
     for c in (comm_g, comm_w):
         if c is not None:
             lib.hlm_nccl_comm_destroy(c)
+    return line
+
+
+WIDE_POINTS = {"c4": (2, 4, 6), "c5": (1, 2)}
+
+
+def run_wide(args):
+    """N1: the 72B-width (C4) and 120B-width (C5) decoders do not fit a 196 GB
+    host at full depth (1.15 / 1.69 TB of FP32 master + Adam), so each is measured at full
+    width over a depth sweep — same step, same options as the headline, each point in its
+    own process after the headline's store is gone — and the full-depth step is projected
+    from a per-layer fit t(L) = a + b L. Projections are labelled as such."""
+    out = {}
+    for cfg, depths in WIDE_POINTS.items():
+        if args.wide_only and cfg not in args.wide_only.split(","):
+            continue
+        pts = []
+        for L in depths:
+            cmd = [sys.executable, os.path.abspath(__file__), "--config", cfg, "--layers", str(L),
+                   "--steps", str(args.wide_steps), "--warmup", "2", "--no-hybrid",
+                   "--no-cpu-baseline", "--no-wide"]
+            t0 = time.time()
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+            lines = [x for x in r.stdout.splitlines() if x.startswith("{")]
+            if r.returncode != 0 or not lines:
+                pts.append({"layers": L, "error": (r.stderr or r.stdout)[-400:]})
+                continue
+            d = json.loads(lines[-1])
+            pts.append({"layers": L, "params": d["config"]["params"], "value": d["value"],
+                        "ms_per_step": d["ms_per_step"], "tflops": d["tflops"],
+                        "e2e": d["e2e"]["value"], "h2d_overlap": d["stream"]["h2d_overlap"],
+                        "overlap": d["stream"]["overlap"], "host_adam_s": d["stream"]["host_adam_s"],
+                        "compute_busy_s": d["stream"]["compute_busy_s"],
+                        "gemm_tflops_in_step": d["roofline"]["achieved"],
+                        "gemm_frac": d["roofline"]["frac"],
+                        "attn_fwd_tflops": d["attention_roofline"]["attn_fwd"]["tflops"],
+                        "attn_bwd_tflops": d["attention_roofline"]["attn_bwd"]["tflops"],
+                        "step_roofline_frac": d["step_roofline"]["frac"],
+                        "host_roofline_frac": d["host_roofline"]["frac"],
+                        "clocks": d["clocks"], "wall_s": time.time() - t0})
+        ok = [p for p in pts if "ms_per_step" in p]
+        entry = {"points": pts, "width": {k: CONFIGS[cfg][k] for k in
+                                          ("hidden", "ffn", "vocab", "seq", "batch", "n_heads")}}
+        if len(ok) >= 2:
+            Ls = np.array([p["layers"] for p in ok], float)
+            ts = np.array([p["ms_per_step"] / 1e3 for p in ok])
+            b, a = np.polyfit(Ls, ts, 1)
+            full = dict(CONFIGS[cfg])
+            nums = model_numbers(full)
+            t_full = a + b * full["layers"]
+            _, _, tf_sus, _ = peaks()
+            t_roof = max(nums["hw_flops"] / (tf_sus * 1e12), nums["h2d"] / (PCIE_ASSUMED_GBS * 1e9),
+                         nums["d2h"] / (PCIE_ASSUMED_GBS * 1e9))
+            entry["projection"] = {
+                "label": "PROJECTION from the measured depth sweep (not a measured step)",
+                "fit": {"a_s": a, "b_s_per_layer": b,
+                        "max_residual_s": float(np.max(np.abs(a + b * Ls - ts)))},
+                "layers": full["layers"], "params": nums["params"], "t_step_s": t_full,
+                "tokens_per_s": nums["T"] / t_full, "tflops": nums["model_flops"] / t_full / 1e12,
+                "north_star_roofline": {"t_roof_s": t_roof, "frac": t_roof / t_full,
+                                        "def": "max(HW_FLOPS/sustained bf16, H2D/55GB/s, D2H/55GB/s)"},
+                "host_store_bytes": nums["params"] * 14}
+        out[cfg] = entry
+    return out
 
 
 def main():
@@ -655,6 +788,10 @@ def main():
     ap.add_argument("--layers", type=int, default=0,
                     help="partial depth of the config's full-width decoder (C3-C5 do not fit a 196 GB "
                          "host at full depth); the workload name says so")
+    ap.add_argument("--no-wide", action="store_true",
+                    help="skip the C4 / C5 full-width depth sweeps reported beside a C2 headline")
+    ap.add_argument("--wide-only", default="", help="comma list of wide configs to sweep (c4,c5)")
+    ap.add_argument("--wide-steps", type=int, default=3, help="timed steps per wide point")
     args = ap.parse_args()
     m = dict(CONFIGS[args.config])
     name = NAMES[args.config]
@@ -663,8 +800,19 @@ def main():
         m["layers"] = args.layers
     if args.impl == "reference":
         run_reference(args, m, name)
-    else:
-        run_ours(args, m, name)
+        return
+    line = run_ours(args, m, name)
+    if line is None:
+        return
+    if (not args.no_wide and args.config == "c2" and args.layers == 0 and line["n_gpus"] == 1
+            and not args.force_dp):
+        import gc
+        gc.collect()
+        try:
+            line["wide"] = run_wide(args)
+        except Exception as ex:
+            line["wide"] = {"error": f"{type(ex).__name__}: {ex}"}
+    print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

@@ -11,9 +11,11 @@
 #include "hlm/host_store.hpp"
 
 namespace hlm {
+inline namespace b200 {
 
 void save_checkpoint(const MasterStore& store, const std::string& path);
 // Loads into a store of identical geometry; throws ConfigError otherwise.
 void load_checkpoint(MasterStore& store, const std::string& path);
 
+}  // inline namespace b200
 }  // namespace hlm

@@ -18,6 +18,7 @@
 #include "hlm/model_config.hpp"
 
 namespace hlm {
+inline namespace b200 {
 
 enum class Region : int { Stream0 = 0, Stream1 = 1, Stack = 2, Anchors = 3, Workspace = 4, WeightCache = 5 };
 inline constexpr int kRegionCount = 6;
@@ -154,4 +155,5 @@ private:
     i64 h2d_bytes_ = 0;
 };
 
+}  // inline namespace b200
 }  // namespace hlm

@@ -27,6 +27,7 @@
 #include "hlm/trace.hpp"
 
 namespace hlm {
+inline namespace b200 {
 
 struct Batch {
     std::vector<std::int32_t> tokens;    // batch * seq
@@ -345,4 +346,5 @@ private:
 // (reference proj/src/engine.cpp:434-441).
 Batch make_copy_task_batch(const ModelConfig& m, Rng& rng);
 
+}  // inline namespace b200
 }  // namespace hlm

@@ -7,6 +7,7 @@
 #include "hlm/model_config.hpp"
 
 namespace hlm {
+inline namespace b200 {
 
 inline i64 fwd_flops(i64 n_params, i64 tokens) { return 2 * n_params * tokens; }
 inline i64 bwd_flops(i64 n_params, i64 tokens) { return 2 * fwd_flops(n_params, tokens); }
@@ -33,4 +34,5 @@ inline double hw_flops(const ModelConfig& m) {
                                 (2.0 * static_cast<double>(m.block_matmul_params()) * T + attn_fwd_flops(m));
 }
 
+}  // inline namespace b200
 }  // namespace hlm

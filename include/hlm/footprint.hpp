@@ -16,6 +16,7 @@
 #include "hlm_cuda.h"
 
 namespace hlm {
+inline namespace b200 {
 
 inline HlmBlockDims block_dims(const ModelConfig& m, int flags = 0) {
     HlmBlockDims d{};
@@ -104,4 +105,5 @@ inline ArenaFootprint arena_footprint(const ModelConfig& m, i64 weight_cache_byt
 // Persistent host bytes per parameter: fp32 master + m + v, bf16 shadow.
 inline i64 persistent_bytes_per_param() { return 14; }
 
+}  // inline namespace b200
 }  // namespace hlm

@@ -28,6 +28,7 @@
 #include "hlm/tensor.hpp"
 
 namespace hlm {
+inline namespace b200 {
 
 struct NamedRegion {
     std::string name;
@@ -302,4 +303,5 @@ struct HostBytesReport {
     i64 total = 0;
 };
 
+}  // inline namespace b200
 }  // namespace hlm

@@ -13,6 +13,7 @@
 #include <vector>
 
 namespace hlm {
+inline namespace b200 {
 
 int numa_node_count();                        // nodes under /sys/devices/system/node (>= 1)
 int gpu_numa_node(int device);                // -1 when unknown
@@ -49,4 +50,5 @@ private:
     bool active_ = false;
 };
 
+}  // inline namespace b200
 }  // namespace hlm

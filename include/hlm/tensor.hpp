@@ -6,6 +6,7 @@
 #include <random>
 
 namespace hlm {
+inline namespace b200 {
 
 // BF16 / FP32: the reference store dtypes (how build_store rounds the initial
 // weights). The B200 store always keeps an FP32 master + FP32 Adam moments
@@ -54,4 +55,5 @@ private:
     float spare_ = 0.0f;
 };
 
+}  // inline namespace b200
 }  // namespace hlm

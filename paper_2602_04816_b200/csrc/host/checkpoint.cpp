@@ -7,6 +7,7 @@
 #include <vector>
 
 namespace hlm {
+inline namespace b200 {
 
 namespace {
 
@@ -102,4 +103,5 @@ void load_checkpoint(MasterStore& store, const std::string& path) {
     store.set_adam_steps(static_cast<i64>(h.adam_steps));
 }
 
+}  // inline namespace b200
 }  // namespace hlm

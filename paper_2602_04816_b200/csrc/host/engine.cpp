@@ -24,6 +24,7 @@
 #include "nccl_dyn.h"
 
 namespace hlm {
+inline namespace b200 {
 
 namespace {
 
@@ -1683,4 +1684,5 @@ Batch make_copy_task_batch(const ModelConfig& m, Rng& rng) {
     return b;
 }
 
+}  // inline namespace b200
 }  // namespace hlm

@@ -23,6 +23,7 @@
 #include "hlm/bf16.hpp"
 
 namespace hlm {
+inline namespace b200 {
 
 namespace {
 
@@ -769,11 +770,14 @@ void accumulate_grads(LayerTile& tile, const float* g) {
     }
 }
 
+}  // inline namespace b200
 }  // namespace hlm
 
 namespace hlm {
+inline namespace b200 {
 double triad_gbs_impl(int64_t bytes_per_array, int reps);
-}
+}  // inline namespace b200
+}  // namespace hlm
 
 // STREAM triad on a thread of its own with a team pinned like the optimizer's (one
 // thread per allowed CPU), so the roofline denominator sees the same placement.
@@ -803,6 +807,7 @@ extern "C" double hlm_host_triad_gbs(int64_t bytes_per_array, int reps) {
 }
 
 namespace hlm {
+inline namespace b200 {
 double triad_gbs_impl(int64_t bytes_per_array, int reps) {
     const hlm::i64 n = bytes_per_array / 4;
     float* a = static_cast<float*>(hlm::map_huge_public(static_cast<size_t>(n) * 4));
@@ -827,4 +832,5 @@ double triad_gbs_impl(int64_t bytes_per_array, int reps) {
     munmap(c, static_cast<size_t>(n) * 4);
     return best;
 }
+}  // inline namespace b200
 }  // namespace hlm

@@ -8,6 +8,7 @@
 #include "hlm/errors.hpp"
 
 namespace hlm {
+inline namespace b200 {
 
 const NcclApi& nccl() {
     static NcclApi api{};
@@ -40,4 +41,5 @@ void nccl_check(ncclResult_t r, const char* what) {
     if (r != ncclSuccess) throw CudaError(std::string(what) + ": " + nccl().GetErrorString(r));
 }
 
+}  // inline namespace b200
 }  // namespace hlm

@@ -6,6 +6,7 @@
 #include <nccl.h>
 
 namespace hlm {
+inline namespace b200 {
 
 struct NcclApi {
     ncclResult_t (*GetUniqueId)(ncclUniqueId*);
@@ -21,4 +22,5 @@ struct NcclApi {
 const NcclApi& nccl();
 void nccl_check(ncclResult_t r, const char* what);
 
+}  // inline namespace b200
 }  // namespace hlm

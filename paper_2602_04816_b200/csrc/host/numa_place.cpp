@@ -15,6 +15,7 @@
 #include <string>
 
 namespace hlm {
+inline namespace b200 {
 namespace {
 
 constexpr int kMpolPreferred = 1;   // linux/mempolicy.h
@@ -145,4 +146,5 @@ ScopedPreferNode::~ScopedPreferNode() {
     if (active_) (void)syscall(SYS_set_mempolicy, 0 /* MPOL_DEFAULT */, nullptr, 0);
 }
 
+}  // inline namespace b200
 }  // namespace hlm

@@ -6,6 +6,7 @@
 #include <sstream>
 
 namespace hlm {
+inline namespace b200 {
 
 const char* stream_name(StreamId s) {
     switch (s) {
@@ -48,4 +49,5 @@ std::string trace_to_jsonl(const EventTrace& t) {
     return o.str();
 }
 
+}  // inline namespace b200
 }  // namespace hlm

@@ -1,0 +1,144 @@
+// A reference-style C++ caller linked against libhlm_b200.so through the C++ API in
+// include/hlm/*.hpp — the shape of the reference's own call sites
+// (proj/tools/hlm_main.cpp:191-236 cmd_train, proj/src/trainer.cpp:8-42,
+// proj/tests/test_engine.cpp phase-API tests). INTEGRATION.md §1 quotes it.
+//
+//   integration_caller train  L h f V S B K heads steps   -> one "loss <hex> <value>" line per step
+//   integration_caller phases L h f V S B K heads          -> loss of one step via the phase API
+//   integration_caller errors                              -> exercises the exception mapping
+#include <cinttypes>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "hlm/engine.hpp"
+#include "hlm/trainer.hpp"
+
+namespace {
+
+hlm::ModelConfig config_from(char** a) {
+    hlm::ModelConfig m;
+    m.layers = std::atoll(a[0]);
+    m.hidden = std::atoll(a[1]);
+    m.ffn = std::atoll(a[2]);
+    m.vocab = std::atoll(a[3]);
+    m.seq = std::atoll(a[4]);
+    m.batch = std::atoll(a[5]);
+    m.k_ckpt = std::atoll(a[6]);
+    m.n_heads = std::atoi(a[7]);
+    m.rope_theta = m.n_heads > 1 ? 1e6 : 0.0;
+    return m;
+}
+
+void print_loss(double loss) {
+    std::uint64_t bits;
+    std::memcpy(&bits, &loss, sizeof bits);
+    std::printf("loss %016" PRIx64 " %.9g\n", bits, loss);
+}
+
+int train(char** a) {
+    hlm::RunConfig cfg;
+    cfg.model = config_from(a);
+    cfg.model.validate();
+    cfg.run.steps = std::atoll(a[8]);
+    cfg.run.seed = 1234;
+    cfg.run.eager_optim = true;
+    cfg.run.threaded_accum = true;
+    cfg.run.n_slab = 3;
+    cfg.hyper.lr = 3e-3;
+    auto store = hlm::build_store(cfg.model, cfg.run.seed, hlm::Dtype::BF16, hlm::InitMode::Reference);
+    hlm::DeviceArena arena(cfg.model);
+    const hlm::TrainOutput out =
+        hlm::run_training(cfg, *store, arena, [](const hlm::StepTelemetry& t) { print_loss(t.loss); });
+    std::printf("h2d %" PRId64 " d2h %" PRId64 " steps %" PRId64 "\n", out.steps.back().h2d_bytes,
+                out.steps.back().d2h_bytes, store->adam_steps());
+    return 0;
+}
+
+int phases(char** a) {
+    const hlm::ModelConfig m = config_from(a);
+    auto store = hlm::build_store(m, 1234, hlm::Dtype::BF16, hlm::InitMode::Reference);
+    hlm::DeviceArena arena(m);
+    hlm::EngineOptions opts;
+    opts.skip_optimizer = true;
+    hlm::Engine engine(*store, arena, hlm::HyperParams{}, opts);
+    hlm::Rng data(1235);
+    engine.begin_step(hlm::make_copy_task_batch(m, data));
+    engine.forward_streaming();
+    const double loss = engine.anchor_loss();
+    engine.backward_blockwise();
+    const hlm::StepResult r = engine.finish_step();
+    print_loss(loss);
+    print_loss(r.loss);
+    std::printf("recompute_forwards %" PRId64 "\n", r.recompute_forwards);
+    return 0;
+}
+
+// The reference's error contract (errors.hpp:13-50, hlm_main.cpp:418-430) across the
+// shared-library boundary: the exception types thrown inside libhlm_b200.so are
+// caught by their C++ type here.
+int errors() {
+    hlm::ModelConfig m;
+    m.layers = 2; m.hidden = 64; m.ffn = 128; m.vocab = 64; m.seq = 32; m.batch = 2; m.k_ckpt = 1;
+    int seen = 0;
+    try {
+        hlm::ModelConfig bad = m;
+        bad.hidden = 0;
+        bad.validate();
+    } catch (const std::invalid_argument& e) {   // model_config.hpp:28-40
+        std::printf("invalid_argument: %s\n", e.what());
+        ++seen;
+    }
+    try {
+        hlm::DeviceArena tiny(m, std::optional<hlm::i64>(4096));
+    } catch (const hlm::ArenaOomError& e) {
+        std::printf("ArenaOomError region=%s requested=%" PRId64 " capacity=%" PRId64 "\n",
+                    e.region().c_str(), e.requested(), e.capacity());
+        ++seen;
+    }
+    auto store = hlm::build_store(m, 7, hlm::Dtype::BF16);
+    hlm::DeviceArena arena(m);
+    hlm::Engine engine(*store, arena, hlm::HyperParams{});
+    try {
+        engine.forward_streaming();   // before begin_step
+    } catch (const hlm::ProtocolError& e) {
+        std::printf("ProtocolError: %s\n", e.what());
+        ++seen;
+    }
+    try {
+        hlm::Batch b;
+        b.tokens.assign(static_cast<size_t>(m.batch * m.seq), 0);
+        b.targets = b.tokens;
+        b.tokens[5] = static_cast<std::int32_t>(m.vocab);   // out of range
+        engine.train_step(b);
+    } catch (const std::out_of_range& e) {
+        std::printf("out_of_range: %s\n", e.what());
+        ++seen;
+    }
+    std::printf("errors caught %d\n", seen);
+    return seen == 4 ? 0 : 1;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    try {
+        const std::string mode = argc > 1 ? argv[1] : "";
+        if (mode == "train" && argc == 11) return train(argv + 2);
+        if (mode == "phases" && argc == 10) return phases(argv + 2);
+        if (mode == "errors") return errors();
+        std::fprintf(stderr, "usage: %s train L h f V S B K heads steps | phases L h f V S B K heads | errors\n",
+                     argv[0]);
+        return 64;
+    } catch (const std::invalid_argument& e) {
+        std::fprintf(stderr, "config error: %s\n", e.what());
+        return 2;
+    } catch (const hlm::ArenaOomError& e) {
+        std::fprintf(stderr, "arena OOM: %s\n", e.what());
+        return 3;
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "error: %s\n", e.what());
+        return 4;
+    }
+}

@@ -33,6 +33,9 @@ def test_bench_line_contract_c1():
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
     assert d["stream"]["trace_violations"] == 0
+    mc1 = d["cpu_baseline"]["measured_c1"]   # the reference's full train_step, measured
+    assert "error" not in mc1, mc1
+    assert mc1["s_per_step"] > 0 and mc1["ours"]["s_per_step"] > 0 and mc1["nproc"] >= 1
     hv = d["hbm_resident_variant"]
     assert hv is not None and "error" not in hv and hv["value"] > 0
 
@@ -41,3 +44,4 @@ def test_reference_arm_line_c1():
     d = _line(["--config", "c1", "--impl", "reference", "--steps", "1", "--warmup", "0"])
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["cpu_baseline"]["cores"] >= 1 and d["e2e"]["h2d_bytes_per_step"] == 0
+    assert d["cpu_baseline"]["measured_c1"]["s_per_step"] > 0

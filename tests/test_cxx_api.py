@@ -1,0 +1,140 @@
+"""The C++ boundary: a reference-style C++ caller (tests/cxx/integration_caller.cpp, the
+INTEGRATION.md §1 snippet) compiles against include/hlm/*.hpp and links against
+libhlm_b200.so — the drop-in the reference's own callers need
+(proj/tools/hlm_main.cpp:191-236, proj/src/trainer.cpp:8-42,
+proj/python/bindings.cpp:79-96) — and on the GPU trains bit-identically to the C-ABI path.
+
+CPU: compile + link, the exported C++ symbol set, and a link next to the reference's
+own object files (the inline namespace hlm::b200 keeps the two libraries apart).
+GPU: the caller's losses equal the ctypes (C ABI) path's bit for bit, the phase API
+matches train_step, and the reference's exception types cross the library boundary.
+"""
+import glob
+import os
+import shutil
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIBDIR = os.path.join(ROOT, "paper_2602_04816_b200")
+SRC = os.path.join(ROOT, "tests", "cxx", "integration_caller.cpp")
+REF_OBJ = os.path.join(ROOT, "oracle", "_ref", "obj")
+
+# The reference C++ API a caller binds (proj/include/hlm/*.hpp), by demangled prefix.
+REQUIRED = [
+    "hlm::b200::Engine::Engine(",
+    "hlm::b200::Engine::train_step(",
+    "hlm::b200::Engine::begin_step(",
+    "hlm::b200::Engine::forward_streaming(",
+    "hlm::b200::Engine::anchor_loss(",
+    "hlm::b200::Engine::backward_blockwise(",
+    "hlm::b200::Engine::finish_step(",
+    "hlm::b200::Engine::~Engine(",
+    "hlm::b200::build_store(",
+    "hlm::b200::adam_step(",
+    "hlm::b200::adam_step_tile(",
+    "hlm::b200::DeviceArena::DeviceArena(",
+    "hlm::b200::make_copy_task_batch(",
+    "hlm::b200::run_training(",
+    "hlm::b200::save_checkpoint(",
+    "hlm::b200::load_checkpoint(",
+    "typeinfo for hlm::b200::ArenaOomError",
+    "typeinfo for hlm::b200::ProtocolError",
+]
+
+
+def _compile(out, extra=()):
+    cmd = ["g++", "-std=c++17", "-O2", f"-I{ROOT}/include", SRC, *extra, f"-L{LIBDIR}",
+           "-lhlm_b200", f"-Wl,-rpath,{LIBDIR}", "-o", out]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-4000:]
+    return out
+
+
+@pytest.fixture(scope="module")
+def caller(tmp_path_factory):
+    if shutil.which("g++") is None:
+        pytest.skip("g++ not available")
+    return _compile(str(tmp_path_factory.mktemp("cxx") / "integration_caller"))
+
+
+def test_caller_compiles_and_links(caller):
+    r = subprocess.run([caller], capture_output=True, text=True)
+    assert r.returncode == 64 and "usage" in r.stderr
+
+
+def test_library_exports_the_reference_cxx_api():
+    so = os.path.join(LIBDIR, "libhlm_b200.so")
+    out = subprocess.run(["nm", "-DC", "--defined-only", so], capture_output=True, text=True,
+                         check=True).stdout
+    missing = [s for s in REQUIRED if s not in out]
+    assert not missing, missing
+    # nothing of the CUDA runtime or the kernels leaks out of the library
+    names = [ln.split(" ", 2)[-1] for ln in out.splitlines() if ln.strip()]
+    stray = [n for n in names if not (n.startswith("hlm_") or "hlm::b200::" in n)]
+    assert not stray, stray[:10]
+
+
+@pytest.mark.skipif(not glob.glob(os.path.join(REF_OBJ, "*.o")),
+                    reason="reference objects not built (oracle/_ref is built only where "
+                           "/root/reference exists)")
+def test_links_beside_the_reference_core(tmp_path):
+    """The reference's libhlm_core objects (namespace hlm) and libhlm_b200.so
+    (hlm::b200) link into one executable without a duplicate or mis-bound symbol."""
+    objs = sorted(glob.glob(os.path.join(REF_OBJ, "*.o")))
+    _compile(str(tmp_path / "both"), extra=(*objs, "-lpthread"))
+
+
+def _c1():
+    return ["4", "256", "1024", "1024", "128", "4", "1", "2"]
+
+
+@pytest.mark.gpu
+def test_cxx_caller_trains_bitwise_like_the_c_abi(caller):
+    from paper_2602_04816_b200 import engine as E
+
+    r = subprocess.run([caller, "train", *_c1(), "3"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    bits = [int(ln.split()[1], 16) for ln in r.stdout.splitlines() if ln.startswith("loss")]
+    assert len(bits) == 3
+
+    c = E.ModelConfig(4, 256, 1024, 1024, 128, 4, k_ckpt=1, n_heads=2, rope_theta=1e6)
+    store = E.Store(c, 1234, "bf16")
+    losses = store.run_training(E.HyperParams(lr=3e-3), 1234, 3,
+                                E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=3))
+    want = [int(v) for v in np.asarray(losses, np.float64).view(np.uint64)]
+    assert bits == want, ([hex(b) for b in bits], [hex(w) for w in want])
+    # the step's byte counters follow the reference formula (planner.cpp:22-30)
+    tail = [ln for ln in r.stdout.splitlines() if ln.startswith("h2d")][0].split()
+    n, Vh = c.block_params(), c.vocab * c.hidden
+    assert int(tail[1]) == 2 * (2 * 4 * n + 2 * Vh) and int(tail[3]) == 4 * (4 * n + 2 * Vh)
+    assert int(tail[5]) == 3
+
+
+@pytest.mark.gpu
+def test_cxx_phase_api_matches_train_step(caller):
+    from paper_2602_04816_b200 import engine as E
+
+    r = subprocess.run([caller, "phases", *_c1()], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.splitlines()
+    b0, b1 = (int(lines[i].split()[1], 16) for i in (0, 1))
+    assert b0 == b1
+    c = E.ModelConfig(4, 256, 1024, 1024, 128, 4, k_ckpt=1, n_heads=2, rope_theta=1e6)
+    s = E.Store(c, 1234, "bf16")
+    e = E.Engine(s, E.Arena(c), E.HyperParams(), E.EngineOptions(skip_optimizer=True))
+    loss = e.train_step(E.make_copy_task_batch(c, 1235)).loss
+    assert int(np.float64(loss).view(np.uint64)) == b0
+    assert lines[2] == "recompute_forwards 4"
+
+
+@pytest.mark.gpu
+def test_cxx_exceptions_cross_the_library_boundary(caller):
+    r = subprocess.run([caller, "errors"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    out = r.stdout
+    assert "errors caught 4" in out
+    # ArenaOomError names the region that did not fit (reference test_arena.cpp:171-205)
+    assert "ArenaOomError region=" in out
