@@ -428,7 +428,10 @@ def run_ours(args, m, name):
         comm_g = E.nccl_comm(uids[0], world, rank)
         comm_w = E.nccl_comm(uids[1], world, rank)
         shm = f"hlm_bench_{os.environ.get('MASTER_PORT', os.getpid())}"
-        store = E.Store(cfg, 1234, "bf16", init="parallel", shared=shm, rank=rank, world=world)
+        import hashlib   # per-run nonce: a stale segment of a crashed run is never attached
+        nonce = int.from_bytes(hashlib.blake2b(uids[0], digest_size=8).digest(), "little")
+        store = E.Store(cfg, 1234, "bf16", init="parallel", shared=shm, rank=rank, world=world,
+                        nonce=nonce)
     else:
         store = E.Store(cfg, 1234, "bf16", init="parallel")
     # HBM weight cache for the backward turnaround: all blocks when they fit next to the arena

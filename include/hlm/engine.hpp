@@ -294,6 +294,8 @@ private:
     bool is_resident(i64 tile) const { return resident_of_[static_cast<size_t>(tile)] >= 0; }
     void resident_update(i64 tile, int gbuf, i64 dep_op);   // device finiteness scan + Adam
     void sync_resident();
+    void upload_resident();
+    i64 resident_epoch_ = 0;
     std::vector<void*> saved_acts_;        // per logical tile: HBM activations kept from the forward
     void* saved_mem_ = nullptr;
     // transit tiles (EngineOptions::transit_blocks)

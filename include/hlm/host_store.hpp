@@ -18,6 +18,7 @@
 #include <condition_variable>
 #include <cstdint>
 #include <deque>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -126,6 +127,11 @@ struct SharedStoreSpec {
     std::string name;
     int rank = 0;
     int world = 1;
+    // Per-run token every rank agrees on (e.g. derived from the NCCL unique id). Rank 0
+    // writes it into the segment header; an attaching rank accepts only a segment that
+    // carries it, so a stale segment of a crashed run under the same name is never used.
+    // 0 = no token (the dims are still checked).
+    std::uint64_t nonce = 0;
 };
 
 class MasterStore {
@@ -166,6 +172,36 @@ public:
     // while the count is non-zero: the file would silently hold stale tiles.
     void add_device_newer(int d) { device_newer_.fetch_add(d); }
     int device_newer() const { return device_newer_.load(); }
+    // An attached Engine registers a hook that brings the store up to date: it waits for
+    // the optimizer tail it may still be running on a worker thread (train_step returns
+    // before the head / top blocks of an overlapped tail are optimised) and copies
+    // HBM-resident tiles back. save_checkpoint / load_checkpoint / export / import call
+    // quiesce() first, so a file never mixes tiles from two steps and a load is never
+    // overwritten by a late tail update.
+    void set_quiesce(std::function<void()> hook, const void* owner) {
+        std::lock_guard<std::mutex> lk(quiesce_mu_);
+        quiesce_ = std::move(hook);
+        quiesce_owner_ = owner;
+    }
+    void clear_quiesce(const void* owner) {
+        std::lock_guard<std::mutex> lk(quiesce_mu_);
+        if (quiesce_owner_ == owner) {
+            quiesce_ = nullptr;
+            quiesce_owner_ = nullptr;
+        }
+    }
+    void quiesce() const {
+        std::function<void()> f;
+        {
+            std::lock_guard<std::mutex> lk(quiesce_mu_);
+            f = quiesce_;
+        }
+        if (f) f();
+    }
+    // Bumped whenever the store's state is replaced from outside (load_checkpoint,
+    // import_master): an engine holding HBM-resident tiles re-uploads them.
+    i64 epoch() const { return epoch_.load(); }
+    void bump_epoch() { epoch_.fetch_add(1); }
 
     bool bitwise_equal(const MasterStore& other) const;   // master, moments, shadow
 
@@ -180,6 +216,7 @@ public:
     void wait_ready() const;      // other ranks
 
 private:
+    void attach_shared(std::uint64_t nonce);
     ModelConfig config_;
     Dtype dtype_;
     std::vector<std::unique_ptr<LayerTile>> tiles_;
@@ -199,6 +236,10 @@ private:
     int rank_ = 0, world_ = 1;
     bool registered_ = false;
     std::atomic<int> device_newer_{0};
+    std::atomic<i64> epoch_{0};
+    mutable std::mutex quiesce_mu_;
+    std::function<void()> quiesce_;
+    const void* quiesce_owner_ = nullptr;
 };
 
 // Allocates and initialises a store: trunc_normal(0.02) matrices, unit norm

@@ -308,9 +308,12 @@ int hlm_store_export(const HlmStore* s, int field, float* out);
 int hlm_store_import_master(HlmStore* s, const float* w);   /* master := w, shadow re-packed */
 int hlm_store_bitwise_equal(const HlmStore* a, const HlmStore* b);
 /* Shared host store for one-process-per-GPU data parallelism: rank 0 creates
- * /dev/shm/<name> and initialises it, the other ranks attach. */
+ * /dev/shm/<name> and initialises it, the other ranks attach. `nonce` is a per-run
+ * token all ranks share (e.g. a hash of the NCCL unique id): an attaching rank only
+ * accepts the segment rank 0 stamped with it, never a stale one of a crashed run;
+ * it also checks the segment's model dims / world size (HLM_ERR_CONFIG otherwise). */
 int hlm_store_create_shared(const HlmModelConfig* cfg, uint64_t seed, int dtype, int init_mode, int pin_shadow,
-                            const char* name, int rank, int world, HlmStore** out);
+                            const char* name, int rank, int world, uint64_t nonce, HlmStore** out);
 /* Data-parallel host Adam: this rank updates its 1/world shard of every tile
  * from full-size gradients (store layout) and bumps its version counters. */
 int hlm_store_adam_shard(HlmStore* s, const float* grads, const HlmHyper* hp, int64_t t, int rank, int world);

@@ -160,10 +160,10 @@ int hlm_store_create(const HlmModelConfig* cfg, uint64_t seed, int dtype, int in
 }
 
 int hlm_store_create_shared(const HlmModelConfig* cfg, uint64_t seed, int dtype, int init_mode, int pin_shadow,
-                            const char* name, int rank, int world, HlmStore** out) {
+                            const char* name, int rank, int world, uint64_t nonce, HlmStore** out) {
     return guarded([&] {
         if (!name || !*name) throw std::invalid_argument("shared store needs a name");
-        hlm::SharedStoreSpec spec{name, rank, world};
+        hlm::SharedStoreSpec spec{name, rank, world, nonce};
         auto st = std::make_unique<HlmStore>();
         st->s = hlm::build_store(to_model(cfg), seed, dtype == 1 ? hlm::Dtype::FP32 : hlm::Dtype::BF16,
                                  init_mode == 1 ? hlm::InitMode::Parallel : hlm::InitMode::Reference, pin_shadow != 0,
@@ -246,6 +246,7 @@ int64_t hlm_store_adam_steps(const HlmStore* s) { return s ? s->s->adam_steps() 
 int hlm_store_export(const HlmStore* s, int field, float* out) {
     return guarded([&] {
         const hlm::MasterStore& st = *s->s;
+        st.quiesce();   // an attached engine's optimizer tail / resident tiles land first
         for (hlm::i64 p = 0; p < st.physical_tiles(); ++p) {
             const hlm::LayerTile& t = st.physical(p);
             const size_t n = static_cast<size_t>(t.n_params());
@@ -272,12 +273,14 @@ int hlm_store_export(const HlmStore* s, int field, float* out) {
 int hlm_store_import_master(HlmStore* s, const float* w) {
     return guarded([&] {
         hlm::MasterStore& st = *s->s;
+        st.quiesce();
         for (hlm::i64 p = 0; p < st.physical_tiles(); ++p) {
             hlm::LayerTile& t = st.physical(p);
             std::memcpy(t.master(), w, static_cast<size_t>(t.n_params()) * 4);
             w += t.n_params();
         }
         st.repack_shadow();
+        st.bump_epoch();
     });
 }
 

@@ -33,6 +33,7 @@ void fill_dims(const ModelConfig& m, std::int64_t* d) {
 }  // namespace
 
 void save_checkpoint(const MasterStore& store, const std::string& path) {
+    store.quiesce();   // an attached engine's optimizer tail and resident tiles land first
     if (store.device_newer() > 0)
         throw ProtocolError("save_checkpoint: an engine holds HBM-resident tiles newer than the store; "
                             "call Engine::sync() first");
@@ -67,6 +68,7 @@ void save_checkpoint(const MasterStore& store, const std::string& path) {
 }
 
 void load_checkpoint(MasterStore& store, const std::string& path) {
+    store.quiesce();   // no late tail update of an attached engine may overwrite the load
     std::ifstream f(path, std::ios::binary);
     if (!f) throw ConfigError("cannot open checkpoint file: " + path);
     Header h{};
@@ -101,6 +103,7 @@ void load_checkpoint(MasterStore& store, const std::string& path) {
     }
     store.repack_shadow();
     store.set_adam_steps(static_cast<i64>(h.adam_steps));
+    store.bump_epoch();   // engines holding HBM-resident tiles re-upload them
 }
 
 }  // inline namespace b200

@@ -191,14 +191,11 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
             LayerTile& t = store_.tile(id);
             Resident r{id, t.n_params(), reinterpret_cast<float*>(q),
                        reinterpret_cast<uint16_t*>(q + 12 * t.n_params())};
-            ck(cudaMemcpy(r.state, t.master(), static_cast<size_t>(12 * r.n), cudaMemcpyHostToDevice),
-               "upload resident state");
-            ck(cudaMemcpy(r.w16, t.shadow(), static_cast<size_t>(2 * r.n), cudaMemcpyHostToDevice),
-               "upload resident weights");
             resident_of_[static_cast<size_t>(id)] = static_cast<i64>(residents_.size());
             residents_.push_back(r);
             q += (t.n_params() * 14 + 255) / 256 * 256;
         }
+        upload_resident();
     }
     // saved activations: the top blocks' forward activations stay in HBM for their backward
     saved_acts_.assign(static_cast<size_t>(m.tile_count()), nullptr);
@@ -281,6 +278,13 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
         }
     }
     if (opts_.threaded_accum) worker_ = std::thread([this] { worker_loop(); });
+    store_.set_quiesce(
+        [this] {
+            if (phase_ != Phase::Idle)
+                throw ProtocolError("the store was saved / loaded while its engine is inside a step");
+            sync();
+        },
+        this);
 }
 
 // Order in which the next forward needs the tiles (embedding, blocks, head); with
@@ -292,6 +296,7 @@ i64 Engine::tail_key(i64 layer) const {
 }
 
 Engine::~Engine() {
+    store_.clear_quiesce(this);
     try {
         sync();
     } catch (...) {
@@ -969,6 +974,19 @@ void Engine::sync() {
     sync_resident();
 }
 
+// FP32 state and BF16 weights of the HBM-resident tiles from the store (construction,
+// and again when load_checkpoint / import_master replaced the store: epoch changed).
+void Engine::upload_resident() {
+    for (const auto& r : residents_) {
+        const LayerTile& t = store_.tile(r.tile);
+        ck(cudaMemcpy(r.state, t.master(), static_cast<size_t>(12 * r.n), cudaMemcpyHostToDevice),
+           "upload resident state");
+        ck(cudaMemcpy(r.w16, t.shadow(), static_cast<size_t>(2 * r.n), cudaMemcpyHostToDevice),
+           "upload resident weights");
+    }
+    resident_epoch_ = store_.epoch();
+}
+
 void Engine::wait_optimizer() {
     if (!opts_.threaded_accum) return;
     {
@@ -1007,6 +1025,15 @@ void Engine::begin_step(const Batch& batch) {
     if (static_cast<i64>(batch.tokens.size()) != T || static_cast<i64>(batch.targets.size()) != T)
         throw ConfigError("batch size does not match model config");
     batch_ = batch;
+    if (!residents_.empty() && store_.epoch() != resident_epoch_) {
+        // the store was replaced (sync() ran first through the quiesce hook, so nothing
+        // newer lives on the device): train on the loaded state
+        if (resident_dirty_) {
+            resident_dirty_ = false;
+            store_.add_device_newer(-1);
+        }
+        upload_resident();
+    }
     arena_.begin_step();
     arena_.claim_workspace();
     trace_ = EventTrace{};

@@ -11,6 +11,7 @@
 #include <pthread.h>
 #include <fcntl.h>
 #include <sys/mman.h>
+#include <sys/stat.h>
 #include <sys/statvfs.h>
 #include <unistd.h>
 
@@ -186,6 +187,7 @@ struct ShmHeader {
     std::uint64_t magic;
     std::atomic<std::uint64_t> ready;
     std::int64_t dims[8];
+    std::uint64_t nonce;
 };
 size_t align2m(size_t x) { return (x + (2u << 20) - 1) & ~size_t((2u << 20) - 1); }
 }  // namespace
@@ -233,19 +235,11 @@ MasterStore::MasterStore(const ModelConfig& config, Dtype dtype, bool pin_shadow
             if (shm_fd_ < 0) throw ConfigError("shared store: shm_open(create) failed for " + shm_name_);
             if (ftruncate(shm_fd_, static_cast<off_t>(map_bytes_)) != 0)
                 throw ConfigError("shared store: ftruncate failed");
+            map_base_ = mmap(nullptr, map_bytes_, PROT_READ | PROT_WRITE, MAP_SHARED, shm_fd_, 0);
+            if (map_base_ == MAP_FAILED) throw ConfigError("shared store: mmap failed");
         } else {
-            for (int i = 0; i < 60000 && shm_fd_ < 0; ++i) {
-                shm_fd_ = shm_open(shm_name_.c_str(), O_RDWR, 0600);
-                if (shm_fd_ < 0) std::this_thread::sleep_for(std::chrono::milliseconds(10));
-            }
-            if (shm_fd_ < 0) throw ConfigError("shared store: rank 0 never created " + shm_name_);
-            for (int i = 0; i < 60000; ++i) {   // wait for the full size
-                if (lseek(shm_fd_, 0, SEEK_END) >= static_cast<off_t>(map_bytes_)) break;
-                std::this_thread::sleep_for(std::chrono::milliseconds(10));
-            }
+            attach_shared(shared->nonce);
         }
-        map_base_ = mmap(nullptr, map_bytes_, PROT_READ | PROT_WRITE, MAP_SHARED, shm_fd_, 0);
-        if (map_base_ == MAP_FAILED) throw ConfigError("shared store: mmap failed");
         char* b = static_cast<char*>(map_base_);
         auto* hdr = reinterpret_cast<ShmHeader*>(b);
         state_base_ = reinterpret_cast<float*>(b + kShmHeader);
@@ -255,7 +249,12 @@ MasterStore::MasterStore(const ModelConfig& config, Dtype dtype, bool pin_shadow
                                       config_.tie_embeddings ? 1 : 0, static_cast<std::int64_t>(world_), 0, 0};
         if (rank_ == 0) {
             hdr->magic = kShmMagic;
+            hdr->nonce = shared->nonce;
             std::memcpy(hdr->dims, dims, sizeof dims);
+        } else if (std::memcmp(hdr->dims, dims, sizeof dims) != 0) {
+            throw ConfigError("shared store: " + shm_name_ + " was created for another model / world size");
+        }
+        if (rank_ == 0) {
             if (world_ > 1 && numa_node_count() > 1) {
                 // multi-socket host: each rank's shard of every tile (master, m, v, shadow)
                 // in the DRAM of its GPU's socket, where its Adam team and its DMA run
@@ -377,6 +376,43 @@ bool MasterStore::bitwise_equal(const MasterStore& o) const {
 void MasterStore::mark_ready() {
     if (shm_fd_ < 0) return;
     reinterpret_cast<ShmHeader*>(map_base_)->ready.store(1, std::memory_order_release);
+}
+
+// Attaching rank: open the segment under the name, wait for its full size, map it and
+// accept it only once it carries this run's nonce. A segment left by a crashed run
+// (same name, magic, even ready == 1) has another nonce: drop the mapping and re-open
+// by name, which yields rank 0's fresh segment once rank 0 unlinked and recreated it.
+void MasterStore::attach_shared(std::uint64_t nonce) {
+    for (int attempt = 0; attempt < 120000; ++attempt) {
+        if (attempt) std::this_thread::sleep_for(std::chrono::milliseconds(5));
+        if (shm_fd_ < 0) shm_fd_ = shm_open(shm_name_.c_str(), O_RDWR, 0600);
+        if (shm_fd_ < 0) continue;
+        if (lseek(shm_fd_, 0, SEEK_END) < static_cast<off_t>(map_bytes_)) {
+            // too small: still being sized by rank 0, or a stale segment of another model
+            struct stat by_fd {}, by_name {};
+            const int nfd = shm_open(shm_name_.c_str(), O_RDONLY, 0600);
+            const bool replaced = nfd >= 0 && fstat(shm_fd_, &by_fd) == 0 && fstat(nfd, &by_name) == 0 &&
+                                  by_fd.st_ino != by_name.st_ino;
+            if (nfd >= 0) close(nfd);
+            if (replaced) {
+                close(shm_fd_);
+                shm_fd_ = -1;
+            }
+            continue;
+        }
+        void* base = mmap(nullptr, map_bytes_, PROT_READ | PROT_WRITE, MAP_SHARED, shm_fd_, 0);
+        if (base == MAP_FAILED) throw ConfigError("shared store: mmap failed");
+        auto* hdr = reinterpret_cast<volatile ShmHeader*>(base);
+        if (hdr->magic == kShmMagic && hdr->nonce == nonce) {
+            map_base_ = base;
+            return;
+        }
+        munmap(base, map_bytes_);
+        close(shm_fd_);   // stale or not yet stamped: look the name up again
+        shm_fd_ = -1;
+    }
+    throw ConfigError("shared store: no segment " + shm_name_ + " with this run's nonce appeared (rank 0 never "
+                      "created it, or a stale segment is in the way)");
 }
 
 void MasterStore::wait_ready() const {

@@ -726,18 +726,26 @@ __global__ void head_certify_kernel(const __nv_bfloat16* __restrict__ x, long lo
 // first[0] = min index of a non-finite element (INT64 max when none): the
 // reference's "validate before any mutation" check (host_store.cpp:340-345),
 // run at HBM speed before the gradient leaves the GPU.
+// Any alignment of g (a data-parallel shard starts at rank * n / world elements): the
+// first `head` elements up to the next 16-byte boundary are scanned scalar, the rest
+// as float4.
 __global__ void nonfinite_kernel(const float* __restrict__ g, long long n, unsigned long long* first) {
+  const long long head = min(n, (long long)(((16u - ((uintptr_t)g & 15u)) & 15u) / 4u));
+  if (blockIdx.x == 0 && threadIdx.x < head)
+    if (!isfinite(g[threadIdx.x])) atomicMin(first, (unsigned long long)threadIdx.x);
+  const float* body = g + head;
+  const long long nb = n - head;
   const long long stride = (long long)gridDim.x * blockDim.x * 4;
-  for (long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < n; i += stride) {
-    if (i + 4 <= n) {
-      const float4 v = *reinterpret_cast<const float4*>(g + i);
+  for (long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < nb; i += stride) {
+    if (i + 4 <= nb) {
+      const float4 v = *reinterpret_cast<const float4*>(body + i);
       const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        if (!isfinite(e[k])) atomicMin(first, (unsigned long long)(i + k));
+        if (!isfinite(e[k])) atomicMin(first, (unsigned long long)(head + i + k));
     } else {
-      for (long long k = i; k < n; ++k)
-        if (!isfinite(g[k])) atomicMin(first, (unsigned long long)k);
+      for (long long k = i; k < nb; ++k)
+        if (!isfinite(body[k])) atomicMin(first, (unsigned long long)(head + k));
     }
   }
 }

@@ -146,7 +146,7 @@ def _L():
                                                 P(HyperParams), ctypes.c_int64]
         L.hlm_store_create_shared.argtypes = [P(ModelConfig), ctypes.c_uint64, ctypes.c_int,
                                               ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
-                                              ctypes.c_int, ctypes.c_int, P(_vp)]
+                                              ctypes.c_int, ctypes.c_int, ctypes.c_uint64, P(_vp)]
         L.hlm_store_adam_shard.argtypes = [_vp, _f32p, P(HyperParams), ctypes.c_int64, ctypes.c_int,
                                            ctypes.c_int]
         L.hlm_store_tile_version.argtypes = [_vp, ctypes.c_int64]
@@ -190,15 +190,16 @@ class Store:
     init 'reference' (bit-identical to the reference) | 'parallel'."""
 
     def __init__(self, cfg, seed, dtype="bf16", init="reference", pin=True, shared=None, rank=0,
-                 world=1):
+                 world=1, nonce=0):
         """shared: name of a /dev/shm object for a one-process-per-GPU store
-        (rank 0 creates and initialises it, other ranks attach)."""
+        (rank 0 creates and initialises it, other ranks attach); nonce: per-run token
+        shared by all ranks (a stale segment of another run is never attached)."""
         self.cfg = cfg
         h = _vp()
         dt, im = (1 if dtype == "fp32" else 0), (1 if init == "parallel" else 0)
         if shared:
             _check(_L().hlm_store_create_shared(ctypes.byref(cfg), seed, dt, im, int(pin),
-                                                shared.encode(), rank, world, ctypes.byref(h)))
+                                                shared.encode(), rank, world, nonce, ctypes.byref(h)))
         else:
             _check(_L().hlm_store_create(ctypes.byref(cfg), seed, dt, im, int(pin), ctypes.byref(h)))
         self.h = h

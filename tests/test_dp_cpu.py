@@ -78,3 +78,53 @@ def test_microbatch_split_sums_to_full_batch():
     g = sum(p[1] for p in parts)
     assert abs(loss - loss_full) < 1e-6 * abs(loss_full)
     assert np.abs(g - g_full).max() <= 1e-6 * np.abs(g_full).max()
+
+
+def _stale_segment(name, cfg_args):
+    """A run that crashed after initialising its shared store: the segment stays
+    behind under `name` with magic, ready == 1 and that run's nonce."""
+    from paper_2602_04816_b200 import engine as E
+    s = E.Store(E.ModelConfig(*cfg_args), 5, "fp32", pin=False, shared=name, rank=0, world=2,
+                nonce=111)
+    assert s.total_params > 0
+    os._exit(0)   # no destructor: the segment is not unlinked
+
+
+def _late_owner_worker(rank, world, port, name, out_path):
+    import time
+
+    import torch.distributed as dist
+    from paper_2602_04816_b200 import engine as E
+    cfg = E.ModelConfig(3, 16, 32, 24, 4, 2)
+    if rank == 0:
+        time.sleep(1.0)   # the attaching rank finds the stale segment first
+    s = E.Store(cfg, 77, "fp32", pin=False, shared=name, rank=rank, world=world, nonce=222)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    dist.barrier()
+    np.save(out_path + f".{rank}.npy", s.weights())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_attach_ignores_a_stale_segment_of_a_crashed_run():
+    """a non-zero rank must never train on a stale /dev/shm segment that a
+    crashed run left under the same name (same magic, ready == 1)."""
+    import multiprocessing
+
+    import torch.multiprocessing as mp
+    name = f"hlm_stale_{os.getpid()}"
+    p = multiprocessing.get_context("spawn").Process(target=_stale_segment,
+                                                     args=(name, (3, 16, 32, 24, 4, 2)))
+    p.start()
+    p.join(120)
+    assert os.path.exists(f"/dev/shm/{name}")
+    out = os.path.join(tempfile.mkdtemp(), "w")
+    try:
+        mp.start_processes(_late_owner_worker, args=(2, _free_port(), name, out), nprocs=2,
+                           start_method="spawn")
+    finally:
+        if os.path.exists(f"/dev/shm/{name}"):
+            os.unlink(f"/dev/shm/{name}")
+    w0, w1 = np.load(out + ".0.npy"), np.load(out + ".1.npy")
+    assert np.array_equal(w0, w1)   # rank 1 sees rank 0's fresh store (seed 77), not seed 5's

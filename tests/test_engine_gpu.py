@@ -315,13 +315,15 @@ def test_hbm_resident_optimizer_tiles_are_bitwise_neutral(res, tmp_path):
                                   overlap_optimizer_tail=True, tail_blocks=1, **res))
     l1 = [e1.train_step(t) for t in toks]
     assert validate_trace(e1.last_trace(), c.layers) == []
-    ck = str(tmp_path / "stale.hlm2")
-    with pytest.raises(Exception, match="sync"):
-        s.save(ck)          # the store's resident tiles are stale until sync()
-    e1.sync()
+    # save brings the store up to date itself (quiesce hook: optimizer tail + resident
+    # write-back), so the file holds the state after step 3 of every tile
+    ck = str(tmp_path / "now.hlm2")
     s.save(ck)
     assert l0 == [r.loss for r in l1]
     assert ref.bitwise_equal(s)
+    back = E.Store(c, 1)
+    back.load(ck)
+    assert back.bitwise_equal(ref)
     streamed = 2 * (c.vocab * c.hidden * (0 if res.get("resident_embed") else 1) +
                     c.vocab * c.hidden + 2 * (c.layers - res.get("resident_blocks", 0)) * c.block_params())
     assert l1[-1].h2d_bytes == streamed
@@ -494,3 +496,53 @@ def test_bench_feature_set_tracks_oracle_for_20_steps():
     l = np.array(losses)
     assert np.all(np.abs(l - ref) / ref < 1e-2), (l, ref)
     assert l[-1] < 0.9 * l[0]
+
+
+def test_save_right_after_train_step_waits_for_the_optimizer_tail(tmp_path):
+    """with an overlapped optimizer tail, train_step returns while the head and
+    top blocks are still being optimised on the worker; a save right then must not mix
+    tiles from two steps under a header that says step t."""
+    c = E.ModelConfig(6, 32, 64, 32, 16, 2, k_ckpt=1, n_heads=2, rope_theta=1e4)
+    toks = [E.make_copy_task_batch(c, 4, skip=i) for i in range(3)]
+    hp = E.HyperParams(lr=2e-3, weight_decay=0.01)
+    ref = E.Store(c, 8)
+    e0 = E.Engine(ref, E.Arena(c), hp, E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=4))
+    for t in toks:
+        e0.train_step(t)
+    e0.sync()
+    s = E.Store(c, 8)
+    e1 = E.Engine(s, E.Arena(c), hp,
+                  E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=4, overlap_optimizer_tail=True,
+                                  tail_blocks=6, accum_delay_us=2000))
+    for t in toks:
+        e1.train_step(t)
+    s.save(tmp_path / "tail.hlm2")   # no sync(): the tail is still running (accum_delay_us)
+    r = E.Store(c, 1)
+    r.load(tmp_path / "tail.hlm2")
+    assert r.adam_steps == 3 and r.bitwise_equal(ref)
+
+
+def test_load_checkpoint_reuploads_hbm_resident_tiles(tmp_path):
+    """load_checkpoint into a store whose live engine keeps HBM-resident tiles:
+    the engine must train on the loaded state, not on its stale device copy (which its
+    next sync() would otherwise write over the load)."""
+    c = E.ModelConfig(6, 32, 64, 32, 16, 2, k_ckpt=1, n_heads=2, rope_theta=1e4)
+    toks = [E.make_copy_task_batch(c, 4, skip=i) for i in range(3)]
+    hp = E.HyperParams(lr=2e-3, weight_decay=0.01)
+    ref = E.Store(c, 8)
+    e0 = E.Engine(ref, E.Arena(c), hp, E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=4))
+    l0 = [e0.train_step(t).loss for t in toks]
+    e0.sync()
+    s = E.Store(c, 8)
+    e1 = E.Engine(s, E.Arena(c), hp,
+                  E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=4, resident_embed=True,
+                                  resident_blocks=3, overlap_optimizer_tail=True, tail_blocks=1))
+    e1.train_step(toks[0])
+    e1.train_step(toks[1])
+    s.save(tmp_path / "two.hlm2")
+    first = e1.train_step(toks[2]).loss
+    s.load(tmp_path / "two.hlm2")    # back to the state after step 2
+    again = e1.train_step(toks[2]).loss
+    e1.sync()
+    assert first == l0[2] and again == l0[2]
+    assert s.adam_steps == 3 and s.bitwise_equal(ref)
