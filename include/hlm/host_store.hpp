@@ -336,6 +336,8 @@ void* map_huge_public(size_t bytes);
 
 // True when every element is finite (parallel scan).
 bool all_finite(const float* g, i64 n);
+// "avx512" or "generic": the host loop bodies this process selected at load time.
+const char* host_isa();
 
 struct HostBytesReport {
     i64 persistent = 0;

@@ -369,6 +369,10 @@ int hlm_engine_last_trace(HlmEngine* e, char* buf, size_t cap, size_t* needed);
 /* Host DRAM bandwidth probe (all OpenMP threads): STREAM triad a = b + s*c over
  * three arrays of `bytes_per_array`, best of `reps`; GB/s counting 3 arrays. */
 double hlm_host_triad_gbs(int64_t bytes_per_array, int reps);
+/* "avx512" | "generic": host Adam / BF16-pack / finiteness loop bodies selected at load
+ * time from the CPU (x86-64-v3 baseline; HLM_HOST_ISA=generic forces the portable ones).
+ * Both are bit-identical to the reference's scalar arithmetic. */
+const char* hlm_host_isa(void);
 
 /* HLM2 checkpoint of the host store (master, m, v, Adam step count); load
  * re-derives the BF16 shadow and rejects mismatched geometry (HLM_ERR_CONFIG). */

@@ -284,6 +284,8 @@ int hlm_store_import_master(HlmStore* s, const float* w) {
     });
 }
 
+const char* hlm_host_isa(void) { return hlm::host_isa(); }
+
 int hlm_store_bitwise_equal(const HlmStore* a, const HlmStore* b) { return a->s->bitwise_equal(*b->s) ? 1 : 0; }
 
 int hlm_store_adam_embed_rows(HlmStore* s, const int32_t* rows, int64_t n_rows, const float* compact,

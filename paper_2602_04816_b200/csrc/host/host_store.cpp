@@ -19,6 +19,7 @@
 #include <thread>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "hlm/bf16.hpp"
@@ -51,8 +52,24 @@ void parallel_zero(void* p, size_t bytes) {
     }
 }
 
+// Host ISA: the library is compiled for x86-64-v3 (any AVX2 host); the hot host loops
+// (Adam, BF16 packing, finiteness) have AVX-512 bodies selected at run time when the CPU
+// has AVX-512F/BW/VL/DQ, else portable scalar bodies. Both do the same IEEE single ops
+// in the same order (no FMA contraction), so results are bit-identical either way.
+// HLM_HOST_ISA=generic forces the portable bodies (tests).
+#define HLM_AVX512 __attribute__((target("avx512f,avx512bw,avx512vl,avx512dq")))
+
+bool detect_avx512() {
+    const char* force = std::getenv("HLM_HOST_ISA");
+    if (force && std::strcmp(force, "generic") == 0) return false;
+    __builtin_cpu_init();
+    return __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw") &&
+           __builtin_cpu_supports("avx512vl") && __builtin_cpu_supports("avx512dq");
+}
+const bool g_avx512 = detect_avx512();
+
 // RNE float -> bf16 for 16 lanes (bf16.hpp semantics incl. NaN quieting).
-inline __m256i bf16x16(__m512 x) {
+HLM_AVX512 inline __m256i bf16x16(__m512 x) {
     const __m512i b = _mm512_castps_si512(x);
     const __m512i lsb = _mm512_and_si512(_mm512_srli_epi32(b, 16), _mm512_set1_epi32(1));
     const __m512i rounded = _mm512_srli_epi32(_mm512_add_epi32(_mm512_add_epi32(b, _mm512_set1_epi32(0x7FFF)), lsb), 16);
@@ -65,16 +82,27 @@ inline __m256i bf16x16(__m512 x) {
     return _mm512_cvtepi32_epi16(r);
 }
 
+HLM_AVX512 void pack_range_avx512(const float* src, std::uint16_t* dst, i64 b, i64 e) {
+    i64 i = b;
+    for (; i + 16 <= e; i += 16)
+        _mm256_storeu_si256(reinterpret_cast<__m256i*>(dst + i), bf16x16(_mm512_loadu_ps(src + i)));
+    for (; i < e; ++i) dst[i] = bf16_bits_from_f32(src[i]);
+}
+
+void pack_range_generic(const float* src, std::uint16_t* dst, i64 b, i64 e) {
+    for (i64 i = b; i < e; ++i) dst[i] = bf16_bits_from_f32(src[i]);
+}
+
 void pack_shadow(const float* src, std::uint16_t* dst, i64 n) {
     const i64 chunk = 1 << 16;
     const i64 nc = (n + chunk - 1) / chunk;
 #pragma omp parallel for schedule(static)
     for (i64 c = 0; c < nc; ++c) {
         const i64 b = c * chunk, e = std::min(n, b + chunk);
-        i64 i = b;
-        for (; i + 16 <= e; i += 16)
-            _mm256_storeu_si256(reinterpret_cast<__m256i*>(dst + i), bf16x16(_mm512_loadu_ps(src + i)));
-        for (; i < e; ++i) dst[i] = bf16_bits_from_f32(src[i]);
+        if (g_avx512)
+            pack_range_avx512(src, dst, b, e);
+        else
+            pack_range_generic(src, dst, b, e);
     }
 }
 
@@ -604,24 +632,43 @@ void SlabPool::wait_all_free() {
 }
 
 // ------------------------------------------------------------------ Adam
+namespace {
+HLM_AVX512 bool finite_range_avx512(const float* g, i64 b, i64 e) {
+    i64 i = b;
+    __mmask16 acc = 0;
+    for (; i + 16 <= e; i += 16) {
+        const __m512i x = _mm512_castps_si512(_mm512_loadu_ps(g + i));
+        acc |= _mm512_cmpeq_epi32_mask(_mm512_and_si512(x, _mm512_set1_epi32(0x7F800000)),
+                                       _mm512_set1_epi32(0x7F800000));
+    }
+    for (; i < e; ++i)
+        if (!std::isfinite(g[i])) acc = 1;
+    return acc == 0;
+}
+
+bool finite_range_generic(const float* g, i64 b, i64 e) {
+    std::uint32_t acc = 0;   // branch-free: exponent all ones = Inf / NaN
+    for (i64 i = b; i < e; ++i) {
+        std::uint32_t bits;
+        std::memcpy(&bits, g + i, 4);
+        acc |= static_cast<std::uint32_t>((bits & 0x7F800000u) == 0x7F800000u);
+    }
+    return acc == 0;
+}
+}  // namespace
+
 bool all_finite(const float* g, i64 n) {
     int bad = 0;
 #pragma omp parallel for schedule(static) reduction(| : bad)
     for (i64 c = 0; c < (n + 65535) / 65536; ++c) {
         const i64 b = c * 65536, e = std::min(n, b + 65536);
-        i64 i = b;
-        __mmask16 acc = 0;
-        for (; i + 16 <= e; i += 16) {
-            const __m512i x = _mm512_castps_si512(_mm512_loadu_ps(g + i));
-            acc |= _mm512_cmpeq_epi32_mask(_mm512_and_si512(x, _mm512_set1_epi32(0x7F800000)),
-                                           _mm512_set1_epi32(0x7F800000));
-        }
-        for (; i < e; ++i)
-            if (!std::isfinite(g[i])) acc = 1;
-        if (acc) bad = 1;
+        const bool ok = g_avx512 ? finite_range_avx512(g, b, e) : finite_range_generic(g, b, e);
+        if (!ok) bad = 1;
     }
     return bad == 0;
 }
+
+const char* host_isa() { return g_avx512 ? "avx512" : "generic"; }
 
 namespace {
 
@@ -631,57 +678,87 @@ i64 first_non_finite(const float* g, i64 n) {
     return -1;
 }
 
-// Reference host_store.cpp:342-361 in 16-wide lanes. Every operation is an
-// IEEE single op in the same order (this TU is compiled with
-// -ffp-contract=off), so lanes equal the scalar reference bit for bit.
+// Reference host_store.cpp:342-361. Every operation is an IEEE single op in the
+// reference's order (this TU is compiled with -ffp-contract=off), so the 16-wide lanes
+// and the scalar bodies equal the scalar reference bit for bit. `g == nullptr` is an
+// all-zero gradient that is never read (row-sparse embedding update).
+struct AdamScalars {
+    float lr, b1, b2, eps, wd, bc1, bc2;
+};
+
+inline void adam_scalar(float* w, float* m, float* v, std::uint16_t* shadow, const float* g, i64 i,
+                        const AdamScalars& a) {
+    const float gv = g ? g[i] : 0.0f;
+    m[i] = a.b1 * m[i] + (1.0f - a.b1) * gv;
+    v[i] = a.b2 * v[i] + (1.0f - a.b2) * gv * gv;
+    const float mhat = m[i] / a.bc1;
+    const float vhat = v[i] / a.bc2;
+    float th = w[i];
+    th -= a.lr * (mhat / (std::sqrt(vhat) + a.eps) + a.wd * th);
+    w[i] = th;
+    shadow[i] = bf16_bits_from_f32(th);
+}
+
+// stream_shadow: the shadow is only read by the next H2D DMA, so full 32-byte groups
+// are stored non-temporally (no read-for-ownership of the destination lines).
+HLM_AVX512 void adam_range_avx512(float* __restrict w, float* __restrict m, float* __restrict v,
+                                  std::uint16_t* __restrict shadow, const float* __restrict g, i64 b, i64 e,
+                                  const AdamScalars& a, float* zero_after, bool stream_shadow) {
+    const __m512 vb1 = _mm512_set1_ps(a.b1), vb2 = _mm512_set1_ps(a.b2), vo1 = _mm512_set1_ps(1.0f - a.b1),
+                 vo2 = _mm512_set1_ps(1.0f - a.b2), vbc1 = _mm512_set1_ps(a.bc1), vbc2 = _mm512_set1_ps(a.bc2),
+                 veps = _mm512_set1_ps(a.eps), vwd = _mm512_set1_ps(a.wd), vlr = _mm512_set1_ps(a.lr);
+    i64 i = b;
+    for (; i + 16 <= e; i += 16) {
+        const __m512 gg = g ? _mm512_loadu_ps(g + i) : _mm512_setzero_ps();
+        __m512 mm = _mm512_loadu_ps(m + i);
+        __m512 vv = _mm512_loadu_ps(v + i);
+        __m512 th = _mm512_loadu_ps(w + i);
+        mm = _mm512_add_ps(_mm512_mul_ps(vb1, mm), _mm512_mul_ps(vo1, gg));
+        vv = _mm512_add_ps(_mm512_mul_ps(vb2, vv), _mm512_mul_ps(_mm512_mul_ps(vo2, gg), gg));
+        const __m512 mhat = _mm512_div_ps(mm, vbc1);
+        const __m512 vhat = _mm512_div_ps(vv, vbc2);
+        const __m512 upd = _mm512_add_ps(_mm512_div_ps(mhat, _mm512_add_ps(_mm512_sqrt_ps(vhat), veps)),
+                                         _mm512_mul_ps(vwd, th));
+        th = _mm512_sub_ps(th, _mm512_mul_ps(vlr, upd));
+        _mm512_storeu_ps(m + i, mm);
+        _mm512_storeu_ps(v + i, vv);
+        _mm512_storeu_ps(w + i, th);
+        if (stream_shadow && (reinterpret_cast<uintptr_t>(shadow + i) & 31) == 0)
+            _mm256_stream_si256(reinterpret_cast<__m256i*>(shadow + i), bf16x16(th));
+        else
+            _mm256_storeu_si256(reinterpret_cast<__m256i*>(shadow + i), bf16x16(th));
+        if (zero_after) _mm512_storeu_ps(zero_after + i, _mm512_setzero_ps());
+    }
+    for (; i < e; ++i) {
+        adam_scalar(w, m, v, shadow, g, i, a);
+        if (zero_after) zero_after[i] = 0.0f;
+    }
+}
+
+void adam_range_generic(float* __restrict w, float* __restrict m, float* __restrict v,
+                        std::uint16_t* __restrict shadow, const float* __restrict g, i64 b, i64 e,
+                        const AdamScalars& a, float* zero_after) {
+    for (i64 i = b; i < e; ++i) {
+        adam_scalar(w, m, v, shadow, g, i, a);
+        if (zero_after) zero_after[i] = 0.0f;
+    }
+}
+
 void adam_kernel(float* __restrict w, float* __restrict m, float* __restrict v, std::uint16_t* __restrict shadow,
                  const float* __restrict g, i64 n, float lr, float b1, float b2, float eps, float wd, float bc1,
                  float bc2, float* zero_after) {
     const i64 chunk = 1 << 15;
     const i64 nc = (n + chunk - 1) / chunk;
-    const float omb1 = 1.0f - b1, omb2 = 1.0f - b2;
+    const AdamScalars a{lr, b1, b2, eps, wd, bc1, bc2};
 #pragma omp parallel for schedule(static)
     for (i64 c = 0; c < nc; ++c) {
         const i64 b = c * chunk, e = std::min(n, b + chunk);
-        const __m512 vb1 = _mm512_set1_ps(b1), vb2 = _mm512_set1_ps(b2), vo1 = _mm512_set1_ps(omb1),
-                     vo2 = _mm512_set1_ps(omb2), vbc1 = _mm512_set1_ps(bc1), vbc2 = _mm512_set1_ps(bc2),
-                     veps = _mm512_set1_ps(eps), vwd = _mm512_set1_ps(wd), vlr = _mm512_set1_ps(lr);
-        i64 i = b;
-        for (; i + 16 <= e; i += 16) {
-            const __m512 gg = _mm512_loadu_ps(g + i);
-            __m512 mm = _mm512_loadu_ps(m + i);
-            __m512 vv = _mm512_loadu_ps(v + i);
-            __m512 th = _mm512_loadu_ps(w + i);
-            mm = _mm512_add_ps(_mm512_mul_ps(vb1, mm), _mm512_mul_ps(vo1, gg));
-            vv = _mm512_add_ps(_mm512_mul_ps(vb2, vv), _mm512_mul_ps(_mm512_mul_ps(vo2, gg), gg));
-            const __m512 mhat = _mm512_div_ps(mm, vbc1);
-            const __m512 vhat = _mm512_div_ps(vv, vbc2);
-            const __m512 upd = _mm512_add_ps(_mm512_div_ps(mhat, _mm512_add_ps(_mm512_sqrt_ps(vhat), veps)),
-                                             _mm512_mul_ps(vwd, th));
-            th = _mm512_sub_ps(th, _mm512_mul_ps(vlr, upd));
-            _mm512_storeu_ps(m + i, mm);
-            _mm512_storeu_ps(v + i, vv);
-            _mm512_storeu_ps(w + i, th);
-            // the shadow is only read by the next H2D DMA: stream it past the cache (no RFO)
-            if ((reinterpret_cast<uintptr_t>(shadow + i) & 31) == 0)
-                _mm256_stream_si256(reinterpret_cast<__m256i*>(shadow + i), bf16x16(th));
-            else
-                _mm256_storeu_si256(reinterpret_cast<__m256i*>(shadow + i), bf16x16(th));
-            if (zero_after) _mm512_storeu_ps(zero_after + i, _mm512_setzero_ps());
+        if (g_avx512) {
+            adam_range_avx512(w, m, v, shadow, g, b, e, a, zero_after, true);
+            _mm_sfence();   // order this thread's non-temporal shadow stores
+        } else {
+            adam_range_generic(w, m, v, shadow, g, b, e, a, zero_after);
         }
-        for (; i < e; ++i) {
-            const float gv = g[i];
-            m[i] = b1 * m[i] + (1.0f - b1) * gv;
-            v[i] = b2 * v[i] + (1.0f - b2) * gv * gv;
-            const float mhat = m[i] / bc1;
-            const float vhat = v[i] / bc2;
-            float th = w[i];
-            th -= lr * (mhat / (std::sqrt(vhat) + eps) + wd * th);
-            w[i] = th;
-            shadow[i] = bf16_bits_from_f32(th);
-            if (zero_after) zero_after[i] = 0.0f;
-        }
-        _mm_sfence();
     }
 }
 
@@ -728,7 +805,7 @@ void adam_step_rows_sparse(LayerTile& tile, i64 rows, i64 width, const std::int3
                 wd = static_cast<float>(hyper.weight_decay);
     const float bc1 = 1.0f - std::pow(b1, static_cast<float>(t));
     const float bc2 = 1.0f - std::pow(b2, static_cast<float>(t));
-    const float omb1 = 1.0f - b1, omb2 = 1.0f - b2;
+    const AdamScalars a{lr, b1, b2, eps, wd, bc1, bc2};
     float* W = tile.master();
     float* M = tile.moment_m();
     float* Vv = tile.moment_v();
@@ -736,39 +813,12 @@ void adam_step_rows_sparse(LayerTile& tile, i64 rows, i64 width, const std::int3
 #pragma omp parallel for schedule(static, 16)
     for (i64 r = 0; r < rows; ++r) {
         const i64 b = r * width, e = b + width;
+        // adam_kernel's lane sequence; an untouched row's zero gradient is not read
         const float* g = row_map[r] >= 0 ? compact + static_cast<i64>(row_map[r]) * width - b : nullptr;
-        const __m512 vb1 = _mm512_set1_ps(b1), vb2 = _mm512_set1_ps(b2), vo1 = _mm512_set1_ps(omb1),
-                     vo2 = _mm512_set1_ps(omb2), vbc1 = _mm512_set1_ps(bc1), vbc2 = _mm512_set1_ps(bc2),
-                     veps = _mm512_set1_ps(eps), vwd = _mm512_set1_ps(wd), vlr = _mm512_set1_ps(lr);
-        i64 i = b;
-        for (; i + 16 <= e; i += 16) {   // adam_kernel's lane sequence; a zero gradient is not read
-            const __m512 gg = g ? _mm512_loadu_ps(g + i) : _mm512_setzero_ps();
-            __m512 mm = _mm512_loadu_ps(M + i);
-            __m512 vv = _mm512_loadu_ps(Vv + i);
-            __m512 th = _mm512_loadu_ps(W + i);
-            mm = _mm512_add_ps(_mm512_mul_ps(vb1, mm), _mm512_mul_ps(vo1, gg));
-            vv = _mm512_add_ps(_mm512_mul_ps(vb2, vv), _mm512_mul_ps(_mm512_mul_ps(vo2, gg), gg));
-            const __m512 mhat = _mm512_div_ps(mm, vbc1);
-            const __m512 vhat = _mm512_div_ps(vv, vbc2);
-            const __m512 upd = _mm512_add_ps(_mm512_div_ps(mhat, _mm512_add_ps(_mm512_sqrt_ps(vhat), veps)),
-                                             _mm512_mul_ps(vwd, th));
-            th = _mm512_sub_ps(th, _mm512_mul_ps(vlr, upd));
-            _mm512_storeu_ps(M + i, mm);
-            _mm512_storeu_ps(Vv + i, vv);
-            _mm512_storeu_ps(W + i, th);
-            _mm256_storeu_si256(reinterpret_cast<__m256i*>(SH + i), bf16x16(th));
-        }
-        for (; i < e; ++i) {
-            const float gv = g ? g[i] : 0.0f;
-            M[i] = b1 * M[i] + (1.0f - b1) * gv;
-            Vv[i] = b2 * Vv[i] + (1.0f - b2) * gv * gv;
-            const float mhat = M[i] / bc1;
-            const float vhat = Vv[i] / bc2;
-            float th = W[i];
-            th -= lr * (mhat / (std::sqrt(vhat) + eps) + wd * th);
-            W[i] = th;
-            SH[i] = bf16_bits_from_f32(th);
-        }
+        if (g_avx512)
+            adam_range_avx512(W, M, Vv, SH, g, b, e, a, nullptr, false);
+        else
+            adam_range_generic(W, M, Vv, SH, g, b, e, a, nullptr);
     }
     tile.bump_version(0);
 }

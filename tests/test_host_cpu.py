@@ -178,3 +178,52 @@ def test_rank_cpu_slices_follow_gpu_numa_nodes_and_never_overlap():
     assert _cpu_slice(0, [0], list(range(16)), 16, [0] * 16) == list(range(16))
     # a node with no allowed CPU (memory-only node) falls back to the whole set
     assert _cpu_slice(0, [2, 2], list(range(4)), 4, [0] * 4) == [0, 1]
+
+
+_ISA_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2602_04816_b200 import engine as E, _lib
+import ctypes
+L = _lib.lib(); L.hlm_host_isa.restype = ctypes.c_char_p
+c = E.ModelConfig(2, 64, 96, 37, 4, 1)
+s = E.Store(c, 3, "fp32", pin=False, init="parallel")
+rng = np.random.default_rng(0)
+for t in (1, 2, 3):
+    g = (rng.standard_normal(s.total_params) * 1e-2).astype(np.float32)
+    g[::7] = 0.0
+    s.adam_step(g, E.HyperParams(lr=3e-3, weight_decay=0.01), t)
+rows = np.array([0, 3, 4, 36], np.int32)
+s.adam_embed_rows(rows, (rng.standard_normal(4 * 64) * 1e-2).astype(np.float32), E.HyperParams(), 4)
+bad = np.zeros(s.total_params, np.float32); bad[1001] = np.inf
+try:
+    s.adam_step(bad, E.HyperParams(), 5); rejected = False
+except E.NumericsError:
+    rejected = True
+np.savez(sys.argv[2], isa=L.hlm_host_isa().decode(), rejected=rejected,
+         **{f: s.export(k) for f, k in (("w", E.FIELD_MASTER), ("m", E.FIELD_M), ("v", E.FIELD_V),
+                                       ("sh", E.FIELD_SHADOW))})
+"""
+
+
+def test_portable_host_isa_is_bitwise_equal_to_avx512(tmp_path):
+    """The library targets x86-64-v3 and picks AVX-512 host loop bodies at run time; the
+    portable bodies (HLM_HOST_ISA=generic, what a host without AVX-512 runs) give the
+    same bits for Adam (dense and row-sparse), BF16 packing and the finiteness check."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "isa.py"
+    script.write_text(_ISA_SCRIPT)
+    out = {}
+    for isa in ("default", "generic"):
+        env = dict(os.environ)
+        if isa == "generic":
+            env["HLM_HOST_ISA"] = "generic"
+        dst = tmp_path / f"{isa}.npz"
+        subprocess.run([sys.executable, str(script), root, str(dst)], check=True, env=env)
+        out[isa] = np.load(dst)
+    assert str(out["generic"]["isa"]) == "generic"
+    for f in ("w", "m", "v", "sh"):
+        assert np.array_equal(out["default"][f].view(np.uint32), out["generic"][f].view(np.uint32)), f
+    assert bool(out["default"]["rejected"]) and bool(out["generic"]["rejected"])
