@@ -1,12 +1,13 @@
-"""One transformer block at the C2 (Qwen2.5-7B-shaped) width — h 3584, f 18944,
-28 heads of 128, RoPE theta 1e6 — through the C ABI (hlm_cuda_block_fwd / _bwd:
-the 2-CTA and K-grouped tcgen05 GEMMs, the ping-pong flash attention, the fused
-RMSNorm / RoPE / SwiGLU kernels at production shapes), against a plain PyTorch fp32
-autograd restatement of the same block (oracle/hlm_oracle.cpp block_forward /
-block_backward semantics: pre-RMSNorm eps 1e-6, x.W with W (in, out), rotate-half
-RoPE, causal softmax(q k^T / sqrt(hd)), SwiGLU down(up * silu(gate)), residuals).
-Tolerance: BF16 GEMM operands / FP32 accumulation — relative L2 2e-2 on the output,
-5e-2 on every gradient (w_q / w_k: 1e-1, their gradients are tiny at init)."""
+"""One transformer block at the C2 (Qwen2.5-7B), C4 (72B) and C5 (120B-class) widths
+through the C ABI (hlm_cuda_block_fwd / _bwd: the 2-CTA and K-grouped tcgen05 GEMMs, the
+ping-pong flash attention, the fused RMSNorm / RoPE / SwiGLU kernels at production
+shapes), against the exact PyTorch restatement (tests/parity_model.py, fp32 with TF32
+off; oracle/hlm_oracle.cpp block_forward / block_backward semantics).
+
+Tolerance, calibrated: the same restatement rounding to BF16 where
+the kernels round measures the inherent noise of the recipe per output (block output,
+input gradient, each weight tensor's gradient); ours must be within 3x that noise.
+"""
 import ctypes
 
 import numpy as np
@@ -69,8 +70,10 @@ def torch_block(x, W, h, f, H, S, theta, eps=1e-6):
 
 
 @pytest.mark.parametrize("h,f,H,B,S", [(3584, 18944, 28, 2, 1024),     # C2 (Qwen2.5-7B width)
-                                       (8192, 29568, 64, 1, 1024)])    # C4 (72B width; ragged N tiles)
-def test_c2_width_block_matches_torch_fp32(h, f, H, B, S):
+                                       (8192, 29568, 64, 1, 1024),     # C4 (72B width; ragged N tiles)
+                                       (12288, 49152, 96, 1, 1024)])   # C5 (120B-class width)
+def test_wide_block_within_calibrated_bf16_noise(h, f, H, B, S):
+    import parity_model as PM
     theta = 1e6
     T = B * S
     dev = "cuda"
@@ -95,22 +98,18 @@ def test_c2_width_block_matches_torch_fp32(h, f, H, B, S):
     L.check(Lb.hlm_cuda_block_bwd(ctypes.byref(d), vp(Wb), vp(x), vp(acts), vp(g_out), vp(g_in), vp(grad),
                                   vp(ws), vp(cs), vp(sn), None))
     torch.cuda.synchronize()
-
-    W = Wb.float().requires_grad_(True)
-    xr = x.clone().requires_grad_(True)
-    y_ref = torch_block(xr, W, h, f, H, S, theta)
-    y_ref.backward(g_out)
-    errs = {"out": rel(y, y_ref.detach()), "g_in": rel(g_in, xr.grad)}
-    # BF16 rounding of n1, q/k/v, attention output, n2, act grows slightly with width:
-    # 3.8e-3 at h 3584, 1.0e-2 at h 8192
-    assert errs["out"] < 2e-2
-    assert errs["g_in"] < 5e-2
+    del acts, ws
     assert not torch.isnan(grad).any()
-    o = 0
-    for name, n in (("w_q", h * h), ("w_k", h * h), ("w_v", h * h), ("w_o", h * h), ("w_up", h * f),
-                    ("w_gate", h * f), ("w_down", f * h), ("norm1", h), ("norm2", h)):
-        e = rel(grad[o:o + n], W.grad[o:o + n])
-        errs[name] = e
-        assert e < (1e-1 if name in ("w_q", "w_k") else 5e-2), (name, e)
-        o += n
-    print(f"h={h} block rel-L2:", {k: f"{v:.1e}" for k, v in errs.items()})
+
+    W = Wb.float()
+    del Wb
+    yx, gx, Gx = PM.block_forward_backward(x, W, g_out, h, f, S, B, H, theta, exact=True)
+    ye, ge, Ge = PM.block_forward_backward(x, W, g_out, h, f, S, B, H, theta, exact=False)
+    rows = {"out": (rel(y, yx), rel(ye, yx)), "g_in": (rel(g_in, gx), rel(ge, gx))}
+    lay, _ = PM.block_layout(h, f)
+    for name, off, shape in lay:
+        n = int(np.prod(shape))
+        rows[name] = (rel(grad[off:off + n], Gx[off:off + n]), rel(Ge[off:off + n], Gx[off:off + n]))
+    print(f"h={h} block relL2 ours / noise:", {k: f"{a:.1e}/{b:.1e}" for k, (a, b) in rows.items()})
+    bad = {k: (a, b) for k, (a, b) in rows.items() if a > 3.0 * b + 1e-6}
+    assert not bad, bad
