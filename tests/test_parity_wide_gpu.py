@@ -39,7 +39,7 @@ pytestmark = pytest.mark.gpu
 BOUND = 3.0        # x the inherent BF16 noise, per tensor
 FLOOR = 1e-6       # the exact restatement's own fp32 accumulation error
 S, B = 512, 2
-LR = 1e-3
+LR = 1e-5          # one Adam step moves every weight by ~LR: the copy task stays unsolved
 
 CASES = [  # name, layers, h, f, V, heads, exact dtype, adam step
     ("c2w", 2, 3584, 18944, 152064, 28, torch.float64, True),
@@ -55,7 +55,7 @@ def _norms(a, b, tensors):
         d2 = r2 = 0.0
         for c0 in range(off, off + n, 1 << 26):
             c1 = min(off + n, c0 + (1 << 26))
-            x, y = a[c0:c1].double(), b[c0:c1].double()
+            x, y = a[c0:c1].to(b.device).double(), b[c0:c1].double()
             d2 += float(((x - y) ** 2).sum())
             r2 += float((y ** 2).sum())
         out[name] = (math.sqrt(d2), math.sqrt(r2))
@@ -78,21 +78,23 @@ def test_engine_step_within_calibrated_bf16_noise(case):
     del eng
     gc.collect()
     W = torch.from_numpy(store.export(E.FIELD_SHADOW)).cuda()
-    G_ours = torch.from_numpy(store.grads()).cuda()
+    G_ours = torch.from_numpy(store.grads())   # host; compared chunk by chunk
     tensors = PM.model_tensors(L, h, f, V)
 
     loss_x, G_x = PM.forward_backward(W, tok_t, L, h, f, V, S, B, H, exact=True, dtype=xdt)
     err = _norms(G_ours, G_x, tensors)
-    del G_ours
     torch.cuda.empty_cache()
     loss_e, G_e = PM.forward_backward(W, tok_t, L, h, f, V, S, B, H, exact=False, dtype=torch.float32)
     noise = _norms(G_e, G_x, tensors)
+    vs_emu = _norms(G_ours, G_e, tensors)   # ours against the emulation itself
+    del G_ours
 
     rows, bad = {}, []
     for t, _, _ in tensors:
         e = err[t][0] / max(err[t][1], 1e-30)
         nz = noise[t][0] / max(noise[t][1], 1e-30)
-        rows[t] = {"ours": e, "noise": nz, "ratio": e / max(nz, 1e-30), "bound": BOUND * nz + FLOOR}
+        rows[t] = {"ours": e, "noise": nz, "ratio": e / max(nz, 1e-30), "bound": BOUND * nz + FLOOR,
+                   "ours_vs_emu": vs_emu[t][0] / max(vs_emu[t][1], 1e-30)}
         if e > BOUND * nz + FLOOR:
             bad.append((t, e, nz))
     dl_ours, dl_emu = abs(loss_ours - loss_x) / loss_x, abs(loss_e - loss_x) / loss_x
