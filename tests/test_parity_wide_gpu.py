@@ -38,6 +38,9 @@ pytestmark = pytest.mark.gpu
 
 BOUND = 3.0        # x the inherent BF16 noise, per tensor
 FLOOR = 1e-6       # the exact restatement's own fp32 accumulation error
+# A scalar loss has one noise sample, not millions: its floor covers the ours-vs-emulation
+# distance (summation order, ex2.approx) when the emulation happens to land on the exact value.
+LOSS_FLOOR = 2e-5
 S, B = 512, 2
 LR = 1e-5          # one Adam step moves every weight by ~LR: the copy task stays unsolved
 
@@ -99,7 +102,7 @@ def test_engine_step_within_calibrated_bf16_noise(case):
             bad.append((t, e, nz))
     dl_ours, dl_emu = abs(loss_ours - loss_x) / loss_x, abs(loss_e - loss_x) / loss_x
     rows["loss"] = {"ours": dl_ours, "noise": dl_emu, "ratio": dl_ours / max(dl_emu, 1e-30),
-                    "bound": BOUND * dl_emu + FLOOR}
+                    "bound": BOUND * dl_emu + LOSS_FLOOR}
     report = {"case": name, "shape": dict(L=L, h=h, f=f, V=V, heads=H, S=S, B=B),
               "exact_dtype": str(xdt), "loss": {"ours": loss_ours, "exact": loss_x, "emu": loss_e},
               "tensors": rows}
@@ -120,11 +123,11 @@ def test_engine_step_within_calibrated_bf16_noise(case):
         loss2_e, _ = PM.forward_backward(W1, tok_t, L, h, f, V, S, B, H, exact=False, dtype=torch.float32)
         d2o, d2e = abs(loss2_ours - loss2_x) / loss2_x, abs(loss2_e - loss2_x) / loss2_x
         rows["loss_after_adam"] = {"ours": d2o, "noise": d2e, "ratio": d2o / max(d2e, 1e-30),
-                                   "bound": BOUND * d2e + FLOOR}
+                                   "bound": BOUND * d2e + LOSS_FLOOR}
         report["loss_after_adam"] = {"ours": loss2_ours, "exact": loss2_x, "emu": loss2_e}
-        if d2o > BOUND * d2e + FLOOR:
+        if d2o > BOUND * d2e + LOSS_FLOOR:
             bad.append(("loss_after_adam", d2o, d2e))
-    if dl_ours > BOUND * dl_emu + FLOOR:
+    if dl_ours > BOUND * dl_emu + LOSS_FLOOR:
         bad.append(("loss", dl_ours, dl_emu))
 
     # per-tensor-kind summary (max over layers) for the docs
