@@ -72,6 +72,8 @@ def _group(name):
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
 def test_engine_step_within_calibrated_bf16_noise(case):
     name, L, h, f, V, H, xdt, adam = case
+    gc.collect()
+    torch.cuda.empty_cache()   # the engine's arena is a plain cudaMalloc beside torch's cache
     cfg = E.ModelConfig(L, h, f, V, S, B, k_ckpt=1, n_heads=H, rope_theta=1e6)
     tok = E.make_copy_task_batch(cfg, 1235)
     tok_t = torch.from_numpy(tok).cuda()
