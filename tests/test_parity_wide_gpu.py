@@ -78,12 +78,18 @@ def test_engine_step_within_calibrated_bf16_noise(case):
     tok = E.make_copy_task_batch(cfg, 1235)
     tok_t = torch.from_numpy(tok).cuda()
     store = E.Store(cfg, 1234, "bf16", init="parallel")
-    eng = E.Engine(store, E.Arena(cfg), E.HyperParams(lr=LR), E.EngineOptions(skip_optimizer=True))
+    # n_slab 4: the host holds the store (14 B/param) plus only four pinned gradient slabs
+    opts = E.EngineOptions(skip_optimizer=True, n_slab=4)
+    eng = E.Engine(store, E.Arena(cfg), E.HyperParams(lr=LR), opts)
     loss_ours = eng.train_step(tok).loss
     del eng
     gc.collect()
     W = torch.from_numpy(store.export(E.FIELD_SHADOW)).cuda()
+    gc.collect()
     G_ours = torch.from_numpy(store.grads())   # host; compared chunk by chunk
+    if not adam:
+        del store   # C5: 103 GB of host store; only the gradients are needed from here
+        gc.collect()
     tensors = PM.model_tensors(L, h, f, V)
 
     loss_x, G_x = PM.forward_backward(W, tok_t, L, h, f, V, S, B, H, exact=True, dtype=xdt)
@@ -113,7 +119,7 @@ def test_engine_step_within_calibrated_bf16_noise(case):
         master = torch.from_numpy(store.export(E.FIELD_MASTER)).cuda()
         # ours: the store's host Adam on our gradients, then the engine's next loss
         store.adam_step(store.grads(), E.HyperParams(lr=LR), 1)
-        eng = E.Engine(store, E.Arena(cfg), E.HyperParams(lr=LR), E.EngineOptions(skip_optimizer=True))
+        eng = E.Engine(store, E.Arena(cfg), E.HyperParams(lr=LR), opts)
         loss2_ours = eng.train_step(tok).loss
         del eng
         gc.collect()
