@@ -201,10 +201,11 @@ def block_forward_backward(x, Wtile, g_out, h, f, S, B, H, theta=1e6, exact=True
         return y.detach(), xd.grad.detach(), Wd.grad.detach()
 
 
-def forward_backward(W, tokens, L, h, f, V, S, B, H, theta=1e6, exact=True, dtype=torch.float32):
+def forward_backward(W, tokens, L, h, f, V, S, B, H, theta=1e6, exact=True, dtype=torch.float32,
+                     return_rows=False):
     """Loss and per-parameter gradients (flat, store layout, untied) of one step.
     W: flat parameters (the BF16 shadow values), tokens: (B*S,) int (targets = tokens,
-    the copy task). Returns (loss: float, grad: flat tensor of `dtype`)."""
+    the copy task). Returns (loss: float, grad: flat tensor of `dtype`[, per-row losses])."""
     with _NoTF32():
         Wd = W.detach().to(dtype).requires_grad_(True)
         ctx = _Ctx(S, B, h, H, theta, exact, dtype, W.device)
@@ -217,8 +218,11 @@ def forward_backward(W, tokens, L, h, f, V, S, B, H, theta=1e6, exact=True, dtyp
             x = ctx.block(x, blk)
         head = Wd[o:o + V * h].view(V, h)
         logits = ctx.rg(ctx.rf(x) @ head.t())
-        loss = torch.nn.functional.cross_entropy(logits, tok)
+        rows = torch.nn.functional.cross_entropy(logits, tok, reduction="none")
+        loss = rows.mean()
         loss.backward()
+        if return_rows:
+            return float(loss.detach()), Wd.grad.detach(), rows.detach()
         return float(loss.detach()), Wd.grad.detach()
 
 
