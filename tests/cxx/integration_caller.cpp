@@ -6,6 +6,10 @@
 //   integration_caller train  L h f V S B K heads steps   -> one "loss <hex> <value>" line per step
 //   integration_caller phases L h f V S B K heads          -> loss of one step via the phase API
 //   integration_caller errors                              -> exercises the exception mapping
+//   integration_caller arena                               -> DeviceArena / ledger contract
+//                                                             (reference proj/tests/test_arena.cpp:160-215)
+//   integration_caller ledger L h f V S B K heads           -> footprint vs the live ledger after one step
+//                                                             (reference proj/tests/test_planner.cpp:43-72)
 #include <cinttypes>
 #include <cstdio>
 #include <cstdlib>
@@ -120,6 +124,104 @@ int errors() {
     return seen == 4 ? 0 : 1;
 }
 
+int failures = 0;
+void expect(bool ok, const char* what) {
+    std::printf("%s %s\n", ok ? "ok" : "FAIL", what);
+    if (!ok) ++failures;
+}
+
+template <typename Ex, typename F>
+bool throws(F&& f) {
+    try {
+        f();
+    } catch (const Ex&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+int arena() {
+    hlm::ModelConfig m;
+    m.layers = 8; m.hidden = 64; m.ffn = 128; m.vocab = 64; m.seq = 32; m.batch = 2; m.k_ckpt = 2;
+    const hlm::ArenaFootprint fp = hlm::arena_footprint(m);
+    expect(!throws<std::exception>([&] { hlm::DeviceArena a(m, fp.total()); }), "an exact budget cap fits");
+    try {
+        hlm::DeviceArena a(m, fp.total() - 1);
+        expect(false, "budget cap total-1 throws");
+    } catch (const hlm::ArenaOomError& e) {
+        expect(e.region() == "workspace", "budget cap total-1 names the last region to claim (workspace)");
+    }
+    try {
+        hlm::DeviceArena a(m, 16);
+        expect(false, "budget cap 16 throws");
+    } catch (const hlm::ArenaOomError& e) {
+        expect(e.region() == "stream_buf[0]", "budget cap 16 names stream_buf[0]");
+    }
+    hlm::DeviceArena arena(m);
+    arena.begin_step();
+    const hlm::i64 start = arena.ledger().current(hlm::Region::Stack);
+    arena.push_acts();
+    arena.push_acts();   // capacity: K = 2 slabs
+    expect(arena.ledger().current(hlm::Region::Stack) == start + fp.stack, "two pushes fill the K-slab stack");
+    try {
+        arena.push_acts();
+        expect(false, "third push throws");
+    } catch (const hlm::ArenaOomError& e) {
+        expect(e.region() == "activation_stack" && e.requested() > e.capacity(),
+               "stack overflow is an OOM naming activation_stack, requested > capacity");
+    }
+    arena.pop_acts();
+    arena.pop_acts();
+    expect(arena.ledger().current(hlm::Region::Stack) == start, "pops return the stack to its start");
+    expect(throws<hlm::ProtocolError>([&] { arena.pop_acts(); }), "pop of an empty stack is a ProtocolError");
+    arena.anchor_checkpoint(0);
+    arena.anchor_checkpoint(4);
+    arena.anchor_checkpoint(8);
+    expect(arena.ledger().current(hlm::Region::Anchors) == 3 * fp.anchor_slot, "three anchors claimed");
+    expect(throws<hlm::ProtocolError>([&] { arena.load_checkpoint(6); }), "never-anchored load throws");
+    expect(throws<hlm::ProtocolError>([&] { arena.anchor_checkpoint(3); }), "anchor off the K grid throws");
+    arena.release_checkpoint(4);
+    expect(throws<hlm::ProtocolError>([&] { arena.load_checkpoint(4); }), "released anchor cannot be loaded");
+    arena.release_checkpoint(0);
+    arena.release_checkpoint(8);
+    expect(arena.ledger().current(hlm::Region::Anchors) == 0, "anchors released");
+    expect(throws<hlm::ProtocolError>([&] {
+               arena.claim_buffer(0, 1, 8);
+               arena.claim_buffer(0, 2, 8);
+           }),
+           "stream_in into a busy buffer is a ProtocolError");
+    std::printf("arena failures %d\n", failures);
+    return failures ? 1 : 0;
+}
+
+int ledger(char** a) {
+    const hlm::ModelConfig m = config_from(a);
+    auto store = hlm::build_store(m, 1234, hlm::Dtype::BF16, hlm::InitMode::Reference);
+    hlm::DeviceArena arena(m);
+    hlm::EngineOptions opts;
+    opts.eager_optim = true;
+    opts.threaded_accum = true;
+    opts.n_slab = 4;
+    hlm::Engine engine(*store, arena, hlm::HyperParams{}, opts);
+    hlm::Rng data(1235);
+    const hlm::StepResult r = engine.train_step(hlm::make_copy_task_batch(m, data));
+    const hlm::ArenaFootprint fp = hlm::arena_footprint(m);
+    std::printf("footprint total %" PRId64 " core %" PRId64 " anchors %" PRId64 " stream_buf %" PRId64
+                " stack %" PRId64 " workspace %" PRId64 " widest_tile_bytes %" PRId64 "\n",
+                fp.total(), fp.core_total(), fp.anchors_total(), fp.stream_buf, fp.stack, fp.workspace,
+                2 * m.max_tile_params());
+    for (const auto& rs : r.arena.regions)
+        std::printf("region %s capacity %" PRId64 " current %" PRId64 " step_peak %" PRId64 "\n", rs.name.c_str(),
+                    rs.capacity, rs.current, rs.step_peak);
+    std::printf("committed %" PRId64 " peak %" PRId64 " peak_non_anchor %" PRId64 "\n", r.arena.committed_total,
+                r.arena.step_peak_total, r.arena.step_peak_non_anchor);
+    std::printf("host persistent %" PRId64 " slabs %" PRId64 " total %" PRId64 " params %" PRId64 "\n",
+                r.host.persistent, r.host.slabs, r.host.total, store->total_params());
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -128,7 +230,9 @@ int main(int argc, char** argv) {
         if (mode == "train" && argc == 11) return train(argv + 2);
         if (mode == "phases" && argc == 10) return phases(argv + 2);
         if (mode == "errors") return errors();
-        std::fprintf(stderr, "usage: %s train L h f V S B K heads steps | phases L h f V S B K heads | errors\n",
+        if (mode == "arena") return arena();
+        if (mode == "ledger" && argc == 10) return ledger(argv + 2);
+        std::fprintf(stderr, "usage: %s train L h f V S B K heads steps | phases L h f V S B K heads | errors | arena | ledger L h f V S B K heads\n",
                      argv[0]);
         return 64;
     } catch (const std::invalid_argument& e) {

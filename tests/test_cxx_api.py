@@ -138,3 +138,56 @@ def test_cxx_exceptions_cross_the_library_boundary(caller):
     assert "errors caught 4" in out
     # ArenaOomError names the region that did not fit (reference test_arena.cpp:171-205)
     assert "ArenaOomError region=" in out
+
+
+@pytest.mark.gpu
+def test_arena_contract_through_the_cxx_api(caller):
+    """DeviceArena / ArenaLedger contract (reference proj/tests/test_arena.cpp:160-215):
+    budget caps and stack overflow raise ArenaOomError naming the region, anchors only on
+    the K grid, protocol errors on misuse — exercised through the exported C++ API."""
+    r = subprocess.run([caller, "arena"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "FAIL" not in r.stdout and "arena failures 0" in r.stdout
+
+
+def _parse_ledger(out):
+    """'region <name> k v k v ...', 'footprint k v ...', 'host k v ...', 'committed v k v ...'."""
+    regions, kv = {}, {}
+    for ln in out.splitlines():
+        w = ln.split()
+        if not w:
+            continue
+        if w[0] == "region":
+            regions[w[1]] = {w[i]: int(w[i + 1]) for i in range(2, len(w) - 1, 2)}
+        elif w[0] in ("footprint", "host"):
+            kv.update({f"{w[0]}.{w[i]}": int(w[i + 1]) for i in range(1, len(w) - 1, 2)})
+        elif w[0] == "committed":
+            kv.update({w[i]: int(w[i + 1]) for i in range(0, len(w) - 1, 2)})
+    return regions, kv
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("K", [1, 2])
+def test_live_ledger_equals_the_footprint_estimate(caller, K):
+    """Plan == ledger (reference proj/tests/test_planner.cpp:43-72): after one step every
+    region's live peak reaches exactly the capacity the footprint formula reserved — the
+    estimate neither over- nor under-commits — and the host ledger equals 14 B/param."""
+    L, h, f, V, S, B = 4, 256, 1024, 1024, 128, 4
+    r = subprocess.run([caller, "ledger", str(L), str(h), str(f), str(V), str(S), str(B), str(K), "2"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    regions, kv = _parse_ledger(r.stdout)
+    assert kv["committed"] == kv["footprint.total"]
+    assert sum(x["capacity"] for x in regions.values()) == kv["footprint.total"]
+    for name in ("activation_stack", "ckpt_anchors", "workspace"):
+        assert regions[name]["step_peak"] == regions[name]["capacity"], (name, regions[name])
+    widest = kv["footprint.widest_tile_bytes"]
+    for name in ("stream_buf[0]", "stream_buf[1]"):
+        assert regions[name]["capacity"] == kv["footprint.stream_buf"]
+        assert regions[name]["step_peak"] == widest, (name, regions[name])
+        assert regions[name]["current"] == 0          # nothing left streamed in after the step
+    assert regions["ckpt_anchors"]["current"] == 0
+    n = 4 * h * h + 3 * h * f + 2 * h
+    params = 2 * V * h + L * n
+    assert kv["host.params"] == params and kv["host.persistent"] == 14 * params
+    assert kv["host.total"] == kv["host.persistent"] + kv["host.slabs"]
