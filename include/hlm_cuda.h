@@ -383,6 +383,14 @@ int hlm_store_load(HlmStore* s, const char* path);
 int hlm_nccl_unique_id(uint8_t* out128);
 int hlm_nccl_comm_create(const uint8_t* id128, int world, int rank, void** comm);
 void hlm_nccl_comm_destroy(void* comm);
+/* The data-parallel exchange steps for callers that keep their own engine:
+ * per-layer fp32 gradient reduce-scatter (sum; `count` elements land on each rank, send
+ * holds world x count), bf16 weight all-gather (each rank contributes `count`), and the
+ * loss all-reduce (sum, in place allowed). Stream-ordered on `stream`; status codes as
+ * everywhere else (HLM_ERR_CUDA on an NCCL failure). */
+int hlm_nccl_reduce_scatter_f32(void* comm, const float* send, float* recv, int64_t count, void* stream);
+int hlm_nccl_all_gather_bf16(void* comm, const void* send, void* recv, int64_t count, void* stream);
+int hlm_nccl_allreduce_f32(void* comm, const float* send, float* recv, int64_t count, void* stream);
 
 int hlm_make_copy_task_batch(const HlmModelConfig* cfg, uint64_t data_seed, int64_t skip, int32_t* tokens);
 /* run_training (trainer.hpp): store from seed, data seed+1, `steps` steps;

@@ -238,6 +238,33 @@ void hlm_nccl_comm_destroy(void* comm) {
     if (comm) hlm::nccl().CommDestroy(static_cast<ncclComm_t>(comm));
 }
 
+int hlm_nccl_reduce_scatter_f32(void* comm, const float* send, float* recv, int64_t count, void* stream) {
+    return guarded([&] {
+        if (!comm || count < 0) throw std::invalid_argument("reduce-scatter: communicator and count >= 0 required");
+        hlm::nccl_check(hlm::nccl().ReduceScatter(send, recv, static_cast<size_t>(count), ncclFloat32, ncclSum,
+                                                  static_cast<ncclComm_t>(comm), static_cast<cudaStream_t>(stream)),
+                        "ncclReduceScatter");
+    });
+}
+
+int hlm_nccl_all_gather_bf16(void* comm, const void* send, void* recv, int64_t count, void* stream) {
+    return guarded([&] {
+        if (!comm || count < 0) throw std::invalid_argument("all-gather: communicator and count >= 0 required");
+        hlm::nccl_check(hlm::nccl().AllGather(send, recv, static_cast<size_t>(count), ncclBfloat16,
+                                              static_cast<ncclComm_t>(comm), static_cast<cudaStream_t>(stream)),
+                        "ncclAllGather");
+    });
+}
+
+int hlm_nccl_allreduce_f32(void* comm, const float* send, float* recv, int64_t count, void* stream) {
+    return guarded([&] {
+        if (!comm || count < 0) throw std::invalid_argument("all-reduce: communicator and count >= 0 required");
+        hlm::nccl_check(hlm::nccl().AllReduce(send, recv, static_cast<size_t>(count), ncclFloat32, ncclSum,
+                                              static_cast<ncclComm_t>(comm), static_cast<cudaStream_t>(stream)),
+                        "ncclAllReduce");
+    });
+}
+
 void hlm_store_destroy(HlmStore* s) { delete s; }
 
 int64_t hlm_store_total_params(const HlmStore* s) { return s ? s->s->total_params() : -1; }

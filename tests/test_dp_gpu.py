@@ -83,3 +83,30 @@ def test_dp_two_gpus_matches_global_batch():
     assert np.allclose(l_dp, l_ref, rtol=1e-4)
     w = np.load(os.path.join(out, "w.npy"))
     assert np.linalg.norm(w - ref.weights()) / np.linalg.norm(ref.weights()) < 1e-3
+
+
+def test_collective_entry_points_world1():
+    """hlm_nccl_reduce_scatter_f32 / all_gather_bf16 / allreduce_f32 on a
+    world-1 communicator: identity exchanges, bit for bit, stream-ordered."""
+    import ctypes
+
+    import torch
+    from paper_2602_04816_b200 import _lib
+    lib = _lib.lib()
+    for fn in ("hlm_nccl_reduce_scatter_f32", "hlm_nccl_all_gather_bf16", "hlm_nccl_allreduce_f32"):
+        getattr(lib, fn).argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int64, ctypes.c_void_p]
+    comm = E.nccl_comm(E.nccl_unique_id(), 1, 0)
+    x = torch.randn(1 << 20, device="cuda")
+    y = torch.empty_like(x)
+    _lib.check(lib.hlm_nccl_reduce_scatter_f32(comm, x.data_ptr(), y.data_ptr(), x.numel(), None))
+    torch.cuda.synchronize()
+    assert torch.equal(x, y)
+    b = torch.randn(4096, device="cuda").bfloat16()
+    bo = torch.empty_like(b)
+    _lib.check(lib.hlm_nccl_all_gather_bf16(comm, b.data_ptr(), bo.data_ptr(), b.numel(), None))
+    z = torch.empty_like(x)
+    _lib.check(lib.hlm_nccl_allreduce_f32(comm, x.data_ptr(), z.data_ptr(), x.numel(), None))
+    torch.cuda.synchronize()
+    assert torch.equal(b, bo) and torch.equal(x, z)
+    lib.hlm_nccl_comm_destroy.argtypes = [ctypes.c_void_p]
+    lib.hlm_nccl_comm_destroy(comm)
