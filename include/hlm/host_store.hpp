@@ -178,7 +178,9 @@ public:
     // HBM-resident tiles back. save_checkpoint / load_checkpoint / export / import call
     // quiesce() first, so a file never mixes tiles from two steps and a load is never
     // overwritten by a late tail update.
-    void set_quiesce(std::function<void()> hook, const void* owner) {
+    // strict: mid-step calls are a ProtocolError (save / load / import); a non-strict read
+    // (export) during a step just sees the store as it is.
+    void set_quiesce(std::function<void(bool strict)> hook, const void* owner) {
         std::lock_guard<std::mutex> lk(quiesce_mu_);
         quiesce_ = std::move(hook);
         quiesce_owner_ = owner;
@@ -190,13 +192,13 @@ public:
             quiesce_owner_ = nullptr;
         }
     }
-    void quiesce() const {
-        std::function<void()> f;
+    void quiesce(bool strict = true) const {
+        std::function<void(bool)> f;
         {
             std::lock_guard<std::mutex> lk(quiesce_mu_);
             f = quiesce_;
         }
-        if (f) f();
+        if (f) f(strict);
     }
     // Bumped whenever the store's state is replaced from outside (load_checkpoint,
     // import_master): an engine holding HBM-resident tiles re-uploads them.
@@ -238,7 +240,7 @@ private:
     std::atomic<int> device_newer_{0};
     std::atomic<i64> epoch_{0};
     mutable std::mutex quiesce_mu_;
-    std::function<void()> quiesce_;
+    std::function<void(bool)> quiesce_;
     const void* quiesce_owner_ = nullptr;
 };
 

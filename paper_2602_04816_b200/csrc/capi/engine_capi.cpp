@@ -273,7 +273,7 @@ int64_t hlm_store_adam_steps(const HlmStore* s) { return s ? s->s->adam_steps() 
 int hlm_store_export(const HlmStore* s, int field, float* out) {
     return guarded([&] {
         const hlm::MasterStore& st = *s->s;
-        st.quiesce();   // an attached engine's optimizer tail / resident tiles land first
+        st.quiesce(false);   // an attached engine's optimizer tail / resident tiles land first
         for (hlm::i64 p = 0; p < st.physical_tiles(); ++p) {
             const hlm::LayerTile& t = st.physical(p);
             const size_t n = static_cast<size_t>(t.n_params());

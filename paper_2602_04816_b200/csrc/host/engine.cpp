@@ -279,9 +279,11 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
     }
     if (opts_.threaded_accum) worker_ = std::thread([this] { worker_loop(); });
     store_.set_quiesce(
-        [this] {
-            if (phase_ != Phase::Idle)
-                throw ProtocolError("the store was saved / loaded while its engine is inside a step");
+        [this](bool strict) {
+            if (phase_ != Phase::Idle) {
+                if (strict) throw ProtocolError("the store was saved / loaded while its engine is inside a step");
+                return;
+            }
             sync();
         },
         this);
