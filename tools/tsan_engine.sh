@@ -14,9 +14,11 @@ g++ -std=c++17 -O1 -g -fsanitize=thread -Iinclude tests/cxx/integration_caller.c
 mkdir -p gpurun_out
 export TSAN_OPTIONS="suppressions=$PWD/tools/tsan.supp halt_on_error=0 second_deadlock_stack=1"
 rc=0
+i=0
 for mode in "train 4 256 1024 1024 128 4 1 2 4" "train 6 64 128 96 64 2 2 2 5" "phases 4 256 1024 1024 128 4 1 2" \
             "errors" "arena" "ledger 4 256 1024 1024 128 4 2 2"; do
-    tag=$(echo "$mode" | cut -d' ' -f1)
+    i=$((i + 1))
+    tag="${i}_$(echo "$mode" | cut -d' ' -f1)"
     ./tools/integration_caller_tsan $mode > gpurun_out/tsan_${tag}.log 2>&1 || rc=1
     echo "$mode: exit $? warnings $(grep -c 'WARNING: ThreadSanitizer' gpurun_out/tsan_${tag}.log)"
 done
