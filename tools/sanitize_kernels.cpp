@@ -187,7 +187,7 @@ int main(int argc, char** argv) {
     for (int a = 0; a < 2; ++a)
         for (int b = 0; b < 2; ++b) gemm(128, 256, 128, a, b, HLM_EPI_F32);
     gemm(512, 512, 256, 0, 1, HLM_EPI_BF16);
-    gemm(520, 300, 200, 1, 1, HLM_EPI_F32);
+    gemm(520, 296, 200, 1, 1, HLM_EPI_F32);   // ragged M / N edges (ld multiple of 8 for TMA)
     gemm(512, 512, 256, 0, 1, HLM_EPI_F32_ADD);
     gemm(256, 384, 512, 0, 1, HLM_EPI_BF16, 3, 0);     // N-grouped (qkv)
     gemm(256, 256, 384, 0, 0, HLM_EPI_F32, 2, 1);      // K-grouped (dgrad up|gate)
