@@ -4,6 +4,7 @@
 // proj/tests/test_engine.cpp phase-API tests). INTEGRATION.md §1 quotes it.
 //
 //   integration_caller train  L h f V S B K heads steps   -> one "loss <hex> <value>" line per step
+//   integration_caller trainx ...                          -> the same with bench.py's scheduling features
 //   integration_caller phases L h f V S B K heads          -> loss of one step via the phase API
 //   integration_caller errors                              -> exercises the exception mapping
 //   integration_caller arena                               -> DeviceArena / ledger contract
@@ -41,7 +42,7 @@ void print_loss(double loss) {
     std::printf("loss %016" PRIx64 " %.9g\n", bits, loss);
 }
 
-int train(char** a) {
+int train(char** a, bool bench_features = false) {
     hlm::RunConfig cfg;
     cfg.model = config_from(a);
     cfg.model.validate();
@@ -52,9 +53,21 @@ int train(char** a) {
     cfg.run.n_slab = 3;
     cfg.hyper.lr = 3e-3;
     auto store = hlm::build_store(cfg.model, cfg.run.seed, hlm::Dtype::BF16, hlm::InitMode::Reference);
-    hlm::DeviceArena arena(cfg.model);
+    hlm::EngineOptions opts;   // `trainx`: bench.py's feature set (every host thread hand-off)
+    hlm::i64 cache = 0;
+    if (bench_features) {
+        opts.overlap_optimizer_tail = true;
+        opts.tail_blocks = 2;
+        opts.piece_elems = 4096;
+        opts.grad_buffers = 4;
+        opts.sparse_embed_grad = true;
+        opts.embed_gather_host = true;
+        opts.head_piece_vocab = 128;
+        cache = 2 * (2 * cfg.model.block_params() + 255) / 256 * 256;
+    }
+    hlm::DeviceArena arena(cfg.model, std::nullopt, -1, cache);
     const hlm::TrainOutput out =
-        hlm::run_training(cfg, *store, arena, [](const hlm::StepTelemetry& t) { print_loss(t.loss); });
+        hlm::run_training(cfg, *store, arena, [](const hlm::StepTelemetry& t) { print_loss(t.loss); }, opts);
     std::printf("h2d %" PRId64 " d2h %" PRId64 " steps %" PRId64 "\n", out.steps.back().h2d_bytes,
                 out.steps.back().d2h_bytes, store->adam_steps());
     return 0;
@@ -228,11 +241,12 @@ int main(int argc, char** argv) {
     try {
         const std::string mode = argc > 1 ? argv[1] : "";
         if (mode == "train" && argc == 11) return train(argv + 2);
+        if (mode == "trainx" && argc == 11) return train(argv + 2, true);
         if (mode == "phases" && argc == 10) return phases(argv + 2);
         if (mode == "errors") return errors();
         if (mode == "arena") return arena();
         if (mode == "ledger" && argc == 10) return ledger(argv + 2);
-        std::fprintf(stderr, "usage: %s train L h f V S B K heads steps | phases L h f V S B K heads | errors | arena | ledger L h f V S B K heads\n",
+        std::fprintf(stderr, "usage: %s train|trainx L h f V S B K heads steps | phases L h f V S B K heads | errors | arena | ledger L h f V S B K heads\n",
                      argv[0]);
         return 64;
     } catch (const std::invalid_argument& e) {

@@ -111,6 +111,14 @@ def test_cxx_caller_trains_bitwise_like_the_c_abi(caller):
     n, Vh = c.block_params(), c.vocab * c.hidden
     assert int(tail[1]) == 2 * (2 * 4 * n + 2 * Vh) and int(tail[3]) == 4 * (4 * n + 2 * Vh)
     assert int(tail[5]) == 3
+    # bench.py's scheduling features (overlapped tail, pieces, sparse embedding, vocab-chunked
+    # head, weight cache) leave the numerics unchanged: the same losses bit for bit, except the
+    # head chunking's d_x summation order (<= 2e-4), so compare the first step bitwise
+    rx = subprocess.run([caller, "trainx", *_c1(), "3"], capture_output=True, text=True, timeout=600)
+    assert rx.returncode == 0, rx.stderr
+    bx = [int(ln.split()[1], 16) for ln in rx.stdout.splitlines() if ln.startswith("loss")]
+    lx = [float(ln.split()[2]) for ln in rx.stdout.splitlines() if ln.startswith("loss")]
+    assert bx[0] == bits[0] and np.allclose(lx, losses, rtol=1e-5)
 
 
 @pytest.mark.gpu

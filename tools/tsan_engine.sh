@@ -15,7 +15,7 @@ mkdir -p gpurun_out
 export TSAN_OPTIONS="suppressions=$PWD/tools/tsan.supp halt_on_error=0 second_deadlock_stack=1"
 rc=0
 i=0
-for mode in "train 4 256 1024 1024 128 4 1 2 4" "train 6 64 128 96 64 2 2 2 5" "phases 4 256 1024 1024 128 4 1 2" \
+for mode in "train 4 256 1024 1024 128 4 1 2 4" "train 6 64 128 96 64 2 2 2 5" "trainx 4 256 1024 1024 128 4 1 2 4" "phases 4 256 1024 1024 128 4 1 2" \
             "errors" "arena" "ledger 4 256 1024 1024 128 4 2 2"; do
     i=$((i + 1))
     tag="${i}_$(echo "$mode" | cut -d' ' -f1)"
