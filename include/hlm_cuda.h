@@ -63,8 +63,29 @@ long long hlm_cuda_launch_count(void);
  * Groups (G >= 1): operand g lives at base + g*gstride when *_grouped.
  *   kgroup == 0: one output per group at C + g*c_gstride
  *   kgroup == 1: single output, C = sum_g A[g] . B[g]
- * Epilogues: BF16 store, FP32 store, FP32 store of R + acc (R may alias C). */
-enum HlmEpilogue { HLM_EPI_BF16 = 0, HLM_EPI_F32 = 1, HLM_EPI_F32_ADD = 2 };
+ * Epilogues: BF16 store, FP32 store, FP32 store of R + acc (R may alias C).
+ * Fused epilogues (the block's elementwise steps done on the accumulator, never
+ * re-reading an intermediate from HBM; bit-identical to the separate kernels):
+ *   HLM_EPI_BF16_ROPE  N-grouped q|k|v projection: BF16 store, with groups 0 and 1
+ *                      (q, k) rotated by RoPE (rotate-half, tables rope_cos / rope_sin
+ *                      [rope_seq][head_dim/2], position = row % rope_seq); head_dim
+ *                      64 / 128 / 256. Replaces the GEMM + hlm rope pass.
+ *   HLM_EPI_SWIGLU     up|gate projection with G = 2 (B groups w_up, w_gate; B MN-major):
+ *                      each tile computes the same output columns of up and gate, stores
+ *                      both BF16 (C, C + c_gstride) and act = up * silu(gate) BF16 to C2
+ *                      (ldc2). Replaces the GEMM + swiglu_fwd.
+ *   HLM_EPI_SWIGLU_BWD d_act = dY . W_down^T rounded to BF16, then with up / gate read
+ *                      from aux (aux_ld, gate at aux + aux_gstride): d_up -> C,
+ *                      d_gate -> C + c_gstride (BF16). Replaces the BF16 d_act store +
+ *                      swiglu_bwd. */
+enum HlmEpilogue {
+  HLM_EPI_BF16 = 0,
+  HLM_EPI_F32 = 1,
+  HLM_EPI_F32_ADD = 2,
+  HLM_EPI_BF16_ROPE = 3,
+  HLM_EPI_SWIGLU = 4,
+  HLM_EPI_SWIGLU_BWD = 5
+};
 
 typedef struct HlmGemmDesc {
   int M, N, K, G;
@@ -80,6 +101,14 @@ typedef struct HlmGemmDesc {
   long long ldc, c_gstride;
   const float* R;
   long long ldr, r_gstride;
+  /* fused epilogues (appended; zero for the plain ones) */
+  const float* rope_cos;
+  const float* rope_sin;
+  int rope_seq, rope_head_dim;
+  const void* aux;
+  long long aux_ld, aux_gstride;
+  void* C2;
+  long long ldc2;
 } HlmGemmDesc;
 
 int hlm_cuda_gemm(const HlmGemmDesc* desc, void* stream);
@@ -105,7 +134,9 @@ typedef struct HlmBlockDims {
 } HlmBlockDims;
 
 enum HlmBlockFlags {
-  HLM_BLOCK_GENERIC_ATTENTION = 1 /* force the any-head_dim CUDA-core attention */
+  HLM_BLOCK_GENERIC_ATTENTION = 1, /* force the any-head_dim CUDA-core attention */
+  HLM_BLOCK_UNFUSED = 2            /* separate RoPE / SwiGLU kernels instead of the fused GEMM
+                                      epilogues (bit-identical; A/B and tests) */
 };
 
 size_t hlm_cuda_block_acts_bytes(const HlmBlockDims* d);

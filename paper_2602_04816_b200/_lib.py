@@ -33,10 +33,14 @@ class HlmGemmDesc(ctypes.Structure):
         ("B", ctypes.c_void_p), ("ldb", ctypes.c_longlong), ("b_gstride", ctypes.c_longlong),
         ("C", ctypes.c_void_p), ("ldc", ctypes.c_longlong), ("c_gstride", ctypes.c_longlong),
         ("R", ctypes.c_void_p), ("ldr", ctypes.c_longlong), ("r_gstride", ctypes.c_longlong),
+        ("rope_cos", ctypes.c_void_p), ("rope_sin", ctypes.c_void_p),
+        ("rope_seq", ctypes.c_int), ("rope_head_dim", ctypes.c_int),
+        ("aux", ctypes.c_void_p), ("aux_ld", ctypes.c_longlong), ("aux_gstride", ctypes.c_longlong),
+        ("C2", ctypes.c_void_p), ("ldc2", ctypes.c_longlong),
     ]
 
 
-EPI_BF16, EPI_F32, EPI_F32_ADD = 0, 1, 2
+EPI_BF16, EPI_F32, EPI_F32_ADD, EPI_BF16_ROPE, EPI_SWIGLU, EPI_SWIGLU_BWD = 0, 1, 2, 3, 4, 5
 
 
 def lib():
@@ -69,6 +73,7 @@ class HlmBlockDims(ctypes.Structure):
 
 
 BLOCK_GENERIC_ATTENTION = 1
+BLOCK_UNFUSED = 2
 _vp = ctypes.c_void_p
 
 

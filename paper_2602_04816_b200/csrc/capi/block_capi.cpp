@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -137,6 +138,17 @@ void timed(int kind, double bytes, cudaStream_t s, F&& launch) {
   hlm_capi::ktimer_end(tk, s, kind, bytes);
 }
 
+// Fused GEMM epilogues (RoPE, SwiGLU fwd / bwd) unless the caller asks for the separate
+// kernels (HLM_BLOCK_UNFUSED) or HLM_FUSE=0 is set for an A/B run.
+bool fused(const HlmBlockDims& d) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = std::getenv("HLM_FUSE");
+    env = (e && *e == '0') ? 0 : 1;
+  }
+  return env && !(d.flags & HLM_BLOCK_UNFUSED);
+}
+
 void validate(const HlmBlockDims* d) {
   if (!d || d->batch <= 0 || d->seq <= 0 || d->hidden <= 0 || d->ffn <= 0 || d->n_heads <= 0)
     throw Failure{"block dims must be positive", HLM_ERR_CONFIG};
@@ -229,16 +241,26 @@ int hlm_cuda_block_fwd(const HlmBlockDims* d, const void* w_tile, const float* h
     const uint16_t* W = static_cast<const uint16_t*>(w_tile);
     BlockActs a = carve_acts(*d, acts, nullptr);
 
+    const bool fuse = fused(*d);
+    const int hd = (int)(h / d->n_heads);
+    const bool rope_fused = fuse && rope_cos && (hd == 64 || hd == 128 || hd == 256) && h % 32 == 0;
     timed(HLM_KTIMER_RMSNORM_FWD, 6.0 * T * h, s, [&] { chk(hlm_ops_rmsnorm_fwd(h_in, W + off.norm1, a.n1, T, hi, s), "rmsnorm1"); });
     HlmGemmDesc g = gdesc(Ti, hi, hi, a.n1, h, 0, W + off.q, h, 1, a.qkv, h, HLM_EPI_BF16);
     g.G = 3;
     g.b_grouped = 1;
     g.b_gstride = h * h;
     g.c_gstride = T * h;
+    if (rope_fused) {   // RoPE of q and k in the projection's epilogue
+      g.epi = HLM_EPI_BF16_ROPE;
+      g.rope_cos = rope_cos;
+      g.rope_sin = rope_sin;
+      g.rope_seq = (int)d->seq;
+      g.rope_head_dim = hd;
+    }
     chk_gemm(g, s, "qkv");
-    if (rope_cos)
+    if (rope_cos && !rope_fused)
       timed(HLM_KTIMER_ROPE, 8.0 * T * h, s, [&] {
-        chk(hlm_ops_rope(a.qkv, rope_cos, rope_sin, T, hi, hi / d->n_heads, (int)d->seq, 0, 2, T * h, s), "rope");
+        chk(hlm_ops_rope(a.qkv, rope_cos, rope_sin, T, hi, hd, (int)d->seq, 0, 2, T * h, s), "rope");
       });
     attention_fwd(*d, a.qkv, a.qkv + T * h, a.qkv + 2 * T * h, a.o, a.lse, h, s);
     g = gdesc(Ti, hi, hi, a.o, h, 0, W + off.o, h, 1, a.y, h, HLM_EPI_F32_ADD);
@@ -251,8 +273,14 @@ int hlm_cuda_block_fwd(const HlmBlockDims* d, const void* w_tile, const float* h
     g.b_grouped = 1;
     g.b_gstride = h * f;
     g.c_gstride = T * f;
+    if (fuse) {   // act = up * silu(gate) in the epilogue of paired up|gate tiles
+      g.epi = HLM_EPI_SWIGLU;
+      g.C2 = a.act;
+      g.ldc2 = f;
+    }
     chk_gemm(g, s, "up|gate");
-    timed(HLM_KTIMER_SWIGLU_FWD, 6.0 * T * f, s, [&] { chk(hlm_ops_swiglu_fwd(a.ug, a.act, T * f, s), "swiglu"); });
+    if (!fuse)
+      timed(HLM_KTIMER_SWIGLU_FWD, 6.0 * T * f, s, [&] { chk(hlm_ops_swiglu_fwd(a.ug, a.act, T * f, s), "swiglu"); });
     g = gdesc(Ti, hi, fi, a.act, f, 0, W + off.down, h, 1, h_out, h, HLM_EPI_F32_ADD);
     g.R = a.y;
     g.ldr = h;
@@ -277,8 +305,17 @@ int hlm_cuda_block_bwd(const HlmBlockDims* d, const void* w_tile, const float* h
     // MLP branch
     timed(HLM_KTIMER_CAST, 6.0 * T * h, s, [&] { chk(hlm_ops_cast_bf16(g_out, w.g_bf, T * h, s), "cast g_out"); });
     chk_gemm(gdesc(fi, hi, Ti, a.act, f, 1, w.g_bf, h, 1, G + off.down, h, HLM_EPI_F32), s, "wgrad down");
-    chk_gemm(gdesc(Ti, fi, hi, w.g_bf, h, 0, W + off.down, h, 0, w.d_act, f, HLM_EPI_BF16), s, "dgrad down");
-    timed(HLM_KTIMER_SWIGLU_BWD, 10.0 * T * f, s, [&] { chk(hlm_ops_swiglu_bwd(w.d_act, a.ug, w.dug, T * f, s), "swiglu bwd"); });
+    if (fused(*d)) {   // d_act never stored: the SwiGLU backward runs in the dgrad epilogue
+      HlmGemmDesc gd = gdesc(Ti, fi, hi, w.g_bf, h, 0, W + off.down, h, 0, w.dug, f, HLM_EPI_SWIGLU_BWD);
+      gd.c_gstride = T * f;
+      gd.aux = a.ug;
+      gd.aux_ld = f;
+      gd.aux_gstride = T * f;
+      chk_gemm(gd, s, "dgrad down + swiglu bwd");
+    } else {
+      chk_gemm(gdesc(Ti, fi, hi, w.g_bf, h, 0, W + off.down, h, 0, w.d_act, f, HLM_EPI_BF16), s, "dgrad down");
+      timed(HLM_KTIMER_SWIGLU_BWD, 10.0 * T * f, s, [&] { chk(hlm_ops_swiglu_bwd(w.d_act, a.ug, w.dug, T * f, s), "swiglu bwd"); });
+    }
     HlmGemmDesc g = gdesc(hi, fi, Ti, a.n2, h, 1, w.dug, f, 1, G + off.up, f, HLM_EPI_F32);
     g.G = 2;
     g.b_grouped = 1;

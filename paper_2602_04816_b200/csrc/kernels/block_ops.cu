@@ -16,6 +16,7 @@
 #include <cstdlib>
 
 #include "block_ops.h"
+#include "fused_math.cuh"
 #include "hlm_cuda.h"
 
 namespace {
@@ -352,7 +353,6 @@ __global__ void cast_f32_bf16_kernel(const float* __restrict__ in, __nv_bfloat16
 }
 
 // ------------------------------------------------------------------ SwiGLU
-__device__ __forceinline__ float silu_f(float z) { return z * (1.0f / (1.0f + __expf(-z))); }
 
 // act = up * silu(gate) ; ug = [2][rows][f] (up then gate)
 __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ ug, __nv_bfloat16* __restrict__ act,
@@ -371,11 +371,11 @@ __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ ug, __nv_bfl
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const float2 uf = __bfloat1622float2(u2[k]), gf = __bfloat1622float2(g2[k]);
-        o2[k] = __floats2bfloat162_rn(uf.x * silu_f(gf.x), uf.y * silu_f(gf.y));
+        o2[k] = __floats2bfloat162_rn(hlm_fused::swiglu(uf.x, gf.x), hlm_fused::swiglu(uf.y, gf.y));
       }
       *reinterpret_cast<uint4*>(act + i) = o;
     } else {
-      for (long long k = i; k < n; ++k) act[k] = __float2bfloat16_rn(bf(up[k]) * silu_f(bf(gate[k])));
+      for (long long k = i; k < n; ++k) act[k] = __float2bfloat16_rn(hlm_fused::swiglu(bf(up[k]), bf(gate[k])));
     }
   }
 }
@@ -398,19 +398,20 @@ __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ dact, const 
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const float2 da = __bfloat1622float2(d2[k]), u = __bfloat1622float2(u2[k]), z = __bfloat1622float2(z2[k]);
-        const float sx = 1.0f / (1.0f + __expf(-z.x)), sy = 1.0f / (1.0f + __expf(-z.y));
-        ou2[k] = __floats2bfloat162_rn(da.x * z.x * sx, da.y * z.y * sy);
-        og2[k] = __floats2bfloat162_rn(da.x * u.x * (sx * (1.0f + z.x * (1.0f - sx))),
-                                       da.y * u.y * (sy * (1.0f + z.y * (1.0f - sy))));
+        float dux, duy, dgx, dgy;
+        hlm_fused::swiglu_bwd(da.x, u.x, z.x, dux, dgx);
+        hlm_fused::swiglu_bwd(da.y, u.y, z.y, duy, dgy);
+        ou2[k] = __floats2bfloat162_rn(dux, duy);
+        og2[k] = __floats2bfloat162_rn(dgx, dgy);
       }
       *reinterpret_cast<uint4*>(dug + i) = ou;
       *reinterpret_cast<uint4*>(dug + n + i) = og;
     } else {
       for (long long k = i; k < n; ++k) {
-        const float da = bf(dact[k]), u = bf(ug[k]), z = bf(ug[n + k]);
-        const float sg = 1.0f / (1.0f + __expf(-z));
-        dug[k] = __float2bfloat16_rn(da * z * sg);
-        dug[n + k] = __float2bfloat16_rn(da * u * (sg * (1.0f + z * (1.0f - sg))));
+        float du, dg;
+        hlm_fused::swiglu_bwd(bf(dact[k]), bf(ug[k]), bf(ug[n + k]), du, dg);
+        dug[k] = __float2bfloat16_rn(du);
+        dug[n + k] = __float2bfloat16_rn(dg);
       }
     }
   }
@@ -434,14 +435,10 @@ __global__ void rope_kernel(__nv_bfloat16* __restrict__ x, const float* __restri
     const int pos = (int)(r % S);
     __nv_bfloat16* v = x + m * mat_stride + r * h + head * hd;
     const float c = cs[pos * half + i], s = sn[pos * half + i];
-    const float a = bf(v[i]), b = bf(v[i + half]);
-    if (!inverse) {
-      v[i] = __float2bfloat16_rn(a * c - b * s);
-      v[i + half] = __float2bfloat16_rn(b * c + a * s);
-    } else {
-      v[i] = __float2bfloat16_rn(a * c + b * s);
-      v[i + half] = __float2bfloat16_rn(b * c - a * s);
-    }
+    float oa, ob;
+    hlm_fused::rope_rotate(bf(v[i]), bf(v[i + half]), c, s, inverse != 0, oa, ob);
+    v[i] = __float2bfloat16_rn(oa);
+    v[i + half] = __float2bfloat16_rn(ob);
   }
 }
 
@@ -472,13 +469,14 @@ __global__ void rope8_kernel(__nv_bfloat16* __restrict__ x, const float* __restr
     const float sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
     __nv_bfloat162* a2 = reinterpret_cast<__nv_bfloat162*>(&ua);
     __nv_bfloat162* b2 = reinterpret_cast<__nv_bfloat162*>(&ub);
-    const float sg = inverse ? -1.0f : 1.0f;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const float2 a = __bfloat1622float2(a2[q]), b = __bfloat1622float2(b2[q]);
-      const float cx = c[2 * q], cy = c[2 * q + 1], sx = sg * sv[2 * q], sy = sg * sv[2 * q + 1];
-      a2[q] = __floats2bfloat162_rn(a.x * cx - b.x * sx, a.y * cy - b.y * sy);
-      b2[q] = __floats2bfloat162_rn(b.x * cx + a.x * sx, b.y * cy + a.y * sy);
+      float oax, obx, oay, oby;
+      hlm_fused::rope_rotate(a.x, b.x, c[2 * q], sv[2 * q], inverse != 0, oax, obx);
+      hlm_fused::rope_rotate(a.y, b.y, c[2 * q + 1], sv[2 * q + 1], inverse != 0, oay, oby);
+      a2[q] = __floats2bfloat162_rn(oax, oay);
+      b2[q] = __floats2bfloat162_rn(obx, oby);
     }
     *reinterpret_cast<uint4*>(v) = ua;
     *reinterpret_cast<uint4*>(v + half) = ub;

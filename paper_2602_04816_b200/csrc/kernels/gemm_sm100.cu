@@ -28,6 +28,7 @@
 #include "gemm.h"
 #include "sm100_ptx.cuh"
 #include "block_ops.h"
+#include "fused_math.cuh"
 
 using namespace hlm_sm100;
 
@@ -51,6 +52,15 @@ struct KArgs {
   const float* R;
   long long ldr, r_gstride;
   int epi;
+  // fused epilogues (HLM_EPI_BF16_ROPE / SWIGLU / SWIGLU_BWD, include/hlm_cuda.h)
+  int paired;            // SWIGLU: B atoms of groups 0 | 1 for the same output columns
+  const float* rope_cos;
+  const float* rope_sin;
+  int rope_seq, rope_hd;
+  const __nv_bfloat16* aux;
+  long long aux_ld, aux_gstride;
+  __nv_bfloat16* C2;
+  long long ldc2;
 };
 
 __device__ __forceinline__ void tile_coords(const KArgs& a, int t, int& g, int& m, int& n) {
@@ -67,7 +77,7 @@ __device__ __forceinline__ void tile_coords(const KArgs& a, int t, int& g, int& 
 }
 
 // TMEM accumulator row (32x32b loads, 8 chunks of 32 columns) -> global C.
-__device__ __forceinline__ void epilogue_store(const KArgs& args, uint32_t taddr, int row, int tg, int col_base) {
+__device__ __forceinline__ void epilogue_plain(const KArgs& args, uint32_t taddr, int row, int tg, int col_base) {
   const bool row_ok = row < args.M;
   const long long c_off = (long long)tg * args.c_gstride + (long long)row * args.ldc;
   const long long r_off = (long long)tg * args.r_gstride + (long long)row * args.ldr;
@@ -123,6 +133,149 @@ __device__ __forceinline__ void epilogue_store(const KArgs& args, uint32_t taddr
         }
       }
     }
+}
+
+// 32 consecutive bf16 values of one row (16-byte stores when the chunk is whole and aligned).
+__device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float (&v)[32], int valid) {
+  if (valid == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      d4[j] = make_uint4(pack_bf16x2(v[8 * j + 0], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                         pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < valid) dst[j] = __float2bfloat16_rn(v[j]);
+  }
+}
+
+__device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* src, float (&v)[32], int valid) {
+  if (valid == 32 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint4 q = s4[j];
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        v[8 * j + 2 * e] = __uint_as_float(w[e] << 16);
+        v[8 * j + 2 * e + 1] = __uint_as_float(w[e] & 0xFFFF0000u);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = j < valid ? __bfloat162float(src[j]) : 0.0f;
+  }
+}
+
+// q|k|v projection + RoPE: groups 0 (q) and 1 (k) are rotated in registers before the
+// BF16 store (rotate-half pairs (i, i + hd/2) of a head sit in chunks c and c + hd/64 of
+// the same thread's row); group 2 (v) is a plain BF16 store. Same rounding points as
+// the GEMM's BF16 epilogue followed by the in-place rope pass.
+__device__ __forceinline__ void epilogue_rope(const KArgs& args, uint32_t taddr, int row, int tg, int col_base) {
+  if (tg >= 2) {
+    epilogue_plain(args, taddr, row, tg, col_base);
+    return;
+  }
+  const int hd = args.rope_hd, half = hd >> 1, dist = half >> 5;
+  const bool row_ok = row < args.M;
+  const int pos = row_ok ? row % args.rope_seq : 0;
+  __nv_bfloat16* crow = reinterpret_cast<__nv_bfloat16*>(args.C) + (long long)tg * args.c_gstride +
+                        (long long)row * args.ldc;
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    const int w = (c * 32) & (hd - 1);
+    if (w >= half) continue;   // second half of a head: rotated together with chunk c - dist
+    uint32_t ra[32], rb[32];
+    tmem_ld_32x32(taddr + c * 32, ra);
+    tmem_ld_32x32(taddr + (c + dist) * 32, rb);
+    tmem_ld_wait();
+    const int col0 = col_base + c * 32;
+    if (!row_ok || col0 >= args.N) continue;
+    const float4* cp = reinterpret_cast<const float4*>(args.rope_cos + (long long)pos * half + w);
+    const float4* sp = reinterpret_cast<const float4*>(args.rope_sin + (long long)pos * half + w);
+    float oa[32], ob[32];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 c4 = cp[q], s4 = sp[q];
+      const float cv[4] = {c4.x, c4.y, c4.z, c4.w}, sv[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int j = 4 * q + e;
+        hlm_fused::rope_rotate(hlm_fused::round_bf16(__uint_as_float(ra[j])),
+                               hlm_fused::round_bf16(__uint_as_float(rb[j])), cv[e], sv[e], false, oa[j], ob[j]);
+      }
+    }
+    store_bf16x32(crow + col0, oa, 32);
+    store_bf16x32(crow + col0 + half, ob, 32);
+  }
+}
+
+// up|gate projection (paired tile: TMEM columns 0..127 = up, 128..255 = gate of the same
+// 128 output columns): up, gate rounded to BF16 and stored for the backward, and
+// act = up * silu(gate) from the rounded values — the swiglu_fwd kernel's arithmetic.
+__device__ __forceinline__ void epilogue_swiglu(const KArgs& args, uint32_t taddr, int row, int col_base) {
+  const bool row_ok = row < args.M;
+  __nv_bfloat16* up_row = reinterpret_cast<__nv_bfloat16*>(args.C) + (long long)row * args.ldc;
+  __nv_bfloat16* gate_row = up_row + args.c_gstride;
+  __nv_bfloat16* act_row = args.C2 + (long long)row * args.ldc2;
+#pragma unroll 1
+  for (int c = 0; c < BN / 64; ++c) {
+    uint32_t ru[32], rg[32];
+    tmem_ld_32x32(taddr + c * 32, ru);
+    tmem_ld_32x32(taddr + BN / 2 + c * 32, rg);
+    tmem_ld_wait();
+    const int col0 = col_base + c * 32;
+    if (!row_ok || col0 >= args.N) continue;
+    const int valid = min(32, args.N - col0);
+    float u[32], z[32], a[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      u[j] = hlm_fused::round_bf16(__uint_as_float(ru[j]));
+      z[j] = hlm_fused::round_bf16(__uint_as_float(rg[j]));
+      a[j] = hlm_fused::swiglu(u[j], z[j]);
+    }
+    store_bf16x32(up_row + col0, u, valid);
+    store_bf16x32(gate_row + col0, z, valid);
+    store_bf16x32(act_row + col0, a, valid);
+  }
+}
+
+// down-projection dgrad: d_act rounded to BF16 (the plain epilogue's value), then the
+// swiglu_bwd kernel's arithmetic against up / gate read from aux.
+__device__ __forceinline__ void epilogue_swiglu_bwd(const KArgs& args, uint32_t taddr, int row, int col_base) {
+  const bool row_ok = row < args.M;
+  __nv_bfloat16* du_row = reinterpret_cast<__nv_bfloat16*>(args.C) + (long long)row * args.ldc;
+  __nv_bfloat16* dg_row = du_row + args.c_gstride;
+  const __nv_bfloat16* up_row = args.aux + (long long)row * args.aux_ld;
+  const __nv_bfloat16* gate_row = up_row + args.aux_gstride;
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    uint32_t rd[32];
+    tmem_ld_32x32(taddr + c * 32, rd);
+    tmem_ld_wait();
+    const int col0 = col_base + c * 32;
+    if (!row_ok || col0 >= args.N) continue;
+    const int valid = min(32, args.N - col0);
+    float u[32], z[32], du[32], dg[32];
+    load_bf16x32(up_row + col0, u, valid);
+    load_bf16x32(gate_row + col0, z, valid);
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      hlm_fused::swiglu_bwd(hlm_fused::round_bf16(__uint_as_float(rd[j])), u[j], z[j], du[j], dg[j]);
+    store_bf16x32(du_row + col0, du, valid);
+    store_bf16x32(dg_row + col0, dg, valid);
+  }
+}
+
+__device__ __forceinline__ void epilogue_store(const KArgs& args, uint32_t taddr, int row, int tg, int tn) {
+  switch (args.epi) {
+    case HLM_EPI_BF16_ROPE: epilogue_rope(args, taddr, row, tg, tn * BN); break;
+    case HLM_EPI_SWIGLU: epilogue_swiglu(args, taddr, row, tn * (BN / 2)); break;
+    case HLM_EPI_SWIGLU_BWD: epilogue_swiglu_bwd(args, taddr, row, tn * BN); break;
+    default: epilogue_plain(args, taddr, row, tg, tn * BN);
+  }
 }
 
 template <bool A_MN, bool B_MN>
@@ -190,9 +343,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               tma_load_3d(a_dst, &map_a, &full[stage], k0, m0, ag);
             }
             if (B_MN) {
+              if (args.paired) {   // atoms 0,1: group 0 (up); atoms 2,3: group 1 (gate), same columns
+                const int np = tn * (BN / 2);
 #pragma unroll
-              for (int j = 0; j < BN / 64; ++j)
-                tma_load_3d(b_dst + j * ATOM, &map_b, &full[stage], n0 + 64 * j, k0, bg);
+                for (int j = 0; j < BN / 64; ++j)
+                  tma_load_3d(b_dst + j * ATOM, &map_b, &full[stage], np + 64 * (j & 1), k0, j >> 1);
+              } else {
+#pragma unroll
+                for (int j = 0; j < BN / 64; ++j)
+                  tma_load_3d(b_dst + j * ATOM, &map_b, &full[stage], n0 + 64 * j, k0, bg);
+              }
             } else {
               tma_load_3d(b_dst, &map_b, &full[stage], k0, n0, bg);
             }
@@ -259,7 +419,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(&tmem_full[acc], acc_phase);
       tc_fence_after();
       const int row = tm * BM + ew * 32 + lane;
-      epilogue_store(args, tmem_base + acc * BN + ((uint32_t)(ew * 32) << 16), row, tg, tn * BN);
+      epilogue_store(args, tmem_base + acc * BN + ((uint32_t)(ew * 32) << 16), row, tg, tn);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tmem_empty[acc]);
@@ -334,11 +494,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       for (int t = pair; t < args.num_tiles; t += npairs) {
         int tg, tm, tn;
         tile_coords_2sm(args, t, tg, tm, tn);
-        const int m0 = tm * 256 + (int)crank * 128, n0 = tn * 256 + (int)crank * 128;
+        // paired (SWIGLU): both CTAs load the same 128 output columns, CTA 0 of w_up and
+        // CTA 1 of w_gate, so TMEM columns 0..127 / 128..255 are up / gate
+        const int m0 = tm * 256 + (int)crank * 128;
+        const int n0 = args.paired ? tn * 128 : tn * 256 + (int)crank * 128;
         for (int gi = 0; gi < g_iters; ++gi) {
           const int g = args.kgroup ? gi : tg;
           const int ag = args.a_grouped ? g : 0;
-          const int bg = args.b_grouped ? g : 0;
+          const int bg = args.paired ? (int)crank : (args.b_grouped ? g : 0);
           for (int kb = 0; kb < args.kblocks; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
             if (crank == 0) mbar_arrive_expect_tx(&full[stage], 4 * HALF_STAGE);
@@ -420,7 +583,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(&tmem_full[acc], acc_phase);
       tc_fence_after();
       const int row = tm * 256 + (int)crank * 128 + ew * 32 + lane;
-      epilogue_store(args, tmem_base + acc * 256 + ((uint32_t)(ew * 32) << 16), row, tg, tn * 256);
+      epilogue_store(args, tmem_base + acc * 256 + ((uint32_t)(ew * 32) << 16), row, tg, tn);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(acc ? leader_empty1 : leader_empty0);
@@ -521,10 +684,12 @@ int launch(const HlmGemmDesc& d, cudaStream_t stream) {
   a.kgroup = d.kgroup;
   a.a_grouped = d.a_grouped;
   a.b_grouped = d.b_grouped;
+  a.paired = d.epi == HLM_EPI_SWIGLU;
+  const int tile_n = a.paired ? BN / 2 : BN;
   a.tiles_m = (d.M + tile_m - 1) / tile_m;
-  a.tiles_n = (d.N + BN - 1) / BN;
+  a.tiles_n = (d.N + tile_n - 1) / tile_n;
   a.kblocks = (d.K + BK - 1) / BK;
-  a.num_tiles = a.tiles_m * a.tiles_n * (d.kgroup ? 1 : a.G);
+  a.num_tiles = a.tiles_m * a.tiles_n * ((d.kgroup || a.paired) ? 1 : a.G);
   {
     static int gm_env = -1;
     if (gm_env < 0) {
@@ -540,6 +705,15 @@ int launch(const HlmGemmDesc& d, cudaStream_t stream) {
   a.ldr = d.ldr;
   a.r_gstride = d.r_gstride;
   a.epi = d.epi;
+  a.rope_cos = d.rope_cos;
+  a.rope_sin = d.rope_sin;
+  a.rope_seq = d.rope_seq;
+  a.rope_hd = d.rope_head_dim;
+  a.aux = static_cast<const __nv_bfloat16*>(d.aux);
+  a.aux_ld = d.aux_ld;
+  a.aux_gstride = d.aux_gstride;
+  a.C2 = static_cast<__nv_bfloat16*>(d.C2);
+  a.ldc2 = d.ldc2;
 
   if (two) {
     static bool attr2 = false;
@@ -568,6 +742,16 @@ extern "C" int hlm_gemm_launch(const HlmGemmDesc* d, cudaStream_t stream) {
   if (!d) return HLM_GEMM_ERR_ARGS;
   if (d->M <= 0 || d->N <= 0 || d->K <= 0) return 0;
   if (d->epi == HLM_EPI_F32_ADD && d->R == nullptr) return HLM_GEMM_ERR_ARGS;
+  if (d->epi < HLM_EPI_BF16 || d->epi > HLM_EPI_SWIGLU_BWD) return HLM_GEMM_ERR_ARGS;
+  if (d->epi == HLM_EPI_BF16_ROPE) {   // whole heads inside a 256-column tile, q and k groups
+    const int hd = d->rope_head_dim;
+    if (d->kgroup || d->G < 2 || !d->rope_cos || !d->rope_sin || d->rope_seq <= 0 || d->N % 32 ||
+        !(hd == 64 || hd == 128 || hd == 256) || d->N % hd || (d->ldc % 8))
+      return HLM_GEMM_ERR_ARGS;
+  }
+  if (d->epi == HLM_EPI_SWIGLU && (d->G != 2 || d->kgroup || !d->b_mn || !d->b_grouped || !d->C2))
+    return HLM_GEMM_ERR_ARGS;
+  if (d->epi == HLM_EPI_SWIGLU_BWD && (d->G != 1 || d->kgroup || !d->aux)) return HLM_GEMM_ERR_ARGS;
   // TMA: global strides must be multiples of 16 bytes, base 16-byte aligned.
   if ((d->lda * 2) % 16 || (d->ldb * 2) % 16) return HLM_GEMM_ERR_ALIGN;
   if ((reinterpret_cast<uintptr_t>(d->A) & 15) || (reinterpret_cast<uintptr_t>(d->B) & 15))

@@ -1,0 +1,132 @@
+"""Fused GEMM epilogues: RoPE in the q|k|v projection, SwiGLU in the
+paired up|gate projection, the SwiGLU backward in the down-projection dgrad.
+
+* GEMM level: each fused epilogue against torch on the same bf16 operands (fp32
+  accumulation; the rounding points of the unfused path: GEMM output -> BF16 -> op -> BF16).
+* Block level: hlm_cuda_block_fwd / _bwd fused vs HLM_BLOCK_UNFUSED (the separate
+  rope / swiglu kernels) — output, input gradient and the whole tile gradient bit for bit,
+  at 2-CTA (T > 128) and 1-CTA (T <= 128) tile shapes, head_dim 64 / 128, ragged f.
+"""
+import ctypes
+
+import pytest
+import torch
+
+from paper_2602_04816_b200 import _lib as L
+
+pytestmark = pytest.mark.gpu
+
+
+def vp(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def bf(x):
+    return x.to(torch.bfloat16).float()
+
+
+def _rope_tables(S, hd, theta=1e6):
+    Lb = L.blib()
+    cs = torch.empty(S * hd // 2, device="cuda")
+    sn = torch.empty_like(cs)
+    L.check(Lb.hlm_cuda_rope_table(vp(cs), vp(sn), S, hd, theta))
+    return cs, sn
+
+
+@pytest.mark.parametrize("T,h,hd,S", [(512, 512, 128, 256), (96, 256, 64, 32), (384, 768, 256, 128)])
+def test_rope_epilogue(T, h, hd, S):
+    torch.manual_seed(T + h)
+    x = torch.randn(T, h, device="cuda").bfloat16()
+    W = (torch.randn(3, h, h, device="cuda") * 0.05).bfloat16()       # (in, out) per group
+    C = torch.full((3, T, h), float("nan"), device="cuda").bfloat16()
+    cs, sn = _rope_tables(S, hd)
+    d = L.HlmGemmDesc()
+    d.M, d.N, d.K, d.G = T, h, h, 3
+    d.a_mn, d.b_mn, d.b_grouped, d.epi = 0, 1, 1, L.EPI_BF16_ROPE
+    d.A, d.lda = x.data_ptr(), h
+    d.B, d.ldb, d.b_gstride = W.data_ptr(), h, h * h
+    d.C, d.ldc, d.c_gstride = C.data_ptr(), h, T * h
+    d.rope_cos, d.rope_sin, d.rope_seq, d.rope_head_dim = cs.data_ptr(), sn.data_ptr(), S, hd
+    L.gemm(d)
+    torch.cuda.synchronize()
+    ref = bf(torch.einsum("tk,gkn->gtn", x.float(), W.float()))
+    half = hd // 2
+    c = cs.view(S, half)[torch.arange(T, device="cuda") % S]
+    s = sn.view(S, half)[torch.arange(T, device="cuda") % S]
+    for gi in range(2):
+        v = ref[gi].view(T, h // hd, hd)
+        a, b = v[..., :half], v[..., half:]
+        ref[gi] = bf(torch.cat([a * c[:, None] - b * s[:, None], b * c[:, None] + a * s[:, None]], -1).view(T, h))
+    err = (C.float() - ref).abs().max().item()
+    assert err <= 2e-2 * ref.abs().max().item(), err   # fp32 sum order moves a BF16 rounding, not more
+
+
+@pytest.mark.parametrize("T,h,f", [(512, 256, 512), (640, 128, 200), (64, 256, 384)])
+def test_swiglu_epilogues(T, h, f):
+    torch.manual_seed(T + f)
+    dev = "cuda"
+    n2 = torch.randn(T, h, device=dev).bfloat16()
+    Wug = (torch.randn(2, h, f, device=dev) * 0.1).bfloat16()
+    ug = torch.full((2, T, f), float("nan"), device=dev).bfloat16()
+    act = torch.full((T, f), float("nan"), device=dev).bfloat16()
+    d = L.HlmGemmDesc()
+    d.M, d.N, d.K, d.G = T, f, h, 2
+    d.a_mn, d.b_mn, d.b_grouped, d.epi = 0, 1, 1, L.EPI_SWIGLU
+    d.A, d.lda = n2.data_ptr(), h
+    d.B, d.ldb, d.b_gstride = Wug.data_ptr(), f, h * f
+    d.C, d.ldc, d.c_gstride = ug.data_ptr(), f, T * f
+    d.C2, d.ldc2 = act.data_ptr(), f
+    L.gemm(d)
+    torch.cuda.synchronize()
+    ref_ug = bf(torch.einsum("tk,gkn->gtn", n2.float(), Wug.float()))
+    assert (ug.float() - ref_ug).abs().max().item() <= 2e-2 * ref_ug.abs().max().item()
+    u, z = ug[0].float(), ug[1].float()   # act from the stored (rounded) up / gate
+    ref_act = bf(u * (z * torch.sigmoid(z)))
+    assert (act.float() - ref_act).abs().max().item() <= 1e-2 * ref_act.abs().max().item() + 1e-6
+
+    g = torch.randn(T, h, device=dev).bfloat16()
+    Wd = (torch.randn(f, h, device=dev) * 0.1).bfloat16()   # (in=f, out=h)
+    dug = torch.full((2, T, f), float("nan"), device=dev).bfloat16()
+    d = L.HlmGemmDesc()
+    d.M, d.N, d.K, d.G = T, f, h, 1
+    d.a_mn, d.b_mn, d.epi = 0, 0, L.EPI_SWIGLU_BWD
+    d.A, d.lda = g.data_ptr(), h
+    d.B, d.ldb = Wd.data_ptr(), h
+    d.C, d.ldc, d.c_gstride = dug.data_ptr(), f, T * f
+    d.aux, d.aux_ld, d.aux_gstride = ug.data_ptr(), f, T * f
+    L.gemm(d)
+    torch.cuda.synchronize()
+    da = bf(g.float() @ Wd.float().t())
+    sg = torch.sigmoid(z)
+    ref_du, ref_dg = bf(da * z * sg), bf(da * u * (sg * (1 + z * (1 - sg))))
+    for got, ref in ((dug[0], ref_du), (dug[1], ref_dg)):
+        assert (got.float() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item() + 1e-6
+
+
+@pytest.mark.parametrize("B,S,h,f,H", [(2, 256, 256, 512, 2), (1, 128, 256, 200, 4), (2, 128, 512, 1024, 4)])
+def test_block_fused_equals_unfused_bitwise(B, S, h, f, H):
+    torch.manual_seed(S + f)
+    dev = "cuda"
+    T = B * S
+    n = 4 * h * h + 3 * h * f + 2 * h
+    Wb = torch.cat([(torch.randn(n - 2 * h, device=dev) * 0.02), 1 + 0.1 * torch.randn(2 * h, device=dev)]).bfloat16()
+    x = torch.randn(T, h, device=dev)
+    g_out = torch.randn(T, h, device=dev) * 1e-2
+    hd = h // H
+    cs, sn = _rope_tables(S, hd)
+    Lb = L.blib()
+    outs = []
+    for flags in (0, L.BLOCK_UNFUSED):
+        d = L.HlmBlockDims(B, S, h, f, H, flags)
+        acts = torch.zeros(Lb.hlm_cuda_block_acts_bytes(ctypes.byref(d)), dtype=torch.uint8, device=dev)
+        ws = torch.zeros(Lb.hlm_cuda_block_ws_bytes(ctypes.byref(d)), dtype=torch.uint8, device=dev)
+        y = torch.empty_like(x)
+        L.check(Lb.hlm_cuda_block_fwd(ctypes.byref(d), vp(Wb), vp(x), vp(y), vp(acts), vp(ws), vp(cs), vp(sn), None))
+        g_in = torch.empty_like(x)
+        grad = torch.full((n,), float("nan"), device=dev)
+        L.check(Lb.hlm_cuda_block_bwd(ctypes.byref(d), vp(Wb), vp(x), vp(acts), vp(g_out), vp(g_in), vp(grad),
+                                      vp(ws), vp(cs), vp(sn), None))
+        torch.cuda.synchronize()
+        outs.append((y, g_in, grad))
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a, b)
