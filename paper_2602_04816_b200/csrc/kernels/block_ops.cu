@@ -239,16 +239,16 @@ __global__ void __launch_bounds__(THREADS, MINB)
   const long long r1 = r0 + rows_per_chunk < rows ? r0 + rows_per_chunk : rows;
   int par = 0;
   for (long long r = r0; r < r1; ++r, par ^= 1) {
-    float4 xv[V], gv[V], rv[V];
+    // x and g stay in registers between the row reduction and the output pass; the
+    // residual is read in the output pass only (keeping it live spilled at 3 CTAs / SM)
+    float4 xv[V], gv[V];
     float ss = 0.f, dot = 0.f;
 #pragma unroll
     for (int k = 0; k < V; ++k) {
       const int q = tid + k * THREADS;
-      rv[k] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (q < nv) {
         xv[k] = __ldcs(reinterpret_cast<const float4*>(x + r * h) + q);
         gv[k] = __ldcs(reinterpret_cast<const float4*>(g + r * h) + q);
-        if (resid) rv[k] = __ldcs(reinterpret_cast<const float4*>(resid + r * h) + q);
         ss += xv[k].x * xv[k].x + xv[k].y * xv[k].y + xv[k].z * xv[k].z + xv[k].w * xv[k].w;
         dot += gv[k].x * sc[k].x * xv[k].x + gv[k].y * sc[k].y * xv[k].y + gv[k].z * sc[k].z * xv[k].z +
                gv[k].w * sc[k].w * xv[k].w;
@@ -275,10 +275,12 @@ __global__ void __launch_bounds__(THREADS, MINB)
     for (int k = 0; k < V; ++k) {
       const int q = tid + k * THREADS;
       if (q < nv) {
-        const float4 v = make_float4(gv[k].x * sc[k].x * inv - c * xv[k].x + rv[k].x,
-                                     gv[k].y * sc[k].y * inv - c * xv[k].y + rv[k].y,
-                                     gv[k].z * sc[k].z * inv - c * xv[k].z + rv[k].z,
-                                     gv[k].w * sc[k].w * inv - c * xv[k].w + rv[k].w);
+        const float4 rv = resid ? __ldcs(reinterpret_cast<const float4*>(resid + r * h) + q)
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 v = make_float4(gv[k].x * sc[k].x * inv - c * xv[k].x + rv.x,
+                                     gv[k].y * sc[k].y * inv - c * xv[k].y + rv.y,
+                                     gv[k].z * sc[k].z * inv - c * xv[k].z + rv.z,
+                                     gv[k].w * sc[k].w * inv - c * xv[k].w + rv.w);
         __stcs(reinterpret_cast<float4*>(out + r * h) + q, v);
         if (out_bf) {
           __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
@@ -1014,7 +1016,15 @@ int hlm_ops_rmsnorm_bwd(const float* x, const void* scale, const float* g, const
                         cudaStream_t s) {
   const int rpc = HLM_NORM_ROWS_PER_CHUNK;
   const int chunks = (int)((rows + rpc - 1) / rpc);
-  if (h % 4 == 0 && h <= 4 * 256 * 4) {
+  static int minb = -1;   // HLM_RMSNORM_BWD_MINB=2: 128-register variant (A/B)
+  if (minb < 0) {
+    const char* e = std::getenv("HLM_RMSNORM_BWD_MINB");
+    minb = (e && *e == '2') ? 2 : 3;
+  }
+  if (h % 4 == 0 && h <= 4 * 256 * 4 && minb == 2) {
+    rmsnorm_bwd_reg_kernel<256, 4, 2><<<chunks, 256, 0, s>>>(x, (const __nv_bfloat16*)scale, g, resid, out,
+                                                             (__nv_bfloat16*)out_bf, inv_buf, partial, rows, h, rpc);
+  } else if (h % 4 == 0 && h <= 4 * 256 * 4) {
     rmsnorm_bwd_reg_kernel<256, 4, 3><<<chunks, 256, 0, s>>>(x, (const __nv_bfloat16*)scale, g, resid, out,
                                                              (__nv_bfloat16*)out_bf, inv_buf, partial, rows, h, rpc);
   } else if (h % 4 == 0 && h <= 4 * 512 * 6) {
