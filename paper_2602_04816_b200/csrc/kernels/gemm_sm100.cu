@@ -77,7 +77,8 @@ __device__ __forceinline__ void tile_coords(const KArgs& a, int t, int& g, int& 
 }
 
 // TMEM accumulator row (32x32b loads, 8 chunks of 32 columns) -> global C.
-__device__ __forceinline__ void epilogue_plain(const KArgs& args, uint32_t taddr, int row, int tg, int col_base) {
+__device__ __forceinline__ void epilogue_plain(const KArgs& args, uint32_t taddr, int row, int tg, int col_base,
+                                               int epi) {
   const bool row_ok = row < args.M;
   const long long c_off = (long long)tg * args.c_gstride + (long long)row * args.ldc;
   const long long r_off = (long long)tg * args.r_gstride + (long long)row * args.ldr;
@@ -89,7 +90,7 @@ __device__ __forceinline__ void epilogue_plain(const KArgs& args, uint32_t taddr
     const int col0 = col_base + c * 32;
       if (!row_ok || col0 >= args.N) continue;
       const bool full_chunk = col0 + 32 <= args.N;
-      if (args.epi == HLM_EPI_BF16) {
+      if (epi == HLM_EPI_BF16) {
         __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.C) + c_off + col0;
         if (full_chunk && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
           uint4* d4 = reinterpret_cast<uint4*>(dst);
@@ -109,7 +110,7 @@ __device__ __forceinline__ void epilogue_plain(const KArgs& args, uint32_t taddr
         }
       } else {
         float* dst = reinterpret_cast<float*>(args.C) + c_off + col0;
-        const float* res = args.epi == HLM_EPI_F32_ADD ? args.R + r_off + col0 : nullptr;
+        const float* res = epi == HLM_EPI_F32_ADD ? args.R + r_off + col0 : nullptr;
         if (full_chunk && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) &&
             (res == nullptr || (reinterpret_cast<uintptr_t>(res) & 15) == 0)) {
           float4* d4 = reinterpret_cast<float4*>(dst);
@@ -174,8 +175,8 @@ __device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* src, float (&v
 // the same thread's row); group 2 (v) is a plain BF16 store. Same rounding points as
 // the GEMM's BF16 epilogue followed by the in-place rope pass.
 __device__ __forceinline__ void epilogue_rope(const KArgs& args, uint32_t taddr, int row, int tg, int col_base) {
-  if (tg >= 2) {
-    epilogue_plain(args, taddr, row, tg, col_base);
+  if (tg >= 2) {   // v: the plain BF16 store
+    epilogue_plain(args, taddr, row, tg, col_base, HLM_EPI_BF16);
     return;
   }
   const int hd = args.rope_hd, half = hd >> 1, dist = half >> 5;
@@ -243,29 +244,72 @@ __device__ __forceinline__ void epilogue_swiglu(const KArgs& args, uint32_t tadd
 }
 
 // down-projection dgrad: d_act rounded to BF16 (the plain epilogue's value), then the
-// swiglu_bwd kernel's arithmetic against up / gate read from aux.
+// swiglu_bwd kernel's arithmetic against up / gate read from aux. The up / gate loads of
+// chunk c + 1 are issued before chunk c's math, so their latency hides under it and the
+// epilogue keeps pace with the next tile's MMAs.
 __device__ __forceinline__ void epilogue_swiglu_bwd(const KArgs& args, uint32_t taddr, int row, int col_base) {
   const bool row_ok = row < args.M;
   __nv_bfloat16* du_row = reinterpret_cast<__nv_bfloat16*>(args.C) + (long long)row * args.ldc;
   __nv_bfloat16* dg_row = du_row + args.c_gstride;
   const __nv_bfloat16* up_row = args.aux + (long long)row * args.aux_ld;
   const __nv_bfloat16* gate_row = up_row + args.aux_gstride;
+  // whole 32-column chunks of 16-byte aligned rows use the prefetched vector path
+  const bool vec = ((args.aux_ld & 7) == 0) && ((reinterpret_cast<uintptr_t>(args.aux) & 15) == 0) &&
+                   ((args.aux_gstride & 7) == 0);
+  auto whole = [&](int c) { return row_ok && vec && col_base + c * 32 + 32 <= args.N; };
+  uint4 pu[4], pz[4];
+  if (whole(0)) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      pu[j] = reinterpret_cast<const uint4*>(up_row + col_base)[j];
+      pz[j] = reinterpret_cast<const uint4*>(gate_row + col_base)[j];
+    }
+  }
 #pragma unroll 1
   for (int c = 0; c < BN / 32; ++c) {
     uint32_t rd[32];
     tmem_ld_32x32(taddr + c * 32, rd);
-    tmem_ld_wait();
     const int col0 = col_base + c * 32;
-    if (!row_ok || col0 >= args.N) continue;
-    const int valid = min(32, args.N - col0);
-    float u[32], z[32], du[32], dg[32];
-    load_bf16x32(up_row + col0, u, valid);
-    load_bf16x32(gate_row + col0, z, valid);
+    uint4 nu[4], nz[4];
+    if (c + 1 < BN / 32 && whole(c + 1)) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
-      hlm_fused::swiglu_bwd(hlm_fused::round_bf16(__uint_as_float(rd[j])), u[j], z[j], du[j], dg[j]);
-    store_bf16x32(du_row + col0, du, valid);
-    store_bf16x32(dg_row + col0, dg, valid);
+      for (int j = 0; j < 4; ++j) {
+        nu[j] = reinterpret_cast<const uint4*>(up_row + col0 + 32)[j];
+        nz[j] = reinterpret_cast<const uint4*>(gate_row + col0 + 32)[j];
+      }
+    }
+    tmem_ld_wait();
+    if (row_ok && col0 < args.N) {
+      const int valid = min(32, args.N - col0);
+      float u[32], z[32], du[32], dg[32];
+      if (whole(c)) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t wu[4] = {pu[j].x, pu[j].y, pu[j].z, pu[j].w};
+          const uint32_t wz[4] = {pz[j].x, pz[j].y, pz[j].z, pz[j].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            u[8 * j + 2 * e] = __uint_as_float(wu[e] << 16);
+            u[8 * j + 2 * e + 1] = __uint_as_float(wu[e] & 0xFFFF0000u);
+            z[8 * j + 2 * e] = __uint_as_float(wz[e] << 16);
+            z[8 * j + 2 * e + 1] = __uint_as_float(wz[e] & 0xFFFF0000u);
+          }
+        }
+      } else {
+        load_bf16x32(up_row + col0, u, valid);
+        load_bf16x32(gate_row + col0, z, valid);
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        hlm_fused::swiglu_bwd(hlm_fused::round_bf16(__uint_as_float(rd[j])), u[j], z[j], du[j], dg[j]);
+      store_bf16x32(du_row + col0, du, valid);
+      store_bf16x32(dg_row + col0, dg, valid);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      pu[j] = nu[j];
+      pz[j] = nz[j];
+    }
   }
 }
 
@@ -274,7 +318,7 @@ __device__ __forceinline__ void epilogue_store(const KArgs& args, uint32_t taddr
     case HLM_EPI_BF16_ROPE: epilogue_rope(args, taddr, row, tg, tn * BN); break;
     case HLM_EPI_SWIGLU: epilogue_swiglu(args, taddr, row, tn * (BN / 2)); break;
     case HLM_EPI_SWIGLU_BWD: epilogue_swiglu_bwd(args, taddr, row, tn * BN); break;
-    default: epilogue_plain(args, taddr, row, tg, tn * BN);
+    default: epilogue_plain(args, taddr, row, tg, tn * BN, args.epi);
   }
 }
 
