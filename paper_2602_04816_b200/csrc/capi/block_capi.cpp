@@ -149,6 +149,19 @@ bool fused(const HlmBlockDims& d) {
   return env && !(d.flags & HLM_BLOCK_UNFUSED);
 }
 
+// The SwiGLU backward in the down-dgrad epilogue is off by default: measured at C2 (ncu,
+// tools/block_bench.py) the epilogue's up / gate reads stall the accumulator hand-off and
+// the GEMM drops to 50 % tensor-pipe activity (2.24 ms vs 1.46 ms + 0.47 ms for the
+// separate swiglu_bwd kernel). HLM_FUSE_SWIGLU_BWD=1 turns it on (bit-identical).
+bool fuse_swiglu_bwd() {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = std::getenv("HLM_FUSE_SWIGLU_BWD");
+    env = (e && *e == '1') ? 1 : 0;
+  }
+  return env != 0;
+}
+
 void validate(const HlmBlockDims* d) {
   if (!d || d->batch <= 0 || d->seq <= 0 || d->hidden <= 0 || d->ffn <= 0 || d->n_heads <= 0)
     throw Failure{"block dims must be positive", HLM_ERR_CONFIG};
@@ -305,7 +318,7 @@ int hlm_cuda_block_bwd(const HlmBlockDims* d, const void* w_tile, const float* h
     // MLP branch
     timed(HLM_KTIMER_CAST, 6.0 * T * h, s, [&] { chk(hlm_ops_cast_bf16(g_out, w.g_bf, T * h, s), "cast g_out"); });
     chk_gemm(gdesc(fi, hi, Ti, a.act, f, 1, w.g_bf, h, 1, G + off.down, h, HLM_EPI_F32), s, "wgrad down");
-    if (fused(*d)) {   // d_act never stored: the SwiGLU backward runs in the dgrad epilogue
+    if (fused(*d) && fuse_swiglu_bwd()) {   // d_act never stored: SwiGLU backward in the dgrad epilogue
       HlmGemmDesc gd = gdesc(Ti, fi, hi, w.g_bf, h, 0, W + off.down, h, 0, w.dug, f, HLM_EPI_SWIGLU_BWD);
       gd.c_gstride = T * f;
       gd.aux = a.ug;

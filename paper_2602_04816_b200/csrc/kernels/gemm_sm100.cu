@@ -61,6 +61,7 @@ struct KArgs {
   long long aux_ld, aux_gstride;
   __nv_bfloat16* C2;
   long long ldc2;
+  int l2_prefetch;       // SWIGLU_BWD: bulk-prefetch the next tile's up / gate into L2 (A/B)
 };
 
 __device__ __forceinline__ void tile_coords(const KArgs& a, int t, int& g, int& m, int& n) {
@@ -137,13 +138,15 @@ __device__ __forceinline__ void epilogue_plain(const KArgs& args, uint32_t taddr
 }
 
 // 32 consecutive bf16 values of one row (16-byte stores when the chunk is whole and aligned).
+// Streaming (evict-first) stores: the fused epilogues' outputs must not push the GEMM's
+// operand panels out of L2.
 __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float (&v)[32], int valid) {
   if (valid == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
     uint4* d4 = reinterpret_cast<uint4*>(dst);
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      d4[j] = make_uint4(pack_bf16x2(v[8 * j + 0], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
-                         pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+      __stcs(d4 + j, make_uint4(pack_bf16x2(v[8 * j + 0], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                                pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7])));
   } else {
 #pragma unroll
     for (int j = 0; j < 32; ++j)
@@ -243,6 +246,16 @@ __device__ __forceinline__ void epilogue_swiglu(const KArgs& args, uint32_t tadd
   }
 }
 
+// 16-byte streaming load issued where it is written: volatile asm keeps the compiler from
+// sinking a prefetch down to its use (it does that under register pressure).
+__device__ __forceinline__ uint4 ld_cs_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.cs.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
 // down-projection dgrad: d_act rounded to BF16 (the plain epilogue's value), then the
 // swiglu_bwd kernel's arithmetic against up / gate read from aux. The up / gate loads of
 // chunk c + 1 are issued before chunk c's math, so their latency hides under it and the
@@ -261,8 +274,8 @@ __device__ __forceinline__ void epilogue_swiglu_bwd(const KArgs& args, uint32_t 
   if (whole(0)) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      pu[j] = reinterpret_cast<const uint4*>(up_row + col_base)[j];
-      pz[j] = reinterpret_cast<const uint4*>(gate_row + col_base)[j];
+      pu[j] = ld_cs_v4(reinterpret_cast<const uint4*>(up_row + col_base) + j);
+      pz[j] = ld_cs_v4(reinterpret_cast<const uint4*>(gate_row + col_base) + j);
     }
   }
 #pragma unroll 1
@@ -274,8 +287,8 @@ __device__ __forceinline__ void epilogue_swiglu_bwd(const KArgs& args, uint32_t 
     if (c + 1 < BN / 32 && whole(c + 1)) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        nu[j] = reinterpret_cast<const uint4*>(up_row + col0 + 32)[j];
-        nz[j] = reinterpret_cast<const uint4*>(gate_row + col0 + 32)[j];
+        nu[j] = ld_cs_v4(reinterpret_cast<const uint4*>(up_row + col0 + 32) + j);
+        nz[j] = ld_cs_v4(reinterpret_cast<const uint4*>(gate_row + col0 + 32) + j);
       }
     }
     tmem_ld_wait();
@@ -311,6 +324,19 @@ __device__ __forceinline__ void epilogue_swiglu_bwd(const KArgs& args, uint32_t 
       pz[j] = nz[j];
     }
   }
+}
+
+// SWIGLU_BWD: pull the up / gate row segments a tile's epilogue will read into L2 while
+// that tile's MMAs are still running (issued one tile ahead by the epilogue threads).
+__device__ __forceinline__ void epilogue_prefetch(const KArgs& args, int row, int tn) {
+  if (!args.l2_prefetch || args.epi != HLM_EPI_SWIGLU_BWD || row >= args.M) return;
+  const int col0 = tn * BN;
+  if (col0 >= args.N || (args.aux_ld & 7) || (args.aux_gstride & 7) || (reinterpret_cast<uintptr_t>(args.aux) & 15))
+    return;
+  const uint32_t bytes = (uint32_t)((min(BN, args.N - col0) * 2 + 15) & ~15);
+  const __nv_bfloat16* up = args.aux + (long long)row * args.aux_ld + col0;
+  l2_prefetch_bulk(up, bytes);
+  l2_prefetch_bulk(up + args.aux_gstride, bytes);
 }
 
 __device__ __forceinline__ void epilogue_store(const KArgs& args, uint32_t taddr, int row, int tg, int tn) {
@@ -460,6 +486,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tile_coords(args, t, tg, tm, tn);
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
+      if (local == 0) epilogue_prefetch(args, tm * BM + ew * 32 + lane, tn);
+      if (t + (int)gridDim.x < args.num_tiles) {   // the next tile's epilogue inputs
+        int ng, nm, nn;
+        tile_coords(args, t + gridDim.x, ng, nm, nn);
+        epilogue_prefetch(args, nm * BM + ew * 32 + lane, nn);
+      }
       mbar_wait(&tmem_full[acc], acc_phase);
       tc_fence_after();
       const int row = tm * BM + ew * 32 + lane;
@@ -624,6 +656,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       tile_coords_2sm(args, t, tg, tm, tn);
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
+      if (local == 0) epilogue_prefetch(args, tm * 256 + (int)crank * 128 + ew * 32 + lane, tn);
+      if (t + npairs < args.num_tiles) {   // the next tile's epilogue inputs
+        int ng, nm, nn;
+        tile_coords_2sm(args, t + npairs, ng, nm, nn);
+        epilogue_prefetch(args, nm * 256 + (int)crank * 128 + ew * 32 + lane, nn);
+      }
       mbar_wait(&tmem_full[acc], acc_phase);
       tc_fence_after();
       const int row = tm * 256 + (int)crank * 128 + ew * 32 + lane;
@@ -758,6 +796,14 @@ int launch(const HlmGemmDesc& d, cudaStream_t stream) {
   a.aux_gstride = d.aux_gstride;
   a.C2 = static_cast<__nv_bfloat16*>(d.C2);
   a.ldc2 = d.ldc2;
+  {
+    static int pf = -1;
+    if (pf < 0) {
+      const char* e = std::getenv("HLM_GEMM_L2_PREFETCH");
+      pf = (e && *e == '1') ? 1 : 0;
+    }
+    a.l2_prefetch = pf;
+  }
 
   if (two) {
     static bool attr2 = false;

@@ -8,6 +8,7 @@ paired up|gate projection, the SwiGLU backward in the down-projection dgrad.
   at 2-CTA (T > 128) and 1-CTA (T <= 128) tile shapes, head_dim 64 / 128, ragged f.
 """
 import ctypes
+import os
 
 import pytest
 import torch
@@ -104,7 +105,19 @@ def test_swiglu_epilogues(T, h, f):
 
 
 @pytest.mark.parametrize("B,S,h,f,H", [(2, 256, 256, 512, 2), (1, 128, 256, 200, 4), (2, 128, 512, 1024, 4)])
-def test_block_fused_equals_unfused_bitwise(B, S, h, f, H):
+@pytest.mark.parametrize("swiglu_bwd", ["0", "1"])
+def test_block_fused_equals_unfused_bitwise(B, S, h, f, H, swiglu_bwd):
+    # the SwiGLU-backward epilogue is opt-in (HLM_FUSE_SWIGLU_BWD, read once per process):
+    # run this case in a child process with the variable set
+    if swiglu_bwd == "1" and os.environ.get("HLM_FUSE_SWIGLU_BWD") != "1":
+        import subprocess
+        import sys
+        env = dict(os.environ, HLM_FUSE_SWIGLU_BWD="1")
+        r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x",
+                            f"{__file__}::test_block_fused_equals_unfused_bitwise[1-{B}-{S}-{h}-{f}-{H}]"],
+                           env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout[-3000:]
+        return
     torch.manual_seed(S + f)
     dev = "cuda"
     T = B * S

@@ -36,13 +36,16 @@ def run(cfg="c2", iters=10):
     sn = torch.empty_like(cs)
     L.check(Lb.hlm_cuda_rope_table(vp(cs), vp(sn), S, hd, 1e6))
     out = {}
+    # the two variants alternate iteration by iteration so clock / power drift hits both
+    runs = {}
     for name, flags in (("fused", 0), ("unfused", L.BLOCK_UNFUSED)):
         d = L.HlmBlockDims(B, S, h, f, H, flags)
         acts = torch.empty(Lb.hlm_cuda_block_acts_bytes(ctypes.byref(d)), dtype=torch.uint8, device=dev)
         ws = torch.empty(Lb.hlm_cuda_block_ws_bytes(ctypes.byref(d)), dtype=torch.uint8, device=dev)
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        tf, tb = [], []
-        for i in range(iters + 2):
+        runs[name] = (d, acts, ws, [], [])
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    for i in range(iters + 2):
+        for name, (d, acts, ws, tf, tb) in runs.items():
             ev[0].record()
             L.check(Lb.hlm_cuda_block_fwd(ctypes.byref(d), vp(W), vp(x), vp(y), vp(acts), vp(ws), vp(cs), vp(sn),
                                           None))
@@ -54,6 +57,7 @@ def run(cfg="c2", iters=10):
             if i >= 2:
                 tf.append(ev[0].elapsed_time(ev[1]))
                 tb.append(ev[1].elapsed_time(ev[2]))
+    for name, (_, _, _, tf, tb) in runs.items():
         tf.sort(), tb.sort()
         out[name] = (tf[len(tf) // 2], tb[len(tb) // 2])
         print(f"{cfg} {name:8s} fwd {out[name][0]:7.3f} ms  bwd {out[name][1]:7.3f} ms  "
