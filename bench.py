@@ -376,6 +376,10 @@ def run_hybrid(args, m, nums, E, lib, store, arena, holder, opts, batches, trace
 
 def run_ours(args, m, name):
     rank, world, local = dist_env()
+    if args.scaling == "strong":   # global B fixed (8), rows split over the ranks
+        if m["batch"] % world:
+            raise SystemExit(f"--scaling strong: global batch {m['batch']} not divisible by {world} ranks")
+        m = dict(m, batch=m["batch"] // world)
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
     # ranks on one host split its cores for their shard of the Adam (init keeps all cores);
     # pinned, the engine sizes each rank's team from its NUMA-local CPU slice itself
@@ -604,11 +608,11 @@ def run_ours(args, m, name):
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic copy-task tokens, random-init weights (parallel trunc-normal 0.02)",
         "config": {"workload": name, "global_batch": m["batch"] * world, "seq_len": m["seq"],
                    "tokens_per_step": nums["T"] * world, "params": nums["params"],
-                   "parallelism": f"dp{world}" if world > 1 else "single-gpu",
+                   "parallelism": f"dp{world}" if (world > 1 or dp) else "single-gpu",
                    "n_heads": m["n_heads"], "k_ckpt": 1, "l2": "inputs larger than L2 (weights "
                    "streamed from host every step)",
                    "gradient_slabs": n_slab, "optimizer_tail_blocks": tail,
@@ -791,6 +795,9 @@ def main():
     ap.add_argument("--layers", type=int, default=0,
                     help="partial depth of the config's full-width decoder (C3-C5 do not fit a 196 GB "
                          "host at full depth); the workload name says so")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: B rows per GPU (global batch grows with N); strong: the config's global "
+                         "batch split over the N ranks (SURVEY 8d)")
     ap.add_argument("--no-wide", action="store_true",
                     help="skip the C4 / C5 full-width depth sweeps reported beside a C2 headline")
     ap.add_argument("--wide-only", default="", help="comma list of wide configs to sweep (c4,c5)")

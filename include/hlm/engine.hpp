@@ -186,7 +186,13 @@ private:
     void worker_loop();
     void drain();
     bool eligible(const Pending& p) const;   // mu_ held
-    void wait_tile_current(i64 tile_id);
+    // all_ranks: every rank's shard of the tile must be current (a full H2D or a zero-copy
+    // read of the host shadow); otherwise only this rank's shard (sharded H2D + all-gather:
+    // the other shards arrive over NVLink from ranks that waited on their own versions)
+    void wait_tile_current(i64 tile_id, bool all_ranks);
+    bool sharded_h2d(const LayerTile& tile) const {
+        return opts_.comm_weights && tile.n_params() % opts_.world == 0;
+    }
     i64 op_begin(StreamOp op, void* stream);
     void op_end(i64 id, void* stream);
     void rethrow_worker_error();
@@ -200,6 +206,8 @@ private:
     void* h2d_ = nullptr;
     void* compute_ = nullptr;
     void* d2h_ = nullptr;
+    void* comm_ = nullptr;           // data parallel: per-layer gradient reduce-scatter
+    std::vector<void*> ev_rs_done_;  // per gradient buffer: reduce-scatter finished (comm_ -> d2h_)
     void* opt_ = nullptr;            // device Adam of HBM-resident tiles, beside the backward
     void* ev_res_grad_ = nullptr;    // a resident tile's gradient is complete (compute -> opt_)
     void* ev_w_ready_[2] = {};

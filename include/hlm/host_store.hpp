@@ -93,6 +93,11 @@ public:
         else
             version.fetch_add(1, std::memory_order_acq_rel);
     }
+    // this rank's own counter (its shard's completed updates)
+    i64 rank_version(int rank) const {
+        if (!shared_versions_) return version.load(std::memory_order_acquire);
+        return shared_versions_[rank].load(std::memory_order_acquire);
+    }
     i64 min_version() const {
         if (!shared_versions_) return version.load(std::memory_order_acquire);
         i64 v = shared_versions_[0].load(std::memory_order_acquire);

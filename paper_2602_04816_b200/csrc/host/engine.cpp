@@ -89,6 +89,10 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
     d2h_ = s;
     ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
     opt_ = s;
+    if (opts_.comm_grad) {
+        ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+        comm_ = s;
+    }
     ev_res_grad_ = new_event(false);
     for (int i = 0; i < 2; ++i) {
         ev_w_ready_[i] = new_event(false);
@@ -106,6 +110,7 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
         }
         for (i64 i = 0; i < n_gb; ++i) {
             ev_grad_ready_.push_back(new_event(false));
+            ev_rs_done_.push_back(new_event(false));
             ev_gradbuf_free_.push_back(new_event(false));
             ck(cudaEventRecord(E(ev_gradbuf_free_.back()), S(compute_)), "record");
         }
@@ -255,8 +260,8 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
         ck(cudaMalloc(&embed_rows_dev_, static_cast<size_t>(m.vocab) * 4), "cudaMalloc embed rows");
         embed_row_map_.assign(static_cast<size_t>(m.vocab), -1);
     }
-    if (opts_.embed_gather_host && !m.tie_embeddings && resident_of_[0] < 0 && opts_.world == 1 &&
-        !opts_.comm_weights && store_.shadow_pinned()) {
+    // (data parallel too: each rank gathers its own rows of the shared host shadow)
+    if (opts_.embed_gather_host && !m.tie_embeddings && resident_of_[0] < 0 && store_.shadow_pinned()) {
         void* dp = nullptr;
         if (cudaHostGetDevicePointer(&dp, const_cast<uint16_t*>(store_.tile(m.embed_tile_id()).shadow()), 0) ==
             cudaSuccess)
@@ -327,6 +332,7 @@ Engine::~Engine() {
     for (void* e : ev_slab_done_) cudaEventDestroy(E(e));
     for (void* e : ev_slab_flag_) cudaEventDestroy(E(e));
     for (void* e : ev_grad_ready_) cudaEventDestroy(E(e));
+    for (void* e : ev_rs_done_) cudaEventDestroy(E(e));
     for (void* e : ev_gradbuf_free_) cudaEventDestroy(E(e));
     if (gbuf_mem_) cudaFree(gbuf_mem_);
     if (embed_rows_host_) cudaFreeHost(embed_rows_host_);
@@ -343,6 +349,7 @@ Engine::~Engine() {
     cudaStreamDestroy(S(compute_));
     cudaStreamDestroy(S(d2h_));
     cudaStreamDestroy(S(opt_));
+    if (comm_) cudaStreamDestroy(S(comm_));
     if (tin_) {
         cudaStreamSynchronize(S(tin_));
         cudaStreamSynchronize(S(tout_));
@@ -421,15 +428,23 @@ void* Engine::weights_ptr(int buf) const {
     return buf >= 2 ? arena_.cache_slot(buf - 2) : arena_.buffer(buf);
 }
 
-void Engine::wait_tile_current(i64 tile_id) {
+void Engine::wait_tile_current(i64 tile_id, bool all_ranks) {
     if (!opts_.overlap_optimizer_tail) return;
     const i64 p = store_.physical_index(tile_id);
     const LayerTile& tile = store_.physical(p);
+    const i64 target = target_version_[static_cast<size_t>(p)];
+    const bool others = all_ranks && opts_.world > 1;
+    auto ready = [&] {
+        return (others ? tile.min_version() : tile.rank_version(opts_.rank)) >= target || worker_error_ != nullptr;
+    };
     std::unique_lock<std::mutex> lk(mu_);
-    cv_.wait(lk, [&] {
-        return tile.min_version() >= target_version_[static_cast<size_t>(p)] ||
-               worker_error_ != nullptr;
-    });
+    if (others) {
+        // other ranks bump their counters in the shared mapping from other processes, which
+        // never signal this process's condition variable: poll
+        while (!ready()) cv_.wait_for(lk, std::chrono::microseconds(100));
+    } else {
+        cv_.wait(lk, ready);
+    }
     lk.unlock();
     rethrow_worker_error();
 }
@@ -441,8 +456,10 @@ bool Engine::wait_elems_current(i64 tile_id, i64 end) {
     const LayerTile& tile = store_.physical(p);
     bool whole = false;
     std::unique_lock<std::mutex> lk(mu_);
+    // this rank's updates only: the piecewise H2D copies this rank's shard (all of the
+    // tile at world 1); progress_ counts elements of that shard
     cv_.wait(lk, [&] {
-        whole = tile.min_version() >= target_version_[static_cast<size_t>(p)];
+        whole = tile.rank_version(opts_.rank) >= target_version_[static_cast<size_t>(p)];
         return whole || progress_[static_cast<size_t>(p)] >= end || worker_error_ != nullptr;
     });
     lk.unlock();
@@ -452,15 +469,21 @@ bool Engine::wait_elems_current(i64 tile_id, i64 end) {
 
 int Engine::stream_tile(i64 tile_id, i64* op_id, bool forward_pass) {
     const i64 slot = cache_slot_of_[static_cast<size_t>(tile_id)];
-    // forward into a cache slot, single GPU: copy piece by piece behind the optimizer
+    // forward into a cache slot: copy piece by piece behind the optimizer — the whole tile
+    // (single GPU) or this rank's shard, then the NVLink all-gather (data parallel with
+    // sharded weight H2D; every rank's optimizer publishes progress over its own shard)
+    const LayerTile& stile = store_.tile(tile_id);
     const bool piecewise = slot >= 0 && forward_pass && cache_xfer_op_[static_cast<size_t>(slot)] < 0 &&
-                           opts_.overlap_optimizer_tail && opts_.world == 1 && !opts_.comm_weights;
-    if (!piecewise && !(slot >= 0 && cache_xfer_op_[static_cast<size_t>(slot)] >= 0)) wait_tile_current(tile_id);
+                           opts_.overlap_optimizer_tail && (opts_.world == 1 || sharded_h2d(stile));
+    if (!piecewise && !(slot >= 0 && cache_xfer_op_[static_cast<size_t>(slot)] >= 0))
+        wait_tile_current(tile_id, !sharded_h2d(stile));
     if (piecewise) {
-        const LayerTile& tile = store_.tile(tile_id);
-        const i64 n = tile.n_params();
+        const LayerTile& tile = stile;
+        const bool shard = sharded_h2d(tile);
+        const i64 n = shard ? tile.n_params() / opts_.world : tile.n_params();
+        const i64 base = shard ? opts_.rank * n : 0;
         arena_.claim_cache_slot(slot);
-        uint16_t* dst = static_cast<uint16_t*>(arena_.cache_slot(slot));
+        uint16_t* dst = static_cast<uint16_t*>(arena_.cache_slot(slot)) + base;
         bool waiting = true;
         i64 id = -1;
         const i64 hp = std::min(piece_elems_, kPublishElems);
@@ -475,12 +498,16 @@ int Engine::stream_tile(i64 tile_id, i64* op_id, bool forward_pass) {
             op.bytes = 2 * len;
             op.pinned = store_.shadow_pinned();
             id = op_begin(std::move(op), h2d_);
-            ck(cudaMemcpyAsync(dst + off, tile.shadow() + off, static_cast<size_t>(len) * 2, cudaMemcpyHostToDevice,
-                               S(h2d_)),
+            ck(cudaMemcpyAsync(dst + off, tile.shadow() + base + off, static_cast<size_t>(len) * 2,
+                               cudaMemcpyHostToDevice, S(h2d_)),
                "H2D weight piece");
             arena_.add_h2d(2 * len);
             op_end(id, h2d_);
         }
+        if (shard)
+            nccl_check(nccl().AllGather(dst, static_cast<uint16_t*>(arena_.cache_slot(slot)), static_cast<size_t>(n),
+                                        ncclBfloat16, static_cast<ncclComm_t>(opts_.comm_weights), S(h2d_)),
+                       "all-gather weights");
         ck(cudaEventRecord(E(ev_cache_ready_[static_cast<size_t>(slot)]), S(h2d_)), "record cache ready");
         cache_xfer_op_[static_cast<size_t>(slot)] = id;
         *op_id = id;
@@ -592,15 +619,21 @@ void Engine::evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op, bool spars
     op.bytes = bytes;
     op.deps.push_back(lb_op);
     if (last_accum_op_[static_cast<size_t>(slab)] >= 0) op.deps.push_back(last_accum_op_[static_cast<size_t>(slab)]);
-    ck(cudaStreamWaitEvent(S(d2h_), E(ev_grad_ready_[gbuf]), 0), "wait grad ready");
-    const i64 id = op_begin(std::move(op), d2h_);
     float* src = grad_buf(gbuf);
-    if (opts_.comm_grad) {   // in-place reduce-scatter over NVLink, then D2H of this rank's shard
+    if (opts_.comm_grad) {
+        // in-place reduce-scatter over NVLink on its own stream, so layer i's shard D2H
+        // (d2h_) runs beside layer i-1's reduce-scatter (comm_); then D2H of this rank's shard
         src += opts_.rank * cnt;
+        ck(cudaStreamWaitEvent(S(comm_), E(ev_grad_ready_[gbuf]), 0), "wait grad ready (comm)");
         nccl_check(nccl().ReduceScatter(grad_buf(gbuf), src, static_cast<size_t>(cnt), ncclFloat32, ncclSum,
-                                        static_cast<ncclComm_t>(opts_.comm_grad), S(d2h_)),
+                                        static_cast<ncclComm_t>(opts_.comm_grad), S(comm_)),
                    "reduce-scatter grads");
+        ck(cudaEventRecord(E(ev_rs_done_[static_cast<size_t>(gbuf)]), S(comm_)), "record rs done");
+        ck(cudaStreamWaitEvent(S(d2h_), E(ev_rs_done_[static_cast<size_t>(gbuf)]), 0), "wait rs done");
+    } else {
+        ck(cudaStreamWaitEvent(S(d2h_), E(ev_grad_ready_[gbuf]), 0), "wait grad ready");
     }
+    const i64 id = op_begin(std::move(op), d2h_);
     // the reference's "all gradients finite before any mutation" check, on the GPU;
     // its flag lands first, then the gradient in pieces (the optimizer starts on piece 0)
     ck_hlm(hlm_cuda_nonfinite(src, cnt, nf_dev_ + slab, d2h_), "nonfinite scan");
@@ -673,13 +706,11 @@ void Engine::consume(const Pending& p) {
             for (i64 so = 0; so < len; so += kPublishElems) {
                 const i64 sl = std::min(kPublishElems, len - so);
                 adam_step_range(tile, g + off + so, base + off + so, sl, hyper_, p.t, /*prechecked=*/true);
-                if (opts_.world == 1) {
-                    {
-                        std::lock_guard<std::mutex> lk(mu_);
-                        progress_[pi] = off + so + sl;
-                    }
-                    cv_.notify_all();
+                {   // elements of this rank's range done (the piecewise forward H2D follows)
+                    std::lock_guard<std::mutex> lk(mu_);
+                    progress_[pi] = off + so + sl;
                 }
+                cv_.notify_all();
             }
         }
         {   // the version now covers the whole tile; progress counts the next update
@@ -1101,8 +1132,8 @@ void Engine::forward_streaming() {
     i64 w_op = -1;
     const bool embed_res = is_resident(m.embed_tile_id());
     const bool embed_zc = !embed_res && embed_host_dev_ != nullptr;
-    if (embed_zc) {   // zero-copy gather: only the table version must be current
-        wait_tile_current(m.embed_tile_id());
+    if (embed_zc) {   // zero-copy gather: only the table version must be current (every shard)
+        wait_tile_current(m.embed_tile_id(), true);
         arena_.add_h2d(T * m.hidden * 2);
     }
     const int ebuf = embed_res ? -2 : embed_zc ? -3 : stream_tile(m.embed_tile_id(), &w_op);
@@ -1535,12 +1566,14 @@ StepResult Engine::finish_step() {
     const float* lr = reinterpret_cast<const float*>(loss_host_ + 2 * T);
     for (i64 r = 0; r < T; ++r) loss += static_cast<double>(lr[r]);
     if (opts_.comm_grad) {   // sum of every rank's (1/global_rows)-scaled partial loss
-        ck(cudaMemcpyAsync(loss_dev_, &loss, sizeof(double), cudaMemcpyHostToDevice, S(compute_)), "H2D loss");
+        // on the communicator's own stream, behind this step's reduce-scatters: one stream
+        // per communicator keeps the collectives in the same order on every rank
+        ck(cudaMemcpyAsync(loss_dev_, &loss, sizeof(double), cudaMemcpyHostToDevice, S(comm_)), "H2D loss");
         nccl_check(nccl().AllReduce(loss_dev_, loss_dev_, 1, ncclFloat64, ncclSum,
-                                    static_cast<ncclComm_t>(opts_.comm_grad), S(compute_)),
+                                    static_cast<ncclComm_t>(opts_.comm_grad), S(comm_)),
                    "all-reduce loss");
-        ck(cudaMemcpyAsync(&loss, loss_dev_, sizeof(double), cudaMemcpyDeviceToHost, S(compute_)), "D2H loss");
-        ck(cudaStreamSynchronize(S(compute_)), "sync loss");
+        ck(cudaMemcpyAsync(&loss, loss_dev_, sizeof(double), cudaMemcpyDeviceToHost, S(comm_)), "D2H loss");
+        ck(cudaStreamSynchronize(S(comm_)), "sync loss");
     }
 
     // host ops into the trace, in consumption order
