@@ -94,6 +94,25 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x on the FMA pipe for two lanes (the MUFU ex2 is the forward softmax's bottleneck):
+// x = j + f, j = rint(x) via the 1.5 * 2^23 shift, 2^f on [-1/2, 1/2] by a degree-3
+// polynomial (max relative error 1.0e-4, far below the bf16 rounding of P), 2^j added to
+// the exponent field. x is clamped at -127, where the result is exactly +0 (masked scores).
+__device__ __forceinline__ void ex2_poly2(float& y0, float& y1, float x0, float x1) {
+  x0 = fmaxf(x0, -127.f);
+  x1 = fmaxf(x1, -127.f);
+  float t0, t1, f0, f1, p0, p1;
+  asm("{\n.reg .b64 x, t, m, f;\n"
+      "mov.b64 x, {%4, %5};\nmov.b64 m, {%6, %6};\n"
+      "add.rn.f32x2 t, x, m;\nsub.rn.f32x2 f, t, m;\nsub.rn.f32x2 f, x, f;\n"
+      "mov.b64 {%0, %1}, t;\nmov.b64 {%2, %3}, f;\n}"
+      : "=f"(t0), "=f"(t1), "=f"(f0), "=f"(f1) : "f"(x0), "f"(x1), "f"(12582912.f));
+  fma2v(p0, p1, f0, f1, 0.05499936f, 0.05499936f, 0.24221137f, 0.24221137f);
+  fma2v(p0, p1, p0, p1, f0, f1, 0.69328505f, 0.69328505f);
+  fma2v(p0, p1, p0, p1, f0, f1, 1.0f, 1.0f);
+  y0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+  y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
+}
 // the two softmax warps sharing TMEM lanes 32q..32q+31 (named barrier 1 + q, 64 threads)
 __device__ __forceinline__ void pair_sync(int q) { asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory"); }
 
@@ -350,6 +369,10 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, u
       "}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
+// 32 lanes x 16 columns of 32-bit
+__device__ __forceinline__ void tmem_ld_32x16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]) : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_st_32x32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]) : "memory");
 }
@@ -358,6 +381,8 @@ __device__ __forceinline__ void tmem_st_32x16(uint32_t taddr, const uint32_t (&r
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// kEmu of every 4 exponentials per thread run on the FMA pipe (ex2_poly2), the rest on MUFU
+template <int kEmu>
 __global__ void __launch_bounds__(PP_THREADS, 1)
     flash_fwd_pp(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                  const __grid_constant__ CUtensorMap map_v, __nv_bfloat16* __restrict__ o, float* __restrict__ lse,
@@ -428,15 +453,11 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       const int st = j & 1;
       mbar_wait(&bars->k_full[st], (j >> 1) & 1);
       tc_fence_after();
-      if (lane == 0) {
-        const uint32_t q_base = smem_u32(sQ(t)), k_base = smem_u32(sK(st));
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk)
-          umma_bf16(tmem + t * 128, kmajor_desc(q_base, kk), kmajor_desc(k_base, kk), idesc_s, kk ? 1u : 0u);
-        umma_commit(&bars->s_full[t]);
-        if (t == 1) umma_commit(&bars->k_empty[st]);
-      }
-      __syncwarp();
+      const uint32_t q_base = smem_u32(sQ(t)), k_base = smem_u32(sK(st));
+      umma_chain_w<8, ATOM_BYTES / 16, 2, ATOM_BYTES / 16, 2>(tmem + t * 128, kmajor_desc(q_base, 0),
+                                                             kmajor_desc(k_base, 0), idesc_s, 0u);
+      umma_commit_w(&bars->s_full[t]);
+      if (t == 1) umma_commit_w(&bars->k_empty[st]);
     };
     // O_t += P_t V_j with P_t in TMEM (the first 64 columns of S_t); V_j released by tile B's PV
     auto issue_pv = [&](int t, int j) {
@@ -444,15 +465,12 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       mbar_wait(&bars->p_full[t], j & 1);
       mbar_wait(&bars->v_full[st], (j >> 1) & 1);
       tc_fence_after();
-      if (lane == 0) {
-        const uint32_t v_base = smem_u32(sV(st));
+      const uint32_t v_base = smem_u32(sV(st));
 #pragma unroll
-        for (int kk = 0; kk < TK / 16; ++kk)
-          umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, mnmajor_desc(v_base, kk), idesc_o,
+      for (int kk = 0; kk < TK / 16; ++kk)
+        umma_bf16_ts_w(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, mnmajor_desc(v_base, kk), idesc_o,
                        (j > 0 || kk > 0) ? 1u : 0u);
-        if (t == 1) umma_commit(&bars->v_empty[st]);
-      }
-      __syncwarp();
+      if (t == 1) umma_commit_w(&bars->v_empty[st]);
     };
     issue_s(0, 0);
     issue_s(1, 0);
@@ -462,16 +480,14 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         if (j + 1 < ntile_b - 1) {
           issue_s(0, j + 1);
         } else {
-          if (lane == 0) umma_commit(&bars->o_final[0]);
-          __syncwarp();
+          umma_commit_w(&bars->o_final[0]);
         }
       }
       issue_pv(1, j);
       if (j + 1 < ntile_b) {
         issue_s(1, j + 1);
       } else {
-        if (lane == 0) umma_commit(&bars->o_final[1]);
-        __syncwarp();
+        umma_commit_w(&bars->o_final[1]);
       }
     }
   } else {
@@ -516,13 +532,13 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         const float mn = fmaxf(m, mx);
         const float alpha = ex2(m - mn);
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t ov[32];
-          tmem_ld_32x32(o_addr + c * 32, ov);
+        for (int c = 0; c < 8; ++c) {   // 16 columns at a time: the 128 scores stay in registers
+          uint32_t ov[16];
+          tmem_ld_32x16(o_addr + c * 16, ov);
           tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-          tmem_st_32x32(o_addr + c * 32, ov);
+          for (int e = 0; e < 16; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+          tmem_st_32x16(o_addr + c * 16, ov);
         }
         l *= alpha;
         m = mn;
@@ -537,7 +553,13 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         for (int e = 0; e < 16; ++e) {
           float a0, a1;
           ffma2(a0, a1, __uint_as_float(sv[c][2 * e]), __uint_as_float(sv[c][2 * e + 1]), scale_log2, negm);
-          const float p0 = ex2(a0), p1 = ex2(a1);
+          float p0, p1;
+          if ((e & 3) < kEmu) {
+            ex2_poly2(p0, p1, a0, a1);
+          } else {
+            p0 = ex2(a0);
+            p1 = ex2(a1);
+          }
           fadd2(l8[2 * (e & 3)], l8[2 * (e & 3) + 1], p0, p1);
           pk[e] = pack_bf16x2(p0, p1);
         }
@@ -604,10 +626,6 @@ __device__ __forceinline__ void store_acc_half(__nv_bfloat16* dst, uint32_t tadd
   }
 }
 
-// 32 lanes x 16 columns of 32-bit
-__device__ __forceinline__ void tmem_ld_32x16(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]) : "r"(taddr));
-}
 // 16 columns (c16-th group of 16 along the 128) of row r of a K-major SW128 bf16 tile
 __device__ __forceinline__ void store_row16_kmajor(uint8_t* tile, int r, int c16, const uint32_t (&pk)[8]) {
   uint8_t* row = tile + (c16 >> 2) * ATOM_BYTES + r * 128;
@@ -992,11 +1010,383 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+// ------------------------------------------------------------------ backward, 64-wide steps
+// The two kernels above hold one S / dP pair in TMEM, so the tensor core idles while the
+// elementwise warps turn S, dP into P, dS. These step over the inner sequence dimension 64
+// at a time: S and dP of a step take 64 TMEM columns each and are double-buffered, so the
+// MMAs of step i+1 (and the accumulating MMAs of step i-1) run under the elementwise work
+// of step i. The elementwise warps copy S / dP into registers and release the TMEM buffer
+// before computing. Same per-element arithmetic as the 128-wide kernels.
+constexpr int HALF_TILE = 64 * HD * 2;   // 16 KiB: 64 rows x 128 columns (two 64x64 SW128 boxes)
+constexpr int HALF_ATOM = 64 * 64 * 2;   // 8 KiB: one 64-row x 64-column swizzle box
+
+// K-major descriptor for K step kk of a 64-row x 128-column tile (two 8 KiB boxes)
+__device__ __forceinline__ uint64_t kmajor_desc64(uint32_t base, int kk) {
+  return make_sw128_desc(base + (kk >> 2) * HALF_ATOM + (kk & 3) * 32, 16, 1024);
+}
+// MN-major descriptor of the same 64-row tile used as B with N = its 128 columns, K = its rows
+__device__ __forceinline__ uint64_t mnmajor_desc64(uint32_t base, int kk) {
+  return make_sw128_desc(base + kk * 2048, HALF_ATOM, 1024);
+}
+// K-major descriptor of a 128-row x 64-column bf16 tile (one swizzle atom column), K step kk < 4
+__device__ __forceinline__ uint64_t kmajor_desc_narrow(uint32_t base, int kk) {
+  return make_sw128_desc(base + kk * 32, 16, 1024);
+}
+// 16 bf16 columns (group c16 < 4) of row r of a 128 x 64 K-major SW128 tile
+__device__ __forceinline__ void store_row16_narrow(uint8_t* tile, int r, int c16, const uint32_t (&pk)[8]) {
+  uint8_t* row = tile + r * 128;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int chunk = c16 * 2 + q;
+    *reinterpret_cast<uint4*>(row + ((chunk ^ (r & 7)) << 4)) =
+        make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+  }
+}
+
+// P, dS of 16 (row, column) scores held by one thread, the reference backward's
+// dS = P (dP - D) (kernels.hpp:269-299), P from the forward's log-sum-exp.
+//   nl[e] = -lse * log2(e) of column e; dn[e] = D of column e (row sums for dQ, column
+//   values for dK/dV); masked entries (kDiag, e >= keep) get P = 0.
+template <bool kDiag>
+__device__ __forceinline__ void p_ds_16(const uint32_t (&sv)[16], const uint32_t (&dpv)[16], const float (&nl)[16],
+                                        const float (&dn)[16], float scale_log2, int keep_from, bool mask_below,
+                                        uint32_t (&pk)[8], uint32_t (&dk8)[8]) {
+#pragma unroll
+  for (int e = 0; e < 16; e += 2) {
+    float x0, x1, d0, d1;
+    fma2v(x0, x1, __uint_as_float(sv[e]), __uint_as_float(sv[e + 1]), scale_log2, scale_log2, nl[e], nl[e + 1]);
+    float p0 = ex2(x0), p1 = ex2(x1);
+    if (kDiag) {
+      // dK/dV (mask_below): column e is masked when e < keep_from; dQ: when e > keep_from
+      if (mask_below ? (e < keep_from) : (e > keep_from)) p0 = 0.f;
+      if (mask_below ? (e + 1 < keep_from) : (e + 1 > keep_from)) p1 = 0.f;
+    }
+    submul2(d0, d1, __uint_as_float(dpv[e]), __uint_as_float(dpv[e + 1]), dn[e], dn[e + 1], p0, p1);
+    pk[e / 2] = pack_bf16x2(p0, p1);
+    dk8[e / 2] = pack_bf16x2(d0, d1);
+  }
+}
+
+// dK, dV for one 128-key tile, 64 queries per step.
+//   TMEM: S^T[2] [0,128) (64 each), dP^T[2] [128,256), dV [256,384), dK [384,512)
+//   smem: K, V (fixed); Q|dO ring of KV2_STAGES 64-row stages; P^T, dS^T (128 keys x 64
+//   queries, K-major), single-buffered: written once the previous step's dV/dK MMAs read them.
+//   MMA order: S0 dP0 S1 dP1 | dV0 dK0 S2 dP2 | dV1 dK1 S3 dP3 | ...
+constexpr int KV2_STAGES = 4;
+struct BwdKV2Bars {
+  uint64_t kv_full, q_full[KV2_STAGES], q_empty[KV2_STAGES], s_full[2], s_free[2], p_full, p_free, acc_full;
+  uint32_t tmem;
+};
+constexpr int BWD_KV2_SMEM = TILE_BYTES * 2 + KV2_STAGES * 2 * HALF_TILE + 2 * HALF_TILE + 1024 + 256;
+constexpr int BWD_KV2_THREADS = 640;   // 4 control warps + 16 elementwise warps
+
+__global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
+    flash_bwd_dkv_tc2(const __grid_constant__ CUtensorMap map_q64, const __grid_constant__ CUtensorMap map_k,
+                      const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do64,
+                      const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dk,
+                      __nv_bfloat16* __restrict__ dv, int S, int H, int ld, float scale, float scale_log2) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sK = smem, *sV = smem + TILE_BYTES;
+  auto sQ = [&](int st) { return smem + 2 * TILE_BYTES + st * 2 * HALF_TILE; };
+  auto sdO = [&](int st) { return smem + 2 * TILE_BYTES + st * 2 * HALF_TILE + HALF_TILE; };
+  uint8_t* sPT = smem + 2 * TILE_BYTES + KV2_STAGES * 2 * HALF_TILE;
+  uint8_t* sdST = sPT + HALF_TILE;
+  BwdKV2Bars* bars = reinterpret_cast<BwdKV2Bars*>(sdST + HALF_TILE);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int kt = (int)blockIdx.x;        // key tile (early tiles have the longest loops: launched first)
+  const int i0 = 2 * kt, n = S / 64 - i0;   // query steps i0 .. S/64 - 1
+  const int bh = blockIdx.y, b = bh / H, hh = bh % H;
+  const int row0 = b * S, col0 = hh * HD;
+  if (threadIdx.x == 0) {
+    tma_prefetch(&map_q64);
+    tma_prefetch(&map_k);
+    tma_prefetch(&map_v);
+    tma_prefetch(&map_do64);
+    mbar_init(&bars->kv_full, 1);
+    for (int i = 0; i < KV2_STAGES; ++i) {
+      mbar_init(&bars->q_full[i], 1);
+      mbar_init(&bars->q_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars->s_full[i], 1);
+      mbar_init(&bars->s_free[i], 16);
+    }
+    mbar_init(&bars->p_full, 16);
+    mbar_init(&bars->p_free, 1);
+    mbar_init(&bars->acc_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(&bars->tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&bars->kv_full, 2 * TILE_BYTES);
+      tma_load_2d(sK, &map_k, &bars->kv_full, col0, row0 + kt * TK);
+      tma_load_2d(sK + ATOM_BYTES, &map_k, &bars->kv_full, col0 + 64, row0 + kt * TK);
+      tma_load_2d(sV, &map_v, &bars->kv_full, col0, row0 + kt * TK);
+      tma_load_2d(sV + ATOM_BYTES, &map_v, &bars->kv_full, col0 + 64, row0 + kt * TK);
+      for (int it = 0; it < n; ++it) {
+        const int st = it % KV2_STAGES, ph = (it / KV2_STAGES) & 1;
+        const int r = row0 + (i0 + it) * 64;
+        mbar_wait(&bars->q_empty[st], ph ^ 1);
+        mbar_arrive_expect_tx(&bars->q_full[st], 2 * HALF_TILE);
+        tma_load_2d(sQ(st), &map_q64, &bars->q_full[st], col0, r);
+        tma_load_2d(sQ(st) + HALF_ATOM, &map_q64, &bars->q_full[st], col0 + 64, r);
+        tma_load_2d(sdO(st), &map_do64, &bars->q_full[st], col0, r);
+        tma_load_2d(sdO(st) + HALF_ATOM, &map_do64, &bars->q_full[st], col0 + 64, r);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_s = make_idesc_bf16(128, 64, false, false);    // S^T, dP^T: N = 64 queries
+    constexpr uint32_t idesc_acc = make_idesc_bf16(128, 128, false, true);  // dV, dK: B MN-major
+    const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV), pt_base = smem_u32(sPT),
+                   dst_base = smem_u32(sdST);
+    mbar_wait(&bars->kv_full, 0);
+    auto issue_sdp = [&](int it) {
+      const int st = it % KV2_STAGES, bb = it & 1;
+      mbar_wait(&bars->q_full[st], (it / KV2_STAGES) & 1);
+      if (it >= 2) mbar_wait(&bars->s_free[bb], ((it - 2) >> 1) & 1);
+      tc_fence_after();
+      const uint32_t q_base = smem_u32(sQ(st)), do_base = smem_u32(sdO(st));
+      umma_chain_w<8, ATOM_BYTES / 16, 2, HALF_ATOM / 16, 2>(tmem + bb * 64, kmajor_desc(k_base, 0),
+                                                            kmajor_desc64(q_base, 0), idesc_s, 0u);
+      umma_chain_w<8, ATOM_BYTES / 16, 2, HALF_ATOM / 16, 2>(tmem + 128 + bb * 64, kmajor_desc(v_base, 0),
+                                                            kmajor_desc64(do_base, 0), idesc_s, 0u);
+      umma_commit_w(&bars->s_full[bb]);
+    };
+    issue_sdp(0);
+    if (n > 1) issue_sdp(1);
+    for (int it = 0; it < n; ++it) {
+      const int st = it % KV2_STAGES;
+      mbar_wait(&bars->p_full, it & 1);
+      tc_fence_after();
+      const uint32_t q_base = smem_u32(sQ(st)), do_base = smem_u32(sdO(st));
+      umma_chain_w<4, 0, 2, 512, 128>(tmem + 256, kmajor_desc_narrow(pt_base, 0), mnmajor_desc64(do_base, 0),
+                                      idesc_acc, it > 0 ? 1u : 0u);
+      umma_chain_w<4, 0, 2, 512, 128>(tmem + 384, kmajor_desc_narrow(dst_base, 0), mnmajor_desc64(q_base, 0),
+                                      idesc_acc, it > 0 ? 1u : 0u);
+      umma_commit_w(&bars->p_free);
+      umma_commit_w(&bars->q_empty[st]);
+      if (it + 2 < n) issue_sdp(it + 2);
+    }
+    umma_commit_w(&bars->acc_full);
+  } else if (warp >= 4) {
+    // warp w: key rows 32*(w%4).. (its TMEM lanes), query columns [16*cq, +16) of each step
+    const int cq = (warp - 4) >> 2, quarter = warp & 3;
+    const int r = quarter * 32 + lane;             // key row within the tile
+    const int key = kt * TK + r;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const float* L = lse + (long long)bh * S;
+    const float* Dr = dsum + (long long)bh * S;
+    for (int it = 0; it < n; ++it) {
+      const int bb = it & 1;
+      const int q0 = (i0 + it) * 64 + cq * 16;     // first query column of this thread's 16
+      float nl[16], dn[16];
+#pragma unroll
+      for (int e4 = 0; e4 < 4; ++e4) {
+        const float4 lv = __ldg(reinterpret_cast<const float4*>(L + q0) + e4);
+        const float4 dv4 = __ldg(reinterpret_cast<const float4*>(Dr + q0) + e4);
+        nl[4 * e4] = -lv.x * kLog2e;
+        nl[4 * e4 + 1] = -lv.y * kLog2e;
+        nl[4 * e4 + 2] = -lv.z * kLog2e;
+        nl[4 * e4 + 3] = -lv.w * kLog2e;
+        dn[4 * e4] = dv4.x;
+        dn[4 * e4 + 1] = dv4.y;
+        dn[4 * e4 + 2] = dv4.z;
+        dn[4 * e4 + 3] = dv4.w;
+      }
+      mbar_wait(&bars->s_full[bb], (it >> 1) & 1);
+      tc_fence_after();
+      uint32_t sv[16], dpv[16];
+      tmem_ld_32x16(tmem + bb * 64 + cq * 16 + lane_off, sv);
+      tmem_ld_32x16(tmem + 128 + bb * 64 + cq * 16 + lane_off, dpv);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->s_free[bb]);
+      uint32_t pk[8], dk8[8];
+      // causal: P = 0 where key > query, i.e. column e < key - q0 + 1 ... (e + q0 < key)
+      if (q0 < kt * TK + TK)   // warp-uniform: only the two diagonal steps mask
+        p_ds_16<true>(sv, dpv, nl, dn, scale_log2, key - q0, true, pk, dk8);
+      else
+        p_ds_16<false>(sv, dpv, nl, dn, scale_log2, 0, true, pk, dk8);
+      if (it > 0) mbar_wait(&bars->p_free, (it - 1) & 1);   // dV/dK of the previous step read P^T, dS^T
+      store_row16_narrow(sPT, r, cq, pk);
+      store_row16_narrow(sdST, r, cq, dk8);
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->p_full);
+    }
+    mbar_wait(&bars->acc_full, 0);
+    tc_fence_after();
+    store_acc_32(dv + (long long)(row0 + key) * ld + col0 + cq * 32, tmem + 256 + cq * 32 + lane_off, 1.0f);
+    store_acc_32(dk + (long long)(row0 + key) * ld + col0 + cq * 32, tmem + 384 + cq * 32 + lane_off, scale);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+// dQ for one 128-query tile, 64 keys per step.
+//   TMEM: S[2] [0,128), dP[2] [128,256), dQ [256,384)
+//   smem: Q, dO (fixed); K|V ring of Q2_STAGES 64-row stages; dS (128 x 64, K-major).
+//   MMA order: S0 dP0 S1 dP1 | dQ0 S2 dP2 | dQ1 S3 dP3 | ...
+constexpr int Q2_STAGES = 4;
+struct BwdQ2Bars {
+  uint64_t q_full, kv_full[Q2_STAGES], kv_empty[Q2_STAGES], s_full[2], s_free[2], ds_full, ds_free, acc_full;
+  uint32_t tmem;
+};
+constexpr int BWD_Q2_SMEM = TILE_BYTES * 2 + Q2_STAGES * 2 * HALF_TILE + HALF_TILE + 1024 + 256;
+constexpr int BWD_Q2_THREADS = 640;
+
+__global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
+    flash_bwd_dq_tc2(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k64,
+                     const __grid_constant__ CUtensorMap map_v64, const __grid_constant__ CUtensorMap map_do,
+                     const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dq,
+                     int S, int H, int ld, float scale, float scale_log2) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sQ = smem, *sdO = smem + TILE_BYTES;
+  auto sK = [&](int st) { return smem + 2 * TILE_BYTES + st * 2 * HALF_TILE; };
+  auto sV = [&](int st) { return smem + 2 * TILE_BYTES + st * 2 * HALF_TILE + HALF_TILE; };
+  uint8_t* sdS = smem + 2 * TILE_BYTES + Q2_STAGES * 2 * HALF_TILE;
+  BwdQ2Bars* bars = reinterpret_cast<BwdQ2Bars*>(sdS + HALF_TILE);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int qt = (int)(gridDim.x - 1 - blockIdx.x);
+  const int bh = blockIdx.y, b = bh / H, hh = bh % H;
+  const int row0 = b * S, col0 = hh * HD;
+  const int n = 2 * qt + 2;                        // 64-key steps 0 .. 2 qt + 1
+  if (threadIdx.x == 0) {
+    tma_prefetch(&map_q);
+    tma_prefetch(&map_k64);
+    tma_prefetch(&map_v64);
+    tma_prefetch(&map_do);
+    mbar_init(&bars->q_full, 1);
+    for (int i = 0; i < Q2_STAGES; ++i) {
+      mbar_init(&bars->kv_full[i], 1);
+      mbar_init(&bars->kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars->s_full[i], 1);
+      mbar_init(&bars->s_free[i], 16);
+    }
+    mbar_init(&bars->ds_full, 16);
+    mbar_init(&bars->ds_free, 1);
+    mbar_init(&bars->acc_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(&bars->tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&bars->q_full, 2 * TILE_BYTES);
+      tma_load_2d(sQ, &map_q, &bars->q_full, col0, row0 + qt * TQ);
+      tma_load_2d(sQ + ATOM_BYTES, &map_q, &bars->q_full, col0 + 64, row0 + qt * TQ);
+      tma_load_2d(sdO, &map_do, &bars->q_full, col0, row0 + qt * TQ);
+      tma_load_2d(sdO + ATOM_BYTES, &map_do, &bars->q_full, col0 + 64, row0 + qt * TQ);
+      for (int j = 0; j < n; ++j) {
+        const int st = j % Q2_STAGES, ph = (j / Q2_STAGES) & 1;
+        const int r = row0 + j * 64;
+        mbar_wait(&bars->kv_empty[st], ph ^ 1);
+        mbar_arrive_expect_tx(&bars->kv_full[st], 2 * HALF_TILE);
+        tma_load_2d(sK(st), &map_k64, &bars->kv_full[st], col0, r);
+        tma_load_2d(sK(st) + HALF_ATOM, &map_k64, &bars->kv_full[st], col0 + 64, r);
+        tma_load_2d(sV(st), &map_v64, &bars->kv_full[st], col0, r);
+        tma_load_2d(sV(st) + HALF_ATOM, &map_v64, &bars->kv_full[st], col0 + 64, r);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_s = make_idesc_bf16(128, 64, false, false);
+    constexpr uint32_t idesc_acc = make_idesc_bf16(128, 128, false, true);
+    const uint32_t q_base = smem_u32(sQ), do_base = smem_u32(sdO), ds_base = smem_u32(sdS);
+    mbar_wait(&bars->q_full, 0);
+    auto issue_sdp = [&](int j) {
+      const int st = j % Q2_STAGES, bb = j & 1;
+      mbar_wait(&bars->kv_full[st], (j / Q2_STAGES) & 1);
+      if (j >= 2) mbar_wait(&bars->s_free[bb], ((j - 2) >> 1) & 1);
+      tc_fence_after();
+      const uint32_t k_base = smem_u32(sK(st)), v_base = smem_u32(sV(st));
+      umma_chain_w<8, ATOM_BYTES / 16, 2, HALF_ATOM / 16, 2>(tmem + bb * 64, kmajor_desc(q_base, 0),
+                                                            kmajor_desc64(k_base, 0), idesc_s, 0u);
+      umma_chain_w<8, ATOM_BYTES / 16, 2, HALF_ATOM / 16, 2>(tmem + 128 + bb * 64, kmajor_desc(do_base, 0),
+                                                            kmajor_desc64(v_base, 0), idesc_s, 0u);
+      umma_commit_w(&bars->s_full[bb]);
+    };
+    issue_sdp(0);
+    issue_sdp(1);
+    for (int j = 0; j < n; ++j) {
+      const int st = j % Q2_STAGES;
+      mbar_wait(&bars->ds_full, j & 1);
+      tc_fence_after();
+      const uint32_t k_base = smem_u32(sK(st));
+      umma_chain_w<4, 0, 2, 512, 128>(tmem + 256, kmajor_desc_narrow(ds_base, 0), mnmajor_desc64(k_base, 0),
+                                      idesc_acc, j > 0 ? 1u : 0u);
+      umma_commit_w(&bars->ds_free);
+      umma_commit_w(&bars->kv_empty[st]);
+      if (j + 2 < n) issue_sdp(j + 2);
+    }
+    umma_commit_w(&bars->acc_full);
+  } else if (warp >= 4) {
+    // warp w: query rows 32*(w%4).. (its TMEM lanes), key columns [16*ck, +16) of each step
+    const int ck = (warp - 4) >> 2, quarter = warp & 3;
+    const int r = quarter * 32 + lane;             // query row within the tile
+    const int qpos = qt * TQ + r;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const float nl0 = -lse[(long long)bh * S + qpos] * kLog2e;
+    const float D = dsum[(long long)bh * S + qpos];
+    float nl[16], dn[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      nl[e] = nl0;
+      dn[e] = D;
+    }
+    for (int j = 0; j < n; ++j) {
+      const int bb = j & 1;
+      const int k0 = j * 64 + ck * 16;             // first key column of this thread's 16
+      mbar_wait(&bars->s_full[bb], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t sv[16], dpv[16];
+      tmem_ld_32x16(tmem + bb * 64 + ck * 16 + lane_off, sv);
+      tmem_ld_32x16(tmem + 128 + bb * 64 + ck * 16 + lane_off, dpv);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->s_free[bb]);
+      uint32_t pk[8], ds8[8];
+      // causal: P = 0 where key > query, i.e. column e > qpos - k0
+      if (j >= 2 * qt)   // warp-uniform: the two diagonal steps
+        p_ds_16<true>(sv, dpv, nl, dn, scale_log2, qpos - k0, false, pk, ds8);
+      else
+        p_ds_16<false>(sv, dpv, nl, dn, scale_log2, 0, false, pk, ds8);
+      if (j > 0) mbar_wait(&bars->ds_free, (j - 1) & 1);   // dQ of the previous step read dS
+      store_row16_narrow(sdS, r, ck, ds8);
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->ds_full);
+    }
+    mbar_wait(&bars->acc_full, 0);
+    tc_fence_after();
+    store_acc_32(dq + (long long)(row0 + qpos) * ld + col0 + ck * 32, tmem + 256 + ck * 32 + lane_off, scale);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-bool make_map_2d(CUtensorMap* map, const void* ptr, long long rows, int ld) {
+bool make_map_2d(CUtensorMap* map, const void* ptr, long long rows, int ld, int box_rows = 128) {
   static EncodeTiledFn fn = nullptr;
   if (!fn) {
     cudaDriverEntryPointQueryResult q;
@@ -1008,7 +1398,7 @@ bool make_map_2d(CUtensorMap* map, const void* ptr, long long rows, int ld) {
   }
   cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-  cuuint32_t box[2] = {64, 128};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1033,10 +1423,16 @@ int hlm_flash_fwd_tc(const void* q, const void* k, const void* v, void* o, float
   }
   static const bool pp = std::getenv("HLM_ATTN_FWD_V1") == nullptr;
   if (pp && S % (2 * TQ) == 0) {   // two query tiles per CTA
-    auto kern = flash_fwd_pp;
+    static const int emu = [] {
+      const char* e = std::getenv("HLM_ATTN_EXP_EMU");
+      return e ? std::atoi(e) : 1;
+    }();
+    auto kern = emu >= 2 ? flash_fwd_pp<2> : emu == 1 ? flash_fwd_pp<1> : flash_fwd_pp<0>;
     static bool attr_pp = false;
     if (!attr_pp) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PP_SMEM);
+      cudaFuncSetAttribute(flash_fwd_pp<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, PP_SMEM);
+      cudaFuncSetAttribute(flash_fwd_pp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, PP_SMEM);
+      cudaFuncSetAttribute(flash_fwd_pp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, PP_SMEM);
       attr_pp = true;
     }
     dim3 grid(S / (2 * TQ), B * H);
@@ -1068,6 +1464,25 @@ int hlm_flash_bwd_tc(const void* q, const void* k, const void* v, const void* d_
   }
   const float scale = 1.0f / sqrtf((float)HD);
   dim3 grid(S / TQ, B * H);
+  static const bool v1 = std::getenv("HLM_ATTN_BWD_V1") != nullptr;
+  if (!v1) {   // 64-wide steps, double-buffered S / dP (default)
+    CUtensorMap mq64, mk64, mv64, mdo64;
+    if (!make_map_2d(&mq64, q, rows, ld, 64) || !make_map_2d(&mk64, k, rows, ld, 64) ||
+        !make_map_2d(&mv64, v, rows, ld, 64) || !make_map_2d(&mdo64, d_o, rows, ld, 64))
+      return 3;
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaFuncSetAttribute(flash_bwd_dkv_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_KV2_SMEM);
+      cudaFuncSetAttribute(flash_bwd_dq_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_Q2_SMEM);
+      attr2 = true;
+    }
+    flash_bwd_dkv_tc2<<<grid, BWD_KV2_THREADS, BWD_KV2_SMEM, s>>>(
+        mq64, mk, mv, mdo64, lse, dsum, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, S, H, ld, scale, scale * kLog2e);
+    flash_bwd_dq_tc2<<<grid, BWD_Q2_THREADS, BWD_Q2_SMEM, s>>>(mq, mk64, mv64, mdo, lse, dsum, (__nv_bfloat16*)dq,
+                                                              S, H, ld, scale, scale * kLog2e);
+    hlm_count_launches(2);
+    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+  }
   flash_bwd_dkv_tc<<<grid, BWD_KV_THREADS, BWD_KV_SMEM, s>>>(mq, mk, mv, mdo, lse, dsum, (__nv_bfloat16*)dk,
                                                    (__nv_bfloat16*)dv, S, H, ld, scale, scale * kLog2e);
   flash_bwd_dq_tc<<<grid, FWD_THREADS, BWD_Q_SMEM, s>>>(mq, mk, mv, mdo, lse, dsum, (__nv_bfloat16*)dq, S, H, ld, scale,

@@ -91,6 +91,89 @@ __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a_desc, uint
       "}\n" ::"r"(d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
+// Warp-converged issue: the whole warp executes these and elect.sync picks the issuing
+// thread inside the asm. With the operands warp-uniform, ptxas emits one UTCHMMA per call
+// straight from uniform registers; behind `if (lane == 0)` it instead wraps every MMA in
+// an ELECT / R2UR.BROADCAST / BRA.U.ANY loop (~14 instructions, which bounds the issue
+// rate of short MMAs such as the attention tiles' N = 64 / 128 ones).
+__device__ __forceinline__ void umma_bf16_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// A operand from TMEM (a_tmem), B from shared memory
+__device__ __forceinline__ void umma_bf16_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// A chain of N (4 or 8) MMAs along K into one accumulator, both operands in shared memory,
+// from two base descriptors: step kk adds (kk / 4) * HI + (kk % 4) * LO (16-byte units) to
+// each descriptor's address field, in PTX, so ptxas moves the bases into uniform registers
+// once and advances them with UIADD3.64 (K-major SW128: LO 2, HI = swizzle-atom bytes / 16;
+// MN-major: LO 128, HI 512). The first MMA accumulates iff acc_first != 0.
+template <int N, int AHI, int ALO, int BHI, int BLO>
+__device__ __forceinline__ void umma_chain_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t acc_first) {
+  static_assert(N == 4 || N == 8, "chain of 4 or 8");
+#define HLM_MMA_STEP(k)                                             \
+  "add.s64 ta, %1, " #k "a; add.s64 tb, %2, " #k "b;\n"              \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %3, 1;\n"
+  if constexpr (N == 4) {
+    asm volatile(
+        "{\n.reg .pred e, p;\n.reg .b64 ta, tb;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "add.s64 ta, %1, %5; add.s64 tb, %2, %6;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %3, 1;\n"
+        "add.s64 ta, %1, %7; add.s64 tb, %2, %8;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %3, 1;\n"
+        "add.s64 ta, %1, %9; add.s64 tb, %2, %10;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %3, 1;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(acc_first), "n"(ALO), "n"(BLO), "n"(2 * ALO), "n"(2 * BLO),
+        "n"(3 * ALO), "n"(3 * BLO));
+  } else {
+    asm volatile(
+        "{\n.reg .pred e, p;\n.reg .b64 ta, tb;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "add.s64 ta, %1, %5; add.s64 tb, %2, %6;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %3, 1;\n"
+        "add.s64 ta, %1, %7; add.s64 tb, %2, %8;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %3, 1;\n"
+        "add.s64 ta, %1, %9; add.s64 tb, %2, %10;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %3, 1;\n"
+        "add.s64 ta, %1, %11; add.s64 tb, %2, %12;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %3, 1;\n"
+        "add.s64 ta, %1, %13; add.s64 tb, %2, %14;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %3, 1;\n"
+        "add.s64 ta, %1, %15; add.s64 tb, %2, %16;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %3, 1;\n"
+        "add.s64 ta, %1, %17; add.s64 tb, %2, %18;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %3, 1;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(acc_first), "n"(ALO), "n"(BLO), "n"(2 * ALO), "n"(2 * BLO),
+        "n"(3 * ALO), "n"(3 * BLO), "n"(AHI), "n"(BHI), "n"(AHI + ALO), "n"(BHI + BLO), "n"(AHI + 2 * ALO),
+        "n"(BHI + 2 * BLO), "n"(AHI + 3 * ALO), "n"(BHI + 3 * BLO));
+  }
+#undef HLM_MMA_STEP
+}
+
+__device__ __forceinline__ void umma_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 // Arrive on an mbarrier once every previously issued tcgen05.mma completed.
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile(

@@ -97,3 +97,68 @@ def test_pingpong_forward_many_tiles(S, B, H, scale):
     _, _, _, o_ref, lse_ref = torch_ref(q, k, v, B, S, H, hd)
     assert rel(o, o_ref.permute(0, 2, 1, 3).reshape(T, h)) < 1e-2
     assert torch.allclose(lse.view(B, H, S), lse_ref, atol=5e-3 * scale, rtol=1e-4)
+
+
+@pytest.mark.parametrize("S,B,H,scale", [(2048, 1, 1, 1.0), (1024, 2, 2, 3.0)])
+def test_backward_long_sequence(S, B, H, scale):
+    """The 64-wide backward steps over many query / key tiles (Q|dO and K|V rings wrap,
+    S / dP TMEM buffers alternate) with spread-out scores, against torch fp32."""
+    torch.manual_seed(S + B)
+    dev, hd = "cuda", 128
+    h, T = H * hd, B * S
+    q, k = ((torch.randn(T, h, device=dev) * scale).bfloat16() for _ in range(2))
+    v, do = (torch.randn(T, h, device=dev).bfloat16() for _ in range(2))
+    o = torch.empty(T, h, device=dev, dtype=torch.bfloat16)
+    lse = torch.empty(B * H * S, device=dev)
+    d = L.HlmBlockDims(B, S, h, 8, H, 0)
+    Lb = L.blib()
+    L.check(Lb.hlm_cuda_attention_fwd(ctypes.byref(d), vp(q), vp(k), vp(v), vp(o), vp(lse), h, None))
+    dq, dk, dv = (torch.empty_like(q) for _ in range(3))
+    dsum = torch.empty(B * H * S, device=dev)
+    L.check(Lb.hlm_cuda_attention_bwd(ctypes.byref(d), vp(q), vp(k), vp(v), vp(o), vp(do), vp(lse),
+                                      vp(dsum), vp(dq), vp(dk), vp(dv), h, None))
+    torch.cuda.synchronize()
+    qf, kf, vf, o_ref, _ = torch_ref(q, k, v, B, S, H, hd)
+    o_ref.permute(0, 2, 1, 3).reshape(T, h).backward(do.float())
+    for got, ref in ((dq, qf.grad), (dk, kf.grad), (dv, vf.grad)):
+        assert rel(got, ref.permute(0, 2, 1, 3).reshape(T, h)) < 2e-2
+
+
+_VARIANT_SCRIPT = r"""
+import ctypes, sys, torch
+sys.path.insert(0, {root!r})
+from paper_2602_04816_b200 import _lib as L
+torch.manual_seed(5)
+B, S, H, hd = 1, 512, 2, 128
+h, T = H * hd, B * S
+q, k, v, do = (torch.randn(T, h, device="cuda").bfloat16() for _ in range(4))
+o = torch.empty_like(q); lse = torch.empty(B * H * S, device="cuda")
+dq, dk, dv = (torch.empty_like(q) for _ in range(3)); ds = torch.empty_like(lse)
+d = L.HlmBlockDims(B, S, h, 8, H, 0)
+vp = lambda t: ctypes.c_void_p(t.data_ptr())
+Lb = L.blib()
+L.check(Lb.hlm_cuda_attention_fwd(ctypes.byref(d), vp(q), vp(k), vp(v), vp(o), vp(lse), h, None))
+L.check(Lb.hlm_cuda_attention_bwd(ctypes.byref(d), vp(q), vp(k), vp(v), vp(o), vp(do), vp(lse), vp(ds),
+                                  vp(dq), vp(dk), vp(dv), h, None))
+torch.save({{"o": o.cpu(), "dq": dq.cpu(), "dk": dk.cpu(), "dv": dv.cpu()}}, sys.argv[1])
+"""
+
+
+def test_kernel_variants_agree(tmp_path):
+    """Every selectable variant (exp2 on MUFU vs partly on the FMA pipe; 128- vs 64-wide
+    backward steps) gives the same attention within bf16 noise."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "v.py"
+    script.write_text(_VARIANT_SCRIPT.format(root=root))
+    outs = {}
+    for name, env in (("default", {}), ("emu0", {"HLM_ATTN_EXP_EMU": "0"}), ("emu2", {"HLM_ATTN_EXP_EMU": "2"}),
+                      ("bwd_v1", {"HLM_ATTN_BWD_V1": "1"})):
+        path = tmp_path / f"{name}.pt"
+        subprocess.run([sys.executable, str(script), str(path)], check=True, env={**os.environ, **env})
+        outs[name] = torch.load(path)
+    for name, o in outs.items():
+        for key in ("o", "dq", "dk", "dv"):
+            assert rel(o[key], outs["emu0"][key]) < 1e-2, (name, key)

@@ -1,10 +1,12 @@
-"""Causal attention forward / backward timing at the C2 shape (B8 S2048 H28 hd128)."""
+"""Causal attention forward / backward timing at the C2 shape (B8 S2048 H28 hd128).
+Kernel variants are chosen by environment (HLM_ATTN_EXP_EMU, HLM_ATTN_BWD_V1), read once
+per process: run this once per variant."""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2602_04816_b200 import _lib as L
 Lb = L.blib()
-B, S, H, hd = 8, 2048, 28, 128
+B, S, H, hd = (int(x) for x in os.environ.get("ATTN_SHAPE", "8,2048,28,128").split(","))
 h, T = H * hd, B * S
 dev = "cuda"
 q, k, v, do = (torch.randn(T, h, device=dev).bfloat16() for _ in range(4))
@@ -14,7 +16,7 @@ d = L.HlmBlockDims(B, S, h, 8, H, 0)
 vp = lambda t: ctypes.c_void_p(t.data_ptr())
 fwd = lambda: L.check(Lb.hlm_cuda_attention_fwd(ctypes.byref(d), vp(q), vp(k), vp(v), vp(o), vp(lse), h, None))
 bwd = lambda: L.check(Lb.hlm_cuda_attention_bwd(ctypes.byref(d), vp(q), vp(k), vp(v), vp(o), vp(do), vp(lse), vp(ds), vp(dq), vp(dk), vp(dv), h, None))
-def t(fn, it=10):
+def t(fn, it=20):
     for _ in range(3): fn()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(True), torch.cuda.Event(True)
@@ -24,4 +26,6 @@ def t(fn, it=10):
     return a.elapsed_time(b) / it
 fl = 2.0 * B * S * S * h   # causal fwd: QK^T and PV over the lower triangle
 tf = t(fwd); tb = t(bwd)
-print(f"fwd {tf:.3f} ms = {fl/tf/1e9:.0f} TFLOP/s ; bwd {tb:.3f} ms = {2.5*fl/tb/1e9:.0f} TFLOP/s (2.5x fwd flops)")
+tag = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("HLM_ATTN"))
+print(f"[{tag or 'default'}] fwd {tf:.3f} ms = {fl/tf/1e9:.0f} TFLOP/s ; bwd {tb:.3f} ms = "
+      f"{2.5*fl/tb/1e9:.0f} TFLOP/s (2.5x fwd flops)")
