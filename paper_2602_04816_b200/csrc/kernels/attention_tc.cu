@@ -124,6 +124,17 @@ __device__ __forceinline__ uint64_t kmajor_desc(uint32_t base, int kk) {
 __device__ __forceinline__ uint64_t mnmajor_desc(uint32_t base, int kk) {
   return make_sw128_desc(base + kk * 2048, ATOM_BYTES, 1024);
 }
+// 64-row tiles (64-wide steps): two 64 x 64 boxes
+constexpr int HALF_TILE = 64 * HD * 2;   // 16 KiB: 64 rows x 128 columns (two 64x64 SW128 boxes)
+constexpr int HALF_ATOM = 64 * 64 * 2;   // 8 KiB: one 64-row x 64-column swizzle box
+// K-major descriptor for K step kk of a 64-row x 128-column tile (two 8 KiB boxes)
+__device__ __forceinline__ uint64_t kmajor_desc64(uint32_t base, int kk) {
+  return make_sw128_desc(base + (kk >> 2) * HALF_ATOM + (kk & 3) * 32, 16, 1024);
+}
+// MN-major descriptor of the same 64-row tile used as B with N = its 128 columns, K = its rows
+__device__ __forceinline__ uint64_t mnmajor_desc64(uint32_t base, int kk) {
+  return make_sw128_desc(base + kk * 2048, HALF_ATOM, 1024);
+}
 
 __global__ void __launch_bounds__(FWD_THREADS, 1)
     flash_fwd_tc(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
@@ -595,6 +606,231 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
+// ------------------------------------------------------------------ forward, 64-key steps
+// Same two-query-tile ping-pong, but over 64-key steps with S double-buffered per tile:
+//   TMEM: S_A[2] [0,128) (64 each), S_B[2] [128,256), O_A [256,384), O_B [384,512).
+// S_t(j+2) goes into the buffer P_t(j) came from, right behind PV_t(j) (in-order tensor
+// pipe), so S_t(j+1) is already computed when tile t's softmax of step j ends: the
+// softmax of a tile no longer waits a PV + S round trip per step, only the tensor pipe.
+// K / V: KF_STAGES-deep ring of 64-row stages, released by tile B's PV (B uses every key).
+// A rare lazy rescale of O_t (row max up by more than 2^8) first waits for PV_t(j-1).
+constexpr int KF_STAGES = 4;
+struct PP2Bars {
+  uint64_t q_full, kv_full[KF_STAGES], kv_empty[KF_STAGES], s_full[2][2], p_full[2][2], pv_done[2], o_final[2];
+  uint32_t tmem;
+};
+constexpr int PP2_SMEM = TILE_BYTES * 2 + KF_STAGES * 2 * HALF_TILE + 1024 + 256;
+
+template <int kEmu>
+__global__ void __launch_bounds__(PP_THREADS, 1)
+    flash_fwd_pp2(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k64,
+                  const __grid_constant__ CUtensorMap map_v64, __nv_bfloat16* __restrict__ o, float* __restrict__ lse,
+                  int S, int H, int ld, float scale_log2) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  auto sQ = [&](int t) { return smem + t * TILE_BYTES; };
+  auto sK = [&](int st) { return smem + 2 * TILE_BYTES + st * 2 * HALF_TILE; };
+  auto sV = [&](int st) { return smem + 2 * TILE_BYTES + st * 2 * HALF_TILE + HALF_TILE; };
+  PP2Bars* bars = reinterpret_cast<PP2Bars*>(smem + 2 * TILE_BYTES + KF_STAGES * 2 * HALF_TILE);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int pair = (int)(gridDim.x - 1 - blockIdx.x);   // long (late) query tiles first
+  const int nb = 4 * pair + 4;                          // 64-key steps of query tile B (A: two fewer)
+  const int bh = blockIdx.y, b = bh / H, hh = bh % H;
+  const int row0 = b * S;
+  const int col0 = hh * HD;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&map_q);
+    tma_prefetch(&map_k64);
+    tma_prefetch(&map_v64);
+    mbar_init(&bars->q_full, 1);
+    for (int i = 0; i < KF_STAGES; ++i) {
+      mbar_init(&bars->kv_full[i], 1);
+      mbar_init(&bars->kv_empty[i], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&bars->s_full[t][0], 1);
+      mbar_init(&bars->s_full[t][1], 1);
+      mbar_init(&bars->p_full[t][0], 4);   // per buffer: a softmax can run a step ahead of its PV
+      mbar_init(&bars->p_full[t][1], 4);
+      mbar_init(&bars->pv_done[t], 1);
+      mbar_init(&bars->o_final[t], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&bars->tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&bars->q_full, 2 * TILE_BYTES);
+      for (int t = 0; t < 2; ++t) {
+        tma_load_2d(sQ(t), &map_q, &bars->q_full, col0, row0 + (2 * pair + t) * TQ);
+        tma_load_2d(sQ(t) + ATOM_BYTES, &map_q, &bars->q_full, col0 + 64, row0 + (2 * pair + t) * TQ);
+      }
+      for (int j = 0; j < nb; ++j) {
+        const int st = j % KF_STAGES;
+        const int r = row0 + j * 64;
+        mbar_wait(&bars->kv_empty[st], ((j / KF_STAGES) & 1) ^ 1);
+        mbar_arrive_expect_tx(&bars->kv_full[st], 2 * HALF_TILE);
+        tma_load_2d(sK(st), &map_k64, &bars->kv_full[st], col0, r);
+        tma_load_2d(sK(st) + HALF_ATOM, &map_k64, &bars->kv_full[st], col0 + 64, r);
+        tma_load_2d(sV(st), &map_v64, &bars->kv_full[st], col0, r);
+        tma_load_2d(sV(st) + HALF_ATOM, &map_v64, &bars->kv_full[st], col0 + 64, r);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_s = make_idesc_bf16(128, 64, false, false);
+    constexpr uint32_t idesc_o = make_idesc_bf16(128, 128, false, true);
+    const int n_t[2] = {nb - 2, nb};
+    mbar_wait(&bars->q_full, 0);
+    auto issue_s = [&](int t, int j) {
+      const int st = j % KF_STAGES;
+      mbar_wait(&bars->kv_full[st], (j / KF_STAGES) & 1);
+      tc_fence_after();
+      umma_chain_w<8, ATOM_BYTES / 16, 2, HALF_ATOM / 16, 2>(tmem + t * 128 + (j & 1) * 64,
+                                                            kmajor_desc(smem_u32(sQ(t)), 0),
+                                                            kmajor_desc64(smem_u32(sK(st)), 0), idesc_s, 0u);
+      umma_commit_w(&bars->s_full[t][j & 1]);
+    };
+    // O_t += P_t(j) V_j, P_t(j) (bf16) in the first 32 columns of S_t[j % 2]
+    auto issue_pv = [&](int t, int j) {
+      const int st = j % KF_STAGES;
+      mbar_wait(&bars->p_full[t][j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t v_base = smem_u32(sV(st));
+      const uint32_t p_tmem = tmem + t * 128 + (j & 1) * 64;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        umma_bf16_ts_w(tmem + 256 + t * 128, p_tmem + kk * 8, mnmajor_desc64(v_base, kk), idesc_o,
+                       (j > 0 || kk > 0) ? 1u : 0u);
+      umma_commit_w(&bars->pv_done[t]);
+      if (t == 1) umma_commit_w(&bars->kv_empty[st]);
+      if (j + 1 == n_t[t]) umma_commit_w(&bars->o_final[t]);
+    };
+    issue_s(0, 0);
+    issue_s(1, 0);
+    issue_s(0, 1);
+    issue_s(1, 1);
+    for (int j = 0; j < nb; ++j) {
+      for (int t = 0; t < 2; ++t) {
+        if (j >= n_t[t]) continue;
+        issue_pv(t, j);
+        if (j + 2 < n_t[t]) issue_s(t, j + 2);
+      }
+    }
+  } else {
+    const int t = (warp - 2) >> 2;                 // query tile A (0) or B (1)
+    const int quarter = warp & 3;                  // TMEM lanes 32*quarter ..
+    const int r = quarter * 32 + lane;             // query row within the tile
+    const int qt = 2 * pair + t, n = 2 * qt + 2;
+    const int qpos = qt * TQ + r;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const uint32_t s_base = tmem + t * 128 + lane_off, o_addr = tmem + 256 + t * 128 + lane_off;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < n; ++j) {
+      const uint32_t s_addr = s_base + (j & 1) * 64;
+      mbar_wait(&bars->s_full[t][j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t sv[2][32];
+      tmem_ld_32x32(s_addr, sv[0]);
+      tmem_ld_32x32(s_addr + 32, sv[1]);
+      tmem_ld_wait();
+      if (j >= 2 * qt) {   // the two diagonal steps (warp-uniform): mask keys above the row
+        const int k0 = j * 64;
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (k0 + c * 32 + e > qpos) sv[c][e] = __float_as_uint(-INFINITY);
+      }
+      float mx8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) mx8[u] = fmaxf(__uint_as_float(sv[0][u]), __uint_as_float(sv[0][u + 8]));
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int e = (c == 0 ? 16 : 0); e < 32; e += 2)
+          mx8[e & 7] = fmax3(mx8[e & 7], __uint_as_float(sv[c][e]), __uint_as_float(sv[c][e + 1]));
+      const float mx = scale_log2 * fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                          fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+      if (j == 0) {
+        m = mx;
+      } else if (__any_sync(0xffffffffu, mx > m + kRescaleLog2)) {
+        // O_t holds P V of steps < j; PV_t(j-1) may still run: wait for it, then rescale
+        mbar_wait(&bars->pv_done[t], (j - 1) & 1);
+        tc_fence_after();
+        const float mn = fmaxf(m, mx);
+        const float alpha = ex2(m - mn);
+#pragma unroll 1
+        for (int c = 0; c < 8; ++c) {
+          uint32_t ov[16];
+          tmem_ld_32x16(o_addr + c * 16, ov);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+          tmem_st_32x16(o_addr + c * 16, ov);
+        }
+        tmem_st_wait();
+        l *= alpha;
+        m = mn;
+      }
+      // P = 2^(s * scale_log2 - m) <= 2^8 as bf16 pairs into the first 32 columns of S_t[j % 2]
+      const float negm = -m;
+      float l8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          float a0, a1;
+          ffma2(a0, a1, __uint_as_float(sv[c][2 * e]), __uint_as_float(sv[c][2 * e + 1]), scale_log2, negm);
+          float p0, p1;
+          if ((e & 3) < kEmu) {
+            ex2_poly2(p0, p1, a0, a1);
+          } else {
+            p0 = ex2(a0);
+            p1 = ex2(a1);
+          }
+          fadd2(l8[2 * (e & 3)], l8[2 * (e & 3) + 1], p0, p1);
+          pk[e] = pack_bf16x2(p0, p1);
+        }
+        tmem_st_32x16(s_addr + c * 16, pk);
+      }
+      l += ((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7]));
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->p_full[t][j & 1]);
+    }
+    mbar_wait(&bars->o_final[t], 0);
+    tc_fence_after();
+    const float il = 1.f / l;
+    __nv_bfloat16* orow = o + (long long)(row0 + qpos) * ld + col0;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t ov[32];
+      tmem_ld_32x32(o_addr + c * 32, ov);
+      tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        reinterpret_cast<uint4*>(orow + c * 32)[q] =
+            make_uint4(pack_bf16x2(__uint_as_float(ov[8 * q]) * il, __uint_as_float(ov[8 * q + 1]) * il),
+                       pack_bf16x2(__uint_as_float(ov[8 * q + 2]) * il, __uint_as_float(ov[8 * q + 3]) * il),
+                       pack_bf16x2(__uint_as_float(ov[8 * q + 4]) * il, __uint_as_float(ov[8 * q + 5]) * il),
+                       pack_bf16x2(__uint_as_float(ov[8 * q + 6]) * il, __uint_as_float(ov[8 * q + 7]) * il));
+    }
+    lse[(long long)bh * S + qpos] = (m + log2f(l)) / kLog2e;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
 // ------------------------------------------------------------------ backward
 // Shared pieces: a 128-row bf16 tile written by 128 threads (thread = row) into
 // the K-major SW128 layout the MMA A operand expects (two 64-column atoms).
@@ -1017,17 +1253,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 // MMAs of step i+1 (and the accumulating MMAs of step i-1) run under the elementwise work
 // of step i. The elementwise warps copy S / dP into registers and release the TMEM buffer
 // before computing. Same per-element arithmetic as the 128-wide kernels.
-constexpr int HALF_TILE = 64 * HD * 2;   // 16 KiB: 64 rows x 128 columns (two 64x64 SW128 boxes)
-constexpr int HALF_ATOM = 64 * 64 * 2;   // 8 KiB: one 64-row x 64-column swizzle box
-
-// K-major descriptor for K step kk of a 64-row x 128-column tile (two 8 KiB boxes)
-__device__ __forceinline__ uint64_t kmajor_desc64(uint32_t base, int kk) {
-  return make_sw128_desc(base + (kk >> 2) * HALF_ATOM + (kk & 3) * 32, 16, 1024);
-}
-// MN-major descriptor of the same 64-row tile used as B with N = its 128 columns, K = its rows
-__device__ __forceinline__ uint64_t mnmajor_desc64(uint32_t base, int kk) {
-  return make_sw128_desc(base + kk * 2048, HALF_ATOM, 1024);
-}
 // K-major descriptor of a 128-row x 64-column bf16 tile (one swizzle atom column), K step kk < 4
 __device__ __forceinline__ uint64_t kmajor_desc_narrow(uint32_t base, int kk) {
   return make_sw128_desc(base + kk * 32, 16, 1024);
@@ -1069,16 +1294,43 @@ __device__ __forceinline__ void p_ds_16(const uint32_t (&sv)[16], const uint32_t
 
 // dK, dV for one 128-key tile, 64 queries per step.
 //   TMEM: S^T[2] [0,128) (64 each), dP^T[2] [128,256), dV [256,384), dK [384,512)
-//   smem: K, V (fixed); Q|dO ring of KV2_STAGES 64-row stages; P^T, dS^T (128 keys x 64
-//   queries, K-major), single-buffered: written once the previous step's dV/dK MMAs read them.
+//   smem: K, V (fixed); a ring of KV2_STAGES stages, each Q|dO (64 rows) plus that step's
+//   log-sum-exp and D (bulk-copied beside them, read as broadcasts); P^T, dS^T (128 keys x
+//   64 queries, K-major), double-buffered so step i+1 stores while dV/dK of step i run.
 //   MMA order: S0 dP0 S1 dP1 | dV0 dK0 S2 dP2 | dV1 dK1 S3 dP3 | ...
-constexpr int KV2_STAGES = 4;
+constexpr int KV2_STAGES = 3;
 struct BwdKV2Bars {
-  uint64_t kv_full, q_full[KV2_STAGES], q_empty[KV2_STAGES], s_full[2], s_free[2], p_full, p_free, acc_full;
+  uint64_t kv_full, q_full[KV2_STAGES], q_empty[KV2_STAGES], s_full[2], s_free[2], p_full[2], p_free[2], acc_full;
   uint32_t tmem;
 };
-constexpr int BWD_KV2_SMEM = TILE_BYTES * 2 + KV2_STAGES * 2 * HALF_TILE + 2 * HALF_TILE + 1024 + 256;
+constexpr int KV2_LD_BYTES = 2 * 64 * 4;   // per stage: lse[64], D[64]
+constexpr int BWD_KV2_SMEM =
+    TILE_BYTES * 2 + KV2_STAGES * 2 * HALF_TILE + 4 * HALF_TILE + KV2_STAGES * KV2_LD_BYTES + 1024 + 256;
 constexpr int BWD_KV2_THREADS = 640;   // 4 control warps + 16 elementwise warps
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ float4 ld_shared_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+// 16 bf16 columns (group c16 < 4) of row r of a 128 x 64 K-major SW128 tile at shared address `tile`
+__device__ __forceinline__ void st_row16_narrow(uint32_t tile, int r, int c16, const uint32_t (&pk)[8]) {
+  const uint32_t row = tile + r * 128;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int chunk = c16 * 2 + q;
+    st_shared_v4(row + ((chunk ^ (r & 7)) << 4), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+  }
+}
 
 __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
     flash_bwd_dkv_tc2(const __grid_constant__ CUtensorMap map_q64, const __grid_constant__ CUtensorMap map_k,
@@ -1090,9 +1342,11 @@ __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
   uint8_t *sK = smem, *sV = smem + TILE_BYTES;
   auto sQ = [&](int st) { return smem + 2 * TILE_BYTES + st * 2 * HALF_TILE; };
   auto sdO = [&](int st) { return smem + 2 * TILE_BYTES + st * 2 * HALF_TILE + HALF_TILE; };
-  uint8_t* sPT = smem + 2 * TILE_BYTES + KV2_STAGES * 2 * HALF_TILE;
-  uint8_t* sdST = sPT + HALF_TILE;
-  BwdKV2Bars* bars = reinterpret_cast<BwdKV2Bars*>(sdST + HALF_TILE);
+  uint8_t* sPT0 = smem + 2 * TILE_BYTES + KV2_STAGES * 2 * HALF_TILE;   // P^T[2] then dS^T[2]
+  auto sPT = [&](int bb) { return sPT0 + bb * HALF_TILE; };
+  auto sdST = [&](int bb) { return sPT0 + (2 + bb) * HALF_TILE; };
+  float* sLD = reinterpret_cast<float*>(sPT0 + 4 * HALF_TILE);         // [stage][lse 64 | D 64]
+  BwdKV2Bars* bars = reinterpret_cast<BwdKV2Bars*>(sPT0 + 4 * HALF_TILE + KV2_STAGES * KV2_LD_BYTES);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int kt = (int)blockIdx.x;        // key tile (early tiles have the longest loops: launched first)
   const int i0 = 2 * kt, n = S / 64 - i0;   // query steps i0 .. S/64 - 1
@@ -1111,9 +1365,9 @@ __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars->s_full[i], 1);
       mbar_init(&bars->s_free[i], 16);
+      mbar_init(&bars->p_full[i], 16);
+      mbar_init(&bars->p_free[i], 1);
     }
-    mbar_init(&bars->p_full, 16);
-    mbar_init(&bars->p_free, 1);
     mbar_init(&bars->acc_full, 1);
     fence_barrier_init();
   }
@@ -1130,22 +1384,25 @@ __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
       tma_load_2d(sK + ATOM_BYTES, &map_k, &bars->kv_full, col0 + 64, row0 + kt * TK);
       tma_load_2d(sV, &map_v, &bars->kv_full, col0, row0 + kt * TK);
       tma_load_2d(sV + ATOM_BYTES, &map_v, &bars->kv_full, col0 + 64, row0 + kt * TK);
+      const float* L = lse + (long long)bh * S;
+      const float* Dr = dsum + (long long)bh * S;
       for (int it = 0; it < n; ++it) {
         const int st = it % KV2_STAGES, ph = (it / KV2_STAGES) & 1;
-        const int r = row0 + (i0 + it) * 64;
+        const int q0 = (i0 + it) * 64;
         mbar_wait(&bars->q_empty[st], ph ^ 1);
-        mbar_arrive_expect_tx(&bars->q_full[st], 2 * HALF_TILE);
-        tma_load_2d(sQ(st), &map_q64, &bars->q_full[st], col0, r);
-        tma_load_2d(sQ(st) + HALF_ATOM, &map_q64, &bars->q_full[st], col0 + 64, r);
-        tma_load_2d(sdO(st), &map_do64, &bars->q_full[st], col0, r);
-        tma_load_2d(sdO(st) + HALF_ATOM, &map_do64, &bars->q_full[st], col0 + 64, r);
+        mbar_arrive_expect_tx(&bars->q_full[st], 2 * HALF_TILE + KV2_LD_BYTES);
+        tma_load_2d(sQ(st), &map_q64, &bars->q_full[st], col0, row0 + q0);
+        tma_load_2d(sQ(st) + HALF_ATOM, &map_q64, &bars->q_full[st], col0 + 64, row0 + q0);
+        tma_load_2d(sdO(st), &map_do64, &bars->q_full[st], col0, row0 + q0);
+        tma_load_2d(sdO(st) + HALF_ATOM, &map_do64, &bars->q_full[st], col0 + 64, row0 + q0);
+        bulk_load(sLD + st * 128, L + q0, 256, &bars->q_full[st]);
+        bulk_load(sLD + st * 128 + 64, Dr + q0, 256, &bars->q_full[st]);
       }
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc_s = make_idesc_bf16(128, 64, false, false);    // S^T, dP^T: N = 64 queries
     constexpr uint32_t idesc_acc = make_idesc_bf16(128, 128, false, true);  // dV, dK: B MN-major
-    const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV), pt_base = smem_u32(sPT),
-                   dst_base = smem_u32(sdST);
+    const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV);
     mbar_wait(&bars->kv_full, 0);
     auto issue_sdp = [&](int it) {
       const int st = it % KV2_STAGES, bb = it & 1;
@@ -1162,15 +1419,15 @@ __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
     issue_sdp(0);
     if (n > 1) issue_sdp(1);
     for (int it = 0; it < n; ++it) {
-      const int st = it % KV2_STAGES;
-      mbar_wait(&bars->p_full, it & 1);
+      const int st = it % KV2_STAGES, bb = it & 1;
+      mbar_wait(&bars->p_full[bb], (it >> 1) & 1);
       tc_fence_after();
       const uint32_t q_base = smem_u32(sQ(st)), do_base = smem_u32(sdO(st));
-      umma_chain_w<4, 0, 2, 512, 128>(tmem + 256, kmajor_desc_narrow(pt_base, 0), mnmajor_desc64(do_base, 0),
-                                      idesc_acc, it > 0 ? 1u : 0u);
-      umma_chain_w<4, 0, 2, 512, 128>(tmem + 384, kmajor_desc_narrow(dst_base, 0), mnmajor_desc64(q_base, 0),
-                                      idesc_acc, it > 0 ? 1u : 0u);
-      umma_commit_w(&bars->p_free);
+      umma_chain_w<4, 0, 2, 512, 128>(tmem + 256, kmajor_desc_narrow(smem_u32(sPT(bb)), 0),
+                                      mnmajor_desc64(do_base, 0), idesc_acc, it > 0 ? 1u : 0u);
+      umma_chain_w<4, 0, 2, 512, 128>(tmem + 384, kmajor_desc_narrow(smem_u32(sdST(bb)), 0),
+                                      mnmajor_desc64(q_base, 0), idesc_acc, it > 0 ? 1u : 0u);
+      umma_commit_w(&bars->p_free[bb]);
       umma_commit_w(&bars->q_empty[st]);
       if (it + 2 < n) issue_sdp(it + 2);
     }
@@ -1181,16 +1438,21 @@ __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
     const int r = quarter * 32 + lane;             // key row within the tile
     const int key = kt * TK + r;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    const float* L = lse + (long long)bh * S;
-    const float* Dr = dsum + (long long)bh * S;
+    const uint32_t ld_base = smem_u32(sLD) + cq * 64;   // this warp's 16 columns of lse / D
     for (int it = 0; it < n; ++it) {
-      const int bb = it & 1;
+      const int bb = it & 1, st = it % KV2_STAGES;
       const int q0 = (i0 + it) * 64 + cq * 16;     // first query column of this thread's 16
+      mbar_wait(&bars->s_full[bb], (it >> 1) & 1);
+      tc_fence_after();
+      uint32_t sv[16], dpv[16];
+      tmem_ld_32x16(tmem + bb * 64 + cq * 16 + lane_off, sv);
+      tmem_ld_32x16(tmem + 128 + bb * 64 + cq * 16 + lane_off, dpv);
+      mbar_wait(&bars->q_full[st], (it / KV2_STAGES) & 1);   // lse / D landed with this step's Q
       float nl[16], dn[16];
 #pragma unroll
       for (int e4 = 0; e4 < 4; ++e4) {
-        const float4 lv = __ldg(reinterpret_cast<const float4*>(L + q0) + e4);
-        const float4 dv4 = __ldg(reinterpret_cast<const float4*>(Dr + q0) + e4);
+        const float4 lv = ld_shared_f4(ld_base + st * KV2_LD_BYTES + e4 * 16);
+        const float4 dv4 = ld_shared_f4(ld_base + st * KV2_LD_BYTES + 256 + e4 * 16);
         nl[4 * e4] = -lv.x * kLog2e;
         nl[4 * e4 + 1] = -lv.y * kLog2e;
         nl[4 * e4 + 2] = -lv.z * kLog2e;
@@ -1200,27 +1462,22 @@ __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
         dn[4 * e4 + 2] = dv4.z;
         dn[4 * e4 + 3] = dv4.w;
       }
-      mbar_wait(&bars->s_full[bb], (it >> 1) & 1);
-      tc_fence_after();
-      uint32_t sv[16], dpv[16];
-      tmem_ld_32x16(tmem + bb * 64 + cq * 16 + lane_off, sv);
-      tmem_ld_32x16(tmem + 128 + bb * 64 + cq * 16 + lane_off, dpv);
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->s_free[bb]);
       uint32_t pk[8], dk8[8];
-      // causal: P = 0 where key > query, i.e. column e < key - q0 + 1 ... (e + q0 < key)
+      // causal: P = 0 where key > query, i.e. column e < key - q0
       if (q0 < kt * TK + TK)   // warp-uniform: only the two diagonal steps mask
         p_ds_16<true>(sv, dpv, nl, dn, scale_log2, key - q0, true, pk, dk8);
       else
         p_ds_16<false>(sv, dpv, nl, dn, scale_log2, 0, true, pk, dk8);
-      if (it > 0) mbar_wait(&bars->p_free, (it - 1) & 1);   // dV/dK of the previous step read P^T, dS^T
-      store_row16_narrow(sPT, r, cq, pk);
-      store_row16_narrow(sdST, r, cq, dk8);
+      if (it >= 2) mbar_wait(&bars->p_free[bb], ((it - 2) >> 1) & 1);   // dV/dK of step it-2 read buffer bb
+      st_row16_narrow(smem_u32(sPT(bb)), r, cq, pk);
+      st_row16_narrow(smem_u32(sdST(bb)), r, cq, dk8);
       fence_proxy_async();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars->p_full);
+      if (lane == 0) mbar_arrive(&bars->p_full[bb]);
     }
     mbar_wait(&bars->acc_full, 0);
     tc_fence_after();
@@ -1234,14 +1491,14 @@ __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
 
 // dQ for one 128-query tile, 64 keys per step.
 //   TMEM: S[2] [0,128), dP[2] [128,256), dQ [256,384)
-//   smem: Q, dO (fixed); K|V ring of Q2_STAGES 64-row stages; dS (128 x 64, K-major).
+//   smem: Q, dO (fixed); K|V ring of Q2_STAGES 64-row stages; dS[2] (128 x 64, K-major).
 //   MMA order: S0 dP0 S1 dP1 | dQ0 S2 dP2 | dQ1 S3 dP3 | ...
 constexpr int Q2_STAGES = 4;
 struct BwdQ2Bars {
-  uint64_t q_full, kv_full[Q2_STAGES], kv_empty[Q2_STAGES], s_full[2], s_free[2], ds_full, ds_free, acc_full;
+  uint64_t q_full, kv_full[Q2_STAGES], kv_empty[Q2_STAGES], s_full[2], s_free[2], ds_full[2], ds_free[2], acc_full;
   uint32_t tmem;
 };
-constexpr int BWD_Q2_SMEM = TILE_BYTES * 2 + Q2_STAGES * 2 * HALF_TILE + HALF_TILE + 1024 + 256;
+constexpr int BWD_Q2_SMEM = TILE_BYTES * 2 + Q2_STAGES * 2 * HALF_TILE + 2 * HALF_TILE + 1024 + 256;
 constexpr int BWD_Q2_THREADS = 640;
 
 __global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
@@ -1254,8 +1511,9 @@ __global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
   uint8_t *sQ = smem, *sdO = smem + TILE_BYTES;
   auto sK = [&](int st) { return smem + 2 * TILE_BYTES + st * 2 * HALF_TILE; };
   auto sV = [&](int st) { return smem + 2 * TILE_BYTES + st * 2 * HALF_TILE + HALF_TILE; };
-  uint8_t* sdS = smem + 2 * TILE_BYTES + Q2_STAGES * 2 * HALF_TILE;
-  BwdQ2Bars* bars = reinterpret_cast<BwdQ2Bars*>(sdS + HALF_TILE);
+  uint8_t* sdS0 = smem + 2 * TILE_BYTES + Q2_STAGES * 2 * HALF_TILE;
+  auto sdS = [&](int bb) { return sdS0 + bb * HALF_TILE; };
+  BwdQ2Bars* bars = reinterpret_cast<BwdQ2Bars*>(sdS0 + 2 * HALF_TILE);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int qt = (int)(gridDim.x - 1 - blockIdx.x);
   const int bh = blockIdx.y, b = bh / H, hh = bh % H;
@@ -1274,9 +1532,9 @@ __global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars->s_full[i], 1);
       mbar_init(&bars->s_free[i], 16);
+      mbar_init(&bars->ds_full[i], 16);
+      mbar_init(&bars->ds_free[i], 1);
     }
-    mbar_init(&bars->ds_full, 16);
-    mbar_init(&bars->ds_free, 1);
     mbar_init(&bars->acc_full, 1);
     fence_barrier_init();
   }
@@ -1307,7 +1565,7 @@ __global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
   } else if (warp == 1) {
     constexpr uint32_t idesc_s = make_idesc_bf16(128, 64, false, false);
     constexpr uint32_t idesc_acc = make_idesc_bf16(128, 128, false, true);
-    const uint32_t q_base = smem_u32(sQ), do_base = smem_u32(sdO), ds_base = smem_u32(sdS);
+    const uint32_t q_base = smem_u32(sQ), do_base = smem_u32(sdO);
     mbar_wait(&bars->q_full, 0);
     auto issue_sdp = [&](int j) {
       const int st = j % Q2_STAGES, bb = j & 1;
@@ -1324,13 +1582,13 @@ __global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
     issue_sdp(0);
     issue_sdp(1);
     for (int j = 0; j < n; ++j) {
-      const int st = j % Q2_STAGES;
-      mbar_wait(&bars->ds_full, j & 1);
+      const int st = j % Q2_STAGES, bb = j & 1;
+      mbar_wait(&bars->ds_full[bb], (j >> 1) & 1);
       tc_fence_after();
       const uint32_t k_base = smem_u32(sK(st));
-      umma_chain_w<4, 0, 2, 512, 128>(tmem + 256, kmajor_desc_narrow(ds_base, 0), mnmajor_desc64(k_base, 0),
-                                      idesc_acc, j > 0 ? 1u : 0u);
-      umma_commit_w(&bars->ds_free);
+      umma_chain_w<4, 0, 2, 512, 128>(tmem + 256, kmajor_desc_narrow(smem_u32(sdS(bb)), 0),
+                                      mnmajor_desc64(k_base, 0), idesc_acc, j > 0 ? 1u : 0u);
+      umma_commit_w(&bars->ds_free[bb]);
       umma_commit_w(&bars->kv_empty[st]);
       if (j + 2 < n) issue_sdp(j + 2);
     }
@@ -1367,11 +1625,11 @@ __global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
         p_ds_16<true>(sv, dpv, nl, dn, scale_log2, qpos - k0, false, pk, ds8);
       else
         p_ds_16<false>(sv, dpv, nl, dn, scale_log2, 0, false, pk, ds8);
-      if (j > 0) mbar_wait(&bars->ds_free, (j - 1) & 1);   // dQ of the previous step read dS
-      store_row16_narrow(sdS, r, ck, ds8);
+      if (j >= 2) mbar_wait(&bars->ds_free[bb], ((j - 2) >> 1) & 1);   // dQ of step j-2 read buffer bb
+      st_row16_narrow(smem_u32(sdS(bb)), r, ck, ds8);
       fence_proxy_async();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars->ds_full);
+      if (lane == 0) mbar_arrive(&bars->ds_full[bb]);
     }
     mbar_wait(&bars->acc_full, 0);
     tc_fence_after();
@@ -1427,6 +1685,24 @@ int hlm_flash_fwd_tc(const void* q, const void* k, const void* v, void* o, float
       const char* e = std::getenv("HLM_ATTN_EXP_EMU");
       return e ? std::atoi(e) : 1;
     }();
+    static const bool v2 = std::getenv("HLM_ATTN_FWD_PP1") == nullptr;
+    if (v2) {   // 64-key steps, S double-buffered per tile (default)
+      CUtensorMap mk64, mv64;
+      if (!make_map_2d(&mk64, k, rows, ld, 64) || !make_map_2d(&mv64, v, rows, ld, 64)) return 3;
+      auto kern2 = emu >= 2 ? flash_fwd_pp2<2> : emu == 1 ? flash_fwd_pp2<1> : flash_fwd_pp2<0>;
+      static bool attr_pp2 = false;
+      if (!attr_pp2) {
+        cudaFuncSetAttribute(flash_fwd_pp2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, PP2_SMEM);
+        cudaFuncSetAttribute(flash_fwd_pp2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, PP2_SMEM);
+        cudaFuncSetAttribute(flash_fwd_pp2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, PP2_SMEM);
+        attr_pp2 = true;
+      }
+      dim3 grid(S / (2 * TQ), B * H);
+      kern2<<<grid, PP_THREADS, PP2_SMEM, s>>>(mq, mk64, mv64, (__nv_bfloat16*)o, lse, S, H, ld,
+                                               (1.0f / sqrtf((float)HD)) * kLog2e);
+      hlm_count_launches(1);
+      return cudaGetLastError() == cudaSuccess ? 0 : 1;
+    }
     auto kern = emu >= 2 ? flash_fwd_pp<2> : emu == 1 ? flash_fwd_pp<1> : flash_fwd_pp<0>;
     static bool attr_pp = false;
     if (!attr_pp) {
