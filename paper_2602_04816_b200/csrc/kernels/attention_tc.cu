@@ -390,6 +390,11 @@ __device__ __forceinline__ void tmem_st_32x32(uint32_t taddr, const uint32_t (&r
 __device__ __forceinline__ void tmem_st_32x16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]) : "memory");
 }
+__device__ __forceinline__ void tmem_st_32x8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // kEmu of every 4 exponentials per thread run on the FMA pipe (ex2_poly2), the rest on MUFU
@@ -1294,18 +1299,22 @@ __device__ __forceinline__ void p_ds_16(const uint32_t (&sv)[16], const uint32_t
 
 // dK, dV for one 128-key tile, 64 queries per step.
 //   TMEM: S^T[2] [0,128) (64 each), dP^T[2] [128,256), dV [256,384), dK [384,512)
+//   P^T and dS^T (bf16) are written back over S^T[b] / dP^T[b] and feed dV / dK as
+//   A operands from TMEM: the tensor core reads only Q and dO from shared memory (the
+//   shared-memory operand traffic of the 64-wide steps bounded the previous version).
+//   Warp cq turns its 16 query columns of S^T / dP^T into 8 packed columns at the same
+//   offset (16 cq), so the dV / dK MMA of K step kk reads its A at column 16 kk.
 //   smem: K, V (fixed); a ring of KV2_STAGES stages, each Q|dO (64 rows) plus that step's
-//   log-sum-exp and D (bulk-copied beside them, read as broadcasts); P^T, dS^T (128 keys x
-//   64 queries, K-major), double-buffered so step i+1 stores while dV/dK of step i run.
-//   MMA order: S0 dP0 S1 dP1 | dV0 dK0 S2 dP2 | dV1 dK1 S3 dP3 | ...
-constexpr int KV2_STAGES = 3;
+//   log-sum-exp and D (bulk-copied beside them, read as broadcasts).
+//   MMA order: S0 dP0 S1 dP1 | dV0 dK0 S2 dP2 | dV1 dK1 S3 dP3 | ...; S(i+2) reuses the
+//   buffers of step i behind dV(i) / dK(i) (in-order tensor pipe).
+constexpr int KV2_STAGES = 4;
 struct BwdKV2Bars {
-  uint64_t kv_full, q_full[KV2_STAGES], q_empty[KV2_STAGES], s_full[2], s_free[2], p_full[2], p_free[2], acc_full;
+  uint64_t kv_full, q_full[KV2_STAGES], q_empty[KV2_STAGES], s_full[2], p_full[2], acc_full;
   uint32_t tmem;
 };
 constexpr int KV2_LD_BYTES = 2 * 64 * 4;   // per stage: lse[64], D[64]
-constexpr int BWD_KV2_SMEM =
-    TILE_BYTES * 2 + KV2_STAGES * 2 * HALF_TILE + 4 * HALF_TILE + KV2_STAGES * KV2_LD_BYTES + 1024 + 256;
+constexpr int BWD_KV2_SMEM = TILE_BYTES * 2 + KV2_STAGES * 2 * HALF_TILE + KV2_STAGES * KV2_LD_BYTES + 1024 + 256;
 constexpr int BWD_KV2_THREADS = 640;   // 4 control warps + 16 elementwise warps
 
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -1332,6 +1341,9 @@ __device__ __forceinline__ void st_row16_narrow(uint32_t tile, int r, int c16, c
   }
 }
 
+// kExp (timing experiments only, results invalid when != 0): 1 skips the elementwise math,
+// 2 also skips the S / dP TMEM loads (HLM_ATTN_BWD_EXPERIMENT)
+template <int kExp>
 __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
     flash_bwd_dkv_tc2(const __grid_constant__ CUtensorMap map_q64, const __grid_constant__ CUtensorMap map_k,
                       const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do64,
@@ -1342,11 +1354,8 @@ __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
   uint8_t *sK = smem, *sV = smem + TILE_BYTES;
   auto sQ = [&](int st) { return smem + 2 * TILE_BYTES + st * 2 * HALF_TILE; };
   auto sdO = [&](int st) { return smem + 2 * TILE_BYTES + st * 2 * HALF_TILE + HALF_TILE; };
-  uint8_t* sPT0 = smem + 2 * TILE_BYTES + KV2_STAGES * 2 * HALF_TILE;   // P^T[2] then dS^T[2]
-  auto sPT = [&](int bb) { return sPT0 + bb * HALF_TILE; };
-  auto sdST = [&](int bb) { return sPT0 + (2 + bb) * HALF_TILE; };
-  float* sLD = reinterpret_cast<float*>(sPT0 + 4 * HALF_TILE);         // [stage][lse 64 | D 64]
-  BwdKV2Bars* bars = reinterpret_cast<BwdKV2Bars*>(sPT0 + 4 * HALF_TILE + KV2_STAGES * KV2_LD_BYTES);
+  float* sLD = reinterpret_cast<float*>(smem + 2 * TILE_BYTES + KV2_STAGES * 2 * HALF_TILE);   // [stage][lse|D]
+  BwdKV2Bars* bars = reinterpret_cast<BwdKV2Bars*>(reinterpret_cast<uint8_t*>(sLD) + KV2_STAGES * KV2_LD_BYTES);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int kt = (int)blockIdx.x;        // key tile (early tiles have the longest loops: launched first)
   const int i0 = 2 * kt, n = S / 64 - i0;   // query steps i0 .. S/64 - 1
@@ -1364,9 +1373,7 @@ __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars->s_full[i], 1);
-      mbar_init(&bars->s_free[i], 16);
       mbar_init(&bars->p_full[i], 16);
-      mbar_init(&bars->p_free[i], 1);
     }
     mbar_init(&bars->acc_full, 1);
     fence_barrier_init();
@@ -1407,7 +1414,6 @@ __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
     auto issue_sdp = [&](int it) {
       const int st = it % KV2_STAGES, bb = it & 1;
       mbar_wait(&bars->q_full[st], (it / KV2_STAGES) & 1);
-      if (it >= 2) mbar_wait(&bars->s_free[bb], ((it - 2) >> 1) & 1);
       tc_fence_after();
       const uint32_t q_base = smem_u32(sQ(st)), do_base = smem_u32(sdO(st));
       umma_chain_w<8, ATOM_BYTES / 16, 2, HALF_ATOM / 16, 2>(tmem + bb * 64, kmajor_desc(k_base, 0),
@@ -1423,11 +1429,14 @@ __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
       mbar_wait(&bars->p_full[bb], (it >> 1) & 1);
       tc_fence_after();
       const uint32_t q_base = smem_u32(sQ(st)), do_base = smem_u32(sdO(st));
-      umma_chain_w<4, 0, 2, 512, 128>(tmem + 256, kmajor_desc_narrow(smem_u32(sPT(bb)), 0),
-                                      mnmajor_desc64(do_base, 0), idesc_acc, it > 0 ? 1u : 0u);
-      umma_chain_w<4, 0, 2, 512, 128>(tmem + 384, kmajor_desc_narrow(smem_u32(sdST(bb)), 0),
-                                      mnmajor_desc64(q_base, 0), idesc_acc, it > 0 ? 1u : 0u);
-      umma_commit_w(&bars->p_free[bb]);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        umma_bf16_ts_w(tmem + 256, tmem + bb * 64 + 16 * kk, mnmajor_desc64(do_base, kk), idesc_acc,
+                       (it > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        umma_bf16_ts_w(tmem + 384, tmem + 128 + bb * 64 + 16 * kk, mnmajor_desc64(q_base, kk), idesc_acc,
+                       (it > 0 || kk > 0) ? 1u : 0u);
       umma_commit_w(&bars->q_empty[st]);
       if (it + 2 < n) issue_sdp(it + 2);
     }
@@ -1445,8 +1454,13 @@ __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
       mbar_wait(&bars->s_full[bb], (it >> 1) & 1);
       tc_fence_after();
       uint32_t sv[16], dpv[16];
-      tmem_ld_32x16(tmem + bb * 64 + cq * 16 + lane_off, sv);
-      tmem_ld_32x16(tmem + 128 + bb * 64 + cq * 16 + lane_off, dpv);
+      if (kExp < 2) {
+        tmem_ld_32x16(tmem + bb * 64 + cq * 16 + lane_off, sv);
+        tmem_ld_32x16(tmem + 128 + bb * 64 + cq * 16 + lane_off, dpv);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) sv[e] = dpv[e] = (uint32_t)e;
+      }
       mbar_wait(&bars->q_full[st], (it / KV2_STAGES) & 1);   // lse / D landed with this step's Q
       float nl[16], dn[16];
 #pragma unroll
@@ -1463,19 +1477,20 @@ __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
         dn[4 * e4 + 3] = dv4.w;
       }
       tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars->s_free[bb]);
       uint32_t pk[8], dk8[8];
       // causal: P = 0 where key > query, i.e. column e < key - q0
-      if (q0 < kt * TK + TK)   // warp-uniform: only the two diagonal steps mask
+      if (kExp >= 1) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) pk[e] = dk8[e] = sv[e] ^ dpv[e + 8] ^ __float_as_uint(nl[e] + dn[e]);
+      } else if (q0 < kt * TK + TK)   // warp-uniform: only the two diagonal steps mask
         p_ds_16<true>(sv, dpv, nl, dn, scale_log2, key - q0, true, pk, dk8);
       else
         p_ds_16<false>(sv, dpv, nl, dn, scale_log2, 0, true, pk, dk8);
-      if (it >= 2) mbar_wait(&bars->p_free[bb], ((it - 2) >> 1) & 1);   // dV/dK of step it-2 read buffer bb
-      st_row16_narrow(smem_u32(sPT(bb)), r, cq, pk);
-      st_row16_narrow(smem_u32(sdST(bb)), r, cq, dk8);
-      fence_proxy_async();
+      // P^T / dS^T over the columns this warp just read (A operands of dV / dK)
+      tmem_st_32x8(tmem + bb * 64 + cq * 16 + lane_off, pk);
+      tmem_st_32x8(tmem + 128 + bb * 64 + cq * 16 + lane_off, dk8);
+      tmem_st_wait();
+      tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->p_full[bb]);
     }
@@ -1490,50 +1505,63 @@ __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
 }
 
 // dQ for one 128-query tile, 64 keys per step.
-//   TMEM: S[2] [0,128), dP[2] [128,256), dQ [256,384)
-//   smem: Q, dO (fixed); K|V ring of Q2_STAGES 64-row stages; dS[2] (128 x 64, K-major).
-//   MMA order: S0 dP0 S1 dP1 | dQ0 S2 dP2 | dQ1 S3 dP3 | ...
-constexpr int Q2_STAGES = 4;
+//   TMEM: S[2] [0,128), dP[2] [128,256), dQ [256,384), Q [384,448), dO [448,512) (bf16 pairs)
+//   Q and dO are written into TMEM once by the elementwise warps (thread = row) and feed S
+//   and dP as A operands; dS (bf16) goes back over the dP columns it came from (warp ck:
+//   columns 16 ck .. +8) and feeds dQ as the A operand at column 16 kk. The tensor core
+//   reads only K and V from shared memory: 48 KB per step instead of 144 KB.
+//   smem: K|V ring of Q2_STAGES 64-row stages.
+//   MMA order: S0 dP0 S1 dP1 | dQ0 S2 dP2 | dQ1 S3 dP3 | ...; S / dP (j+2) reuse the
+//   buffers of step j behind dQ(j) (in-order tensor pipe).
+constexpr int Q2_STAGES = 6;
 struct BwdQ2Bars {
-  uint64_t q_full, kv_full[Q2_STAGES], kv_empty[Q2_STAGES], s_full[2], s_free[2], ds_full[2], ds_free[2], acc_full;
+  uint64_t q_ready, kv_full[Q2_STAGES], kv_empty[Q2_STAGES], s_full[2], ds_full[2], acc_full;
   uint32_t tmem;
 };
-constexpr int BWD_Q2_SMEM = TILE_BYTES * 2 + Q2_STAGES * 2 * HALF_TILE + 2 * HALF_TILE + 1024 + 256;
+constexpr int BWD_Q2_SMEM = Q2_STAGES * 2 * HALF_TILE + 1024 + 256;
 constexpr int BWD_Q2_THREADS = 640;
 
+// 32 bf16 of a global row into 16 TMEM columns (one tcgen05.st per warp: thread = lane = row)
+__device__ __forceinline__ void row32_to_tmem(uint32_t taddr, const __nv_bfloat16* src) {
+  uint32_t w[16];
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint4 v = __ldg(s4 + q);
+    w[4 * q] = v.x;
+    w[4 * q + 1] = v.y;
+    w[4 * q + 2] = v.z;
+    w[4 * q + 3] = v.w;
+  }
+  tmem_st_32x16(taddr, w);
+}
+
 __global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
-    flash_bwd_dq_tc2(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k64,
-                     const __grid_constant__ CUtensorMap map_v64, const __grid_constant__ CUtensorMap map_do,
+    flash_bwd_dq_tc2(const __nv_bfloat16* __restrict__ q, const __grid_constant__ CUtensorMap map_k64,
+                     const __grid_constant__ CUtensorMap map_v64, const __nv_bfloat16* __restrict__ d_o,
                      const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dq,
                      int S, int H, int ld, float scale, float scale_log2) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t *sQ = smem, *sdO = smem + TILE_BYTES;
-  auto sK = [&](int st) { return smem + 2 * TILE_BYTES + st * 2 * HALF_TILE; };
-  auto sV = [&](int st) { return smem + 2 * TILE_BYTES + st * 2 * HALF_TILE + HALF_TILE; };
-  uint8_t* sdS0 = smem + 2 * TILE_BYTES + Q2_STAGES * 2 * HALF_TILE;
-  auto sdS = [&](int bb) { return sdS0 + bb * HALF_TILE; };
-  BwdQ2Bars* bars = reinterpret_cast<BwdQ2Bars*>(sdS0 + 2 * HALF_TILE);
+  auto sK = [&](int st) { return smem + st * 2 * HALF_TILE; };
+  auto sV = [&](int st) { return smem + st * 2 * HALF_TILE + HALF_TILE; };
+  BwdQ2Bars* bars = reinterpret_cast<BwdQ2Bars*>(smem + Q2_STAGES * 2 * HALF_TILE);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int qt = (int)(gridDim.x - 1 - blockIdx.x);
   const int bh = blockIdx.y, b = bh / H, hh = bh % H;
   const int row0 = b * S, col0 = hh * HD;
   const int n = 2 * qt + 2;                        // 64-key steps 0 .. 2 qt + 1
   if (threadIdx.x == 0) {
-    tma_prefetch(&map_q);
     tma_prefetch(&map_k64);
     tma_prefetch(&map_v64);
-    tma_prefetch(&map_do);
-    mbar_init(&bars->q_full, 1);
+    mbar_init(&bars->q_ready, 16);
     for (int i = 0; i < Q2_STAGES; ++i) {
       mbar_init(&bars->kv_full[i], 1);
       mbar_init(&bars->kv_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars->s_full[i], 1);
-      mbar_init(&bars->s_free[i], 16);
       mbar_init(&bars->ds_full[i], 16);
-      mbar_init(&bars->ds_free[i], 1);
     }
     mbar_init(&bars->acc_full, 1);
     fence_barrier_init();
@@ -1546,11 +1574,6 @@ __global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(&bars->q_full, 2 * TILE_BYTES);
-      tma_load_2d(sQ, &map_q, &bars->q_full, col0, row0 + qt * TQ);
-      tma_load_2d(sQ + ATOM_BYTES, &map_q, &bars->q_full, col0 + 64, row0 + qt * TQ);
-      tma_load_2d(sdO, &map_do, &bars->q_full, col0, row0 + qt * TQ);
-      tma_load_2d(sdO + ATOM_BYTES, &map_do, &bars->q_full, col0 + 64, row0 + qt * TQ);
       for (int j = 0; j < n; ++j) {
         const int st = j % Q2_STAGES, ph = (j / Q2_STAGES) & 1;
         const int r = row0 + j * 64;
@@ -1565,18 +1588,20 @@ __global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
   } else if (warp == 1) {
     constexpr uint32_t idesc_s = make_idesc_bf16(128, 64, false, false);
     constexpr uint32_t idesc_acc = make_idesc_bf16(128, 128, false, true);
-    const uint32_t q_base = smem_u32(sQ), do_base = smem_u32(sdO);
-    mbar_wait(&bars->q_full, 0);
+    mbar_wait(&bars->q_ready, 0);
+    tc_fence_after();
     auto issue_sdp = [&](int j) {
       const int st = j % Q2_STAGES, bb = j & 1;
       mbar_wait(&bars->kv_full[st], (j / Q2_STAGES) & 1);
-      if (j >= 2) mbar_wait(&bars->s_free[bb], ((j - 2) >> 1) & 1);
       tc_fence_after();
       const uint32_t k_base = smem_u32(sK(st)), v_base = smem_u32(sV(st));
-      umma_chain_w<8, ATOM_BYTES / 16, 2, HALF_ATOM / 16, 2>(tmem + bb * 64, kmajor_desc(q_base, 0),
-                                                            kmajor_desc64(k_base, 0), idesc_s, 0u);
-      umma_chain_w<8, ATOM_BYTES / 16, 2, HALF_ATOM / 16, 2>(tmem + 128 + bb * 64, kmajor_desc(do_base, 0),
-                                                            kmajor_desc64(v_base, 0), idesc_s, 0u);
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk)
+        umma_bf16_ts_w(tmem + bb * 64, tmem + 384 + kk * 8, kmajor_desc64(k_base, kk), idesc_s, kk ? 1u : 0u);
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk)
+        umma_bf16_ts_w(tmem + 128 + bb * 64, tmem + 448 + kk * 8, kmajor_desc64(v_base, kk), idesc_s,
+                       kk ? 1u : 0u);
       umma_commit_w(&bars->s_full[bb]);
     };
     issue_sdp(0);
@@ -1586,9 +1611,10 @@ __global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
       mbar_wait(&bars->ds_full[bb], (j >> 1) & 1);
       tc_fence_after();
       const uint32_t k_base = smem_u32(sK(st));
-      umma_chain_w<4, 0, 2, 512, 128>(tmem + 256, kmajor_desc_narrow(smem_u32(sdS(bb)), 0),
-                                      mnmajor_desc64(k_base, 0), idesc_acc, j > 0 ? 1u : 0u);
-      umma_commit_w(&bars->ds_free[bb]);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        umma_bf16_ts_w(tmem + 256, tmem + 128 + bb * 64 + 16 * kk, mnmajor_desc64(k_base, kk), idesc_acc,
+                       (j > 0 || kk > 0) ? 1u : 0u);
       umma_commit_w(&bars->kv_empty[st]);
       if (j + 2 < n) issue_sdp(j + 2);
     }
@@ -1599,6 +1625,14 @@ __global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
     const int r = quarter * 32 + lane;             // query row within the tile
     const int qpos = qt * TQ + r;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    // this row's Q / dO, hd columns [32 ck, +32), into TMEM as bf16 pairs
+    const long long grow = (long long)(row0 + qpos) * ld + col0 + ck * 32;
+    row32_to_tmem(tmem + 384 + ck * 16 + lane_off, q + grow);
+    row32_to_tmem(tmem + 448 + ck * 16 + lane_off, d_o + grow);
+    tmem_st_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bars->q_ready);
     const float nl0 = -lse[(long long)bh * S + qpos] * kLog2e;
     const float D = dsum[(long long)bh * S + qpos];
     float nl[16], dn[16];
@@ -1616,18 +1650,15 @@ __global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
       tmem_ld_32x16(tmem + bb * 64 + ck * 16 + lane_off, sv);
       tmem_ld_32x16(tmem + 128 + bb * 64 + ck * 16 + lane_off, dpv);
       tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars->s_free[bb]);
       uint32_t pk[8], ds8[8];
       // causal: P = 0 where key > query, i.e. column e > qpos - k0
       if (j >= 2 * qt)   // warp-uniform: the two diagonal steps
         p_ds_16<true>(sv, dpv, nl, dn, scale_log2, qpos - k0, false, pk, ds8);
       else
         p_ds_16<false>(sv, dpv, nl, dn, scale_log2, 0, false, pk, ds8);
-      if (j >= 2) mbar_wait(&bars->ds_free[bb], ((j - 2) >> 1) & 1);   // dQ of step j-2 read buffer bb
-      st_row16_narrow(smem_u32(sdS(bb)), r, ck, ds8);
-      fence_proxy_async();
+      tmem_st_32x8(tmem + 128 + bb * 64 + ck * 16 + lane_off, ds8);   // over the dP columns just read
+      tmem_st_wait();
+      tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->ds_full[bb]);
     }
@@ -1748,14 +1779,22 @@ int hlm_flash_bwd_tc(const void* q, const void* k, const void* v, const void* d_
       return 3;
     static bool attr2 = false;
     if (!attr2) {
-      cudaFuncSetAttribute(flash_bwd_dkv_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_KV2_SMEM);
+      cudaFuncSetAttribute(flash_bwd_dkv_tc2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_KV2_SMEM);
+      cudaFuncSetAttribute(flash_bwd_dkv_tc2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_KV2_SMEM);
+      cudaFuncSetAttribute(flash_bwd_dkv_tc2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_KV2_SMEM);
       cudaFuncSetAttribute(flash_bwd_dq_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_Q2_SMEM);
       attr2 = true;
     }
-    flash_bwd_dkv_tc2<<<grid, BWD_KV2_THREADS, BWD_KV2_SMEM, s>>>(
+    static const int xp = [] {
+      const char* e = std::getenv("HLM_ATTN_BWD_EXPERIMENT");
+      return e ? std::atoi(e) : 0;
+    }();
+    auto kv_kern = xp == 1 ? flash_bwd_dkv_tc2<1> : xp == 2 ? flash_bwd_dkv_tc2<2> : flash_bwd_dkv_tc2<0>;
+    kv_kern<<<grid, BWD_KV2_THREADS, BWD_KV2_SMEM, s>>>(
         mq64, mk, mv, mdo64, lse, dsum, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, S, H, ld, scale, scale * kLog2e);
-    flash_bwd_dq_tc2<<<grid, BWD_Q2_THREADS, BWD_Q2_SMEM, s>>>(mq, mk64, mv64, mdo, lse, dsum, (__nv_bfloat16*)dq,
-                                                              S, H, ld, scale, scale * kLog2e);
+    flash_bwd_dq_tc2<<<grid, BWD_Q2_THREADS, BWD_Q2_SMEM, s>>>(
+        (const __nv_bfloat16*)q, mk64, mv64, (const __nv_bfloat16*)d_o, lse, dsum, (__nv_bfloat16*)dq, S, H, ld, scale,
+        scale * kLog2e);
     hlm_count_launches(2);
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
   }
