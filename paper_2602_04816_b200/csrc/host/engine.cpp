@@ -118,8 +118,10 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
     for (i64 i = 0; i < pool_->size(); ++i) ev_slab_done_.push_back(new_event(false));
     if (opts_.piece_elems > 0) piece_elems_ = opts_.piece_elems;
     max_pieces_ = std::max<i64>(1, (pool_->slab_capacity() / 4 + piece_elems_ - 1) / piece_elems_);
-    // vocab-chunked head (single GPU, untied): pieces of head_vc_ vocab rows
-    if (!opts_.comm_grad && !m.tie_embeddings && opts_.head_piece_vocab >= 0) {
+    // vocab-chunked head (untied): pieces of head_vc_ vocab rows. One rank only: the pieces
+    // go D2H without a reduce-scatter (at world 1 the reduction is the identity; at world > 1
+    // the head gradient takes the per-tile reduce-scatter of evacuate)
+    if ((!opts_.comm_grad || opts_.world == 1) && !m.tie_embeddings && opts_.head_piece_vocab >= 0) {
         i64 vc = opts_.head_piece_vocab;
         if (vc == 0 && m.embed_params() >= 2 * piece_elems_)
             vc = std::max<i64>(128, piece_elems_ / m.hidden / 128 * 128);
@@ -251,8 +253,10 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
         ev_transit_done_ = new_event(false);
         transit_slot_.assign(transits_.size(), -1);
     }
+    // row-sparse embedding gradient: one rank (at world > 1 the ranks' token rows differ and
+    // the dense table takes the per-tile reduce-scatter)
     sparse_embed_ = opts_.sparse_embed_grad && !m.tie_embeddings && resident_of_[0] < 0 && opts_.world == 1 &&
-                    !opts_.comm_grad && opts_.eager_optim && !opts_.skip_optimizer;
+                    opts_.eager_optim && !opts_.skip_optimizer;
     if (sparse_embed_) {
         ck(cudaHostAlloc(reinterpret_cast<void**>(&embed_rows_host_), static_cast<size_t>(m.vocab) * 4,
                          cudaHostAllocPortable),
@@ -721,7 +725,7 @@ void Engine::consume(const Pending& p) {
         cv_.notify_all();
         rec.topt1 = now_us();
     };
-    if (opts_.comm_grad) {   // this rank's shard [begin, begin + cnt)
+    if (opts_.comm_grad && !p.sparse_rows) {   // this rank's shard [begin, begin + cnt)
         const i64 cnt = shard_elems(tile.n_params()), begin = opts_.rank * cnt;
         const float* g = pool_->data(p.slab);
         if (piecewise) {

@@ -13,12 +13,18 @@ from paper_2602_04816_b200 import engine as E
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("extra", [dict(), dict(piece_elems=1000, grad_buffers=4)])
+@pytest.mark.parametrize("extra", [dict(), dict(piece_elems=1000, grad_buffers=4),
+                                   dict(piece_elems=1000, grad_buffers=4, sparse_embed_grad=True,
+                                        embed_gather_host=True, head_piece_vocab=32)])
 def test_dp_world1_nccl_paths_match_single_process_engine(extra):
     c = E.ModelConfig(4, 64, 128, 96, 32, 2, k_ckpt=1, n_heads=1)
     toks = [E.make_copy_task_batch(c, 5, skip=i) for i in range(3)]
     ref = E.Store(c, 11)
-    e0 = E.Engine(ref, E.Arena(c), E.HyperParams(lr=2e-3), E.EngineOptions(eager_optim=True))
+    # the same feature options without the communicators (at world 1 the DP path keeps the
+    # row-sparse embedding gradient and the vocab-chunked head)
+    e0 = E.Engine(ref, E.Arena(c), E.HyperParams(lr=2e-3),
+                  E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=4, overlap_optimizer_tail=True,
+                                  tail_blocks=1, **extra))
     l0 = [e0.train_step(t).loss for t in toks]
 
     comm_g = E.nccl_comm(E.nccl_unique_id(), 1, 0)
