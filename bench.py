@@ -450,7 +450,7 @@ def run_ours(args, m, name):
                            tail_blocks=max(0, tail), rank=rank, world=world,
                            comm_grad=comm_g, comm_weights=comm_w, host_threads=adam_threads,
                            resident_embed=args.resident_embed, resident_blocks=args.resident_blocks,
-                           transit_blocks=args.transit_blocks, saved_act_layers=args.saved_act_layers)
+                           saved_act_layers=args.saved_act_layers)
     eng = E.Engine(store, arena, E.HyperParams(lr=1e-4), opts)
     setup_s = time.time() - t0
     # one global token stream (reference RNG, global batch = world x local), sliced by rank
@@ -783,8 +783,6 @@ def main():
                     help="variant: recompute every block instead of keeping spare-HBM activations")
     ap.add_argument("--saved-act-layers", type=int, default=0,
                     help="top blocks whose forward activations stay in HBM (no recompute)")
-    ap.add_argument("--transit-blocks", type=int, default=0,
-                    help="top blocks whose host FP32 state is streamed through HBM for a device Adam")
     ap.add_argument("--resident-blocks", type=int, default=0,
                     help="blocks 1..N keep FP32 master + Adam state in HBM (device Adam, no streaming)")
     ap.add_argument("--resident-embed", action="store_true",

@@ -91,15 +91,6 @@ struct EngineOptions {
     // Pin the host optimizer's OpenMP team to cores (scheduling only).
     bool pin_threads = true;
     bool resident_embed = false;
-    // Transit tiles (same conditions as resident tiles): blocks L - transit_blocks + 1
-    // .. L keep FP32 master, m, v in the host store between steps; in the backward
-    // their state is copied into one of two HBM slots, updated by the device Adam
-    // (bit-identical to the host Adam) from the gradient that never leaves the GPU,
-    // and copied back with the new BF16 weights. Per parameter the host moves 12 + 14
-    // bytes of DMA instead of 36 bytes of gradient DMA, host Adam and weight traffic:
-    // the GPU, idle in a host-bound step, absorbs part of the optimizer while PCIe
-    // has headroom. Blocks that are HBM-resident are never transit.
-    i64 transit_blocks = 0;
     // Blocks L - saved_act_layers + 1 .. L (K == 1, fused recompute) keep the activations
     // their forward computed in HBM until their backward, which then skips the recompute
     // (the same kernels on the same inputs and weights would reproduce them bit for bit).
@@ -306,31 +297,6 @@ private:
     i64 resident_epoch_ = 0;
     std::vector<void*> saved_acts_;        // per logical tile: HBM activations kept from the forward
     void* saved_mem_ = nullptr;
-    // transit tiles (EngineOptions::transit_blocks)
-    static constexpr int kTransitSlots = 2;
-    std::vector<i64> transit_of_;          // per logical tile: index into transits_ or -1
-    std::vector<i64> transits_;            // logical tile ids
-    std::vector<int> transit_slot_;        // per transit tile: this step's HBM slot, -1 before the fetch
-    int transit_next_ = 0;
-    i64 transit_cursor_ = -1;            // next transit tile (index, descending) to fetch
-    void* ev_transit_done_ = nullptr;
-    float* transit_state(int slot) const;
-    uint16_t* transit_w16(int slot) const;
-    i64 transit_slot_elems_ = 0;           // widest transit tile
-    void* transit_mem_ = nullptr;          // kTransitSlots x [master | m | v | bf16 weights]
-    void* tin_ = nullptr;                  // transit state H2D
-    void* tout_ = nullptr;                 // transit state + weights D2H
-    void* ev_transit_in_[kTransitSlots] = {};
-    void* ev_transit_adam_[kTransitSlots] = {};
-    void* ev_transit_free_[kTransitSlots] = {};
-    std::vector<void*> transit_registered_;
-    unsigned long long* transit_bad_ = nullptr;       // device: per transit tile, first non-finite index
-    unsigned long long* transit_bad_host_ = nullptr;
-    i64 transit_d2h_ = 0;
-    bool transit_active_ = false;          // a transit update was issued this step
-    bool is_transit(i64 tile) const { return transit_of_[static_cast<size_t>(tile)] >= 0; }
-    void transit_fetch(i64 tile);          // state H2D into the next slot (tin_)
-    void transit_update(i64 tile, int gbuf, i64 dep_op);   // scan + device Adam + D2H back
     i64 shard_elems(i64 n) const;          // n / world (throws unless divisible)
     void h2d_tile(void* dst, const LayerTile& tile, i64 bytes);
     double* loss_dev_ = nullptr;

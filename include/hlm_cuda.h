@@ -304,10 +304,6 @@ typedef struct HlmEngineOptions {
   int32_t embed_gather_host;
   /* 1: leave the host optimizer's OpenMP team unpinned (default: pinned to cores) */
   int32_t no_pin_threads;
-  /* transit tiles: blocks L - transit_blocks + 1 .. L keep their FP32 master / m / v
-   * in the host store, streamed through HBM each step for a device Adam (bit-identical
-   * to the host Adam) instead of their gradient going to the host optimizer */
-  int64_t transit_blocks;
   /* blocks L - saved_act_layers + 1 .. L keep their forward activations in HBM until
    * their backward (no recompute; bit-identical: the recompute would reproduce them) */
   int64_t saved_act_layers;

@@ -9,7 +9,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhlm_b200.so")
+# HLM_LIB_PATH: an alternative build of the same library (A/B timing tools only)
+LIB_PATH = os.environ.get("HLM_LIB_PATH") or os.path.join(_HERE, "libhlm_b200.so")
 
 _lib = None
 

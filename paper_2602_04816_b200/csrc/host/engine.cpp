@@ -213,46 +213,6 @@ Engine::Engine(MasterStore& store, DeviceArena& arena, const HyperParams& hyper,
         for (i64 k = 0; k < n; ++k)
             saved_acts_[static_cast<size_t>(m.layers - k)] = static_cast<char*>(saved_mem_) + static_cast<size_t>(k) * bytes;
     }
-    // transit tiles: the top blocks, host state streamed through two HBM slots
-    transit_of_.assign(static_cast<size_t>(m.tile_count()), -1);
-    if (opts_.transit_blocks > 0) {
-        if (!resident_ok)
-            throw ConfigError("engine: transit tiles need the eager optimizer, one process, untied embeddings, "
-                              "k_ckpt 1 and fused recompute");
-        for (i64 l = std::max<i64>(1, m.layers - opts_.transit_blocks + 1); l <= m.layers; ++l)
-            if (!is_resident(l)) {
-                transit_of_[static_cast<size_t>(l)] = static_cast<i64>(transits_.size());
-                transits_.push_back(l);
-            }
-    }
-    if (!transits_.empty()) {
-        for (i64 id : transits_) transit_slot_elems_ = std::max(transit_slot_elems_, store_.tile(id).n_params());
-        const size_t slot_bytes = static_cast<size_t>((14 * transit_slot_elems_ + 255) / 256 * 256);
-        ck(cudaMalloc(&transit_mem_, kTransitSlots * slot_bytes), "cudaMalloc transit slots");
-        ck(cudaMalloc(&transit_bad_, transits_.size() * 8), "cudaMalloc transit flags");
-        ck(cudaHostAlloc(reinterpret_cast<void**>(&transit_bad_host_), transits_.size() * 8, cudaHostAllocPortable),
-           "cudaHostAlloc transit flags");
-        for (i64 id : transits_) {   // the state DMA needs page-locked host memory (4 KiB-aligned slots)
-            LayerTile& t = store_.tile(id);
-            const size_t bytes = static_cast<size_t>((12 * t.n_params() + 4095) / 4096 * 4096);
-            if (cudaHostRegister(t.master(), bytes, cudaHostRegisterPortable) != cudaSuccess) {
-                (void)cudaGetLastError();
-                throw ConfigError("engine: cannot page-lock the host state of transit tile " + std::to_string(id));
-            }
-            transit_registered_.push_back(t.master());
-        }
-        ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-        tin_ = s;
-        ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-        tout_ = s;
-        for (int i = 0; i < kTransitSlots; ++i) {
-            ev_transit_in_[i] = new_event(false);
-            ev_transit_adam_[i] = new_event(false);
-            ev_transit_free_[i] = new_event(false);
-        }
-        ev_transit_done_ = new_event(false);
-        transit_slot_.assign(transits_.size(), -1);
-    }
     // row-sparse embedding gradient: one rank (at world > 1 the ranks' token rows differ and
     // the dense table takes the per-tile reduce-scatter)
     sparse_embed_ = opts_.sparse_embed_grad && !m.tie_embeddings && resident_of_[0] < 0 && opts_.world == 1 &&
@@ -354,23 +314,7 @@ Engine::~Engine() {
     cudaStreamDestroy(S(d2h_));
     cudaStreamDestroy(S(opt_));
     if (comm_) cudaStreamDestroy(S(comm_));
-    if (tin_) {
-        cudaStreamSynchronize(S(tin_));
-        cudaStreamSynchronize(S(tout_));
-        cudaStreamDestroy(S(tin_));
-        cudaStreamDestroy(S(tout_));
-        for (int i = 0; i < kTransitSlots; ++i) {
-            cudaEventDestroy(E(ev_transit_in_[i]));
-            cudaEventDestroy(E(ev_transit_adam_[i]));
-            cudaEventDestroy(E(ev_transit_free_[i]));
-        }
-        cudaEventDestroy(E(ev_transit_done_));
-    }
-    for (void* p : transit_registered_) cudaHostUnregister(p);
-    if (transit_mem_) cudaFree(transit_mem_);
     if (saved_mem_) cudaFree(saved_mem_);
-    if (transit_bad_) cudaFree(transit_bad_);
-    if (transit_bad_host_) cudaFreeHost(transit_bad_host_);
     if (loss_host_) cudaFreeHost(loss_host_);
     if (loss_dev_) cudaFree(loss_dev_);
     if (nf_dev_) cudaFree(nf_dev_);
@@ -810,71 +754,6 @@ void Engine::resident_update(i64 tile, int gbuf, i64 dep_op) {
     resident_dirty_ = true;
 }
 
-float* Engine::transit_state(int slot) const {
-    const size_t slot_bytes = static_cast<size_t>((14 * transit_slot_elems_ + 255) / 256 * 256);
-    return reinterpret_cast<float*>(static_cast<char*>(transit_mem_) + static_cast<size_t>(slot) * slot_bytes);
-}
-
-uint16_t* Engine::transit_w16(int slot) const {
-    return reinterpret_cast<uint16_t*>(transit_state(slot) + 3 * transit_slot_elems_);
-}
-
-// State of a transit tile -> the next HBM slot, once the slot's previous tile is back
-// on the host. The host copy is current: only this tile's own D2H writes it, and the
-// previous step's finish_step synchronised that.
-void Engine::transit_fetch(i64 tile) {
-    const i64 ti = transit_of_[static_cast<size_t>(tile)];
-    const int s = transit_next_;
-    transit_next_ = (transit_next_ + 1) % kTransitSlots;
-    transit_slot_[static_cast<size_t>(ti)] = s;
-    const LayerTile& t = store_.tile(tile);
-    ck(cudaStreamWaitEvent(S(tin_), E(ev_transit_free_[s]), 0), "wait transit slot free");
-    ck(cudaMemcpyAsync(transit_state(s), t.master(), static_cast<size_t>(12 * t.n_params()), cudaMemcpyHostToDevice,
-                       S(tin_)),
-       "H2D transit state");
-    ck(cudaEventRecord(E(ev_transit_in_[s]), S(tin_)), "record transit state in");
-    arena_.add_h2d(12 * t.n_params());
-}
-
-// Gradient of a transit tile: finiteness scan and device Adam on the optimizer stream
-// (a flagged gradient leaves the state untouched; finish_step raises), then master,
-// m, v and the new BF16 weights back into the host store; the next prefetch follows.
-void Engine::transit_update(i64 tile, int gbuf, i64 dep_op) {
-    const i64 ti = transit_of_[static_cast<size_t>(tile)];
-    const int s = transit_slot_[static_cast<size_t>(ti)];
-    if (s < 0) throw ProtocolError("transit tile updated before its state was fetched");
-    LayerTile& t = store_.tile(tile);
-    const i64 n = t.n_params();
-    float* st = transit_state(s);
-    uint16_t* w = transit_w16(s);
-    ck(cudaEventRecord(E(ev_res_grad_), S(compute_)), "record transit grad");
-    ck(cudaStreamWaitEvent(S(opt_), E(ev_res_grad_), 0), "wait transit grad");
-    ck(cudaStreamWaitEvent(S(opt_), E(ev_transit_in_[s]), 0), "wait transit state");
-    StreamOp op;
-    op.stream = StreamId::Compute;   // trace schema: a GPU op of the step (on the optimizer stream)
-    op.kind = OpKind::OptStep;
-    op.layer = tile;
-    op.params = n;
-    op.deps.push_back(dep_op);
-    const i64 id = op_begin(op, opt_);
-    ck_hlm(hlm_cuda_nonfinite(grad_buf(gbuf), n, transit_bad_ + ti, opt_), "nonfinite (transit)");
-    HlmHyper hp{hyper_.lr, hyper_.beta1, hyper_.beta2, hyper_.eps, hyper_.weight_decay};
-    ck_hlm(hlm_cuda_adam(st, st + n, st + 2 * n, w, grad_buf(gbuf), n, transit_bad_ + ti, &hp, step_t_, opt_),
-           "device adam (transit)");
-    op_end(id, opt_);
-    ck(cudaEventRecord(E(ev_gradbuf_free_[gbuf]), S(opt_)), "record grad buf free (transit)");
-    ck(cudaEventRecord(E(ev_transit_adam_[s]), S(opt_)), "record transit adam");
-    ck(cudaStreamWaitEvent(S(tout_), E(ev_transit_adam_[s]), 0), "wait transit adam");
-    ck(cudaMemcpyAsync(t.master(), st, static_cast<size_t>(12 * n), cudaMemcpyDeviceToHost, S(tout_)),
-       "D2H transit state");
-    ck(cudaMemcpyAsync(t.shadow(), w, static_cast<size_t>(2 * n), cudaMemcpyDeviceToHost, S(tout_)),
-       "D2H transit weights");
-    ck(cudaEventRecord(E(ev_transit_free_[s]), S(tout_)), "record transit slot free");
-    transit_d2h_ += 14 * n;
-    transit_active_ = true;
-    if (transit_cursor_ >= 0) transit_fetch(transits_[static_cast<size_t>(transit_cursor_--)]);
-}
-
 void Engine::process_oldest_inline() {
     Pending p;
     {
@@ -1089,9 +968,7 @@ void Engine::begin_step(const Batch& batch) {
         ++step_index_;
         regular_left_ = 0;
         for (i64 t = 0; t < m.tile_count(); ++t)
-            if (!deferred_[static_cast<size_t>(t)] && resident_of_[static_cast<size_t>(t)] < 0 &&
-                transit_of_[static_cast<size_t>(t)] < 0)
-                ++regular_left_;
+            if (!deferred_[static_cast<size_t>(t)] && resident_of_[static_cast<size_t>(t)] < 0) ++regular_left_;
         tail_open_ = !opts_.overlap_optimizer_tail || regular_left_ == 0;
         if (!opts_.overlap_optimizer_tail) pending_.clear();
         consumers_left_.assign(static_cast<size_t>(store_.physical_tiles()), 0);
@@ -1099,10 +976,6 @@ void Engine::begin_step(const Batch& batch) {
             consumers_left_[static_cast<size_t>(p)] = store_.consumer_count(p);
     }
     std::fill(cache_xfer_op_.begin(), cache_xfer_op_.end(), -1);
-    std::fill(transit_slot_.begin(), transit_slot_.end(), -1);
-    transit_cursor_ = static_cast<i64>(transits_.size()) - 1;
-    transit_active_ = false;
-    transit_d2h_ = 0;
     step_t_ = store_.adam_steps() + 1;
     d2h_base_ = pool_->d2h_bytes();
     recompute_forwards_ = 0;
@@ -1355,8 +1228,6 @@ void Engine::backward_blockwise() {
     const bool fused = opts_.fused_recompute && K == 1;
     const size_t act_bytes = static_cast<size_t>(block_act_bytes(m));
     (void)act_bytes;
-    for (int k = 0; k < kTransitSlots && transit_cursor_ >= 0; ++k)   // the first transit tiles' state
-        transit_fetch(transits_[static_cast<size_t>(transit_cursor_--)]);
 
     for (i64 b = m.layers / K; b >= 0; --b) {
         const i64 lo = b * K + 1, hi = std::min((b + 1) * K, m.layers);
@@ -1403,9 +1274,6 @@ void Engine::backward_blockwise() {
             op_end(lb, compute_);
             if (res) {
                 resident_update(lo, gb, lb);
-            } else if (is_transit(lo)) {
-                compute_done_with(buf, lb);
-                transit_update(lo, gb, lb);
             } else {
                 compute_done_with(buf, lb);
                 evacuate(lo, gb, n_block, lb);
@@ -1526,13 +1394,9 @@ StepResult Engine::finish_step() {
     if (phase_ != Phase::Optimize) throw ProtocolError("finish_step out of order");
     const ModelConfig& m = store_.config();
     const i64 T = m.rows();
-    if (resident_dirty_ || transit_active_) {   // the step's GPU span includes the device Adam
+    if (resident_dirty_) {   // the step's GPU span includes the device Adam
         ck(cudaEventRecord(E(ev_res_grad_), S(opt_)), "record optimizer stream done");
         ck(cudaStreamWaitEvent(S(compute_), E(ev_res_grad_), 0), "wait optimizer stream");
-    }
-    if (transit_active_) {   // ... and the transit tiles' return to the host
-        ck(cudaEventRecord(E(ev_transit_done_), S(tout_)), "record transit done");
-        ck(cudaStreamWaitEvent(S(compute_), E(ev_transit_done_), 0), "wait transit done");
     }
     ck(cudaEventRecord(E(ev_step_end_), S(compute_)), "record step end");
     drain();
@@ -1540,21 +1404,6 @@ StepResult Engine::finish_step() {
     ck(cudaStreamSynchronize(S(d2h_)), "sync d2h");
     ck(cudaStreamSynchronize(S(h2d_)), "sync h2d");
     ck(cudaStreamSynchronize(S(opt_)), "sync optimizer stream");
-    if (transit_active_) {
-        ck(cudaStreamSynchronize(S(tin_)), "sync transit in");
-        ck(cudaStreamSynchronize(S(tout_)), "sync transit out");
-        {   // the transit tiles' host state and weights are this step's: current for the next H2D
-            std::lock_guard<std::mutex> lk(mu_);
-            for (i64 id : transits_) store_.tile(id).bump_version(opts_.rank);
-        }
-        cv_.notify_all();
-        ck(cudaMemcpy(transit_bad_host_, transit_bad_, transits_.size() * 8, cudaMemcpyDeviceToHost),
-           "D2H transit flags");
-        for (size_t i = 0; i < transits_.size(); ++i)
-            if (transit_bad_host_[i] != ~0ull)
-                throw NumericsError("non-finite gradient in layer " + std::to_string(transits_[i]) + " at element " +
-                                    std::to_string(transit_bad_host_[i]) + "; step aborted");
-    }
     if (!residents_.empty()) {
         ck(cudaMemcpy(resident_bad_host_, resident_bad_, residents_.size() * 8, cudaMemcpyDeviceToHost),
            "D2H resident flags");
@@ -1687,7 +1536,7 @@ StepResult Engine::finish_step() {
     r.host.slabs = pool_->pool_bytes();
     r.host.total = r.host.persistent + r.host.slabs;
     r.h2d_bytes = arena_.h2d_bytes();
-    r.d2h_bytes = pool_->d2h_bytes() - d2h_base_ + transit_d2h_;
+    r.d2h_bytes = pool_->d2h_bytes() - d2h_base_;
     r.recompute_forwards = recompute_forwards_;
     r.gpu_ms = ms;
     phase_ = Phase::Idle;

@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < args.kblocks; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          if (lane == 0) {
+          {
             const uint32_t a_base = smem_u32(sA + stage * A_STAGE);
             const uint32_t b_base = smem_u32(sB + stage * B_STAGE);
 #pragma unroll
@@ -462,11 +462,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                        : make_sw128_desc(a_base + kk * 32, 16, 1024);
               const uint64_t bd = B_MN ? make_sw128_desc(b_base + kk * 2048, ATOM, 1024)
                                        : make_sw128_desc(b_base + kk * 32, 16, 1024);
-              umma_bf16(d_tmem, ad, bd, idesc, (first && kk == 0) ? 0u : 1u);
+              umma_bf16_w(d_tmem, ad, bd, idesc, (first && kk == 0) ? 0u : 1u);
             }
-            umma_commit(&empty[stage]);
+            umma_commit_w(&empty[stage]);
           }
-          __syncwarp();
           first = false;
           if (++stage == STAGES) {
             stage = 0;
@@ -474,8 +473,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
-      if (lane == 0) umma_commit(&tmem_full[acc]);
-      __syncwarp();
+      umma_commit_w(&tmem_full[acc]);
     }
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue: TMEM -> regs -> global
@@ -621,7 +619,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           for (int kb = 0; kb < args.kblocks; ++kb) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
-            if (lane == 0) {
+            {
               const uint32_t a_base = smem_u32(sA + stage * HALF_STAGE);
               const uint32_t b_base = smem_u32(sB + stage * HALF_STAGE);
 #pragma unroll
@@ -630,11 +628,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                                          : make_sw128_desc(a_base + kk * 32, 16, 1024);
                 const uint64_t bd = B_MN ? make_sw128_desc(b_base + kk * 2048, ATOM, 1024)
                                          : make_sw128_desc(b_base + kk * 32, 16, 1024);
-                umma_bf16_2sm(d_tmem, ad, bd, idesc, (first && kk == 0) ? 0u : 1u);
+                umma_bf16_2sm_w(d_tmem, ad, bd, idesc, (first && kk == 0) ? 0u : 1u);
               }
-              umma_commit_2sm_mc(&empty[stage]);
+              umma_commit_2sm_mc_w(&empty[stage]);
             }
-            __syncwarp();
             first = false;
             if (++stage == STAGES2) {
               stage = 0;
@@ -642,8 +639,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             }
           }
         }
-        if (lane == 0) umma_commit_2sm_mc(&tmem_full[acc]);
-        __syncwarp();
+        umma_commit_2sm_mc_w(&tmem_full[acc]);
       }
     }
   } else if (warp >= 4) {

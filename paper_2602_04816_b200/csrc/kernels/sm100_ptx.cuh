@@ -277,6 +277,29 @@ __device__ __forceinline__ void umma_bf16_2sm(uint32_t d_tmem, uint64_t a_desc, 
       "}\n" ::"r"(d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
+// warp-converged forms of the two above (elect.sync inside the asm; see umma_bf16_w)
+__device__ __forceinline__ void umma_bf16_2sm_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit_2sm_mc_w(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      ".reg .b16 m;\n"
+      "mov.b16 m, 3;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n"
+      "}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
 // Arrive on the same-offset mbarrier of both CTAs of the pair once all prior MMAs completed.
 __device__ __forceinline__ void umma_commit_2sm_mc(uint64_t* bar) {
   asm volatile(

@@ -329,41 +329,8 @@ def test_hbm_resident_optimizer_tiles_are_bitwise_neutral(res, tmp_path):
     assert l1[-1].h2d_bytes == streamed
 
 
-@pytest.mark.parametrize("opts", [dict(transit_blocks=2), dict(transit_blocks=6),
-                                  dict(transit_blocks=3, resident_blocks=4, resident_embed=True),
-                                  dict(transit_blocks=1, tail_blocks=0, sparse_embed_grad=True, grad_buffers=4)])
-def test_transit_tiles_are_bitwise_neutral(opts):
-    """Top blocks' host FP32 state streamed through HBM for a device Adam each step:
-    same losses and, without any sync(), the same store bit for bit as the host Adam
-    (the state and weights are back on the host at the end of every step)."""
-    from paper_2602_04816_b200.trace import validate_trace
-    c = E.ModelConfig(6, 32, 64, 32, 16, 2, k_ckpt=1, n_heads=2, rope_theta=1e4)
-    toks = [E.make_copy_task_batch(c, 4, skip=i) for i in range(4)]
-    hp = E.HyperParams(lr=2e-3, weight_decay=0.01)
-    ref = E.Store(c, 8)
-    e0 = E.Engine(ref, E.Arena(c), hp, E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=4))
-    l0 = [e0.train_step(t).loss for t in toks]
-    e0.sync()
-    s = E.Store(c, 8)
-    o = dict(eager_optim=True, threaded_accum=True, n_slab=4, overlap_optimizer_tail=True, tail_blocks=1)
-    o.update(opts)
-    e1 = E.Engine(s, E.Arena(c), hp, E.EngineOptions(**o))
-    l1 = [e1.train_step(t) for t in toks]
-    assert validate_trace(e1.last_trace(), c.layers) == []
-    assert l0 == [r.loss for r in l1]
-    if not opts.get("resident_blocks"):
-        e1.wait_optimizer()   # host tiles only: no device write-back needed for the transit ones
-        assert ref.bitwise_equal(s)
-    e1.sync()
-    assert ref.bitwise_equal(s)
-    k = min(opts["transit_blocks"], c.layers - opts.get("resident_blocks", 0))
-    # the transit tiles' state comes in (12 B/param) and goes back with the weights (14 B/param)
-    assert l1[-1].d2h_bytes >= 14 * k * c.block_params()
-
-
 @pytest.mark.parametrize("opts", [dict(saved_act_layers=2), dict(saved_act_layers=6),
-                                  dict(saved_act_layers=3, resident_blocks=4, resident_embed=True),
-                                  dict(saved_act_layers=2, transit_blocks=3)])
+                                  dict(saved_act_layers=3, resident_blocks=4, resident_embed=True)])
 def test_saved_activations_are_bitwise_neutral(opts):
     """Top blocks' forward activations kept in HBM (no recompute in their backward):
     the same losses and store bit for bit, and that many fewer recompute forwards."""
@@ -385,33 +352,6 @@ def test_saved_activations_are_bitwise_neutral(opts):
     assert l0 == [r.loss for r in l1]
     assert ref.bitwise_equal(s)
     assert l1[-1].recompute_forwards == c.layers - opts["saved_act_layers"]
-
-
-def test_transit_checkpoint_mid_run_resumes_bitwise(tmp_path):
-    """The transit tiles' state is back in the store at the end of every step: a
-    checkpoint taken without sync() (host optimizer drained only) resumes bit for bit."""
-    c = E.ModelConfig(6, 32, 64, 32, 16, 2, k_ckpt=1, n_heads=2, rope_theta=1e4)
-    toks = [E.make_copy_task_batch(c, 4, skip=i) for i in range(5)]
-    hp = E.HyperParams(lr=2e-3, weight_decay=0.01)
-    o = dict(eager_optim=True, threaded_accum=True, n_slab=4, overlap_optimizer_tail=True, tail_blocks=1,
-             transit_blocks=3)
-    ref = E.Store(c, 8)
-    e0 = E.Engine(ref, E.Arena(c), hp, E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=4))
-    l0 = [e0.train_step(t).loss for t in toks]
-    e0.sync()
-    s = E.Store(c, 8)
-    e1 = E.Engine(s, E.Arena(c), hp, E.EngineOptions(**o))
-    l1 = [e1.train_step(t).loss for t in toks[:2]]
-    e1.wait_optimizer()
-    s.save(tmp_path / "mid.hlm2")
-    del e1
-    r = E.Store(c, 1)
-    r.load(tmp_path / "mid.hlm2")
-    e2 = E.Engine(r, E.Arena(c), hp, E.EngineOptions(**o))
-    l2 = [e2.train_step(t).loss for t in toks[2:]]
-    e2.sync()
-    assert l1 + l2 == l0
-    assert r.bitwise_equal(ref)
 
 
 @pytest.mark.parametrize("pieces", [dict(piece_elems=1000), dict(piece_elems=4096, head_piece_vocab=8),
@@ -455,24 +395,6 @@ def test_sparse_embedding_gradient_non_finite_names_the_table_element():
     e = E.Engine(s, E.Arena(c), E.HyperParams(), E.EngineOptions(eager_optim=True, sparse_embed_grad=True))
     with pytest.raises(E.NumericsError, match="non-finite gradient in layer"):
         e.train_step(tok)
-
-
-def test_transit_tile_non_finite_gradient_raises_and_keeps_state():
-    """A non-finite gradient in a transit tile: the device Adam is a no-op for it, the
-    (unchanged) state still returns to the store, and finish_step raises."""
-    c = E.ModelConfig(3, 16, 32, 13, 4, 1, k_ckpt=1)
-    s = E.Store(c, 5, "fp32")
-    w = s.weights()
-    lo = c.vocab * c.hidden + (c.layers - 1) * c.block_params()   # block L: the transit tile
-    w[lo + 7] = np.inf
-    s.import_master(w)
-    before = s.weights()[lo:lo + c.block_params()].copy()
-    e = E.Engine(s, E.Arena(c), E.HyperParams(),
-                 E.EngineOptions(eager_optim=True, threaded_accum=True, n_slab=4, transit_blocks=1))
-    with pytest.raises(E.NumericsError, match="non-finite gradient in layer"):
-        e.train_step(E.make_copy_task_batch(c, 2))
-    after = s.weights()[lo:lo + c.block_params()]
-    assert np.array_equal(before, after, equal_nan=True)
 
 
 def test_bench_feature_set_tracks_oracle_for_20_steps():
