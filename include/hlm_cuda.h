@@ -227,6 +227,10 @@ int hlm_cuda_adam(float* w, float* m, float* v, void* w16, const float* g, int64
                   const unsigned long long* bad, const struct HlmHyper* hp, int64_t t, void* stream);
 /* *first (device u64) := smallest index of a non-finite element of g, ~0 when all finite */
 int hlm_cuda_nonfinite(const float* g, int64_t n, unsigned long long* first, void* stream);
+/* the same scan only when *certificate (device, from hlm_cuda_head_stats) is
+ * HLM_HEAD_UNCERTIFIED; otherwise *first := ~0 and g is not read */
+int hlm_cuda_nonfinite_if_uncertified(const float* g, int64_t n, unsigned long long* first,
+                                      const unsigned long long* certificate, void* stream);
 
 /* Device-event timer for harnesses: record(slot) synchronises the device and
  * records an event on the legacy stream; elapsed_ms(a, b) between two slots. */

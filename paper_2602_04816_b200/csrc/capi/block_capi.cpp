@@ -606,7 +606,14 @@ int hlm_cuda_adam(float* w, float* m, float* v, void* w16, const float* g, int64
 }
 
 int hlm_cuda_nonfinite(const float* g, int64_t n, unsigned long long* first, void* stream) {
-  return guarded([&] { chk(hlm_ops_nonfinite(g, n, first, static_cast<cudaStream_t>(stream)), "nonfinite"); });
+  return guarded([&] { chk(hlm_ops_nonfinite(g, n, first, nullptr, static_cast<cudaStream_t>(stream)), "nonfinite"); });
+}
+
+int hlm_cuda_nonfinite_if_uncertified(const float* g, int64_t n, unsigned long long* first,
+                                      const unsigned long long* certificate, void* stream) {
+  return guarded([&] {
+    chk(hlm_ops_nonfinite(g, n, first, certificate, static_cast<cudaStream_t>(stream)), "nonfinite (fallback)");
+  });
 }
 
 int hlm_cuda_cast_bf16(const float* in, void* out, int64_t n, void* stream) {

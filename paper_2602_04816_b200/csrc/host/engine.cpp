@@ -554,11 +554,17 @@ i64 Engine::acquire_slab(i64 bytes) {
 // reference engine.cpp:103-121: acquire a slab (inline back-pressure
 // consumes the oldest READY slab), D2H the fp32 gradient, emit GradXfer.
 void Engine::evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op, bool sparse_rows) {
-    ck(cudaEventRecord(E(ev_grad_ready_[gbuf]), S(compute_)), "record grad ready");
     const i64 cnt = opts_.comm_grad ? shard_elems(n_params) : n_params;
     const i64 bytes = 4 * cnt;
     const i64 slab = acquire_slab(bytes);
     pool_->mark_in_flight(slab, tile_id, bytes);
+    // the reference's "all gradients finite before any mutation" check, on the GPU, in
+    // stream order behind the kernels that wrote the gradient (single GPU: the compute
+    // stream; data parallel: the communicator's stream, behind the reduce-scatter, since a
+    // sum of finite shards can overflow). A scan on a side stream would take SMs from the
+    // persistent GEMM that follows on the compute stream and stall its static tile schedule.
+    if (!opts_.comm_grad) ck_hlm(hlm_cuda_nonfinite(grad_buf(gbuf), cnt, nf_dev_ + slab, compute_), "nonfinite scan");
+    ck(cudaEventRecord(E(ev_grad_ready_[gbuf]), S(compute_)), "record grad ready");
     StreamOp op;
     op.stream = StreamId::D2H;
     op.kind = OpKind::GradXfer;
@@ -576,15 +582,14 @@ void Engine::evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op, bool spars
         nccl_check(nccl().ReduceScatter(grad_buf(gbuf), src, static_cast<size_t>(cnt), ncclFloat32, ncclSum,
                                         static_cast<ncclComm_t>(opts_.comm_grad), S(comm_)),
                    "reduce-scatter grads");
+        ck_hlm(hlm_cuda_nonfinite(src, cnt, nf_dev_ + slab, comm_), "nonfinite scan");
         ck(cudaEventRecord(E(ev_rs_done_[static_cast<size_t>(gbuf)]), S(comm_)), "record rs done");
         ck(cudaStreamWaitEvent(S(d2h_), E(ev_rs_done_[static_cast<size_t>(gbuf)]), 0), "wait rs done");
     } else {
         ck(cudaStreamWaitEvent(S(d2h_), E(ev_grad_ready_[gbuf]), 0), "wait grad ready");
     }
     const i64 id = op_begin(std::move(op), d2h_);
-    // the reference's "all gradients finite before any mutation" check, on the GPU;
-    // its flag lands first, then the gradient in pieces (the optimizer starts on piece 0)
-    ck_hlm(hlm_cuda_nonfinite(src, cnt, nf_dev_ + slab, d2h_), "nonfinite scan");
+    // the finiteness flag lands first, then the gradient in pieces (the optimizer starts on piece 0)
     ck(cudaMemcpyAsync(nf_host_ + slab, nf_dev_ + slab, 8, cudaMemcpyDeviceToHost, S(d2h_)), "D2H nf flag");
     ck(cudaEventRecord(E(ev_slab_flag_[static_cast<size_t>(slab)]), S(d2h_)), "record slab flag");
     const i64 pieces = (cnt + piece_elems_ - 1) / piece_elems_;
@@ -1203,7 +1208,7 @@ void Engine::anchor_loss_pieces(int buf, i64 w_op) {
     }
     compute_done_with(buf, last_lb);
     // the certificate's fallback: the full scan of the head gradient
-    ck_hlm(hlm_cuda_nonfinite(g, n, nf2_dev_ + slab, d2h_), "nonfinite scan (head)");
+    ck_hlm(hlm_cuda_nonfinite_if_uncertified(g, n, nf2_dev_ + slab, head_cert_dev_, d2h_), "nonfinite scan (head)");
     ck(cudaMemcpyAsync(nf2_host_ + slab, nf2_dev_ + slab, 8, cudaMemcpyDeviceToHost, S(d2h_)), "D2H nf2 flag");
     ck(cudaEventRecord(E(ev_slab_done_[static_cast<size_t>(slab)]), S(d2h_)), "record slab done");
     ck(cudaEventRecord(E(ev_gradbuf_free_[gb]), S(d2h_)), "record grad buf free");

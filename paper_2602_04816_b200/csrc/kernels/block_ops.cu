@@ -729,7 +729,11 @@ __global__ void head_certify_kernel(const __nv_bfloat16* __restrict__ x, long lo
 // Any alignment of g (a data-parallel shard starts at rank * n / world elements): the
 // first `head` elements up to the next 16-byte boundary are scanned scalar, the rest
 // as float4.
-__global__ void nonfinite_kernel(const float* __restrict__ g, long long n, unsigned long long* first) {
+// `only_if` (may be null): scan only when *only_if == HLM_HEAD_UNCERTIFIED (the vocab-chunked
+// head's fallback; a certified head gradient costs one read per CTA).
+__global__ void nonfinite_kernel(const float* __restrict__ g, long long n, unsigned long long* first,
+                                 const unsigned long long* __restrict__ only_if) {
+  if (only_if != nullptr && *only_if != HLM_HEAD_UNCERTIFIED) return;
   const long long head = min(n, (long long)(((16u - ((uintptr_t)g & 15u)) & 15u) / 4u));
   if (blockIdx.x == 0 && threadIdx.x < head)
     if (!isfinite(g[threadIdx.x])) atomicMin(first, (unsigned long long)threadIdx.x);
@@ -979,9 +983,10 @@ int hlm_ops_fill_random_bf16(void* p, long long n, unsigned seed, cudaStream_t s
   HLM_CHECK_LAUNCH();
 }
 
-int hlm_ops_nonfinite(const float* g, long long n, unsigned long long* first, cudaStream_t s) {
+int hlm_ops_nonfinite(const float* g, long long n, unsigned long long* first, const unsigned long long* only_if,
+                      cudaStream_t s) {
   cudaMemsetAsync(first, 0xFF, sizeof(unsigned long long), s);
-  nonfinite_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, s>>>(g, n, first);
+  nonfinite_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, s>>>(g, n, first, only_if);
   hlm_count_launches(1);
   HLM_CHECK_LAUNCH();
 }

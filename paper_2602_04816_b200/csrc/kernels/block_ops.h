@@ -45,7 +45,8 @@ long long hlm_launches_total();
 // Deterministic pseudo-random bf16 fill (bench / probe inputs), |x| < 1.
 int hlm_ops_fill_random_bf16(void* p, long long n, unsigned seed, cudaStream_t s);
 // first[0] := smallest index of a non-finite element of g[0..n), ~0ull when none.
-int hlm_ops_nonfinite(const float* g, long long n, unsigned long long* first, cudaStream_t s);
+int hlm_ops_nonfinite(const float* g, long long n, unsigned long long* first, const unsigned long long* only_if,
+                      cudaStream_t s);
 // Adam on HBM-resident optimizer state (bit-identical to the host kernel); no-op when *bad != ~0.
 int hlm_ops_adam_device(float* w, float* m, float* v, void* w16, const float* g, long long n,
                         const unsigned long long* bad, float lr, float b1, float b2, float eps, float wd, float bc1,
