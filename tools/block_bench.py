@@ -57,6 +57,29 @@ def run(cfg="c2", iters=10):
             if i >= 2:
                 tf.append(ev[0].elapsed_time(ev[1]))
                 tb.append(ev[1].elapsed_time(ev[2]))
+    # per-kind split of one more iteration of each variant (in-library kernel timer)
+    Lb.hlm_ktimer_enable.argtypes = [ctypes.c_int]
+    Lb.hlm_ktimer_collect.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                      ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
+    kinds = ("gemm", "attn_fwd", "attn_bwd", "rmsnorm_fwd", "rmsnorm_bwd", "swiglu_fwd", "swiglu_bwd", "rope",
+             "cast")
+    for name, (d, acts, ws, _, _) in runs.items():
+        Lb.hlm_ktimer_reset()
+        Lb.hlm_ktimer_enable(1)
+        L.check(Lb.hlm_cuda_block_fwd(ctypes.byref(d), vp(W), vp(x), vp(y), vp(acts), vp(ws), vp(cs), vp(sn), None))
+        L.check(Lb.hlm_cuda_block_bwd(ctypes.byref(d), vp(W), vp(x), vp(acts), vp(g), vp(gi), vp(grad), vp(ws),
+                                      vp(cs), vp(sn), None))
+        torch.cuda.synchronize()
+        Lb.hlm_ktimer_enable(0)
+        parts = []
+        for k, kname in enumerate(kinds):
+            ms_k, w_k, n_k = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+            Lb.hlm_ktimer_collect(k, ctypes.byref(ms_k), ctypes.byref(w_k), ctypes.byref(n_k))
+            if n_k.value:
+                rate = f" {w_k.value / ms_k.value / 1e9:.0f} TF/s" if k < 3 else ""
+                parts.append(f"{kname} {ms_k.value:.3f} ms x{n_k.value}{rate}")
+        print(f"{cfg} {name:8s} " + "; ".join(parts), flush=True)
+        Lb.hlm_ktimer_reset()
     for name, (_, _, _, tf, tb) in runs.items():
         tf.sort(), tb.sort()
         out[name] = (tf[len(tf) // 2], tb[len(tb) // 2])
