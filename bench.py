@@ -531,8 +531,9 @@ def run_ours(args, m, name):
     gpu_span_s = float(np.mean(gpu_ms)) / 1e3   # step-start .. step-end events on the compute stream
 
     hbm, tf_burst, tf_sus, peak_kind = peaks()
-    # DRAM bytes per launch of the probe's 12 GEMMs from the committed ncu --set full capture
-    tp = os.path.join(ROOT, "profiles", "r01_gemm_probe_traffic.json")
+    # DRAM bytes per launch of one block's 12 GEMMs (fused epilogues, as timed in-step) from
+    # the committed ncu --set full capture of the same kernels
+    tp = os.path.join(ROOT, "profiles", "r02", "r02_gemm_block_traffic.json")
     gemm_traffic = json.load(open(tp)) if os.path.exists(tp) and m["hidden"] == 3584 else {}
     elementwise = {k: {"gbs": ew_gbs[i], "ms": ew_ms[i], "frac": ew_gbs[i] / hbm}
                    for i, k in enumerate(ew_names)}
