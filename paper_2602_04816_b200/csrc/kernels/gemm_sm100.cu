@@ -62,6 +62,7 @@ struct KArgs {
   __nv_bfloat16* C2;
   long long ldc2;
   int l2_prefetch;       // SWIGLU_BWD: bulk-prefetch the next tile's up / gate into L2 (A/B)
+  int l2_hint;           // 2-CTA operand loads: 0 evict_normal, 1 evict_last, 2 evict_first
 };
 
 __device__ __forceinline__ void tile_coords(const KArgs& a, int t, int& g, int& m, int& n) {
@@ -565,6 +566,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      // operand panels are read by every tile of the wave that shares them: L2 evict_last
+      // (HLM_GEMM_L2_HINT=0 leaves the default policy, 2 = evict_first)
+      const uint64_t pol = args.l2_hint == 2 ? l2_policy_evict_first()
+                           : args.l2_hint == 1 ? l2_policy_evict_last() : l2_policy_evict_normal();
       for (int t = pair; t < args.num_tiles; t += npairs) {
         int tg, tm, tn;
         tile_coords_2sm(args, t, tg, tm, tn);
@@ -583,16 +588,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             uint8_t* a_dst = sA + stage * HALF_STAGE;
             uint8_t* b_dst = sB + stage * HALF_STAGE;
             if (A_MN) {
-              tma_load_3d_2sm(a_dst, &map_a, &full[stage], m0, k0, ag);
-              tma_load_3d_2sm(a_dst + ATOM, &map_a, &full[stage], m0 + 64, k0, ag);
+              tma_load_3d_2sm_hint(a_dst, &map_a, &full[stage], m0, k0, ag, pol);
+              tma_load_3d_2sm_hint(a_dst + ATOM, &map_a, &full[stage], m0 + 64, k0, ag, pol);
             } else {
-              tma_load_3d_2sm(a_dst, &map_a, &full[stage], k0, m0, ag);
+              tma_load_3d_2sm_hint(a_dst, &map_a, &full[stage], k0, m0, ag, pol);
             }
             if (B_MN) {
-              tma_load_3d_2sm(b_dst, &map_b, &full[stage], n0, k0, bg);
-              tma_load_3d_2sm(b_dst + ATOM, &map_b, &full[stage], n0 + 64, k0, bg);
+              tma_load_3d_2sm_hint(b_dst, &map_b, &full[stage], n0, k0, bg, pol);
+              tma_load_3d_2sm_hint(b_dst + ATOM, &map_b, &full[stage], n0 + 64, k0, bg, pol);
             } else {
-              tma_load_3d_2sm(b_dst, &map_b, &full[stage], k0, n0, bg);
+              tma_load_3d_2sm_hint(b_dst, &map_b, &full[stage], k0, n0, bg, pol);
             }
             if (++stage == STAGES2) {
               stage = 0;
@@ -799,6 +804,14 @@ int launch(const HlmGemmDesc& d, cudaStream_t stream) {
       pf = (e && *e == '1') ? 1 : 0;
     }
     a.l2_prefetch = pf;
+  }
+  {
+    static int hint = -1;
+    if (hint < 0) {
+      const char* e = std::getenv("HLM_GEMM_L2_HINT");
+      hint = e ? std::atoi(e) : 1;   // evict_last: -5 % DRAM, -2 % time (block GEMMs, ncu)
+    }
+    a.l2_hint = hint;
   }
 
   if (two) {
