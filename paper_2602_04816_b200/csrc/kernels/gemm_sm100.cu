@@ -327,6 +327,55 @@ __device__ __forceinline__ void epilogue_swiglu_bwd(const KArgs& args, uint32_t 
   }
 }
 
+// F32 + residual (the o / down projections' h + x W): the residual of chunk c + 1 is loaded
+// while chunk c's accumulator comes out of TMEM, and both streams bypass L2 retention
+// (evict-first loads / stores) so they do not push the operand panels out. Same fp32 adds
+// as the plain epilogue. (Loading the residual per float4 right before its store, behind
+// the previous store to a possibly aliasing row, serialised eight global latencies per
+// chunk and left the tensor pipe 39 % idle in this GEMM.)
+__device__ __forceinline__ void epilogue_f32_add(const KArgs& args, uint32_t taddr, int row, int tg, int col_base) {
+  const bool row_ok = row < args.M;
+  float* crow = reinterpret_cast<float*>(args.C) + (long long)tg * args.c_gstride + (long long)row * args.ldc;
+  const float* rrow = args.R + (long long)tg * args.r_gstride + (long long)row * args.ldr;
+  const bool vec = row_ok && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(rrow) & 15) == 0) && ((args.ldc & 3) == 0) && ((args.ldr & 3) == 0);
+  auto whole = [&](int c) { return vec && col_base + c * 32 + 32 <= args.N; };
+  uint4 pr[8];
+  if (whole(0)) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) pr[j] = ld_cs_v4(rrow + col_base + 4 * j);
+  }
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    uint32_t r[32];
+    tmem_ld_32x32(taddr + c * 32, r);
+    const int col0 = col_base + c * 32;
+    uint4 nr[8];
+    if (c + 1 < BN / 32 && whole(c + 1)) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) nr[j] = ld_cs_v4(rrow + col0 + 32 + 4 * j);
+    }
+    tmem_ld_wait();
+    if (row_ok && col0 < args.N) {
+      if (whole(c)) {
+        float4* d4 = reinterpret_cast<float4*>(crow + col0);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          __stcs(d4 + j, make_float4(__uint_as_float(r[4 * j + 0]) + __uint_as_float(pr[j].x),
+                                     __uint_as_float(r[4 * j + 1]) + __uint_as_float(pr[j].y),
+                                     __uint_as_float(r[4 * j + 2]) + __uint_as_float(pr[j].z),
+                                     __uint_as_float(r[4 * j + 3]) + __uint_as_float(pr[j].w)));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (col0 + j < args.N) crow[col0 + j] = __uint_as_float(r[j]) + rrow[col0 + j];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) pr[j] = nr[j];
+  }
+}
+
 // SWIGLU_BWD: pull the up / gate row segments a tile's epilogue will read into L2 while
 // that tile's MMAs are still running (issued one tile ahead by the epilogue threads).
 __device__ __forceinline__ void epilogue_prefetch(const KArgs& args, int row, int tn) {
@@ -345,6 +394,7 @@ __device__ __forceinline__ void epilogue_store(const KArgs& args, uint32_t taddr
     case HLM_EPI_BF16_ROPE: epilogue_rope(args, taddr, row, tg, tn * BN); break;
     case HLM_EPI_SWIGLU: epilogue_swiglu(args, taddr, row, tn * (BN / 2)); break;
     case HLM_EPI_SWIGLU_BWD: epilogue_swiglu_bwd(args, taddr, row, tn * BN); break;
+    case HLM_EPI_F32_ADD: epilogue_f32_add(args, taddr, row, tg, tn * BN); break;
     default: epilogue_plain(args, taddr, row, tg, tn * BN, args.epi);
   }
 }
