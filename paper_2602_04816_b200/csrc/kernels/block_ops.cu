@@ -1021,10 +1021,13 @@ int hlm_ops_rmsnorm_bwd(const float* x, const void* scale, const float* g, const
                         cudaStream_t s) {
   const int rpc = HLM_NORM_ROWS_PER_CHUNK;
   const int chunks = (int)((rows + rpc - 1) / rpc);
-  static int minb = -1;   // HLM_RMSNORM_BWD_MINB=2: 128-register variant (A/B)
+  // 2 CTAs / SM (128 registers, no spills) by default: 268 vs 287 us at C2 against 3 CTAs / SM
+  // (80 registers, 16 B spilled), alternating on one box; HLM_RMSNORM_BWD_MINB=3 for A/B.
+  // (A next-row x / g prefetch at 2 CTAs / SM measured 317 us.)
+  static int minb = -1;
   if (minb < 0) {
     const char* e = std::getenv("HLM_RMSNORM_BWD_MINB");
-    minb = (e && *e == '2') ? 2 : 3;
+    minb = (e && *e == '3') ? 3 : 2;
   }
   if (h % 4 == 0 && h <= 4 * 256 * 4 && minb == 2) {
     rmsnorm_bwd_reg_kernel<256, 4, 2><<<chunks, 256, 0, s>>>(x, (const __nv_bfloat16*)scale, g, resid, out,
