@@ -308,6 +308,9 @@ typedef struct HlmEngineOptions {
   int32_t embed_gather_host;
   /* 1: leave the host optimizer's OpenMP team unpinned (default: pinned to cores) */
   int32_t no_pin_threads;
+  /* was transit_blocks (the transit-tile mode, removed in round 2): kept so the fields after
+   * it keep their offsets; must be 0 (a non-zero value is rejected with HLM_ERR_CONFIG) */
+  int64_t reserved_transit_blocks;
   /* blocks L - saved_act_layers + 1 .. L keep their forward activations in HBM until
    * their backward (no recompute; bit-identical: the recompute would reproduce them) */
   int64_t saved_act_layers;

@@ -118,6 +118,8 @@ hlm::EngineOptions to_opts(const HlmEngineOptions* o) {
         e.sparse_embed_grad = o->sparse_embed_grad != 0;
         e.embed_gather_host = o->embed_gather_host != 0;
         e.pin_threads = o->no_pin_threads == 0;
+        if (o->reserved_transit_blocks != 0)
+            throw hlm::ConfigError("engine options: transit tiles (transit_blocks) were removed; the field must be 0");
         e.saved_act_layers = o->saved_act_layers > 0 ? o->saved_act_layers : 0;
     }
     return e;

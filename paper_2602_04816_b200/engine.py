@@ -96,7 +96,7 @@ class EngineOptions(ctypes.Structure):
                 ("head_piece_vocab", ctypes.c_int64), ("piece_elems", ctypes.c_int64),
                 ("grad_buffers", ctypes.c_int64), ("sparse_embed_grad", ctypes.c_int32),
                 ("embed_gather_host", ctypes.c_int32), ("no_pin_threads", ctypes.c_int32),
-                ("saved_act_layers", ctypes.c_int64)]
+                ("reserved_transit_blocks", ctypes.c_int64), ("saved_act_layers", ctypes.c_int64)]
 
     def __init__(self, eager_optim=False, threaded_accum=False, n_slab=12, accum_delay_us=0,
                  skip_optimizer=False, fused_recompute=True, record_trace=True, block_flags=0,
@@ -111,7 +111,7 @@ class EngineOptions(ctypes.Structure):
                          comm_weights.value if isinstance(comm_weights, ctypes.c_void_p)
                          else comm_weights, host_threads, int(resident_embed), resident_blocks,
                          head_piece_vocab, piece_elems, grad_buffers, int(sparse_embed_grad),
-                         int(embed_gather_host), int(not pin_threads), saved_act_layers)
+                         int(embed_gather_host), int(not pin_threads), 0, saved_act_layers)
 
 
 class StepResult(ctypes.Structure):

@@ -468,3 +468,12 @@ def test_load_checkpoint_reuploads_hbm_resident_tiles(tmp_path):
     e1.sync()
     assert first == l0[2] and again == l0[2]
     assert s.adam_steps == 3 and s.bitwise_equal(ref)
+
+
+def test_removed_transit_field_is_rejected():
+    """The removed transit-tile mode keeps its C-ABI field (layout) and refuses non-zero."""
+    c = E.ModelConfig(2, 16, 32, 13, 4, 1)
+    o = E.EngineOptions(eager_optim=True)
+    o.reserved_transit_blocks = 1
+    with pytest.raises(E.HlmConfigError, match="transit"):
+        E.Engine(E.Store(c, 5), E.Arena(c), E.HyperParams(), o)
