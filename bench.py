@@ -411,6 +411,9 @@ def run_ours(args, m, name):
     # probes on a fresh GPU, before the store / engine exist (after a long host-bound run
     # the same launches read up to 25 % slower): the 12 block GEMMs and the elementwise /
     # norm kernels at the workload's shapes, back to back on random data
+    # attention first: measured after the GEMM probe the same launches read 1.4-1.7x slower
+    # (the GPU leaves its burst clocks under the GEMMs' power draw for a while)
+    attn_probe = attention_probe(lib, m)
     dims = _lib.HlmBlockDims(m["batch"], m["seq"], m["hidden"], m["ffn"], m["n_heads"], 0)
     ew_names = ("rmsnorm_fwd", "rmsnorm_bwd", "swiglu_fwd", "swiglu_bwd", "rope", "cast_bf16")
     ew_gbs, ew_ms = (ctypes.c_double * 6)(), (ctypes.c_double * 6)()
@@ -650,7 +653,9 @@ def run_ours(args, m, name):
                                "ms_per_launch": ms_launch.value,
                                "def": "the 12 block GEMMs at the workload shapes on random data, "
                                       "back to back (hlm_cuda_bench_block_gemms)"}},
-        "attention_roofline": {k: dict(kt[k], frac=(kt[k]["tflops"] or 0) / tf_burst, peak=tf_burst)
+        "attention_roofline": {k: dict(kt[k], frac=(kt[k]["tflops"] or 0) / tf_burst, peak=tf_burst,
+                                       frac_of_sustained=(kt[k]["tflops"] or 0) / tf_sus, peak_sustained=tf_sus,
+                                       standalone=attn_probe.get(k))
                                for k in ("attn_fwd", "attn_bwd")},
         "elementwise_roofline": {"peak_gbs": hbm, "unit": "GB/s", "in_step": ew_step, "probe": elementwise,
                                  "def": "algorithmic bytes (each tensor read/written once) / CUDA-event time; "
@@ -750,6 +755,46 @@ def run_wide(args):
                 "host_store_bytes": nums["params"] * 14}
         out[cfg] = entry
     return out
+
+
+def attention_probe(lib, m, iters=10):
+    """The attention kernels alone at the workload shape (random q/k/v/dO, CUDA events,
+    back to back, before the store exists): the standalone reference point for the in-step
+    attention numbers, which run at the clocks the GEMMs leave."""
+    import ctypes
+    import torch
+    from paper_2602_04816_b200 import _lib
+    B, S, H, h = m["batch"], m["seq"], m["n_heads"], m["hidden"]
+    T = B * S
+    try:
+        q, k, v, do = (torch.randn(T, h, device="cuda").bfloat16() for _ in range(4))
+        o, dq, dk, dv = (torch.empty_like(q) for _ in range(4))
+        lse, ds = torch.empty(B * H * S, device="cuda"), torch.empty(B * H * S, device="cuda")
+        d = _lib.HlmBlockDims(B, S, h, m["ffn"], H, 0)
+        vp = lambda t: ctypes.c_void_p(t.data_ptr())
+        fwd = lambda: _lib.check(lib.hlm_cuda_attention_fwd(ctypes.byref(d), vp(q), vp(k), vp(v), vp(o), vp(lse), h,
+                                                             None))
+        bwd = lambda: _lib.check(lib.hlm_cuda_attention_bwd(ctypes.byref(d), vp(q), vp(k), vp(v), vp(o), vp(do),
+                                                             vp(lse), vp(ds), vp(dq), vp(dk), vp(dv), h, None))
+        out = {}
+        fl = 2.0 * B * S * S * h   # causal: the reference's flop count (SURVEY §8d)
+        for name, fn, work in (("attn_fwd", fwd, fl), ("attn_bwd", bwd, 2.5 * fl)):
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(iters):
+                fn()
+            b.record()
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(b) / iters
+            out[name] = {"ms": ms, "tflops": work / (ms / 1e3) / 1e12}
+        del q, k, v, do, o, dq, dk, dv, lse, ds
+        torch.cuda.empty_cache()
+        return out
+    except Exception as ex:   # a probe, not the measurement: never fail the bench on it
+        return {"error": f"{type(ex).__name__}: {ex}"}
 
 
 def main():
