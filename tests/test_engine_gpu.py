@@ -53,6 +53,11 @@ CFGS = [
     ("tied-K3", E.ModelConfig(4, 8, 24, 11, 8, 2, k_ckpt=3, tie_embeddings=True)),
     ("c1-ref", E.ModelConfig(4, 256, 1024, 1024, 128, 4, k_ckpt=1)),
     ("c1-qwen", E.ModelConfig(4, 256, 1024, 1024, 128, 4, k_ckpt=1, n_heads=2, rope_theta=1e6)),
+    # the attention paths by shape: two-query-tile forward + 64-wide backward over several
+    # tiles (S 512), the one-tile forward (S % 256 != 0), head_dim 64 (mma.sync kernels)
+    ("qwen-s512", E.ModelConfig(2, 256, 512, 512, 512, 2, k_ckpt=1, n_heads=2, rope_theta=1e6)),
+    ("qwen-s384", E.ModelConfig(2, 256, 512, 512, 384, 2, k_ckpt=1, n_heads=2, rope_theta=1e6)),
+    ("qwen-hd64", E.ModelConfig(2, 256, 512, 512, 256, 2, k_ckpt=1, n_heads=4, rope_theta=1e6)),
 ]
 
 
