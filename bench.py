@@ -262,7 +262,7 @@ def run_reference(args, m, name):
     if rank != 0:
         return
     steps = max(1, args.steps)
-    warmup = min(1, args.warmup)
+    warmup = max(0, args.warmup)   # the same W untimed samples as our arm
     cores = int(os.environ.get("HLM_REF_CORES", 0)) or (os.cpu_count() or 1)
     avail = _mem_available()
     if avail:   # ~6.5 GB per replica at C2 width
