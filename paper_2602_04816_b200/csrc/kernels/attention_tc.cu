@@ -713,7 +713,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       for (int kk = 0; kk < 4; ++kk)
         umma_bf16_ts_w(tmem + 256 + t * 128, p_tmem + kk * 8, mnmajor_desc64(v_base, kk), idesc_o,
                        (j > 0 || kk > 0) ? 1u : 0u);
-      umma_commit_w(&bars->pv_done[t]);
+      if (j + 2 == n_t[t]) umma_commit_w(&bars->pv_done[t]);   // PV_t(n-2): for a rescale at the last step
       if (t == 1) umma_commit_w(&bars->kv_empty[st]);
       if (j + 1 == n_t[t]) umma_commit_w(&bars->o_final[t]);
     };
@@ -766,8 +766,13 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       if (j == 0) {
         m = mx;
       } else if (__any_sync(0xffffffffu, mx > m + kRescaleLog2)) {
-        // O_t holds P V of steps < j; PV_t(j-1) may still run: wait for it, then rescale
-        mbar_wait(&bars->pv_done[t], (j - 1) & 1);
+        // O_t holds P V of steps < j; PV_t(j-1) may still run: wait for it, then rescale.
+        // S_t(j+1) was issued right behind PV_t(j-1) (in-order tensor pipe), so its s_full
+        // covers it; the last step has no S_t(j+1) and waits pv_done (PV_t(n-2) only)
+        if (j + 1 < n)
+          mbar_wait(&bars->s_full[t][(j + 1) & 1], ((j + 1) >> 1) & 1);
+        else
+          mbar_wait(&bars->pv_done[t], 0);
         tc_fence_after();
         const float mn = fmaxf(m, mx);
         const float alpha = ex2(m - mn);
@@ -813,6 +818,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       if (lane == 0) mbar_arrive(&bars->p_full[t][j & 1]);
     }
     mbar_wait(&bars->o_final[t], 0);
+    mbar_wait(&bars->pv_done[t], 0);   // its one phase (complete with o_final)
     tc_fence_after();
     const float il = 1.f / l;
     __nv_bfloat16* orow = o + (long long)(row0 + qpos) * ld + col0;

@@ -194,7 +194,9 @@ int main(int argc, char** argv) {
     gemm(256, 512, 1024, 1, 1, HLM_EPI_F32, 2, 0);     // wgrad (MN-major A and B), grouped
     if (!quick) gemm(1024, 768, 1536, 0, 1, HLM_EPI_F32);
     // attention: tcgen05 (hd 128, S % 128) and mma.sync (hd 64) paths, plus the generic one
-    attention(1, 256, 2, 128, 0);
+    attention(1, 256, 2, 128, 0);   // two-query-tile forward (64-key steps), 64-wide backward
+    attention(1, 512, 1, 128, 0);   // the same over 8 steps: K / V and Q / dO rings wrap
+    attention(1, 384, 1, 128, 0);   // one-tile forward (S % 256 != 0)
     attention(2, 128, 2, 64, 0);
     attention(1, 64, 2, 32, 1);
     // a whole block with RoPE (hd 128), the head + CE both ways
