@@ -694,7 +694,8 @@ def run_ours(args, m, name):
     return line
 
 
-WIDE_POINTS = {"c4": (2, 4, 6), "c5": (1, 2)}
+WIDE_POINTS = {"c3": (4, 8), "c4": (2, 4, 6), "c5": (1, 2)}
+WIDE_DEFAULT = ("c4", "c5")   # the north-star target width and the largest; c3 on request (--wide-only)
 
 
 def run_wide(args):
@@ -705,7 +706,7 @@ def run_wide(args):
     from a per-layer fit t(L) = a + b L. Projections are labelled as such."""
     out = {}
     for cfg, depths in WIDE_POINTS.items():
-        if args.wide_only and cfg not in args.wide_only.split(","):
+        if cfg not in (args.wide_only.split(",") if args.wide_only else WIDE_DEFAULT):
             continue
         pts = []
         for L in depths:
@@ -844,7 +845,7 @@ def main():
                          "batch split over the N ranks (SURVEY 8d)")
     ap.add_argument("--no-wide", action="store_true",
                     help="skip the C4 / C5 full-width depth sweeps reported beside a C2 headline")
-    ap.add_argument("--wide-only", default="", help="comma list of wide configs to sweep (c4,c5)")
+    ap.add_argument("--wide-only", default="", help="comma list of wide configs to sweep (default c4,c5; c3 too)")
     ap.add_argument("--wide-steps", type=int, default=3, help="timed steps per wide point")
     args = ap.parse_args()
     m = dict(CONFIGS[args.config])
