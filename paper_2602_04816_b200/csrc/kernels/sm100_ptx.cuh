@@ -128,9 +128,6 @@ template <int N, int AHI, int ALO, int BHI, int BLO>
 __device__ __forceinline__ void umma_chain_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                              uint32_t acc_first) {
   static_assert(N == 4 || N == 8, "chain of 4 or 8");
-#define HLM_MMA_STEP(k)                                             \
-  "add.s64 ta, %1, " #k "a; add.s64 tb, %2, " #k "b;\n"              \
-  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ta, tb, %3, 1;\n"
   if constexpr (N == 4) {
     asm volatile(
         "{\n.reg .pred e, p;\n.reg .b64 ta, tb;\n"
@@ -161,7 +158,6 @@ __device__ __forceinline__ void umma_chain_w(uint32_t d_tmem, uint64_t a_desc, u
         "n"(3 * ALO), "n"(3 * BLO), "n"(AHI), "n"(BHI), "n"(AHI + ALO), "n"(BHI + BLO), "n"(AHI + 2 * ALO),
         "n"(BHI + 2 * BLO), "n"(AHI + 3 * ALO), "n"(BHI + 3 * BLO));
   }
-#undef HLM_MMA_STEP
 }
 
 __device__ __forceinline__ void umma_commit_w(uint64_t* bar) {
