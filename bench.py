@@ -675,10 +675,14 @@ def run_ours(args, m, name):
                                  "bandwidth)"},
         "stream": {"h2d_gbs": h2d_gbs, "d2h_gbs": d2h_gbs, "overlap": overlap,
                    "h2d_overlap": rep["h2d_overlap"], "h2d_exposed_s": rep["h2d_exposed_ms"] / 1e3,
+                   "d2h_overlap": rep["d2h_overlap"], "d2h_exposed_s": rep["d2h_exposed_ms"] / 1e3,
+                   "transfer_overlap": rep["transfer_overlap"],
                    "compute_idle_s": rep["compute_idle_ms"] / 1e3,
                    "overlap_def": "overlap: share of H2D + D2H busy time with the compute stream busy; "
                                   "h2d_overlap: 1 - (compute idle while a weight transfer it waits on "
-                                  "is in flight) / H2D busy time",
+                                  "is in flight) / H2D busy time; d2h_overlap: the same for a backward "
+                                  "waiting on its gradient buffer's D2H; transfer_overlap: both "
+                                  "directions, 1 - exposed transfer / transfer (SURVEY 8d)",
                    "gpu_span_s": gpu_span_s, "compute_busy_s": rep["compute_busy_ms"] / 1e3,
                    "host_adam_s": adam_s,
                    "h2d_bytes_measured": int(h2d_step), "trace_violations": len(violations)},

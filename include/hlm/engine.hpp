@@ -210,6 +210,10 @@ private:
     void* gbuf_mem_ = nullptr;
     std::vector<void*> ev_grad_ready_;
     std::vector<void*> ev_gradbuf_free_;
+    // trace: the op after which each gradient buffer is free (its D2H, or the device Adam of
+    // a resident tile), attached as a dependency of the next backward writing that buffer
+    std::vector<i64> gbuf_free_op_;
+    i64 gbuf_dep_ = -1;
     float* grad_buf(int i) const { return gbuf_[static_cast<size_t>(i)]; }
     std::vector<void*> ev_slab_done_;
     // Large gradients land in pieces of kPieceElems: per slab, an event after the

@@ -346,6 +346,10 @@ void Engine::h2d_tile(void* dst, const LayerTile& tile, i64 bytes) {
 
 // ------------------------------------------------------------------ trace helpers
 i64 Engine::op_begin(StreamOp op, void* stream) {
+    if (op.kind == OpKind::LocalBackward && gbuf_dep_ >= 0) {   // waits for its gradient buffer
+        op.deps.push_back(gbuf_dep_);
+        gbuf_dep_ = -1;
+    }
     const i64 id = trace_.add(std::move(op));
     if (opts_.record_trace && stream) {
         if (timing_used_ + 2 > timing_events_.size()) {
@@ -524,6 +528,7 @@ int Engine::next_grad_buf() {
     const int gb = next_gbuf_;
     next_gbuf_ = (next_gbuf_ + 1) % static_cast<int>(gbuf_.size());
     ck(cudaStreamWaitEvent(S(compute_), E(ev_gradbuf_free_[gb]), 0), "wait grad buf");
+    gbuf_dep_ = static_cast<size_t>(gb) < gbuf_free_op_.size() ? gbuf_free_op_[static_cast<size_t>(gb)] : -1;
     return gb;
 }
 
@@ -589,6 +594,7 @@ void Engine::evacuate(i64 tile_id, int gbuf, i64 n_params, i64 lb_op, bool spars
         ck(cudaStreamWaitEvent(S(d2h_), E(ev_grad_ready_[gbuf]), 0), "wait grad ready");
     }
     const i64 id = op_begin(std::move(op), d2h_);
+    gbuf_free_op_[static_cast<size_t>(gbuf)] = id;
     // the finiteness flag lands first, then the gradient in pieces (the optimizer starts on piece 0)
     ck(cudaMemcpyAsync(nf_host_ + slab, nf_dev_ + slab, 8, cudaMemcpyDeviceToHost, S(d2h_)), "D2H nf flag");
     ck(cudaEventRecord(E(ev_slab_flag_[static_cast<size_t>(slab)]), S(d2h_)), "record slab flag");
@@ -754,6 +760,7 @@ void Engine::resident_update(i64 tile, int gbuf, i64 dep_op) {
                          resident_bad_ + ri, &hp, step_t_, opt_),
            "device adam");
     op_end(id, opt_);
+    gbuf_free_op_[static_cast<size_t>(gbuf)] = id;
     ck(cudaEventRecord(E(ev_gradbuf_free_[gbuf]), S(opt_)), "record grad buf free (resident)");
     if (!resident_dirty_) store_.add_device_newer(1);
     resident_dirty_ = true;
@@ -958,6 +965,8 @@ void Engine::begin_step(const Batch& batch) {
     arena_.begin_step();
     arena_.claim_workspace();
     trace_ = EventTrace{};
+    gbuf_free_op_.assign(gbuf_.size(), -1);   // op ids are per step
+    gbuf_dep_ = -1;
     trace_.meta = TraceMeta{m.layers, 2, pool_->size(), m.embed_tile_id(), m.head_tile_id()};
     op_events_.clear();
     timing_used_ = 0;
@@ -1205,6 +1214,7 @@ void Engine::anchor_loss_pieces(int buf, i64 w_op) {
         ck(cudaEventRecord(E(ev_piece_[static_cast<size_t>(slab * max_pieces_ + k)]), S(d2h_)), "record piece");
         if (k == 0) first_gx = gxid;
         last_lb = lbid;
+        gbuf_free_op_[static_cast<size_t>(gb)] = gxid;
     }
     compute_done_with(buf, last_lb);
     // the certificate's fallback: the full scan of the head gradient

@@ -172,25 +172,35 @@ def exposed_weights(ops):
     transfer to be issued at all (the host optimizer had not finished that tile)
     or for other work. h2d_overlap = 1 - exposed / H2D busy time: the per-layer
     compute/transfer overlap of the north-star target, separated from host-paced
-    idling."""
+    idling; d2h_overlap the same for the gradient D2H (a backward waiting for its gradient
+    buffer to drain), transfer_overlap both directions together (SURVEY §8d's
+    1 - exposed transfer / transfer)."""
     by_id = {o["id"]: o for o in ops}
     comp = sorted((o for o in ops if o["stream"] == "compute" and o["t_end_us"] > o["t_start_us"] >= 0),
                   key=lambda o: o["t_start_us"])
-    prev, idle, exposed = 0.0, 0.0, 0.0   # timestamps are relative to the step-start event
+    prev, idle = 0.0, 0.0   # timestamps are relative to the step-start event
+    exposed = {"h2d": 0.0, "d2h": 0.0}
     for c in comp:
         if c["t_start_us"] > prev:
             g0, g1 = prev, c["t_start_us"]
             idle += g1 - g0
-            spans = []
-            for d in c["deps"]:
-                x = by_id.get(d)
-                if x and x["stream"] == "h2d" and x["t_end_us"] > x["t_start_us"] >= 0:
-                    lo, hi = max(g0, x["t_start_us"]), min(g1, x["t_end_us"])
-                    if hi > lo:
-                        spans.append((lo, hi))
-            exposed += sum(e - s for s, e in _union(spans))
+            for st in exposed:
+                spans = []
+                for d in c["deps"]:
+                    x = by_id.get(d)
+                    if x and x["stream"] == st and x["t_end_us"] > x["t_start_us"] >= 0:
+                        lo, hi = max(g0, x["t_start_us"]), min(g1, x["t_end_us"])
+                        if hi > lo:
+                            spans.append((lo, hi))
+                exposed[st] += sum(e - s for s, e in _union(spans))
         prev = max(prev, c["t_end_us"])
-    busy = sum(o["t_end_us"] - o["t_start_us"] for o in ops
-               if o["stream"] == "h2d" and o["t_end_us"] > o["t_start_us"] >= 0)
-    return {"compute_idle_ms": idle / 1e3, "h2d_exposed_ms": exposed / 1e3,
-            "h2d_overlap": 1.0 - exposed / busy if busy > 0 else None}
+    busy = {st: sum(o["t_end_us"] - o["t_start_us"] for o in ops
+                    if o["stream"] == st and o["t_end_us"] > o["t_start_us"] >= 0) for st in exposed}
+    both = busy["h2d"] + busy["d2h"]
+    # d2h exposure: the compute stream idling on a gradient D2H that must drain before the
+    # next backward can write that gradient buffer (the backward's dependency on it)
+    return {"compute_idle_ms": idle / 1e3, "h2d_exposed_ms": exposed["h2d"] / 1e3,
+            "h2d_overlap": 1.0 - exposed["h2d"] / busy["h2d"] if busy["h2d"] > 0 else None,
+            "d2h_exposed_ms": exposed["d2h"] / 1e3,
+            "d2h_overlap": 1.0 - exposed["d2h"] / busy["d2h"] if busy["d2h"] > 0 else None,
+            "transfer_overlap": 1.0 - (exposed["h2d"] + exposed["d2h"]) / both if both > 0 else None}

@@ -117,3 +117,29 @@ def test_exposed_weights_counts_only_waits_on_inflight_transfers():
     assert abs(r["compute_idle_ms"] - 0.5) < 1e-9        # 100 -> 600
     assert abs(r["h2d_exposed_ms"] - 0.1) < 1e-9         # only 500 -> 600 had the transfer in flight
     assert abs(r["h2d_overlap"] - (1 - 100.0 / 150.0)) < 1e-9
+
+
+def test_exposed_gradient_drain_counts_waits_on_the_buffer_d2h():
+    """d2h_overlap: a backward that waits for its gradient buffer's previous D2H to drain
+    exposes that transfer; a D2H that drained under compute is hidden. transfer_overlap
+    combines both directions."""
+    from paper_2602_04816_b200.trace import exposed_weights
+    ops = [
+        {"id": 0, "stream": "compute", "kind": "LocalBackward", "layer": 3, "deps": [], "t_start_us": 0.0,
+         "t_end_us": 100.0, "bytes": 0},
+        {"id": 1, "stream": "d2h", "kind": "GradXfer", "layer": 3, "deps": [0], "t_start_us": 100.0,
+         "t_end_us": 400.0, "bytes": 1000},
+        # the next backward reuses the buffer: it starts only when the D2H is done (300 us exposed)
+        {"id": 2, "stream": "compute", "kind": "LocalBackward", "layer": 2, "deps": [1], "t_start_us": 400.0,
+         "t_end_us": 500.0, "bytes": 0},
+        {"id": 3, "stream": "d2h", "kind": "GradXfer", "layer": 2, "deps": [2], "t_start_us": 500.0,
+         "t_end_us": 600.0, "bytes": 1000},
+        # a later backward on that buffer with the drain already hidden under other compute
+        {"id": 4, "stream": "compute", "kind": "LocalBackward", "layer": 1, "deps": [3], "t_start_us": 500.0,
+         "t_end_us": 700.0, "bytes": 0},
+    ]
+    r = exposed_weights(ops)
+    assert abs(r["d2h_exposed_ms"] - 0.3) < 1e-9
+    assert abs(r["d2h_overlap"] - (1 - 300.0 / 400.0)) < 1e-9
+    assert r["h2d_overlap"] is None
+    assert abs(r["transfer_overlap"] - (1 - 300.0 / 400.0)) < 1e-9
