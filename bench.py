@@ -727,6 +727,7 @@ def run_wide(args):
             pts.append({"layers": L, "params": d["config"]["params"], "value": d["value"],
                         "ms_per_step": d["ms_per_step"], "tflops": d["tflops"],
                         "e2e": d["e2e"]["value"], "h2d_overlap": d["stream"]["h2d_overlap"],
+                        "transfer_overlap": d["stream"].get("transfer_overlap"),
                         "overlap": d["stream"]["overlap"], "host_adam_s": d["stream"]["host_adam_s"],
                         "compute_busy_s": d["stream"]["compute_busy_s"],
                         "gemm_tflops_in_step": d["roofline"]["achieved"],
