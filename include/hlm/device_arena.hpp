@@ -29,24 +29,33 @@ struct LedgerEvent {
     i64 delta;
 };
 
+// Byte accounting per region (the reference ArenaLedger's contract: per-region and
+// whole-arena step peaks, a peak excluding the checkpoint anchors, an event log, the
+// region named in the ArenaOomError of an over-claim).
 class ArenaLedger {
 public:
-    void init_region(Region r, i64 capacity) { cap_[static_cast<int>(r)] = capacity; }
+    void init_region(Region r, i64 capacity) { slot(r).cap = capacity; }
     void claim(Region r, i64 bytes);
     void release(Region r, i64 bytes);
     void begin_step();
-    i64 capacity(Region r) const { return cap_[static_cast<int>(r)]; }
-    i64 current(Region r) const { return cur_[static_cast<int>(r)]; }
-    i64 step_peak(Region r) const { return peak_[static_cast<int>(r)]; }
+    i64 capacity(Region r) const { return slot(r).cap; }
+    i64 current(Region r) const { return slot(r).cur; }
+    i64 step_peak(Region r) const { return slot(r).peak; }
     i64 total_capacity() const;
-    i64 total_current() const { return total_cur_; }
-    i64 step_peak_total() const { return total_peak_; }
-    i64 step_peak_non_anchor() const { return na_peak_; }
+    i64 total_current() const { return all_.cur; }
+    i64 step_peak_total() const { return all_.peak; }
+    i64 step_peak_non_anchor() const { return non_anchor_.peak; }
     const std::vector<LedgerEvent>& events() const { return events_; }
 
 private:
-    std::array<i64, kRegionCount> cap_{}, cur_{}, peak_{};
-    i64 total_cur_ = 0, total_peak_ = 0, na_cur_ = 0, na_peak_ = 0;
+    struct Level {   // a running byte count and its high-water mark since begin_step()
+        i64 cap = 0, cur = 0, peak = 0;
+        void add(i64 b) { cur += b; peak = cur > peak ? cur : peak; }
+    };
+    Level& slot(Region r) { return regions_[static_cast<size_t>(r)]; }
+    const Level& slot(Region r) const { return regions_[static_cast<size_t>(r)]; }
+    std::array<Level, kRegionCount> regions_{};
+    Level all_, non_anchor_;
     std::vector<LedgerEvent> events_;
 };
 
