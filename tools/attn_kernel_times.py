@@ -1,5 +1,8 @@
+"""Per-kernel device times of one attention backward at the C2 shape (torch profiler):
+the D kernel, dK/dV and dQ separately. Variants via the HLM_ATTN_* environment switches
+(INTEGRATION.md §7)."""
 import ctypes, os, sys
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2602_04816_b200 import _lib as L
 Lb = L.blib()
