@@ -303,6 +303,105 @@ __global__ void __launch_bounds__(THREADS, MINB)
   }
 }
 
+// The same computation with the row's scale and the chunk's scale-gradient partial in
+// shared memory instead of registers (32 registers fewer per thread): 3 CTAs per SM, so
+// three rows' HBM traffic is in flight per SM instead of two. Each thread owns the same
+// float4 columns in both, so the per-column sums run in the same row order: bit-identical
+// to rmsnorm_bwd_reg_kernel.
+template <int THREADS, int V, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB)
+    rmsnorm_bwd_smem_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ scale,
+                            const float* __restrict__ g, const float* __restrict__ resid, float* __restrict__ out,
+                            __nv_bfloat16* __restrict__ out_bf, float* __restrict__ inv_out,
+                            float* __restrict__ partial, long long rows, int h, int rows_per_chunk) {
+  constexpr int NW = THREADS / 32;
+  __shared__ float red[2][2][NW];
+  extern __shared__ float4 dyn4[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nv = h >> 2;
+  float4* ssc = dyn4;          // [nv] row scale
+  float4* sacc = dyn4 + nv;    // [nv] scale-gradient partial of the chunk
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const int q = tid + k * THREADS;
+    if (q < nv) {
+      const uint2 spk = *reinterpret_cast<const uint2*>(scale + 4 * q);
+      const float2 s01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&spk.x));
+      const float2 s23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&spk.y));
+      ssc[q] = make_float4(s01.x, s01.y, s23.x, s23.y);
+      sacc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  const long long r0 = (long long)blockIdx.x * rows_per_chunk;
+  const long long r1 = r0 + rows_per_chunk < rows ? r0 + rows_per_chunk : rows;
+  int par = 0;
+  for (long long r = r0; r < r1; ++r, par ^= 1) {
+    float4 xv[V], gv[V];
+    float ss = 0.f, dot = 0.f;
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      const int q = tid + k * THREADS;
+      if (q < nv) {
+        xv[k] = __ldcs(reinterpret_cast<const float4*>(x + r * h) + q);
+        gv[k] = __ldcs(reinterpret_cast<const float4*>(g + r * h) + q);
+        const float4 sc = ssc[q];
+        ss += xv[k].x * xv[k].x + xv[k].y * xv[k].y + xv[k].z * xv[k].z + xv[k].w * xv[k].w;
+        dot += gv[k].x * sc.x * xv[k].x + gv[k].y * sc.y * xv[k].y + gv[k].z * sc.z * xv[k].z +
+               gv[k].w * sc.w * xv[k].w;
+      }
+    }
+    ss = warp_sum(ss);
+    dot = warp_sum(dot);
+    if (lane == 0) {
+      red[par][0][warp] = ss;
+      red[par][1][warp] = dot;
+    }
+    __syncthreads();   // red[par] complete; red[par ^ 1] (last row) no longer read
+    ss = 0.f;
+    dot = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      ss += red[par][0][w];
+      dot += red[par][1][w];
+    }
+    const float inv = 1.0f / sqrtf(ss / (float)h + kEps);
+    const float c = inv * inv * inv * dot / (float)h;
+    if (tid == 0) inv_out[r] = inv;
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      const int q = tid + k * THREADS;
+      if (q < nv) {
+        const float4 sc = ssc[q];
+        const float4 rv = resid ? __ldcs(reinterpret_cast<const float4*>(resid + r * h) + q)
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 v = make_float4(gv[k].x * sc.x * inv - c * xv[k].x + rv.x,
+                                     gv[k].y * sc.y * inv - c * xv[k].y + rv.y,
+                                     gv[k].z * sc.z * inv - c * xv[k].z + rv.z,
+                                     gv[k].w * sc.w * inv - c * xv[k].w + rv.w);
+        __stcs(reinterpret_cast<float4*>(out + r * h) + q, v);
+        if (out_bf) {
+          __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+          uint2 pk;
+          pk.x = *reinterpret_cast<uint32_t*>(&lo);
+          pk.y = *reinterpret_cast<uint32_t*>(&hi);
+          reinterpret_cast<uint2*>(out_bf + r * h)[q] = pk;
+        }
+        float4 a = sacc[q];
+        a.x += gv[k].x * xv[k].x * inv;
+        a.y += gv[k].y * xv[k].y * inv;
+        a.z += gv[k].z * xv[k].z * inv;
+        a.w += gv[k].w * xv[k].w * inv;
+        sacc[q] = a;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const int q = tid + k * THREADS;
+    if (q < nv) reinterpret_cast<float4*>(partial + (long long)blockIdx.x * h)[q] = sacc[q];
+  }
+}
+
 // partial[c][j] = sum_{r in chunk c} g[r][j] * x[r][j] * inv[r]   (columns across threads)
 __global__ void norm_scale_partial_kernel(const float* __restrict__ x, const float* __restrict__ g,
                                           const float* __restrict__ inv, float* __restrict__ partial,
@@ -1021,15 +1120,19 @@ int hlm_ops_rmsnorm_bwd(const float* x, const void* scale, const float* g, const
                         cudaStream_t s) {
   const int rpc = HLM_NORM_ROWS_PER_CHUNK;
   const int chunks = (int)((rows + rpc - 1) / rpc);
-  // 2 CTAs / SM (128 registers, no spills) by default: 268 vs 287 us at C2 against 3 CTAs / SM
-  // (80 registers, 16 B spilled), alternating on one box; HLM_RMSNORM_BWD_MINB=3 for A/B.
-  // (A next-row x / g prefetch at 2 CTAs / SM measured 317 us.)
+  // Default: scale / partial in shared memory, 3 CTAs / SM (78 registers): 230 us at C2 vs
+  // 267 (registers, 2 CTAs / SM, 117 registers) and 287 (registers, 3 CTAs / SM, 16 B spilled),
+  // alternating on one box; bit-identical (tested). HLM_RMSNORM_BWD_MINB=2 / 3 selects the
+  // register variants. (A next-row x / g prefetch at 2 CTAs / SM measured 317 us.)
   static int minb = -1;
   if (minb < 0) {
     const char* e = std::getenv("HLM_RMSNORM_BWD_MINB");
-    minb = (e && *e == '3') ? 3 : 2;
+    minb = (e && *e == '3') ? 3 : (e && *e == '2') ? 2 : 5;
   }
-  if (h % 4 == 0 && h <= 4 * 256 * 4 && minb == 2) {
+  if (h % 4 == 0 && h <= 4 * 256 * 4 && minb == 5) {   // scale / partial in shared memory, 3 CTAs / SM
+    rmsnorm_bwd_smem_kernel<256, 4, 3><<<chunks, 256, 2 * h * sizeof(float), s>>>(
+        x, (const __nv_bfloat16*)scale, g, resid, out, (__nv_bfloat16*)out_bf, inv_buf, partial, rows, h, rpc);
+  } else if (h % 4 == 0 && h <= 4 * 256 * 4 && minb == 2) {
     rmsnorm_bwd_reg_kernel<256, 4, 2><<<chunks, 256, 0, s>>>(x, (const __nv_bfloat16*)scale, g, resid, out,
                                                              (__nv_bfloat16*)out_bf, inv_buf, partial, rows, h, rpc);
   } else if (h % 4 == 0 && h <= 4 * 256 * 4) {

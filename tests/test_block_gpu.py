@@ -182,3 +182,50 @@ def test_head_loss_is_chunked_and_matches_torch():
     assert abs(loss_rows.double().sum().item() - loss.item()) < 1e-3 * loss.item()
     assert rel_l2(dx.cpu().numpy(), xb.grad.cpu().numpy()) < 2e-2
     assert rel_l2(dhead.cpu().numpy(), hf.grad.cpu().numpy()) < 2e-2
+
+
+_RMS_SCRIPT = r"""
+import ctypes, sys, torch
+sys.path.insert(0, {root!r})
+from paper_2602_04816_b200 import _lib as L
+Lb = L.blib()
+torch.manual_seed(0)
+B, S, h, f, H = 1, 512, 3584, 1024, 28
+T, n = B * S, 4 * h * h + 3 * h * f + 2 * h
+W = torch.cat([torch.randn(n - 2 * h, device="cuda") * 0.02, 1 + 0.1 * torch.randn(2 * h, device="cuda")]).bfloat16()
+x = torch.randn(T, h, device="cuda"); g = torch.randn(T, h, device="cuda") * 1e-2
+y, gi = torch.empty_like(x), torch.empty_like(x); grad = torch.empty(n, device="cuda")
+d = L.HlmBlockDims(B, S, h, f, H, 0)
+acts = torch.empty(Lb.hlm_cuda_block_acts_bytes(ctypes.byref(d)), dtype=torch.uint8, device="cuda")
+ws = torch.empty(Lb.hlm_cuda_block_ws_bytes(ctypes.byref(d)), dtype=torch.uint8, device="cuda")
+hd = h // H
+cs = torch.empty(S * hd // 2, device="cuda"); sn = torch.empty_like(cs)
+vp = lambda t: ctypes.c_void_p(t.data_ptr())
+L.check(Lb.hlm_cuda_rope_table(vp(cs), vp(sn), S, hd, 1e6))
+L.check(Lb.hlm_cuda_block_fwd(ctypes.byref(d), vp(W), vp(x), vp(y), vp(acts), vp(ws), vp(cs), vp(sn), None))
+L.check(Lb.hlm_cuda_block_bwd(ctypes.byref(d), vp(W), vp(x), vp(acts), vp(g), vp(gi), vp(grad), vp(ws), vp(cs),
+                              vp(sn), None))
+torch.cuda.synchronize()
+torch.save({{"gi": gi.cpu(), "grad": grad.cpu()}}, sys.argv[1])
+"""
+
+
+def test_rmsnorm_backward_variants_are_bitwise_equal(tmp_path):
+    """The RMSNorm backward kernels (scale / scale-gradient partial in registers at 2 or 3
+    CTAs per SM, or in shared memory) sum every column in the same row order: a whole
+    block backward is bit-identical across them."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "rms.py"
+    script.write_text(_RMS_SCRIPT.format(root=root))
+    res = {}
+    for m in ("2", "3", "5"):
+        out = tmp_path / f"rms_{m}.pt"
+        subprocess.run([sys.executable, str(script), str(out)], check=True,
+                       env={**os.environ, "HLM_RMSNORM_BWD_MINB": m})
+        res[m] = torch.load(out)
+    for m in ("3", "5"):
+        assert torch.equal(res[m]["gi"], res["2"]["gi"]), m
+        assert torch.equal(res[m]["grad"], res["2"]["grad"]), m
