@@ -498,11 +498,14 @@ __global__ void __launch_bounds__(NW * 32) flash_bwd_dkv(const __nv_bfloat16* __
   }
 }
 
+template <int HD>
 __global__ void dsum_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
-                            float* __restrict__ dsum, int B, int S, int H, int hd, int ld) {
+                            float* __restrict__ dsum, int B, int S, int H, int ld) {
   // D[b][h][i] = rowsum(dO * O) per head. One warp per token row (b, i), walking its
   // H heads contiguously: 16-byte loads, each half-warp covers one head of hd = 128
-  // (hd = 64: a quarter-warp), segmented shuffle reduction. Fully coalesced.
+  // (hd = 64: a quarter-warp), segmented shuffle reduction. Fully coalesced. The loads of
+  // kBatch head groups are issued before any math (more bytes in flight per warp).
+  constexpr int kLanesPerHead = HD / 8, kHeadsPerIter = 32 / kLanesPerHead, kBatch = 4;
   const long long rows = (long long)B * S;
   const long long gw = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (gw >= rows) return;
@@ -510,25 +513,35 @@ __global__ void dsum_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bflo
   const int b = (int)(gw / S), i = (int)(gw % S);
   const __nv_bfloat16* orow = o + gw * ld;
   const __nv_bfloat16* drow = dout + gw * ld;
-  const int lanes_per_head = hd / 8;                 // 16 (hd 128) or 8 (hd 64)
-  const int heads_per_iter = 32 / lanes_per_head;
-  for (int h0 = 0; h0 < H; h0 += heads_per_iter) {
-    const int hh = h0 + lane / lanes_per_head;
-    float s = 0.f;
-    if (hh < H) {
-      const int d = (lane % lanes_per_head) * 8;
-      const uint4 a = *reinterpret_cast<const uint4*>(orow + (long long)hh * hd + d);
-      const uint4 c = *reinterpret_cast<const uint4*>(drow + (long long)hh * hd + d);
-      const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
-      const __nv_bfloat162* c2 = reinterpret_cast<const __nv_bfloat162*>(&c);
+  const int d = (lane % kLanesPerHead) * 8;
+  for (int h0 = 0; h0 < H; h0 += kBatch * kHeadsPerIter) {
+    uint4 a[kBatch], c[kBatch];
+#pragma unroll
+    for (int k = 0; k < kBatch; ++k) {
+      const int hh = h0 + k * kHeadsPerIter + lane / kLanesPerHead;
+      if (hh < H) {
+        a[k] = *reinterpret_cast<const uint4*>(orow + (long long)hh * HD + d);
+        c[k] = *reinterpret_cast<const uint4*>(drow + (long long)hh * HD + d);
+      } else {
+        a[k] = make_uint4(0, 0, 0, 0);
+        c[k] = a[k];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kBatch; ++k) {
+      const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a[k]);
+      const __nv_bfloat162* c2 = reinterpret_cast<const __nv_bfloat162*>(&c[k]);
+      float s = 0.f;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const float2 x = __bfloat1622float2(a2[e]), y = __bfloat1622float2(c2[e]);
         s += x.x * y.x + x.y * y.y;
       }
+#pragma unroll
+      for (int off = kLanesPerHead / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      const int hh = h0 + k * kHeadsPerIter + lane / kLanesPerHead;
+      if (hh < H && lane % kLanesPerHead == 0) dsum[((long long)b * H + hh) * S + i] = s;
     }
-    for (int off = lanes_per_head / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (hh < H && lane % lanes_per_head == 0) dsum[((long long)b * H + hh) * S + i] = s;
   }
 }
 
@@ -571,9 +584,9 @@ int bwd_impl(const void* q, const void* k, const void* v, const void* o, const v
     attr = true;
   }
   const float scale = 1.0f / sqrtf((float)HD);
-  dsum_kernel<<<(unsigned)(((long long)B * S + 7) / 8), 256, 0, s>>>((const __nv_bfloat16*)o,
-                                                                       (const __nv_bfloat16*)dout, dsum, B, S, H,
-                                                                       HD, ld);
+  dsum_kernel<HD><<<(unsigned)(((long long)B * S + 7) / 8), 256, 0, s>>>((const __nv_bfloat16*)o,
+                                                                           (const __nv_bfloat16*)dout, dsum, B, S,
+                                                                           H, ld);
   if (use_tc() && hlm_flash_tc_supported(HD, S, ld)) {
     hlm_count_launches(1);
     return hlm_flash_bwd_tc(q, k, v, dout, lse, dsum, dq, dk, dv, B, S, H, ld, s);

@@ -626,11 +626,30 @@ struct PP2Bars {
 };
 constexpr int PP2_SMEM = TILE_BYTES * 2 + KF_STAGES * 2 * HALF_TILE + 1024 + 256;
 
+// Grid order of the production kernels. grid = (tiles per head, B * H); `rank` 0 is the
+// longest tile (most causal steps). group == 0: head by head, longest tile of each head first.
+// group > 0: the linear grid walks groups of `group` heads and, inside a group, all its heads'
+// longest tiles first — the grid's tail then holds only short tiles, while the ~148 CTAs in
+// flight still span few enough heads for their K / V (1 MB per head at S 2048) to stay in L2.
+__device__ __forceinline__ void tile_order(int group, int& rank, int& bh) {
+  const int nt = (int)gridDim.x, nbh = (int)gridDim.y;
+  if (group <= 0) {
+    rank = (int)blockIdx.x;
+    bh = (int)blockIdx.y;
+    return;
+  }
+  const int lin = (int)blockIdx.x + nt * (int)blockIdx.y;
+  const int g = lin / (nt * group), r = lin - g * nt * group;
+  const int heads = min(group, nbh - g * group);
+  rank = r / heads;
+  bh = g * group + r % heads;
+}
+
 template <int kEmu>
 __global__ void __launch_bounds__(PP_THREADS, 1)
     flash_fwd_pp2(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k64,
                   const __grid_constant__ CUtensorMap map_v64, __nv_bfloat16* __restrict__ o, float* __restrict__ lse,
-                  int S, int H, int ld, float scale_log2) {
+                  int S, int H, int ld, float scale_log2, int order) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   auto sQ = [&](int t) { return smem + t * TILE_BYTES; };
@@ -639,9 +658,11 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
   PP2Bars* bars = reinterpret_cast<PP2Bars*>(smem + 2 * TILE_BYTES + KF_STAGES * 2 * HALF_TILE);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int pair = (int)(gridDim.x - 1 - blockIdx.x);   // long (late) query tiles first
+  int rank, bh;
+  tile_order(order, rank, bh);
+  const int pair = (int)gridDim.x - 1 - rank;           // long (late) query tiles first
   const int nb = 4 * pair + 4;                          // 64-key steps of query tile B (A: two fewer)
-  const int bh = blockIdx.y, b = bh / H, hh = bh % H;
+  const int b = bh / H, hh = bh % H;
   const int row0 = b * S;
   const int col0 = hh * HD;
 
@@ -1354,7 +1375,8 @@ __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
     flash_bwd_dkv_tc2(const __grid_constant__ CUtensorMap map_q64, const __grid_constant__ CUtensorMap map_k,
                       const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do64,
                       const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dk,
-                      __nv_bfloat16* __restrict__ dv, int S, int H, int ld, float scale, float scale_log2) {
+                      __nv_bfloat16* __restrict__ dv, int S, int H, int ld, float scale, float scale_log2,
+                      int order) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sK = smem, *sV = smem + TILE_BYTES;
@@ -1363,9 +1385,10 @@ __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
   float* sLD = reinterpret_cast<float*>(smem + 2 * TILE_BYTES + KV2_STAGES * 2 * HALF_TILE);   // [stage][lse|D]
   BwdKV2Bars* bars = reinterpret_cast<BwdKV2Bars*>(reinterpret_cast<uint8_t*>(sLD) + KV2_STAGES * KV2_LD_BYTES);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int kt = (int)blockIdx.x;        // key tile (early tiles have the longest loops: launched first)
+  int kt, bh;
+  tile_order(order, kt, bh);             // key tile (early tiles have the longest loops: launched first)
   const int i0 = 2 * kt, n = S / 64 - i0;   // query steps i0 .. S/64 - 1
-  const int bh = blockIdx.y, b = bh / H, hh = bh % H;
+  const int b = bh / H, hh = bh % H;
   const int row0 = b * S, col0 = hh * HD;
   if (threadIdx.x == 0) {
     tma_prefetch(&map_q64);
@@ -1546,15 +1569,17 @@ __global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
     flash_bwd_dq_tc2(const __nv_bfloat16* __restrict__ q, const __grid_constant__ CUtensorMap map_k64,
                      const __grid_constant__ CUtensorMap map_v64, const __nv_bfloat16* __restrict__ d_o,
                      const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dq,
-                     int S, int H, int ld, float scale, float scale_log2) {
+                     int S, int H, int ld, float scale, float scale_log2, int order) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   auto sK = [&](int st) { return smem + st * 2 * HALF_TILE; };
   auto sV = [&](int st) { return smem + st * 2 * HALF_TILE + HALF_TILE; };
   BwdQ2Bars* bars = reinterpret_cast<BwdQ2Bars*>(smem + Q2_STAGES * 2 * HALF_TILE);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int qt = (int)(gridDim.x - 1 - blockIdx.x);
-  const int bh = blockIdx.y, b = bh / H, hh = bh % H;
+  int rank, bh;
+  tile_order(order, rank, bh);
+  const int qt = (int)gridDim.x - 1 - rank;
+  const int b = bh / H, hh = bh % H;
   const int row0 = b * S, col0 = hh * HD;
   const int n = 2 * qt + 2;                        // 64-key steps 0 .. 2 qt + 1
   if (threadIdx.x == 0) {
@@ -1700,6 +1725,22 @@ bool make_map_2d(CUtensorMap* map, const void* ptr, long long rows, int ld, int 
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Heads per launch-order group (tile_order). Forward: 16 (0.272 vs 0.279 ms head by head at
+// C2); backward: head by head (dK/dV and dQ re-read K / V / Q / dO more and lose more L2
+// locality than the tail costs: 0.964 vs 0.973 ms at 16). HLM_ATTN_TILE_GROUP /
+// HLM_ATTN_BWD_TILE_GROUP override.
+int tile_group(bool bwd) {
+  static const int g[2] = {[] {
+                             const char* e = std::getenv("HLM_ATTN_TILE_GROUP");
+                             return e ? std::atoi(e) : 16;
+                           }(),
+                           [] {
+                             const char* e = std::getenv("HLM_ATTN_BWD_TILE_GROUP");
+                             return e ? std::atoi(e) : 0;
+                           }()};
+  return g[bwd ? 1 : 0];
+}
+
 }  // namespace
 
 bool hlm_flash_tc_supported(int head_dim, int seq, int ld) {
@@ -1736,7 +1777,7 @@ int hlm_flash_fwd_tc(const void* q, const void* k, const void* v, void* o, float
       }
       dim3 grid(S / (2 * TQ), B * H);
       kern2<<<grid, PP_THREADS, PP2_SMEM, s>>>(mq, mk64, mv64, (__nv_bfloat16*)o, lse, S, H, ld,
-                                               (1.0f / sqrtf((float)HD)) * kLog2e);
+                                               (1.0f / sqrtf((float)HD)) * kLog2e, tile_group(false));
       hlm_count_launches(1);
       return cudaGetLastError() == cudaSuccess ? 0 : 1;
     }
@@ -1797,10 +1838,11 @@ int hlm_flash_bwd_tc(const void* q, const void* k, const void* v, const void* d_
     }();
     auto kv_kern = xp == 1 ? flash_bwd_dkv_tc2<1> : xp == 2 ? flash_bwd_dkv_tc2<2> : flash_bwd_dkv_tc2<0>;
     kv_kern<<<grid, BWD_KV2_THREADS, BWD_KV2_SMEM, s>>>(
-        mq64, mk, mv, mdo64, lse, dsum, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, S, H, ld, scale, scale * kLog2e);
+        mq64, mk, mv, mdo64, lse, dsum, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, S, H, ld, scale, scale * kLog2e,
+        tile_group(true));
     flash_bwd_dq_tc2<<<grid, BWD_Q2_THREADS, BWD_Q2_SMEM, s>>>(
         (const __nv_bfloat16*)q, mk64, mv64, (const __nv_bfloat16*)d_o, lse, dsum, (__nv_bfloat16*)dq, S, H, ld, scale,
-        scale * kLog2e);
+        scale * kLog2e, tile_group(true));
     hlm_count_launches(2);
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
   }
