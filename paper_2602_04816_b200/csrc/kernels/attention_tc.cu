@@ -24,6 +24,9 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <type_traits>
 
 #include "attention.h"
@@ -631,18 +634,19 @@ constexpr int PP2_SMEM = TILE_BYTES * 2 + KF_STAGES * 2 * HALF_TILE + 1024 + 256
 // group > 0: the linear grid walks groups of `group` heads and, inside a group, all its heads'
 // longest tiles first — the grid's tail then holds only short tiles, while the ~148 CTAs in
 // flight still span few enough heads for their K / V (1 MB per head at S 2048) to stay in L2.
-__device__ __forceinline__ void tile_order(int group, int& rank, int& bh) {
-  const int nt = (int)gridDim.x, nbh = (int)gridDim.y;
+__device__ __forceinline__ void tile_decode(int lin, int nt, int nbh, int group, int& rank, int& bh) {
   if (group <= 0) {
-    rank = (int)blockIdx.x;
-    bh = (int)blockIdx.y;
+    rank = lin % nt;
+    bh = lin / nt;
     return;
   }
-  const int lin = (int)blockIdx.x + nt * (int)blockIdx.y;
   const int g = lin / (nt * group), r = lin - g * nt * group;
   const int heads = min(group, nbh - g * group);
   rank = r / heads;
   bh = g * group + r % heads;
+}
+__device__ __forceinline__ void tile_order(int group, int& rank, int& bh) {
+  tile_decode((int)blockIdx.x + (int)gridDim.x * (int)blockIdx.y, (int)gridDim.x, (int)gridDim.y, group, rank, bh);
 }
 
 template <int kEmu>
@@ -1300,6 +1304,28 @@ __device__ __forceinline__ void store_row16_narrow(uint8_t* tile, int r, int c16
   }
 }
 
+#ifdef HLM_ATTN_TIMELINE   // tools/attn_timeline.cu only: per-CTA global-timer stamps
+__device__ unsigned long long* g_attn_tl;
+__device__ __forceinline__ void tl_put_at(int rec, int slot, unsigned long long v) { g_attn_tl[rec * 8 + slot] = v; }
+__device__ __forceinline__ void tl_put(int slot, unsigned long long v) {
+  tl_put_at((int)(blockIdx.x + gridDim.x * blockIdx.y), slot, v);
+}
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define HLM_TL(slot) tl_put(slot, tl_now())
+#define HLM_TL_VAL(slot, v) tl_put(slot, (unsigned long long)(v))
+#define HLM_TL_AT(rec, slot) tl_put_at(rec, slot, tl_now())
+#define HLM_TL_AT_VAL(rec, slot, v) tl_put_at(rec, slot, (unsigned long long)(v))
+#else
+#define HLM_TL_AT(rec, slot) ((void)0)
+#define HLM_TL_AT_VAL(rec, slot, v) ((void)0)
+#define HLM_TL(slot) ((void)0)
+#define HLM_TL_VAL(slot, v) ((void)0)
+#endif
+
 // P, dS of 16 (row, column) scores held by one thread, the reference backward's
 // dS = P (dP - D) (kernels.hpp:269-299), P from the forward's log-sum-exp.
 //   nl[e] = -lse * log2(e) of column e; dn[e] = D of column e (row sums for dQ, column
@@ -1391,6 +1417,14 @@ __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
   const int b = bh / H, hh = bh % H;
   const int row0 = b * S, col0 = hh * HD;
   if (threadIdx.x == 0) {
+    HLM_TL(0);
+    {
+      unsigned smid_v;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_v));
+      (void)smid_v;
+      HLM_TL_VAL(6, smid_v);
+      HLM_TL_VAL(7, n);
+    }
     tma_prefetch(&map_q64);
     tma_prefetch(&map_k);
     tma_prefetch(&map_v);
@@ -1440,6 +1474,7 @@ __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
     constexpr uint32_t idesc_acc = make_idesc_bf16(128, 128, false, true);  // dV, dK: B MN-major
     const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV);
     mbar_wait(&bars->kv_full, 0);
+    if (lane == 0) HLM_TL(1);
     auto issue_sdp = [&](int it) {
       const int st = it % KV2_STAGES, bb = it & 1;
       mbar_wait(&bars->q_full[st], (it / KV2_STAGES) & 1);
@@ -1481,6 +1516,7 @@ __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
       const int bb = it & 1, st = it % KV2_STAGES;
       const int q0 = (i0 + it) * 64 + cq * 16;     // first query column of this thread's 16
       mbar_wait(&bars->s_full[bb], (it >> 1) & 1);
+      if (it == 0 && warp == 4 && lane == 0) HLM_TL(2);
       tc_fence_after();
       uint32_t sv[16], dpv[16];
       if (kExp < 2) {
@@ -1522,11 +1558,298 @@ __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->p_full[bb]);
+      if (it == n - 1 && warp == 4 && lane == 0) HLM_TL(3);
     }
     mbar_wait(&bars->acc_full, 0);
+    if (warp == 4 && lane == 0) HLM_TL(4);
     tc_fence_after();
     store_acc_32(dv + (long long)(row0 + key) * ld + col0 + cq * 32, tmem + 256 + cq * 32 + lane_off, 1.0f);
     store_acc_32(dk + (long long)(row0 + key) * ld + col0 + cq * 32, tmem + 384 + cq * 32 + lane_off, scale);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+  if (threadIdx.x == 0) HLM_TL(5);
+}
+
+// One 128 x 128 fp32 accumulator (TMEM) -> bf16 rows of a global tile, through a 32 KB
+// shared-memory stage so the global stores are row-contiguous (each warp instruction writes two
+// full 256-byte rows; storing straight from the TMEM layout, thread = row, made every warp
+// instruction touch 32 rows: 4.45 us per tile for dK + dV at C2). Called by all 16 elementwise
+// warps (named barrier 1): thread (quarter, cq, lane) owns row 32 quarter + lane, columns
+// 32 cq .. +32 at `taddr`; `et` = 0..511 is its index among the 512 threads. The stage is
+// XOR-swizzled by row (16-byte chunk c of row r at c ^ (r & 7)): conflict-free both ways.
+__device__ __forceinline__ void store_acc_staged(__nv_bfloat16* tile, int ld, uint32_t taddr, float scale,
+                                                 uint32_t stage, int r, int cq, int et) {
+  uint32_t v[32];
+  tmem_ld_32x32(taddr, v);
+  tmem_ld_wait();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int c = cq * 4 + q;
+    st_shared_v4(stage + r * 256 + ((c ^ (r & 7)) << 4),
+                 pack_bf16x2(__uint_as_float(v[8 * q]) * scale, __uint_as_float(v[8 * q + 1]) * scale),
+                 pack_bf16x2(__uint_as_float(v[8 * q + 2]) * scale, __uint_as_float(v[8 * q + 3]) * scale),
+                 pack_bf16x2(__uint_as_float(v[8 * q + 4]) * scale, __uint_as_float(v[8 * q + 5]) * scale),
+                 pack_bf16x2(__uint_as_float(v[8 * q + 6]) * scale, __uint_as_float(v[8 * q + 7]) * scale));
+  }
+  asm volatile("bar.sync 1, 512;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int idx = i * 512 + et, row = idx >> 4, c = idx & 15;
+    uint4 w;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                 : "r"(stage + row * 256 + ((c ^ (row & 7)) << 4)));
+    *reinterpret_cast<uint4*>(tile + (long long)row * ld + c * 8) = w;
+  }
+  asm volatile("bar.sync 1, 512;" ::: "memory");   // the stage is free again
+}
+
+// Persistent dK / dV: one CTA per SM walks the 128-key tiles (fetched from a global counter,
+// so the causal lengths balance dynamically) with the TMEM allocation, barriers and the Q|dO
+// ring kept across tiles. Per tile the work is flash_bwd_dkv_tc2's; what changes is the tile
+// boundary (tools/attn_timeline.cu measured ~7.8 us per CTA of prologue, epilogue and
+// CTA-to-CTA gap at C2 on a 0.8 us step, a third of the kernel):
+//   * the next tile's K / V load as soon as the MMA warp has issued this tile's last S / dP
+//     (kv_empty), i.e. under its last two dV / dK steps;
+//   * the next tile's first S / dP run on the tensor core while the elementwise warps store
+//     this tile's dK / dV (their P / dS hand-off for the next tile doubles as the signal that
+//     the accumulators are free);
+//   * no CTA launch / teardown between tiles.
+// Tile ids go through a 2-slot ring in shared memory written by warp 3 (the fetcher) and read
+// by the producer, the MMA warp and the 16 elementwise warps (tile_empty counts 18 readers).
+struct BwdKV3Bars {
+  uint64_t kv_full, kv_empty, q_full[KV2_STAGES], q_empty[KV2_STAGES], s_full[2], p_full[2], acc_full;
+  uint64_t tile_full[2], tile_empty[2];
+  int tile_id[2];
+  uint32_t tmem;
+};
+constexpr int KV3_TILE_READERS = 18;
+static_assert(sizeof(BwdKV3Bars) <= 256, "barrier block");
+constexpr int BWD_KV3_SMEM = TILE_BYTES * 2 + KV2_STAGES * 2 * HALF_TILE + TILE_BYTES + KV2_STAGES * KV2_LD_BYTES + 256;
+static_assert(BWD_KV3_SMEM <= 227 * 1024, "shared memory");
+
+__global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
+    flash_bwd_dkv_tc3(const __grid_constant__ CUtensorMap map_q64, const __grid_constant__ CUtensorMap map_k,
+                      const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do64,
+                      const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dk,
+                      __nv_bfloat16* __restrict__ dv, int S, int H, int ld, float scale, float scale_log2,
+                      int order, int nbh, int* __restrict__ tile_ctr) {
+  // no alignment slack in BWD_KV3_SMEM (the 32 KB store stage needs it): the dynamic
+  // shared-memory window starts 1024-aligned (no static shared memory here); checked
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if (smem_u32(smem) & 1023) __trap();
+  uint8_t *sK = smem, *sV = smem + TILE_BYTES;
+  auto sQ = [&](int st) { return smem + 2 * TILE_BYTES + st * 2 * HALF_TILE; };
+  auto sdO = [&](int st) { return smem + 2 * TILE_BYTES + st * 2 * HALF_TILE + HALF_TILE; };
+  const uint32_t s_out = smem_u32(smem + 2 * TILE_BYTES + KV2_STAGES * 2 * HALF_TILE);   // 32 KB store stage
+  float* sLD = reinterpret_cast<float*>(smem + 2 * TILE_BYTES + KV2_STAGES * 2 * HALF_TILE + TILE_BYTES);
+  BwdKV3Bars* bars = reinterpret_cast<BwdKV3Bars*>(reinterpret_cast<uint8_t*>(sLD) + KV2_STAGES * KV2_LD_BYTES);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int nt = S / TK, total = nt * nbh;
+  if (threadIdx.x == 0) {
+    tma_prefetch(&map_q64);
+    tma_prefetch(&map_k);
+    tma_prefetch(&map_v);
+    tma_prefetch(&map_do64);
+    mbar_init(&bars->kv_full, 1);
+    mbar_init(&bars->kv_empty, 1);
+    for (int i = 0; i < KV2_STAGES; ++i) {
+      mbar_init(&bars->q_full[i], 1);
+      mbar_init(&bars->q_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars->s_full[i], 1);
+      mbar_init(&bars->p_full[i], 16);
+      mbar_init(&bars->tile_full[i], 1);
+      mbar_init(&bars->tile_empty[i], KV3_TILE_READERS);
+    }
+    mbar_init(&bars->acc_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(&bars->tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem;
+  // j-th tile of this CTA (-1: none left); the caller's lane 0 releases the slot
+  auto next_tile = [&](int j) {
+    const int slot = j & 1;
+    mbar_wait(&bars->tile_full[slot], (j >> 1) & 1);
+    const int id = *reinterpret_cast<volatile int*>(&bars->tile_id[slot]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bars->tile_empty[slot]);
+    return id;
+  };
+
+  if (warp == 3) {
+    if (lane == 0) {
+      for (int j = 0;; ++j) {
+        const int slot = j & 1;
+        mbar_wait(&bars->tile_empty[slot], ((j >> 1) & 1) ^ 1);
+        const int t = atomicAdd(tile_ctr, 1);
+        bars->tile_id[slot] = t < total ? t : -1;
+        mbar_arrive(&bars->tile_full[slot]);
+        if (t >= total) break;
+      }
+    }
+  } else if (warp == 0) {
+    int g = 0;
+    for (int j = 0;; ++j) {
+      const int id = next_tile(j);
+      if (id < 0) break;
+      int kt, bh;
+      tile_decode(id, nt, nbh, order, kt, bh);
+      const int i0 = 2 * kt, n = S / 64 - i0;
+      const int b = bh / H, hh = bh % H, row0 = b * S, col0 = hh * HD;
+      if (lane == 0) {
+        if (j > 0) mbar_wait(&bars->kv_empty, (j - 1) & 1);   // the last tile's S / dP are done with K / V
+        mbar_arrive_expect_tx(&bars->kv_full, 2 * TILE_BYTES);
+        tma_load_2d(sK, &map_k, &bars->kv_full, col0, row0 + kt * TK);
+        tma_load_2d(sK + ATOM_BYTES, &map_k, &bars->kv_full, col0 + 64, row0 + kt * TK);
+        tma_load_2d(sV, &map_v, &bars->kv_full, col0, row0 + kt * TK);
+        tma_load_2d(sV + ATOM_BYTES, &map_v, &bars->kv_full, col0 + 64, row0 + kt * TK);
+        const float* L = lse + (long long)bh * S;
+        const float* Dr = dsum + (long long)bh * S;
+        for (int it = 0; it < n; ++it) {
+          const int gg = g + it, st = gg % KV2_STAGES, ph = (gg / KV2_STAGES) & 1;
+          const int q0 = (i0 + it) * 64;
+          mbar_wait(&bars->q_empty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&bars->q_full[st], 2 * HALF_TILE + KV2_LD_BYTES);
+          tma_load_2d(sQ(st), &map_q64, &bars->q_full[st], col0, row0 + q0);
+          tma_load_2d(sQ(st) + HALF_ATOM, &map_q64, &bars->q_full[st], col0 + 64, row0 + q0);
+          tma_load_2d(sdO(st), &map_do64, &bars->q_full[st], col0, row0 + q0);
+          tma_load_2d(sdO(st) + HALF_ATOM, &map_do64, &bars->q_full[st], col0 + 64, row0 + q0);
+          bulk_load(sLD + st * 128, L + q0, 256, &bars->q_full[st]);
+          bulk_load(sLD + st * 128 + 64, Dr + q0, 256, &bars->q_full[st]);
+        }
+      }
+      __syncwarp();
+      g += n;
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_s = make_idesc_bf16(128, 64, false, false);    // S^T, dP^T: N = 64 queries
+    constexpr uint32_t idesc_acc = make_idesc_bf16(128, 128, false, true);  // dV, dK: B MN-major
+    const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV);
+    int g0 = 0;
+    for (int j = 0;; ++j) {
+      const int id = next_tile(j);
+      if (id < 0) break;
+      int kt, bh;
+      tile_decode(id, nt, nbh, order, kt, bh);
+      const int n = S / 64 - 2 * kt;
+      mbar_wait(&bars->kv_full, j & 1);
+      tc_fence_after();
+      auto issue_sdp = [&](int it) {
+        const int gg = g0 + it, st = gg % KV2_STAGES, bb = gg & 1;
+        mbar_wait(&bars->q_full[st], (gg / KV2_STAGES) & 1);
+        tc_fence_after();
+        const uint32_t q_base = smem_u32(sQ(st)), do_base = smem_u32(sdO(st));
+        umma_chain_w<8, ATOM_BYTES / 16, 2, HALF_ATOM / 16, 2>(tmem + bb * 64, kmajor_desc(k_base, 0),
+                                                              kmajor_desc64(q_base, 0), idesc_s, 0u);
+        umma_chain_w<8, ATOM_BYTES / 16, 2, HALF_ATOM / 16, 2>(tmem + 128 + bb * 64, kmajor_desc(v_base, 0),
+                                                              kmajor_desc64(do_base, 0), idesc_s, 0u);
+        umma_commit_w(&bars->s_full[bb]);
+        if (it == n - 1) umma_commit_w(&bars->kv_empty);   // K / V free for the next tile
+      };
+      issue_sdp(0);
+      issue_sdp(1);   // n >= 2
+      for (int it = 0; it < n; ++it) {
+        const int gg = g0 + it, st = gg % KV2_STAGES, bb = gg & 1;
+        mbar_wait(&bars->p_full[bb], (gg >> 1) & 1);
+        tc_fence_after();
+        const uint32_t q_base = smem_u32(sQ(st)), do_base = smem_u32(sdO(st));
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_bf16_ts_w(tmem + 256, tmem + bb * 64 + 16 * kk, mnmajor_desc64(do_base, kk), idesc_acc,
+                         (it > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_bf16_ts_w(tmem + 384, tmem + 128 + bb * 64 + 16 * kk, mnmajor_desc64(q_base, kk), idesc_acc,
+                         (it > 0 || kk > 0) ? 1u : 0u);
+        umma_commit_w(&bars->q_empty[st]);
+        if (it + 2 < n) issue_sdp(it + 2);
+      }
+      umma_commit_w(&bars->acc_full);
+      g0 += n;
+    }
+  } else if (warp >= 4) {
+    // warp w: key rows 32*(w%4).. (its TMEM lanes), query columns [16*cq, +16) of each step
+    const int cq = (warp - 4) >> 2, quarter = warp & 3;
+    const int r = quarter * 32 + lane;             // key row within the tile
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const uint32_t ld_base = smem_u32(sLD) + cq * 64;   // this warp's 16 columns of lse / D
+    int g0 = 0;
+    for (int j = 0;; ++j) {
+      const int id = next_tile(j);
+      if (id < 0) break;
+      int kt, bh;
+      tile_decode(id, nt, nbh, order, kt, bh);
+      const int i0 = 2 * kt, n = S / 64 - i0;
+      const int b = bh / H, hh = bh % H, row0 = b * S, col0 = hh * HD;
+      const int key = kt * TK + r;
+      const bool stamp = warp == 4 && lane == 0;
+      if (stamp) {
+        HLM_TL_AT(id, 0);
+        unsigned smid_v;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_v));
+        (void)smid_v;
+        HLM_TL_AT_VAL(id, 6, smid_v);
+        HLM_TL_AT_VAL(id, 7, n);
+      }
+      for (int it = 0; it < n; ++it) {
+        const int gg = g0 + it, bb = gg & 1, st = gg % KV2_STAGES;
+        const int q0 = (i0 + it) * 64 + cq * 16;     // first query column of this thread's 16
+        mbar_wait(&bars->s_full[bb], (gg >> 1) & 1);
+        if (stamp && it == 0) HLM_TL_AT(id, 1);
+        tc_fence_after();
+        uint32_t sv[16], dpv[16];
+        tmem_ld_32x16(tmem + bb * 64 + cq * 16 + lane_off, sv);
+        tmem_ld_32x16(tmem + 128 + bb * 64 + cq * 16 + lane_off, dpv);
+        mbar_wait(&bars->q_full[st], (gg / KV2_STAGES) & 1);   // lse / D landed with this step's Q
+        float nl[16], dn[16];
+#pragma unroll
+        for (int e4 = 0; e4 < 4; ++e4) {
+          const float4 lv = ld_shared_f4(ld_base + st * KV2_LD_BYTES + e4 * 16);
+          const float4 dv4 = ld_shared_f4(ld_base + st * KV2_LD_BYTES + 256 + e4 * 16);
+          nl[4 * e4] = -lv.x * kLog2e;
+          nl[4 * e4 + 1] = -lv.y * kLog2e;
+          nl[4 * e4 + 2] = -lv.z * kLog2e;
+          nl[4 * e4 + 3] = -lv.w * kLog2e;
+          dn[4 * e4] = dv4.x;
+          dn[4 * e4 + 1] = dv4.y;
+          dn[4 * e4 + 2] = dv4.z;
+          dn[4 * e4 + 3] = dv4.w;
+        }
+        tmem_ld_wait();
+        uint32_t pk[8], dk8[8];
+        // causal: P = 0 where key > query, i.e. column e < key - q0
+        if (q0 < kt * TK + TK)   // warp-uniform: only the two diagonal steps mask
+          p_ds_16<true>(sv, dpv, nl, dn, scale_log2, key - q0, true, pk, dk8);
+        else
+          p_ds_16<false>(sv, dpv, nl, dn, scale_log2, 0, true, pk, dk8);
+        tmem_st_32x8(tmem + bb * 64 + cq * 16 + lane_off, pk);
+        tmem_st_32x8(tmem + 128 + bb * 64 + cq * 16 + lane_off, dk8);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->p_full[bb]);
+        if (stamp && it == n - 1) HLM_TL_AT(id, 2);
+      }
+      mbar_wait(&bars->acc_full, j & 1);
+      if (stamp) HLM_TL_AT(id, 3);
+      tc_fence_after();
+      const int et = (warp - 4) * 32 + lane;
+      const long long tile_off = (long long)(row0 + kt * TK) * ld + col0;
+      store_acc_staged(dv + tile_off, ld, tmem + 256 + cq * 32 + lane_off, 1.0f, s_out, r, cq, et);
+      store_acc_staged(dk + tile_off, ld, tmem + 384 + cq * 32 + lane_off, scale, s_out, r, cq, et);
+      if (stamp) HLM_TL_AT(id, 4);
+      // the tcgen05.ld above completed (store_acc_32 waits); the next tile's first P / dS
+      // arrive (after tc_fence_before) is what lets the MMA warp overwrite dV / dK
+      g0 += n;
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -1725,6 +2048,31 @@ bool make_map_2d(CUtensorMap* map, const void* ptr, long long rows, int ld, int 
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Work counters of the persistent kernels: a ring of 1024 per device, one slot per launch
+// (zeroed on the launch's stream first), so launches in flight on different streams never
+// share a counter. Allocated on first use; the SM count comes with it.
+bool tile_counter(int** ctr, int* nsm) {
+  constexpr int kSlots = 1024, kDevs = 64;
+  static int* ring[kDevs] = {};
+  static int sms[kDevs] = {};
+  static std::atomic<unsigned> next{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= kDevs) return false;
+  if (!ring[dev]) {
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!ring[dev]) {
+      int* p = nullptr;
+      if (cudaMalloc(&p, kSlots * sizeof(int)) != cudaSuccess) return false;
+      if (cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return false;
+      ring[dev] = p;
+    }
+  }
+  *ctr = ring[dev] + next.fetch_add(1, std::memory_order_relaxed) % kSlots;
+  *nsm = sms[dev];
+  return true;
+}
+
 // Heads per launch-order group (tile_order). Forward: 16 (0.272 vs 0.279 ms head by head at
 // C2); backward: head by head (dK/dV and dQ re-read K / V / Q / dO more and lose more L2
 // locality than the tail costs: 0.964 vs 0.973 ms at 16). HLM_ATTN_TILE_GROUP /
@@ -1836,10 +2184,30 @@ int hlm_flash_bwd_tc(const void* q, const void* k, const void* v, const void* d_
       const char* e = std::getenv("HLM_ATTN_BWD_EXPERIMENT");
       return e ? std::atoi(e) : 0;
     }();
+    static const bool persist = [] {
+      const char* e = std::getenv("HLM_ATTN_BWD_PERSIST");
+      return e ? std::atoi(e) != 0 : true;
+    }();
+    if (persist && xp == 0) {
+      int* ctr = nullptr;
+      int nsm = 0;
+      if (!tile_counter(&ctr, &nsm)) return 1;
+      static bool attr3 = false;
+      if (!attr3) {
+        cudaFuncSetAttribute(flash_bwd_dkv_tc3, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_KV3_SMEM);
+        attr3 = true;
+      }
+      if (cudaMemsetAsync(ctr, 0, sizeof(int), s) != cudaSuccess) return 1;
+      const int tiles = (S / TK) * B * H;
+      flash_bwd_dkv_tc3<<<std::min(nsm, tiles), BWD_KV2_THREADS, BWD_KV3_SMEM, s>>>(
+          mq64, mk, mv, mdo64, lse, dsum, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, S, H, ld, scale, scale * kLog2e,
+          tile_group(true), B * H, ctr);
+    } else {
     auto kv_kern = xp == 1 ? flash_bwd_dkv_tc2<1> : xp == 2 ? flash_bwd_dkv_tc2<2> : flash_bwd_dkv_tc2<0>;
     kv_kern<<<grid, BWD_KV2_THREADS, BWD_KV2_SMEM, s>>>(
         mq64, mk, mv, mdo64, lse, dsum, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, S, H, ld, scale, scale * kLog2e,
         tile_group(true));
+    }
     flash_bwd_dq_tc2<<<grid, BWD_Q2_THREADS, BWD_Q2_SMEM, s>>>(
         (const __nv_bfloat16*)q, mk64, mv64, (const __nv_bfloat16*)d_o, lse, dsum, (__nv_bfloat16*)dq, S, H, ld, scale,
         scale * kLog2e, tile_group(true));

@@ -146,8 +146,8 @@ torch.save({{"o": o.cpu(), "dq": dq.cpu(), "dk": dk.cpu(), "dv": dv.cpu()}}, sys
 
 def test_kernel_variants_agree(tmp_path):
     """Every selectable variant (exp2 on MUFU vs partly on the FMA pipe; 128- vs 64-wide
-    forward / backward steps; one- vs two-query-tile forward) gives the same attention
-    within bf16 noise."""
+    forward / backward steps; one- vs two-query-tile forward; persistent vs one-CTA-per-tile
+    dK/dV) gives the same attention within bf16 noise."""
     import os
     import subprocess
     import sys
@@ -156,7 +156,7 @@ def test_kernel_variants_agree(tmp_path):
     script.write_text(_VARIANT_SCRIPT.format(root=root))
     outs = {}
     for name, env in (("default", {}), ("emu0", {"HLM_ATTN_EXP_EMU": "0"}), ("emu2", {"HLM_ATTN_EXP_EMU": "2"}),
-                      ("bwd_v1", {"HLM_ATTN_BWD_V1": "1"}),
+                      ("bwd_v1", {"HLM_ATTN_BWD_V1": "1"}), ("bwd_grid", {"HLM_ATTN_BWD_PERSIST": "0"}),
                       ("fwd_pp1", {"HLM_ATTN_FWD_PP1": "1"}), ("fwd_v1", {"HLM_ATTN_FWD_V1": "1"})):
         path = tmp_path / f"{name}.pt"
         subprocess.run([sys.executable, str(script), str(path)], check=True, env={**os.environ, **env})
