@@ -1306,7 +1306,7 @@ __device__ __forceinline__ void store_row16_narrow(uint8_t* tile, int r, int c16
 
 #ifdef HLM_ATTN_TIMELINE   // tools/attn_timeline.cu only: per-CTA global-timer stamps
 __device__ unsigned long long* g_attn_tl;
-__device__ __forceinline__ void tl_put_at(int rec, int slot, unsigned long long v) { g_attn_tl[rec * 8 + slot] = v; }
+__device__ __forceinline__ void tl_put_at(int rec, int slot, unsigned long long v) { g_attn_tl[rec * 16 + slot] = v; }
 __device__ __forceinline__ void tl_put(int slot, unsigned long long v) {
   tl_put_at((int)(blockIdx.x + gridDim.x * blockIdx.y), slot, v);
 }
@@ -1617,15 +1617,15 @@ __device__ __forceinline__ void store_acc_staged(__nv_bfloat16* tile, int ld, ui
 //     this tile's dK / dV (their P / dS hand-off for the next tile doubles as the signal that
 //     the accumulators are free);
 //   * no CTA launch / teardown between tiles.
-// Tile ids go through a 2-slot ring in shared memory written by warp 3 (the fetcher) and read
-// by the producer, the MMA warp and the 16 elementwise warps (tile_empty counts 18 readers).
+// Tile ids go through a 2-slot ring in shared memory written by the producer warp (which
+// claims them) and read by the MMA warp and the 16 elementwise warps (tile_empty counts 17).
 struct BwdKV3Bars {
   uint64_t kv_full, kv_empty, q_full[KV2_STAGES], q_empty[KV2_STAGES], s_full[2], p_full[2], acc_full;
   uint64_t tile_full[2], tile_empty[2];
   int tile_id[2];
   uint32_t tmem;
 };
-constexpr int KV3_TILE_READERS = 18;
+constexpr int KV3_TILE_READERS = 17;   // the MMA warp + 16 elementwise warps
 static_assert(sizeof(BwdKV3Bars) <= 256, "barrier block");
 constexpr int BWD_KV3_SMEM = TILE_BYTES * 2 + KV2_STAGES * 2 * HALF_TILE + TILE_BYTES + KV2_STAGES * KV2_LD_BYTES + 256;
 static_assert(BWD_KV3_SMEM <= 227 * 1024, "shared memory");
@@ -1684,22 +1684,27 @@ __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
     return id;
   };
 
-  if (warp == 3) {
+  // the producer claims tile j (global counter) and publishes it to the readers; it claims
+  // the next tile only once this one's loads are issued, so a CTA holds at most the ring's
+  // depth of work in reserve (a whole claimed tile in reserve left long tiles waiting behind
+  // long tiles at the end of the grid)
+  auto claim = [&](int j) {
+    int t = 0;
     if (lane == 0) {
-      for (int j = 0;; ++j) {
-        const int slot = j & 1;
-        mbar_wait(&bars->tile_empty[slot], ((j >> 1) & 1) ^ 1);
-        const int t = atomicAdd(tile_ctr, 1);
-        bars->tile_id[slot] = t < total ? t : -1;
-        mbar_arrive(&bars->tile_full[slot]);
-        if (t >= total) break;
-      }
+      const int slot = j & 1;
+      mbar_wait(&bars->tile_empty[slot], ((j >> 1) & 1) ^ 1);
+      t = atomicAdd(tile_ctr, 1);
+      if (t >= total) t = -1;
+      bars->tile_id[slot] = t;
+      mbar_arrive(&bars->tile_full[slot]);
     }
-  } else if (warp == 0) {
+    return __shfl_sync(0xffffffffu, t, 0);
+  };
+
+  if (warp == 0) {
     int g = 0;
-    for (int j = 0;; ++j) {
-      const int id = next_tile(j);
-      if (id < 0) break;
+    int id = claim(0);
+    for (int j = 0; id >= 0; ++j) {
       int kt, bh;
       tile_decode(id, nt, nbh, order, kt, bh);
       const int i0 = 2 * kt, n = S / 64 - i0;
@@ -1728,6 +1733,7 @@ __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
       }
       __syncwarp();
       g += n;
+      id = claim(j + 1);
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc_s = make_idesc_bf16(128, 64, false, false);    // S^T, dP^T: N = 64 queries
@@ -2025,6 +2031,274 @@ __global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+// Persistent dQ: one CTA per SM walks the 128-query tiles (per-launch counter, as
+// flash_bwd_dkv_tc3), the K|V ring, barriers and TMEM kept across tiles.
+//   smem: K|V ring of Q3_STAGES 64-row stages | the next tile's Q and dO (TMA, 64 KB) | the
+//   32 KB dQ store stage.
+// The producer TMA-loads the next tile's Q / dO as soon as it has claimed the tile (loading
+// them row by row in the elementwise warps took ~4.9 us per tile: every warp load touched 32
+// rows); at the tile boundary the elementwise warps copy them from shared memory into TMEM as
+// soon as this tile's last S / dP have landed, so the tensor core starts the next tile's S / dP
+// while they store dQ (through the store stage, row-contiguous).
+constexpr int Q3_STAGES = 4;
+struct BwdQ3Bars {
+  uint64_t q_ready, kv_full[Q3_STAGES], kv_empty[Q3_STAGES], s_full[2], ds_full[2], acc_full;
+  uint64_t qs_full, qs_empty, tile_full[2], tile_empty[2];
+  int tile_id[2];
+  uint32_t tmem;
+};
+static_assert(sizeof(BwdQ3Bars) <= 256, "barrier block");
+constexpr int BWD_Q3_SMEM = Q3_STAGES * 2 * HALF_TILE + 3 * TILE_BYTES + 256;
+static_assert(BWD_Q3_SMEM <= 227 * 1024, "shared memory");
+
+// 32 bf16 (columns 32 c32 .. +32) of row r of a 128 x 128 tile held as two 128 x 64 SW128
+// K-major atoms at shared address `tile`, into 16 TMEM columns (thread = lane = row)
+__device__ __forceinline__ void smem_row32_to_tmem(uint32_t taddr, uint32_t tile, int r, int c32) {
+  uint32_t w[16];
+  const uint32_t row = tile + (c32 >> 1) * ATOM_BYTES + r * 128;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int chunk = (c32 & 1) * 4 + q;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w[4 * q]), "=r"(w[4 * q + 1]), "=r"(w[4 * q + 2]), "=r"(w[4 * q + 3])
+                 : "r"(row + ((chunk ^ (r & 7)) << 4)));
+  }
+  tmem_st_32x16(taddr, w);
+}
+
+__global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
+    flash_bwd_dq_tc3(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k64,
+                     const __grid_constant__ CUtensorMap map_v64, const __grid_constant__ CUtensorMap map_do,
+                     const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dq,
+                     int S, int H, int ld, float scale, float scale_log2, int order, int nbh,
+                     int* __restrict__ tile_ctr) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;   // 1024-aligned window, no slack in BWD_Q3_SMEM; checked
+  if (smem_u32(smem) & 1023) __trap();
+  auto sK = [&](int st) { return smem + st * 2 * HALF_TILE; };
+  auto sV = [&](int st) { return smem + st * 2 * HALF_TILE + HALF_TILE; };
+  uint8_t* sQ = smem + Q3_STAGES * 2 * HALF_TILE;   // next tile's Q, then dO
+  uint8_t* sdO = sQ + TILE_BYTES;
+  const uint32_t s_out = smem_u32(sQ + 2 * TILE_BYTES);   // 32 KB store stage
+  BwdQ3Bars* bars = reinterpret_cast<BwdQ3Bars*>(sQ + 3 * TILE_BYTES);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int nt = S / TQ, total = nt * nbh;
+  if (threadIdx.x == 0) {
+    tma_prefetch(&map_q);
+    tma_prefetch(&map_do);
+    tma_prefetch(&map_k64);
+    tma_prefetch(&map_v64);
+    mbar_init(&bars->q_ready, 16);
+    for (int i = 0; i < Q3_STAGES; ++i) {
+      mbar_init(&bars->kv_full[i], 1);
+      mbar_init(&bars->kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars->s_full[i], 1);
+      mbar_init(&bars->ds_full[i], 16);
+      mbar_init(&bars->tile_full[i], 1);
+      mbar_init(&bars->tile_empty[i], KV3_TILE_READERS);
+    }
+    mbar_init(&bars->acc_full, 1);
+    mbar_init(&bars->qs_full, 1);
+    mbar_init(&bars->qs_empty, 16);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(&bars->tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem;
+  auto next_tile = [&](int j) {
+    const int slot = j & 1;
+    mbar_wait(&bars->tile_full[slot], (j >> 1) & 1);
+    const int id = *reinterpret_cast<volatile int*>(&bars->tile_id[slot]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bars->tile_empty[slot]);
+    return id;
+  };
+  // tile id -> query tile (long ones first within a head group), (batch, head)
+  auto decode = [&](int id, int& qt, int& bh) {
+    int rank;
+    tile_decode(id, nt, nbh, order, rank, bh);
+    qt = nt - 1 - rank;
+  };
+  // the producer claims tile j, publishes it, and TMA-loads its Q / dO (lane 0)
+  auto claim = [&](int j) {
+    int t = 0;
+    if (lane == 0) {
+      const int slot = j & 1;
+      mbar_wait(&bars->tile_empty[slot], ((j >> 1) & 1) ^ 1);
+      t = atomicAdd(tile_ctr, 1);
+      if (t >= total) t = -1;
+      bars->tile_id[slot] = t;
+      mbar_arrive(&bars->tile_full[slot]);
+      if (t >= 0) {
+        int qt, bh;
+        decode(t, qt, bh);
+        const int r0 = (bh / H) * S + qt * TQ, c0 = (bh % H) * HD;
+        mbar_wait(&bars->qs_empty, (j & 1) ^ 1);   // the previous tile's Q / dO are in TMEM
+        mbar_arrive_expect_tx(&bars->qs_full, 2 * TILE_BYTES);
+        tma_load_2d(sQ, &map_q, &bars->qs_full, c0, r0);
+        tma_load_2d(sQ + ATOM_BYTES, &map_q, &bars->qs_full, c0 + 64, r0);
+        tma_load_2d(sdO, &map_do, &bars->qs_full, c0, r0);
+        tma_load_2d(sdO + ATOM_BYTES, &map_do, &bars->qs_full, c0 + 64, r0);
+      }
+    }
+    return __shfl_sync(0xffffffffu, t, 0);
+  };
+
+  if (warp == 0) {
+    int g = 0;
+    int id = claim(0);
+    for (int j = 0; id >= 0; ++j) {
+      int qt, bh;
+      decode(id, qt, bh);
+      const int n = 2 * qt + 2, row0 = (bh / H) * S, col0 = (bh % H) * HD;
+      if (lane == 0) {
+        for (int jj = 0; jj < n; ++jj) {
+          const int gg = g + jj, st = gg % Q3_STAGES, ph = (gg / Q3_STAGES) & 1;
+          const int r = row0 + jj * 64;
+          mbar_wait(&bars->kv_empty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&bars->kv_full[st], 2 * HALF_TILE);
+          tma_load_2d(sK(st), &map_k64, &bars->kv_full[st], col0, r);
+          tma_load_2d(sK(st) + HALF_ATOM, &map_k64, &bars->kv_full[st], col0 + 64, r);
+          tma_load_2d(sV(st), &map_v64, &bars->kv_full[st], col0, r);
+          tma_load_2d(sV(st) + HALF_ATOM, &map_v64, &bars->kv_full[st], col0 + 64, r);
+        }
+      }
+      __syncwarp();
+      g += n;
+      id = claim(j + 1);
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_s = make_idesc_bf16(128, 64, false, false);
+    constexpr uint32_t idesc_acc = make_idesc_bf16(128, 128, false, true);
+    int g0 = 0;
+    for (int j = 0;; ++j) {
+      const int id = next_tile(j);
+      if (id < 0) break;
+      int qt, bh;
+      decode(id, qt, bh);
+      const int n = 2 * qt + 2;
+      mbar_wait(&bars->q_ready, j & 1);
+      tc_fence_after();
+      auto issue_sdp = [&](int jj) {
+        const int gg = g0 + jj, st = gg % Q3_STAGES, bb = gg & 1;
+        mbar_wait(&bars->kv_full[st], (gg / Q3_STAGES) & 1);
+        tc_fence_after();
+        const uint32_t k_base = smem_u32(sK(st)), v_base = smem_u32(sV(st));
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          umma_bf16_ts_w(tmem + bb * 64, tmem + 384 + kk * 8, kmajor_desc64(k_base, kk), idesc_s, kk ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          umma_bf16_ts_w(tmem + 128 + bb * 64, tmem + 448 + kk * 8, kmajor_desc64(v_base, kk), idesc_s,
+                         kk ? 1u : 0u);
+        umma_commit_w(&bars->s_full[bb]);
+      };
+      issue_sdp(0);
+      issue_sdp(1);
+      for (int jj = 0; jj < n; ++jj) {
+        const int gg = g0 + jj, st = gg % Q3_STAGES, bb = gg & 1;
+        mbar_wait(&bars->ds_full[bb], (gg >> 1) & 1);
+        tc_fence_after();
+        const uint32_t k_base = smem_u32(sK(st));
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_bf16_ts_w(tmem + 256, tmem + 128 + bb * 64 + 16 * kk, mnmajor_desc64(k_base, kk), idesc_acc,
+                         (jj > 0 || kk > 0) ? 1u : 0u);
+        umma_commit_w(&bars->kv_empty[st]);
+        if (jj + 2 < n) issue_sdp(jj + 2);
+      }
+      umma_commit_w(&bars->acc_full);
+      g0 += n;
+    }
+  } else if (warp >= 4) {
+    // warp w: query rows 32*(w%4).. (its TMEM lanes), key columns [16*ck, +16) of each step
+    const int ck = (warp - 4) >> 2, quarter = warp & 3;
+    const int r = quarter * 32 + lane;             // query row within the tile
+    const int et = (warp - 4) * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    // tile j's Q / dO rows (hd columns [32 ck, +32)) from shared memory into TMEM; q_ready
+    auto load_q = [&](int j) {
+      mbar_wait(&bars->qs_full, j & 1);
+      smem_row32_to_tmem(tmem + 384 + ck * 16 + lane_off, smem_u32(sQ), r, ck);
+      smem_row32_to_tmem(tmem + 448 + ck * 16 + lane_off, smem_u32(sdO), r, ck);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&bars->q_ready);
+        mbar_arrive(&bars->qs_empty);
+      }
+    };
+    int id = next_tile(0), qt = 0, bh = 0;
+    float nl0 = 0.f, D = 0.f;
+    if (id >= 0) {
+      decode(id, qt, bh);
+      load_q(0);
+      nl0 = -lse[(long long)bh * S + qt * TQ + r] * kLog2e;
+      D = dsum[(long long)bh * S + qt * TQ + r];
+    }
+    int g0 = 0;
+    for (int j = 0; id >= 0; ++j) {
+      const int n = 2 * qt + 2, row0 = (bh / H) * S, col0 = (bh % H) * HD;
+      const int qpos = qt * TQ + r;
+      float nl[16], dn[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        nl[e] = nl0;
+        dn[e] = D;
+      }
+      for (int jj = 0; jj < n; ++jj) {
+        const int gg = g0 + jj, bb = gg & 1;
+        const int k0 = jj * 64 + ck * 16;             // first key column of this thread's 16
+        mbar_wait(&bars->s_full[bb], (gg >> 1) & 1);
+        tc_fence_after();
+        uint32_t sv[16], dpv[16];
+        tmem_ld_32x16(tmem + bb * 64 + ck * 16 + lane_off, sv);
+        tmem_ld_32x16(tmem + 128 + bb * 64 + ck * 16 + lane_off, dpv);
+        tmem_ld_wait();
+        uint32_t pk[8], ds8[8];
+        // causal: P = 0 where key > query, i.e. column e > qpos - k0
+        if (jj >= 2 * qt)   // warp-uniform: the two diagonal steps
+          p_ds_16<true>(sv, dpv, nl, dn, scale_log2, qpos - k0, false, pk, ds8);
+        else
+          p_ds_16<false>(sv, dpv, nl, dn, scale_log2, 0, false, pk, ds8);
+        tmem_st_32x8(tmem + 128 + bb * 64 + ck * 16 + lane_off, ds8);   // over the dP columns just read
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->ds_full[bb]);
+      }
+      g0 += n;
+      // this tile's S / dP have all landed (s_full of its last step): Q / dO columns are free
+      const int nid = next_tile(j + 1);
+      int nqt = 0, nbh2 = 0;
+      float nnl0 = 0.f, nD = 0.f;
+      if (nid >= 0) {
+        decode(nid, nqt, nbh2);
+        load_q(j + 1);
+        nnl0 = -lse[(long long)nbh2 * S + nqt * TQ + r] * kLog2e;   // latency under the dQ store
+        nD = dsum[(long long)nbh2 * S + nqt * TQ + r];
+      }
+      mbar_wait(&bars->acc_full, j & 1);
+      tc_fence_after();
+      store_acc_staged(dq + (long long)(row0 + qt * TQ) * ld + col0, ld, tmem + 256 + ck * 32 + lane_off, scale,
+                       s_out, r, ck, et);
+      id = nid;
+      qt = nqt;
+      bh = nbh2;
+      nl0 = nnl0;
+      D = nD;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -2208,6 +2482,21 @@ int hlm_flash_bwd_tc(const void* q, const void* k, const void* v, const void* d_
         mq64, mk, mv, mdo64, lse, dsum, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, S, H, ld, scale, scale * kLog2e,
         tile_group(true));
     }
+    if (persist) {
+      int* ctr = nullptr;
+      int nsm = 0;
+      if (!tile_counter(&ctr, &nsm)) return 1;
+      static bool attr_q3 = false;
+      if (!attr_q3) {
+        cudaFuncSetAttribute(flash_bwd_dq_tc3, cudaFuncAttributeMaxDynamicSharedMemorySize, BWD_Q3_SMEM);
+        attr_q3 = true;
+      }
+      if (cudaMemsetAsync(ctr, 0, sizeof(int), s) != cudaSuccess) return 1;
+      const int tiles = (S / TQ) * B * H;
+      flash_bwd_dq_tc3<<<std::min(nsm, tiles), BWD_Q2_THREADS, BWD_Q3_SMEM, s>>>(
+          mq, mk64, mv64, mdo, lse, dsum, (__nv_bfloat16*)dq, S, H, ld, scale, scale * kLog2e, tile_group(true),
+          B * H, ctr);
+    } else
     flash_bwd_dq_tc2<<<grid, BWD_Q2_THREADS, BWD_Q2_SMEM, s>>>(
         (const __nv_bfloat16*)q, mk64, mv64, (const __nv_bfloat16*)d_o, lse, dsum, (__nv_bfloat16*)dq, S, H, ld, scale,
         scale * kLog2e, tile_group(true));

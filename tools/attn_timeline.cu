@@ -35,15 +35,20 @@ int main() {
   cudaMemset(dsum, 0, (size_t)B * H * S * 4);
   const int ctas = (S / TQ) * B * H;
   unsigned long long* tl;
-  cudaMalloc(&tl, (size_t)ctas * 8 * 8);
+  cudaMalloc(&tl, (size_t)2 * ctas * 16 * 8);
   cudaMemcpyToSymbol(g_attn_tl, &tl, sizeof(tl));
   for (int rep = 0; rep < 3; ++rep)
     if (hlm_flash_bwd_tc(q, k, v, dout, lse, dsum, dq, dk, dv, B, S, H, ld, 0) != 0) return 1;
   if (cudaDeviceSynchronize() != cudaSuccess) return 2;
-  std::vector<unsigned long long> h((size_t)ctas * 8);
-  cudaMemcpy(h.data(), tl, h.size() * 8, cudaMemcpyDeviceToHost);
+  std::vector<unsigned long long> h16((size_t)ctas * 16), h((size_t)ctas * 8);
+  cudaMemcpy(h16.data(), tl + (std::getenv("TIMELINE_DQ") ? (size_t)ctas * 16 : 0), h16.size() * 8,
+             cudaMemcpyDeviceToHost);
+  for (int c = 0; c < ctas; ++c)
+    for (int k = 0; k < 8; ++k) h[c * 8 + k] = h16[c * 16 + k];
 
   const bool persist = std::getenv("HLM_ATTN_BWD_PERSIST") == nullptr || std::atoi(std::getenv("HLM_ATTN_BWD_PERSIST"));
+  // flash_bwd_dq_tc3 stamps the records after dK/dV's (TIMELINE_DQ=1 analyses those)
+  const bool dq_kernel = std::getenv("TIMELINE_DQ") != nullptr;
   if (persist) {
     // records per tile: 0 fetched, 1 first S/dP landed, 2 last P/dS handed over, 3 accumulators
     // done, 4 dK/dV stored (elementwise warp 4), 6 SM, 7 steps
@@ -72,11 +77,37 @@ int main() {
         ++nb;
       }
     }
-    std::printf("persistent dK/dV: span %.1f us, %d tiles on %zu SMs\n", (t1 - t0) / 1e3, ctas, per_sm.size());
+    std::printf(dq_kernel ? "persistent dQ: span %.1f us, %d tiles on %zu SMs\n" : "persistent dK/dV: span %.1f us, %d tiles on %zu SMs\n", (t1 - t0) / 1e3, ctas, per_sm.size());
     std::printf("per tile (us): fetched -> first S/dP landed %.2f, steady step %.3f, last P/dS -> accumulators "
                 "%.2f, store dK/dV %.2f; previous tile stored -> next fetched %.2f\n",
                 fetch_to_s / ctas / 1e3, step / nstep / 1e3, tail / ctas / 1e3, epi / ctas / 1e3,
                 between / nb / 1e3);
+    if (dq_kernel) {   // slot 5: the next tile's Q / dO written to TMEM (before the dQ accumulator wait)
+      double nextq = 0, accw = 0;
+      for (int c = 0; c < ctas; ++c) {
+        const unsigned long long* r = &h[c * 8];
+        nextq += double(r[5] - r[2]);
+        accw += double(r[3] - r[5]);
+      }
+      std::printf("dQ boundary (us): last dS -> next tile's Q/dO in TMEM %.2f, then -> dQ accumulator %.2f\n",
+                  nextq / ctas / 1e3, accw / ctas / 1e3);
+      // 8: id seen by the elementwise warps, 9: Q/dO in TMEM, 10: claimed by the producer,
+      // 11: q_ready seen by the MMA warp, 12: first S/dP issued (all of the tile's own record)
+      double claim_to_seen = 0, seen_to_q = 0, q_to_mma = 0, mma_issue = 0;
+      int cnt = 0;
+      for (int c = 0; c < ctas; ++c) {
+        const unsigned long long* r = &h16[c * 16];
+        if (!r[8] || !r[10]) continue;
+        claim_to_seen += double(r[8]) - double(r[10]);
+        seen_to_q += double(r[9]) - double(r[8]);
+        q_to_mma += double(r[11]) - double(r[9]);
+        mma_issue += double(r[12]) - double(r[11]);
+        ++cnt;
+      }
+      std::printf("  claimed -> seen by elementwise %.2f, -> Q/dO in TMEM %.2f, -> q_ready at MMA warp %.2f, "
+                  "-> first S/dP issued %.2f (%d tiles)\n",
+                  claim_to_seen / cnt / 1e3, seen_to_q / cnt / 1e3, q_to_mma / cnt / 1e3, mma_issue / cnt / 1e3, cnt);
+    }
     return 0;
   }
   unsigned long long t0 = ~0ull, t1 = 0;
