@@ -622,6 +622,9 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
 // softmax of a tile no longer waits a PV + S round trip per step, only the tensor pipe.
 // K / V: KF_STAGES-deep ring of 64-row stages, released by tile B's PV (B uses every key).
 // A rare lazy rescale of O_t (row max up by more than 2^8) first waits for PV_t(j-1).
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
 constexpr int KF_STAGES = 4;
 struct PP2Bars {
   uint64_t q_full, kv_full[KF_STAGES], kv_empty[KF_STAGES], s_full[2][2], p_full[2][2], pv_done[2], o_final[2];
@@ -846,21 +849,38 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
     mbar_wait(&bars->pv_done[t], 0);   // its one phase (complete with o_final)
     tc_fence_after();
     const float il = 1.f / l;
-    __nv_bfloat16* orow = o + (long long)(row0 + qpos) * ld + col0;
+    // O through shared memory (this tile's Q buffer: every S_t MMA has completed with o_final)
+    // so the global stores are row-contiguous: a warp store straight from the TMEM layout
+    // (thread = row) touches 32 rows (XOR swizzle by row: conflict-free both ways)
+    const uint32_t stage = smem_u32(sQ(t));
 #pragma unroll 1
     for (int c = 0; c < 4; ++c) {
       uint32_t ov[32];
       tmem_ld_32x32(o_addr + c * 32, ov);
       tmem_ld_wait();
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        reinterpret_cast<uint4*>(orow + c * 32)[q] =
-            make_uint4(pack_bf16x2(__uint_as_float(ov[8 * q]) * il, __uint_as_float(ov[8 * q + 1]) * il),
-                       pack_bf16x2(__uint_as_float(ov[8 * q + 2]) * il, __uint_as_float(ov[8 * q + 3]) * il),
-                       pack_bf16x2(__uint_as_float(ov[8 * q + 4]) * il, __uint_as_float(ov[8 * q + 5]) * il),
-                       pack_bf16x2(__uint_as_float(ov[8 * q + 6]) * il, __uint_as_float(ov[8 * q + 7]) * il));
+      for (int q = 0; q < 4; ++q) {
+        const int ch = c * 4 + q;
+        st_shared_v4(stage + r * 256 + ((ch ^ (r & 7)) << 4),
+                     pack_bf16x2(__uint_as_float(ov[8 * q]) * il, __uint_as_float(ov[8 * q + 1]) * il),
+                     pack_bf16x2(__uint_as_float(ov[8 * q + 2]) * il, __uint_as_float(ov[8 * q + 3]) * il),
+                     pack_bf16x2(__uint_as_float(ov[8 * q + 4]) * il, __uint_as_float(ov[8 * q + 5]) * il),
+                     pack_bf16x2(__uint_as_float(ov[8 * q + 6]) * il, __uint_as_float(ov[8 * q + 7]) * il));
+      }
     }
     lse[(long long)bh * S + qpos] = (m + log2f(l)) / kLog2e;
+    asm volatile("bar.sync %0, 128;" ::"r"(1 + t) : "memory");   // this tile's 4 warps
+    __nv_bfloat16* otile = o + (long long)(row0 + qt * TQ) * ld + col0;
+    const int et = quarter * 32 + lane;
+#pragma unroll 4
+    for (int i = 0; i < 16; ++i) {
+      const int idx = i * 128 + et, row = idx >> 4, ch = idx & 15;
+      uint4 w;
+      asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                   : "r"(stage + row * 256 + ((ch ^ (row & 7)) << 4)));
+      *reinterpret_cast<uint4*>(otile + (long long)row * ld + ch * 8) = w;
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -1375,9 +1395,6 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
                    smem_u32(dst)),
                "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
-}
-__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 __device__ __forceinline__ float4 ld_shared_f4(uint32_t addr) {
   float4 v;
