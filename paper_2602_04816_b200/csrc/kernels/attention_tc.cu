@@ -622,6 +622,28 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
 // softmax of a tile no longer waits a PV + S round trip per step, only the tensor pipe.
 // K / V: KF_STAGES-deep ring of 64-row stages, released by tile B's PV (B uses every key).
 // A rare lazy rescale of O_t (row max up by more than 2^8) first waits for PV_t(j-1).
+#ifdef HLM_ATTN_TIMELINE   // tools/attn_timeline.cu only: per-CTA global-timer stamps
+__device__ unsigned long long* g_attn_tl;
+__device__ __forceinline__ void tl_put_at(int rec, int slot, unsigned long long v) { g_attn_tl[rec * 16 + slot] = v; }
+__device__ __forceinline__ void tl_put(int slot, unsigned long long v) {
+  tl_put_at((int)(blockIdx.x + gridDim.x * blockIdx.y), slot, v);
+}
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define HLM_TL(slot) tl_put(slot, tl_now())
+#define HLM_TL_VAL(slot, v) tl_put(slot, (unsigned long long)(v))
+#define HLM_TL_AT(rec, slot) tl_put_at(rec, slot, tl_now())
+#define HLM_TL_AT_VAL(rec, slot, v) tl_put_at(rec, slot, (unsigned long long)(v))
+#else
+#define HLM_TL_AT(rec, slot) ((void)0)
+#define HLM_TL_AT_VAL(rec, slot, v) ((void)0)
+#define HLM_TL(slot) ((void)0)
+#define HLM_TL_VAL(slot, v) ((void)0)
+#endif
+
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
@@ -674,6 +696,14 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
   const int col0 = hh * HD;
 
   if (threadIdx.x == 0) {
+    HLM_TL(0);
+    {
+      unsigned smid_v;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_v));
+      (void)smid_v;
+      HLM_TL_VAL(6, smid_v);
+      HLM_TL_VAL(7, nb);
+    }
     tma_prefetch(&map_q);
     tma_prefetch(&map_k64);
     tma_prefetch(&map_v64);
@@ -721,6 +751,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
     constexpr uint32_t idesc_o = make_idesc_bf16(128, 128, false, true);
     const int n_t[2] = {nb - 2, nb};
     mbar_wait(&bars->q_full, 0);
+    if (lane == 0) HLM_TL(1);
     auto issue_s = [&](int t, int j) {
       const int st = j % KF_STAGES;
       mbar_wait(&bars->kv_full[st], (j / KF_STAGES) & 1);
@@ -768,6 +799,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
     for (int j = 0; j < n; ++j) {
       const uint32_t s_addr = s_base + (j & 1) * 64;
       mbar_wait(&bars->s_full[t][j & 1], (j >> 1) & 1);
+      if (j == 0 && warp == 6 && lane == 0) HLM_TL(2);
       tc_fence_after();
       uint32_t sv[2][32];
       tmem_ld_32x32(s_addr, sv[0]);
@@ -847,6 +879,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
     }
     mbar_wait(&bars->o_final[t], 0);
     mbar_wait(&bars->pv_done[t], 0);   // its one phase (complete with o_final)
+    if (warp == 6 && lane == 0) HLM_TL(3);
     tc_fence_after();
     const float il = 1.f / l;
     // O through shared memory (this tile's Q buffer: every S_t MMA has completed with o_final)
@@ -881,10 +914,12 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
                    : "r"(stage + row * 256 + ((ch ^ (row & 7)) << 4)));
       *reinterpret_cast<uint4*>(otile + (long long)row * ld + ch * 8) = w;
     }
+    if (warp == 6 && lane == 0) HLM_TL(4);
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<512>(tmem);
+  if (threadIdx.x == 0) HLM_TL(5);
 }
 
 // ------------------------------------------------------------------ backward
@@ -1324,27 +1359,6 @@ __device__ __forceinline__ void store_row16_narrow(uint8_t* tile, int r, int c16
   }
 }
 
-#ifdef HLM_ATTN_TIMELINE   // tools/attn_timeline.cu only: per-CTA global-timer stamps
-__device__ unsigned long long* g_attn_tl;
-__device__ __forceinline__ void tl_put_at(int rec, int slot, unsigned long long v) { g_attn_tl[rec * 16 + slot] = v; }
-__device__ __forceinline__ void tl_put(int slot, unsigned long long v) {
-  tl_put_at((int)(blockIdx.x + gridDim.x * blockIdx.y), slot, v);
-}
-__device__ __forceinline__ unsigned long long tl_now() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#define HLM_TL(slot) tl_put(slot, tl_now())
-#define HLM_TL_VAL(slot, v) tl_put(slot, (unsigned long long)(v))
-#define HLM_TL_AT(rec, slot) tl_put_at(rec, slot, tl_now())
-#define HLM_TL_AT_VAL(rec, slot, v) tl_put_at(rec, slot, (unsigned long long)(v))
-#else
-#define HLM_TL_AT(rec, slot) ((void)0)
-#define HLM_TL_AT_VAL(rec, slot, v) ((void)0)
-#define HLM_TL(slot) ((void)0)
-#define HLM_TL_VAL(slot, v) ((void)0)
-#endif
 
 // P, dS of 16 (row, column) scores held by one thread, the reference backward's
 // dS = P (dP - D) (kernels.hpp:269-299), P from the forward's log-sum-exp.
@@ -2360,7 +2374,12 @@ bool tile_counter(int** ctr, int* nsm) {
     }
   }
   *ctr = ring[dev] + next.fetch_add(1, std::memory_order_relaxed) % kSlots;
-  *nsm = sms[dev];
+  // HLM_ATTN_PERSIST_CTAS caps the persistent grids (tests: many tiles per CTA at small shapes)
+  static const int cap = [] {
+    const char* e = std::getenv("HLM_ATTN_PERSIST_CTAS");
+    return e ? std::atoi(e) : 0;
+  }();
+  *nsm = cap > 0 ? std::min(cap, sms[dev]) : sms[dev];
   return true;
 }
 

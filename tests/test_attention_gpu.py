@@ -164,3 +164,53 @@ def test_kernel_variants_agree(tmp_path):
     for name, o in outs.items():
         for key in ("o", "dq", "dk", "dv"):
             assert rel(o[key], outs["emu0"][key]) < 1e-2, (name, key)
+
+
+_PERSIST_SCRIPT = r"""
+import ctypes, sys, torch
+sys.path.insert(0, {root!r})
+from paper_2602_04816_b200 import _lib as L
+torch.manual_seed(11)
+B, S, H, hd = 2, 512, 3, 128
+h, T = H * hd, B * S
+q, k, v, do = (torch.randn(T, h, device="cuda").bfloat16() for _ in range(4))
+o = torch.empty_like(q); lse = torch.empty(B * H * S, device="cuda")
+dq, dk, dv = (torch.empty_like(q) for _ in range(3)); ds = torch.empty_like(lse)
+d = L.HlmBlockDims(B, S, h, 8, H, 0)
+vp = lambda t: ctypes.c_void_p(t.data_ptr())
+Lb = L.blib()
+for _ in range(2):   # a second launch: the per-launch tile counters start from zero again
+    L.check(Lb.hlm_cuda_attention_fwd(ctypes.byref(d), vp(q), vp(k), vp(v), vp(o), vp(lse), h, None))
+    L.check(Lb.hlm_cuda_attention_bwd(ctypes.byref(d), vp(q), vp(k), vp(v), vp(o), vp(do), vp(lse), vp(ds),
+                                      vp(dq), vp(dk), vp(dv), h, None))
+torch.save({{"q": q.cpu(), "k": k.cpu(), "v": v.cpu(), "do": do.cpu(), "o": o.cpu(), "dq": dq.cpu(),
+             "dk": dk.cpu(), "dv": dv.cpu()}}, sys.argv[1])
+"""
+
+
+@pytest.mark.parametrize("ctas", ["1", "3", "7"])
+def test_persistent_backward_many_tiles_per_cta(tmp_path, ctas):
+    """The persistent dK/dV and dQ kernels with their grids capped (HLM_ATTN_PERSIST_CTAS) so each
+    CTA walks many tiles (24 here; tile boundaries at both barrier parities, K/V and Q/dO handed
+    over between tiles, the store stage reused): bitwise equal to the uncapped launch (a tile's
+    arithmetic does not depend on which CTA runs it) and close to torch fp32."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "p.py"
+    script.write_text(_PERSIST_SCRIPT.format(root=root))
+    outs = {}
+    for name, env in (("full", {}), ("capped", {"HLM_ATTN_PERSIST_CTAS": ctas})):
+        path = tmp_path / f"{name}.pt"
+        subprocess.run([sys.executable, str(script), str(path)], check=True, env={**os.environ, **env})
+        outs[name] = torch.load(path)
+    for key in ("o", "dq", "dk", "dv"):
+        assert torch.equal(outs["full"][key], outs["capped"][key]), key
+    x = outs["capped"]
+    B, S, H, hd = 2, 512, 3, 128
+    T, h = B * S, H * hd
+    qf, kf, vf, o_ref, _ = torch_ref(x["q"].cuda(), x["k"].cuda(), x["v"].cuda(), B, S, H, hd)
+    o_ref.permute(0, 2, 1, 3).reshape(T, h).backward(x["do"].cuda().float())
+    for key, ref in (("dq", qf.grad), ("dk", kf.grad), ("dv", vf.grad)):
+        assert rel(x[key].cuda(), ref.permute(0, 2, 1, 3).reshape(T, h)) < 2e-2, key

@@ -37,6 +37,49 @@ int main() {
   unsigned long long* tl;
   cudaMalloc(&tl, (size_t)2 * ctas * 16 * 8);
   cudaMemcpyToSymbol(g_attn_tl, &tl, sizeof(tl));
+  if (std::getenv("TIMELINE_FWD")) {   // flash_fwd_pp2: 0 start, 1 Q landed, 2 tile B's first S,
+                                       // 3 tile B's O final, 4 tile B's O stored, 5 end, 6 SM, 7 steps
+    const int fctas = (S / 256) * B * H;
+    for (int rep = 0; rep < 3; ++rep)
+      if (hlm_flash_fwd_tc(q, k, v, dq, lse, B, S, H, ld, 0) != 0) return 1;
+    if (cudaDeviceSynchronize() != cudaSuccess) return 2;
+    std::vector<unsigned long long> f((size_t)fctas * 16);
+    cudaMemcpy(f.data(), tl, f.size() * 8, cudaMemcpyDeviceToHost);
+    double q = 0, s0 = 0, fin = 0, st = 0, end = 0, gap = 0;
+    int ngap = 0;
+    std::map<int, std::vector<std::pair<unsigned long long, unsigned long long>>> per_sm;
+    std::map<int, std::vector<double>> by_n;
+    unsigned long long t0 = ~0ull, t1 = 0;
+    for (int c = 0; c < fctas; ++c) {
+      const unsigned long long* r = &f[c * 16];
+      t0 = std::min(t0, r[0]);
+      t1 = std::max(t1, r[5]);
+      q += double(r[1] - r[0]);
+      s0 += double(r[2] - r[0]);
+      fin += double(r[3] - r[0]);
+      st += double(r[4] - r[3]);
+      end += double(r[5] - r[4]);
+      per_sm[(int)r[6]].push_back({r[0], r[5]});
+      by_n[(int)r[7]].push_back(double(r[5] - r[0]));
+    }
+    for (auto& [sm, v] : per_sm) {
+      std::sort(v.begin(), v.end());
+      for (size_t i = 1; i < v.size(); ++i) {
+        gap += double(v[i].first) - double(v[i - 1].second);
+        ++ngap;
+      }
+    }
+    std::printf("forward span %.1f us, %d CTAs; per CTA (us): start -> Q landed %.2f, -> first S %.2f, "
+                "-> O final %.2f, O store %.2f, -> end %.2f; gap between CTAs on an SM %.2f\n",
+                (t1 - t0) / 1e3, fctas, q / fctas / 1e3, s0 / fctas / 1e3, fin / fctas / 1e3, st / fctas / 1e3,
+                end / fctas / 1e3, gap / ngap / 1e3);
+    for (auto& [n, v] : by_n) {
+      double sum = 0;
+      for (double d : v) sum += d;
+      std::printf("  %2d key steps: %4zu CTAs, avg %.2f us\n", n, v.size(), sum / v.size() / 1e3);
+    }
+    return 0;
+  }
   for (int rep = 0; rep < 3; ++rep)
     if (hlm_flash_bwd_tc(q, k, v, dout, lse, dsum, dq, dk, dv, B, S, H, ld, 0) != 0) return 1;
   if (cudaDeviceSynchronize() != cudaSuccess) return 2;
