@@ -2383,10 +2383,10 @@ bool tile_counter(int** ctr, int* nsm) {
   return true;
 }
 
-// Heads per launch-order group (tile_order). Forward: 16 (0.272 vs 0.279 ms head by head at
-// C2); backward: head by head (dK/dV and dQ re-read K / V / Q / dO more and lose more L2
-// locality than the tail costs: 0.964 vs 0.973 ms at 16). HLM_ATTN_TILE_GROUP /
-// HLM_ATTN_BWD_TILE_GROUP override.
+// Heads per tile-order group (tile_decode). Forward: 16 (0.272 vs 0.279 ms head by head at
+// C2). Backward (persistent kernels, tiles claimed in this order): 8 (dK/dV 453 vs 462 us head
+// by head, dQ indifferent; with one CTA per tile, grouping lost more L2 locality than the tail
+// cost). HLM_ATTN_TILE_GROUP / HLM_ATTN_BWD_TILE_GROUP override.
 int tile_group(bool bwd) {
   static const int g[2] = {[] {
                              const char* e = std::getenv("HLM_ATTN_TILE_GROUP");
@@ -2394,7 +2394,7 @@ int tile_group(bool bwd) {
                            }(),
                            [] {
                              const char* e = std::getenv("HLM_ATTN_BWD_TILE_GROUP");
-                             return e ? std::atoi(e) : 0;
+                             return e ? std::atoi(e) : 8;
                            }()};
   return g[bwd ? 1 : 0];
 }
