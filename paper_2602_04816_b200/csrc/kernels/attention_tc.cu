@@ -2334,7 +2334,7 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-bool make_map_2d(CUtensorMap* map, const void* ptr, long long rows, int ld, int box_rows = 128) {
+bool encode_map_2d(CUtensorMap* map, const void* ptr, long long rows, int ld, int box_rows) {
   static EncodeTiledFn fn = nullptr;
   if (!fn) {
     cudaDriverEntryPointQueryResult q;
@@ -2351,6 +2351,37 @@ bool make_map_2d(CUtensorMap* map, const void* ptr, long long rows, int ld, int 
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Tensor maps by (pointer, rows, ld, box): a block's attention runs on the same arena
+// buffers layer after layer, and encoding a map costs microseconds of host time per call
+// (8 per backward) on the thread that feeds the compute stream. Direct-mapped, 128 entries;
+// a map depends only on its key, so a hit is exact.
+bool make_map_2d(CUtensorMap* map, const void* ptr, long long rows, int ld, int box_rows = 128) {
+  struct Entry {
+    const void* ptr;
+    long long rows;
+    int ld, box;
+    bool valid;
+    CUtensorMap map;
+  };
+  constexpr int kEntries = 128;
+  static Entry cache[kEntries];
+  static std::mutex mu;
+  const size_t slot = ((reinterpret_cast<uintptr_t>(ptr) >> 7) ^ (size_t)rows * 131u ^ (size_t)ld * 31u ^
+                       (size_t)box_rows) % kEntries;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    const Entry& e = cache[slot];
+    if (e.valid && e.ptr == ptr && e.rows == rows && e.ld == ld && e.box == box_rows) {
+      *map = e.map;
+      return true;
+    }
+  }
+  if (!encode_map_2d(map, ptr, rows, ld, box_rows)) return false;
+  std::lock_guard<std::mutex> lock(mu);
+  cache[slot] = Entry{ptr, rows, ld, box_rows, true, *map};
+  return true;
 }
 
 // Work counters of the persistent kernels: a ring of 1024 per device, one slot per launch
