@@ -655,7 +655,13 @@ def run_ours(args, m, name):
                                       "back to back (hlm_cuda_bench_block_gemms)"}},
         "attention_roofline": {k: dict(kt[k], frac=(kt[k]["tflops"] or 0) / tf_burst, peak=tf_burst,
                                        frac_of_sustained=(kt[k]["tflops"] or 0) / tf_sus, peak_sustained=tf_sus,
-                                       standalone=attn_probe.get(k))
+                                       standalone=attn_probe.get(k),
+                                       note="in-step: CUDA events around each attention call of the timed steps; "
+                                            "in this host-bound step the pair also counts the compute stream "
+                                            "waiting for its host thread to enqueue the launch (the ncu launch "
+                                            "list, profiles/r02/r02_launches_c2.csv, has the kernels within 7 % "
+                                            "of standalone); standalone: the same call back to back at the "
+                                            "workload shape")
                                for k in ("attn_fwd", "attn_bwd")},
         "elementwise_roofline": {"peak_gbs": hbm, "unit": "GB/s", "in_step": ew_step, "probe": elementwise,
                                  "def": "algorithmic bytes (each tensor read/written once) / CUDA-event time; "
