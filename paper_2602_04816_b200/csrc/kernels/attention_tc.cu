@@ -922,6 +922,324 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
   if (threadIdx.x == 0) HLM_TL(5);
 }
 
+// Persistent forward: one CTA per SM walks the query-tile pairs (claimed from a per-launch
+// counter by the producer, as the persistent backward kernels), everything else as
+// flash_fwd_pp2 per pair. The tile boundary (the timeline's forward mode: ~5 us per CTA of Q
+// load, first S, O store and CTA-to-CTA gap on a 0.94 us step):
+//   * O goes out through a dedicated 32 KB stage (used by A and B in turn, stage_done), so a
+//     tile's Q buffer frees as soon as its last S MMA completes (q_free, committed by the MMA
+//     warp) and the producer loads the next pair's Q there while the tile finishes;
+//   * the next pair's first S MMAs follow this pair's last PV on the tensor pipe, under the
+//     O stores;
+//   * per-tile S / P buffers and their barrier parities continue across pairs (global step
+//     counts); pv_done / o_final / q_full / q_free complete once per pair.
+struct PP3Bars {
+  uint64_t q_full[2], q_free[2], kv_full[KF_STAGES], kv_empty[KF_STAGES], s_full[2][2], p_full[2][2], pv_done[2],
+      o_final[2], stage_done, tile_full[2], tile_empty[2];
+  int tile_id[2];
+  uint32_t tmem;
+};
+static_assert(sizeof(PP3Bars) <= 256, "barrier block");
+constexpr int PP3_SMEM = TILE_BYTES * 2 + KF_STAGES * 2 * HALF_TILE + TILE_BYTES + 256;
+static_assert(PP3_SMEM <= 227 * 1024, "shared memory");
+constexpr int PP3_TILE_READERS = 9;   // the MMA warp + 8 softmax warps
+
+template <int kEmu>
+__global__ void __launch_bounds__(PP_THREADS, 1)
+    flash_fwd_pp3(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k64,
+                  const __grid_constant__ CUtensorMap map_v64, __nv_bfloat16* __restrict__ o, float* __restrict__ lse,
+                  int S, int H, int ld, float scale_log2, int order, int nbh, int* __restrict__ tile_ctr) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;   // 1024-aligned window, no slack in PP3_SMEM; checked
+  if (smem_u32(smem) & 1023) __trap();
+  auto sQ = [&](int t) { return smem + t * TILE_BYTES; };
+  auto sK = [&](int st) { return smem + 2 * TILE_BYTES + st * 2 * HALF_TILE; };
+  auto sV = [&](int st) { return smem + 2 * TILE_BYTES + st * 2 * HALF_TILE + HALF_TILE; };
+  const uint32_t s_out = smem_u32(smem + 2 * TILE_BYTES + KF_STAGES * 2 * HALF_TILE);
+  PP3Bars* bars = reinterpret_cast<PP3Bars*>(smem + 3 * TILE_BYTES + KF_STAGES * 2 * HALF_TILE);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int npairs = S / (2 * TQ), total = npairs * nbh;
+  if (threadIdx.x == 0) {
+    tma_prefetch(&map_q);
+    tma_prefetch(&map_k64);
+    tma_prefetch(&map_v64);
+    for (int i = 0; i < KF_STAGES; ++i) {
+      mbar_init(&bars->kv_full[i], 1);
+      mbar_init(&bars->kv_empty[i], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&bars->q_full[t], 1);
+      mbar_init(&bars->q_free[t], 1);
+      mbar_init(&bars->s_full[t][0], 1);
+      mbar_init(&bars->s_full[t][1], 1);
+      mbar_init(&bars->p_full[t][0], 4);
+      mbar_init(&bars->p_full[t][1], 4);
+      mbar_init(&bars->pv_done[t], 1);
+      mbar_init(&bars->o_final[t], 1);
+      mbar_init(&bars->tile_full[t], 1);
+      mbar_init(&bars->tile_empty[t], PP3_TILE_READERS);
+    }
+    mbar_init(&bars->stage_done, 4);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&bars->tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem;
+  auto next_tile = [&](int j) {
+    const int slot = j & 1;
+    mbar_wait(&bars->tile_full[slot], (j >> 1) & 1);
+    const int id = *reinterpret_cast<volatile int*>(&bars->tile_id[slot]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bars->tile_empty[slot]);
+    return id;
+  };
+  auto decode = [&](int id, int& pair, int& bh) {
+    int rank;
+    tile_decode(id, npairs, nbh, order, rank, bh);
+    pair = npairs - 1 - rank;   // long (late) query tiles first
+  };
+
+  if (warp == 0) {
+    // claim pair p, publish it, load its Q (each tile's buffer once that tile's last S of
+    // the previous pair has completed), then stream its K / V steps through the ring
+    auto claim = [&](int p) {
+      int t = 0;
+      if (lane == 0) {
+        const int slot = p & 1;
+        mbar_wait(&bars->tile_empty[slot], ((p >> 1) & 1) ^ 1);
+        t = atomicAdd(tile_ctr, 1);
+        if (t >= total) t = -1;
+        bars->tile_id[slot] = t;
+        mbar_arrive(&bars->tile_full[slot]);
+      }
+      return __shfl_sync(0xffffffffu, t, 0);
+    };
+    int g = 0;
+    int id = claim(0);
+    for (int p = 0; id >= 0; ++p) {
+      int pair, bh;
+      decode(id, pair, bh);
+      const int nb = 4 * pair + 4, row0 = (bh / H) * S, col0 = (bh % H) * HD;
+      if (lane == 0) {
+        for (int t = 0; t < 2; ++t) {
+          if (p > 0) mbar_wait(&bars->q_free[t], (p - 1) & 1);
+          mbar_arrive_expect_tx(&bars->q_full[t], TILE_BYTES);
+          tma_load_2d(sQ(t), &map_q, &bars->q_full[t], col0, row0 + (2 * pair + t) * TQ);
+          tma_load_2d(sQ(t) + ATOM_BYTES, &map_q, &bars->q_full[t], col0 + 64, row0 + (2 * pair + t) * TQ);
+        }
+        for (int j = 0; j < nb; ++j) {
+          const int gg = g + j, st = gg % KF_STAGES;
+          const int r = row0 + j * 64;
+          mbar_wait(&bars->kv_empty[st], ((gg / KF_STAGES) & 1) ^ 1);
+          mbar_arrive_expect_tx(&bars->kv_full[st], 2 * HALF_TILE);
+          tma_load_2d(sK(st), &map_k64, &bars->kv_full[st], col0, r);
+          tma_load_2d(sK(st) + HALF_ATOM, &map_k64, &bars->kv_full[st], col0 + 64, r);
+          tma_load_2d(sV(st), &map_v64, &bars->kv_full[st], col0, r);
+          tma_load_2d(sV(st) + HALF_ATOM, &map_v64, &bars->kv_full[st], col0 + 64, r);
+        }
+      }
+      __syncwarp();
+      g += nb;
+      id = claim(p + 1);
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_s = make_idesc_bf16(128, 64, false, false);
+    constexpr uint32_t idesc_o = make_idesc_bf16(128, 128, false, true);
+    int g0 = 0, base[2] = {0, 0};
+    for (int p = 0;; ++p) {
+      const int id = next_tile(p);
+      if (id < 0) break;
+      int pair, bh;
+      decode(id, pair, bh);
+      const int nb = 4 * pair + 4;
+      const int n_t[2] = {nb - 2, nb};
+      auto issue_s = [&](int t, int j) {
+        const int gg = g0 + j, st = gg % KF_STAGES, gs = base[t] + j;
+        mbar_wait(&bars->kv_full[st], (gg / KF_STAGES) & 1);
+        tc_fence_after();
+        umma_chain_w<8, ATOM_BYTES / 16, 2, HALF_ATOM / 16, 2>(tmem + t * 128 + (gs & 1) * 64,
+                                                              kmajor_desc(smem_u32(sQ(t)), 0),
+                                                              kmajor_desc64(smem_u32(sK(st)), 0), idesc_s, 0u);
+        umma_commit_w(&bars->s_full[t][gs & 1]);
+        if (j + 1 == n_t[t]) umma_commit_w(&bars->q_free[t]);   // Q_t read for the last time
+      };
+      // O_t += P_t(j) V_j, P_t(j) (bf16) in the first 32 columns of S_t[gs % 2]
+      auto issue_pv = [&](int t, int j) {
+        const int gg = g0 + j, st = gg % KF_STAGES, gs = base[t] + j;
+        mbar_wait(&bars->p_full[t][gs & 1], (gs >> 1) & 1);
+        tc_fence_after();
+        const uint32_t v_base = smem_u32(sV(st));
+        const uint32_t p_tmem = tmem + t * 128 + (gs & 1) * 64;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_bf16_ts_w(tmem + 256 + t * 128, p_tmem + kk * 8, mnmajor_desc64(v_base, kk), idesc_o,
+                         (j > 0 || kk > 0) ? 1u : 0u);
+        if (j + 2 == n_t[t]) umma_commit_w(&bars->pv_done[t]);   // PV_t(n-2): for a rescale at the last step
+        if (t == 1) umma_commit_w(&bars->kv_empty[st]);
+        if (j + 1 == n_t[t]) umma_commit_w(&bars->o_final[t]);
+      };
+      mbar_wait(&bars->q_full[0], p & 1);
+      issue_s(0, 0);
+      issue_s(0, 1);
+      mbar_wait(&bars->q_full[1], p & 1);
+      issue_s(1, 0);
+      issue_s(1, 1);
+      for (int j = 0; j < nb; ++j) {
+        for (int t = 0; t < 2; ++t) {
+          if (j >= n_t[t]) continue;
+          issue_pv(t, j);
+          if (j + 2 < n_t[t]) issue_s(t, j + 2);
+        }
+      }
+      g0 += nb;
+      base[0] += n_t[0];
+      base[1] += n_t[1];
+    }
+  } else {
+    const int t = (warp - 2) >> 2;                 // query tile A (0) or B (1)
+    const int quarter = warp & 3;                  // TMEM lanes 32*quarter ..
+    const int r = quarter * 32 + lane;             // query row within the tile
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const uint32_t s_base = tmem + t * 128 + lane_off, o_addr = tmem + 256 + t * 128 + lane_off;
+    int base = 0;
+    for (int p = 0;; ++p) {
+      const int id = next_tile(p);
+      if (id < 0) break;
+      int pair, bh;
+      decode(id, pair, bh);
+      const int row0 = (bh / H) * S, col0 = (bh % H) * HD;
+      const int qt = 2 * pair + t, n = 2 * qt + 2;
+      const int qpos = qt * TQ + r;
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < n; ++j) {
+        const int gs = base + j;
+        const uint32_t s_addr = s_base + (gs & 1) * 64;
+        mbar_wait(&bars->s_full[t][gs & 1], (gs >> 1) & 1);
+        tc_fence_after();
+        uint32_t sv[2][32];
+        tmem_ld_32x32(s_addr, sv[0]);
+        tmem_ld_32x32(s_addr + 32, sv[1]);
+        tmem_ld_wait();
+        if (j >= 2 * qt) {   // the two diagonal steps (warp-uniform): mask keys above the row
+          const int k0 = j * 64;
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (k0 + c * 32 + e > qpos) sv[c][e] = __float_as_uint(-INFINITY);
+        }
+        float mx8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) mx8[u] = fmaxf(__uint_as_float(sv[0][u]), __uint_as_float(sv[0][u + 8]));
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int e = (c == 0 ? 16 : 0); e < 32; e += 2)
+            mx8[e & 7] = fmax3(mx8[e & 7], __uint_as_float(sv[c][e]), __uint_as_float(sv[c][e + 1]));
+        const float mx = scale_log2 * fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                            fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        if (j == 0) {
+          m = mx;
+        } else if (__any_sync(0xffffffffu, mx > m + kRescaleLog2)) {
+          // O_t holds P V of steps < j; PV_t(j-1) may still run: wait for it (S_t(j+1), issued
+          // behind it, or at the last step the pair's pv_done), then rescale
+          if (j + 1 < n)
+            mbar_wait(&bars->s_full[t][(gs + 1) & 1], ((gs + 1) >> 1) & 1);
+          else
+            mbar_wait(&bars->pv_done[t], p & 1);
+          tc_fence_after();
+          const float mn = fmaxf(m, mx);
+          const float alpha = ex2(m - mn);
+#pragma unroll 1
+          for (int c = 0; c < 8; ++c) {
+            uint32_t ov[16];
+            tmem_ld_32x16(o_addr + c * 16, ov);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+            tmem_st_32x16(o_addr + c * 16, ov);
+          }
+          tmem_st_wait();
+          l *= alpha;
+          m = mn;
+        }
+        const float negm = -m;
+        float l8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            float a0, a1;
+            ffma2(a0, a1, __uint_as_float(sv[c][2 * e]), __uint_as_float(sv[c][2 * e + 1]), scale_log2, negm);
+            float p0, p1;
+            if ((e & 3) < kEmu) {
+              ex2_poly2(p0, p1, a0, a1);
+            } else {
+              p0 = ex2(a0);
+              p1 = ex2(a1);
+            }
+            fadd2(l8[2 * (e & 3)], l8[2 * (e & 3) + 1], p0, p1);
+            pk[e] = pack_bf16x2(p0, p1);
+          }
+          tmem_st_32x16(s_addr + c * 16, pk);
+        }
+        l += ((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7]));
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->p_full[t][gs & 1]);
+      }
+      base += n;
+      mbar_wait(&bars->o_final[t], p & 1);
+      mbar_wait(&bars->pv_done[t], p & 1);   // this pair's phase (complete with o_final)
+      tc_fence_after();
+      const float il = 1.f / l;
+      // the O stage goes A(0), B(0), A(1), B(1), ...: epilogue k = 2p + t waits for k - 1
+      const int k = 2 * p + t;
+      if (k > 0) mbar_wait(&bars->stage_done, (k - 1) & 1);
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t ov[32];
+        tmem_ld_32x32(o_addr + c * 32, ov);
+        tmem_ld_wait();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int ch = c * 4 + q;
+          st_shared_v4(s_out + r * 256 + ((ch ^ (r & 7)) << 4),
+                       pack_bf16x2(__uint_as_float(ov[8 * q]) * il, __uint_as_float(ov[8 * q + 1]) * il),
+                       pack_bf16x2(__uint_as_float(ov[8 * q + 2]) * il, __uint_as_float(ov[8 * q + 3]) * il),
+                       pack_bf16x2(__uint_as_float(ov[8 * q + 4]) * il, __uint_as_float(ov[8 * q + 5]) * il),
+                       pack_bf16x2(__uint_as_float(ov[8 * q + 6]) * il, __uint_as_float(ov[8 * q + 7]) * il));
+        }
+      }
+      // O_t is read out: the next pair's first PV_t may overwrite it once this tile's next
+      // P arrives (tc_fence_before there orders the loads above)
+      lse[(long long)bh * S + qpos] = (m + log2f(l)) / kLog2e;
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + t) : "memory");   // this tile's 4 warps
+      __nv_bfloat16* otile = o + (long long)(row0 + qt * TQ) * ld + col0;
+      const int et = quarter * 32 + lane;
+#pragma unroll 4
+      for (int i = 0; i < 16; ++i) {
+        const int idx = i * 128 + et, row = idx >> 4, ch = idx & 15;
+        uint4 w;
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                     : "r"(s_out + row * 256 + ((ch ^ (row & 7)) << 4)));
+        *reinterpret_cast<uint4*>(otile + (long long)row * ld + ch * 8) = w;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->stage_done);   // this warp's stage reads are done
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
 // ------------------------------------------------------------------ backward
 // Shared pieces: a 128-row bf16 tile written by 128 threads (thread = row) into
 // the K-major SW128 layout the MMA A operand expects (two 64-column atoms).
@@ -2453,7 +2771,33 @@ int hlm_flash_fwd_tc(const void* q, const void* k, const void* v, void* o, float
       return e ? std::atoi(e) : 1;
     }();
     static const bool v2 = std::getenv("HLM_ATTN_FWD_PP1") == nullptr;
-    if (v2) {   // 64-key steps, S double-buffered per tile (default)
+    static const bool persist = [] {
+      const char* e = std::getenv("HLM_ATTN_FWD_PERSIST");
+      return e ? std::atoi(e) != 0 : true;
+    }();
+    if (v2 && persist) {   // persistent over query-tile pairs (default)
+      CUtensorMap mk64, mv64;
+      if (!make_map_2d(&mk64, k, rows, ld, 64) || !make_map_2d(&mv64, v, rows, ld, 64)) return 3;
+      auto kern3 = emu >= 2 ? flash_fwd_pp3<2> : emu == 1 ? flash_fwd_pp3<1> : flash_fwd_pp3<0>;
+      static bool attr_pp3 = false;
+      if (!attr_pp3) {
+        cudaFuncSetAttribute(flash_fwd_pp3<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, PP3_SMEM);
+        cudaFuncSetAttribute(flash_fwd_pp3<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, PP3_SMEM);
+        cudaFuncSetAttribute(flash_fwd_pp3<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, PP3_SMEM);
+        attr_pp3 = true;
+      }
+      int* ctr = nullptr;
+      int nsm = 0;
+      if (!tile_counter(&ctr, &nsm)) return 1;
+      if (cudaMemsetAsync(ctr, 0, sizeof(int), s) != cudaSuccess) return 1;
+      const int pairs = (S / (2 * TQ)) * B * H;
+      kern3<<<std::min(nsm, pairs), PP_THREADS, PP3_SMEM, s>>>(mq, mk64, mv64, (__nv_bfloat16*)o, lse, S, H, ld,
+                                                                (1.0f / sqrtf((float)HD)) * kLog2e,
+                                                                tile_group(false), B * H, ctr);
+      hlm_count_launches(1);
+      return cudaGetLastError() == cudaSuccess ? 0 : 1;
+    }
+    if (v2) {   // 64-key steps, S double-buffered per tile, one CTA per pair
       CUtensorMap mk64, mv64;
       if (!make_map_2d(&mk64, k, rows, ld, 64) || !make_map_2d(&mv64, v, rows, ld, 64)) return 3;
       auto kern2 = emu >= 2 ? flash_fwd_pp2<2> : emu == 1 ? flash_fwd_pp2<1> : flash_fwd_pp2<0>;

@@ -147,7 +147,7 @@ torch.save({{"o": o.cpu(), "dq": dq.cpu(), "dk": dk.cpu(), "dv": dv.cpu()}}, sys
 def test_kernel_variants_agree(tmp_path):
     """Every selectable variant (exp2 on MUFU vs partly on the FMA pipe; 128- vs 64-wide
     forward / backward steps; one- vs two-query-tile forward; persistent vs one-CTA-per-tile
-    dK/dV) gives the same attention within bf16 noise."""
+    kernels) gives the same attention within bf16 noise."""
     import os
     import subprocess
     import sys
@@ -157,6 +157,7 @@ def test_kernel_variants_agree(tmp_path):
     outs = {}
     for name, env in (("default", {}), ("emu0", {"HLM_ATTN_EXP_EMU": "0"}), ("emu2", {"HLM_ATTN_EXP_EMU": "2"}),
                       ("bwd_v1", {"HLM_ATTN_BWD_V1": "1"}), ("bwd_grid", {"HLM_ATTN_BWD_PERSIST": "0"}),
+                      ("fwd_grid", {"HLM_ATTN_FWD_PERSIST": "0"}),
                       ("fwd_pp1", {"HLM_ATTN_FWD_PP1": "1"}), ("fwd_v1", {"HLM_ATTN_FWD_V1": "1"})):
         path = tmp_path / f"{name}.pt"
         subprocess.run([sys.executable, str(script), str(path)], check=True, env={**os.environ, **env})
@@ -190,7 +191,7 @@ torch.save({{"q": q.cpu(), "k": k.cpu(), "v": v.cpu(), "do": do.cpu(), "o": o.cp
 
 @pytest.mark.parametrize("ctas", ["1", "3", "7"])
 def test_persistent_backward_many_tiles_per_cta(tmp_path, ctas):
-    """The persistent dK/dV and dQ kernels with their grids capped (HLM_ATTN_PERSIST_CTAS) so each
+    """The persistent forward, dK/dV and dQ kernels with their grids capped (HLM_ATTN_PERSIST_CTAS) so each
     CTA walks many tiles (24 here; tile boundaries at both barrier parities, K/V and Q/dO handed
     over between tiles, the store stage reused): bitwise equal to the uncapped launch (a tile's
     arithmetic does not depend on which CTA runs it) and close to torch fp32."""
