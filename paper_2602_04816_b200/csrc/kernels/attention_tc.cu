@@ -58,6 +58,16 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// TMA store of one box (shared -> global, bulk-group completion)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 // Blackwell packed fp32 (two lanes per instruction, each rounded like FFMA / FADD)
 // and the three-input max: fewer issue slots per score in the softmax loop.
 __device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b, float c) {
@@ -1955,6 +1965,37 @@ __device__ __forceinline__ void store_acc_staged(__nv_bfloat16* tile, int ld, ui
   asm volatile("bar.sync 1, 512;" ::: "memory");   // the stage is free again
 }
 
+// The same 128 x 128 accumulator -> bf16 tile, written by TMA from the 32 KB stage laid out as
+// the store map's two 128 x 64 SW128 boxes: the warps only move TMEM -> shared memory, the
+// copy engine writes global memory while they go on. The stage is reused after the previous
+// store has read it (the issuing thread, et == 0, waits for that before the first barrier);
+// the caller waits for all stores (bulk_wait0 by et == 0) before the CTA exits.
+__device__ __forceinline__ void store_acc_tma(const CUtensorMap* map, int c0, int r0, uint32_t taddr, float scale,
+                                              uint32_t stage, int r, int cq, int et) {
+  uint32_t v[32];
+  tmem_ld_32x32(taddr, v);
+  if (et == 0) bulk_wait_read0();
+  asm volatile("bar.sync 1, 512;" ::: "memory");
+  tmem_ld_wait();
+  const uint32_t row = stage + (cq >> 1) * ATOM_BYTES + r * 128;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int chunk = (cq & 1) * 4 + q;
+    st_shared_v4(row + ((chunk ^ (r & 7)) << 4),
+                 pack_bf16x2(__uint_as_float(v[8 * q]) * scale, __uint_as_float(v[8 * q + 1]) * scale),
+                 pack_bf16x2(__uint_as_float(v[8 * q + 2]) * scale, __uint_as_float(v[8 * q + 3]) * scale),
+                 pack_bf16x2(__uint_as_float(v[8 * q + 4]) * scale, __uint_as_float(v[8 * q + 5]) * scale),
+                 pack_bf16x2(__uint_as_float(v[8 * q + 6]) * scale, __uint_as_float(v[8 * q + 7]) * scale));
+  }
+  fence_proxy_async();
+  asm volatile("bar.sync 1, 512;" ::: "memory");
+  if (et == 0) {
+    tma_store_2d(map, stage, c0, r0);
+    tma_store_2d(map, stage + ATOM_BYTES, c0 + 64, r0);
+    bulk_commit();
+  }
+}
+
 // Persistent dK / dV: one CTA per SM walks the 128-key tiles (fetched from a global counter,
 // so the causal lengths balance dynamically) with the TMEM allocation, barriers and the Q|dO
 // ring kept across tiles. Per tile the work is flash_bwd_dkv_tc2's; what changes is the tile
@@ -1984,7 +2025,8 @@ __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
                       const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do64,
                       const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dk,
                       __nv_bfloat16* __restrict__ dv, int S, int H, int ld, float scale, float scale_log2,
-                      int order, int nbh, int* __restrict__ tile_ctr) {
+                      int order, int nbh, int* __restrict__ tile_ctr, const __grid_constant__ CUtensorMap map_dk,
+                      const __grid_constant__ CUtensorMap map_dv, int tma_out) {
   // no alignment slack in BWD_KV3_SMEM (the 32 KB store stage needs it): the dynamic
   // shared-memory window starts 1024-aligned (no static shared memory here); checked
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -2198,14 +2240,20 @@ __global__ void __launch_bounds__(BWD_KV2_THREADS, 1)
       tc_fence_after();
       const int et = (warp - 4) * 32 + lane;
       const long long tile_off = (long long)(row0 + kt * TK) * ld + col0;
-      store_acc_staged(dv + tile_off, ld, tmem + 256 + cq * 32 + lane_off, 1.0f, s_out, r, cq, et);
-      store_acc_staged(dk + tile_off, ld, tmem + 384 + cq * 32 + lane_off, scale, s_out, r, cq, et);
+      if (tma_out) {
+        store_acc_tma(&map_dv, col0, row0 + kt * TK, tmem + 256 + cq * 32 + lane_off, 1.0f, s_out, r, cq, et);
+        store_acc_tma(&map_dk, col0, row0 + kt * TK, tmem + 384 + cq * 32 + lane_off, scale, s_out, r, cq, et);
+      } else {
+        store_acc_staged(dv + tile_off, ld, tmem + 256 + cq * 32 + lane_off, 1.0f, s_out, r, cq, et);
+        store_acc_staged(dk + tile_off, ld, tmem + 384 + cq * 32 + lane_off, scale, s_out, r, cq, et);
+      }
       if (stamp) HLM_TL_AT(id, 4);
       // the tcgen05.ld above completed (store_acc_32 waits); the next tile's first P / dS
       // arrive (after tc_fence_before) is what lets the MMA warp overwrite dV / dK
       g0 += n;
     }
   }
+  if (tma_out && warp == 4 && lane == 0) bulk_wait0();   // et == 0: every dK / dV store has landed
   tc_fence_before();
   __syncthreads();
   if (warp == 2) tmem_dealloc<512>(tmem);
@@ -2420,7 +2468,7 @@ __global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
                      const __grid_constant__ CUtensorMap map_v64, const __grid_constant__ CUtensorMap map_do,
                      const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dq,
                      int S, int H, int ld, float scale, float scale_log2, int order, int nbh,
-                     int* __restrict__ tile_ctr) {
+                     int* __restrict__ tile_ctr, const __grid_constant__ CUtensorMap map_dq, int tma_out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;   // 1024-aligned window, no slack in BWD_Q3_SMEM; checked
   if (smem_u32(smem) & 1023) __trap();
@@ -2634,8 +2682,11 @@ __global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
       }
       mbar_wait(&bars->acc_full, j & 1);
       tc_fence_after();
-      store_acc_staged(dq + (long long)(row0 + qt * TQ) * ld + col0, ld, tmem + 256 + ck * 32 + lane_off, scale,
-                       s_out, r, ck, et);
+      if (tma_out)
+        store_acc_tma(&map_dq, col0, row0 + qt * TQ, tmem + 256 + ck * 32 + lane_off, scale, s_out, r, ck, et);
+      else
+        store_acc_staged(dq + (long long)(row0 + qt * TQ) * ld + col0, ld, tmem + 256 + ck * 32 + lane_off, scale,
+                         s_out, r, ck, et);
       id = nid;
       qt = nqt;
       bh = nbh2;
@@ -2643,6 +2694,7 @@ __global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
       D = nD;
     }
   }
+  if (tma_out && warp == 4 && lane == 0) bulk_wait0();   // et == 0: every dQ store has landed
   tc_fence_before();
   __syncthreads();
   if (warp == 2) tmem_dealloc<512>(tmem);
@@ -2730,6 +2782,16 @@ bool tile_counter(int** ctr, int* nsm) {
   }();
   *nsm = cap > 0 ? std::min(cap, sms[dev]) : sms[dev];
   return true;
+}
+
+// Persistent backward kernels store dK / dV / dQ by TMA from their stage (default) or with
+// row-contiguous st.global (HLM_ATTN_TMA_STORE=0).
+int tma_out() {
+  static const int v = [] {
+    const char* e = std::getenv("HLM_ATTN_TMA_STORE");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
 }
 
 // Heads per tile-order group (tile_decode). Forward: 16 (0.272 vs 0.279 ms head by head at
@@ -2884,9 +2946,11 @@ int hlm_flash_bwd_tc(const void* q, const void* k, const void* v, const void* d_
       }
       if (cudaMemsetAsync(ctr, 0, sizeof(int), s) != cudaSuccess) return 1;
       const int tiles = (S / TK) * B * H;
+      CUtensorMap mdk, mdv;
+      if (!make_map_2d(&mdk, dk, rows, ld) || !make_map_2d(&mdv, dv, rows, ld)) return 3;
       flash_bwd_dkv_tc3<<<std::min(nsm, tiles), BWD_KV2_THREADS, BWD_KV3_SMEM, s>>>(
           mq64, mk, mv, mdo64, lse, dsum, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, S, H, ld, scale, scale * kLog2e,
-          tile_group(true), B * H, ctr);
+          tile_group(true), B * H, ctr, mdk, mdv, tma_out());
     } else {
     auto kv_kern = xp == 1 ? flash_bwd_dkv_tc2<1> : xp == 2 ? flash_bwd_dkv_tc2<2> : flash_bwd_dkv_tc2<0>;
     kv_kern<<<grid, BWD_KV2_THREADS, BWD_KV2_SMEM, s>>>(
@@ -2904,9 +2968,11 @@ int hlm_flash_bwd_tc(const void* q, const void* k, const void* v, const void* d_
       }
       if (cudaMemsetAsync(ctr, 0, sizeof(int), s) != cudaSuccess) return 1;
       const int tiles = (S / TQ) * B * H;
+      CUtensorMap mdq;
+      if (!make_map_2d(&mdq, dq, rows, ld)) return 3;
       flash_bwd_dq_tc3<<<std::min(nsm, tiles), BWD_Q2_THREADS, BWD_Q3_SMEM, s>>>(
           mq, mk64, mv64, mdo, lse, dsum, (__nv_bfloat16*)dq, S, H, ld, scale, scale * kLog2e, tile_group(true),
-          B * H, ctr);
+          B * H, ctr, mdq, tma_out());
     } else
     flash_bwd_dq_tc2<<<grid, BWD_Q2_THREADS, BWD_Q2_SMEM, s>>>(
         (const __nv_bfloat16*)q, mk64, mv64, (const __nv_bfloat16*)d_o, lse, dsum, (__nv_bfloat16*)dq, S, H, ld, scale,
