@@ -2520,10 +2520,10 @@ __global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
     tile_decode(id, nt, nbh, order, rank, bh);
     qt = nt - 1 - rank;
   };
-  // the producer claims tile j, publishes it, and TMA-loads its Q / dO (lane 0)
-  auto claim = [&](int j) {
+  // the producer claims tile j, publishes it, and TMA-loads its Q / dO (lane 0 only)
+  auto claim_lane0 = [&](int j) {
     int t = 0;
-    if (lane == 0) {
+    {
       const int slot = j & 1;
       mbar_wait(&bars->tile_empty[slot], ((j >> 1) & 1) ^ 1);
       t = atomicAdd(tile_ctr, 1);
@@ -2542,18 +2542,24 @@ __global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
         tma_load_2d(sdO + ATOM_BYTES, &map_do, &bars->qs_full, c0 + 64, r0);
       }
     }
-    return __shfl_sync(0xffffffffu, t, 0);
+    return t;
   };
+  // the next tile is claimed kClaimAhead steps before this one's last K / V load: its Q / dO
+  // (TMA, ~1.5 us) then land before the elementwise warps reach the boundary
+  constexpr int kClaimAhead = 8;
 
   if (warp == 0) {
     int g = 0;
-    int id = claim(0);
+    int id = __shfl_sync(0xffffffffu, lane == 0 ? claim_lane0(0) : 0, 0);
     for (int j = 0; id >= 0; ++j) {
       int qt, bh;
       decode(id, qt, bh);
       const int n = 2 * qt + 2, row0 = (bh / H) * S, col0 = (bh % H) * HD;
+      int nid = 0;
       if (lane == 0) {
+        const int ahead = n > kClaimAhead ? n - kClaimAhead : 0;
         for (int jj = 0; jj < n; ++jj) {
+          if (jj == ahead) nid = claim_lane0(j + 1);
           const int gg = g + jj, st = gg % Q3_STAGES, ph = (gg / Q3_STAGES) & 1;
           const int r = row0 + jj * 64;
           mbar_wait(&bars->kv_empty[st], ph ^ 1);
@@ -2564,9 +2570,8 @@ __global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
           tma_load_2d(sV(st) + HALF_ATOM, &map_v64, &bars->kv_full[st], col0 + 64, r);
         }
       }
-      __syncwarp();
       g += n;
-      id = claim(j + 1);
+      id = __shfl_sync(0xffffffffu, nid, 0);
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc_s = make_idesc_bf16(128, 64, false, false);
@@ -2642,6 +2647,15 @@ __global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
     for (int j = 0; id >= 0; ++j) {
       const int n = 2 * qt + 2, row0 = (bh / H) * S, col0 = (bh % H) * HD;
       const int qpos = qt * TQ + r;
+      const bool stamp = warp == 4 && lane == 0;
+      if (stamp) {
+        HLM_TL_AT(id + total, 0);
+        unsigned smid_v;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_v));
+        (void)smid_v;
+        HLM_TL_AT_VAL(id + total, 6, smid_v);
+        HLM_TL_AT_VAL(id + total, 7, n);
+      }
       float nl[16], dn[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
@@ -2652,6 +2666,7 @@ __global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
         const int gg = g0 + jj, bb = gg & 1;
         const int k0 = jj * 64 + ck * 16;             // first key column of this thread's 16
         mbar_wait(&bars->s_full[bb], (gg >> 1) & 1);
+        if (stamp && jj == 0) HLM_TL_AT(id + total, 1);
         tc_fence_after();
         uint32_t sv[16], dpv[16];
         tmem_ld_32x16(tmem + bb * 64 + ck * 16 + lane_off, sv);
@@ -2668,6 +2683,7 @@ __global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars->ds_full[bb]);
+        if (stamp && jj == n - 1) HLM_TL_AT(id + total, 2);
       }
       g0 += n;
       // this tile's S / dP have all landed (s_full of its last step): Q / dO columns are free
@@ -2677,20 +2693,23 @@ __global__ void __launch_bounds__(BWD_Q2_THREADS, 1)
       if (nid >= 0) {
         decode(nid, nqt, nbh2);
         load_q(j + 1);
-        nnl0 = -lse[(long long)nbh2 * S + nqt * TQ + r] * kLog2e;   // latency under the dQ store
+        nnl0 = lse[(long long)nbh2 * S + nqt * TQ + r];   // first used after the dQ store (latency hidden)
         nD = dsum[(long long)nbh2 * S + nqt * TQ + r];
       }
+      if (stamp) HLM_TL_AT(id + total, 5);
       mbar_wait(&bars->acc_full, j & 1);
+      if (stamp) HLM_TL_AT(id + total, 3);
       tc_fence_after();
       if (tma_out)
         store_acc_tma(&map_dq, col0, row0 + qt * TQ, tmem + 256 + ck * 32 + lane_off, scale, s_out, r, ck, et);
       else
         store_acc_staged(dq + (long long)(row0 + qt * TQ) * ld + col0, ld, tmem + 256 + ck * 32 + lane_off, scale,
                          s_out, r, ck, et);
+      if (stamp) HLM_TL_AT(id + total, 4);
       id = nid;
       qt = nqt;
       bh = nbh2;
-      nl0 = nnl0;
+      nl0 = -nnl0 * kLog2e;
       D = nD;
     }
   }

@@ -37,7 +37,8 @@ int main() {
   unsigned long long* tl;
   cudaMalloc(&tl, (size_t)2 * ctas * 16 * 8);
   cudaMemcpyToSymbol(g_attn_tl, &tl, sizeof(tl));
-  if (std::getenv("TIMELINE_FWD")) {   // flash_fwd_pp2: 0 start, 1 Q landed, 2 tile B's first S,
+  if (std::getenv("TIMELINE_FWD")) {
+    setenv("HLM_ATTN_FWD_PERSIST", "0", 1);   // the stamps are in the one-CTA-per-pair kernel   // flash_fwd_pp2: 0 start, 1 Q landed, 2 tile B's first S,
                                        // 3 tile B's O final, 4 tile B's O stored, 5 end, 6 SM, 7 steps
     const int fctas = (S / 256) * B * H;
     for (int rep = 0; rep < 3; ++rep)
@@ -122,7 +123,7 @@ int main() {
     }
     std::printf(dq_kernel ? "persistent dQ: span %.1f us, %d tiles on %zu SMs\n" : "persistent dK/dV: span %.1f us, %d tiles on %zu SMs\n", (t1 - t0) / 1e3, ctas, per_sm.size());
     std::printf("per tile (us): fetched -> first S/dP landed %.2f, steady step %.3f, last P/dS -> accumulators "
-                "%.2f, store dK/dV %.2f; previous tile stored -> next fetched %.2f\n",
+                "%.2f, store %.2f; previous tile stored -> next fetched %.2f\n",
                 fetch_to_s / ctas / 1e3, step / nstep / 1e3, tail / ctas / 1e3, epi / ctas / 1e3,
                 between / nb / 1e3);
     if (dq_kernel) {   // slot 5: the next tile's Q / dO written to TMEM (before the dQ accumulator wait)
@@ -134,22 +135,7 @@ int main() {
       }
       std::printf("dQ boundary (us): last dS -> next tile's Q/dO in TMEM %.2f, then -> dQ accumulator %.2f\n",
                   nextq / ctas / 1e3, accw / ctas / 1e3);
-      // 8: id seen by the elementwise warps, 9: Q/dO in TMEM, 10: claimed by the producer,
-      // 11: q_ready seen by the MMA warp, 12: first S/dP issued (all of the tile's own record)
-      double claim_to_seen = 0, seen_to_q = 0, q_to_mma = 0, mma_issue = 0;
-      int cnt = 0;
-      for (int c = 0; c < ctas; ++c) {
-        const unsigned long long* r = &h16[c * 16];
-        if (!r[8] || !r[10]) continue;
-        claim_to_seen += double(r[8]) - double(r[10]);
-        seen_to_q += double(r[9]) - double(r[8]);
-        q_to_mma += double(r[11]) - double(r[9]);
-        mma_issue += double(r[12]) - double(r[11]);
-        ++cnt;
-      }
-      std::printf("  claimed -> seen by elementwise %.2f, -> Q/dO in TMEM %.2f, -> q_ready at MMA warp %.2f, "
-                  "-> first S/dP issued %.2f (%d tiles)\n",
-                  claim_to_seen / cnt / 1e3, seen_to_q / cnt / 1e3, q_to_mma / cnt / 1e3, mma_issue / cnt / 1e3, cnt);
+
     }
     return 0;
   }
