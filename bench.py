@@ -664,6 +664,9 @@ def run_ours(args, m, name):
                                             "workload shape")
                                for k in ("attn_fwd", "attn_bwd")},
         "elementwise_roofline": {"peak_gbs": hbm, "unit": "GB/s", "in_step": ew_step, "probe": elementwise,
+                                 "note": "in_step event pairs also count host enqueue waits in this host-bound "
+                                         "step; per-kernel in-step durations from ncu (profiles/r02/"
+                                         "r02_launches_c2.csv) give 0.95-1.03 of HBM for these kernels",
                                  "def": "algorithmic bytes (each tensor read/written once) / CUDA-event time; "
                                         "in_step: every launch of the timed steps; probe: back-to-back "
                                         "launches at the workload shape after the steps"},
