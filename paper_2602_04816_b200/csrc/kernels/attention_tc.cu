@@ -1,23 +1,23 @@
-// Causal flash-attention FORWARD on tcgen05 (head_dim 128, seq % 128 == 0).
+// Causal flash attention on tcgen05 / TMEM / TMA (head_dim 128, seq % 128 == 0), forward
+// and backward. Same contract as the mma.sync kernels (attention_flash.cu) and the reference
+// attention_fwd / attention_bwd (proj/include/hlm/kernels.hpp:207-299): per head, scale
+// 1/sqrt(hd), O and the row log-sum-exp forward; dQ, dK, dV from O, dO, lse and D = rowsum(dO.O).
 //
-// Same contract as flash_fwd (attention_flash.cu; reference attention_fwd,
-// proj/include/hlm/kernels.hpp:207-245): O and the row log-sum-exp per head.
-// One CTA per (128-query tile, batch*head), 256 threads:
-//   warp 0  TMA producer: Q once, K/V tiles into a 2-stage ring (SW128, 2 boxes
-//           of 64 columns per 128x128 tile = two K-major swizzle atoms)
-//   warp 1  MMA issuer (one lane): S_j = Q K_j^T into TMEM S[j%2] (M=N=128,
-//           K=128), then O_j = P_j V_j into TMEM O[j%2] (V as an MN-major B
-//           operand, P from shared memory); S_{j+1} is issued before PV_j so the
-//           tensor core overlaps the softmax of tile j
-//   warp 2  TMEM allocator (512 columns: S0 S1 O0 O1)
-//   warps 4-11 softmax, 384 threads in all: warp w owns TMEM lanes 32*(w%4)..
-//           (thread = query row) and column half (w-4)/4 of S and O (64 keys /
-//           64 head dims). Per tile: ONE TMEM load of its 64 S columns (kept in
-//           registers), the row max exchanged with the partner warp of the other
-//           half through smem, exp2 + row sum + bf16 P written to its swizzled
-//           smem atom, then the online rescale O_acc = alpha * O_acc + O_j of its
-//           64 O columns in registers (one TMEM load). Two warps per scheduler and
-//           one exposed TMEM latency per pass instead of four.
+// Production kernels (defaults; the others stay selectable for A/B):
+//   flash_fwd_pp3      persistent forward: one CTA per SM walks query-tile PAIRS (two 128-query
+//                      tiles ping-ponging on the tensor core, 64-key steps, S double-buffered
+//                      per tile in TMEM, P written over S, O accumulated in TMEM, lazy 2^8
+//                      rescale), O stored through a shared-memory stage
+//   flash_bwd_dkv_tc3  persistent dK/dV: 128-key tiles, 64-query steps, S^T / dP^T
+//                      double-buffered in TMEM, P^T / dS^T written back over them as A operands
+//                      from TMEM, dK / dV accumulated in TMEM, TMA-stored through a stage
+//   flash_bwd_dq_tc3   persistent dQ: 128-query tiles, 64-key steps, Q / dO TMEM-resident as A
+//                      operands (TMA-loaded for the next tile while this one runs), dS over dP
+// Persistent kernels claim tiles from a per-launch counter (tile_counter) in grouped
+// longest-first order (tile_decode). Earlier versions kept for comparison: flash_fwd_tc (one
+// query tile per CTA, round 1), flash_fwd_pp (128-key steps), flash_fwd_pp2 (one CTA per pair),
+// flash_bwd_dkv_tc / flash_bwd_dq_tc (128-wide steps), flash_bwd_dkv_tc2 / flash_bwd_dq_tc2 (one
+// CTA per tile). DESIGN.md "Attention" has the measurements behind each step.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -149,6 +149,10 @@ __device__ __forceinline__ uint64_t mnmajor_desc64(uint32_t base, int kk) {
   return make_sw128_desc(base + kk * 2048, HALF_ATOM, 1024);
 }
 
+// Round-1 forward (HLM_ATTN_FWD_V1=1): one CTA per (128-query tile, batch*head). Warp 0 TMA
+// (Q once, K/V into a 2-stage ring), warp 1 MMA (S_j = Q K_j^T into TMEM S[j%2], O_j = P_j V_j
+// into O[j%2] with P from shared memory; S_{j+1} issued before PV_j), warp 2 TMEM allocator,
+// warps 4-11 softmax (thread = query row, column halves exchanged through shared memory).
 __global__ void __launch_bounds__(FWD_THREADS, 1)
     flash_fwd_tc(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                  const __grid_constant__ CUtensorMap map_v, __nv_bfloat16* __restrict__ o, float* __restrict__ lse,
