@@ -409,9 +409,14 @@ double hlm_host_triad_gbs(int64_t bytes_per_array, int reps);
 const char* hlm_host_isa(void);
 
 /* HLM2 checkpoint of the host store (master, m, v, Adam step count); load
- * re-derives the BF16 shadow and rejects mismatched geometry (HLM_ERR_CONFIG). */
+ * re-derives the BF16 shadow and rejects mismatched geometry (HLM_ERR_CONFIG).
+ * hlm_store_load also reads the reference's HLM1 files (replaces hlm::load_checkpoint,
+ * /root/reference/proj/src/checkpoint.cpp:71-120: same checks and messages);
+ * hlm_store_save_hlm1 writes HLM1 for the reference's loader (replaces
+ * hlm::save_checkpoint, checkpoint.cpp:38-69). */
 int hlm_store_save(const HlmStore* s, const char* path);
 int hlm_store_load(HlmStore* s, const char* path);
+int hlm_store_save_hlm1(const HlmStore* s, const char* path);
 
 /* NCCL (loaded at run time): 128-byte unique id, communicator create / destroy */
 int hlm_nccl_unique_id(uint8_t* out128);

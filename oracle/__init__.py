@@ -51,6 +51,38 @@ def total_params(c):
     return n + c.layers * (4 * c.hidden ** 2 + 3 * c.hidden * c.ffn + 2 * c.hidden)
 
 
+def read_hlm1(path):
+    """Parse a reference HLM1 checkpoint (restates proj/src/checkpoint.cpp:38-69 and the
+    tile layout of proj/include/hlm/host_store.hpp:40-66): returns dict with dtype
+    ("bf16" | "fp32"), adam_steps, alias (logical -> physical) and per physical tile the
+    weights (float32, widened exactly from bf16), grads, m, v."""
+    buf = open(path, "rb").read()
+    assert buf[:4] == b"HLM1", "not an HLM1 file"
+    ver, n_phys, dtype = np.frombuffer(buf, np.uint32, 3, 4)
+    assert ver == 1
+    total, steps = np.frombuffer(buf, np.uint64, 2, 16)
+    n = np.frombuffer(buf, np.uint64, int(n_phys), 32).astype(np.int64)
+    pos = 32 + 8 * int(n_phys)
+    n_log = int(np.frombuffer(buf, np.uint32, 1, pos)[0])
+    alias = np.frombuffer(buf, np.uint32, n_log, pos + 4).astype(np.int64)
+    pos += 4 + 4 * n_log
+    e = 2 if dtype == 0 else 4
+    tiles = []
+    for k in n:
+        k = int(k)
+        pos = (pos + 4095) // 4096 * 4096
+        raw = [np.frombuffer(buf, np.uint16 if e == 2 else np.float32, k, pos + j * e * k) for j in (0, 1)]
+        if e == 2:
+            raw = [(r.astype(np.uint32) << 16).view(np.float32) for r in raw]
+        m = np.frombuffer(buf, np.float32, k, pos + 2 * e * k)
+        v = np.frombuffer(buf, np.float32, k, pos + 2 * e * k + 4 * k)
+        tiles.append({"weights": raw[0].copy(), "grads": raw[1].copy(), "m": m.copy(), "v": v.copy()})
+        pos += 2 * e * k + 8 * k
+    assert sum(int(x) for x in n) == int(total)
+    return {"dtype": "bf16" if dtype == 0 else "fp32", "adam_steps": int(steps), "alias": alias,
+            "tiles": tiles}
+
+
 def block_params(c):
     return 4 * c.hidden ** 2 + 3 * c.hidden * c.ffn + 2 * c.hidden
 
@@ -234,6 +266,27 @@ class Reference(_Lib):
         self._ok(self.lib.ref_train(ctypes.byref(c), ctypes.byref(hp), seed, int(bf16), steps,
                                     losses, w))
         return losses, w
+
+    def train_save_hlm1(self, c, hp, seed, bf16, steps, path):
+        """run_training for `steps` steps, then the reference's save_checkpoint (HLM1)."""
+        L = self.lib
+        L.ref_train_save_hlm1.argtypes = [ctypes.POINTER(OrcCfg), ctypes.POINTER(OrcHyper),
+                                          ctypes.c_uint64, ctypes.c_int, ctypes.c_int64, ctypes.c_char_p]
+        self._ok(L.ref_train_save_hlm1(ctypes.byref(c), ctypes.byref(hp), seed, int(bf16), steps,
+                                       str(path).encode()))
+
+    def load_hlm1(self, c, bf16, path):
+        """The reference's load_checkpoint of `path`: (weights, m, v, adam_steps), flat in
+        physical tile order."""
+        n = total_params(c)
+        w, m, v = (np.empty(n, np.float32) for _ in range(3))
+        steps = ctypes.c_int64()
+        L = self.lib
+        L.ref_load_hlm1.argtypes = [ctypes.POINTER(OrcCfg), ctypes.c_int, ctypes.c_char_p, _f32p, _f32p,
+                                    _f32p, ctypes.POINTER(ctypes.c_int64)]
+        self._ok(L.ref_load_hlm1(ctypes.byref(c), int(bf16), str(path).encode(), w, m, v,
+                                 ctypes.byref(steps)))
+        return w, m, v, steps.value
 
     def time_train_step(self, c, bf16=True, steps=3, warmup=1):
         t = self.lib.ref_time_train_step(ctypes.byref(c), int(bf16), steps, warmup)

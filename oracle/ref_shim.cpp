@@ -9,6 +9,7 @@
 //   make_copy_task_batch   proj/src/engine.cpp:434-441
 //   block_forward/backward proj/include/hlm/kernels.hpp:313-383
 //   bf16_bits_from_f32     proj/include/hlm/bf16.hpp:15-25
+//   save/load_checkpoint   proj/src/checkpoint.cpp:38-120 (HLM1)
 #include <chrono>
 #include <memory>
 #include <cstring>
@@ -16,6 +17,7 @@
 #include <string>
 
 #include "hlm/bf16.hpp"
+#include "hlm/checkpoint.hpp"
 #include "hlm/engine.hpp"
 #include "hlm/kernels.hpp"
 #include "hlm/oracle.hpp"
@@ -218,6 +220,54 @@ int ref_train(const OrcCfg* c, const OrcHyper* hp, uint64_t seed, int bf16, int6
     const TrainOutput out = run_training(cfg, *store, arena);
     for (std::size_t i = 0; i < out.steps.size(); ++i) losses[i] = out.steps[i].loss;
     if (final_weights) export_weights(*store, final_weights);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// run_training for `steps` steps, then the reference's HLM1 save_checkpoint of the store
+// (golden checkpoint files; tests/golden/make_golden.py).
+int ref_train_save_hlm1(const OrcCfg* c, const OrcHyper* hp, uint64_t seed, int bf16, int64_t steps,
+                        const char* path) {
+  try {
+    RunConfig cfg;
+    cfg.model = to_model(c);
+    cfg.has_model = true;
+    cfg.hyper.lr = hp->lr;
+    cfg.hyper.beta1 = hp->beta1;
+    cfg.hyper.beta2 = hp->beta2;
+    cfg.hyper.eps = hp->eps;
+    cfg.hyper.weight_decay = hp->weight_decay;
+    cfg.run.steps = steps;
+    cfg.run.seed = seed;
+    cfg.run.dtype = bf16 ? Dtype::BF16 : Dtype::FP32;
+    auto store = build_store(cfg.model, seed, cfg.run.dtype);
+    DeviceArena arena(cfg.model, cfg.run.dtype);
+    run_training(cfg, *store, arena);
+    save_checkpoint(*store, path);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// The reference's load_checkpoint of `path` into a store of this geometry; exports the
+// loaded weights (as f32), m, v (flat, physical tile order) and the Adam step count.
+int ref_load_hlm1(const OrcCfg* c, int bf16, const char* path, float* weights, float* m, float* v,
+                  int64_t* adam_steps) {
+  try {
+    auto store = build_store(to_model(c), 1, bf16 ? Dtype::BF16 : Dtype::FP32);
+    load_checkpoint(*store, path);
+    export_weights(*store, weights);
+    for (i64 p = 0; p < store->physical_tiles(); ++p) {
+      LayerTile& t = store->physical(p);
+      std::memcpy(m, t.moment_m(), static_cast<size_t>(t.n_params()) * 4);
+      std::memcpy(v, t.moment_v(), static_cast<size_t>(t.n_params()) * 4);
+      m += t.n_params();
+      v += t.n_params();
+    }
+    *adam_steps = store->adam_steps();
     return 0;
   } catch (const std::exception& e) {
     return fail(e);

@@ -199,6 +199,10 @@ int hlm_store_load(HlmStore* s, const char* path) {
     return guarded([&] { hlm::load_checkpoint(*s->s, path); });
 }
 
+int hlm_store_save_hlm1(const HlmStore* s, const char* path) {
+    return guarded([&] { hlm::save_checkpoint_hlm1(*s->s, path); });
+}
+
 int hlm_run_training_store(HlmStore* s, const HlmHyper* hp, uint64_t seed, int64_t steps,
                            const HlmEngineOptions* o, double* losses) {
     return guarded([&] {

@@ -153,6 +153,7 @@ def _L():
         L.hlm_store_tile_version.restype = ctypes.c_int64
         L.hlm_store_save.argtypes = [_vp, ctypes.c_char_p]
         L.hlm_store_load.argtypes = [_vp, ctypes.c_char_p]
+        L.hlm_store_save_hlm1.argtypes = [_vp, ctypes.c_char_p]
         L.hlm_run_training_store.argtypes = [_vp, P(HyperParams), ctypes.c_uint64, ctypes.c_int64,
                                              P(EngineOptions), _f64p]
         L.hlm_nccl_unique_id.argtypes = [ctypes.c_char_p]
@@ -248,7 +249,12 @@ class Store:
         _check(_L().hlm_store_save(self.h, str(path).encode()))
 
     def load(self, path):
+        """HLM2, or a reference HLM1 file (master := its weights, m / v / step restored)."""
         _check(_L().hlm_store_load(self.h, str(path).encode()))
+
+    def save_hlm1(self, path):
+        """The reference's HLM1 container (its load_checkpoint reads it)."""
+        _check(_L().hlm_store_save_hlm1(self.h, str(path).encode()))
 
     def run_training(self, hyper, seed, steps, options=None):
         """run_training on this store (resume-aware: replays the data stream)."""

@@ -79,6 +79,23 @@ def main():
     np.savez_compressed(os.path.join(OUT, "ref_c1.npz"), tokens=tok, losses32=l32, losses16=l16)
     print("c1", l32, l16, tok[:8])
 
+    # HLM1 checkpoints written by the reference's save_checkpoint after 3 Adam steps
+    # (proj/src/checkpoint.cpp:38-69): a BF16 store, and a tied FP32 store (alias table)
+    for name, bf16 in (("tiny", True), ("acc_tied", False)):
+        kw = CONFIGS[name]
+        path = os.path.join(OUT, f"ref_{name}_{'bf16' if bf16 else 'fp32'}.hlm1")
+        ref.train_save_hlm1(O.cfg(**kw), O.hyper(lr=3e-3), 1000 + kw["layers"], bf16, 3, path)
+        print("hlm1", path, os.path.getsize(path))
+    # resume from a reference checkpoint on the GPU engine: HLM1 after 3 BF16 steps and the
+    # reference's own 5-step loss trajectory from the same seed (steps 4-5 = the resume)
+    rkw = dict(layers=2, hidden=32, ffn=64, vocab=32, seq=16, batch=2, k_ckpt=1)
+    rc = O.cfg(**rkw)
+    ref.train_save_hlm1(rc, O.hyper(lr=1e-2), 1234, True, 3, os.path.join(OUT, "ref_resume_bf16.hlm1"))
+    rl, _ = ref.train(rc, O.hyper(lr=1e-2), 1234, True, 5)
+    np.savez_compressed(os.path.join(OUT, "ref_resume.npz"), cfg_json=str(rkw), seed=1234, lr=1e-2,
+                        losses16=rl)
+    print("resume", rl)
+
     # acceptance criterion 8 (proj/test_output.txt:20): 200-step fp32 copy task, seed 1234
     cc = O.cfg(**CONFIGS["copytask"])
     l200, _ = ref.train(cc, O.hyper(lr=3e-3), 1234, False, 200)
