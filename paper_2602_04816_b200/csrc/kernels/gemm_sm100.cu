@@ -618,8 +618,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       // operand panels are read by every tile of the wave that shares them: L2 evict_last
       // (HLM_GEMM_L2_HINT=0 leaves the default policy, 2 = evict_first)
-      const uint64_t pol = args.l2_hint == 2 ? l2_policy_evict_first()
-                           : args.l2_hint == 1 ? l2_policy_evict_last() : l2_policy_evict_normal();
+      // l2_hint < 10: both operands; otherwise tens digit = A's policy, units digit = B's
+      auto policy = [](int h) {
+        return h == 2 ? l2_policy_evict_first() : h == 1 ? l2_policy_evict_last() : l2_policy_evict_normal();
+      };
+      const uint64_t pol_a = policy(args.l2_hint < 10 ? args.l2_hint : args.l2_hint / 10 % 10);
+      const uint64_t pol_b = policy(args.l2_hint < 10 ? args.l2_hint : args.l2_hint % 10);
       for (int t = pair; t < args.num_tiles; t += npairs) {
         int tg, tm, tn;
         tile_coords_2sm(args, t, tg, tm, tn);
@@ -638,16 +642,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             uint8_t* a_dst = sA + stage * HALF_STAGE;
             uint8_t* b_dst = sB + stage * HALF_STAGE;
             if (A_MN) {
-              tma_load_3d_2sm_hint(a_dst, &map_a, &full[stage], m0, k0, ag, pol);
-              tma_load_3d_2sm_hint(a_dst + ATOM, &map_a, &full[stage], m0 + 64, k0, ag, pol);
+              tma_load_3d_2sm_hint(a_dst, &map_a, &full[stage], m0, k0, ag, pol_a);
+              tma_load_3d_2sm_hint(a_dst + ATOM, &map_a, &full[stage], m0 + 64, k0, ag, pol_a);
             } else {
-              tma_load_3d_2sm_hint(a_dst, &map_a, &full[stage], k0, m0, ag, pol);
+              tma_load_3d_2sm_hint(a_dst, &map_a, &full[stage], k0, m0, ag, pol_a);
             }
             if (B_MN) {
-              tma_load_3d_2sm_hint(b_dst, &map_b, &full[stage], n0, k0, bg, pol);
-              tma_load_3d_2sm_hint(b_dst + ATOM, &map_b, &full[stage], n0 + 64, k0, bg, pol);
+              tma_load_3d_2sm_hint(b_dst, &map_b, &full[stage], n0, k0, bg, pol_b);
+              tma_load_3d_2sm_hint(b_dst + ATOM, &map_b, &full[stage], n0 + 64, k0, bg, pol_b);
             } else {
-              tma_load_3d_2sm_hint(b_dst, &map_b, &full[stage], k0, n0, bg, pol);
+              tma_load_3d_2sm_hint(b_dst, &map_b, &full[stage], k0, n0, bg, pol_b);
             }
             if (++stage == STAGES2) {
               stage = 0;
