@@ -20,6 +20,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -63,6 +64,7 @@ struct KArgs {
   long long ldc2;
   int l2_prefetch;       // SWIGLU_BWD: bulk-prefetch the next tile's up / gate into L2 (A/B)
   int l2_hint;           // 2-CTA operand loads: 0 evict_normal, 1 evict_last, 2 evict_first
+  int* tile_ctr;         // 2-CTA: tiles claimed from this per-launch counter (nullptr: static stride)
 };
 
 __device__ __forceinline__ void tile_coords(const KArgs& a, int t, int& g, int& m, int& n) {
@@ -586,11 +588,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tmem_full = empty + STAGES2;
   uint64_t* tmem_empty = tmem_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  // dynamic schedule: a 4-slot ring of claimed tile ids, written by the leader's producer
+  // into both CTAs; tile_empty (leader) collects the 10 readers (leader MMA + 4 epilogue
+  // warps, peer producer + 4 epilogue warps)
+  uint64_t* tile_full = tmem_empty + 3;
+  uint64_t* tile_empty = tile_full + 4;
+  int* tile_ids = reinterpret_cast<int*>(tile_empty + 4);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const uint32_t crank = cluster_ctarank();
   const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+  const bool dyn = args.tile_ctr != nullptr;
+  // the i-th tile of this pair (static: pair + i * npairs), or -1 when none is left; readers
+  // release their slot as soon as they hold the id
+  auto read_tile = [&](int i, bool release_lane) -> int {
+    if (!dyn) {
+      const int t = pair + i * npairs;
+      return t < args.num_tiles ? t : -1;
+    }
+    const int slot = i & 3;
+    const uint32_t ph = (i >> 2) & 1;
+    if (crank == 0) mbar_wait(&tile_full[slot], ph);
+    else mbar_wait_cluster(&tile_full[slot], ph);
+    const int t = *reinterpret_cast<volatile int*>(&tile_ids[slot]);
+    __syncwarp(__activemask());
+    if (release_lane) {
+      if (crank == 0) mbar_arrive(&tile_empty[slot]);
+      else mbar_arrive_cluster(mapa(&tile_empty[slot], 0));
+    }
+    return t;
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&map_a);
@@ -602,6 +630,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tmem_full[s], 1);
       mbar_init(&tmem_empty[s], 8);   // 4 epilogue warps x 2 CTAs
+    }
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(&tile_full[s], 1);
+      mbar_init(&tile_empty[s], 10);
     }
     fence_barrier_init();
   }
@@ -624,7 +656,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       };
       const uint64_t pol_a = policy(args.l2_hint < 10 ? args.l2_hint : args.l2_hint / 10 % 10);
       const uint64_t pol_b = policy(args.l2_hint < 10 ? args.l2_hint : args.l2_hint % 10);
-      for (int t = pair; t < args.num_tiles; t += npairs) {
+      for (int i = 0;; ++i) {
+        int t;
+        if (dyn && crank == 0) {   // claim the next tile and publish it to both CTAs
+          const int slot = i & 3;
+          mbar_wait(&tile_empty[slot], ((i >> 2) & 1) ^ 1);
+          t = atomicAdd(args.tile_ctr, 1);
+          if (t >= args.num_tiles) t = -1;
+          tile_ids[slot] = t;
+          st_shared_cluster_u32(mapa(&tile_ids[slot], 1), (uint32_t)t);
+          mbar_arrive(&tile_full[slot]);
+          mbar_arrive_cluster(mapa(&tile_full[slot], 1));
+        } else {
+          t = read_tile(i, true);
+        }
+        if (t < 0) break;
         int tg, tm, tn;
         tile_coords_2sm(args, t, tg, tm, tn);
         // paired (SWIGLU): both CTAs load the same 128 output columns, CTA 0 of w_up and
@@ -666,8 +712,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       constexpr uint32_t idesc = make_idesc_bf16(256, 256, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
-      int local = 0;
-      for (int t = pair; t < args.num_tiles; t += npairs, ++local) {
+      for (int local = 0;; ++local) {
+        if (read_tile(local, lane == 0) < 0) break;
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
         mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
@@ -705,14 +751,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const int ew = warp - 4;
     const uint32_t leader_empty0 = mapa(&tmem_empty[0], 0);
     const uint32_t leader_empty1 = mapa(&tmem_empty[1], 0);
-    int local = 0;
-    for (int t = pair; t < args.num_tiles; t += npairs, ++local) {
+    for (int local = 0;; ++local) {
+      const int t = read_tile(local, lane == 0);
+      if (t < 0) break;
       int tg, tm, tn;
       tile_coords_2sm(args, t, tg, tm, tn);
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
-      if (local == 0) epilogue_prefetch(args, tm * 256 + (int)crank * 128 + ew * 32 + lane, tn);
-      if (t + npairs < args.num_tiles) {   // the next tile's epilogue inputs
+      // epilogue inputs: static schedule one tile ahead; dynamic: the next id is not known yet
+      if (local == 0 || dyn) epilogue_prefetch(args, tm * 256 + (int)crank * 128 + ew * 32 + lane, tn);
+      if (!dyn && t + npairs < args.num_tiles) {   // the next tile's epilogue inputs
         int ng, nm, nn;
         tile_coords_2sm(args, t + npairs, ng, nm, nn);
         epilogue_prefetch(args, nm * 256 + (int)crank * 128 + ew * 32 + lane, nn);
@@ -777,6 +825,37 @@ int sm_count() {
     if (n <= 0) n = 148;
   }
   return n;
+}
+
+// HLM_GEMM_DYNAMIC=1: CTA pairs claim tiles from a per-launch counter in raster order, so
+// the tiles in flight stay a contiguous window of the raster however far individual pairs
+// drift (the static stride lets a slow pair fall whole tiles behind its wave, and the wave
+// then stops sharing operand panels in L2).
+bool dynamic_schedule() {
+  static const int v = [] {
+    const char* e = std::getenv("HLM_GEMM_DYNAMIC");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v != 0;
+}
+
+// Per-launch tile counters: a ring of 1024 per device, one slot per launch (zeroed on the
+// launch's stream first), so launches in flight on different streams never share one.
+int* tile_counter() {
+  constexpr int kSlots = 1024, kDevs = 64;
+  static int* ring[kDevs] = {};
+  static std::atomic<unsigned> next{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= kDevs) return nullptr;
+  if (!ring[dev]) {
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!ring[dev] && cudaMalloc(&ring[dev], kSlots * sizeof(int)) != cudaSuccess) {
+      ring[dev] = nullptr;
+      return nullptr;
+    }
+  }
+  return ring[dev] + next.fetch_add(1, std::memory_order_relaxed) % kSlots;
 }
 
 // HLM_GEMM_1SM=1 forces the 1-CTA kernel (A/B comparisons); otherwise the
@@ -875,6 +954,12 @@ int launch(const HlmGemmDesc& d, cudaStream_t stream) {
       attr2 = true;
     }
     const int pairs = a.num_tiles < sm_count() / 2 ? a.num_tiles : sm_count() / 2;
+    a.tile_ctr = nullptr;
+    if (dynamic_schedule() && a.num_tiles > pairs) {
+      a.tile_ctr = tile_counter();
+      if (!a.tile_ctr || cudaMemsetAsync(a.tile_ctr, 0, sizeof(int), stream) != cudaSuccess)
+        return HLM_GEMM_ERR_LAUNCH;
+    }
     gemm_kernel_2sm<A_MN, B_MN><<<2 * pairs, NUM_THREADS, SMEM2_BYTES, stream>>>(ma, mb, a);
   } else {
     static bool attr_set = false;

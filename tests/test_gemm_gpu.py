@@ -94,3 +94,58 @@ def test_gemm_groups():
     for g in range(3):
         ref = X.float().t() @ dY[g].float()
         assert torch.allclose(dW[g], ref, rtol=1e-3, atol=1e-2)
+
+
+_SCHED_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, {root!r})
+sys.path.insert(0, {tests!r})
+from paper_2602_04816_b200 import _lib as L
+from test_gemm_gpu import _desc
+torch.manual_seed(5)
+dev = "cuda"
+out = {{}}
+# 8 x 16 = 128 pair tiles (more than the 74 pairs: several tiles per pair), plain + residual
+M, N, K = 2048, 4096, 512
+A = torch.randn(M, K, device=dev).bfloat16()
+B = torch.randn(N, K, device=dev).bfloat16()
+R = torch.randn(M, N, device=dev)
+C = torch.empty(M, N, device=dev)
+L.gemm(_desc(M, N, K, A, B, C, 0, 0))
+out["plain"] = C.clone()
+L.gemm(_desc(M, N, K, A, B, C, 0, 0, epi=L.EPI_F32_ADD, R=R))
+out["resid"] = C.clone()
+# N-grouped (3 outputs) and K-grouped (2 K groups) with MN-major operands
+G = 3
+Bg = torch.randn(G, K, 1024, device=dev).bfloat16()
+Cg = torch.empty(G, M, 1024, device=dev)
+L.gemm(_desc(M, 1024, K, A, Bg, Cg, 0, 1, G=G, b_grouped=1))
+out["ngroup"] = Cg.clone()
+Ak = torch.randn(2, M, K, device=dev).bfloat16()
+Bk = torch.randn(2, 1024, K, device=dev).bfloat16()
+Ck = torch.empty(M, 1024, device=dev)
+L.gemm(_desc(M, 1024, K, Ak, Bk, Ck, 0, 0, G=2, kgroup=1, a_grouped=1, b_grouped=1))
+out["kgroup"] = Ck.clone()
+torch.cuda.synchronize()
+torch.save({{k: v.cpu() for k, v in out.items()}}, sys.argv[1])
+"""
+
+
+def test_dynamic_tile_schedule_is_bitwise_identical(tmp_path):
+    """HLM_GEMM_DYNAMIC=1 (CTA pairs claim tiles from a per-launch counter) computes every
+    tile exactly as the static stride does: same tiles, same k order, bitwise-equal C."""
+    import os
+    import subprocess
+    import sys
+    tests = os.path.dirname(os.path.abspath(__file__))
+    script = tmp_path / "s.py"
+    script.write_text(_SCHED_SCRIPT.format(root=os.path.dirname(tests), tests=tests))
+    outs = {}
+    for name, env in (("static", {"HLM_GEMM_DYNAMIC": "0"}), ("dynamic", {"HLM_GEMM_DYNAMIC": "1"})):
+        path = tmp_path / f"{name}.pt"
+        subprocess.run([sys.executable, str(script), str(path)], check=True, timeout=300,
+                       env={**os.environ, **env})
+        outs[name] = torch.load(path)
+    for key, v in outs["static"].items():
+        assert torch.equal(v, outs["dynamic"][key]), key
+        assert torch.isfinite(v).all(), key
