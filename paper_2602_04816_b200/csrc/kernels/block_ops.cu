@@ -425,8 +425,18 @@ __global__ void __launch_bounds__(256) norm_scale_reduce_kernel(const float* __r
   const int col = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int j = blockIdx.x * 32 + col;
   float acc = 0.f;
-  if (j < h)
-    for (int c = grp; c < chunks; c += 8) acc += partial[(long long)c * h + j];
+  if (j < h) {
+    // eight loads in flight per thread, added in the same chunk order (bit-identical sums)
+    int c = grp;
+    for (; c + 7 * 8 < chunks; c += 8 * 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = partial[(long long)(c + u * 8) * h + j];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += v[u];
+    }
+    for (; c < chunks; c += 8) acc += partial[(long long)c * h + j];
+  }
   red[grp][col] = acc;
   __syncthreads();
   if (grp == 0 && j < h) {
