@@ -120,9 +120,13 @@ def test_checkpoint_roundtrip_and_geometry_checks(tmp_path):
     assert r.bitwise_equal(s) and r.adam_steps == 2
     with pytest.raises(E.HlmConfigError, match="geometry"):
         E.Store(E.ModelConfig(3, 16, 32, 13, 4, 1), 1, pin=False).load(p)
-    (tmp_path / "bad").write_bytes(b"HLM1xxxxxxxx")
-    with pytest.raises(E.HlmConfigError, match="not an HLM2"):
+    (tmp_path / "bad").write_bytes(b"HLMxxxxxxxxx")
+    with pytest.raises(E.HlmConfigError, match="not an HLM2 or HLM1"):
         r.load(tmp_path / "bad")
+    # an HLM1 header is parsed as the reference's container (tests/test_hlm1.py), with its checks
+    (tmp_path / "bad1").write_bytes(b"HLM1xxxxxxxx")
+    with pytest.raises(E.HlmConfigError, match="unsupported HLM1 version"):
+        r.load(tmp_path / "bad1")
 
 
 def test_sparse_embedding_adam_is_bitwise_the_dense_adam():
