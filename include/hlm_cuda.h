@@ -52,6 +52,37 @@ const char* hlm_cuda_last_error(void);
 /* Select this process's GPU (call before creating stores, communicators or arenas). */
 int hlm_cuda_set_device(int device);
 
+/* ------------------------------------------------------------------ device runtime
+ * SURVEY.md §8b's runtime entry points, for a host caller that keeps its own
+ * scheduler (the reference's Engine::stream_tile / evacuate, proj/src/engine.cpp:55-71,
+ * 186-203, and its DeviceArena, proj/src/device_arena.cpp): streams, events and the
+ * arena are opaque pointers, so the caller never includes a CUDA header.
+ * hlm_cuda_init selects the device and fills caps; HLM_ERR_CONFIG when the device is
+ * not sm_100 (this build carries sm_100a code only). */
+typedef struct HlmCaps {
+  int device, sm_count, cc_major, cc_minor;
+  int64_t hbm_bytes, l2_bytes, smem_per_block_optin;
+  char name[64];
+} HlmCaps;
+enum HlmStreamKind { HLM_STREAM_COMPUTE = 0, HLM_STREAM_H2D = 1, HLM_STREAM_D2H = 2, HLM_STREAM_COMM = 3,
+                     HLM_STREAM_OPT = 4 };
+#define HLM_NOT_READY 1   /* hlm_cuda_event_query: recorded work still pending */
+int hlm_cuda_init(int device, HlmCaps* caps);
+int hlm_cuda_arena_create(size_t bytes, void** base);   /* one device allocation; HLM_ERR_OOM */
+int hlm_cuda_arena_destroy(void* base);
+int hlm_cuda_stream_create(int kind, void** stream);    /* non-blocking; compute at top priority */
+int hlm_cuda_stream_destroy(void* stream);
+int hlm_cuda_stream_sync(void* stream);
+int hlm_cuda_event_create(void** event);
+int hlm_cuda_event_destroy(void* event);
+int hlm_cuda_event_record(void* event, void* stream);
+int hlm_cuda_event_wait(void* stream, void* event);     /* stream waits for event (no host block) */
+int hlm_cuda_event_sync(void* event);
+int hlm_cuda_event_query(void* event);                  /* HLM_OK done, HLM_NOT_READY pending */
+int hlm_cuda_event_elapsed_ms(void* start, void* end, float* ms);
+int hlm_cuda_h2d_async(void* dst, const void* pinned_src, size_t bytes, void* stream);
+int hlm_cuda_d2h_async(void* pinned_dst, const void* src, size_t bytes, void* stream);
+
 /* Number of CUDA kernels this library has launched since it was loaded. */
 long long hlm_cuda_launch_count(void);
 
@@ -203,6 +234,17 @@ int hlm_cuda_head_loss(int64_t rows, int64_t hidden, int64_t vocab, const void* 
                        const float* x, const int32_t* targets, float inv_rows, float* d_x,
                        float* d_head, int accumulate_d_head, float* loss_rows, void* ws,
                        void* stream);
+/* The same head + cross-entropy in SURVEY.md §8b's argument order (head_fwd +
+ * ce_loss_and_grad + head_bwd, proj/include/hlm/kernels.hpp:410-446; d_head overwritten):
+ * per-row losses in loss_rows (device); loss_sum_out (host, optional) = their sum in row
+ * order in double after the stream drains, as Engine::anchor_loss computes it. ws as
+ * hlm_cuda_head_loss (hlm_cuda_head_ws_bytes). */
+typedef struct HlmHeadDims {
+  int64_t rows, hidden, vocab;
+} HlmHeadDims;
+int hlm_cuda_head_fwd_ce_bwd(const HlmHeadDims* dims, const void* head_bf16, const float* h,
+                             const int32_t* targets, float inv_global_rows, float* d_h, float* d_head_fp32,
+                             float* loss_rows, double* loss_sum_out, void* ws, void* stream);
 
 /* ------------------------------------------------------------------ embedding
  * embed_fwd: out[t] = table[tokens[t]] widened to fp32 (kernels.hpp:385-394);
