@@ -165,7 +165,7 @@ class ClockSampler:
 
 
 class FastClockSampler:
-    """SM clock of this rank's GPU every 2 ms through NVML during the timed region. The
+    """SM clock of this rank's GPU every 5 ms through NVML during the timed region. The
     200 ms nvidia-smi samples above mostly land in the GPU's idle gaps of a host-bound
     step (median = the maximum clock); 2 ms samples resolve the GEMM bursts, where the
     power cap pulls the SM clock down to the sustained regime (the clock the kernels'
@@ -196,7 +196,7 @@ class FastClockSampler:
                 self.clk.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
             except Exception:
                 return
-            time.sleep(0.002)
+            time.sleep(0.005)
 
     def stop(self):
         self.stop_ = True
@@ -206,7 +206,7 @@ class FastClockSampler:
         c = np.array(self.clk, dtype=np.float64)
         return {"sm_mhz_median": float(np.median(c)), "sm_mhz_p10": float(np.percentile(c, 10)),
                 "sm_mhz_p90": float(np.percentile(c, 90)), "share_below_1900": float((c < 1900).mean()),
-                "samples": int(c.size), "period_ms": 2}
+                "samples": int(c.size), "period_ms": 5}
 
 
 def nvml_index(local):
