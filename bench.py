@@ -167,7 +167,7 @@ class ClockSampler:
 class FastClockSampler:
     """SM clock of this rank's GPU every 5 ms through NVML during the timed region. The
     200 ms nvidia-smi samples above mostly land in the GPU's idle gaps of a host-bound
-    step (median = the maximum clock); 2 ms samples resolve the GEMM bursts, where the
+    step (median = the maximum clock); 5 ms samples resolve the GEMM bursts, where the
     power cap pulls the SM clock down to the sustained regime (the clock the kernels'
     roofline peak must match)."""
 
@@ -696,7 +696,7 @@ def run_ours(args, m, name):
                      "achieved": kt["gemm"]["tflops"], "peak": tf_sus, "unit": "TFLOP/s",
                      "frac": (kt["gemm"]["tflops"] or 0) / tf_sus,
                      "peak_kind": f"{peak_kind} sustained: the GEMMs are timed inside a long step whose "
-                                  "GEMM bursts run at power-capped clocks (clocks.fast: 2 ms NVML samples "
+                                  "GEMM bursts run at power-capped clocks (clocks.fast: 5 ms NVML samples "
                                   "of the timed region; tools/instep_probe.py: the same in-step GEMM time "
                                   "with the host Adam off, so host contention is not the cause)",
                      "frac_of_burst": (kt["gemm"]["tflops"] or 0) / tf_burst, "peak_burst": tf_burst,
