@@ -827,14 +827,16 @@ int sm_count() {
   return n;
 }
 
-// HLM_GEMM_DYNAMIC=1: CTA pairs claim tiles from a per-launch counter in raster order, so
-// the tiles in flight stay a contiguous window of the raster however far individual pairs
-// drift (the static stride lets a slow pair fall whole tiles behind its wave, and the wave
-// then stops sharing operand panels in L2).
+// Default: CTA pairs claim tiles from a per-launch counter in raster order, so the tiles in
+// flight stay a contiguous window of the raster however far individual pairs drift (the
+// static stride lets a slow pair fall whole tiles behind its wave). Measured at C2: -2 %
+// serialized block-GEMM time under ncu, the GPU-bound HBM-resident bench variant +2 %
+// (908 vs 924-930 ms per step, two A/B pairs), the host-bound headline unchanged (five A/B
+// pairs); bitwise equal to the static stride. HLM_GEMM_DYNAMIC=0 restores the static stride.
 bool dynamic_schedule() {
   static const int v = [] {
     const char* e = std::getenv("HLM_GEMM_DYNAMIC");
-    return e ? std::atoi(e) : 0;
+    return e ? std::atoi(e) : 1;
   }();
   return v != 0;
 }

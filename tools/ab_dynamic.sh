@@ -1,0 +1,8 @@
+# A/B of the GEMM tile schedule on the full C2 bench (headline + HBM-resident variant), alternating
+mkdir -p gpurun_out/ab
+for i in 3 4 5; do
+  for d in 0 1; do
+    HLM_GEMM_DYNAMIC=$d timeout 600 python bench.py --no-wide --no-cpu-baseline --no-hybrid > gpurun_out/ab/d${d}_$i.json 2> gpurun_out/ab/d${d}_$i.err
+    echo "d$d run$i rc=$?" >> gpurun_out/ab/rc.txt
+  done
+done
