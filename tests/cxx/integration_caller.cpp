@@ -11,12 +11,15 @@
 //                                                             (reference proj/tests/test_arena.cpp:160-215)
 //   integration_caller ledger L h f V S B K heads           -> footprint vs the live ledger after one step
 //                                                             (reference proj/tests/test_planner.cpp:43-72)
+//   integration_caller hlm1 in out L h f V S B K heads      -> load_checkpoint of a reference HLM1 file,
+//                                                             save_checkpoint_hlm1 back (host only, no GPU)
 #include <cinttypes>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
 
+#include "hlm/checkpoint.hpp"
 #include "hlm/engine.hpp"
 #include "hlm/trainer.hpp"
 
@@ -235,6 +238,24 @@ int ledger(char** a) {
     return 0;
 }
 
+// The reference's checkpoint call sites (hlm_main.cpp cmd_train --resume / --checkpoint):
+// a reference HLM1 file loads into this store and is written back as HLM1.
+int hlm1(char** a) {
+    const hlm::ModelConfig m = config_from(a + 2);
+    m.validate();
+    auto store = hlm::build_store(m, 99, hlm::Dtype::BF16, hlm::InitMode::Reference, /*pin_shadow=*/false);
+    hlm::load_checkpoint(*store, a[0]);
+    hlm::save_checkpoint_hlm1(*store, a[1]);
+    double s = 0.0;
+    for (hlm::i64 p = 0; p < store->physical_tiles(); ++p) {
+        const hlm::LayerTile& t = store->physical(p);
+        for (hlm::i64 i = 0; i < t.n_params(); ++i) s += static_cast<double>(t.master()[i]);
+    }
+    std::printf("adam_steps %" PRId64 " params %" PRId64 " master_sum %.17g\n", store->adam_steps(),
+                store->total_params(), s);
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -246,7 +267,8 @@ int main(int argc, char** argv) {
         if (mode == "errors") return errors();
         if (mode == "arena") return arena();
         if (mode == "ledger" && argc == 10) return ledger(argv + 2);
-        std::fprintf(stderr, "usage: %s train|trainx L h f V S B K heads steps | phases L h f V S B K heads | errors | arena | ledger L h f V S B K heads\n",
+        if (mode == "hlm1" && argc == 12) return hlm1(argv + 2);
+        std::fprintf(stderr, "usage: %s train|trainx L h f V S B K heads steps | phases L h f V S B K heads | errors | arena | ledger L h f V S B K heads | hlm1 in out L h f V S B K heads\n",
                      argv[0]);
         return 64;
     } catch (const std::invalid_argument& e) {

@@ -40,6 +40,7 @@ REQUIRED = [
     "hlm::b200::run_training(",
     "hlm::b200::save_checkpoint(",
     "hlm::b200::load_checkpoint(",
+    "hlm::b200::save_checkpoint_hlm1(",
     "typeinfo for hlm::b200::ArenaOomError",
     "typeinfo for hlm::b200::ProtocolError",
 ]
@@ -199,3 +200,24 @@ def test_live_ledger_equals_the_footprint_estimate(caller, K):
     params = 2 * V * h + L * n
     assert kv["host.params"] == params and kv["host.persistent"] == 14 * params
     assert kv["host.total"] == kv["host.persistent"] + kv["host.slabs"]
+
+
+def test_cxx_caller_round_trips_a_reference_hlm1_checkpoint(caller, tmp_path):
+    """hlm::load_checkpoint reads the reference's HLM1 (golden file written by the reference's
+    save_checkpoint) and hlm::save_checkpoint_hlm1 writes it back byte for byte: a BF16 store's
+    master is the file's BF16 weights exactly, m / v / step count unchanged, and the reference
+    container carries the gradient region as zeros (last-step scratch, not restored)."""
+    import oracle as O
+    src = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ref_tiny_bf16.hlm1")
+    out = tmp_path / "back.hlm1"
+    # tiny: L2 h8 f16 V11 S4 B1 K1, one head (tests/golden/make_golden.py)
+    r = subprocess.run([caller, "hlm1", src, str(out), "2", "8", "16", "11", "4", "1", "1", "1"],
+                       capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    assert "adam_steps 3 " in r.stdout
+    a, b = O.read_hlm1(src), O.read_hlm1(str(out))
+    assert a["adam_steps"] == b["adam_steps"] and list(a["alias"]) == list(b["alias"])
+    for ta, tb in zip(a["tiles"], b["tiles"]):
+        for key in ("weights", "m", "v"):
+            assert np.array_equal(ta[key].view(np.uint32), tb[key].view(np.uint32)), key
+        assert not tb["grads"].any()
