@@ -555,7 +555,8 @@ def run_ours(args, m, name):
         clk = {"sm_mhz": float(np.median(meds)) if meds else None,
                "sm_max_mhz": max((c["sm_max_mhz"] for c in per if c.get("sm_max_mhz")), default=None),
                "reasons": sorted(set(r for c in per for r in c["reasons"])),
-               "samples": sum(c["samples"] for c in per), "per_rank_sm_mhz": [c.get("sm_mhz") for c in per]}
+               "samples": sum(c["samples"] for c in per), "per_rank_sm_mhz": [c.get("sm_mhz") for c in per],
+               "fast_per_rank": [c.get("fast") for c in per]}
     lib.hlm_ktimer_enable(0)
     kt = {}
     for kind, kname in ((0, "gemm"), (1, "attn_fwd"), (2, "attn_bwd")):
