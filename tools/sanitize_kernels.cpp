@@ -192,6 +192,7 @@ int main(int argc, char** argv) {
     gemm(256, 384, 512, 0, 1, HLM_EPI_BF16, 3, 0);     // N-grouped (qkv)
     gemm(256, 256, 384, 0, 0, HLM_EPI_F32, 2, 1);      // K-grouped (dgrad up|gate)
     gemm(256, 512, 1024, 1, 1, HLM_EPI_F32, 2, 0);     // wgrad (MN-major A and B), grouped
+    gemm(4096, 4096, 128, 0, 1, HLM_EPI_F32);          // 256 pair tiles > 74 pairs: dynamic tile claiming
     if (!quick) gemm(1024, 768, 1536, 0, 1, HLM_EPI_F32);
     // attention: tcgen05 (hd 128, S % 128) and mma.sync (hd 64) paths, plus the generic one
     attention(1, 256, 2, 128, 0);   // two-query-tile forward (64-key steps), 64-wide backward
