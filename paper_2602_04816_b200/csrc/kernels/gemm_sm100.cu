@@ -40,7 +40,7 @@ constexpr int A_STAGE = BM * BK * 2;   // 16 KiB
 constexpr int B_STAGE = BN * BK * 2;   // 32 KiB
 constexpr int ATOM = 64 * BK * 2;      // one 64-wide MN atom of a MN-major stage: 8 KiB
 constexpr int NUM_THREADS = 256;
-constexpr int GROUP_M = 16;            // raster: 16 M-tiles share each B panel in L2 (default)
+constexpr int GROUP_M = 8;             // raster: 8 M-tiles share each B panel in L2 (default; see launch())
 constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + 1024 /*align*/ + 256 /*barriers*/;
 
 struct KArgs {
@@ -914,6 +914,9 @@ int launch(const HlmGemmDesc& d, cudaStream_t stream) {
       const char* e = std::getenv("HLM_GEMM_GROUP_M");
       gm_env = e ? std::atoi(e) : 0;
     }
+    // 8 under the dynamic schedule: the 74 tiles in flight span 8 M x ~9 N tiles. Block fwd+bwd
+    // at C2 (tools/block_bench.py, power-capped back-to-back): 22.28 vs 22.76 ms with 16; full
+    // bench HBM-resident variant 896-901 vs 914-933 ms (profiles/r02/r02_gemm_group_m_ab.jsonl)
     a.group_m = gm_env > 0 ? gm_env : GROUP_M;
   }
   a.C = d.C;
